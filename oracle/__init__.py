@@ -1,0 +1,297 @@
+"""ctypes wrapper of the CPU oracle (oracle/lc_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py. The product package
+(paper_2603_17201_b200) never imports this module, and this module never
+imports the product package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "lc_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+COUNTER_NAMES = [
+    "queries", "skip_bad", "skip_found", "cull_depth", "cull_bounds", "cull_dist",
+    "cull_angle", "candidates", "no_cand", "over_th", "ratio_rej", "proposals",
+    "winners", "orient_rej", "add", "victim_prop", "loop_skip", "bad_slot",
+    "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
+]
+NONE64 = np.iinfo(np.int64).max
+
+# query status codes
+Q_BAD, Q_FOUND, Q_DEPTH, Q_BOUNDS, Q_DIST, Q_ANGLE = -1, -2, -3, -4, -5, -6
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (plain C, -ffp-contract=off so fp64 runs in written order)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+                               "-shared", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+class _Camera(C.Structure):
+    _fields_ = [("model", C.c_int32), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("k", C.c_double * 4),
+                ("min_x", C.c_double), ("max_x", C.c_double), ("min_y", C.c_double),
+                ("max_y", C.c_double)]
+
+
+class _Params(C.Structure):
+    _fields_ = [("th", C.c_int32), ("max_hamming", C.c_int32), ("ratio_num", C.c_int32),
+                ("ratio_den", C.c_int32), ("check_orientation", C.c_int32)]
+
+
+class _Map(C.Structure):
+    _fields_ = [("n_kf", C.c_int32), ("n_feat", C.c_int32), ("n_mp", C.c_int32),
+                ("n_levels", C.c_int32), ("scale_factor", C.c_double),
+                ("kf_pose", C.c_void_p), ("kf_cam", C.c_void_p), ("kf_feat_begin", C.c_void_p),
+                ("feat_uv", C.c_void_p), ("feat_octave", C.c_void_p), ("feat_angle", C.c_void_p),
+                ("feat_desc", C.c_void_p), ("feat_mp", C.c_void_p), ("mp_pos", C.c_void_p),
+                ("mp_normal", C.c_void_p), ("mp_max_dist", C.c_void_p), ("mp_desc", C.c_void_p),
+                ("mp_angle", C.c_void_p), ("mp_ref_kf", C.c_void_p), ("mp_flags", C.c_void_p),
+                ("mp_replaced_by", C.c_void_p), ("mp_nobs", C.c_void_p),
+                ("mp_corr_ref", C.c_void_p), ("kf_in_window", C.c_void_p),
+                ("kf_S_corr", C.c_void_p), ("cams", C.c_void_p), ("n_cams", C.c_int32)]
+
+
+class _QRes(C.Structure):
+    _fields_ = [("status", C.c_int32), ("u", C.c_double), ("v", C.c_double),
+                ("level", C.c_int32), ("radius", C.c_double), ("ncand", C.c_int32),
+                ("best_f", C.c_int32), ("best_h", C.c_int32), ("second_h", C.c_int32),
+                ("edge", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        _lib.orc_hamming.restype = C.c_int
+        _lib.orc_predict_level.restype = C.c_int
+        _lib.orc_predict_level.argtypes = [C.c_double, C.c_double, C.c_void_p, C.c_int32]
+        for fn in ("orc_correct_window", "orc_correct_all", "orc_fuse", "orc_search_by_projection"):
+            getattr(_lib, fn).restype = C.c_int
+    return _lib
+
+
+def _p(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def make_camera(cam) -> _Camera:
+    d = cam.as_dict() if hasattr(cam, "as_dict") else dict(cam)
+    c = _Camera()
+    c.model = d["model"]
+    c.fx, c.fy, c.cx, c.cy = d["fx"], d["fy"], d["cx"], d["cy"]
+    for i in range(4):
+        c.k[i] = d["k"][i]
+    c.min_x, c.max_x, c.min_y, c.max_y = d["min_x"], d["max_x"], d["min_y"], d["max_y"]
+    return c
+
+
+def make_params(p) -> _Params:
+    th, mh, rn, rd, co = p
+    return _Params(th, mh, rn, rd, co)
+
+
+# ----------------------------------------------------------------------------
+# primitives (pinned directly by tests/test_oracle_pins.py)
+# ----------------------------------------------------------------------------
+def hamming(a, b) -> int:
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    return int(lib().orc_hamming(_p(a), _p(b)))
+
+
+def _sim3_call(fn, *args):
+    out = np.zeros(13 if fn != "orc_sim3_apply" else 3, np.float64)
+    arrs = [np.ascontiguousarray(a, np.float64) for a in args]
+    getattr(lib(), fn)(*[_p(a) for a in arrs], _p(out))
+    return out
+
+
+def sim3_apply(S, p):
+    return _sim3_call("orc_sim3_apply", S, p)
+
+
+def sim3_compose(A, B):
+    return _sim3_call("orc_sim3_compose", A, B)
+
+
+def sim3_inverse(S):
+    return _sim3_call("orc_sim3_inverse", S)
+
+
+def sim3_se3(S):
+    return _sim3_call("orc_sim3_se3", S)
+
+
+def project(cam, pc):
+    c = make_camera(cam)
+    pc = np.ascontiguousarray(pc, np.float64)
+    uv = np.zeros(2, np.float64)
+    lib().orc_project(C.byref(c), _p(pc), _p(uv))
+    return uv
+
+
+def scale_table(L=8, f=1.2):
+    out = np.zeros(L, np.float64)
+    lib().orc_scale_table(C.c_int32(L), C.c_double(f), _p(out))
+    return out
+
+
+def predict_level(d, dmax, L=8, f=1.2):
+    st = scale_table(L, f)
+    return int(lib().orc_predict_level(C.c_double(d), C.c_double(dmax), _p(st), C.c_int32(L)))
+
+
+# ----------------------------------------------------------------------------
+# map state
+# ----------------------------------------------------------------------------
+class OracleMap:
+    """Mutable copy of a world's map plus the loop state, driven by the C oracle."""
+
+    def __init__(self, world=None, *, arrays=None, cams=None, n_levels=8, scale_factor=1.2):
+        a = arrays if arrays is not None else world.map_arrays()
+        cams = cams if cams is not None else [world.cam]
+        self.kf_pose = np.array(a["kf_pose"], np.float64, order="C").reshape(-1, 13)
+        self.kf_cam = np.ascontiguousarray(a["kf_cam"], np.int32)
+        self.kf_feat_begin = np.ascontiguousarray(a["kf_feat_begin"], np.int32)
+        self.feat_uv = np.ascontiguousarray(a["feat_uv"], np.float32).reshape(-1, 2)
+        self.feat_octave = np.ascontiguousarray(a["feat_octave"], np.uint8)
+        self.feat_angle = np.ascontiguousarray(a["feat_angle"], np.float32)
+        self.feat_desc = np.ascontiguousarray(a["feat_desc"], np.uint8).reshape(-1, 32)
+        self.feat_mp = np.array(a["feat_mp"], np.int32)
+        self.mp_pos = np.array(a["mp_pos"], np.float32).reshape(-1, 3)
+        self.mp_normal = np.ascontiguousarray(a["mp_normal"], np.float32).reshape(-1, 3)
+        self.mp_max_dist = np.ascontiguousarray(a["mp_max_dist"], np.float32)
+        self.mp_desc = np.ascontiguousarray(a["mp_desc"], np.uint8).reshape(-1, 32)
+        self.mp_angle = np.ascontiguousarray(a["mp_angle"], np.float32)
+        self.mp_ref_kf = np.ascontiguousarray(a["mp_ref_kf"], np.int32)
+        self.mp_flags = np.array(a["mp_flags"], np.uint8)
+        n_kf, n_mp = self.kf_pose.shape[0], self.mp_pos.shape[0]
+        self.mp_replaced_by = np.full(n_mp, -1, np.int32)
+        self.mp_nobs = np.bincount(self.feat_mp[self.feat_mp >= 0], minlength=n_mp).astype(np.int32)
+        self.mp_corr_ref = np.full(n_mp, -1, np.int32)
+        self.kf_in_window = np.zeros(n_kf, np.int32)
+        self.kf_S_corr = np.zeros((n_kf, 13), np.float64)
+        self._cams = (_Camera * len(cams))(*[make_camera(c) for c in cams])
+        m = _Map()
+        m.n_kf, m.n_feat, m.n_mp = n_kf, self.feat_uv.shape[0], n_mp
+        m.n_levels, m.scale_factor = n_levels, scale_factor
+        for name in ("kf_pose", "kf_cam", "kf_feat_begin", "feat_uv", "feat_octave", "feat_angle",
+                     "feat_desc", "feat_mp", "mp_pos", "mp_normal", "mp_max_dist", "mp_desc",
+                     "mp_angle", "mp_ref_kf", "mp_flags", "mp_replaced_by", "mp_nobs",
+                     "mp_corr_ref", "kf_in_window", "kf_S_corr"):
+            setattr(m, name, getattr(self, name).ctypes.data)
+        m.cams = C.cast(self._cams, C.c_void_p).value
+        m.n_cams = len(cams)
+        self._m = m
+
+    @property
+    def n_kf(self):
+        return self.kf_pose.shape[0]
+
+    @property
+    def n_mp(self):
+        return self.mp_pos.shape[0]
+
+    def n_feat_of(self, k):
+        return int(self.kf_feat_begin[k + 1] - self.kf_feat_begin[k])
+
+    # -- single query (pins) --------------------------------------------------
+    def query(self, k, S_kw, q, params, taken=None, mode=0):
+        r = _QRes()
+        S = np.ascontiguousarray(S_kw, np.float64)
+        t = None if taken is None else np.ascontiguousarray(taken, np.int32)
+        prm = make_params(params)
+        lib().orc_query(C.byref(self._m), C.c_int32(k), _p(S), C.c_int32(q), C.byref(prm),
+                        _p(t), C.c_int32(mode), C.byref(r))
+        return {f: getattr(r, f) for f, _ in _QRes._fields_}
+
+    # -- O3 ------------------------------------------------------------------
+    def correct_window(self, cur_kf, S_cw_corr, window):
+        window = np.ascontiguousarray(window, np.int32)
+        S = np.ascontiguousarray(S_cw_corr, np.float64)
+        out_S = np.zeros((len(window), 13), np.float64)
+        cnt = np.zeros(len(COUNTER_NAMES), np.int64)
+        rc = lib().orc_correct_window(C.byref(self._m), C.c_int32(cur_kf), _p(S),
+                                      C.c_int32(len(window)), _p(window), _p(out_S), _p(cnt))
+        if rc != 0:
+            raise ValueError("orc_correct_window: invalid arguments")
+        return out_S, dict(zip(COUNTER_NAMES, cnt.tolist()))
+
+    # -- O10 -----------------------------------------------------------------
+    def correct_all(self, S_opt):
+        S = np.ascontiguousarray(S_opt, np.float64).reshape(-1, 13)
+        cnt = np.zeros(len(COUNTER_NAMES), np.int64)
+        lib().orc_correct_all(C.byref(self._m), _p(S), _p(cnt))
+        return dict(zip(COUNTER_NAMES, cnt.tolist()))
+
+    # -- O4-O9 ---------------------------------------------------------------
+    def window_feat_total(self, window):
+        return int(sum(self.n_feat_of(int(k)) for k in window))
+
+    def fuse(self, window, mp_list, params, *, window_S=None, win_list_begin=None, phase=3,
+             w_lo=0, w_hi=None, winner=None, victim=None, debug=False):
+        window = np.ascontiguousarray(window, np.int32)
+        n_w = len(window)
+        w_hi = n_w if w_hi is None else w_hi
+        mp_list = np.ascontiguousarray(mp_list, np.int32)
+        wb = None if win_list_begin is None else np.ascontiguousarray(win_list_begin, np.int32)
+        wS = None if window_S is None else np.ascontiguousarray(window_S, np.float64).reshape(-1, 13)
+        nwf = self.window_feat_total(window)
+        winner = np.full(nwf, NONE64, np.int64) if winner is None else winner
+        victim = np.full(self.n_mp, NONE64, np.int64) if victim is None else victim
+        action = np.zeros(nwf, np.int8)
+        nq = int(wb[-1]) if wb is not None else n_w * len(mp_list)
+        dbg = {}
+        if debug:
+            dbg = dict(status=np.zeros(nq, np.int32), best=np.zeros(nq, np.int64),
+                       uv=np.zeros((nq, 2), np.float64), ncand=np.zeros(nq, np.int32),
+                       edge=np.zeros(nq, np.uint8))
+        cnt = np.zeros(len(COUNTER_NAMES), np.int64)
+        prm = make_params(params)
+        lib().orc_fuse(C.byref(self._m), C.c_int32(phase), C.c_int32(w_lo), C.c_int32(w_hi),
+                       C.c_int32(n_w), _p(window), _p(wS), _p(wb), _p(mp_list),
+                       C.c_int32(len(mp_list)), C.byref(prm), _p(winner), _p(victim), _p(action),
+                       _p(dbg.get("status")), _p(dbg.get("best")), _p(dbg.get("uv")),
+                       _p(dbg.get("ncand")), _p(dbg.get("edge")), _p(cnt))
+        return dict(winner=winner, victim=victim, action=action,
+                    counts=dict(zip(COUNTER_NAMES, cnt.tolist())), **dbg)
+
+    # -- batched projection search -------------------------------------------
+    def search_by_projection(self, pair_kf, pair_S, pair_param, params, pair_list_begin, mp_list,
+                             pair_taken=None, debug=False):
+        pair_kf = np.ascontiguousarray(pair_kf, np.int32)
+        pair_S = np.ascontiguousarray(pair_S, np.float64).reshape(-1, 13)
+        pair_param = np.ascontiguousarray(pair_param, np.int32)
+        plb = np.ascontiguousarray(pair_list_begin, np.int32)
+        mp_list = np.ascontiguousarray(mp_list, np.int32)
+        taken = None if pair_taken is None else np.ascontiguousarray(pair_taken, np.int32)
+        prms = (_Params * len(params))(*[make_params(p) for p in params])
+        ntot = int(sum(self.n_feat_of(int(k)) for k in pair_kf))
+        out_mp = np.zeros(ntot, np.int32)
+        out_dist = np.zeros(ntot, np.int32)
+        nq = int(plb[-1])
+        dbg = {}
+        if debug:
+            dbg = dict(best=np.zeros(nq, np.int64), uv=np.zeros((nq, 2), np.float64),
+                       ncand=np.zeros(nq, np.int32), edge=np.zeros(nq, np.uint8))
+        cnt = np.zeros((len(pair_kf), len(COUNTER_NAMES)), np.int64)
+        lib().orc_search_by_projection(C.byref(self._m), C.c_int32(len(pair_kf)), _p(pair_kf),
+                                       _p(pair_S), _p(pair_param), prms, _p(plb), _p(mp_list),
+                                       _p(taken), _p(out_mp), _p(out_dist), _p(dbg.get("best")),
+                                       _p(dbg.get("uv")), _p(dbg.get("ncand")),
+                                       _p(dbg.get("edge")), _p(cnt))
+        return dict(feat_mp=out_mp, feat_dist=out_dist, counts=cnt, **dbg)

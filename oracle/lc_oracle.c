@@ -1,0 +1,635 @@
+/*
+ * lc_oracle.c -- plain, slow, obviously-correct CPU oracle for the loop-closing
+ * fuse/correct hot path of arXiv 2603.17201 ("FastLoop").
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product path
+ * (paper_2603_17201_b200/, csrc/) never links, imports or calls it, and this file
+ * shares no code, header, table or constant generator with csrc/.
+ *
+ * What it computes (PAPER.md line + section; SURVEY.md §8(c) reading ids):
+ *   - Loop-correction Sim3 pose correction of the window keyframes and the map
+ *     points they observe ("correcting their poses using the estimated Sim3
+ *     transformation", §III.B)                     -> orc_correct_window  (O3)
+ *   - Loop fusion: project the loop map points into every window keyframe,
+ *     match by descriptor "within close spatial proximity", and merge
+ *     duplicates (§III.B; §IV.D.3)  -> orc_fuse        (O4-O9)
+ *   - Projection search PS1 / PS2a||PS2b / PS3a-c, one result batch per
+ *     (keyframe, transform) pair (§IV.C; §IV.D.1-2)
+ *                                                               -> orc_search_by_projection
+ *   - Propagation of the optimised Sim3 of every keyframe to the whole map
+ *     ("propagates the loop correction to the rest of the map")
+ *                                                               -> orc_correct_all   (O10)
+ * The paper gives no matching math (SURVEY.md §0 "Key finding"); every
+ * constant and tie-break is a DESIGN.md reading (A1-A32), noted inline.
+ *
+ * Style: brute force, ascending loops, fp64 arithmetic evaluated in the order
+ * written (compile with -O2 -ffp-contract=off, no -ffast-math), fp32 only for
+ * stored values. No grid, no atomics, no reordering.
+ *
+ * Parity status: every function is pinned by tests/test_oracle_pins.py except
+ * the orientation-histogram rule beyond its hand-built cases (A15), which is
+ * "parity unpinned" against the paper (the paper prints nothing about it).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_NONE INT64_MAX
+
+/* counter slots (same meaning/order as DESIGN.md "Counters"; tests match by name) */
+enum {
+  C_QUERIES = 0, C_SKIP_BAD, C_SKIP_FOUND, C_CULL_DEPTH, C_CULL_BOUNDS, C_CULL_DIST,
+  C_CULL_ANGLE, C_CANDIDATES, C_NO_CAND, C_OVER_TH, C_RATIO_REJ, C_PROPOSALS,
+  C_WINNERS, C_ORIENT_REJ, C_ADD, C_VICTIM_PROP, C_LOOP_SKIP, C_BAD_SLOT,
+  C_VICTIMS, C_REWIRED, C_DUP_CLEARED, C_ADDED, C_CORR_KF, C_CORR_MP, C_N
+};
+
+/* query status codes written to out_status (negative = culled/skipped) */
+enum { Q_MATCHED_STAGE = 0, Q_BAD = -1, Q_FOUND = -2, Q_DEPTH = -3, Q_BOUNDS = -4,
+       Q_DIST = -5, Q_ANGLE = -6 };
+
+typedef struct {
+  int32_t model;            /* 0 pinhole, 1 Kannala-Brandt-8 */
+  double fx, fy, cx, cy;
+  double k[4];
+  double min_x, max_x, min_y, max_y;
+} orc_camera;
+
+typedef struct {
+  int32_t th, max_hamming, ratio_num, ratio_den, check_orientation;
+} orc_params;
+
+typedef struct {
+  int32_t n_kf, n_feat, n_mp, n_levels;
+  double scale_factor;
+  double *kf_pose;          /* [n_kf][13] R row-major, t, s  (mutable: corrections) */
+  const int32_t *kf_cam;
+  const int32_t *kf_feat_begin;
+  const float *feat_uv;     /* [n_feat][2] */
+  const uint8_t *feat_octave;
+  const float *feat_angle;
+  const uint8_t *feat_desc; /* [n_feat][32] */
+  int32_t *feat_mp;         /* mutable (fusion) */
+  float *mp_pos;            /* [n_mp][3] mutable (corrections) */
+  const float *mp_normal;
+  const float *mp_max_dist;
+  const uint8_t *mp_desc;   /* [n_mp][32] */
+  const float *mp_angle;
+  const int32_t *mp_ref_kf;
+  uint8_t *mp_flags;        /* bit0 = bad */
+  int32_t *mp_replaced_by;  /* -1 = none */
+  int32_t *mp_nobs;
+  /* loop state created by orc_correct_window, consumed by orc_correct_all */
+  int32_t *mp_corr_ref;     /* [n_mp] owner KF of this loop's correction, -1 = none */
+  int32_t *kf_in_window;    /* [n_kf] 1 if corrected by the last window correction */
+  double *kf_S_corr;        /* [n_kf][13] S_iw^corr (= S^pre for O10) */
+  const orc_camera *cams;
+  int32_t n_cams;
+} orc_map;
+
+/* ------------------------------------------------------------------------- */
+/* O1  Hamming distance of two 256-bit descriptors: number of differing bits.  */
+/* "descriptor similarity". Bit-by-bit count.      */
+/* ------------------------------------------------------------------------- */
+int orc_hamming(const uint8_t *a, const uint8_t *b) {
+  int n = 0;
+  for (int i = 0; i < 32; ++i) {
+    unsigned x = (unsigned)(a[i] ^ b[i]);
+    for (int bit = 0; bit < 8; ++bit) n += (x >> bit) & 1u;
+  }
+  return n;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O2  Sim3 algebra, S = (R, t, s), S(p) = s*(R p) + t  (reading A1).          */
+/* Row products are evaluated ((a0*b0 + a1*b1) + a2*b2).                     */
+/* ------------------------------------------------------------------------- */
+static double row3(const double *r, const double *p) {
+  return (r[0] * p[0] + r[1] * p[1]) + r[2] * p[2];
+}
+static double col3(const double *R, int i, const double *p) { /* (R^T p)_i */
+  return (R[0 + i] * p[0] + R[3 + i] * p[1]) + R[6 + i] * p[2];
+}
+
+void orc_sim3_apply(const double *S, const double *p, double *out) {
+  double q[3];
+  for (int i = 0; i < 3; ++i) q[i] = row3(S + 3 * i, p);
+  for (int i = 0; i < 3; ++i) out[i] = S[12] * q[i] + S[9 + i];
+}
+
+void orc_sim3_compose(const double *A, const double *B, double *out) {
+  double o[13];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      o[3 * i + j] = (A[3 * i + 0] * B[0 + j] + A[3 * i + 1] * B[3 + j]) + A[3 * i + 2] * B[6 + j];
+  for (int i = 0; i < 3; ++i) o[9 + i] = A[12] * row3(A + 3 * i, B + 9) + A[9 + i];
+  o[12] = A[12] * B[12];
+  memcpy(out, o, sizeof(o));
+}
+
+void orc_sim3_inverse(const double *S, double *out) {
+  double o[13];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) o[3 * i + j] = S[3 * j + i];
+  for (int i = 0; i < 3; ++i) o[9 + i] = -col3(S, i, S + 9) / S[12];
+  o[12] = 1.0 / S[12];
+  memcpy(out, o, sizeof(o));
+}
+
+/* SE3 part of a Sim3: (R, t/s, 1)  (reading A2) */
+void orc_sim3_se3(const double *S, double *out) {
+  double o[13];
+  memcpy(o, S, 9 * sizeof(double));
+  for (int i = 0; i < 3; ++i) o[9 + i] = S[9 + i] / S[12];
+  o[12] = 1.0;
+  memcpy(out, o, sizeof(o));
+}
+
+/* scale table s_0 = 1, s_n = s_{n-1} * f (fp64) */
+void orc_scale_table(int32_t L, double f, double *out) {
+  out[0] = 1.0;
+  for (int n = 1; n < L; ++n) out[n] = out[n - 1] * f;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Camera projection pi(p_c) (reading A29 for Kannala-Brandt-8).              */
+/* ------------------------------------------------------------------------- */
+void orc_project(const orc_camera *c, const double *pc, double *uv) {
+  double x = pc[0], y = pc[1], z = pc[2];
+  if (c->model == 0) {
+    uv[0] = ((c->fx * x) / z) + c->cx;
+    uv[1] = ((c->fy * y) / z) + c->cy;
+    return;
+  }
+  double rho = sqrt((x * x) + (y * y));
+  if (rho == 0.0) { uv[0] = c->cx; uv[1] = c->cy; return; }
+  double th = atan2(rho, z);
+  double t2 = th * th;
+  double a = c->k[3];
+  a = c->k[2] + t2 * a;
+  a = c->k[1] + t2 * a;
+  a = c->k[0] + t2 * a;
+  a = 1.0 + t2 * a;
+  double r = th * a;
+  uv[0] = ((c->fx * r) * (x / rho)) + c->cx;
+  uv[1] = ((c->fy * r) * (y / rho)) + c->cy;
+}
+
+/* predicted level (reading A7): smallest n with d*s_n >= dmax, else L-1 */
+int orc_predict_level(double d, double dmax, const double *scale, int32_t L) {
+  for (int n = 0; n < L; ++n)
+    if (d * scale[n] >= dmax) return n;
+  return L - 1;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O4-O6 one query: keyframe k seen through S_kw, map point q.               */
+/* Returns status (0 = reached matching, <0 = cull code).                    */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t status;
+  double u, v;
+  int32_t level;
+  double radius;
+  int32_t ncand;
+  int32_t best_f;           /* KF-local original feature index, -1 = none */
+  int32_t best_h, second_h; /* 256 when absent */
+  int32_t edge;             /* 1 if a window/bounds decision is within 1e-4 px */
+} orc_qres;
+
+#define EDGE_EPS 1e-4
+
+static int found_in_kf(const orc_map *m, int32_t k, int32_t q) {
+  for (int32_t f = m->kf_feat_begin[k]; f < m->kf_feat_begin[k + 1]; ++f)
+    if (m->feat_mp[f] == q) return 1;
+  return 0;
+}
+
+static int found_in_taken(const int32_t *taken, int32_t nf, int32_t q) {
+  for (int32_t f = 0; f < nf; ++f)
+    if (taken[f] == q) return 1;
+  return 0;
+}
+
+/* mode 0 = fuse (already found = associated in k), 1 = SBP (already found = in taken) */
+static void query_one(const orc_map *m, int32_t k, const double *S_kw, int32_t q,
+                      const orc_params *prm, const int32_t *taken, int mode,
+                      const double *scale, orc_qres *r) {
+  memset(r, 0, sizeof(*r));
+  r->best_f = -1; r->best_h = 256; r->second_h = 256; r->level = -1;
+  int32_t nf = m->kf_feat_begin[k + 1] - m->kf_feat_begin[k];
+  if (m->mp_flags[q] & 1u) { r->status = Q_BAD; return; }
+  if (mode == 0 ? found_in_kf(m, k, q) : (taken && found_in_taken(taken, nf, q))) {
+    r->status = Q_FOUND; return;
+  }
+  double T[13], Ow[3], p[3], pc[3];
+  orc_sim3_se3(S_kw, T);                                  /* A2 */
+  for (int i = 0; i < 3; ++i) Ow[i] = -col3(T, i, T + 9);
+  for (int i = 0; i < 3; ++i) p[i] = (double)m->mp_pos[3 * q + i];
+  for (int i = 0; i < 3; ++i) pc[i] = row3(T + 3 * i, p) + T[9 + i];
+  if (pc[2] <= 0.0) { r->status = Q_DEPTH; return; }      /* A3 */
+  const orc_camera *cam = &m->cams[m->kf_cam[k]];
+  double uv[2];
+  orc_project(cam, pc, uv);
+  r->u = uv[0]; r->v = uv[1];
+  if (fabs(uv[0] - cam->min_x) < EDGE_EPS || fabs(uv[0] - cam->max_x) < EDGE_EPS ||
+      fabs(uv[1] - cam->min_y) < EDGE_EPS || fabs(uv[1] - cam->max_y) < EDGE_EPS) r->edge = 1;
+  if (!(uv[0] >= cam->min_x && uv[0] < cam->max_x && uv[1] >= cam->min_y && uv[1] < cam->max_y)) {
+    r->status = Q_BOUNDS; return;                         /* A4 */
+  }
+  double PO[3];
+  for (int i = 0; i < 3; ++i) PO[i] = p[i] - Ow[i];
+  double d = sqrt((PO[0] * PO[0] + PO[1] * PO[1]) + PO[2] * PO[2]);
+  double dmax = (double)m->mp_max_dist[q];
+  double dmin_inv = 0.8 * (dmax / scale[m->n_levels - 1]);
+  double dmax_inv = 1.2 * dmax;
+  if (d < dmin_inv || d > dmax_inv) { r->status = Q_DIST; return; }  /* A5 */
+  double n[3];
+  for (int i = 0; i < 3; ++i) n[i] = (double)m->mp_normal[3 * q + i];
+  if (row3(PO, n) < 0.5 * d) { r->status = Q_ANGLE; return; }        /* A6 */
+  int lvl = orc_predict_level(d, dmax, scale, m->n_levels);          /* A7 */
+  double rad = (double)prm->th * scale[lvl];                          /* A8, A11 */
+  r->level = lvl; r->radius = rad;
+  int32_t f0 = m->kf_feat_begin[k];
+  const uint8_t *dq = m->mp_desc + 32 * (size_t)q;
+  for (int32_t f = 0; f < nf; ++f) {                                  /* O5 brute force */
+    if (taken && taken[f] >= 0) continue;                             /* A19 (SBP) */
+    int oct = m->feat_octave[f0 + f];
+    if (oct < lvl - 1 || oct > lvl) continue;                         /* A9 */
+    double du = fabs((double)m->feat_uv[2 * (f0 + f)] - uv[0]);
+    double dv = fabs((double)m->feat_uv[2 * (f0 + f) + 1] - uv[1]);
+    if (du < rad + EDGE_EPS && dv < rad + EDGE_EPS &&
+        (du > rad - EDGE_EPS || dv > rad - EDGE_EPS)) r->edge = 1;
+    if (!(du < rad && dv < rad)) continue;
+    r->ncand++;
+    int h = orc_hamming(dq, m->feat_desc + 32 * (size_t)(f0 + f));
+    if (h < r->best_h || (h == r->best_h && f < r->best_f)) {          /* O6, A12, A13 */
+      if (r->best_f >= 0 && r->best_h < r->second_h) r->second_h = r->best_h;
+      r->best_h = h; r->best_f = f;
+    } else if (h < r->second_h) {
+      r->second_h = h;
+    }
+  }
+  r->status = Q_MATCHED_STAGE;
+}
+
+/* exposed for pin tests */
+void orc_query(const orc_map *m, int32_t k, const double *S_kw, int32_t q,
+               const orc_params *prm, const int32_t *taken, int32_t mode, orc_qres *r) {
+  double scale[64];
+  orc_scale_table(m->n_levels, m->scale_factor, scale);
+  query_one(m, k, S_kw, q, prm, taken, mode, scale, r);
+}
+
+/* proposal test O6 (A10 threshold inclusive, A14 integer ratio) */
+static int proposal_ok(const orc_qres *r, const orc_params *prm, int64_t *cnt) {
+  if (r->ncand == 0) { cnt[C_NO_CAND]++; return 0; }
+  if (r->best_h > prm->max_hamming) { cnt[C_OVER_TH]++; return 0; }
+  if (prm->ratio_den > 0 &&
+      (int64_t)prm->ratio_den * r->best_h > (int64_t)prm->ratio_num * r->second_h) {
+    cnt[C_RATIO_REJ]++; return 0;
+  }
+  cnt[C_PROPOSALS]++;
+  return 1;
+}
+
+/* O8 rotation-consistency filter over the winners of one keyframe (A15).
+ * winners: [nf] packed (H<<32)|q or ORC_NONE; removes rejected ones. */
+static void orientation_filter(const orc_map *m, int32_t k, int64_t *win, int32_t nf,
+                               int64_t *cnt) {
+  int hist[30];
+  memset(hist, 0, sizeof(hist));
+  int32_t f0 = m->kf_feat_begin[k];
+  int *bin_of = (int *)malloc(sizeof(int) * (nf > 0 ? nf : 1));
+  for (int32_t f = 0; f < nf; ++f) {
+    bin_of[f] = -1;
+    if (win[f] == ORC_NONE) continue;
+    int32_t q = (int32_t)(win[f] & 0xffffffff);
+    float rot = m->feat_angle[f0 + f] - m->mp_angle[q];
+    if (rot < 0.0f) rot += 360.0f;
+    long b = lroundf(rot * (30.0f / 360.0f));
+    if (b == 30) b = 0;
+    bin_of[f] = (int)b;
+    hist[b]++;
+  }
+  int max1 = 0, max2 = 0, max3 = 0, ind1 = -1, ind2 = -1, ind3 = -1;
+  for (int i = 0; i < 30; ++i) {                           /* ComputeThreeMaxima (EXT) */
+    int s = hist[i];
+    if (s > max1) { max3 = max2; max2 = max1; max1 = s; ind3 = ind2; ind2 = ind1; ind1 = i; }
+    else if (s > max2) { max3 = max2; max2 = s; ind3 = ind2; ind2 = i; }
+    else if (s > max3) { max3 = s; ind3 = i; }
+  }
+  if ((float)max2 < 0.1f * (float)max1) { ind2 = -1; ind3 = -1; }
+  else if ((float)max3 < 0.1f * (float)max1) { ind3 = -1; }
+  for (int32_t f = 0; f < nf; ++f) {
+    if (win[f] == ORC_NONE) continue;
+    int b = bin_of[f];
+    if (b != ind1 && b != ind2 && b != ind3) { win[f] = ORC_NONE; cnt[C_ORIENT_REJ]++; }
+  }
+  free(bin_of);
+}
+
+/* ------------------------------------------------------------------------- */
+/* O3 window correction (SPEC.md:391-399 gives the shape).       */
+/* ------------------------------------------------------------------------- */
+int orc_correct_window(orc_map *m, int32_t cur_kf, const double *S_cw_corr, int32_t n_w,
+                       const int32_t *window, double *out_S_corr, int64_t *cnt) {
+  if (n_w <= 0 || window[0] != cur_kf) return -1;
+  for (int32_t i = 0; i < m->n_mp; ++i) m->mp_corr_ref[i] = -1;
+  for (int32_t k = 0; k < m->n_kf; ++k) m->kf_in_window[k] = 0;
+  /* 1. S_iw^corr from the OLD poses */
+  double Tc_inv[13];
+  orc_sim3_inverse(m->kf_pose + 13 * (size_t)cur_kf, Tc_inv);
+  double *Sc = (double *)malloc(sizeof(double) * 13 * (size_t)n_w);
+  for (int32_t i = 0; i < n_w; ++i) {
+    int32_t k = window[i];
+    if (k == cur_kf) { memcpy(Sc + 13 * i, S_cw_corr, 13 * sizeof(double)); continue; }
+    double S_ic[13];
+    orc_sim3_compose(m->kf_pose + 13 * (size_t)k, Tc_inv, S_ic);
+    orc_sim3_compose(S_ic, S_cw_corr, Sc + 13 * i);
+  }
+  /* 2-4. owner = first window KF (list order) observing the non-bad MP */
+  int32_t *owner = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_mp > 0 ? m->n_mp : 1));
+  for (int32_t q = 0; q < m->n_mp; ++q) owner[q] = -1;
+  for (int32_t i = 0; i < n_w; ++i) {
+    int32_t k = window[i];
+    for (int32_t f = m->kf_feat_begin[k]; f < m->kf_feat_begin[k + 1]; ++f) {
+      int32_t q = m->feat_mp[f];
+      if (q < 0 || (m->mp_flags[q] & 1u)) continue;
+      if (owner[q] < 0) owner[q] = i;
+    }
+  }
+  for (int32_t q = 0; q < m->n_mp; ++q) {
+    if (owner[q] < 0) continue;
+    int32_t i = owner[q];
+    int32_t k = window[i];
+    double p[3], pc[3], pw[3], Sinv[13];
+    for (int j = 0; j < 3; ++j) p[j] = (double)m->mp_pos[3 * q + j];
+    orc_sim3_apply(m->kf_pose + 13 * (size_t)k, p, pc);       /* T_owner,w^old (p) */
+    orc_sim3_inverse(Sc + 13 * i, Sinv);
+    orc_sim3_apply(Sinv, pc, pw);                              /* inverse(S^corr)(.) */
+    for (int j = 0; j < 3; ++j) m->mp_pos[3 * q + j] = (float)pw[j];
+    m->mp_corr_ref[q] = k;
+    cnt[C_CORR_MP]++;
+  }
+  /* 5. write back T_iw <- SE3(S_iw^corr); keep S^corr as S^pre for O10 */
+  for (int32_t i = 0; i < n_w; ++i) {
+    int32_t k = window[i];
+    memcpy(m->kf_S_corr + 13 * (size_t)k, Sc + 13 * i, 13 * sizeof(double));
+    m->kf_in_window[k] = 1;
+    orc_sim3_se3(Sc + 13 * i, m->kf_pose + 13 * (size_t)k);
+    if (out_S_corr) memcpy(out_S_corr + 13 * i, Sc + 13 * i, 13 * sizeof(double));
+    cnt[C_CORR_KF]++;
+  }
+  free(owner);
+  free(Sc);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O10 propagation of the optimised Sim3 of every keyframe.    */
+/* ------------------------------------------------------------------------- */
+int orc_correct_all(orc_map *m, const double *S_opt, int64_t *cnt) {
+  double *Spre = (double *)malloc(sizeof(double) * 13 * (size_t)m->n_kf);
+  for (int32_t k = 0; k < m->n_kf; ++k)
+    memcpy(Spre + 13 * k, m->kf_in_window[k] ? m->kf_S_corr + 13 * (size_t)k
+                                             : m->kf_pose + 13 * (size_t)k, 13 * sizeof(double));
+  for (int32_t q = 0; q < m->n_mp; ++q) {
+    if (m->mp_flags[q] & 1u) continue;
+    int32_t r = m->mp_corr_ref[q] >= 0 ? m->mp_corr_ref[q] : m->mp_ref_kf[q];   /* A26 */
+    double p[3], pc[3], pw[3], Sinv[13];
+    for (int j = 0; j < 3; ++j) p[j] = (double)m->mp_pos[3 * q + j];
+    orc_sim3_apply(Spre + 13 * (size_t)r, p, pc);
+    orc_sim3_inverse(S_opt + 13 * (size_t)r, Sinv);
+    orc_sim3_apply(Sinv, pc, pw);
+    for (int j = 0; j < 3; ++j) m->mp_pos[3 * q + j] = (float)pw[j];
+    cnt[C_CORR_MP]++;
+  }
+  for (int32_t k = 0; k < m->n_kf; ++k) {
+    orc_sim3_se3(S_opt + 13 * (size_t)k, m->kf_pose + 13 * (size_t)k);
+    cnt[C_CORR_KF]++;
+  }
+  for (int32_t q = 0; q < m->n_mp; ++q) m->mp_corr_ref[q] = -1;   /* loop state consumed */
+  for (int32_t k = 0; k < m->n_kf; ++k) m->kf_in_window[k] = 0;
+  free(Spre);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O4-O9 loop fusion.                        */
+/*  phase 1 = PLAN over window positions [w_lo, w_hi) (winner + victim words)  */
+/*  phase 2 = APPLY from the (merged) winner/victim tables                    */
+/*  phase 3 = both, over the whole window                                     */
+/* ------------------------------------------------------------------------- */
+static void list_of(int32_t i, const int32_t *wb, const int32_t *mp_list, int32_t n_list,
+                    const int32_t **lst, int32_t *n) {
+  if (wb) { *lst = mp_list + wb[i]; *n = wb[i + 1] - wb[i]; }
+  else { *lst = mp_list; *n = n_list; }
+}
+
+int orc_fuse(orc_map *m, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_w,
+             const int32_t *window, const double *window_S, const int32_t *win_list_begin,
+             const int32_t *mp_list, int32_t n_list, const orc_params *prm,
+             int64_t *io_winner, int64_t *io_victim, int8_t *out_action,
+             int32_t *out_status, int64_t *out_best, double *out_uv, int32_t *out_ncand,
+             uint8_t *out_edge, int64_t *cnt) {
+  double scale[64];
+  orc_scale_table(m->n_levels, m->scale_factor, scale);
+  int64_t *woff = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_w + 1));
+  woff[0] = 0;
+  for (int32_t i = 0; i < n_w; ++i)
+    woff[i + 1] = woff[i] + (m->kf_feat_begin[window[i] + 1] - m->kf_feat_begin[window[i]]);
+  int64_t *qoff = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_w + 1));
+  qoff[0] = 0;
+  for (int32_t i = 0; i < n_w; ++i) {
+    const int32_t *l; int32_t n;
+    list_of(i, win_list_begin, mp_list, n_list, &l, &n);
+    qoff[i + 1] = qoff[i] + n;
+  }
+
+  if (phase & 1) {
+    for (int64_t j = 0; j < woff[n_w]; ++j) io_winner[j] = ORC_NONE;
+    for (int32_t q = 0; q < m->n_mp; ++q) io_victim[q] = ORC_NONE;
+    /* LoopSet = union of all window KFs' loop lists (A21) */
+    uint8_t *loopset = (uint8_t *)calloc((size_t)(m->n_mp > 0 ? m->n_mp : 1), 1);
+    for (int32_t i = 0; i < n_w; ++i) {
+      const int32_t *l; int32_t n;
+      list_of(i, win_list_begin, mp_list, n_list, &l, &n);
+      for (int32_t j = 0; j < n; ++j) loopset[l[j]] = 1;
+    }
+    for (int32_t i = w_lo; i < w_hi; ++i) {
+      int32_t k = window[i];
+      const double *S = window_S ? window_S + 13 * (size_t)i : m->kf_S_corr + 13 * (size_t)k;
+      int32_t nf = m->kf_feat_begin[k + 1] - m->kf_feat_begin[k];
+      int32_t f0 = m->kf_feat_begin[k];
+      int64_t *win = io_winner + woff[i];
+      const int32_t *l; int32_t n;
+      list_of(i, win_list_begin, mp_list, n_list, &l, &n);
+      for (int32_t j = 0; j < n; ++j) {
+        int32_t q = l[j];
+        orc_qres r;
+        cnt[C_QUERIES]++;
+        query_one(m, k, S, q, prm, NULL, 0, scale, &r);
+        int64_t qi = qoff[i] + j;
+        if (out_status) out_status[qi] = r.status;
+        if (out_uv) { out_uv[2 * qi] = r.u; out_uv[2 * qi + 1] = r.v; }
+        if (out_ncand) out_ncand[qi] = r.ncand;
+        if (out_edge) out_edge[qi] = (uint8_t)r.edge;
+        if (out_best) out_best[qi] = r.status < 0 ? (int64_t)r.status
+            : (((int64_t)r.best_h << 48) | ((int64_t)r.second_h << 32) | (uint32_t)r.best_f);
+        switch (r.status) {
+          case Q_BAD: cnt[C_SKIP_BAD]++; continue;
+          case Q_FOUND: cnt[C_SKIP_FOUND]++; continue;
+          case Q_DEPTH: cnt[C_CULL_DEPTH]++; continue;
+          case Q_BOUNDS: cnt[C_CULL_BOUNDS]++; continue;
+          case Q_DIST: cnt[C_CULL_DIST]++; continue;
+          case Q_ANGLE: cnt[C_CULL_ANGLE]++; continue;
+          default: break;
+        }
+        cnt[C_CANDIDATES] += r.ncand;
+        if (!proposal_ok(&r, prm, cnt)) continue;
+        int64_t key = ((int64_t)r.best_h << 32) | (int64_t)q;          /* O7, A17 */
+        if (key < win[r.best_f]) win[r.best_f] = key;
+      }
+      for (int32_t f = 0; f < nf; ++f) if (win[f] != ORC_NONE) cnt[C_WINNERS]++;
+      if (out_action) for (int32_t f = 0; f < nf; ++f) out_action[woff[i] + f] = 0;
+      if (prm->check_orientation) {
+        int64_t *before = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nf > 0 ? nf : 1));
+        memcpy(before, win, sizeof(int64_t) * (size_t)nf);
+        orientation_filter(m, k, win, nf, cnt);
+        if (out_action)
+          for (int32_t f = 0; f < nf; ++f)
+            if (before[f] != ORC_NONE && win[f] == ORC_NONE) out_action[woff[i] + f] = 4;
+        free(before);
+      }
+      for (int32_t f = 0; f < nf; ++f) {                                /* O9.1 actions */
+        if (win[f] == ORC_NONE) continue;
+        int32_t slot = m->feat_mp[f0 + f];
+        int8_t act;
+        if (slot < 0) { act = 1; cnt[C_ADD]++; }
+        else if (m->mp_flags[slot] & 1u) { act = 5; cnt[C_BAD_SLOT]++; }
+        else if (loopset[slot]) { act = 3; cnt[C_LOOP_SKIP]++; }
+        else {
+          act = 2; cnt[C_VICTIM_PROP]++;
+          if (win[f] < io_victim[slot]) io_victim[slot] = win[f];      /* A20, A21 */
+        }
+        if (out_action) out_action[woff[i] + f] = act;
+      }
+    }
+    free(loopset);
+  }
+
+  if (phase & 2) {                                                      /* O9.3 apply */
+    int32_t *win_pos = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_kf > 0 ? m->n_kf : 1));
+    for (int32_t k = 0; k < m->n_kf; ++k) win_pos[k] = -1;
+    for (int32_t i = 0; i < n_w; ++i) win_pos[window[i]] = i;
+    for (int32_t q = 0; q < m->n_mp; ++q) if (io_victim[q] != ORC_NONE) cnt[C_VICTIMS]++;
+    for (int32_t k = 0; k < m->n_kf; ++k) {
+      int32_t f0 = m->kf_feat_begin[k], nf = m->kf_feat_begin[k + 1] - f0;
+      int32_t *nv = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nf > 0 ? nf : 1));
+      int *prio = (int *)malloc(sizeof(int) * (size_t)(nf > 0 ? nf : 1));
+      for (int32_t f = 0; f < nf; ++f) {
+        int32_t s = m->feat_mp[f0 + f];
+        nv[f] = s; prio[f] = 0;
+        if (s >= 0 && io_victim[s] != ORC_NONE) {
+          nv[f] = (int32_t)(io_victim[s] & 0xffffffff); prio[f] = 2; cnt[C_REWIRED]++;
+        } else if (s < 0 && win_pos[k] >= 0 && io_winner[woff[win_pos[k]] + f] != ORC_NONE) {
+          nv[f] = (int32_t)(io_winner[woff[win_pos[k]] + f] & 0xffffffff); prio[f] = 1;
+        }
+      }
+      /* (iii) keep the least (priority, f) slot of every MP occupying > 1 slot (A22) */
+      uint8_t *clear = (uint8_t *)calloc((size_t)(nf > 0 ? nf : 1), 1);
+      for (int32_t f = 0; f < nf; ++f) {
+        if (nv[f] < 0) continue;
+        for (int32_t g = 0; g < nf; ++g)
+          if (g != f && nv[g] == nv[f] && (prio[g] < prio[f] || (prio[g] == prio[f] && g < f)))
+            clear[f] = 1;
+      }
+      for (int32_t f = 0; f < nf; ++f) {
+        if (clear[f]) { nv[f] = -1; cnt[C_DUP_CLEARED]++; }
+        else if (prio[f] == 1) cnt[C_ADDED]++;
+        m->feat_mp[f0 + f] = nv[f];
+      }
+      free(clear);
+      free(nv); free(prio);
+    }
+    for (int32_t q = 0; q < m->n_mp; ++q) {                             /* (iv) */
+      if (io_victim[q] == ORC_NONE) continue;
+      m->mp_flags[q] |= 1u;
+      m->mp_replaced_by[q] = (int32_t)(io_victim[q] & 0xffffffff);
+    }
+    for (int32_t q = 0; q < m->n_mp; ++q) m->mp_nobs[q] = 0;             /* (v) recount */
+    for (int32_t f = 0; f < m->n_feat; ++f)
+      if (m->feat_mp[f] >= 0) m->mp_nobs[m->feat_mp[f]]++;
+    free(win_pos);
+  }
+  free(woff);
+  free(qoff);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Projection search over (keyframe, Sim3, parameter set, MP list) pairs:    */
+/* PS1, PS2a||PS2b, PS3a-c. Read-only.      */
+/* ------------------------------------------------------------------------- */
+int orc_search_by_projection(const orc_map *m, int32_t n_pairs, const int32_t *pair_kf,
+                             const double *pair_S, const int32_t *pair_param,
+                             const orc_params *params, const int32_t *pair_list_begin,
+                             const int32_t *mp_list, const int32_t *pair_taken,
+                             int32_t *out_feat_mp, int32_t *out_feat_dist, int64_t *out_best,
+                             double *out_uv, int32_t *out_ncand, uint8_t *out_edge,
+                             int64_t *cnt /* [n_pairs][C_N] */) {
+  double scale[64];
+  orc_scale_table(m->n_levels, m->scale_factor, scale);
+  int64_t off = 0;
+  for (int32_t p = 0; p < n_pairs; ++p) {
+    int32_t k = pair_kf[p];
+    int32_t nf = m->kf_feat_begin[k + 1] - m->kf_feat_begin[k];
+    const orc_params *prm = &params[pair_param[p]];
+    const int32_t *taken = pair_taken ? pair_taken + off : NULL;
+    int64_t *c = cnt + (size_t)C_N * p;
+    int64_t *win = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nf > 0 ? nf : 1));
+    for (int32_t f = 0; f < nf; ++f) win[f] = ORC_NONE;
+    for (int32_t j = pair_list_begin[p]; j < pair_list_begin[p + 1]; ++j) {
+      int32_t q = mp_list[j];
+      orc_qres r;
+      c[C_QUERIES]++;
+      query_one(m, k, pair_S + 13 * (size_t)p, q, prm, taken, 1, scale, &r);
+      if (out_uv) { out_uv[2 * j] = r.u; out_uv[2 * j + 1] = r.v; }
+      if (out_ncand) out_ncand[j] = r.ncand;
+      if (out_edge) out_edge[j] = (uint8_t)r.edge;
+      if (out_best) out_best[j] = r.status < 0 ? (int64_t)r.status
+          : (((int64_t)r.best_h << 48) | ((int64_t)r.second_h << 32) | (uint32_t)r.best_f);
+      switch (r.status) {
+        case Q_BAD: c[C_SKIP_BAD]++; continue;
+        case Q_FOUND: c[C_SKIP_FOUND]++; continue;
+        case Q_DEPTH: c[C_CULL_DEPTH]++; continue;
+        case Q_BOUNDS: c[C_CULL_BOUNDS]++; continue;
+        case Q_DIST: c[C_CULL_DIST]++; continue;
+        case Q_ANGLE: c[C_CULL_ANGLE]++; continue;
+        default: break;
+      }
+      c[C_CANDIDATES] += r.ncand;
+      if (!proposal_ok(&r, prm, c)) continue;
+      int64_t key = ((int64_t)r.best_h << 32) | (int64_t)q;
+      if (key < win[r.best_f]) win[r.best_f] = key;
+    }
+    for (int32_t f = 0; f < nf; ++f) if (win[f] != ORC_NONE) c[C_WINNERS]++;
+    if (prm->check_orientation) orientation_filter(m, k, win, nf, c);
+    for (int32_t f = 0; f < nf; ++f) {
+      int32_t t = taken ? taken[f] : -1;
+      if (t >= 0) { out_feat_mp[off + f] = t; out_feat_dist[off + f] = -1; }
+      else if (win[f] != ORC_NONE) {
+        out_feat_mp[off + f] = (int32_t)(win[f] & 0xffffffff);
+        out_feat_dist[off + f] = (int32_t)(win[f] >> 32);
+      } else { out_feat_mp[off + f] = -1; out_feat_dist[off + f] = -1; }
+    }
+    free(win);
+    off += nf;
+  }
+  return 0;
+}
+
+int32_t orc_ncount(void) { return C_N; }
