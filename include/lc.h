@@ -1,0 +1,351 @@
+/*
+ * lc.h -- C ABI of the B200 (sm_100a) loop-closing fuse/correct core.
+ *
+ * The data-parallel core of the GPU loop-closing module of arXiv 2603.17201
+ * ("FastLoop", an ORB-SLAM3 loop closer), re-designed for B200:
+ *
+ *   lc_upload_map            GPU-resident keyframe / map-point storage, each
+ *                            keyframe transferred once as a "lightweight wrapper
+ *                            structure" (§IV.A; §IV.E)
+ *   lc_correct_sim3          Sim3 correction of the window keyframes and the map
+ *                            points they observe (§III.B), and
+ *                            propagation of optimised keyframe Sim3s to the whole
+ *                            map (§IV.F)
+ *   lc_fuse                  loop fusion: project the loop map points into every
+ *                            connected keyframe, match descriptors "within close
+ *                            spatial proximity", merge duplicates (
+ *                            PAPER.md:226-228 §IV.D.3)
+ *   lc_search_by_projection  batched projection search PS1 / PS2a||PS2b / PS3a-c
+ *                            over (keyframe, Sim3, parameter set) pairs, results
+ *                            returned as one batch per pair (§IV.C;
+ *                            PAPER.md:215-224 §IV.D.1-2)
+ *
+ * The paper states no matching constants or tie-breaks; the readings this ABI
+ * implements are listed in DESIGN.md ("Readings", A1-A32) and are identical to
+ * the CPU oracle's (oracle/lc_oracle.c), which shares no code with this library.
+ *
+ * Conventions
+ *  - Poses are world->camera Sim3 transforms, p_c = s * (R p) + t, R row-major
+ *    (reading A1). Keyframe poses are SE3 (s = 1) in the store.
+ *  - Indices are dense and 0-based: keyframe k, map point q, feature f. A
+ *    keyframe's features are the global range [kf_feat_begin[k], kf_feat_begin[k+1]);
+ *    "local feature index" = global index - kf_feat_begin[k].
+ *  - Packed match words: (H << 32) | q as int64, H = Hamming distance in
+ *    [0, 256]; LC_NONE (INT64_MAX) = empty. Signed int64 so that an NCCL MIN
+ *    all-reduce merges them (lowest H, then lowest q).
+ *  - Pointers marked [host|dev] may be host memory (pageable or pinned) or
+ *    device memory of the context's device; the library detects which
+ *    (cudaPointerGetAttributes) and copies host data through its own pinned
+ *    staging. Pointers marked [host] must be host memory (small control
+ *    arrays the library validates and uses to configure launches).
+ *  - Asynchrony: every call enqueues work on `cuda_stream` (a cudaStream_t,
+ *    NULL = legacy default stream) and returns; outputs (device or host) are
+ *    valid once that stream has reached the call's work. Inputs must stay valid
+ *    until then (as with cuBLAS). A context is single-stream and not
+ *    thread-safe; use one per device per process.
+ *  - Ownership: the library owns the device map store (allocated once by
+ *    lc_upload_map and reused) and a scratch arena that only grows (no
+ *    allocation in steady state). Caller buffers are borrowed for the call.
+ *  - Errors: every call returns an lc_status; no C++ exception crosses the ABI.
+ *    LC_EINVAL / LC_ERANGE / LC_ECAPACITY / LC_ESTATE are detected before any
+ *    work is enqueued. LC_ECUDA makes the context unusable until lc_destroy.
+ *    lc_last_error() describes the last failure.
+ */
+#ifndef LC_H_
+#define LC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LC_ABI_VERSION 1
+#define LC_NONE INT64_MAX
+#define LC_MAX_FEAT_PER_KF 8192
+#define LC_MAX_LEVELS 16
+
+typedef struct lc_ctx lc_ctx;
+
+typedef enum {
+  LC_OK = 0,
+  LC_EINVAL = -1,     /* malformed argument (null required pointer, bad size, bad params) */
+  LC_ESTATE = -2,     /* call not valid in the context's state (e.g. no map uploaded)    */
+  LC_ECUDA = -3,      /* CUDA runtime failure; context unusable                         */
+  LC_ENOMEM = -4,     /* device or pinned allocation failed                             */
+  LC_ERANGE = -5,     /* index out of range (keyframe, map point, feature, octave)       */
+  LC_ECAPACITY = -6   /* a per-keyframe limit was exceeded (LC_MAX_FEAT_PER_KF)          */
+} lc_status;
+
+/* Sim3 / SE3 transform: p' = s * (R p) + t, R row-major. 104 bytes. */
+typedef struct { double R[9]; double t[3]; double s; } lc_sim3;
+
+/* Camera: model 0 = pinhole, 1 = Kannala-Brandt-8 (reading A29). Image bounds
+ * are half-open [min_x, max_x) x [min_y, max_y) (reading A4). */
+typedef struct {
+  int32_t model;
+  int32_t reserved;
+  double fx, fy, cx, cy;
+  double k[4];
+  double min_x, max_x, min_y, max_y;
+} lc_camera;
+
+/* Scale pyramid and grid: n_levels (<= LC_MAX_LEVELS), scale_factor (ORB: 8, 1.2),
+ * per-keyframe feature grid grid_cols x grid_rows (ORB: 64 x 48). */
+typedef struct {
+  int32_t n_levels;
+  int32_t grid_cols, grid_rows;
+  int32_t reserved;
+  double scale_factor;
+} lc_map_params;
+
+/* SoA view of the map to upload. All arrays [host|dev], borrowed for the call. */
+typedef struct {
+  int32_t n_kf, n_feat, n_mp;
+  int32_t reserved;
+  const lc_sim3* kf_pose;        /* [n_kf] world->camera, s = 1                     */
+  const int32_t* kf_cam;         /* [n_kf] camera index                             */
+  const int32_t* kf_feat_begin;  /* [n_kf+1] CSR into the feature arrays            */
+  const float* feat_uv;          /* [n_feat][2] keypoint pixel (u, v)               */
+  const uint8_t* feat_octave;    /* [n_feat] pyramid level < n_levels               */
+  const float* feat_angle;       /* [n_feat] keypoint angle, degrees                */
+  const uint8_t* feat_desc;      /* [n_feat][32] 256-bit ORB descriptor             */
+  const int32_t* feat_mp;        /* [n_feat] associated map point, -1 = none        */
+  const float* mp_pos;           /* [n_mp][3] world position                        */
+  const float* mp_normal;        /* [n_mp][3] mean viewing direction (unit)         */
+  const float* mp_max_dist;      /* [n_mp] scale-invariance max distance dmax       */
+  const uint8_t* mp_desc;        /* [n_mp][32] representative descriptor           */
+  const float* mp_angle;         /* [n_mp] angle of the reference observation, deg  */
+  const int32_t* mp_ref_kf;      /* [n_mp] reference keyframe                       */
+  const uint8_t* mp_flags;       /* [n_mp] bit0 = bad                               */
+} lc_map_view;
+
+/* Mutable map state, for download/inspection. Any pointer may be NULL (skipped). */
+typedef struct {
+  lc_sim3* kf_pose;              /* [n_kf]                                          */
+  int32_t* feat_mp;              /* [n_feat] original feature order                 */
+  float* mp_pos;                 /* [n_mp][3]                                       */
+  uint8_t* mp_flags;             /* [n_mp]                                          */
+  int32_t* mp_replaced_by;       /* [n_mp] survivor of a fused victim, -1 = none    */
+  int32_t* mp_nobs;              /* [n_mp] number of slots holding the map point    */
+} lc_map_state;
+
+/* Matching parameters (readings A8-A15). th: window half-size at level 0 in px
+ * (Fuse: 4); max_hamming: inclusive threshold in [0, 256]; ratio test enabled
+ * iff ratio_den > 0, rejecting iff ratio_den*best > ratio_num*second;
+ * check_orientation: 30-bin rotation histogram, keep the three maxima. */
+typedef struct {
+  int32_t th;
+  int32_t max_hamming;
+  int32_t ratio_num, ratio_den;
+  int32_t check_orientation;
+} lc_match_params;
+
+/* Optional per-query debug outputs [host|dev], indexed by query (see lc_fuse /
+ * lc_search_by_projection). best: status < 0 (cull code, LC_Q_*) or
+ * (H_best << 48) | (H_second << 32) | uint32(local feature f_best), with
+ * H_best = H_second = 256 and f = 0xFFFFFFFF when the window is empty;
+ * uv: projected pixel (fp64, 2 per query; 0 when culled before projection);
+ * ncand: number of candidates |C(k,q)|. Any member may be NULL. */
+typedef struct {
+  int64_t* best;
+  double* uv;
+  int32_t* ncand;
+} lc_query_debug;
+
+/* query cull codes in lc_query_debug.best */
+enum { LC_Q_BAD = -1, LC_Q_FOUND = -2, LC_Q_DEPTH = -3, LC_Q_BOUNDS = -4,
+       LC_Q_DIST = -5, LC_Q_ANGLE = -6 };
+
+/* Counter slots of out_counts (int64, overwritten by each call). */
+enum {
+  LC_COUNT_QUERIES = 0,    /* (keyframe, map point) queries                          */
+  LC_COUNT_SKIP_BAD,       /* query map point flagged bad                            */
+  LC_COUNT_SKIP_FOUND,     /* map point already in the keyframe (reading A19)        */
+  LC_COUNT_CULL_DEPTH,     /* z <= 0                                                 */
+  LC_COUNT_CULL_BOUNDS,    /* projection outside the image                           */
+  LC_COUNT_CULL_DIST,      /* outside [0.8 dmax / s_{L-1}, 1.2 dmax]                 */
+  LC_COUNT_CULL_ANGLE,     /* PO . n < 0.5 |PO|                                      */
+  LC_COUNT_CANDIDATES,     /* sum |C(k,q)|: candidate Hamming matches (the metric)   */
+  LC_COUNT_NO_CAND,        /* queries with an empty window                           */
+  LC_COUNT_OVER_TH,        /* best H > max_hamming                                   */
+  LC_COUNT_RATIO_REJ,      /* ratio test failed                                      */
+  LC_COUNT_PROPOSALS,      /* (keyframe, feature, q, H) proposals                    */
+  LC_COUNT_WINNERS,        /* features with a winning proposal                       */
+  LC_COUNT_ORIENT_REJ,     /* winners removed by the rotation histogram              */
+  LC_COUNT_ADD,            /* fuse: winner on an empty slot                          */
+  LC_COUNT_VICTIM_PROP,    /* fuse: winner on a slot holding a fusable map point     */
+  LC_COUNT_LOOP_SKIP,      /* fuse: slot holds a loop map point (reading A21)        */
+  LC_COUNT_BAD_SLOT,       /* fuse: slot holds a bad map point                       */
+  LC_COUNT_VICTIMS,        /* fuse apply: distinct victims                           */
+  LC_COUNT_REWIRED,        /* fuse apply: slots redirected to a survivor             */
+  LC_COUNT_DUP_CLEARED,    /* fuse apply: duplicate slots cleared (reading A22)      */
+  LC_COUNT_ADDED,          /* fuse apply: new associations kept                      */
+  LC_COUNT_CORR_KF,        /* correction: keyframe poses written                     */
+  LC_COUNT_CORR_MP,        /* correction: map points moved                           */
+  LC_NCOUNT
+};
+
+/* lc_correct_sim3 modes */
+#define LC_CORRECT_WINDOW 1
+#define LC_CORRECT_ALL 2
+/* lc_fuse phases */
+#define LC_FUSE_PLAN 1
+#define LC_FUSE_APPLY 2
+#define LC_FUSE_ALL 3
+
+/* ---------------------------------------------------------------------------
+ * Context
+ * ------------------------------------------------------------------------- */
+
+/* Create a context on CUDA device `device` (sm_100a). *out receives it.
+ * Errors: LC_EINVAL (out NULL), LC_ECUDA (no such device / not sm_100). */
+lc_status lc_create(lc_ctx** out, int32_t device);
+
+/* Destroy a context and free everything it owns (synchronises its device). */
+lc_status lc_destroy(lc_ctx* ctx);
+
+/* Message of the last failure on ctx (static storage owned by ctx), or of the
+ * last lc_create failure when ctx is NULL. Never NULL. */
+const char* lc_last_error(const lc_ctx* ctx);
+
+/* Number of this library's kernels launched by ctx since creation (evidence
+ * for the benchmark's gpu_launches). */
+int64_t lc_kernel_launches(const lc_ctx* ctx);
+
+/* ---------------------------------------------------------------------------
+ * lc_upload_map -- GPU-resident keyframe storage.
+ *
+ * Packs the SoA view into the device store: map-point records (position, dmax,
+ * normal, angle, descriptor) as 64-byte AoS rows; keyframe features re-ordered
+ * cell-major per keyframe by a GPU counting sort into grid_cols x grid_rows
+ * cells over [min_x,max_x) x [min_y,max_y) of the keyframe's camera (cell =
+ * floor((u-min_x) * cols / (max_x-min_x)), clamped), keeping the original local
+ * index; association slots, angles and poses in original order. Replaces any
+ * previous map (the store is re-allocated only if it grows). Synchronises the
+ * stream before returning (validation reads back one error count).
+ *   map   [host] struct; its arrays [host|dev]
+ *   cams  [host] n_cams cameras; prm [host]
+ * Errors: LC_EINVAL (null arrays, n_* < 0, non-monotone kf_feat_begin, camera
+ * bounds empty, n_levels outside [1, LC_MAX_LEVELS], scale_factor <= 1, grid
+ * outside [1, 1024]^2), LC_ERANGE (feat_mp / mp_ref_kf / kf_cam / octave out of
+ * range), LC_ECAPACITY (a keyframe with more than LC_MAX_FEAT_PER_KF features),
+ * LC_ENOMEM, LC_ECUDA. */
+lc_status lc_upload_map(lc_ctx* ctx, const lc_map_view* map, const lc_camera* cams,
+                        int32_t n_cams, const lc_map_params* prm, void* cuda_stream);
+
+/* Copy the mutable map state out (any member NULL = skipped). [host|dev]. */
+lc_status lc_download_map(lc_ctx* ctx, const lc_map_state* out, void* cuda_stream);
+
+/* Save / restore the mutable map state (poses, associations, positions, flags,
+ * replaced_by, n_obs, loop state) to / from a device-side copy: checkpoint and
+ * resume of the store without host round trips. restore before save -> LC_ESTATE. */
+lc_status lc_state_save(lc_ctx* ctx, void* cuda_stream);
+lc_status lc_state_restore(lc_ctx* ctx, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * lc_correct_sim3 -- Sim3 pose correction (§III.B).
+ *
+ * mode LC_CORRECT_WINDOW (reading O3; old poses read before any write-back):
+ *   for window position i (window_kf[0] must be cur_kf):
+ *     S_i^corr = (T_iw * inverse(T_cw)) * S_cw_corr   (S_c^corr = S_cw_corr);
+ *   every non-bad map point observed by the window is re-anchored through its
+ *   owner o = the first window keyframe (list order) observing it:
+ *     p <- fl32( inverse(S_o^corr)( T_ow(p) ) );
+ *   then T_iw <- SE3(S_i^corr) = (R, t/s). S_i^corr is kept (loop state) as the
+ *   default projection transform of lc_fuse and as S^pre of LC_CORRECT_ALL.
+ *   cur_kf, S_cw_corr [host]; n_window >= 1 distinct keyframes window_kf [host].
+ *   out_S_corr [host|dev] nullable, [n_window].
+ * mode LC_CORRECT_ALL (reading O10; propagation after pose-graph optimisation):
+ *   S_k^pre = S_k^corr if k was in the last window, else T_kw;
+ *   every non-bad map point p <- fl32( inverse(S_r^opt)( S_r^pre(p) ) ) with
+ *   r = its window owner if corrected by the last WINDOW call, else mp_ref_kf;
+ *   then T_kw <- SE3(S_k^opt) for every k. Consumes the loop state.
+ *   S_opt [host|dev] [n_kf]. cur_kf / S_cw_corr / window ignored.
+ * All transforms are evaluated in fp64 in the order of DESIGN.md "Sim3
+ * arithmetic"; positions are stored fp32 (round to nearest).
+ * out_counts [host|dev] nullable, [LC_NCOUNT] (CORR_KF, CORR_MP).
+ * Errors: LC_ESTATE (no map), LC_EINVAL (bad mode, n_window < 1, window_kf[0]
+ * != cur_kf, duplicate window keyframes, null S), LC_ERANGE (keyframe index). */
+lc_status lc_correct_sim3(lc_ctx* ctx, int32_t mode, int32_t cur_kf, const lc_sim3* S_cw_corr,
+                          int32_t n_window, const int32_t* window_kf, const lc_sim3* S_opt,
+                          lc_sim3* out_S_corr, int64_t* out_counts, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * lc_fuse -- loop fusion (§IV.D.3), readings O4-O9.
+ *
+ * Every window keyframe k (window position i) is matched against its loop
+ * map-point list L_i (win_list_begin != NULL: CSR mp_list[win_list_begin[i] ..
+ * win_list_begin[i+1]); NULL: the whole mp_list for every keyframe, as
+ * ORB-SLAM3's single loop-point list). For each query (k, q), q in L_i, not bad
+ * and not already associated in k: project with SE3(S_k) (window_S[i], or the
+ * S^corr stored by the last WINDOW correction when window_S is NULL), cull
+ * (depth, bounds, distance range, view angle), predict level n, take the
+ * candidates f of k with |u_f-u| < r, |v_f-v| < r, r = th * 1.2^n, octave in
+ * [n-1, n]; best = argmin (H, f), second = min H of the rest (256 if none);
+ * propose (k, f_best, (H<<32)|q) if H <= max_hamming and the ratio test passes.
+ * Per feature the least proposal wins; the orientation filter removes winners
+ * per keyframe. A winner on an empty slot is an ADD; on a slot holding a bad
+ * map point or a map point of LoopSet (union of all L_i) nothing; otherwise it
+ * proposes its word as the victim word of the slot's map point m (least wins).
+ * APPLY (snapshot semantics, reading A18): every slot in the map holding a
+ * victim m is redirected to survivor(m) = low 32 bits of victim[m]; ADDs fill
+ * their slots; in each keyframe a map point occupying several slots keeps the
+ * least (priority, f) slot, priority 0 unchanged / 1 ADD / 2 redirected; victims
+ * get flags |= bad and replaced_by = survivor; n_obs is updated.
+ *
+ * phase LC_FUSE_PLAN  : steps up to the victim words, for window positions
+ *                       [w_lo, w_hi) only (a keyframe shard); initialises all of
+ *                       io_winner and io_victim to LC_NONE first. Map unchanged.
+ * phase LC_FUSE_APPLY : apply from io_winner / io_victim (e.g. after an NCCL MIN
+ *                       all-reduce of the shards' tables). w_lo / w_hi ignored.
+ * phase LC_FUSE_ALL   : PLAN over the whole window, then APPLY.
+ *   window_kf, window_S (nullable), win_list_begin (nullable) [host], n_window >= 1
+ *   distinct keyframes; mp_list [host|dev] n_list entries, each list ascending
+ *   and unique (not checked on device; duplicates give duplicate queries).
+ *   io_winner [host|dev] nullable (internal), [sum_i F(window_kf[i])] window-major,
+ *     local feature order: the surviving winner word per window feature.
+ *   io_victim [host|dev] nullable (internal), [n_mp].
+ *   out_action [host|dev] nullable, [sum_i F(window_kf[i])]: 0 none, 1 add,
+ *     2 victim proposal, 3 loop point in slot, 4 orientation-rejected, 5 bad slot.
+ *   dbg [host] nullable; query index = win_list_begin[i] + j (CSR) or
+ *     i * n_list + j (shared list) for the j-th entry of L_i.
+ *   out_counts [host|dev] nullable, [LC_NCOUNT].
+ * Errors: LC_ESTATE (no map, or window_S NULL and a window keyframe without a
+ * stored correction), LC_EINVAL, LC_ERANGE (keyframe index), LC_ECAPACITY. */
+lc_status lc_fuse(lc_ctx* ctx, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_window,
+                  const int32_t* window_kf, const lc_sim3* window_S,
+                  const int32_t* win_list_begin, const int32_t* mp_list, int64_t n_list,
+                  const lc_match_params* params, int64_t* io_winner, int64_t* io_victim,
+                  int8_t* out_action, const lc_query_debug* dbg, int64_t* out_counts,
+                  void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * lc_search_by_projection -- batched read-only projection search
+ * (PAPER.md:200). Pair p = (keyframe pair_kf[p], transform
+ * pair_S[p], parameter set params[pair_param[p]], list mp_list[pair_list_begin[p]
+ * .. pair_list_begin[p+1])). Same projection/matching/conflict/orientation steps
+ * as lc_fuse, except "already found" (reading A19): features whose entry in
+ * pair_taken is >= 0 are not candidates and map points present in pair_taken are
+ * skipped. No fusion; the map is not modified.
+ *   pair_kf, pair_S, pair_param, params, pair_list_begin [host]; mp_list [host|dev].
+ *   pair_taken [host|dev] nullable, pair-major [sum_p F(pair_kf[p])], -1 = free.
+ *   out_feat_mp / out_feat_dist [host|dev] pair-major [sum_p F(pair_kf[p])]:
+ *     taken entries are copied (dist -1); otherwise the winning map point and
+ *     its H, or -1 / -1.
+ *   dbg [host] nullable; query index = position in mp_list.
+ *   out_counts [host|dev] nullable, [n_pairs][LC_NCOUNT].
+ * Errors: LC_ESTATE (no map), LC_EINVAL (n_pairs < 0, n_params < 1, bad params,
+ * pair_param out of range, null S), LC_ERANGE (keyframe index). */
+lc_status lc_search_by_projection(lc_ctx* ctx, int32_t n_pairs, const int32_t* pair_kf,
+                                  const lc_sim3* pair_S, const int32_t* pair_param,
+                                  const lc_match_params* params, int32_t n_params,
+                                  const int32_t* pair_list_begin, const int32_t* mp_list,
+                                  const int32_t* pair_taken, int32_t* out_feat_mp,
+                                  int32_t* out_feat_dist, const lc_query_debug* dbg,
+                                  int64_t* out_counts, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LC_H_ */

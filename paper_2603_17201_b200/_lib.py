@@ -1,0 +1,113 @@
+"""ctypes declarations of include/lc.h (argument marshalling only).
+
+Loads the in-tree liblc.so and fails loudly when it is missing: there is no CPU
+fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "liblc.so")
+
+LC_OK, LC_EINVAL, LC_ESTATE, LC_ECUDA, LC_ENOMEM, LC_ERANGE, LC_ECAPACITY = 0, -1, -2, -3, -4, -5, -6
+STATUS_NAMES = {0: "LC_OK", -1: "LC_EINVAL", -2: "LC_ESTATE", -3: "LC_ECUDA", -4: "LC_ENOMEM",
+                -5: "LC_ERANGE", -6: "LC_ECAPACITY"}
+LC_NONE = (1 << 63) - 1
+LC_CORRECT_WINDOW, LC_CORRECT_ALL = 1, 2
+LC_FUSE_PLAN, LC_FUSE_APPLY, LC_FUSE_ALL = 1, 2, 3
+COUNTER_NAMES = [
+    "queries", "skip_bad", "skip_found", "cull_depth", "cull_bounds", "cull_dist",
+    "cull_angle", "candidates", "no_cand", "over_th", "ratio_rej", "proposals",
+    "winners", "orient_rej", "add", "victim_prop", "loop_skip", "bad_slot",
+    "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
+]
+LC_NCOUNT = len(COUNTER_NAMES)
+
+
+class lc_sim3(C.Structure):
+    _fields_ = [("R", C.c_double * 9), ("t", C.c_double * 3), ("s", C.c_double)]
+
+
+class lc_camera(C.Structure):
+    _fields_ = [("model", C.c_int32), ("reserved", C.c_int32), ("fx", C.c_double),
+                ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double), ("k", C.c_double * 4),
+                ("min_x", C.c_double), ("max_x", C.c_double), ("min_y", C.c_double),
+                ("max_y", C.c_double)]
+
+
+class lc_map_params(C.Structure):
+    _fields_ = [("n_levels", C.c_int32), ("grid_cols", C.c_int32), ("grid_rows", C.c_int32),
+                ("reserved", C.c_int32), ("scale_factor", C.c_double)]
+
+
+class lc_map_view(C.Structure):
+    _fields_ = [("n_kf", C.c_int32), ("n_feat", C.c_int32), ("n_mp", C.c_int32),
+                ("reserved", C.c_int32)] + [
+        (n, C.c_void_p) for n in ("kf_pose", "kf_cam", "kf_feat_begin", "feat_uv", "feat_octave",
+                                  "feat_angle", "feat_desc", "feat_mp", "mp_pos", "mp_normal",
+                                  "mp_max_dist", "mp_desc", "mp_angle", "mp_ref_kf", "mp_flags")]
+
+
+class lc_map_state(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("kf_pose", "feat_mp", "mp_pos", "mp_flags",
+                                          "mp_replaced_by", "mp_nobs")]
+
+
+class lc_match_params(C.Structure):
+    _fields_ = [("th", C.c_int32), ("max_hamming", C.c_int32), ("ratio_num", C.c_int32),
+                ("ratio_den", C.c_int32), ("check_orientation", C.c_int32)]
+
+
+class lc_query_debug(C.Structure):
+    _fields_ = [("best", C.c_void_p), ("uv", C.c_void_p), ("ncand", C.c_void_p)]
+
+
+class LcError(RuntimeError):
+    def __init__(self, fn, status, msg):
+        super().__init__(f"{fn} failed: {STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def load():
+    """Load liblc.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"liblc.so not found at {LIB_PATH}; run paper_2603_17201_b200/build.py "
+                           "(nvcc, sm_100a). There is no CPU fallback.")
+    lib = C.CDLL(LIB_PATH)
+    vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    P = C.POINTER
+    sig = {
+        "lc_create": (i32, [P(vp), i32]),
+        "lc_destroy": (i32, [vp]),
+        "lc_last_error": (C.c_char_p, [vp]),
+        "lc_kernel_launches": (i64, [vp]),
+        "lc_upload_map": (i32, [vp, P(lc_map_view), vp, i32, P(lc_map_params), vp]),
+        "lc_download_map": (i32, [vp, P(lc_map_state), vp]),
+        "lc_state_save": (i32, [vp, vp]),
+        "lc_state_restore": (i32, [vp, vp]),
+        "lc_correct_sim3": (i32, [vp, i32, i32, vp, i32, vp, vp, vp, vp, vp]),
+        "lc_fuse": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, vp, i64, P(lc_match_params), vp,
+                          vp, vp, vp, vp, vp]),
+        "lc_search_by_projection": (i32, [vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp,
+                                          vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    return ["lc_create", "lc_destroy", "lc_last_error", "lc_kernel_launches", "lc_upload_map",
+            "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse",
+            "lc_search_by_projection"]

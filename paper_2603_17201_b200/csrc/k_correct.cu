@@ -1,0 +1,211 @@
+// k_correct.cu -- Sim3 correction of keyframes and map points.
+//
+// WINDOW (§III.B "correcting their poses using the estimated Sim3
+// transformation"; reading O3) and ALL ("propagates the loop
+// correction to the rest of the map"; reading O10). Both are
+// streaming passes over the map-point records (HBM-bound); the per-keyframe
+// transforms are computed once into a small scratch table first so every
+// point applies two precomputed Sim3s in fp64 (13 doubles each, L1/L2 resident).
+#include <cuda_runtime.h>
+#include <climits>
+
+#include "lc_internal.cuh"
+
+namespace {
+
+// scratch layout for WINDOW: per window position i: S_corr[13] | inv(S_corr)[13] | T_old[13]
+constexpr int WSTR = 39;
+
+__global__ void k_win_prep(int n_kf, int n_mp, int32_t* __restrict__ owner,
+                           int32_t* __restrict__ kf_in_win) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_mp || i < n_kf; i += stride) {
+    if (i < n_mp) owner[i] = INT_MAX;
+    if (i < n_kf) kf_in_win[i] = 0;
+  }
+}
+
+__global__ void k_win_sim3(int n_w, int cur_pos, const int32_t* __restrict__ window,
+                           const double* __restrict__ kf_pose, const double* __restrict__ Scw,
+                           double* __restrict__ scr, double* __restrict__ kf_S_corr,
+                           int32_t* __restrict__ kf_in_win) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_w) return;
+  const int k = window[i];
+  const int c = window[cur_pos];
+  double T[13], S[13], Tci[13], Sic[13], Si[13];
+  for (int j = 0; j < 13; ++j) T[j] = kf_pose[13 * (size_t)k + j];
+  if (i == cur_pos) {
+    for (int j = 0; j < 13; ++j) S[j] = Scw[j];
+  } else {
+    double Tc[13];
+    for (int j = 0; j < 13; ++j) Tc[j] = kf_pose[13 * (size_t)c + j];
+    lc_sim3_inverse(Tc, Tci);
+    lc_sim3_compose(T, Tci, Sic);   // S_ic = T_iw * inverse(T_cw)
+    lc_sim3_compose(Sic, Scw, S);   // S_iw^corr = S_ic * S_cw^corr
+  }
+  lc_sim3_inverse(S, Si);
+  double* o = scr + (size_t)WSTR * i;
+  for (int j = 0; j < 13; ++j) { o[j] = S[j]; o[13 + j] = Si[j]; o[26 + j] = T[j]; }
+  for (int j = 0; j < 13; ++j) kf_S_corr[13 * (size_t)k + j] = S[j];
+  kf_in_win[k] = 1;
+}
+
+// owner = first window position (list order) observing the non-bad map point
+__global__ void __launch_bounds__(LC_NTHREADS) k_win_mark(const int32_t* __restrict__ window,
+                                                          const int32_t* __restrict__ kf_fbeg,
+                                                          const int32_t* __restrict__ feat_mp,
+                                                          const uint8_t* __restrict__ mp_flags,
+                                                          int32_t* __restrict__ owner) {
+  const int i = blockIdx.x;
+  const int k = window[i];
+  const int f0 = kf_fbeg[k], f1 = kf_fbeg[k + 1];
+  for (int f = f0 + threadIdx.x; f < f1; f += blockDim.x) {
+    int m = feat_mp[f];
+    if (m < 0 || (mp_flags[m] & 1u)) continue;
+    atomicMin(&owner[m], i);
+  }
+}
+
+__device__ __forceinline__ void warp_count(uint32_t n, unsigned long long* dst) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(dst, (unsigned long long)n);
+}
+
+// p <- fl32( inverse(S_o^corr)( T_o,w^old(p) ) ), corr_ref <- window[o] (or -1)
+__global__ void k_win_points(int n_mp, const int32_t* __restrict__ owner,
+                             const int32_t* __restrict__ window, const double* __restrict__ scr,
+                             MpRec* __restrict__ rec, int32_t* __restrict__ corr_ref,
+                             unsigned long long* __restrict__ counts) {
+  uint32_t n = 0;
+  const int stride = gridDim.x * blockDim.x;
+  const int base = blockIdx.x * blockDim.x;
+  for (int q0 = base; q0 < n_mp; q0 += stride) {
+    const int q = q0 + threadIdx.x;
+    if (q < n_mp) {
+      const int o = owner[q];
+      if (o == INT_MAX) {
+        corr_ref[q] = -1;
+      } else {
+        const double* S = scr + (size_t)WSTR * o;
+        double p[3] = {rec[q].pos[0], rec[q].pos[1], rec[q].pos[2]}, pc[3], pw[3];
+        lc_sim3_apply(S + 26, p, pc);
+        lc_sim3_apply(S + 13, pc, pw);
+        rec[q].pos[0] = __double2float_rn(pw[0]);
+        rec[q].pos[1] = __double2float_rn(pw[1]);
+        rec[q].pos[2] = __double2float_rn(pw[2]);
+        corr_ref[q] = window[o];
+        ++n;
+      }
+    }
+  }
+  warp_count(n, &counts[LC_COUNT_CORR_MP]);
+}
+
+__global__ void k_win_writeback(int n_w, const int32_t* __restrict__ window,
+                                const double* __restrict__ scr, double* __restrict__ kf_pose,
+                                unsigned long long* __restrict__ counts) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t n = 0;
+  if (i < n_w) {
+    double T[13];
+    lc_sim3_se3(scr + (size_t)WSTR * i, T);
+    for (int j = 0; j < 13; ++j) kf_pose[13 * (size_t)window[i] + j] = T[j];
+    n = 1;
+  }
+  warp_count(n, &counts[LC_COUNT_CORR_KF]);
+}
+
+// ALL: per keyframe S^pre and inverse(S^opt) into scratch, pose <- SE3(S^opt)
+__global__ void k_all_kf(int n_kf, const double* __restrict__ Sopt, double* __restrict__ kf_pose,
+                         const double* __restrict__ kf_S_corr, int32_t* __restrict__ kf_in_win,
+                         double* __restrict__ scr, unsigned long long* __restrict__ counts) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t n = 0;
+  if (k < n_kf) {
+    double pre[13], opt[13], inv[13], T[13];
+    const double* src = kf_in_win[k] ? kf_S_corr + 13 * (size_t)k : kf_pose + 13 * (size_t)k;
+    for (int j = 0; j < 13; ++j) pre[j] = src[j];
+    for (int j = 0; j < 13; ++j) opt[j] = Sopt[13 * (size_t)k + j];
+    lc_sim3_inverse(opt, inv);
+    lc_sim3_se3(opt, T);
+    double* o = scr + 26 * (size_t)k;
+    for (int j = 0; j < 13; ++j) { o[j] = pre[j]; o[13 + j] = inv[j]; }
+    for (int j = 0; j < 13; ++j) kf_pose[13 * (size_t)k + j] = T[j];
+    kf_in_win[k] = 0;
+    n = 1;
+  }
+  warp_count(n, &counts[LC_COUNT_CORR_KF]);
+}
+
+__global__ void k_all_points(int n_mp, const double* __restrict__ scr,
+                             const int32_t* __restrict__ ref_kf, const uint8_t* __restrict__ flags,
+                             MpRec* __restrict__ rec, int32_t* __restrict__ corr_ref,
+                             unsigned long long* __restrict__ counts) {
+  uint32_t n = 0;
+  const int stride = gridDim.x * blockDim.x;
+  for (int q0 = blockIdx.x * blockDim.x; q0 < n_mp; q0 += stride) {
+    const int q = q0 + threadIdx.x;
+    if (q < n_mp) {
+      const int cr = corr_ref[q];
+      if (cr >= 0) corr_ref[q] = -1;
+      if (!(flags[q] & 1u)) {
+        const int r = cr >= 0 ? cr : ref_kf[q];
+        const double* S = scr + 26 * (size_t)r;
+        double p[3] = {rec[q].pos[0], rec[q].pos[1], rec[q].pos[2]}, pc[3], pw[3];
+        lc_sim3_apply(S, p, pc);
+        lc_sim3_apply(S + 13, pc, pw);
+        rec[q].pos[0] = __double2float_rn(pw[0]);
+        rec[q].pos[1] = __double2float_rn(pw[1]);
+        rec[q].pos[2] = __double2float_rn(pw[2]);
+        ++n;
+      }
+    }
+  }
+  warp_count(n, &counts[LC_COUNT_CORR_MP]);
+}
+
+int grid_for(int64_t n) {
+  int64_t b = (n + LC_NTHREADS - 1) / LC_NTHREADS;
+  if (b < 1) b = 1;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)b;
+}
+
+}  // namespace
+
+cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t* d_window,
+                                  const double* d_Scw, double* d_scr, unsigned long long* counts,
+                                  cudaStream_t s) {
+  Store& st = c->st;
+  int64_t n = st.n_mp > st.n_kf ? st.n_mp : st.n_kf;
+  k_win_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(st.n_kf, st.n_mp, st.mp_owner, st.kf_in_win);
+  k_win_sim3<<<(n_w + 127) / 128, 128, 0, s>>>(n_w, cur_pos, d_window, st.kf_pose, d_Scw, d_scr,
+                                              st.kf_S_corr, st.kf_in_win);
+  k_win_mark<<<n_w, LC_NTHREADS, 0, s>>>(d_window, st.kf_fbeg, st.feat_mp, st.mp_flags, st.mp_owner);
+  c->launches += 3;
+  if (st.n_mp > 0) {
+    k_win_points<<<grid_for(st.n_mp), LC_NTHREADS, 0, s>>>(st.n_mp, st.mp_owner, d_window, d_scr,
+                                                          st.mp_rec, st.mp_corr_ref, counts);
+    c->launches++;
+  }
+  k_win_writeback<<<(n_w + 127) / 128, 128, 0, s>>>(n_w, d_window, d_scr, st.kf_pose, counts);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
+                               unsigned long long* counts, cudaStream_t s) {
+  Store& st = c->st;
+  k_all_kf<<<(st.n_kf + 127) / 128, 128, 0, s>>>(st.n_kf, d_Sopt, st.kf_pose, st.kf_S_corr,
+                                                st.kf_in_win, d_scr, counts);
+  c->launches++;
+  if (st.n_mp > 0) {
+    k_all_points<<<grid_for(st.n_mp), LC_NTHREADS, 0, s>>>(st.n_mp, d_scr, st.mp_ref_kf,
+                                                          st.mp_flags, st.mp_rec, st.mp_corr_ref,
+                                                          counts);
+    c->launches++;
+  }
+  return cudaGetLastError();
+}

@@ -1,0 +1,753 @@
+// lc_api.cu -- extern "C" entry points of liblc (include/lc.h): argument
+// validation, host/device marshalling through one pinned argument block per
+// call, scratch arena management and kernel orchestration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "lc_internal.cuh"
+
+namespace {
+
+thread_local std::string g_create_err = "no error";
+
+struct Fail {
+  lc_status st;
+};
+
+void set_err(lc_ctx* c, const std::string& m) {
+  if (c) c->err = m;
+}
+
+#define CK(expr)                                                                         \
+  do {                                                                                   \
+    cudaError_t e__ = (expr);                                                            \
+    if (e__ != cudaSuccess) {                                                            \
+      c->broken = true;                                                                  \
+      set_err(c, std::string("CUDA error ") + cudaGetErrorString(e__) + " at " #expr);   \
+      throw Fail{LC_ECUDA};                                                              \
+    }                                                                                    \
+  } while (0)
+
+#define REQUIRE(cond, code, msg)      \
+  do {                                \
+    if (!(cond)) {                    \
+      set_err(c, msg);                \
+      throw Fail{code};               \
+    }                                 \
+  } while (0)
+
+bool is_device_ptr(lc_ctx* c, const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) {
+    if (at.type == cudaMemoryTypeDevice && at.device != c->device) {
+      set_err(c, "device pointer belongs to another device");
+      throw Fail{LC_EINVAL};
+    }
+    return true;
+  }
+  return false;
+}
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// One API call: scratch slots, a pinned argument block, deferred host outputs.
+struct Call {
+  lc_ctx* c;
+  cudaStream_t s;
+  int slot = 0;
+  std::vector<char> args;                 // host argument block
+  std::vector<std::pair<const void**, size_t>> arg_fix;   // (where to store dev ptr, offset)
+  std::vector<lc_ctx::HostOut> outs;
+  char* d_args = nullptr;
+
+  Call(lc_ctx* ctx, void* stream) : c(ctx), s((cudaStream_t)stream) {}
+
+  void* scratch(size_t bytes) {
+    bytes = std::max<size_t>(round_up(bytes, 256), 256);
+    if ((int)c->scr_ptr.size() <= slot) {
+      c->scr_ptr.push_back(nullptr);
+      c->scr_cap.push_back(0);
+    }
+    if (c->scr_cap[slot] < bytes) {
+      if (c->scr_ptr[slot]) {
+        CK(cudaStreamSynchronize(s));
+        CK(cudaFree(c->scr_ptr[slot]));
+      }
+      c->scr_ptr[slot] = nullptr;
+      c->scr_cap[slot] = 0;
+      size_t cap = bytes + bytes / 2;
+      if (cudaMalloc(&c->scr_ptr[slot], cap) != cudaSuccess) {
+        cudaGetLastError();
+        set_err(c, "scratch allocation failed");
+        throw Fail{LC_ENOMEM};
+      }
+      c->scr_cap[slot] = cap;
+    }
+    return c->scr_ptr[slot++];
+  }
+
+  // small [host] control array -> device copy inside the argument block
+  template <typename T>
+  void arg(const T* host, size_t n, const T** dev_out) {
+    size_t off = round_up(args.size(), 16);
+    args.resize(off + std::max<size_t>(sizeof(T) * n, 1));
+    if (n) memcpy(args.data() + off, host, sizeof(T) * n);
+    arg_fix.push_back({(const void**)dev_out, off});
+  }
+
+  // stage the argument block: one pinned memcpy + one H2D
+  void commit() {
+    if (args.empty()) return;
+    size_t bytes = round_up(args.size(), 16);
+    if (c->pin_ev_pending) {
+      CK(cudaEventSynchronize(c->pin_ev));
+      c->pin_ev_pending = false;
+    }
+    if (c->pin_cap < bytes) {
+      if (c->pin) CK(cudaFreeHost(c->pin));
+      c->pin = nullptr;
+      c->pin_cap = 0;
+      size_t cap = std::max<size_t>(bytes * 2, 1 << 16);
+      if (cudaHostAlloc(&c->pin, cap, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        set_err(c, "pinned staging allocation failed");
+        throw Fail{LC_ENOMEM};
+      }
+      c->pin_cap = cap;
+    }
+    memcpy(c->pin, args.data(), args.size());
+    d_args = (char*)scratch(bytes);
+    CK(cudaMemcpyAsync(d_args, c->pin, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(c->pin_ev, s));
+    c->pin_ev_pending = true;
+    for (auto& f : arg_fix) *f.first = d_args + f.second;
+  }
+
+  // [host|dev] input: device pointer as-is, host data copied to scratch
+  template <typename T>
+  const T* in(const T* p, size_t n) {
+    if (!p || n == 0) return p;
+    if (is_device_ptr(c, p)) return p;
+    T* d = (T*)scratch(sizeof(T) * n);
+    CK(cudaMemcpyAsync(d, p, sizeof(T) * n, cudaMemcpyDefault, s));
+    return d;
+  }
+
+  // [host|dev] output (copy_in: also an input, e.g. io tables in APPLY)
+  template <typename T>
+  T* out(T* p, size_t n, bool copy_in = false) {
+    if (!p) return nullptr;
+    if (n == 0) return p;
+    if (is_device_ptr(c, p)) return p;
+    T* d = (T*)scratch(sizeof(T) * n);
+    if (copy_in) CK(cudaMemcpyAsync(d, p, sizeof(T) * n, cudaMemcpyDefault, s));
+    outs.push_back({p, d, sizeof(T) * n});
+    return d;
+  }
+
+  void finish() {
+    for (auto& o : outs) CK(cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDefault, s));
+    CK(cudaGetLastError());
+  }
+};
+
+template <typename F>
+lc_status guarded(lc_ctx* c, F&& f) {
+  if (!c) return LC_EINVAL;
+  if (c->broken) {
+    return LC_ECUDA;
+  }
+  try {
+    CK(cudaSetDevice(c->device));
+    f();
+    return LC_OK;
+  } catch (const Fail& e) {
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    set_err(c, "host allocation failed");
+    return LC_ENOMEM;
+  }
+}
+
+bool params_ok(const lc_match_params& p) {
+  return p.th > 0 && p.max_hamming >= 0 && p.max_hamming <= 256 && p.ratio_den >= 0 &&
+         (p.ratio_den == 0 || p.ratio_num >= 0);
+}
+
+template <typename T>
+void dev_alloc(lc_ctx* c, T** p, size_t n) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  if (cudaMalloc((void**)p, std::max<size_t>(sizeof(T) * n, 16)) != cudaSuccess) {
+    cudaGetLastError();
+    set_err(c, "device store allocation failed");
+    throw Fail{LC_ENOMEM};
+  }
+}
+
+void free_store(Store& st) {
+  void* ptrs[] = {st.kf_pose, st.kf_cam, st.kf_fbeg, st.kf_cell, st.fc_uv, st.fc_meta,
+                  st.fc_desc, st.feat_mp, st.feat_angle, st.mp_rec, st.mp_flags, st.mp_ref_kf,
+                  st.mp_replaced_by, st.mp_nobs, st.mp_corr_ref, st.mp_loop_ep, st.mp_owner,
+                  st.kf_S_corr, st.kf_in_win, st.kf_win_ep, st.kf_win_pos, st.cams};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  st = Store();
+}
+
+void mark_window(lc_ctx* c, int n_w, const int32_t* window) {
+  REQUIRE(n_w >= 1 && window, LC_EINVAL, "window must hold at least one keyframe");
+  std::vector<char> seen(c->st.n_kf, 0);
+  for (int i = 0; i < n_w; ++i) {
+    int k = window[i];
+    REQUIRE(k >= 0 && k < c->st.n_kf, LC_ERANGE, "window keyframe index out of range");
+    REQUIRE(!seen[k], LC_EINVAL, "duplicate keyframe in window");
+    seen[k] = 1;
+  }
+}
+
+int pick_chunk(int64_t total_q) {
+  int64_t ch = (total_q + 148 * 4 - 1) / (148 * 4);
+  ch = std::max<int64_t>(64, std::min<int64_t>(4096, ch));
+  return (int)round_up((size_t)ch, 32);
+}
+
+void fill_match_store(lc_ctx* c, MatchArgs& a) {
+  Store& st = c->st;
+  a.kf_pose = st.kf_pose;
+  a.kf_cam = st.kf_cam;
+  a.kf_fbeg = st.kf_fbeg;
+  a.kf_cell = st.kf_cell;
+  a.fc_uv = st.fc_uv;
+  a.fc_meta = st.fc_meta;
+  a.fc_desc = st.fc_desc;
+  a.feat_mp = st.feat_mp;
+  a.mp_rec = st.mp_rec;
+  a.mp_flags = st.mp_flags;
+  a.cams = st.cams;
+  a.cols = st.cols;
+  a.rows = st.rows;
+  a.G = st.G;
+  a.n_levels = st.n_levels;
+  for (int i = 0; i < LC_MAX_LEVELS; ++i) a.scale[i] = st.scale[i];
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+lc_status lc_create(lc_ctx** out, int32_t device) {
+  if (!out) return LC_EINVAL;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+    cudaGetLastError();
+    g_create_err = "no such CUDA device";
+    return LC_ECUDA;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10) {
+    cudaGetLastError();
+    g_create_err = "liblc is built for sm_100a (B200); device is sm_" +
+                   std::to_string(prop.major) + std::to_string(prop.minor);
+    return LC_ECUDA;
+  }
+  lc_ctx* c = new (std::nothrow) lc_ctx();
+  if (!c) return LC_ENOMEM;
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->pin_ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    g_create_err = "CUDA context setup failed";
+    delete c;
+    return LC_ECUDA;
+  }
+  *out = c;
+  return LC_OK;
+}
+
+lc_status lc_destroy(lc_ctx* c) {
+  if (!c) return LC_EINVAL;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  free_store(c->st);
+  for (void* p : c->scr_ptr)
+    if (p) cudaFree(p);
+  if (c->pin) cudaFreeHost(c->pin);
+  if (c->sv) cudaFree(c->sv);
+  if (c->pin_ev) cudaEventDestroy(c->pin_ev);
+  cudaGetLastError();
+  delete c;
+  return LC_OK;
+}
+
+const char* lc_last_error(const lc_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int64_t lc_kernel_launches(const lc_ctx* c) { return c ? c->launches : 0; }
+
+// ----------------------------------------------------------------------------
+lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, int32_t n_cams,
+                        const lc_map_params* prm, void* stream) {
+  return guarded(c, [&] {
+    REQUIRE(m && cams && prm && n_cams >= 1, LC_EINVAL, "null map/camera/params");
+    REQUIRE(m->n_kf >= 0 && m->n_feat >= 0 && m->n_mp >= 0, LC_EINVAL, "negative sizes");
+    REQUIRE(prm->n_levels >= 1 && prm->n_levels <= LC_MAX_LEVELS, LC_EINVAL, "n_levels out of range");
+    REQUIRE(prm->scale_factor > 1.0, LC_EINVAL, "scale_factor must be > 1");
+    REQUIRE(prm->grid_cols >= 1 && prm->grid_rows >= 1 && prm->grid_cols <= 1024 &&
+                prm->grid_rows <= 1024 && prm->grid_cols * prm->grid_rows <= 16384,
+            LC_EINVAL, "grid size out of range");
+    for (int i = 0; i < n_cams; ++i) {
+      const lc_camera& k = cams[i];
+      REQUIRE(k.model == 0 || k.model == 1, LC_EINVAL, "camera model must be 0 or 1");
+      REQUIRE(k.max_x > k.min_x && k.max_y > k.min_y, LC_EINVAL, "empty camera bounds");
+    }
+    const bool need = m->n_kf > 0;
+    REQUIRE(!need || (m->kf_pose && m->kf_cam && m->kf_feat_begin), LC_EINVAL, "null keyframe arrays");
+    REQUIRE(m->n_feat == 0 || (m->feat_uv && m->feat_octave && m->feat_angle && m->feat_desc &&
+                               m->feat_mp), LC_EINVAL, "null feature arrays");
+    REQUIRE(m->n_mp == 0 || (m->mp_pos && m->mp_normal && m->mp_max_dist && m->mp_desc &&
+                             m->mp_angle && m->mp_ref_kf && m->mp_flags), LC_EINVAL, "null map-point arrays");
+    Call call(c, stream);
+    cudaStream_t s = call.s;
+    // host copy of the keyframe CSR (validation + launch configuration)
+    std::vector<int32_t> fbeg(m->n_kf + 1, 0);
+    if (m->n_kf > 0) {
+      if (is_device_ptr(c, m->kf_feat_begin)) {
+        CK(cudaMemcpyAsync(fbeg.data(), m->kf_feat_begin, sizeof(int32_t) * (m->n_kf + 1),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+      } else {
+        memcpy(fbeg.data(), m->kf_feat_begin, sizeof(int32_t) * (m->n_kf + 1));
+      }
+    }
+    REQUIRE(fbeg[0] == 0 && fbeg[m->n_kf] == m->n_feat, LC_EINVAL, "kf_feat_begin must span [0, n_feat]");
+    int max_F = 0;
+    for (int k = 0; k < m->n_kf; ++k) {
+      REQUIRE(fbeg[k + 1] >= fbeg[k], LC_EINVAL, "kf_feat_begin not monotone");
+      max_F = std::max(max_F, fbeg[k + 1] - fbeg[k]);
+    }
+    REQUIRE(max_F <= LC_MAX_FEAT_PER_KF, LC_ECAPACITY, "keyframe exceeds LC_MAX_FEAT_PER_KF features");
+
+    CK(cudaStreamSynchronize(s));
+    free_store(c->st);
+    c->has_map = false;
+    c->has_saved = false;
+    Store& st = c->st;
+    st.n_kf = m->n_kf; st.n_feat = m->n_feat; st.n_mp = m->n_mp; st.n_cams = n_cams;
+    st.n_levels = prm->n_levels; st.cols = prm->grid_cols; st.rows = prm->grid_rows;
+    st.G = st.cols * st.rows;
+    st.max_F = max_F;
+    st.scale[0] = 1.0;
+    for (int n = 1; n < LC_MAX_LEVELS; ++n) st.scale[n] = st.scale[n - 1] * prm->scale_factor;
+    st.h_fbeg = fbeg;
+    st.h_in_win.assign(st.n_kf, 0);
+    const size_t NK = st.n_kf, NF = st.n_feat, NM = st.n_mp;
+    dev_alloc(c, &st.kf_pose, 13 * NK);
+    dev_alloc(c, &st.kf_cam, NK);
+    dev_alloc(c, &st.kf_fbeg, NK + 1);
+    dev_alloc(c, &st.kf_cell, NK * (st.G + 1));
+    dev_alloc(c, &st.fc_uv, NF);
+    dev_alloc(c, &st.fc_meta, NF);
+    dev_alloc(c, &st.fc_desc, 2 * NF);
+    dev_alloc(c, &st.feat_mp, NF);
+    dev_alloc(c, &st.feat_angle, NF);
+    dev_alloc(c, &st.mp_rec, NM);
+    dev_alloc(c, &st.mp_flags, NM);
+    dev_alloc(c, &st.mp_ref_kf, NM);
+    dev_alloc(c, &st.mp_replaced_by, NM);
+    dev_alloc(c, &st.mp_nobs, NM);
+    dev_alloc(c, &st.mp_corr_ref, NM);
+    dev_alloc(c, &st.mp_loop_ep, NM);
+    dev_alloc(c, &st.mp_owner, NM);
+    dev_alloc(c, &st.kf_S_corr, 13 * NK);
+    dev_alloc(c, &st.kf_in_win, NK);
+    dev_alloc(c, &st.kf_win_ep, NK);
+    dev_alloc(c, &st.kf_win_pos, NK);
+    dev_alloc(c, &st.cams, n_cams);
+    std::vector<DevCam> dc(n_cams);
+    for (int i = 0; i < n_cams; ++i) {
+      const lc_camera& k = cams[i];
+      DevCam& d = dc[i];
+      memset(&d, 0, sizeof(d));
+      d.model = k.model; d.cols = st.cols; d.rows = st.rows;
+      d.fx = k.fx; d.fy = k.fy; d.cx = k.cx; d.cy = k.cy;
+      for (int j = 0; j < 4; ++j) d.k[j] = k.k[j];
+      d.min_x = k.min_x; d.max_x = k.max_x; d.min_y = k.min_y; d.max_y = k.max_y;
+      d.cell_sx = (double)st.cols / (k.max_x - k.min_x);
+      d.cell_sy = (double)st.rows / (k.max_y - k.min_y);
+    }
+    CK(cudaMemcpyAsync(st.cams, dc.data(), sizeof(DevCam) * n_cams, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(st.kf_fbeg, fbeg.data(), sizeof(int32_t) * (NK + 1), cudaMemcpyHostToDevice, s));
+    auto copy_in = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+    };
+    copy_in(st.kf_pose, m->kf_pose, sizeof(double) * 13 * NK);
+    copy_in(st.kf_cam, m->kf_cam, sizeof(int32_t) * NK);
+    copy_in(st.feat_mp, m->feat_mp, sizeof(int32_t) * NF);
+    copy_in(st.feat_angle, m->feat_angle, sizeof(float) * NF);
+    copy_in(st.mp_flags, m->mp_flags, NM);
+    copy_in(st.mp_ref_kf, m->mp_ref_kf, sizeof(int32_t) * NM);
+    CK(cudaMemsetAsync(st.kf_S_corr, 0, sizeof(double) * 13 * NK, s));
+    CK(cudaMemsetAsync(st.kf_in_win, 0, sizeof(int32_t) * NK, s));
+    CK(cudaMemsetAsync(st.kf_win_ep, 0, sizeof(uint32_t) * NK, s));
+    c->epoch = 0;
+    // raw SoA inputs the packing kernels read (device pointers used in place)
+    const float* pos = call.in(m->mp_pos, 3 * NM);
+    const float* nrm = call.in(m->mp_normal, 3 * NM);
+    const float* dmx = call.in(m->mp_max_dist, NM);
+    const uint8_t* mdesc = call.in(m->mp_desc, 32 * NM);
+    const float* ang = call.in(m->mp_angle, NM);
+    const float* fuv = call.in(m->feat_uv, 2 * NF);
+    const uint8_t* foct = call.in(m->feat_octave, NF);
+    const uint8_t* fdesc = call.in(m->feat_desc, 32 * NF);
+    uint32_t* d_errs = (uint32_t*)call.scratch(64);
+    CK(cudaMemsetAsync(d_errs, 0, 64, s));
+    CK(launch_upload_pack(c, pos, nrm, dmx, mdesc, ang, fuv, foct, fdesc, d_errs, s));
+    uint32_t errs[16];
+    CK(cudaMemcpyAsync(errs, d_errs, 64, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    REQUIRE(errs[0] == 0, LC_ERANGE, "feature octave >= n_levels");
+    REQUIRE(errs[1] == 0, LC_ERANGE, "feat_mp out of range");
+    REQUIRE(errs[2] == 0, LC_ERANGE, "mp_ref_kf out of range");
+    REQUIRE(errs[3] == 0, LC_ERANGE, "kf_cam out of range");
+    c->has_map = true;
+  });
+}
+
+lc_status lc_download_map(lc_ctx* c, const lc_map_state* o, void* stream) {
+  return guarded(c, [&] {
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    REQUIRE(o, LC_EINVAL, "null output struct");
+    Call call(c, stream);
+    Store& st = c->st;
+    auto copy_out = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, call.s));
+    };
+    copy_out(o->kf_pose, st.kf_pose, sizeof(double) * 13 * st.n_kf);
+    copy_out(o->feat_mp, st.feat_mp, sizeof(int32_t) * st.n_feat);
+    copy_out(o->mp_flags, st.mp_flags, st.n_mp);
+    copy_out(o->mp_replaced_by, st.mp_replaced_by, sizeof(int32_t) * st.n_mp);
+    copy_out(o->mp_nobs, st.mp_nobs, sizeof(int32_t) * st.n_mp);
+    if (o->mp_pos && st.n_mp) {
+      float* d = call.out(o->mp_pos, 3 * (size_t)st.n_mp);
+      CK(launch_download_pos(c, d, call.s));
+    }
+    call.finish();
+  });
+}
+
+lc_status lc_state_save(lc_ctx* c, void* stream) {
+  return guarded(c, [&] {
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    CK(launch_state_copy(c, true, (cudaStream_t)stream));
+    c->sv_in_win = c->st.h_in_win;
+    c->has_saved = true;
+  });
+}
+
+lc_status lc_state_restore(lc_ctx* c, void* stream) {
+  return guarded(c, [&] {
+    REQUIRE(c->has_map && c->has_saved, LC_ESTATE, "no saved state");
+    CK(launch_state_copy(c, false, (cudaStream_t)stream));
+    c->st.h_in_win = c->sv_in_win;
+  });
+}
+
+// ----------------------------------------------------------------------------
+lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3* S_cw_corr,
+                          int32_t n_window, const int32_t* window_kf, const lc_sim3* S_opt,
+                          lc_sim3* out_S_corr, int64_t* out_counts, void* stream) {
+  return guarded(c, [&] {
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    REQUIRE(mode == LC_CORRECT_WINDOW || mode == LC_CORRECT_ALL, LC_EINVAL, "bad mode");
+    Store& st = c->st;
+    Call call(c, stream);
+    unsigned long long* cnt = (unsigned long long*)call.scratch(sizeof(uint64_t) * LC_NCOUNT);
+    if (mode == LC_CORRECT_WINDOW) {
+      REQUIRE(S_cw_corr, LC_EINVAL, "null S_cw_corr");
+      REQUIRE(cur_kf >= 0 && cur_kf < st.n_kf, LC_ERANGE, "cur_kf out of range");
+      mark_window(c, n_window, window_kf);
+      REQUIRE(window_kf[0] == cur_kf, LC_EINVAL, "window_kf[0] must be cur_kf");
+      const int32_t* d_win = nullptr;
+      const double* d_S = nullptr;
+      call.arg(window_kf, n_window, &d_win);
+      call.arg((const double*)S_cw_corr, 13, &d_S);
+      call.commit();
+      double* scr = (double*)call.scratch(sizeof(double) * 39 * (size_t)n_window);
+      CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
+      CK(launch_correct_window(c, 0, n_window, d_win, d_S, scr, cnt, call.s));
+      if (out_S_corr) {
+        if (is_device_ptr(c, out_S_corr)) {
+          CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr, sizeof(double) * 39,
+                               sizeof(lc_sim3), n_window, cudaMemcpyDeviceToDevice, call.s));
+        } else {
+          CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr, sizeof(double) * 39,
+                               sizeof(lc_sim3), n_window, cudaMemcpyDefault, call.s));
+        }
+      }
+      std::fill(st.h_in_win.begin(), st.h_in_win.end(), 0);
+      for (int i = 0; i < n_window; ++i) st.h_in_win[window_kf[i]] = 1;
+    } else {
+      REQUIRE(S_opt, LC_EINVAL, "null S_opt");
+      const double* d_opt = call.in((const double*)S_opt, 13 * (size_t)st.n_kf);
+      double* scr = (double*)call.scratch(sizeof(double) * 26 * (size_t)std::max(st.n_kf, 1));
+      CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
+      CK(launch_correct_all(c, d_opt, scr, cnt, call.s));
+      std::fill(st.h_in_win.begin(), st.h_in_win.end(), 0);
+    }
+    if (out_counts) {
+      int64_t* d = call.out(out_counts, LC_NCOUNT);
+      CK(cudaMemcpyAsync(d, cnt, sizeof(uint64_t) * LC_NCOUNT, cudaMemcpyDeviceToDevice, call.s));
+    }
+    call.finish();
+  });
+}
+
+// ----------------------------------------------------------------------------
+lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_window,
+                  const int32_t* window_kf, const lc_sim3* window_S, const int32_t* win_list_begin,
+                  const int32_t* mp_list, int64_t n_list, const lc_match_params* params,
+                  int64_t* io_winner, int64_t* io_victim, int8_t* out_action,
+                  const lc_query_debug* dbg, int64_t* out_counts, void* stream) {
+  return guarded(c, [&] {
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    REQUIRE(phase == LC_FUSE_PLAN || phase == LC_FUSE_APPLY || phase == LC_FUSE_ALL, LC_EINVAL, "bad phase");
+    REQUIRE(params && params_ok(*params), LC_EINVAL, "bad match params");
+    REQUIRE(n_list >= 0 && (n_list == 0 || mp_list), LC_EINVAL, "bad mp_list");
+    Store& st = c->st;
+    mark_window(c, n_window, window_kf);
+    if (phase != LC_FUSE_PLAN) { w_lo = 0; w_hi = n_window; }
+    if (phase == LC_FUSE_APPLY) { w_lo = w_hi = 0; }
+    REQUIRE(0 <= w_lo && w_lo <= w_hi && w_hi <= n_window, LC_EINVAL, "bad shard range");
+    if (win_list_begin) {
+      REQUIRE(win_list_begin[0] == 0 && win_list_begin[n_window] == n_list, LC_EINVAL,
+              "win_list_begin must span [0, n_list]");
+      for (int i = 0; i < n_window; ++i)
+        REQUIRE(win_list_begin[i + 1] >= win_list_begin[i], LC_EINVAL, "win_list_begin not monotone");
+    }
+    if (!window_S && (phase & LC_FUSE_PLAN))
+      for (int i = 0; i < n_window; ++i)
+        REQUIRE(st.h_in_win[window_kf[i]], LC_ESTATE,
+                "window_S NULL but a window keyframe has no stored WINDOW correction");
+    Call call(c, stream);
+    // ---- unit tables (one unit per window position) ----
+    std::vector<int64_t> woff(n_window + 1, 0), lbeg(n_window), qoff(n_window);
+    for (int i = 0; i < n_window; ++i) {
+      int k = window_kf[i];
+      woff[i + 1] = woff[i] + (st.h_fbeg[k + 1] - st.h_fbeg[k]);
+      lbeg[i] = win_list_begin ? win_list_begin[i] : 0;
+      qoff[i] = win_list_begin ? win_list_begin[i] : (int64_t)i * n_list;
+    }
+    const int64_t n_wfeat = woff[n_window];
+    int64_t total_q = 0;
+    int F_max = 0;
+    for (int i = w_lo; i < w_hi; ++i) {
+      int64_t len = win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list;
+      total_q += len;
+      F_max = std::max<int>(F_max, (int)(woff[i + 1] - woff[i]));
+    }
+    const int ch = pick_chunk(total_q);
+    std::vector<int32_t> bunit;
+    std::vector<int64_t> bq0, bq1;
+    for (int i = w_lo; i < w_hi; ++i) {
+      int64_t b = lbeg[i];
+      int64_t e = b + (win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list);
+      for (int64_t q = b; q < e; q += ch) {
+        bunit.push_back(i);
+        bq0.push_back(q);
+        bq1.push_back(std::min<int64_t>(q + ch, e));
+      }
+    }
+    MatchArgs a;
+    memset(&a, 0, sizeof(a));
+    fill_match_store(c, a);
+    const int32_t* d_win = nullptr;
+    const int64_t *d_woff = nullptr, *d_lbeg = nullptr, *d_qoff = nullptr, *d_bq0 = nullptr, *d_bq1 = nullptr;
+    const int32_t* d_bunit = nullptr;
+    const double* d_S = nullptr;
+    const lc_match_params* d_prm = nullptr;
+    call.arg(window_kf, n_window, &d_win);
+    call.arg(woff.data(), n_window + 1, &d_woff);
+    call.arg(lbeg.data(), n_window, &d_lbeg);
+    call.arg(qoff.data(), n_window, &d_qoff);
+    call.arg(bunit.data(), bunit.size(), &d_bunit);
+    call.arg(bq0.data(), bq0.size(), &d_bq0);
+    call.arg(bq1.data(), bq1.size(), &d_bq1);
+    call.arg(params, 1, &d_prm);
+    if (window_S) call.arg((const double*)window_S, 13 * (size_t)n_window, &d_S);
+    call.commit();
+    const int32_t* d_list = call.in(mp_list, (size_t)n_list);
+    unsigned long long* win = (unsigned long long*)call.out(io_winner, (size_t)n_wfeat, phase == LC_FUSE_APPLY);
+    if (!win) win = (unsigned long long*)call.scratch(sizeof(uint64_t) * std::max<int64_t>(n_wfeat, 1));
+    unsigned long long* vic = (unsigned long long*)call.out(io_victim, (size_t)st.n_mp, phase == LC_FUSE_APPLY);
+    if (!vic) vic = (unsigned long long*)call.scratch(sizeof(uint64_t) * std::max(st.n_mp, 1));
+    int8_t* act = call.out(out_action, (size_t)n_wfeat);
+    if (act && (phase & LC_FUSE_PLAN)) CK(cudaMemsetAsync(act, 0, (size_t)n_wfeat, call.s));
+    unsigned long long* cnt = (unsigned long long*)call.scratch(sizeof(uint64_t) * LC_NCOUNT);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
+    const int64_t n_q_all = win_list_begin ? n_list : (int64_t)n_window * n_list;
+    int64_t* dbg_best = nullptr;
+    double* dbg_uv = nullptr;
+    int32_t* dbg_nc = nullptr;
+    if (dbg && (phase & LC_FUSE_PLAN)) {
+      dbg_best = call.out(dbg->best, (size_t)n_q_all, true);
+      dbg_uv = call.out(dbg->uv, 2 * (size_t)n_q_all, true);
+      dbg_nc = call.out(dbg->ncand, (size_t)n_q_all, true);
+    }
+    // ---- epoch (LoopSet stamp / window membership) ----
+    if (++c->epoch == 0) {
+      CK(cudaMemsetAsync(st.mp_loop_ep, 0, sizeof(uint32_t) * st.n_mp, call.s));
+      CK(cudaMemsetAsync(st.kf_win_ep, 0, sizeof(uint32_t) * st.n_kf, call.s));
+      c->epoch = 1;
+    }
+    CK(launch_fuse_prep(c, phase, n_window, d_win, d_woff, n_wfeat, d_list, n_list, win, vic, call.s));
+    if (phase & LC_FUSE_PLAN) {
+      a.unit_kf = d_win;
+      a.unit_S = d_S;
+      a.kf_S_corr = st.kf_S_corr;
+      a.unit_param = nullptr;
+      a.unit_woff = d_woff;
+      a.unit_toff = d_woff;
+      a.unit_lbeg = d_lbeg;
+      a.unit_qoff = d_qoff;
+      a.params = d_prm;
+      a.blk_unit = d_bunit;
+      a.blk_q0 = d_bq0;
+      a.blk_q1 = d_bq1;
+      a.mp_list = d_list;
+      a.taken = nullptr;
+      a.winner = win;
+      a.counts = cnt;
+      a.n_mp = st.n_mp;
+      a.dbg_best = dbg_best;
+      a.dbg_uv = dbg_uv;
+      a.dbg_ncand = dbg_nc;
+      CK(launch_match(c, 0, a, (int)bunit.size(), F_max, call.s));
+      CK(launch_fuse_resolve(c, 0, w_hi - w_lo, d_win + w_lo, d_woff + w_lo, d_woff + w_lo, nullptr,
+                             d_prm, nullptr, win, vic, act, nullptr, nullptr, cnt, F_max, call.s));
+    }
+    if (phase & LC_FUSE_APPLY) CK(launch_fuse_apply(c, d_woff, win, vic, cnt, call.s));
+    if (out_counts) {
+      int64_t* d = call.out(out_counts, LC_NCOUNT);
+      CK(cudaMemcpyAsync(d, cnt, sizeof(uint64_t) * LC_NCOUNT, cudaMemcpyDeviceToDevice, call.s));
+    }
+    call.finish();
+  });
+}
+
+// ----------------------------------------------------------------------------
+lc_status lc_search_by_projection(lc_ctx* c, int32_t n_pairs, const int32_t* pair_kf,
+                                  const lc_sim3* pair_S, const int32_t* pair_param,
+                                  const lc_match_params* params, int32_t n_params,
+                                  const int32_t* pair_list_begin, const int32_t* mp_list,
+                                  const int32_t* pair_taken, int32_t* out_feat_mp,
+                                  int32_t* out_feat_dist, const lc_query_debug* dbg,
+                                  int64_t* out_counts, void* stream) {
+  return guarded(c, [&] {
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    REQUIRE(n_pairs >= 0, LC_EINVAL, "n_pairs < 0");
+    if (n_pairs == 0) return;
+    REQUIRE(pair_kf && pair_S && pair_param && pair_list_begin && params && n_params >= 1,
+            LC_EINVAL, "null pair arrays or params");
+    REQUIRE(out_feat_mp && out_feat_dist, LC_EINVAL, "null outputs");
+    for (int i = 0; i < n_params; ++i) REQUIRE(params_ok(params[i]), LC_EINVAL, "bad match params");
+    Store& st = c->st;
+    REQUIRE(pair_list_begin[0] == 0, LC_EINVAL, "pair_list_begin[0] must be 0");
+    const int64_t n_list = pair_list_begin[n_pairs];
+    REQUIRE(n_list == 0 || mp_list, LC_EINVAL, "null mp_list");
+    std::vector<int64_t> off(n_pairs + 1, 0), lbeg(n_pairs);
+    int F_max = 0;
+    int64_t total_q = 0;
+    for (int p = 0; p < n_pairs; ++p) {
+      int k = pair_kf[p];
+      REQUIRE(k >= 0 && k < st.n_kf, LC_ERANGE, "pair keyframe out of range");
+      REQUIRE(pair_param[p] >= 0 && pair_param[p] < n_params, LC_EINVAL, "pair_param out of range");
+      REQUIRE(pair_list_begin[p + 1] >= pair_list_begin[p], LC_EINVAL, "pair_list_begin not monotone");
+      int F = st.h_fbeg[k + 1] - st.h_fbeg[k];
+      off[p + 1] = off[p] + F;
+      lbeg[p] = pair_list_begin[p];
+      F_max = std::max(F_max, F);
+      total_q += pair_list_begin[p + 1] - pair_list_begin[p];
+    }
+    const int64_t n_tot = off[n_pairs];
+    const int ch = pick_chunk(total_q);
+    std::vector<int32_t> bunit;
+    std::vector<int64_t> bq0, bq1;
+    for (int p = 0; p < n_pairs; ++p)
+      for (int64_t q = pair_list_begin[p]; q < pair_list_begin[p + 1]; q += ch) {
+        bunit.push_back(p);
+        bq0.push_back(q);
+        bq1.push_back(std::min<int64_t>(q + ch, pair_list_begin[p + 1]));
+      }
+    Call call(c, stream);
+    const int32_t *d_kf = nullptr, *d_param = nullptr, *d_bunit = nullptr;
+    const int64_t *d_off = nullptr, *d_lbeg = nullptr, *d_bq0 = nullptr, *d_bq1 = nullptr;
+    const double* d_S = nullptr;
+    const lc_match_params* d_prm = nullptr;
+    call.arg(pair_kf, n_pairs, &d_kf);
+    call.arg(pair_param, n_pairs, &d_param);
+    call.arg(off.data(), n_pairs + 1, &d_off);
+    call.arg(lbeg.data(), n_pairs, &d_lbeg);
+    call.arg(bunit.data(), bunit.size(), &d_bunit);
+    call.arg(bq0.data(), bq0.size(), &d_bq0);
+    call.arg(bq1.data(), bq1.size(), &d_bq1);
+    call.arg((const double*)pair_S, 13 * (size_t)n_pairs, &d_S);
+    call.arg(params, n_params, &d_prm);
+    call.commit();
+    const int32_t* d_list = call.in(mp_list, (size_t)n_list);
+    const int32_t* d_taken = call.in(pair_taken, (size_t)n_tot);
+    int32_t* o_mp = call.out(out_feat_mp, (size_t)n_tot);
+    int32_t* o_dist = call.out(out_feat_dist, (size_t)n_tot);
+    unsigned long long* win = (unsigned long long*)call.scratch(sizeof(uint64_t) * std::max<int64_t>(n_tot, 1));
+    unsigned long long* cnt = (unsigned long long*)call.scratch(sizeof(uint64_t) * LC_NCOUNT * n_pairs);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT * n_pairs, call.s));
+    CK(launch_fill_u64(c, win, n_tot, 0x7FFFFFFFFFFFFFFFull, call.s));
+    MatchArgs a;
+    memset(&a, 0, sizeof(a));
+    fill_match_store(c, a);
+    a.unit_kf = d_kf;
+    a.unit_S = d_S;
+    a.kf_S_corr = st.kf_S_corr;
+    a.unit_param = d_param;
+    a.unit_woff = d_off;
+    a.unit_toff = d_off;
+    a.unit_lbeg = d_lbeg;
+    a.unit_qoff = d_lbeg;
+    a.params = d_prm;
+    a.blk_unit = d_bunit;
+    a.blk_q0 = d_bq0;
+    a.blk_q1 = d_bq1;
+    a.mp_list = d_list;
+    a.taken = d_taken;
+    a.winner = win;
+    a.counts = cnt;
+    a.n_mp = st.n_mp;
+    if (dbg) {
+      a.dbg_best = call.out(dbg->best, (size_t)n_list, true);
+      a.dbg_uv = call.out(dbg->uv, 2 * (size_t)n_list, true);
+      a.dbg_ncand = call.out(dbg->ncand, (size_t)n_list, true);
+    }
+    CK(launch_match(c, 1, a, (int)bunit.size(), F_max, call.s));
+    CK(launch_fuse_resolve(c, 1, n_pairs, d_kf, d_off, d_off, d_param, d_prm, d_taken, win, nullptr,
+                           nullptr, o_mp, o_dist, cnt, F_max, call.s));
+    if (out_counts) {
+      int64_t* d = call.out(out_counts, (size_t)LC_NCOUNT * n_pairs);
+      CK(cudaMemcpyAsync(d, cnt, sizeof(uint64_t) * LC_NCOUNT * n_pairs, cudaMemcpyDeviceToDevice, call.s));
+    }
+    call.finish();
+  });
+}
+
+}  // extern "C"

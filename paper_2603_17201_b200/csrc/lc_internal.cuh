@@ -1,0 +1,253 @@
+// lc_internal.cuh -- device store layout, context and fp64 geometry for liblc.
+//
+// Layout:
+//   kf_pose      double[n_kf][13]       world->camera, mutable by corrections
+//   kf_cam       int32[n_kf]
+//   kf_fbeg      int32[n_kf+1]          CSR into feature arrays
+//   kf_cell      uint16[n_kf][G+1]      per-keyframe cell start offsets (cell-major)
+//   fc_uv        float2[n_feat]         keypoints, cell-major per keyframe
+//   fc_meta      uint32[n_feat]         local original index (bits 0-15) | octave << 16
+//   fc_desc      uint4[n_feat][2]       descriptors, cell-major
+//   feat_mp      int32[n_feat]          associations, ORIGINAL order (mutable)
+//   feat_angle   float[n_feat]          original order
+//   mp_rec       MpRec[n_mp]            64-B rows: pos, dmax, normal, angle, desc
+//   mp_flags     uint8[n_mp]; mp_ref_kf, mp_replaced_by, mp_nobs, mp_corr_ref int32[n_mp]
+//   mp_loop_ep   uint32[n_mp]           LoopSet membership stamp (== fuse epoch)
+//   kf_S_corr    double[n_kf][13]; kf_in_win int32[n_kf]   loop state (WINDOW -> ALL)
+//   kf_win_ep    uint32[n_kf]; kf_win_pos int32[n_kf]      window membership of a fuse call
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "lc.h"
+
+#define LC_NTHREADS 256
+
+struct __align__(16) MpRec {
+  float pos[3];
+  float dmax;
+  float normal[3];
+  float angle;
+  uint4 desc[2];
+};
+static_assert(sizeof(MpRec) == 64, "MpRec must be 64 bytes");
+
+struct DevCam {
+  int model;
+  int cols, rows;
+  int pad;
+  double fx, fy, cx, cy;
+  double k[4];
+  double min_x, max_x, min_y, max_y;
+  double cell_sx, cell_sy;  // cols / (max_x - min_x), rows / (max_y - min_y)
+};
+
+struct Store {
+  int32_t n_kf = 0, n_feat = 0, n_mp = 0, n_cams = 0;
+  int32_t n_levels = 0, cols = 0, rows = 0, G = 0;
+  double scale[LC_MAX_LEVELS];
+  int32_t max_F = 0;
+  // device arrays
+  double* kf_pose = nullptr;
+  int32_t* kf_cam = nullptr;
+  int32_t* kf_fbeg = nullptr;
+  uint16_t* kf_cell = nullptr;
+  float2* fc_uv = nullptr;
+  uint32_t* fc_meta = nullptr;
+  uint4* fc_desc = nullptr;
+  int32_t* feat_mp = nullptr;
+  float* feat_angle = nullptr;
+  MpRec* mp_rec = nullptr;
+  uint8_t* mp_flags = nullptr;
+  int32_t* mp_ref_kf = nullptr;
+  int32_t* mp_replaced_by = nullptr;
+  int32_t* mp_nobs = nullptr;
+  int32_t* mp_corr_ref = nullptr;
+  uint32_t* mp_loop_ep = nullptr;
+  int32_t* mp_owner = nullptr;
+  double* kf_S_corr = nullptr;
+  int32_t* kf_in_win = nullptr;
+  uint32_t* kf_win_ep = nullptr;
+  int32_t* kf_win_pos = nullptr;
+  DevCam* cams = nullptr;
+  // host copies
+  std::vector<int32_t> h_fbeg;
+  std::vector<int32_t> h_in_win;  // mirrors kf_in_win (set by WINDOW, cleared by ALL)
+};
+
+// Parameters of one matching launch, passed by value.
+struct MatchArgs {
+  // store
+  const double* kf_pose;  // unused by the kernel (units carry S)
+  const int32_t* kf_cam;
+  const int32_t* kf_fbeg;
+  const uint16_t* kf_cell;
+  const float2* fc_uv;
+  const uint32_t* fc_meta;
+  const uint4* fc_desc;
+  const int32_t* feat_mp;
+  const MpRec* mp_rec;
+  const uint8_t* mp_flags;
+  const DevCam* cams;
+  int32_t cols, rows, G, n_levels;
+  double scale[LC_MAX_LEVELS];
+  // call
+  const int32_t* unit_kf;      // [n_units]
+  const double* unit_S;        // [n_units][13], or nullptr: kf_S_corr of the unit's keyframe
+  const double* kf_S_corr;     // [n_kf][13] S^corr of the last WINDOW correction
+  int32_t n_mp;
+  const int32_t* unit_param;   // [n_units] (SBP) or nullptr (param 0)
+  const int64_t* unit_woff;    // [n_units] offset into the winner table
+  const int64_t* unit_toff;    // [n_units] offset into pair_taken (SBP)
+  const int64_t* unit_lbeg;    // [n_units] list begin in mp_list
+  const int64_t* unit_qoff;    // [n_units] debug query index of list entry 0
+  const lc_match_params* params;
+  const int32_t* blk_unit;     // [n_blocks]
+  const int64_t* blk_q0;       // [n_blocks] list positions [q0, q1)
+  const int64_t* blk_q1;
+  const int32_t* mp_list;
+  const int32_t* taken;        // SBP pair_taken (pair-major) or nullptr
+  unsigned long long* winner;  // packed (H<<32)|q, window/pair-major
+  unsigned long long* counts;  // [LC_NCOUNT] (fuse) or [n_units][LC_NCOUNT] (SBP)
+  int64_t* dbg_best;
+  double* dbg_uv;
+  int32_t* dbg_ncand;
+  int32_t hash_size;           // power of 2
+};
+
+struct lc_ctx {
+  int device = 0;
+  bool broken = false;
+  std::string err;
+  Store st;
+  bool has_map = false;
+  bool has_saved = false;
+  uint32_t epoch = 0;
+  int64_t launches = 0;
+  // scratch arena: named growable device buffers
+  std::vector<void*> scr_ptr;
+  std::vector<size_t> scr_cap;
+  // pinned staging ring
+  void* pin = nullptr;
+  size_t pin_cap = 0;
+  size_t pin_used = 0;
+  cudaEvent_t pin_ev = nullptr;  // recorded after the last H2D out of staging
+  bool pin_ev_pending = false;
+  // saved state (lc_state_save)
+  void* sv = nullptr;
+  size_t sv_cap = 0;
+  std::vector<int32_t> sv_in_win;
+  // deferred host copies (outputs to host memory)
+  struct HostOut { void* host; const void* dev; size_t bytes; };
+  std::vector<HostOut> host_outs;
+};
+
+// ---------------------------------------------------------------------------
+// fp64 Sim3 arithmetic in the order of DESIGN.md "Sim3 arithmetic" (the build
+// uses -fmad=false so nothing below is contracted into an FMA).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ double lc_row3(const double* r, const double* p) {
+  return (r[0] * p[0] + r[1] * p[1]) + r[2] * p[2];
+}
+__host__ __device__ __forceinline__ double lc_col3(const double* R, int i, const double* p) {
+  return (R[0 + i] * p[0] + R[3 + i] * p[1]) + R[6 + i] * p[2];
+}
+__host__ __device__ __forceinline__ void lc_sim3_apply(const double* S, const double* p, double* o) {
+  double q0 = lc_row3(S + 0, p), q1 = lc_row3(S + 3, p), q2 = lc_row3(S + 6, p);
+  o[0] = S[12] * q0 + S[9];
+  o[1] = S[12] * q1 + S[10];
+  o[2] = S[12] * q2 + S[11];
+}
+__host__ __device__ __forceinline__ void lc_sim3_compose(const double* A, const double* B, double* o) {
+  double r[13];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      r[3 * i + j] = (A[3 * i + 0] * B[0 + j] + A[3 * i + 1] * B[3 + j]) + A[3 * i + 2] * B[6 + j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r[9 + i] = A[12] * lc_row3(A + 3 * i, B + 9) + A[9 + i];
+  r[12] = A[12] * B[12];
+#pragma unroll
+  for (int i = 0; i < 13; ++i) o[i] = r[i];
+}
+__host__ __device__ __forceinline__ void lc_sim3_inverse(const double* S, double* o) {
+  double r[13];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) r[3 * i + j] = S[3 * j + i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r[9 + i] = -lc_col3(S, i, S + 9) / S[12];
+  r[12] = 1.0 / S[12];
+#pragma unroll
+  for (int i = 0; i < 13; ++i) o[i] = r[i];
+}
+__host__ __device__ __forceinline__ void lc_sim3_se3(const double* S, double* o) {
+  double r[13];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) r[i] = S[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r[9 + i] = S[9 + i] / S[12];
+  r[12] = 1.0;
+#pragma unroll
+  for (int i = 0; i < 13; ++i) o[i] = r[i];
+}
+
+// Projection (reading A29). Returns u, v in fp64.
+__device__ __forceinline__ void lc_project(const DevCam& c, double x, double y, double z,
+                                           double& u, double& v) {
+  if (c.model == 0) {
+    u = ((c.fx * x) / z) + c.cx;
+    v = ((c.fy * y) / z) + c.cy;
+    return;
+  }
+  double rho = sqrt((x * x) + (y * y));
+  if (rho == 0.0) { u = c.cx; v = c.cy; return; }
+  double th = atan2(rho, z);
+  double t2 = th * th;
+  double a = c.k[3];
+  a = c.k[2] + t2 * a;
+  a = c.k[1] + t2 * a;
+  a = c.k[0] + t2 * a;
+  a = 1.0 + t2 * a;
+  double r = th * a;
+  u = ((c.fx * r) * (x / rho)) + c.cx;
+  v = ((c.fy * r) * (y / rho)) + c.cy;
+}
+
+// ---------------------------------------------------------------------------
+// kernel launchers (defined in the .cu files)
+// ---------------------------------------------------------------------------
+cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, const float* dmax,
+                               const uint8_t* desc, const float* ang, const float* fuv,
+                               const uint8_t* foct, const uint8_t* fdesc, uint32_t* d_errs,
+                               cudaStream_t s);
+cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max,
+                         cudaStream_t s);
+cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int n_w, const int32_t* d_window,
+                             const int64_t* d_woff, int64_t n_wfeat, const int32_t* mp_list,
+                             int64_t n_list_total, unsigned long long* winner,
+                             unsigned long long* victim, cudaStream_t s);
+cudaError_t launch_fuse_resolve(lc_ctx* c, int mode, int n_units, const int32_t* unit_kf,
+                                const int64_t* unit_woff, const int64_t* unit_toff,
+                                const int32_t* unit_param, const lc_match_params* params,
+                                const int32_t* taken, unsigned long long* winner,
+                                unsigned long long* victim, int8_t* action, int32_t* out_mp,
+                                int32_t* out_dist, unsigned long long* counts, int F_max,
+                                cudaStream_t s);
+cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned long long* winner,
+                              const unsigned long long* victim, unsigned long long* counts,
+                              cudaStream_t s);
+cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t* d_window,
+                                  const double* d_Scw, double* d_scr, unsigned long long* counts,
+                                  cudaStream_t s);
+cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
+                               unsigned long long* counts, cudaStream_t s);
+cudaError_t launch_fill_u64(lc_ctx* c, unsigned long long* p, int64_t n, unsigned long long v,
+                            cudaStream_t s);
+cudaError_t launch_state_copy(lc_ctx* c, bool save, cudaStream_t s);
+cudaError_t launch_download_pos(lc_ctx* c, float* out, cudaStream_t s);

@@ -1,0 +1,273 @@
+"""Thin Python binding of liblc (include/lc.h): same entry points, argument
+marshalling only. Arrays may be torch tensors (CPU or CUDA) or numpy arrays;
+every step of the path runs in liblc's kernels. Outputs are torch CUDA tensors
+(asynchronous, on the current stream) unless `host=True` (numpy, synchronised).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (COUNTER_NAMES, LC_CORRECT_ALL, LC_CORRECT_WINDOW, LC_FUSE_ALL, LC_FUSE_APPLY,
+                   LC_FUSE_PLAN, LC_NCOUNT, LC_NONE, LcError)
+
+__all__ = ["Context", "COUNTER_NAMES", "LC_NONE", "LC_FUSE_ALL", "LC_FUSE_PLAN", "LC_FUSE_APPLY",
+           "LC_CORRECT_WINDOW", "LC_CORRECT_ALL", "counts_dict", "camera_struct"]
+
+
+def counts_dict(arr):
+    a = arr.tolist() if hasattr(arr, "tolist") else list(arr)
+    return dict(zip(COUNTER_NAMES, [int(x) for x in a]))
+
+
+def camera_struct(cam) -> _lib.lc_camera:
+    d = cam.as_dict() if hasattr(cam, "as_dict") else dict(cam)
+    c = _lib.lc_camera()
+    c.model = int(d["model"])
+    c.fx, c.fy, c.cx, c.cy = float(d["fx"]), float(d["fy"]), float(d["cx"]), float(d["cy"])
+    for i in range(4):
+        c.k[i] = float(d["k"][i])
+    c.min_x, c.max_x = float(d["min_x"]), float(d["max_x"])
+    c.min_y, c.max_y = float(d["min_y"]), float(d["max_y"])
+    return c
+
+
+def _params(p) -> _lib.lc_match_params:
+    if isinstance(p, _lib.lc_match_params):
+        return p
+    th, mh, rn, rd, co = p
+    return _lib.lc_match_params(int(th), int(mh), int(rn), int(rd), int(co))
+
+
+_NP = {torch.float32: np.float32, torch.float64: np.float64, torch.int32: np.int32,
+       torch.int64: np.int64, torch.uint8: np.uint8, torch.int8: np.int8}
+
+
+class _Keep:
+    """Holds converted arrays alive for the duration of a call."""
+
+    def __init__(self):
+        self.refs = []
+
+    def ptr(self, x, dtype=None):
+        if x is None:
+            return None
+        if isinstance(x, torch.Tensor):
+            if dtype is not None and _NP.get(x.dtype) != np.dtype(dtype).type:
+                x = x.to(dtype={np.float32: torch.float32, np.float64: torch.float64,
+                                np.int32: torch.int32, np.int64: torch.int64,
+                                np.uint8: torch.uint8, np.int8: torch.int8}[np.dtype(dtype).type])
+            x = x.contiguous()
+            self.refs.append(x)
+            return x.data_ptr()
+        a = np.ascontiguousarray(x, dtype=dtype)
+        self.refs.append(a)
+        return a.ctypes.data
+
+
+class Context:
+    """One liblc context on one CUDA device (lc_create / lc_destroy)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        self.device = int(device)
+        h = C.c_void_p()
+        st = self.lib.lc_create(C.byref(h), self.device)
+        if st != 0:
+            raise LcError("lc_create", st, self.lib.lc_last_error(None).decode())
+        self.h = h
+        self.n_kf = self.n_feat = self.n_mp = 0
+        self.kf_feat_begin = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.lc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- plumbing ---------------------------------------------------------------
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _check(self, fn, st):
+        if st != 0:
+            raise LcError(fn, st, self.lib.lc_last_error(self.h).decode())
+
+    def _dev(self, n, dtype):
+        return torch.empty(int(n), dtype=dtype, device=f"cuda:{self.device}")
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.lc_kernel_launches(self.h))
+
+    def synchronize(self):
+        torch.cuda.current_stream(self.device).synchronize()
+
+    # -- lc_upload_map ------------------------------------------------------------
+    def upload_map(self, arrays: dict, cams, n_levels=8, scale_factor=1.2, grid=(64, 48)):
+        k = _Keep()
+        a = arrays
+        v = _lib.lc_map_view()
+        v.n_kf = int(len(a["kf_feat_begin"]) - 1)
+        v.n_feat = int(a["feat_mp"].shape[0])
+        v.n_mp = int(a["mp_flags"].shape[0])
+        spec = dict(kf_pose=np.float64, kf_cam=np.int32, kf_feat_begin=np.int32,
+                    feat_uv=np.float32, feat_octave=np.uint8, feat_angle=np.float32,
+                    feat_desc=np.uint8, feat_mp=np.int32, mp_pos=np.float32, mp_normal=np.float32,
+                    mp_max_dist=np.float32, mp_desc=np.uint8, mp_angle=np.float32,
+                    mp_ref_kf=np.int32, mp_flags=np.uint8)
+        for name, dt in spec.items():
+            setattr(v, name, k.ptr(a[name], dt))
+        cams = list(cams) if isinstance(cams, (list, tuple)) else [cams]
+        carr = (_lib.lc_camera * len(cams))(*[camera_struct(c) for c in cams])
+        prm = _lib.lc_map_params(int(n_levels), int(grid[0]), int(grid[1]), 0, float(scale_factor))
+        st = self.lib.lc_upload_map(self.h, C.byref(v), carr, len(cams), C.byref(prm), self._stream())
+        self._check("lc_upload_map", st)
+        self.n_kf, self.n_feat, self.n_mp = v.n_kf, v.n_feat, v.n_mp
+        fb = a["kf_feat_begin"]
+        self.kf_feat_begin = (fb.cpu().numpy() if isinstance(fb, torch.Tensor) else np.asarray(fb)).astype(np.int64)
+
+    def n_feat_of(self, kfs):
+        if self.kf_feat_begin is None:   # no map: the library reports LC_ESTATE
+            return 0
+        kfs = np.asarray(kfs, np.int64)
+        if kfs.size and (kfs.min() < 0 or kfs.max() >= self.n_kf):   # library reports LC_ERANGE
+            return 0
+        return int(np.sum(self.kf_feat_begin[kfs + 1] - self.kf_feat_begin[kfs]))
+
+    # -- lc_download_map ----------------------------------------------------------
+    def download_map(self):
+        out = dict(kf_pose=np.zeros((self.n_kf, 13), np.float64),
+                   feat_mp=np.zeros(self.n_feat, np.int32),
+                   mp_pos=np.zeros((self.n_mp, 3), np.float32),
+                   mp_flags=np.zeros(self.n_mp, np.uint8),
+                   mp_replaced_by=np.zeros(self.n_mp, np.int32),
+                   mp_nobs=np.zeros(self.n_mp, np.int32))
+        s = _lib.lc_map_state(*[out[n].ctypes.data for n in ("kf_pose", "feat_mp", "mp_pos",
+                                                              "mp_flags", "mp_replaced_by", "mp_nobs")])
+        self._check("lc_download_map", self.lib.lc_download_map(self.h, C.byref(s), self._stream()))
+        self.synchronize()
+        return out
+
+    def state_save(self):
+        self._check("lc_state_save", self.lib.lc_state_save(self.h, self._stream()))
+
+    def state_restore(self):
+        self._check("lc_state_restore", self.lib.lc_state_restore(self.h, self._stream()))
+
+    # -- lc_correct_sim3 ----------------------------------------------------------
+    def correct_window(self, cur_kf, S_cw_corr, window, host=True):
+        k = _Keep()
+        window = np.ascontiguousarray(window, np.int32)
+        S = np.ascontiguousarray(S_cw_corr, np.float64)
+        if host:
+            outS = np.zeros((len(window), 13), np.float64)
+            cnt = np.zeros(LC_NCOUNT, np.int64)
+        else:
+            outS = self._dev(len(window) * 13, torch.float64)
+            cnt = self._dev(LC_NCOUNT, torch.int64)
+        st = self.lib.lc_correct_sim3(self.h, LC_CORRECT_WINDOW, int(cur_kf), k.ptr(S), len(window),
+                                      k.ptr(window), None, k.ptr(outS), k.ptr(cnt), self._stream())
+        self._check("lc_correct_sim3", st)
+        if host:
+            self.synchronize()
+            return outS, counts_dict(cnt)
+        return outS.view(-1, 13), cnt
+
+    def correct_all(self, S_opt, host=True):
+        k = _Keep()
+        cnt = np.zeros(LC_NCOUNT, np.int64) if host else self._dev(LC_NCOUNT, torch.int64)
+        st = self.lib.lc_correct_sim3(self.h, LC_CORRECT_ALL, 0, None, 0, None,
+                                      k.ptr(S_opt, np.float64), None, k.ptr(cnt), self._stream())
+        self._check("lc_correct_sim3", st)
+        if host:
+            self.synchronize()
+            return counts_dict(cnt)
+        return cnt
+
+    # -- lc_fuse -------------------------------------------------------------------
+    def fuse(self, window, mp_list, params, *, window_S=None, win_list_begin=None,
+             phase=LC_FUSE_ALL, w_lo=0, w_hi=None, winner=None, victim=None, action=True,
+             debug=False, host=True):
+        """Returns dict(winner, victim, action, counts[, best, uv, ncand]).
+        winner / victim: pass tensors to use them in place (PLAN -> NCCL -> APPLY)."""
+        k = _Keep()
+        window = np.ascontiguousarray(window, np.int32)
+        n_w = len(window)
+        w_hi = n_w if w_hi is None else int(w_hi)
+        wb = None if win_list_begin is None else np.ascontiguousarray(win_list_begin, np.int32)
+        wS = None if window_S is None else np.ascontiguousarray(window_S, np.float64)
+        n_list = int(mp_list.shape[0]) if hasattr(mp_list, "shape") else len(mp_list)
+        nwf = self.n_feat_of(window)
+        nq = int(wb[-1]) if wb is not None else n_w * n_list
+        mk = (lambda n, dt, npdt: np.zeros(n, npdt)) if host else (lambda n, dt, npdt: self._dev(n, dt))
+        if winner is None:
+            winner = mk(nwf, torch.int64, np.int64)
+        if victim is None:
+            victim = mk(self.n_mp, torch.int64, np.int64)
+        act = mk(nwf, torch.int8, np.int8) if action else None
+        cnt = mk(LC_NCOUNT, torch.int64, np.int64)
+        dbg = None
+        dd = {}
+        if debug:
+            dd = dict(best=mk(nq, torch.int64, np.int64), uv=mk(2 * nq, torch.float64, np.float64),
+                      ncand=mk(nq, torch.int32, np.int32))
+            dbg = _lib.lc_query_debug(k.ptr(dd["best"]), k.ptr(dd["uv"]), k.ptr(dd["ncand"]))
+        st = self.lib.lc_fuse(self.h, int(phase), int(w_lo), int(w_hi), n_w, k.ptr(window), k.ptr(wS),
+                              k.ptr(wb), k.ptr(mp_list, np.int32), n_list, C.byref(_params(params)),
+                              k.ptr(winner), k.ptr(victim), k.ptr(act),
+                              C.byref(dbg) if dbg is not None else None, k.ptr(cnt), self._stream())
+        self._check("lc_fuse", st)
+        if host:
+            self.synchronize()
+        out = dict(winner=winner, victim=victim, action=act,
+                   counts=counts_dict(cnt) if host else cnt)
+        if debug:
+            dd["uv"] = dd["uv"].reshape(-1, 2) if host else dd["uv"].view(-1, 2)
+            out.update(dd)
+        return out
+
+    # -- lc_search_by_projection ----------------------------------------------------
+    def search_by_projection(self, pair_kf, pair_S, pair_param, params, pair_list_begin, mp_list,
+                             pair_taken=None, debug=False, host=True):
+        k = _Keep()
+        pair_kf = np.ascontiguousarray(pair_kf, np.int32)
+        n_pairs = len(pair_kf)
+        plb = np.ascontiguousarray(pair_list_begin, np.int32)
+        prms = (_lib.lc_match_params * len(params))(*[_params(p) for p in params])
+        ntot = self.n_feat_of(pair_kf)
+        nq = int(plb[-1])
+        mk = (lambda n, dt, npdt: np.zeros(n, npdt)) if host else (lambda n, dt, npdt: self._dev(n, dt))
+        o_mp = mk(ntot, torch.int32, np.int32)
+        o_d = mk(ntot, torch.int32, np.int32)
+        cnt = mk(n_pairs * LC_NCOUNT, torch.int64, np.int64)
+        dbg = None
+        dd = {}
+        if debug:
+            dd = dict(best=mk(nq, torch.int64, np.int64), uv=mk(2 * nq, torch.float64, np.float64),
+                      ncand=mk(nq, torch.int32, np.int32))
+            dbg = _lib.lc_query_debug(k.ptr(dd["best"]), k.ptr(dd["uv"]), k.ptr(dd["ncand"]))
+        st = self.lib.lc_search_by_projection(
+            self.h, n_pairs, k.ptr(pair_kf), k.ptr(pair_S, np.float64), k.ptr(pair_param, np.int32),
+            prms, len(params), k.ptr(plb), k.ptr(mp_list, np.int32), k.ptr(pair_taken, np.int32),
+            k.ptr(o_mp), k.ptr(o_d), C.byref(dbg) if dbg is not None else None, k.ptr(cnt),
+            self._stream())
+        self._check("lc_search_by_projection", st)
+        if host:
+            self.synchronize()
+            cnt = cnt.reshape(n_pairs, LC_NCOUNT)
+        else:
+            cnt = cnt.view(n_pairs, LC_NCOUNT)
+        out = dict(feat_mp=o_mp, feat_dist=o_d, counts=cnt)
+        if debug:
+            dd["uv"] = dd["uv"].reshape(-1, 2) if host else dd["uv"].view(-1, 2)
+            out.update(dd)
+        return out
