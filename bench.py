@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 loop-closing fuse/correct path (BASELINE.json metric:
+"candidate (mappoint x feature) Hamming matches/s; ms per loop fuse+correct").
+
+One step = one loop event over the C5 map (BASELINE.json configs[4]: 5,000 KFs,
+~1M map points, 2,000 features/KF; the whole second pass, 2,500 KFs, is the fusion
+window with per-keyframe loop lists, ~8.8M queries):
+  lc_correct_sim3(WINDOW) -> lc_fuse(ALL) -> lc_correct_sim3(ALL)
+Between steps (untimed) the mutable map state is restored from a device-side copy
+(lc_state_restore) and L2 is flushed by a 512 MB write, so every step does identical
+work from a cold L2. value = candidate matches per step / device step time.
+
+Multi-GPU (torchrun, NCCL): WINDOW and ALL are replicated (~10 us, cheaper than a
+collective), fusion is keyframe-sharded: PLAN on the shard, one all_reduce(MIN) of the
+int64 [winner | victim] words, APPLY on every rank (paper_2603_17201_b200/dist.py).
+Total work is fixed as N grows -> "scaling": "strong".
+
+--impl reference times the CPU oracle (oracle/, the plain definition) on bounded
+samples of the same workload on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate (mappoint×feature) Hamming matches/s; ms per loop fuse+correct"
+UNIT = "matches/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="lc", choices=["lc", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--profile-only", action="store_true",
+                    help="few steps, no e2e/cpu legs (for ncu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.p = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{gpu_index}.csv")
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(mx)) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def roofline_bytes(w, n_queries, n_proposals):
+    """Algorithmic bytes of one k_project_match<fuse> launch (SURVEY.md §8(d) per-unit
+    figures): 48 B per window-keyframe feature (the keyframe block:
+    uv 8 + octave/index 4 + descriptor 32 + association 4), 68 B per query (list entry 4 +
+    64-B map-point record), 8 B per proposal (winner word)."""
+    n_wfeat = int(np.sum(np.diff(w.kf_feat_begin)[w.window]))
+    return 48 * n_wfeat + 68 * int(n_queries) + 8 * int(n_proposals)
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def load_traffic():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------
+def run_reference(args, w, ws, rank):
+    """CPU oracle (as it stands) on bounded samples of the same workload."""
+    import oracle
+    from lcsynth.world import FUSE_PARAMS
+    if rank != 0:
+        return
+    om = oracle.OracleMap(w)
+    om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    # size the fuse sample so one step takes ~2 s
+    n_kf_sample = 4
+    t0 = time.time()
+    om.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin,
+            phase=1, w_lo=0, w_hi=n_kf_sample)
+    per_kf = (time.time() - t0) / n_kf_sample
+    nwin = len(w.window)
+    n_kf_sample = min(nwin, max(1, int(2.0 / max(per_kf, 1e-6))))
+    times, cands, lo = [], [], 0
+    for step in range(args.warmup + args.steps):
+        lo = (lo + n_kf_sample) % max(nwin - n_kf_sample + 1, 1)
+        t0 = time.perf_counter()
+        r = om.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S,
+                    win_list_begin=w.win_list_begin, phase=1, w_lo=lo, w_hi=lo + n_kf_sample)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+            cands.append(r["counts"]["candidates"])
+    value = float(np.sum(cands) / np.sum(times))
+    sample = (f"oracle fuse PLAN (projection + brute-force windowed Hamming match + conflicts) "
+              f"over {n_kf_sample} of {nwin} window keyframes per step ({args.config}, seed {args.seed})")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * float(np.mean(times)), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} sampled: {n_kf_sample} window KFs/step",
+                       "seed": args.seed},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(w, seconds):
+    """Oracle (never tuned) on a bounded sample of the benchmark workload."""
+    import oracle
+    from lcsynth.world import FUSE_PARAMS
+    om = oracle.OracleMap(w)
+    om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    t0 = time.perf_counter()
+    n, cands, lo = 0, 0, 0
+    step = 8
+    while time.perf_counter() - t0 < seconds and lo < len(w.window):
+        r = om.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S,
+                    win_list_begin=w.win_list_begin, phase=1, w_lo=lo, w_hi=min(lo + step, len(w.window)))
+        cands += r["counts"]["candidates"]
+        n += min(step, len(w.window) - lo)
+        lo += step
+    dt = time.perf_counter() - t0
+    return {"value": cands / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"fuse PLAN of the first {n} of {len(w.window)} window keyframes "
+                      f"({cands} candidate matches, {dt:.1f} s, single thread)"}
+
+
+# ----------------------------------------------------------------------------
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    from lcsynth import make_world
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        w = make_world(args.config, args.seed)
+        run_reference(args, w, ws, rank)
+        return
+
+    import torch
+    import torch.distributed as tdist
+    from lcsynth.world import FUSE_PARAMS
+    from paper_2603_17201_b200 import Context
+    from paper_2603_17201_b200 import dist as lcdist
+    from paper_2603_17201_b200 import _lib
+
+    if args.warmup < 3:
+        args.warmup = 3
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if ws > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+    w = make_world(args.config, args.seed)
+    ctx = Context(local)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    ctx.state_save()
+    stream = torch.cuda.current_stream(dev)
+
+    mp_list_d = torch.from_numpy(w.mp_list).to(dev)
+    S_opt_d = torch.from_numpy(w.S_opt).to(dev)
+    n_wfeat = ctx.n_feat_of(w.window)
+    tables = torch.empty(n_wfeat + w.n_mp, dtype=torch.int64, device=dev)
+    win_t, vic_t = tables[:n_wfeat], tables[n_wfeat:]
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    cnt_fuse = None
+
+    def step():
+        ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
+        if ws == 1:
+            r = ctx.fuse(w.window, mp_list_d, FUSE_PARAMS, window_S=w.win_S,
+                         win_list_begin=w.win_list_begin, winner=win_t, victim=vic_t,
+                         action=False, host=False)
+            c = r["counts"]
+        else:
+            c, _, _ = lcdist.fuse_sharded(ctx, w.window, mp_list_d, FUSE_PARAMS, window_S=w.win_S,
+                                          win_list_begin=w.win_list_begin, device=dev, tables=tables)
+        ctx.correct_all(S_opt_d, host=False)
+        return c
+
+    def reset():
+        ctx.state_restore()
+        flush.fill_(1.0)
+
+    # warm-up
+    for _ in range(args.warmup):
+        reset()
+        cnt_fuse = step()
+    torch.cuda.synchronize()
+    counts = _lib.COUNTER_NAMES
+    cf = cnt_fuse.cpu().numpy() if hasattr(cnt_fuse, "cpu") else np.asarray(list(cnt_fuse.values()))
+    cand_rank = int(cf[counts.index("candidates")])
+    q_rank = int(cf[counts.index("queries")])
+    prop_rank = int(cf[counts.index("proposals")])
+
+    # timed region: barrier + sync on both sides, events per step on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if ws > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    l0 = ctx.kernel_launches()
+    ctx.profile_enable(True)
+    for i in range(args.steps):
+        reset()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        tdist.barrier()
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    launches_timed = ctx.kernel_launches() - l0 - prof["state"][1]
+    clk = clocks.stop()
+    ms = np.array([a.elapsed_time(b) for a, b in ev])
+    ms_mean = float(ms.mean())
+    ms_t = torch.tensor([ms_mean], dtype=torch.float64, device=dev)
+    cand_t = torch.tensor([cand_rank], dtype=torch.int64, device=dev)
+    if ws > 1:
+        tdist.all_reduce(ms_t, op=tdist.ReduceOp.MAX)
+        tdist.all_reduce(cand_t, op=tdist.ReduceOp.SUM)
+    ms_step = float(ms_t.item())
+    cand_total = int(cand_t.item())
+    value = cand_total / (ms_step / 1000.0)
+
+    # roofline of the dominant kernel (k_project_match<fuse>)
+    match_ms = prof["match"][0] / args.steps
+    fam_ms = {k: v[0] / args.steps for k, v in prof.items() if v[1]}
+    B = roofline_bytes(w, q_rank, prop_rank) if ws == 1 else None
+    peaks = load_peaks()
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured" if peak else "fallback"
+    peak = peak or 6650.0
+    traffic = load_traffic().get("k_project_match_fuse", {}).get(args.config)
+    roof = None
+    if B is not None and match_ms > 0:
+        ach = B / (match_ms / 1000.0) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": traffic, "kernel": "k_project_match<fuse>",
+                "algorithmic_bytes": B, "kernel_ms": round(match_ms, 5), "peak_source": peak_src,
+                "step_share": round(match_ms / ms_step, 4)}
+
+    # e2e through the public API with host (pinned) buffers: H2D of the loop event's
+    # inputs and D2H of its result (counts + victim table) inside the timed region
+    e2e = None
+    if not args.no_e2e and not args.profile_only and ws == 1:
+        mp_pin = torch.from_numpy(w.mp_list).pin_memory()
+        Sopt_pin = torch.from_numpy(w.S_opt).pin_memory()
+        vic_pin = torch.empty(w.n_mp, dtype=torch.int64).pin_memory()
+        cnt_pin = torch.empty(len(counts), dtype=torch.int64).pin_memory()
+        win_pin = torch.empty(n_wfeat, dtype=torch.int64).pin_memory()
+        h2d = mp_pin.numel() * 4 + Sopt_pin.numel() * 8 + w.win_S.nbytes + w.window.nbytes * 2 \
+            + w.win_list_begin.nbytes + w.S_cw_corr.nbytes
+        d2h = vic_pin.numel() * 8 + cnt_pin.numel() * 8
+        ee = []
+        for i in range(args.warmup + args.steps):
+            reset()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
+            r = ctx.fuse(w.window, mp_pin, FUSE_PARAMS, window_S=w.win_S,
+                         win_list_begin=w.win_list_begin, winner=win_t, victim=vic_pin,
+                         action=False, host=False)
+            ctx.correct_all(Sopt_pin, host=False)
+            cnt_pin.copy_(r["counts"], non_blocking=True)
+            b.record(stream)
+            b.synchronize()
+            if i >= args.warmup:
+                ee.append(a.elapsed_time(b))
+        e_ms = float(np.mean(ee))
+        e2e = {"value": cand_rank / (e_ms / 1000.0), "unit": UNIT, "ms_per_step": round(e_ms, 4),
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_only:
+        cpu = cpu_baseline(w, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32 popcount / f64 geometry", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {w.n_kf} KFs, {w.n_mp} map points, "
+                                   f"{int(np.diff(w.kf_feat_begin).max())} feats/KF, "
+                                   f"{len(w.window)}-KF fusion window, {len(w.mp_list)} queries "
+                                   f"(WINDOW correct + fuse + ALL correct)",
+                       "seed": args.seed, "candidates_per_step": cand_total,
+                       "parallelism": f"keyframe-sharded x{ws}" if ws > 1 else "1 GPU",
+                       "l2": "flushed between steps (512 MB write) after an untimed state restore"},
+            "ms_per_loop": round(ms_step, 5),
+            "kernel_ms_per_step": {k: round(v, 5) for k, v in fam_ms.items()},
+            "gpu_launches": int(launches_timed),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -214,6 +214,19 @@ const char* lc_last_error(const lc_ctx* ctx);
 int64_t lc_kernel_launches(const lc_ctx* ctx);
 
 /* ---------------------------------------------------------------------------
+ * Device-time accounting (tracing). When enabled, each launch group of the
+ * families below is bracketed by CUDA events on the call's stream; lc_profile_read
+ * waits for the recorded events and returns the accumulated device milliseconds
+ * and kernel launches per family since the last enable (ms/launches [host],
+ * LC_NPROF entries each). Enabling (on = 1) resets the accumulators; on = 0 stops.
+ * ------------------------------------------------------------------------- */
+enum { LC_PROF_UPLOAD = 0, LC_PROF_CORRECT_WINDOW, LC_PROF_CORRECT_ALL, LC_PROF_FUSE_PREP,
+       LC_PROF_MATCH, LC_PROF_RESOLVE, LC_PROF_APPLY, LC_PROF_SBP_MATCH, LC_PROF_SBP_RESOLVE,
+       LC_PROF_STATE, LC_NPROF };
+lc_status lc_profile_enable(lc_ctx* ctx, int32_t on);
+lc_status lc_profile_read(lc_ctx* ctx, double* ms, int64_t* launches);
+
+/* ---------------------------------------------------------------------------
  * lc_upload_map -- GPU-resident keyframe storage.
  *
  * Packs the SoA view into the device store: map-point records (position, dmax,

@@ -262,6 +262,8 @@ class OracleMap:
                        edge=np.zeros(nq, np.uint8))
         cnt = np.zeros(len(COUNTER_NAMES), np.int64)
         prm = make_params(params)
+        if not (0 <= w_lo <= w_hi <= n_w):
+            raise ValueError("bad shard range")
         lib().orc_fuse(C.byref(self._m), C.c_int32(phase), C.c_int32(w_lo), C.c_int32(w_hi),
                        C.c_int32(n_w), _p(window), _p(wS), _p(wb), _p(mp_list),
                        C.c_int32(len(mp_list)), C.byref(prm), _p(winner), _p(victim), _p(action),

@@ -435,6 +435,7 @@ int orc_fuse(orc_map *m, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_w,
              int64_t *io_winner, int64_t *io_victim, int8_t *out_action,
              int32_t *out_status, int64_t *out_best, double *out_uv, int32_t *out_ncand,
              uint8_t *out_edge, int64_t *cnt) {
+  if (n_w <= 0 || w_lo < 0 || w_hi > n_w || w_lo > w_hi) return -1;
   double scale[64];
   orc_scale_table(m->n_levels, m->scale_factor, scale);
   int64_t *woff = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_w + 1));

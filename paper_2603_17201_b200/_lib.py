@@ -24,6 +24,8 @@ COUNTER_NAMES = [
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
 ]
 LC_NCOUNT = len(COUNTER_NAMES)
+PROF_NAMES = ["upload", "correct_window", "correct_all", "fuse_prep", "match", "resolve", "apply",
+              "sbp_match", "sbp_resolve", "state"]
 
 
 class lc_sim3(C.Structure):
@@ -89,6 +91,8 @@ def load():
         "lc_destroy": (i32, [vp]),
         "lc_last_error": (C.c_char_p, [vp]),
         "lc_kernel_launches": (i64, [vp]),
+        "lc_profile_enable": (i32, [vp, i32]),
+        "lc_profile_read": (i32, [vp, vp, vp]),
         "lc_upload_map": (i32, [vp, P(lc_map_view), vp, i32, P(lc_map_params), vp]),
         "lc_download_map": (i32, [vp, P(lc_map_state), vp]),
         "lc_state_save": (i32, [vp, vp]),
@@ -108,6 +112,7 @@ def load():
 
 
 def exported_symbols():
-    return ["lc_create", "lc_destroy", "lc_last_error", "lc_kernel_launches", "lc_upload_map",
+    return ["lc_create", "lc_destroy", "lc_last_error", "lc_kernel_launches", "lc_profile_enable",
+            "lc_profile_read", "lc_upload_map",
             "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse",
             "lc_search_by_projection"]

@@ -162,6 +162,38 @@ struct Call {
   }
 };
 
+// Brackets one launch group with timing events when profiling is on.
+struct Prof {
+  lc_ctx* c;
+  int fam;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  int64_t l0 = 0;
+  static cudaEvent_t get(lc_ctx* c) {
+    if (!c->ev_pool.empty()) {
+      cudaEvent_t e = c->ev_pool.back();
+      c->ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    return e;
+  }
+  Prof(lc_ctx* ctx, int f, cudaStream_t st) : c(ctx), fam(f), s(st) {
+    if (!c->prof) return;
+    a = get(c);
+    if (a) cudaEventRecord(a, s);
+    l0 = c->launches;
+  }
+  ~Prof() {
+    if (!a) return;
+    cudaEvent_t b = get(c);
+    if (!b) return;
+    cudaEventRecord(b, s);
+    c->prof_pending.push_back({fam, a, b, c->launches - l0});
+  }
+};
+
 template <typename F>
 lc_status guarded(lc_ctx* c, F&& f) {
   if (!c) return LC_EINVAL;
@@ -288,6 +320,8 @@ lc_status lc_destroy(lc_ctx* c) {
   if (c->pin) cudaFreeHost(c->pin);
   if (c->sv) cudaFree(c->sv);
   if (c->pin_ev) cudaEventDestroy(c->pin_ev);
+  for (auto& r : c->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   cudaGetLastError();
   delete c;
   return LC_OK;
@@ -296,6 +330,36 @@ lc_status lc_destroy(lc_ctx* c) {
 const char* lc_last_error(const lc_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
 
 int64_t lc_kernel_launches(const lc_ctx* c) { return c ? c->launches : 0; }
+
+lc_status lc_profile_enable(lc_ctx* c, int32_t on) {
+  return guarded(c, [&] {
+    for (auto& r : c->prof_pending) { c->ev_pool.push_back(r.a); c->ev_pool.push_back(r.b); }
+    c->prof_pending.clear();
+    if (on) {
+      for (int i = 0; i < LC_NPROF; ++i) { c->prof_ms[i] = 0.0; c->prof_n[i] = 0; }
+    }
+    c->prof = on != 0;
+  });
+}
+
+lc_status lc_profile_read(lc_ctx* c, double* ms, int64_t* launches) {
+  return guarded(c, [&] {
+    for (auto& r : c->prof_pending) {
+      CK(cudaEventSynchronize(r.b));
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, r.a, r.b));
+      c->prof_ms[r.fam] += t;
+      c->prof_n[r.fam] += r.launches;
+      c->ev_pool.push_back(r.a);
+      c->ev_pool.push_back(r.b);
+    }
+    c->prof_pending.clear();
+    for (int i = 0; i < LC_NPROF; ++i) {
+      if (ms) ms[i] = c->prof_ms[i];
+      if (launches) launches[i] = c->prof_n[i];
+    }
+  });
+}
 
 // ----------------------------------------------------------------------------
 lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, int32_t n_cams,
@@ -414,7 +478,10 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
     const uint8_t* fdesc = call.in(m->feat_desc, 32 * NF);
     uint32_t* d_errs = (uint32_t*)call.scratch(64);
     CK(cudaMemsetAsync(d_errs, 0, 64, s));
-    CK(launch_upload_pack(c, pos, nrm, dmx, mdesc, ang, fuv, foct, fdesc, d_errs, s));
+    {
+      Prof pr(c, LC_PROF_UPLOAD, s);
+      CK(launch_upload_pack(c, pos, nrm, dmx, mdesc, ang, fuv, foct, fdesc, d_errs, s));
+    }
     uint32_t errs[16];
     CK(cudaMemcpyAsync(errs, d_errs, 64, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -451,6 +518,7 @@ lc_status lc_download_map(lc_ctx* c, const lc_map_state* o, void* stream) {
 lc_status lc_state_save(lc_ctx* c, void* stream) {
   return guarded(c, [&] {
     REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    Prof pr(c, LC_PROF_STATE, (cudaStream_t)stream);
     CK(launch_state_copy(c, true, (cudaStream_t)stream));
     c->sv_in_win = c->st.h_in_win;
     c->has_saved = true;
@@ -460,6 +528,7 @@ lc_status lc_state_save(lc_ctx* c, void* stream) {
 lc_status lc_state_restore(lc_ctx* c, void* stream) {
   return guarded(c, [&] {
     REQUIRE(c->has_map && c->has_saved, LC_ESTATE, "no saved state");
+    Prof pr(c, LC_PROF_STATE, (cudaStream_t)stream);
     CK(launch_state_copy(c, false, (cudaStream_t)stream));
     c->st.h_in_win = c->sv_in_win;
   });
@@ -487,7 +556,10 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
       call.commit();
       double* scr = (double*)call.scratch(sizeof(double) * 39 * (size_t)n_window);
       CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
-      CK(launch_correct_window(c, 0, n_window, d_win, d_S, scr, cnt, call.s));
+      {
+        Prof pr(c, LC_PROF_CORRECT_WINDOW, call.s);
+        CK(launch_correct_window(c, 0, n_window, d_win, d_S, scr, cnt, call.s));
+      }
       if (out_S_corr) {
         if (is_device_ptr(c, out_S_corr)) {
           CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr, sizeof(double) * 39,
@@ -504,7 +576,10 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
       const double* d_opt = call.in((const double*)S_opt, 13 * (size_t)st.n_kf);
       double* scr = (double*)call.scratch(sizeof(double) * 26 * (size_t)std::max(st.n_kf, 1));
       CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
-      CK(launch_correct_all(c, d_opt, scr, cnt, call.s));
+      {
+        Prof pr(c, LC_PROF_CORRECT_ALL, call.s);
+        CK(launch_correct_all(c, d_opt, scr, cnt, call.s));
+      }
       std::fill(st.h_in_win.begin(), st.h_in_win.end(), 0);
     }
     if (out_counts) {
@@ -612,7 +687,10 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       CK(cudaMemsetAsync(st.kf_win_ep, 0, sizeof(uint32_t) * st.n_kf, call.s));
       c->epoch = 1;
     }
-    CK(launch_fuse_prep(c, phase, n_window, d_win, d_woff, n_wfeat, d_list, n_list, win, vic, call.s));
+    {
+      Prof pr(c, LC_PROF_FUSE_PREP, call.s);
+      CK(launch_fuse_prep(c, phase, n_window, d_win, d_woff, n_wfeat, d_list, n_list, win, vic, call.s));
+    }
     if (phase & LC_FUSE_PLAN) {
       a.unit_kf = d_win;
       a.unit_S = d_S;
@@ -634,11 +712,18 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       a.dbg_best = dbg_best;
       a.dbg_uv = dbg_uv;
       a.dbg_ncand = dbg_nc;
-      CK(launch_match(c, 0, a, (int)bunit.size(), F_max, call.s));
+      {
+        Prof pr(c, LC_PROF_MATCH, call.s);
+        CK(launch_match(c, 0, a, (int)bunit.size(), F_max, call.s));
+      }
+      Prof pr(c, LC_PROF_RESOLVE, call.s);
       CK(launch_fuse_resolve(c, 0, w_hi - w_lo, d_win + w_lo, d_woff + w_lo, d_woff + w_lo, nullptr,
                              d_prm, nullptr, win, vic, act, nullptr, nullptr, cnt, F_max, call.s));
     }
-    if (phase & LC_FUSE_APPLY) CK(launch_fuse_apply(c, d_woff, win, vic, cnt, call.s));
+    if (phase & LC_FUSE_APPLY) {
+      Prof pr(c, LC_PROF_APPLY, call.s);
+      CK(launch_fuse_apply(c, d_woff, win, vic, cnt, call.s));
+    }
     if (out_counts) {
       int64_t* d = call.out(out_counts, LC_NCOUNT);
       CK(cudaMemcpyAsync(d, cnt, sizeof(uint64_t) * LC_NCOUNT, cudaMemcpyDeviceToDevice, call.s));
@@ -739,7 +824,11 @@ lc_status lc_search_by_projection(lc_ctx* c, int32_t n_pairs, const int32_t* pai
       a.dbg_uv = call.out(dbg->uv, 2 * (size_t)n_list, true);
       a.dbg_ncand = call.out(dbg->ncand, (size_t)n_list, true);
     }
-    CK(launch_match(c, 1, a, (int)bunit.size(), F_max, call.s));
+    {
+      Prof pr(c, LC_PROF_SBP_MATCH, call.s);
+      CK(launch_match(c, 1, a, (int)bunit.size(), F_max, call.s));
+    }
+    Prof pr(c, LC_PROF_SBP_RESOLVE, call.s);
     CK(launch_fuse_resolve(c, 1, n_pairs, d_kf, d_off, d_off, d_param, d_prm, d_taken, win, nullptr,
                            nullptr, o_mp, o_dist, cnt, F_max, call.s));
     if (out_counts) {

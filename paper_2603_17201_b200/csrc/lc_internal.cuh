@@ -140,6 +140,13 @@ struct lc_ctx {
   void* sv = nullptr;
   size_t sv_cap = 0;
   std::vector<int32_t> sv_in_win;
+  // device-time accounting (lc_profile_*)
+  bool prof = false;
+  struct ProfRec { int fam; cudaEvent_t a, b; int64_t launches; };
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<ProfRec> prof_pending;
+  double prof_ms[LC_NPROF] = {};
+  int64_t prof_n[LC_NPROF] = {};
   // deferred host copies (outputs to host memory)
   struct HostOut { void* host; const void* dev; size_t bytes; };
   std::vector<HostOut> host_outs;

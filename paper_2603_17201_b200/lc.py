@@ -108,6 +108,17 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self.lib.lc_kernel_launches(self.h))
 
+    def profile_enable(self, on=True):
+        self._check("lc_profile_enable", self.lib.lc_profile_enable(self.h, 1 if on else 0))
+
+    def profile_read(self):
+        """{family: (device ms, kernel launches)} accumulated since profile_enable()."""
+        n = len(_lib.PROF_NAMES)
+        ms = (C.c_double * n)()
+        la = (C.c_int64 * n)()
+        self._check("lc_profile_read", self.lib.lc_profile_read(self.h, ms, la))
+        return {name: (ms[i], la[i]) for i, name in enumerate(_lib.PROF_NAMES)}
+
     def synchronize(self):
         torch.cuda.current_stream(self.device).synchronize()
 

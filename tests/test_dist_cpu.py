@@ -1,0 +1,101 @@
+"""World-size-2 (and 3) gloo tests of the multi-GPU fusion protocol on CPU.
+
+paper_2603_17201_b200.dist.fuse_sharded is run by real torch.distributed processes;
+the per-rank PLAN / APPLY are served by an oracle-backed adapter with Context.fuse's
+signature (the CUDA path is covered by tests/test_gpu_parity.py). The merged result
+must equal the single-process oracle FUSE_ALL bit for bit.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class OracleFuser:
+    """Context.fuse-compatible adapter over the CPU oracle (test infrastructure)."""
+
+    def __init__(self, om):
+        self.om = om
+        self.n_mp = om.n_mp
+
+    def n_feat_of(self, kfs):
+        return self.om.window_feat_total(kfs)
+
+    def fuse(self, window, mp_list, params, *, window_S=None, win_list_begin=None, phase=3,
+             w_lo=0, w_hi=None, winner=None, victim=None, action=True, host=True):
+        return self.om.fuse(window, mp_list, params, window_S=window_S,
+                            win_list_begin=win_list_begin, phase=phase, w_lo=w_lo, w_hi=w_hi,
+                            winner=winner, victim=victim)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, params, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from lcsynth import make_world
+    from paper_2603_17201_b200 import dist as lcdist
+    w = make_world(name, 0)
+    om = oracle.OracleMap(w)
+    if w.win_S is None:
+        om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    plan_c, app_c, tables = lcdist.fuse_sharded(OracleFuser(om), w.window, w.mp_list, params,
+                                                window_S=w.win_S, win_list_begin=w.win_list_begin)
+    plan_sum = lcdist.sum_counts(plan_c)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), feat_mp=om.feat_mp, flags=om.mp_flags,
+             rep=om.mp_replaced_by, nobs=om.mp_nobs, tables=tables.numpy(),
+             cand=plan_sum["candidates"], victims=app_c["victims"])
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world", [("T5", 2), ("C1", 2), ("T5", 3)])
+def test_fuse_sharded_gloo_equals_single(tmp_path, name, world):
+    import oracle
+    from lcsynth import make_world
+    from lcsynth.world import FUSE_PARAMS_CHECKS
+    mp.spawn(_worker, args=(world, _free_port(), name, FUSE_PARAMS_CHECKS, str(tmp_path)),
+             nprocs=world, join=True)
+    w = make_world(name, 0)
+    om = oracle.OracleMap(w)
+    if w.win_S is None:
+        om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    ref = om.fuse(w.window, w.mp_list, FUSE_PARAMS_CHECKS, window_S=w.win_S,
+                  win_list_begin=w.win_list_begin)
+    for r in range(world):
+        z = np.load(tmp_path / f"r{r}.npz")
+        assert np.array_equal(z["feat_mp"], om.feat_mp)
+        assert np.array_equal(z["flags"], om.mp_flags)
+        assert np.array_equal(z["rep"], om.mp_replaced_by)
+        assert np.array_equal(z["nobs"], om.mp_nobs)
+        nw = len(ref["winner"])
+        assert np.array_equal(z["tables"][:nw], ref["winner"])
+        assert np.array_equal(z["tables"][nw:], ref["victim"])
+        assert int(z["cand"]) == ref["counts"]["candidates"]
+        assert int(z["victims"]) == ref["counts"]["victims"]
+
+
+def test_shard_bounds_balanced_and_covering():
+    from paper_2603_17201_b200.dist import shard_bounds
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        n = int(rng.integers(1, 300))
+        wb = np.r_[0, np.cumsum(rng.integers(0, 5000, n))]
+        for W in (1, 2, 3, 4, 8):
+            b = shard_bounds(n, W, wb)
+            assert b[0][0] == 0 and b[-1][1] == n
+            assert all(b[i][1] == b[i + 1][0] for i in range(W - 1))
+            loads = [wb[h] - wb[l] for l, h in b]
+            assert max(loads) <= wb[-1] / W + wb[1:].__sub__(wb[:-1]).max() + 1
+    assert shard_bounds(10, 4, None, 7) == [(0, 3), (3, 5), (5, 8), (8, 10)]
