@@ -144,6 +144,7 @@ def _to13(a):
 
 
 def _noise(rng, sigma):
+    """Small Sim3 perturbation, composed on the camera side (rotation about the camera)."""
     return (1.0 + sigma * rng.standard_normal(), _rodrigues(sigma * rng.standard_normal(3)),
             sigma * rng.standard_normal(3))
 
@@ -429,6 +430,13 @@ def make_world(name: str, seed: int = 0) -> World:
     assoc &= ~drop
 
     mp_ref_kf = obs_kf[ref_obs].astype(np.int32)
+    # number map points in creation order (by reference keyframe), as a SLAM system
+    # that triangulates points when keyframes are inserted does
+    order = np.lexsort((mp_lm, mp_ref_kf))
+    inv = np.empty(n_mp, np.int64)
+    inv[order] = np.arange(n_mp)
+    mp_pass, mp_lm, ref_obs, mp_ref_kf = mp_pass[order], mp_lm[order], ref_obs[order], mp_ref_kf[order]
+    obs_mp = np.where(obs_mp >= 0, inv[np.maximum(obs_mp, 0)], -1)
     p_true = lm_pos[mp_lm]
     mp_pos = np.empty((n_mp, 3))
     for i_pass in range(2):
@@ -516,8 +524,8 @@ def make_world(name: str, seed: int = 0) -> World:
         ideal[k] = _compose(kf_est[k], kf_D[k]) if k >= K else kf_est[k]
     cur = n_kf - 1
     w.cur_kf = cur
-    w.S_cw_corr = _to13(_compose(ideal[cur], _noise(rng, 1e-3)))
-    w.S_opt = np.stack([_to13(_compose(ideal[k], _noise(rng, 1e-4))) if k >= K else _to13(kf_est[k])
+    w.S_cw_corr = _to13(_compose(_noise(rng, 1e-3), ideal[cur]))
+    w.S_opt = np.stack([_to13(_compose(_noise(rng, 1e-4), ideal[k])) if k >= K else _to13(kf_est[k])
                         for k in range(n_kf)])
     covis = _covisibility(w) if (cfg.n_window > 0 or cfg.n_hyp > 0) else None
     if cfg.n_window > 0:
@@ -537,7 +545,7 @@ def make_world(name: str, seed: int = 0) -> World:
             begin.append(begin[-1] + len(lst))
         w.win_list_begin = np.asarray(begin, np.int32)
         w.mp_list = np.concatenate(lists).astype(np.int32)
-        w.win_S = np.stack([_to13(_compose(ideal[int(k)], _noise(rng, 1e-3))) for k in w.window])
+        w.win_S = np.stack([_to13(_compose(_noise(rng, 1e-3), ideal[int(k)])) for k in w.window])
 
     if cfg.n_hyp > 0:
         _make_hypotheses(w, rng, covis, kf_est, ideal, K)
@@ -574,7 +582,7 @@ def _make_hypotheses(w: World, rng, covis, kf_est, ideal, K):
     for h in range(H):
         j = int(round((h + 0.5) * K / H)) % K
         cur = K + j
-        S_cw = _compose(ideal[cur], _noise(rng, 1e-3))
+        S_cw = _compose(_noise(rng, 1e-3), ideal[cur])
         loop_kfs = [j] + _top_covisible(covis, j, w.cfg.loop_covis, lambda x: x < K)
         lst = _kf_mps(w, loop_kfs)
         for kk in [cur] + _top_covisible(covis, cur, 3, lambda x: x >= K):

@@ -13,6 +13,8 @@
 // (H << 32) | q, which is the lowest-(H, q) rule of reading A17.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "lc_internal.cuh"
 
 namespace {
@@ -76,40 +78,97 @@ __device__ __forceinline__ int popc_desc(const uint4& a0, const uint4& a1, const
 }
 
 // ---------------------------------------------------------------------------
+// TMA (cp.async.bulk) + mbarrier helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+// compacted survivor of the geometric culls (phase A -> phase B)
+struct __align__(16) QEnt {
+  int32_t q;
+  int32_t j;     // position in mp_list
+  int32_t lvl;   // predicted level
+  int32_t pad;
+  double u, v;
+};
+// ---------------------------------------------------------------------------
 // MODE 0: fuse (already found = associated in the keyframe)
 // MODE 1: projection search (already found = pair_taken; taken features excluded)
+//
+// One CTA per (unit = keyframe/pair, query chunk); warps work independently
+// (no CTA barrier after staging). Staging: one elected thread issues three 1-D
+// TMA bulk copies (cell offsets, keypoints, octave/index words of the keyframe's
+// cell-major block) on an mbarrier while the CTA builds the already-found hash.
+// Phase A (per warp, 64 queries per batch, 2 per lane): list entry -> {flags,
+// first 32-B sector of the 64-B map-point record} -> fp64 SE3 projection, bounds /
+// distance / view-angle culls, level; survivors are ballot-compacted into the
+// warp's shared-memory ring. Phase B (whenever >= 32 survivors are queued): 4-lane
+// groups take one survivor each (8 per warp step) and stride over the cells of
+// each row of its window; per candidate 2 x uint4 descriptor loads + 8 POPC; the
+// group reduces (H << 16 | f) best and the second-best H with shuffles; the
+// proposal is a u64 atomicMin on (H << 32) | q.
 // ---------------------------------------------------------------------------
 template <int MODE>
-__global__ void __launch_bounds__(LC_NTHREADS) k_project_match(const MatchArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+__device__ void resolve_unit(const MatchArgs& a, int unit);
+
+constexpr int QW = 96;            // per-warp survivor ring (>= 31 + 64)
+constexpr int NWARP = LC_NTHREADS / 32;
+
+template <int MODE>
+__global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t s_bar;
   __shared__ double s_T[12];  // R row-major, tt = t / s
   __shared__ double s_Ow[3];
   __shared__ DevCam s_cam;
+  __shared__ int s_next;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int unit = a.blk_unit[blockIdx.x];
   const int k = a.unit_kf[unit];
   const int fb = a.kf_fbeg[k];
   const int F = a.kf_fbeg[k + 1] - fb;
+  const int fp = a.kf_fpad[k];
   const int H = a.hash_size;
   const int hmask = H - 1;
   const int hshift = 32 - __ffs(H) + 1;
-  float2* s_uv = (float2*)smem;
-  uint32_t* s_meta = (uint32_t*)(s_uv + F);
-  int32_t* s_hash = (int32_t*)(s_meta + F);
-  uint16_t* s_cell = (uint16_t*)(s_hash + H);
-  const int G1 = a.G + 1;
+  uint16_t* s_cell = (uint16_t*)smem;
+  float2* s_uv = (float2*)(smem + a.off_uv);
+  uint32_t* s_meta = (uint32_t*)(smem + a.off_meta);
+  int32_t* s_hash = (int32_t*)(smem + a.off_hash);
+  QEnt* s_q = (QEnt*)(smem + a.off_queue) + warp * QW;
   const int64_t toff = (MODE == 1 && a.taken) ? a.unit_toff[unit] : 0;
 
-  // ---- stage the keyframe ------------------------------------------------------
-  for (int i = threadIdx.x; i < H; i += blockDim.x) s_hash[i] = -1;
-  const uint16_t* gcell = a.kf_cell + (size_t)k * G1;
-  for (int i = threadIdx.x; i < G1; i += blockDim.x) s_cell[i] = gcell[i];
-  for (int p = threadIdx.x; p < F; p += blockDim.x) {
-    s_uv[p] = a.fc_uv[fb + p];
-    uint32_t m = a.fc_meta[fb + p];
-    if (MODE == 1 && a.taken && a.taken[toff + (m & 0xFFFFu)] >= 0) m |= 0x80000000u;
-    s_meta[p] = m;
-  }
-  if (threadIdx.x == 0) {
+  // ---- stage the keyframe (TMA) + already-found hash ---------------------------
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
     double S[13], T[13];
     const double* src = a.unit_S ? a.unit_S + 13 * (size_t)unit : a.kf_S_corr + 13 * (size_t)k;
     for (int i = 0; i < 13; ++i) S[i] = src[i];
@@ -117,18 +176,38 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_project_match(const MatchArgs a
     for (int i = 0; i < 12; ++i) s_T[i] = T[i];
     for (int i = 0; i < 3; ++i) s_Ow[i] = -lc_col3(T, i, T + 9);
     s_cam = a.cams[a.kf_cam[k]];
+    s_next = 0;
   }
+  for (int i = tid; i < H; i += LC_NTHREADS) s_hash[i] = -1;
   __syncthreads();
-  for (int f = threadIdx.x; f < F; f += blockDim.x) {
+  if (tid == 0) {
+    const uint32_t b_cell = (uint32_t)a.Gs * 2u;
+    const uint32_t b_uv = (uint32_t)((F + 1) & ~1) * 8u;
+    const uint32_t b_meta = (uint32_t)((F + 3) & ~3) * 4u;
+    mbar_expect_tx(&s_bar, b_cell + (F > 0 ? b_uv + b_meta : 0u));
+    tma_load_1d(s_cell, a.kf_cell + (size_t)k * a.Gs, b_cell, &s_bar);
+    if (F > 0) {
+      tma_load_1d(s_uv, a.fc_uv + fp, b_uv, &s_bar);
+      tma_load_1d(s_meta, a.fc_meta + fp, b_meta, &s_bar);
+    }
+  }
+  for (int f = tid; f < F; f += LC_NTHREADS) {
     int32_t m = (MODE == 0) ? a.feat_mp[fb + f] : (a.taken ? a.taken[toff + f] : -1);
     if (m >= 0) hash_insert(s_hash, hmask, hshift, m);
+  }
+  if (a.sole) {  // this CTA owns the unit's winner words: initialise them here
+    unsigned long long* w0 = a.winner + a.unit_woff[unit];
+    for (int f = tid; f < F; f += LC_NTHREADS) w0[f] = NONE;
+  }
+  if (MODE == 1 && a.taken) {  // taken features are not candidates (reading A19)
+    mbar_wait(&s_bar, 0);
+    __syncthreads();
+    for (int p = tid; p < F; p += LC_NTHREADS)
+      if (a.taken[toff + (s_meta[p] & 0xFFFFu)] >= 0) s_meta[p] |= 0x80000000u;
   }
   __syncthreads();
 
   const lc_match_params prm = a.params[(MODE == 1 && a.unit_param) ? a.unit_param[unit] : 0];
-  const double R0 = s_T[0], R1 = s_T[1], R2 = s_T[2], R3 = s_T[3], R4 = s_T[4], R5 = s_T[5];
-  const double R6 = s_T[6], R7 = s_T[7], R8 = s_T[8], t0 = s_T[9], t1 = s_T[10], t2 = s_T[11];
-  const double Ow0 = s_Ow[0], Ow1 = s_Ow[1], Ow2 = s_Ow[2];
   const int L = a.n_levels;
   const double sLm1 = a.scale[L - 1];
   const int cols = a.cols, rows = a.rows;
@@ -138,100 +217,185 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_project_match(const MatchArgs a
   uint32_t cnt[M_N];
 #pragma unroll
   for (int i = 0; i < M_N; ++i) cnt[i] = 0;
+  int head = 0, tail = 0;  // warp-uniform ring indices (monotone; slot = idx % QW)
+  bool staged = (MODE == 1 && a.taken);
 
-  const int64_t q1 = a.blk_q1[blockIdx.x];
-  for (int64_t j = a.blk_q0[blockIdx.x] + threadIdx.x; j < q1; j += blockDim.x) {
-    const int32_t q = a.mp_list[j];
-    const int64_t qi = qoff + (j - lbeg);
-    cnt[M_QUERIES]++;
+  // ---- phase A: one query per call; true if it survived (entry written by caller)
+  auto phase_a = [&](int32_t q, int64_t j, bool in_range, uint8_t flag, uint4 r0, uint4 r1,
+                     QEnt& ent) -> bool {
     int status = 0;
     double u = 0.0, v = 0.0;
-    int ncand = 0;
-    uint32_t best = 0xFFFFFFFFu;  // (H << 16) | f
-    int second = 256;
     do {
-      if ((unsigned)q >= (unsigned)a.n_mp || (a.mp_flags[q] & 1u)) {  // out of range: as bad
-        status = LC_Q_BAD; cnt[M_BAD]++; break;
-      }
+      if (!in_range || (flag & 1u)) { status = LC_Q_BAD; cnt[M_BAD]++; break; }
       if (hash_contains(s_hash, hmask, hshift, q)) { status = LC_Q_FOUND; cnt[M_FOUND]++; break; }
-      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + q);
-      const uint4 w0 = __ldg(rp + 0), w1 = __ldg(rp + 1);
-      const double p0 = __uint_as_float(w0.x), p1 = __uint_as_float(w0.y), p2 = __uint_as_float(w0.z);
-      const double dmax = __uint_as_float(w0.w);
-      const double n0 = __uint_as_float(w1.x), n1 = __uint_as_float(w1.y), n2 = __uint_as_float(w1.z);
-      const double x = (R0 * p0 + R1 * p1) + R2 * p2 + t0;
-      const double y = (R3 * p0 + R4 * p1) + R5 * p2 + t1;
-      const double z = (R6 * p0 + R7 * p1) + R8 * p2 + t2;
+      const double p0 = __uint_as_float(r0.x), p1 = __uint_as_float(r0.y), p2 = __uint_as_float(r0.z);
+      const double z = (s_T[6] * p0 + s_T[7] * p1) + s_T[8] * p2 + s_T[11];
       if (z <= 0.0) { status = LC_Q_DEPTH; cnt[M_DEPTH]++; break; }
+      const double x = (s_T[0] * p0 + s_T[1] * p1) + s_T[2] * p2 + s_T[9];
+      const double y = (s_T[3] * p0 + s_T[4] * p1) + s_T[5] * p2 + s_T[10];
       lc_project(s_cam, x, y, z, u, v);
       if (!(u >= s_cam.min_x && u < s_cam.max_x && v >= s_cam.min_y && v < s_cam.max_y)) {
         status = LC_Q_BOUNDS; cnt[M_BOUNDS]++; break;
       }
-      const double PO0 = p0 - Ow0, PO1 = p1 - Ow1, PO2 = p2 - Ow2;
+      const double PO0 = p0 - s_Ow[0], PO1 = p1 - s_Ow[1], PO2 = p2 - s_Ow[2];
       const double d = sqrt((PO0 * PO0 + PO1 * PO1) + PO2 * PO2);
-      const double dmin_i = 0.8 * (dmax / sLm1);
-      const double dmax_i = 1.2 * dmax;
-      if (d < dmin_i || d > dmax_i) { status = LC_Q_DIST; cnt[M_DIST]++; break; }
+      const double dmax = __uint_as_float(r0.w);
+      if (d > 1.2 * dmax || d < 0.8 * (dmax / sLm1)) { status = LC_Q_DIST; cnt[M_DIST]++; break; }
+      const double n0 = __uint_as_float(r1.x), n1 = __uint_as_float(r1.y), n2 = __uint_as_float(r1.z);
       if ((PO0 * n0 + PO1 * n1) + PO2 * n2 < 0.5 * d) { status = LC_Q_ANGLE; cnt[M_ANGLE]++; break; }
       int lvl = L - 1;
       for (int n = 0; n < L; ++n)
         if (d * a.scale[n] >= dmax) { lvl = n; break; }
-      const double r = (double)prm.th * a.scale[lvl];
-      // candidate cells: conservative (1e-6 cell) superset of the exact square window
-      int cx0 = (int)fmax(0.0, floor(((u - r) - s_cam.min_x) * s_cam.cell_sx - 1e-6));
-      int cx1 = (int)fmin((double)(cols - 1), floor(((u + r) - s_cam.min_x) * s_cam.cell_sx + 1e-6));
-      int cy0 = (int)fmax(0.0, floor(((v - r) - s_cam.min_y) * s_cam.cell_sy - 1e-6));
-      int cy1 = (int)fmin((double)(rows - 1), floor(((v + r) - s_cam.min_y) * s_cam.cell_sy + 1e-6));
-      const uint4 d0 = __ldg(rp + 2), d1 = __ldg(rp + 3);
-      const int lo = lvl - 1;
-      for (int cy = cy0; cy <= cy1; ++cy) {
-        const int pb = s_cell[cy * cols + cx0], pe = s_cell[cy * cols + cx1 + 1];
-        for (int p = pb; p < pe; ++p) {
-          const uint32_t meta = s_meta[p];
-          const int oct = (int)((meta >> 16) & 0xFFu);
-          if (oct < lo || oct > lvl) continue;
-          if (MODE == 1 && (meta & 0x80000000u)) continue;
-          const float2 fuv = s_uv[p];
-          const double du = fabs((double)fuv.x - u), dv = fabs((double)fuv.y - v);
-          if (!(du < r && dv < r)) continue;
-          ++ncand;
-          const uint4* dp = a.fc_desc + 2 * (size_t)(fb + p);
-          const int h = popc_desc(d0, d1, __ldg(dp), __ldg(dp + 1));
-          const uint32_t key = ((uint32_t)h << 16) | (meta & 0xFFFFu);
-          if (key < best) {
-            if (best != 0xFFFFFFFFu) second = min(second, (int)(best >> 16));
-            best = key;
-          } else {
-            second = min(second, h);
+      ent.q = q; ent.j = (int32_t)j; ent.lvl = lvl; ent.pad = 0; ent.u = u; ent.v = v;
+      return true;
+    } while (0);
+    const int64_t qi = qoff + (j - lbeg);
+    if (a.dbg_best) a.dbg_best[qi] = status;
+    if (a.dbg_uv) { a.dbg_uv[2 * qi] = u; a.dbg_uv[2 * qi + 1] = v; }
+    if (a.dbg_ncand) a.dbg_ncand[qi] = 0;
+    return false;
+  };
+
+  auto enqueue = [&](bool surv, const QEnt& ent) {
+    const unsigned m = __ballot_sync(0xffffffffu, surv);
+    if (surv) s_q[(tail + __popc(m & ((1u << lane) - 1u))) % QW] = ent;
+    tail += __popc(m);
+  };
+
+  // ---- phase B: 4-lane groups, one survivor per group, 8 per warp step --------
+  auto phase_b = [&](int navail) {
+    const int g = lane >> 2, t = lane & 3;
+    for (int s = 0; s < navail; s += 8) {
+      const bool act = s + g < navail;
+      QEnt e;
+      if (act) e = s_q[(head + s + g) % QW];
+      int ncand = 0;
+      uint32_t best = 0xFFFFFFFFu;  // (H << 16) | f
+      int second = 256;
+      if (act) {
+        const double u = e.u, v = e.v;
+        const int lvl = e.lvl;
+        const double r = (double)prm.th * a.scale[lvl];
+        const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + e.q);
+        const uint4 d0 = __ldg(rp + 2), d1 = __ldg(rp + 3);
+        const int cx0 = (int)fmax(0.0, floor(((u - r) - s_cam.min_x) * s_cam.cell_sx - 1e-6));
+        const int cx1 = (int)fmin((double)(cols - 1), floor(((u + r) - s_cam.min_x) * s_cam.cell_sx + 1e-6));
+        const int cy0 = (int)fmax(0.0, floor(((v - r) - s_cam.min_y) * s_cam.cell_sy - 1e-6));
+        const int cy1 = (int)fmin((double)(rows - 1), floor(((v + r) - s_cam.min_y) * s_cam.cell_sy + 1e-6));
+        const int lo = lvl - 1;
+        for (int cy = cy0; cy <= cy1; ++cy) {
+          const int pe = s_cell[cy * cols + cx1 + 1];
+          for (int p = s_cell[cy * cols + cx0] + t; p < pe; p += 4) {
+            const uint32_t meta = s_meta[p];
+            const int oct = (int)((meta >> 16) & 0xFFu);
+            if (oct < lo || oct > lvl) continue;
+            if (MODE == 1 && (meta & 0x80000000u)) continue;
+            const float2 fuv = s_uv[p];
+            const double du = fabs((double)fuv.x - u), dv = fabs((double)fuv.y - v);
+            if (!(du < r && dv < r)) continue;
+            ++ncand;
+            const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
+            const int h = popc_desc(d0, d1, __ldg(dp), __ldg(dp + 1));
+            const uint32_t key = ((uint32_t)h << 16) | (meta & 0xFFFFu);
+            if (key < best) {
+              if (best != 0xFFFFFFFFu) second = min(second, (int)(best >> 16));
+              best = key;
+            } else {
+              second = min(second, h);
+            }
           }
         }
       }
-      cnt[M_CAND] += ncand;
-      if (ncand == 0) { cnt[M_NOCAND]++; break; }
-      const int hb = (int)(best >> 16);
-      if (hb > prm.max_hamming) { cnt[M_OVERTH]++; break; }
-      if (prm.ratio_den > 0 &&
-          (long long)prm.ratio_den * hb > (long long)prm.ratio_num * second) {
-        cnt[M_RATIO]++; break;
+      // group reduction: best key, second H (exact: keys are unique per feature)
+      uint32_t gbest = best;
+      gbest = min(gbest, __shfl_xor_sync(0xffffffffu, gbest, 1, 4));
+      gbest = min(gbest, __shfl_xor_sync(0xffffffffu, gbest, 2, 4));
+      int sec = second;
+      if (best != gbest && best != 0xFFFFFFFFu) sec = min(sec, (int)(best >> 16));
+      sec = min(sec, __shfl_xor_sync(0xffffffffu, sec, 1, 4));
+      sec = min(sec, __shfl_xor_sync(0xffffffffu, sec, 2, 4));
+      ncand += __shfl_xor_sync(0xffffffffu, ncand, 1, 4);
+      ncand += __shfl_xor_sync(0xffffffffu, ncand, 2, 4);
+      if (act && t == 0) {
+        cnt[M_CAND] += ncand;
+        do {
+          if (ncand == 0) { cnt[M_NOCAND]++; break; }
+          const int hb = (int)(gbest >> 16);
+          if (hb > prm.max_hamming) { cnt[M_OVERTH]++; break; }
+          if (prm.ratio_den > 0 && (long long)prm.ratio_den * hb > (long long)prm.ratio_num * sec) {
+            cnt[M_RATIO]++; break;
+          }
+          cnt[M_PROP]++;
+          atomicMin(&win[gbest & 0xFFFFu], ((unsigned long long)hb << 32) | (unsigned int)e.q);
+        } while (0);
+        const int64_t qi = qoff + ((int64_t)e.j - lbeg);
+        if (a.dbg_best) {
+          long long val;
+          if (ncand == 0) val = (256LL << 48) | (256LL << 32) | 0xFFFFFFFFLL;
+          else val = ((long long)(gbest >> 16) << 48) | ((long long)sec << 32) | (long long)(gbest & 0xFFFFu);
+          a.dbg_best[qi] = val;
+        }
+        if (a.dbg_uv) { a.dbg_uv[2 * qi] = e.u; a.dbg_uv[2 * qi + 1] = e.v; }
+        if (a.dbg_ncand) a.dbg_ncand[qi] = ncand;
       }
-      cnt[M_PROP]++;
-      atomicMin(&win[best & 0xFFFFu], ((unsigned long long)hb << 32) | (unsigned int)q);
-    } while (0);
-    if (a.dbg_best) {
-      long long val;
-      if (status < 0) val = status;
-      else if (ncand == 0) val = (256LL << 48) | (256LL << 32) | 0xFFFFFFFFLL;
-      else val = ((long long)(best >> 16) << 48) | ((long long)second << 32) | (long long)(best & 0xFFFFu);
-      a.dbg_best[qi] = val;
     }
-    if (a.dbg_uv) { a.dbg_uv[2 * qi] = u; a.dbg_uv[2 * qi + 1] = v; }
-    if (a.dbg_ncand) a.dbg_ncand[qi] = ncand;
+    head += navail;
+  };
+
+  const int64_t q0 = a.blk_q0[blockIdx.x], q1 = a.blk_q1[blockIdx.x];
+  while (true) {
+    int bidx = 0;
+    if (lane == 0) bidx = atomicAdd(&s_next, 1);
+    bidx = __shfl_sync(0xffffffffu, bidx, 0);
+    const int64_t base = q0 + (int64_t)bidx * 64;
+    if (base >= q1) break;
+    const int64_t ja = base + lane, jb = base + 32 + lane;
+    const bool va = ja < q1, vb = jb < q1;
+    const int32_t qa = va ? a.mp_list[ja] : -1;
+    const int32_t qb = vb ? a.mp_list[jb] : -1;
+    const bool ia = va && (unsigned)qa < (unsigned)a.n_mp;
+    const bool ib = vb && (unsigned)qb < (unsigned)a.n_mp;
+    uint4 ra0 = make_uint4(0, 0, 0, 0), ra1 = ra0, rb0 = ra0, rb1 = ra0;
+    uint8_t fla = 1, flb = 1;
+    if (ia) {
+      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + qa);
+      ra0 = __ldg(rp); ra1 = __ldg(rp + 1); fla = __ldg(a.mp_flags + qa);
+    }
+    if (ib) {
+      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + qb);
+      rb0 = __ldg(rp); rb1 = __ldg(rp + 1); flb = __ldg(a.mp_flags + qb);
+    }
+    QEnt ea, eb;
+    bool sa = false, sb = false;
+    if (va) { cnt[M_QUERIES]++; sa = phase_a(qa, ja, ia, fla, ra0, ra1, ea); }
+    enqueue(sa, ea);
+    if (vb) { cnt[M_QUERIES]++; sb = phase_a(qb, jb, ib, flb, rb0, rb1, eb); }
+    enqueue(sb, eb);
+    __syncwarp();
+    while (tail - head >= 32) {  // keeps the ring below 32 + 64 <= QW entries
+      if (!staged) { mbar_wait(&s_bar, 0); staged = true; }
+      phase_b(32);
+      __syncwarp();
+    }
   }
+  if (tail > head) {
+    if (!staged) { mbar_wait(&s_bar, 0); staged = true; }
+    phase_b(tail - head);
+  }
+  if (!staged) mbar_wait(&s_bar, 0);  // never leave the CTA with a bulk copy in flight
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
   block_add<M_N>(cnt, kMatchSlot, cdst);
+  if (a.sole) {  // all proposals of this unit are in: resolve it here (no extra launch)
+    __syncthreads();
+    resolve_unit<MODE>(a, unit);
+  }
 }
 
-// Orientation filter + fuse actions (MODE 0) / output tables (MODE 1); one CTA per unit.
+// ---------------------------------------------------------------------------
+// Per-unit resolve: orientation filter (reading A15) + fuse actions (MODE 0,
+// readings O9.1, A20, A21) or output tables (MODE 1). Called by the whole CTA,
+// either as the tail of a sole (one-CTA-per-unit) match CTA or by k_resolve.
+// ---------------------------------------------------------------------------
 enum { R_WINNERS, R_ORIENT, R_ADD, R_VICTIM, R_LOOP, R_BADSLOT, R_N };
 __device__ __constant__ int kResolveSlot[R_N] = {LC_COUNT_WINNERS, LC_COUNT_ORIENT_REJ,
                                                  LC_COUNT_ADD, LC_COUNT_VICTIM_PROP,
@@ -246,24 +410,15 @@ __device__ __forceinline__ int rot_bin(float fa, float qa) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(LC_NTHREADS) k_resolve(
-    const int32_t* __restrict__ unit_kf, const int64_t* __restrict__ unit_woff,
-    const int64_t* __restrict__ unit_toff, const int32_t* __restrict__ unit_param,
-    const lc_match_params* __restrict__ params, const int32_t* __restrict__ kf_fbeg,
-    const int32_t* __restrict__ feat_mp, const float* __restrict__ feat_angle,
-    const MpRec* __restrict__ mp_rec, const uint8_t* __restrict__ mp_flags,
-    const uint32_t* __restrict__ loop_ep, uint32_t epoch, const int32_t* __restrict__ taken,
-    unsigned long long* __restrict__ winner, unsigned long long* __restrict__ victim,
-    int8_t* __restrict__ action, int32_t* __restrict__ out_mp, int32_t* __restrict__ out_dist,
-    unsigned long long* __restrict__ counts) {
+__device__ void resolve_unit(const MatchArgs& a, int unit) {
   __shared__ int s_hist[30];
   __shared__ int s_keep[3];
-  const int unit = blockIdx.x;
-  const int k = unit_kf[unit];
-  const int fb = kf_fbeg[k], F = kf_fbeg[k + 1] - fb;
-  const int64_t woff = unit_woff[unit];
-  const int64_t toff = (MODE == 1 && taken) ? unit_toff[unit] : 0;
-  const lc_match_params prm = params[(MODE == 1 && unit_param) ? unit_param[unit] : 0];
+  const int k = a.unit_kf[unit];
+  const int fb = a.kf_fbeg[k], F = a.kf_fbeg[k + 1] - fb;
+  const int64_t woff = a.unit_woff[unit];
+  const int64_t toff = (MODE == 1 && a.taken) ? a.unit_toff[unit] : 0;
+  const lc_match_params prm = a.params[(MODE == 1 && a.unit_param) ? a.unit_param[unit] : 0];
+  unsigned long long* winner = a.winner;
   uint32_t cnt[R_N];
 #pragma unroll
   for (int i = 0; i < R_N; ++i) cnt[i] = 0;
@@ -274,7 +429,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_resolve(
       unsigned long long w = winner[woff + f];
       if (w == NONE) continue;
       int q = (int)(w & 0xFFFFFFFFull);
-      atomicAdd(&s_hist[rot_bin(feat_angle[fb + f], mp_rec[q].angle)], 1);
+      atomicAdd(&s_hist[rot_bin(a.feat_angle[fb + f], a.mp_rec[q].angle)], 1);
     }
     __syncthreads();
     if (threadIdx.x == 0) {  // ComputeThreeMaxima (EXT), reading A15
@@ -298,7 +453,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_resolve(
       cnt[R_WINNERS]++;
       int q = (int)(w & 0xFFFFFFFFull);
       if (prm.check_orientation) {
-        int b = rot_bin(feat_angle[fb + f], mp_rec[q].angle);
+        int b = rot_bin(a.feat_angle[fb + f], a.mp_rec[q].angle);
         if (b != s_keep[0] && b != s_keep[1] && b != s_keep[2]) {
           w = NONE;
           winner[woff + f] = NONE;
@@ -307,109 +462,151 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_resolve(
         }
       }
       if (MODE == 0 && w != NONE) {
-        int slot = feat_mp[fb + f];
+        int slot = a.feat_mp[fb + f];
         if (slot < 0) { act = 1; cnt[R_ADD]++; }
-        else if (mp_flags[slot] & 1u) { act = 5; cnt[R_BADSLOT]++; }
-        else if (loop_ep[slot] == epoch) { act = 3; cnt[R_LOOP]++; }
-        else { act = 2; cnt[R_VICTIM]++; atomicMin(&victim[slot], w); }
+        else if (a.mp_flags[slot] & 1u) { act = 5; cnt[R_BADSLOT]++; }
+        else if (a.loop_ep[slot] == a.epoch) { act = 3; cnt[R_LOOP]++; }
+        else { act = 2; cnt[R_VICTIM]++; atomicMin(&a.victim[slot], w); }
       }
     }
     if (MODE == 0) {
-      if (action) action[woff + f] = act;
+      if (a.action) a.action[woff + f] = act;
     } else {
-      int t = taken ? taken[toff + f] : -1;
-      if (t >= 0) { out_mp[woff + f] = t; out_dist[woff + f] = -1; }
-      else if (w != NONE) { out_mp[woff + f] = (int)(w & 0xFFFFFFFFull); out_dist[woff + f] = (int)(w >> 32); }
-      else { out_mp[woff + f] = -1; out_dist[woff + f] = -1; }
+      int t = a.taken ? a.taken[toff + f] : -1;
+      if (t >= 0) { a.out_mp[woff + f] = t; a.out_dist[woff + f] = -1; }
+      else if (w != NONE) { a.out_mp[woff + f] = (int)(w & 0xFFFFFFFFull); a.out_dist[woff + f] = (int)(w >> 32); }
+      else { a.out_mp[woff + f] = -1; a.out_dist[woff + f] = -1; }
     }
   }
-  unsigned long long* cdst = counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
+  unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
   block_add<R_N>(cnt, kResolveSlot, cdst);
 }
 
+template <int MODE>
+__global__ void __launch_bounds__(LC_NTHREADS) k_resolve(const MatchArgs a) {
+  resolve_unit<MODE>(a, a.unit_base + blockIdx.x);
+}
+
 // Per-call setup: LoopSet stamps, winner/victim init, window membership.
-__global__ void k_fuse_prep(int phase, uint32_t epoch, int n_w, const int32_t* __restrict__ window,
-                            int64_t n_wfeat, const int32_t* __restrict__ mp_list, int64_t n_list,
-                            int n_mp, unsigned long long* __restrict__ winner,
+__global__ void k_fuse_prep(int phase, int init_winner, uint32_t epoch, int n_w,
+                            const int32_t* __restrict__ window, int64_t n_wfeat,
+                            const int32_t* __restrict__ mp_list, int64_t n_list, int n_mp,
+                            unsigned long long* __restrict__ winner,
                             unsigned long long* __restrict__ victim, uint32_t* __restrict__ loop_ep,
-                            uint32_t* __restrict__ kf_win_ep, int32_t* __restrict__ kf_win_pos) {
+                            uint32_t* __restrict__ kf_win_ep, int32_t* __restrict__ kf_win_pos,
+                            uint32_t* __restrict__ vbits, int n_vbits, int32_t* __restrict__ dirty_n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (int64_t i = t0; i < n_w; i += stride) {
     kf_win_ep[window[i]] = epoch;
     kf_win_pos[window[i]] = (int32_t)i;
   }
+  for (int64_t i = t0; i < n_vbits; i += stride) vbits[i] = 0u;
+  if (t0 == 0) *dirty_n = 0;
   if (!(phase & LC_FUSE_PLAN)) return;
   for (int64_t i = t0; i < n_list; i += stride) {
     const int32_t q = mp_list[i];
     if ((unsigned)q < (unsigned)n_mp) loop_ep[q] = epoch;
   }
-  for (int64_t i = t0; i < n_wfeat; i += stride) winner[i] = NONE;
+  if (init_winner)
+    for (int64_t i = t0; i < n_wfeat; i += stride) winner[i] = NONE;
   for (int64_t i = t0; i < n_mp; i += stride) victim[i] = NONE;
 }
 
-// Victim marking: flags |= bad, replaced_by = survivor (reading O9 (iv)).
+// Victim marking: flags |= bad, replaced_by = survivor (reading O9 (iv)), victim bitmap.
 __global__ void k_fuse_victims(int n_mp, const unsigned long long* __restrict__ victim,
                                uint8_t* __restrict__ flags, int32_t* __restrict__ replaced_by,
-                               unsigned long long* __restrict__ counts) {
+                               uint32_t* __restrict__ vbits, unsigned long long* __restrict__ counts) {
   uint32_t n = 0;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_mp; q += gridDim.x * blockDim.x) {
-    unsigned long long v = victim[q];
-    if (v == NONE) continue;
-    flags[q] |= 1u;
-    replaced_by[q] = (int32_t)(v & 0xFFFFFFFFull);
-    ++n;
+  const int stride = gridDim.x * blockDim.x;
+  for (int q0 = blockIdx.x * blockDim.x; q0 < n_mp; q0 += stride) {
+    const int q = q0 + threadIdx.x;
+    bool isv = false;
+    if (q < n_mp) {
+      unsigned long long v = victim[q];
+      if (v != NONE) {
+        isv = true;
+        flags[q] |= 1u;
+        replaced_by[q] = (int32_t)(v & 0xFFFFFFFFull);
+        ++n;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, isv);   // q0 is a multiple of 32
+    if ((threadIdx.x & 31) == 0 && m) vbits[(q0 + threadIdx.x) >> 5] = m;
   }
   const int slot[1] = {LC_COUNT_VICTIMS};
   uint32_t loc[1] = {n};
   block_add<1>(loc, slot, counts);
 }
 
-// Apply: redirect victims map-wide, add winners to empty window slots, per-keyframe
-// duplicate cleanup by least (priority, f), n_obs deltas. One CTA per keyframe.
-enum { A_REWIRED, A_DUP, A_ADDED, A_N };
-__device__ __constant__ int kApplySlot[A_N] = {LC_COUNT_REWIRED, LC_COUNT_DUP_CLEARED,
-                                               LC_COUNT_ADDED};
-
-__global__ void __launch_bounds__(LC_NTHREADS) k_fuse_apply(
+// Apply pass 1: find the keyframes whose slots change (a victim to redirect or a
+// winner on an empty window slot) -> compact list.
+__global__ void __launch_bounds__(LC_NTHREADS) k_apply_mark(
     uint32_t epoch, const int32_t* __restrict__ kf_fbeg, const uint32_t* __restrict__ kf_win_ep,
     const int32_t* __restrict__ kf_win_pos, const int64_t* __restrict__ woff_of_pos,
-    const unsigned long long* __restrict__ winner, const unsigned long long* __restrict__ victim,
-    int32_t* __restrict__ feat_mp, int32_t* __restrict__ nobs, int hash_size,
-    unsigned long long* __restrict__ counts) {
-  extern __shared__ __align__(16) unsigned char smem[];
+    const unsigned long long* __restrict__ winner, const uint32_t* __restrict__ vbits,
+    const int32_t* __restrict__ feat_mp, int32_t* __restrict__ dirty_list) {
   const int k = blockIdx.x;
   const int fb = kf_fbeg[k], F = kf_fbeg[k + 1] - fb;
   const int wpos = (kf_win_ep[k] == epoch) ? kf_win_pos[k] : -1;
   const int64_t woff = wpos >= 0 ? woff_of_pos[wpos] : 0;
-  int32_t* s_new = (int32_t*)smem;
-  int32_t* s_old = s_new + F;
-  int32_t* s_key = s_old + F;
-  uint32_t* s_val = (uint32_t*)(s_key + hash_size);
-  uint8_t* s_pr = (uint8_t*)(s_val + hash_size);
-  uint32_t cnt[A_N] = {0, 0, 0};
-  int any = 0;
+  int dirty = 0;
   for (int f = threadIdx.x; f < F; f += blockDim.x) {
-    int32_t m = feat_mp[fb + f];
-    int32_t nv = m;
-    uint8_t pr = 0;
-    if (m >= 0) {
-      unsigned long long vw = victim[m];
-      if (vw != NONE) { nv = (int32_t)(vw & 0xFFFFFFFFull); pr = 2; cnt[A_REWIRED]++; }
-    } else if (wpos >= 0) {
-      unsigned long long w = winner[woff + f];
-      if (w != NONE) { nv = (int32_t)(w & 0xFFFFFFFFull); pr = 1; }
-    }
-    s_old[f] = m;
-    s_new[f] = nv;
-    s_pr[f] = pr;
-    any |= (pr != 0);
+    const int32_t m = feat_mp[fb + f];
+    if (m >= 0) dirty |= (vbits[m >> 5] >> (m & 31)) & 1u;
+    else if (wpos >= 0) dirty |= winner[woff + f] != NONE;
   }
-  any = __syncthreads_or(any);
-  if (any) {
+  if (__syncthreads_or(dirty) && threadIdx.x == 0) {
+    const int i = atomicAdd(&dirty_list[0], 1);
+    dirty_list[1 + i] = k;
+  }
+}
+
+// Apply pass 2 (dirty keyframes only): redirect victims, add winners to empty window
+// slots, per-keyframe duplicate cleanup by least (priority, f) (reading A22), n_obs deltas.
+enum { A_REWIRED, A_DUP, A_ADDED, A_N };
+__device__ __constant__ int kApplySlot[A_N] = {LC_COUNT_REWIRED, LC_COUNT_DUP_CLEARED,
+                                               LC_COUNT_ADDED};
+
+__global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
+    uint32_t epoch, const int32_t* __restrict__ kf_fbeg, const uint32_t* __restrict__ kf_win_ep,
+    const int32_t* __restrict__ kf_win_pos, const int64_t* __restrict__ woff_of_pos,
+    const unsigned long long* __restrict__ winner, const unsigned long long* __restrict__ victim,
+    const uint32_t* __restrict__ vbits, const int32_t* __restrict__ dirty_list,
+    int32_t* __restrict__ feat_mp, int32_t* __restrict__ nobs, int hash_size,
+    unsigned long long* __restrict__ counts) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t cnt[A_N] = {0, 0, 0};
+  const int nd = dirty_list[0];
+  for (int di = blockIdx.x; di < nd; di += gridDim.x) {
+    const int k = dirty_list[1 + di];
+    const int fb = kf_fbeg[k], F = kf_fbeg[k + 1] - fb;
+    const int wpos = (kf_win_ep[k] == epoch) ? kf_win_pos[k] : -1;
+    const int64_t woff = wpos >= 0 ? woff_of_pos[wpos] : 0;
+    int32_t* s_new = (int32_t*)smem;
+    int32_t* s_old = s_new + F;
+    int32_t* s_key = s_old + F;
+    uint32_t* s_val = (uint32_t*)(s_key + hash_size);
+    uint8_t* s_pr = (uint8_t*)(s_val + hash_size);
     const int hmask = hash_size - 1;
     const int hshift = 32 - __ffs(hash_size) + 1;
     for (int i = threadIdx.x; i < hash_size; i += blockDim.x) { s_key[i] = -1; s_val[i] = 0xFFFFFFFFu; }
+    for (int f = threadIdx.x; f < F; f += blockDim.x) {
+      int32_t m = feat_mp[fb + f];
+      int32_t nv = m;
+      uint8_t pr = 0;
+      if (m >= 0) {
+        if ((vbits[m >> 5] >> (m & 31)) & 1u) {
+          nv = (int32_t)(victim[m] & 0xFFFFFFFFull); pr = 2; cnt[A_REWIRED]++;
+        }
+      } else if (wpos >= 0) {
+        unsigned long long w = winner[woff + f];
+        if (w != NONE) { nv = (int32_t)(w & 0xFFFFFFFFull); pr = 1; }
+      }
+      s_old[f] = m;
+      s_new[f] = nv;
+      s_pr[f] = pr;
+    }
     __syncthreads();
     for (int f = threadIdx.x; f < F; f += blockDim.x) {
       int32_t nv = s_new[f];
@@ -438,6 +635,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_fuse_apply(
         if (nv >= 0) atomicAdd(&nobs[nv], 1);
       }
     }
+    __syncthreads();
   }
   block_add<A_N>(cnt, kApplySlot, counts);
 }
@@ -461,9 +659,19 @@ cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a_in, int n_block
                          cudaStream_t s) {
   if (n_blocks <= 0) return cudaSuccess;
   MatchArgs a = a_in;
-  a.hash_size = pow2_at_least(2 * (F_max > 0 ? F_max : 1));
-  size_t smem = (size_t)F_max * 12 + (size_t)a.hash_size * 4 + (size_t)(a.G + 1) * 2;
-  smem = (smem + 15) & ~(size_t)15;
+  const int Fm = F_max > 0 ? F_max : 1;
+  a.hash_size = pow2_at_least(2 * Fm);
+  auto r16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+  size_t off = r16((size_t)a.Gs * 2);
+  a.off_uv = (int)off;
+  off += r16((size_t)((Fm + 1) & ~1) * 8);
+  a.off_meta = (int)off;
+  off += r16((size_t)((Fm + 3) & ~3) * 4);
+  a.off_hash = (int)off;
+  off += r16((size_t)a.hash_size * 4);
+  a.off_queue = (int)off;
+  off += (size_t)NWARP * QW * sizeof(QEnt);
+  const size_t smem = off;
   cudaError_t e;
   if (mode == 0) {
     e = cudaFuncSetAttribute(k_project_match<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -478,44 +686,29 @@ cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a_in, int n_block
   return cudaGetLastError();
 }
 
-cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int n_w, const int32_t* d_window,
-                             const int64_t* d_woff, int64_t n_wfeat, const int32_t* mp_list,
-                             int64_t n_list_total, unsigned long long* winner,
-                             unsigned long long* victim, cudaStream_t s) {
-  (void)d_woff;
-  int64_t n = n_w;
-  if (phase & LC_FUSE_PLAN) {
-    n = n > n_list_total ? n : n_list_total;
-    n = n > n_wfeat ? n : n_wfeat;
-    n = n > c->st.n_mp ? n : c->st.n_mp;
-  }
-  k_fuse_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(phase, c->epoch, n_w, d_window, n_wfeat, mp_list,
-                                                 n_list_total, c->st.n_mp, winner, victim,
-                                                 c->st.mp_loop_ep, c->st.kf_win_ep, c->st.kf_win_pos);
+cudaError_t launch_resolve(lc_ctx* c, int mode, const MatchArgs& a, int n_units, cudaStream_t s) {
+  if (n_units <= 0) return cudaSuccess;
+  if (mode == 0) k_resolve<0><<<n_units, LC_NTHREADS, 0, s>>>(a);
+  else k_resolve<1><<<n_units, LC_NTHREADS, 0, s>>>(a);
   c->launches++;
   return cudaGetLastError();
 }
 
-cudaError_t launch_fuse_resolve(lc_ctx* c, int mode, int n_units, const int32_t* unit_kf,
-                                const int64_t* unit_woff, const int64_t* unit_toff,
-                                const int32_t* unit_param, const lc_match_params* params,
-                                const int32_t* taken, unsigned long long* winner,
-                                unsigned long long* victim, int8_t* action, int32_t* out_mp,
-                                int32_t* out_dist, unsigned long long* counts, int F_max,
-                                cudaStream_t s) {
-  (void)F_max;
-  if (n_units <= 0) return cudaSuccess;
+cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, const int32_t* d_window,
+                             int64_t n_wfeat, const int32_t* mp_list, int64_t n_list_total,
+                             unsigned long long* winner, unsigned long long* victim, cudaStream_t s) {
   Store& st = c->st;
-  if (mode == 0)
-    k_resolve<0><<<n_units, LC_NTHREADS, 0, s>>>(unit_kf, unit_woff, unit_toff, unit_param, params,
-                                                 st.kf_fbeg, st.feat_mp, st.feat_angle, st.mp_rec,
-                                                 st.mp_flags, st.mp_loop_ep, c->epoch, taken,
-                                                 winner, victim, action, out_mp, out_dist, counts);
-  else
-    k_resolve<1><<<n_units, LC_NTHREADS, 0, s>>>(unit_kf, unit_woff, unit_toff, unit_param, params,
-                                                 st.kf_fbeg, st.feat_mp, st.feat_angle, st.mp_rec,
-                                                 st.mp_flags, st.mp_loop_ep, c->epoch, taken,
-                                                 winner, victim, action, out_mp, out_dist, counts);
+  const int n_vbits = (st.n_mp + 31) / 32;
+  int64_t n = std::max<int64_t>(n_w, n_vbits);
+  if (phase & LC_FUSE_PLAN) {
+    n = std::max<int64_t>(n, n_list_total);
+    if (init_winner) n = std::max<int64_t>(n, n_wfeat);
+    n = std::max<int64_t>(n, st.n_mp);
+  }
+  k_fuse_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(phase, init_winner, c->epoch, n_w, d_window, n_wfeat,
+                                                 mp_list, n_list_total, st.n_mp, winner, victim,
+                                                 st.mp_loop_ep, st.kf_win_ep, st.kf_win_pos,
+                                                 st.mp_vbits, n_vbits, st.kf_dirty);
   c->launches++;
   return cudaGetLastError();
 }
@@ -526,19 +719,21 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
   Store& st = c->st;
   if (st.n_mp > 0) {
     k_fuse_victims<<<grid_for(st.n_mp), LC_NTHREADS, 0, s>>>(st.n_mp, victim, st.mp_flags,
-                                                             st.mp_replaced_by, counts);
+                                                             st.mp_replaced_by, st.mp_vbits, counts);
     c->launches++;
   }
   if (st.n_kf > 0) {
+    k_apply_mark<<<st.n_kf, LC_NTHREADS, 0, s>>>(c->epoch, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos,
+                                                d_woff, winner, st.mp_vbits, st.feat_mp, st.kf_dirty);
     int H = pow2_at_least(2 * (st.max_F > 0 ? st.max_F : 1));
     size_t smem = (size_t)st.max_F * 9 + (size_t)H * 8;
     smem = (smem + 15) & ~(size_t)15;
-    cudaError_t e = cudaFuncSetAttribute(k_fuse_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_apply_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_fuse_apply<<<st.n_kf, LC_NTHREADS, smem, s>>>(c->epoch, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos,
-                                                   d_woff, winner, victim, st.feat_mp, st.mp_nobs,
-                                                   H, counts);
-    c->launches++;
+    k_apply_fix<<<std::min(st.n_kf, 148 * 4), LC_NTHREADS, smem, s>>>(
+        c->epoch, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos, d_woff, winner, victim, st.mp_vbits,
+        st.kf_dirty, st.feat_mp, st.mp_nobs, H, counts);
+    c->launches += 2;
   }
   return cudaGetLastError();
 }

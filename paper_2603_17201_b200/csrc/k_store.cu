@@ -54,7 +54,8 @@ __global__ void k_count_nobs(int n_feat, int n_mp, const int32_t* __restrict__ f
 // cell = (floor((u-min_x)*cols/(max_x-min_x)), floor((v-min_y)*rows/(max_y-min_y))),
 // clamped; within a cell features keep ascending original index (deterministic).
 __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
-    int n_levels, int n_cams, const int32_t* __restrict__ fbeg, const int32_t* __restrict__ kf_cam,
+    int n_levels, int n_cams, int Gs, const int32_t* __restrict__ fbeg,
+    const int32_t* __restrict__ fpad, const int32_t* __restrict__ kf_cam,
     const DevCam* __restrict__ cams, const float* __restrict__ fuv, const uint8_t* __restrict__ foct,
     const uint8_t* __restrict__ fdesc, uint16_t* __restrict__ kf_cell, float2* __restrict__ fc_uv,
     uint32_t* __restrict__ fc_meta, uint4* __restrict__ fc_desc, uint32_t* __restrict__ errs) {
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
   const int k = blockIdx.x;
   const int fb = fbeg[k];
   const int F = fbeg[k + 1] - fb;
+  const int fp = fpad[k];
   const int ci = kf_cam[k];
   if (ci < 0 || ci >= n_cams) {
     if (threadIdx.x == 0) atomicAdd(&errs[ERR_CAM], 1u);
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
   int acc = s_part[threadIdx.x];
   for (int i = c0; i < c1; ++i) { int x = s_cnt[i]; s_cnt[i] = acc; acc += x; }
   __syncthreads();
-  uint16_t* cell_out = kf_cell + (size_t)k * (G + 1);
+  uint16_t* cell_out = kf_cell + (size_t)k * Gs;
   for (int i = threadIdx.x; i < G; i += blockDim.x) cell_out[i] = (uint16_t)s_cnt[i];
   if (threadIdx.x == 0) { cell_out[G] = (uint16_t)F; s_cnt[G] = F; }
   __syncthreads();
@@ -125,16 +127,16 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
   __syncthreads();
   for (int p = threadIdx.x; p < F; p += blockDim.x) {
     int f = s_perm[p];
-    fc_uv[fb + p] = make_float2(fuv[2 * (fb + f)], fuv[2 * (fb + f) + 1]);
-    fc_meta[fb + p] = (uint32_t)f | ((uint32_t)foct[fb + f] << 16);
+    fc_uv[fp + p] = make_float2(fuv[2 * (fb + f)], fuv[2 * (fb + f) + 1]);
+    fc_meta[fp + p] = (uint32_t)f | ((uint32_t)foct[fb + f] << 16);
     const uint8_t* d = fdesc + 32 * (size_t)(fb + f);
     uint32_t w[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       w[i] = (uint32_t)d[4 * i] | ((uint32_t)d[4 * i + 1] << 8) | ((uint32_t)d[4 * i + 2] << 16) |
              ((uint32_t)d[4 * i + 3] << 24);
-    fc_desc[2 * (size_t)(fb + p)] = make_uint4(w[0], w[1], w[2], w[3]);
-    fc_desc[2 * (size_t)(fb + p) + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+    fc_desc[2 * (size_t)(fp + p)] = make_uint4(w[0], w[1], w[2], w[3]);
+    fc_desc[2 * (size_t)(fp + p) + 1] = make_uint4(w[4], w[5], w[6], w[7]);
   }
 }
 
@@ -199,7 +201,8 @@ cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, co
     cudaError_t e = cudaFuncSetAttribute(k_grid_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    k_grid_build<<<st.n_kf, LC_NTHREADS, smem, s>>>(st.n_levels, st.n_cams, st.kf_fbeg, st.kf_cam,
+    k_grid_build<<<st.n_kf, LC_NTHREADS, smem, s>>>(st.n_levels, st.n_cams, st.Gs, st.kf_fbeg,
+                                                    st.kf_fpad, st.kf_cam,
                                                     st.cams, fuv, foct, fdesc, st.kf_cell,
                                                     st.fc_uv, st.fc_meta, st.fc_desc, d_errs);
     c->launches++;

@@ -229,10 +229,11 @@ void dev_alloc(lc_ctx* c, T** p, size_t n) {
 }
 
 void free_store(Store& st) {
-  void* ptrs[] = {st.kf_pose, st.kf_cam, st.kf_fbeg, st.kf_cell, st.fc_uv, st.fc_meta,
+  void* ptrs[] = {st.kf_pose, st.kf_cam, st.kf_fbeg, st.kf_fpad, st.kf_cell, st.fc_uv, st.fc_meta,
                   st.fc_desc, st.feat_mp, st.feat_angle, st.mp_rec, st.mp_flags, st.mp_ref_kf,
                   st.mp_replaced_by, st.mp_nobs, st.mp_corr_ref, st.mp_loop_ep, st.mp_owner,
-                  st.kf_S_corr, st.kf_in_win, st.kf_win_ep, st.kf_win_pos, st.cams};
+                  st.kf_S_corr, st.kf_in_win, st.kf_win_ep, st.kf_win_pos, st.mp_vbits,
+                  st.kf_dirty, st.cams};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   st = Store();
@@ -260,6 +261,8 @@ void fill_match_store(lc_ctx* c, MatchArgs& a) {
   a.kf_pose = st.kf_pose;
   a.kf_cam = st.kf_cam;
   a.kf_fbeg = st.kf_fbeg;
+  a.kf_fpad = st.kf_fpad;
+  a.Gs = st.Gs;
   a.kf_cell = st.kf_cell;
   a.fc_uv = st.fc_uv;
   a.fc_meta = st.fc_meta;
@@ -412,7 +415,11 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
     st.n_kf = m->n_kf; st.n_feat = m->n_feat; st.n_mp = m->n_mp; st.n_cams = n_cams;
     st.n_levels = prm->n_levels; st.cols = prm->grid_cols; st.rows = prm->grid_rows;
     st.G = st.cols * st.rows;
+    st.Gs = (int32_t)round_up((size_t)st.G + 1, 8);
     st.max_F = max_F;
+    std::vector<int32_t> fpad(st.n_kf + 1, 0);
+    for (int k = 0; k < st.n_kf; ++k) fpad[k + 1] = fpad[k] + (int32_t)round_up((size_t)(fbeg[k + 1] - fbeg[k]), 4);
+    st.n_fpad = fpad[st.n_kf];
     st.scale[0] = 1.0;
     for (int n = 1; n < LC_MAX_LEVELS; ++n) st.scale[n] = st.scale[n - 1] * prm->scale_factor;
     st.h_fbeg = fbeg;
@@ -421,10 +428,16 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
     dev_alloc(c, &st.kf_pose, 13 * NK);
     dev_alloc(c, &st.kf_cam, NK);
     dev_alloc(c, &st.kf_fbeg, NK + 1);
-    dev_alloc(c, &st.kf_cell, NK * (st.G + 1));
-    dev_alloc(c, &st.fc_uv, NF);
-    dev_alloc(c, &st.fc_meta, NF);
-    dev_alloc(c, &st.fc_desc, 2 * NF);
+    const size_t NP = (size_t)st.n_fpad + 4;
+    dev_alloc(c, &st.kf_fpad, NK + 1);
+    dev_alloc(c, &st.kf_cell, NK * (size_t)st.Gs);
+    dev_alloc(c, &st.fc_uv, NP);
+    dev_alloc(c, &st.fc_meta, NP);
+    dev_alloc(c, &st.fc_desc, 2 * NP);
+    CK(cudaMemsetAsync(st.kf_cell, 0, sizeof(uint16_t) * NK * st.Gs, s));
+    CK(cudaMemsetAsync(st.fc_uv, 0, sizeof(float2) * NP, s));
+    CK(cudaMemsetAsync(st.fc_meta, 0, sizeof(uint32_t) * NP, s));
+    CK(cudaMemcpyAsync(st.kf_fpad, fpad.data(), sizeof(int32_t) * (NK + 1), cudaMemcpyHostToDevice, s));
     dev_alloc(c, &st.feat_mp, NF);
     dev_alloc(c, &st.feat_angle, NF);
     dev_alloc(c, &st.mp_rec, NM);
@@ -439,6 +452,8 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
     dev_alloc(c, &st.kf_in_win, NK);
     dev_alloc(c, &st.kf_win_ep, NK);
     dev_alloc(c, &st.kf_win_pos, NK);
+    dev_alloc(c, &st.mp_vbits, (NM + 31) / 32 + 1);
+    dev_alloc(c, &st.kf_dirty, NK + 1);
     dev_alloc(c, &st.cams, n_cams);
     std::vector<DevCam> dc(n_cams);
     for (int i = 0; i < n_cams; ++i) {
@@ -633,12 +648,25 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       total_q += len;
       F_max = std::max<int>(F_max, (int)(woff[i + 1] - woff[i]));
     }
-    const int ch = pick_chunk(total_q);
+    // sole mode: one CTA per window keyframe, which initialises and resolves its own
+    // winner words (no winner-table init pass, no separate resolve launch). Used when
+    // the shard already has enough keyframes to fill the GPU and no list is huge.
+    int64_t max_len = 0;
+    for (int i = w_lo; i < w_hi; ++i)
+      max_len = std::max<int64_t>(max_len, win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list);
+    const bool sole = (w_hi - w_lo) >= 2 * 148 && max_len <= 16384;
+    const int64_t ch = sole ? std::max<int64_t>(max_len, 1) : pick_chunk(total_q);
     std::vector<int32_t> bunit;
     std::vector<int64_t> bq0, bq1;
     for (int i = w_lo; i < w_hi; ++i) {
       int64_t b = lbeg[i];
       int64_t e = b + (win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list);
+      if (sole) {
+        bunit.push_back(i);
+        bq0.push_back(b);
+        bq1.push_back(e);
+        continue;
+      }
       for (int64_t q = b; q < e; q += ch) {
         bunit.push_back(i);
         bq0.push_back(q);
@@ -689,7 +717,8 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     }
     {
       Prof pr(c, LC_PROF_FUSE_PREP, call.s);
-      CK(launch_fuse_prep(c, phase, n_window, d_win, d_woff, n_wfeat, d_list, n_list, win, vic, call.s));
+      CK(launch_fuse_prep(c, phase, sole ? 0 : 1, n_window, d_win, n_wfeat, d_list, n_list, win, vic,
+                          call.s));
     }
     if (phase & LC_FUSE_PLAN) {
       a.unit_kf = d_win;
@@ -712,13 +741,21 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       a.dbg_best = dbg_best;
       a.dbg_uv = dbg_uv;
       a.dbg_ncand = dbg_nc;
+      a.feat_angle = st.feat_angle;
+      a.loop_ep = st.mp_loop_ep;
+      a.epoch = c->epoch;
+      a.victim = vic;
+      a.action = act;
+      a.sole = sole ? 1 : 0;
+      a.unit_base = w_lo;
       {
         Prof pr(c, LC_PROF_MATCH, call.s);
         CK(launch_match(c, 0, a, (int)bunit.size(), F_max, call.s));
       }
-      Prof pr(c, LC_PROF_RESOLVE, call.s);
-      CK(launch_fuse_resolve(c, 0, w_hi - w_lo, d_win + w_lo, d_woff + w_lo, d_woff + w_lo, nullptr,
-                             d_prm, nullptr, win, vic, act, nullptr, nullptr, cnt, F_max, call.s));
+      if (!sole) {
+        Prof pr(c, LC_PROF_RESOLVE, call.s);
+        CK(launch_resolve(c, 0, a, w_hi - w_lo, call.s));
+      }
     }
     if (phase & LC_FUSE_APPLY) {
       Prof pr(c, LC_PROF_APPLY, call.s);
@@ -816,6 +853,11 @@ lc_status lc_search_by_projection(lc_ctx* c, int32_t n_pairs, const int32_t* pai
     a.blk_q1 = d_bq1;
     a.mp_list = d_list;
     a.taken = d_taken;
+    a.feat_angle = st.feat_angle;
+    a.out_mp = o_mp;
+    a.out_dist = o_dist;
+    a.sole = 0;
+    a.unit_base = 0;
     a.winner = win;
     a.counts = cnt;
     a.n_mp = st.n_mp;
@@ -829,8 +871,7 @@ lc_status lc_search_by_projection(lc_ctx* c, int32_t n_pairs, const int32_t* pai
       CK(launch_match(c, 1, a, (int)bunit.size(), F_max, call.s));
     }
     Prof pr(c, LC_PROF_SBP_RESOLVE, call.s);
-    CK(launch_fuse_resolve(c, 1, n_pairs, d_kf, d_off, d_off, d_param, d_prm, d_taken, win, nullptr,
-                           nullptr, o_mp, o_dist, cnt, F_max, call.s));
+    CK(launch_resolve(c, 1, a, n_pairs, call.s));
     if (out_counts) {
       int64_t* d = call.out(out_counts, (size_t)LC_NCOUNT * n_pairs);
       CK(cudaMemcpyAsync(d, cnt, sizeof(uint64_t) * LC_NCOUNT * n_pairs, cudaMemcpyDeviceToDevice, call.s));

@@ -48,12 +48,15 @@ struct DevCam {
 struct Store {
   int32_t n_kf = 0, n_feat = 0, n_mp = 0, n_cams = 0;
   int32_t n_levels = 0, cols = 0, rows = 0, G = 0;
+  int32_t Gs = 0;        // per-keyframe cell-table stride: round_up(G + 1, 8) (16-B rows for TMA)
+  int64_t n_fpad = 0;    // padded feature count of the cell-major arrays
   double scale[LC_MAX_LEVELS];
   int32_t max_F = 0;
   // device arrays
   double* kf_pose = nullptr;
   int32_t* kf_cam = nullptr;
   int32_t* kf_fbeg = nullptr;
+  int32_t* kf_fpad = nullptr;   // [n_kf+1] start of each keyframe's cell-major block (multiple of 4)
   uint16_t* kf_cell = nullptr;
   float2* fc_uv = nullptr;
   uint32_t* fc_meta = nullptr;
@@ -72,6 +75,8 @@ struct Store {
   int32_t* kf_in_win = nullptr;
   uint32_t* kf_win_ep = nullptr;
   int32_t* kf_win_pos = nullptr;
+  uint32_t* mp_vbits = nullptr;  // [(n_mp+31)/32] victim bitmap of the current fuse call
+  int32_t* kf_dirty = nullptr;   // [1 + n_kf] count + keyframes changed by the apply
   DevCam* cams = nullptr;
   // host copies
   std::vector<int32_t> h_fbeg;
@@ -84,6 +89,7 @@ struct MatchArgs {
   const double* kf_pose;  // unused by the kernel (units carry S)
   const int32_t* kf_cam;
   const int32_t* kf_fbeg;
+  const int32_t* kf_fpad;
   const uint16_t* kf_cell;
   const float2* fc_uv;
   const uint32_t* fc_meta;
@@ -92,7 +98,7 @@ struct MatchArgs {
   const MpRec* mp_rec;
   const uint8_t* mp_flags;
   const DevCam* cams;
-  int32_t cols, rows, G, n_levels;
+  int32_t cols, rows, G, n_levels, Gs;
   double scale[LC_MAX_LEVELS];
   // call
   const int32_t* unit_kf;      // [n_units]
@@ -116,6 +122,17 @@ struct MatchArgs {
   double* dbg_uv;
   int32_t* dbg_ncand;
   int32_t hash_size;           // power of 2
+  int32_t off_uv, off_meta, off_hash, off_queue;   // dynamic smem carve (bytes)
+  // resolve (orientation + actions / SBP output tables)
+  const float* feat_angle;
+  const uint32_t* loop_ep;
+  uint32_t epoch;
+  unsigned long long* victim;
+  int8_t* action;
+  int32_t* out_mp;
+  int32_t* out_dist;
+  int32_t sole;        // 1: one CTA per unit -> the match CTA initialises and resolves its unit
+  int32_t unit_base;   // k_resolve: unit = unit_base + blockIdx.x
 };
 
 struct lc_ctx {
@@ -235,17 +252,10 @@ cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, co
                                cudaStream_t s);
 cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max,
                          cudaStream_t s);
-cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int n_w, const int32_t* d_window,
-                             const int64_t* d_woff, int64_t n_wfeat, const int32_t* mp_list,
-                             int64_t n_list_total, unsigned long long* winner,
-                             unsigned long long* victim, cudaStream_t s);
-cudaError_t launch_fuse_resolve(lc_ctx* c, int mode, int n_units, const int32_t* unit_kf,
-                                const int64_t* unit_woff, const int64_t* unit_toff,
-                                const int32_t* unit_param, const lc_match_params* params,
-                                const int32_t* taken, unsigned long long* winner,
-                                unsigned long long* victim, int8_t* action, int32_t* out_mp,
-                                int32_t* out_dist, unsigned long long* counts, int F_max,
-                                cudaStream_t s);
+cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, const int32_t* d_window,
+                             int64_t n_wfeat, const int32_t* mp_list, int64_t n_list_total,
+                             unsigned long long* winner, unsigned long long* victim, cudaStream_t s);
+cudaError_t launch_resolve(lc_ctx* c, int mode, const MatchArgs& a, int n_units, cudaStream_t s);
 cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned long long* winner,
                               const unsigned long long* victim, unsigned long long* counts,
                               cudaStream_t s);
