@@ -4,67 +4,34 @@
 // transformation"; reading O3) and ALL ("propagates the loop
 // correction to the rest of the map"; reading O10). Both are
 // streaming passes over the map-point records (HBM-bound); the per-keyframe
-// transforms are computed once into a small scratch table first so every
-// point applies two precomputed Sim3s in fp64 (13 doubles each, L1/L2 resident).
+// transforms are computed once into a small scratch table first, so every point
+// applies two precomputed Sim3s in fp64 (loaded as 16-B vectors, L1-resident when
+// consecutive map points share their keyframe, as in creation order).
+//
+// WINDOW = 2 kernels (+2 memsets): [owner election || S^corr per window position]
+// then [point re-anchoring || pose write-back]; ALL = 2 kernels.
 #include <cuda_runtime.h>
-#include <climits>
 
 #include "lc_internal.cuh"
 
 namespace {
 
-// scratch layout for WINDOW: per window position i: S_corr[13] | inv(S_corr)[13] | T_old[13]
-constexpr int WSTR = 39;
+// WINDOW scratch per window position i (16-B aligned rows of WSTR doubles):
+//   [0, 13) T_iw^old  |  [14, 27) inverse(S_i^corr)  |  [28, 41) S_i^corr
+constexpr int WSTR = 42;
+// ALL scratch per keyframe: [0, 13) S^pre | [14, 27) inverse(S^opt)
+constexpr int ASTR = 28;
+constexpr int32_t OWNER_NONE = 0x7F7F7F7F;  // memset byte pattern 0x7F
 
-__global__ void k_win_prep(int n_kf, int n_mp, int32_t* __restrict__ owner,
-                           int32_t* __restrict__ kf_in_win) {
-  const int stride = gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_mp || i < n_kf; i += stride) {
-    if (i < n_mp) owner[i] = INT_MAX;
-    if (i < n_kf) kf_in_win[i] = 0;
+__device__ __forceinline__ void load13(const double* __restrict__ src, double* d) {
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const double2 x = __ldg(s2 + i);
+    d[2 * i] = x.x;
+    d[2 * i + 1] = x.y;
   }
-}
-
-__global__ void k_win_sim3(int n_w, int cur_pos, const int32_t* __restrict__ window,
-                           const double* __restrict__ kf_pose, const double* __restrict__ Scw,
-                           double* __restrict__ scr, double* __restrict__ kf_S_corr,
-                           int32_t* __restrict__ kf_in_win) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_w) return;
-  const int k = window[i];
-  const int c = window[cur_pos];
-  double T[13], S[13], Tci[13], Sic[13], Si[13];
-  for (int j = 0; j < 13; ++j) T[j] = kf_pose[13 * (size_t)k + j];
-  if (i == cur_pos) {
-    for (int j = 0; j < 13; ++j) S[j] = Scw[j];
-  } else {
-    double Tc[13];
-    for (int j = 0; j < 13; ++j) Tc[j] = kf_pose[13 * (size_t)c + j];
-    lc_sim3_inverse(Tc, Tci);
-    lc_sim3_compose(T, Tci, Sic);   // S_ic = T_iw * inverse(T_cw)
-    lc_sim3_compose(Sic, Scw, S);   // S_iw^corr = S_ic * S_cw^corr
-  }
-  lc_sim3_inverse(S, Si);
-  double* o = scr + (size_t)WSTR * i;
-  for (int j = 0; j < 13; ++j) { o[j] = S[j]; o[13 + j] = Si[j]; o[26 + j] = T[j]; }
-  for (int j = 0; j < 13; ++j) kf_S_corr[13 * (size_t)k + j] = S[j];
-  kf_in_win[k] = 1;
-}
-
-// owner = first window position (list order) observing the non-bad map point
-__global__ void __launch_bounds__(LC_NTHREADS) k_win_mark(const int32_t* __restrict__ window,
-                                                          const int32_t* __restrict__ kf_fbeg,
-                                                          const int32_t* __restrict__ feat_mp,
-                                                          const uint8_t* __restrict__ mp_flags,
-                                                          int32_t* __restrict__ owner) {
-  const int i = blockIdx.x;
-  const int k = window[i];
-  const int f0 = kf_fbeg[k], f1 = kf_fbeg[k + 1];
-  for (int f = f0 + threadIdx.x; f < f1; f += blockDim.x) {
-    int m = feat_mp[f];
-    if (m < 0 || (mp_flags[m] & 1u)) continue;
-    atomicMin(&owner[m], i);
-  }
+  d[12] = __ldg(src + 12);
 }
 
 __device__ __forceinline__ void warp_count(uint32_t n, unsigned long long* dst) {
@@ -73,48 +40,89 @@ __device__ __forceinline__ void warp_count(uint32_t n, unsigned long long* dst) 
   if ((threadIdx.x & 31) == 0 && n) atomicAdd(dst, (unsigned long long)n);
 }
 
-// p <- fl32( inverse(S_o^corr)( T_o,w^old(p) ) ), corr_ref <- window[o] (or -1)
-__global__ void k_win_points(int n_mp, const int32_t* __restrict__ owner,
-                             const int32_t* __restrict__ window, const double* __restrict__ scr,
-                             MpRec* __restrict__ rec, int32_t* __restrict__ corr_ref,
-                             unsigned long long* __restrict__ counts) {
-  uint32_t n = 0;
-  const int stride = gridDim.x * blockDim.x;
-  const int base = blockIdx.x * blockDim.x;
-  for (int q0 = base; q0 < n_mp; q0 += stride) {
-    const int q = q0 + threadIdx.x;
-    if (q < n_mp) {
-      const int o = owner[q];
-      if (o == INT_MAX) {
-        corr_ref[q] = -1;
-      } else {
-        const double* S = scr + (size_t)WSTR * o;
-        double p[3] = {rec[q].pos[0], rec[q].pos[1], rec[q].pos[2]}, pc[3], pw[3];
-        lc_sim3_apply(S + 26, p, pc);
-        lc_sim3_apply(S + 13, pc, pw);
-        rec[q].pos[0] = __double2float_rn(pw[0]);
-        rec[q].pos[1] = __double2float_rn(pw[1]);
-        rec[q].pos[2] = __double2float_rn(pw[2]);
-        corr_ref[q] = window[o];
-        ++n;
-      }
+// Block i = window position i: thread 0 computes S_i^corr = (T_iw * inverse(T_cw)) *
+// S_cw^corr from the OLD poses (S_c^corr = S_cw^corr) into scratch; all threads elect
+// owner(m) = min window position observing the non-bad map point m (atomicMin).
+__global__ void __launch_bounds__(LC_NTHREADS) k_win_a(
+    int cur_pos, const int32_t* __restrict__ window, const double* __restrict__ kf_pose,
+    const double* __restrict__ Scw, const int32_t* __restrict__ kf_fbeg,
+    const int32_t* __restrict__ feat_mp, const uint8_t* __restrict__ mp_flags,
+    int32_t* __restrict__ owner, double* __restrict__ scr, double* __restrict__ kf_S_corr,
+    int32_t* __restrict__ kf_in_win) {
+  const int i = blockIdx.x;
+  const int k = window[i];
+  if (threadIdx.x == 0) {
+    double T[13], S[13], Si[13];
+    for (int j = 0; j < 13; ++j) T[j] = kf_pose[13 * (size_t)k + j];
+    if (i == cur_pos) {
+      for (int j = 0; j < 13; ++j) S[j] = Scw[j];
+    } else {
+      double Tc[13], Tci[13], Sic[13];
+      const int c = window[cur_pos];
+      for (int j = 0; j < 13; ++j) Tc[j] = kf_pose[13 * (size_t)c + j];
+      lc_sim3_inverse(Tc, Tci);
+      lc_sim3_compose(T, Tci, Sic);   // S_ic = T_iw * inverse(T_cw)
+      lc_sim3_compose(Sic, Scw, S);   // S_iw^corr = S_ic * S_cw^corr
     }
+    lc_sim3_inverse(S, Si);
+    double* o = scr + (size_t)WSTR * i;
+    for (int j = 0; j < 13; ++j) { o[j] = T[j]; o[14 + j] = Si[j]; o[28 + j] = S[j]; }
+    o[13] = o[27] = o[41] = 0.0;
+    for (int j = 0; j < 13; ++j) kf_S_corr[13 * (size_t)k + j] = S[j];
+    kf_in_win[k] = 1;
   }
-  warp_count(n, &counts[LC_COUNT_CORR_MP]);
+  const int f0 = kf_fbeg[k], f1 = kf_fbeg[k + 1];
+  for (int f = f0 + threadIdx.x; f < f1; f += blockDim.x) {
+    const int m = feat_mp[f];
+    if (m < 0 || (mp_flags[m] & 1u)) continue;
+    atomicMin(&owner[m], i);
+  }
 }
 
-__global__ void k_win_writeback(int n_w, const int32_t* __restrict__ window,
-                                const double* __restrict__ scr, double* __restrict__ kf_pose,
-                                unsigned long long* __restrict__ counts) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+// Blocks [0, nb_mp): p <- fl32( inverse(S_o^corr)( T_o,w^old(p) ) ), corr_ref <- window[o]
+// (or -1); blocks [nb_mp, ...): window pose write-back T_iw <- SE3(S_i^corr).
+__global__ void __launch_bounds__(LC_NTHREADS) k_win_b(
+    int n_mp, int nb_mp, int n_w, const int32_t* __restrict__ owner,
+    const int32_t* __restrict__ window, const double* __restrict__ scr, MpRec* __restrict__ rec,
+    int32_t* __restrict__ corr_ref, double* __restrict__ kf_pose,
+    unsigned long long* __restrict__ counts) {
   uint32_t n = 0;
-  if (i < n_w) {
-    double T[13];
-    lc_sim3_se3(scr + (size_t)WSTR * i, T);
-    for (int j = 0; j < 13; ++j) kf_pose[13 * (size_t)window[i] + j] = T[j];
-    n = 1;
+  if ((int)blockIdx.x < nb_mp) {
+    const int stride = nb_mp * blockDim.x;
+    for (int q0 = blockIdx.x * blockDim.x; q0 < n_mp; q0 += stride) {
+      const int q = q0 + threadIdx.x;
+      if (q < n_mp) {
+        const int o = owner[q];
+        if (o == OWNER_NONE) {
+          corr_ref[q] = -1;
+        } else {
+          const double* S = scr + (size_t)WSTR * o;
+          double T[13], Si[13];
+          load13(S, T);
+          load13(S + 14, Si);
+          const float4 pf = *reinterpret_cast<const float4*>(rec + q);
+          double p[3] = {pf.x, pf.y, pf.z}, pc[3], pw[3];
+          lc_sim3_apply(T, p, pc);
+          lc_sim3_apply(Si, pc, pw);
+          rec[q].pos[0] = __double2float_rn(pw[0]);
+          rec[q].pos[1] = __double2float_rn(pw[1]);
+          rec[q].pos[2] = __double2float_rn(pw[2]);
+          corr_ref[q] = window[o];
+          ++n;
+        }
+      }
+    }
+    warp_count(n, &counts[LC_COUNT_CORR_MP]);
+  } else {
+    const int i = (blockIdx.x - nb_mp) * blockDim.x + threadIdx.x;
+    if (i < n_w) {
+      double T[13];
+      lc_sim3_se3(scr + (size_t)WSTR * i + 28, T);
+      for (int j = 0; j < 13; ++j) kf_pose[13 * (size_t)window[i] + j] = T[j];
+      n = 1;
+    }
+    warp_count(n, &counts[LC_COUNT_CORR_KF]);
   }
-  warp_count(n, &counts[LC_COUNT_CORR_KF]);
 }
 
 // ALL: per keyframe S^pre and inverse(S^opt) into scratch, pose <- SE3(S^opt)
@@ -130,8 +138,9 @@ __global__ void k_all_kf(int n_kf, const double* __restrict__ Sopt, double* __re
     for (int j = 0; j < 13; ++j) opt[j] = Sopt[13 * (size_t)k + j];
     lc_sim3_inverse(opt, inv);
     lc_sim3_se3(opt, T);
-    double* o = scr + 26 * (size_t)k;
-    for (int j = 0; j < 13; ++j) { o[j] = pre[j]; o[13 + j] = inv[j]; }
+    double* o = scr + (size_t)ASTR * k;
+    for (int j = 0; j < 13; ++j) { o[j] = pre[j]; o[14 + j] = inv[j]; }
+    o[13] = o[27] = 0.0;
     for (int j = 0; j < 13; ++j) kf_pose[13 * (size_t)k + j] = T[j];
     kf_in_win[k] = 0;
     n = 1;
@@ -139,10 +148,10 @@ __global__ void k_all_kf(int n_kf, const double* __restrict__ Sopt, double* __re
   warp_count(n, &counts[LC_COUNT_CORR_KF]);
 }
 
-__global__ void k_all_points(int n_mp, const double* __restrict__ scr,
-                             const int32_t* __restrict__ ref_kf, const uint8_t* __restrict__ flags,
-                             MpRec* __restrict__ rec, int32_t* __restrict__ corr_ref,
-                             unsigned long long* __restrict__ counts) {
+__global__ void __launch_bounds__(LC_NTHREADS) k_all_points(
+    int n_mp, const double* __restrict__ scr, const int32_t* __restrict__ ref_kf,
+    const uint8_t* __restrict__ flags, MpRec* __restrict__ rec, int32_t* __restrict__ corr_ref,
+    unsigned long long* __restrict__ counts) {
   uint32_t n = 0;
   const int stride = gridDim.x * blockDim.x;
   for (int q0 = blockIdx.x * blockDim.x; q0 < n_mp; q0 += stride) {
@@ -152,10 +161,14 @@ __global__ void k_all_points(int n_mp, const double* __restrict__ scr,
       if (cr >= 0) corr_ref[q] = -1;
       if (!(flags[q] & 1u)) {
         const int r = cr >= 0 ? cr : ref_kf[q];
-        const double* S = scr + 26 * (size_t)r;
-        double p[3] = {rec[q].pos[0], rec[q].pos[1], rec[q].pos[2]}, pc[3], pw[3];
-        lc_sim3_apply(S, p, pc);
-        lc_sim3_apply(S + 13, pc, pw);
+        const double* S = scr + (size_t)ASTR * r;
+        double pre[13], inv[13];
+        load13(S, pre);
+        load13(S + 14, inv);
+        const float4 pf = *reinterpret_cast<const float4*>(rec + q);
+        double p[3] = {pf.x, pf.y, pf.z}, pc[3], pw[3];
+        lc_sim3_apply(pre, p, pc);
+        lc_sim3_apply(inv, pc, pw);
         rec[q].pos[0] = __double2float_rn(pw[0]);
         rec[q].pos[1] = __double2float_rn(pw[1]);
         rec[q].pos[2] = __double2float_rn(pw[2]);
@@ -175,23 +188,24 @@ int grid_for(int64_t n) {
 
 }  // namespace
 
+int correct_window_scratch_stride() { return WSTR; }
+int correct_all_scratch_stride() { return ASTR; }
+
 cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t* d_window,
                                   const double* d_Scw, double* d_scr, unsigned long long* counts,
                                   cudaStream_t s) {
   Store& st = c->st;
-  int64_t n = st.n_mp > st.n_kf ? st.n_mp : st.n_kf;
-  k_win_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(st.n_kf, st.n_mp, st.mp_owner, st.kf_in_win);
-  k_win_sim3<<<(n_w + 127) / 128, 128, 0, s>>>(n_w, cur_pos, d_window, st.kf_pose, d_Scw, d_scr,
-                                              st.kf_S_corr, st.kf_in_win);
-  k_win_mark<<<n_w, LC_NTHREADS, 0, s>>>(d_window, st.kf_fbeg, st.feat_mp, st.mp_flags, st.mp_owner);
-  c->launches += 3;
-  if (st.n_mp > 0) {
-    k_win_points<<<grid_for(st.n_mp), LC_NTHREADS, 0, s>>>(st.n_mp, st.mp_owner, d_window, d_scr,
-                                                          st.mp_rec, st.mp_corr_ref, counts);
-    c->launches++;
-  }
-  k_win_writeback<<<(n_w + 127) / 128, 128, 0, s>>>(n_w, d_window, d_scr, st.kf_pose, counts);
-  c->launches++;
+  cudaError_t e;
+  if (st.n_mp > 0 && (e = cudaMemsetAsync(st.mp_owner, 0x7F, sizeof(int32_t) * st.n_mp, s)) != cudaSuccess)
+    return e;
+  if ((e = cudaMemsetAsync(st.kf_in_win, 0, sizeof(int32_t) * st.n_kf, s)) != cudaSuccess) return e;
+  k_win_a<<<n_w, LC_NTHREADS, 0, s>>>(cur_pos, d_window, st.kf_pose, d_Scw, st.kf_fbeg, st.feat_mp,
+                                      st.mp_flags, st.mp_owner, d_scr, st.kf_S_corr, st.kf_in_win);
+  const int nb_mp = st.n_mp > 0 ? grid_for(st.n_mp) : 0;
+  const int nb_w = (n_w + LC_NTHREADS - 1) / LC_NTHREADS;
+  k_win_b<<<nb_mp + nb_w, LC_NTHREADS, 0, s>>>(st.n_mp, nb_mp, n_w, st.mp_owner, d_window, d_scr,
+                                               st.mp_rec, st.mp_corr_ref, st.kf_pose, counts);
+  c->launches += 2;
   return cudaGetLastError();
 }
 

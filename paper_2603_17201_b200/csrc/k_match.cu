@@ -29,28 +29,6 @@ __device__ __constant__ int kMatchSlot[M_N] = {
     LC_COUNT_CULL_BOUNDS, LC_COUNT_CULL_DIST, LC_COUNT_CULL_ANGLE, LC_COUNT_CANDIDATES,
     LC_COUNT_NO_CAND, LC_COUNT_OVER_TH, LC_COUNT_RATIO_REJ, LC_COUNT_PROPOSALS};
 
-__device__ __forceinline__ uint32_t hash_slot(int32_t key, int shift) {
-  return ((uint32_t)key * 2654435769u) >> shift;
-}
-
-__device__ __forceinline__ void hash_insert(int32_t* tab, int mask, int shift, int32_t key) {
-  uint32_t h = hash_slot(key, shift);
-  while (true) {
-    int32_t prev = atomicCAS(&tab[h], -1, key);
-    if (prev == -1 || prev == key) return;
-    h = (h + 1) & mask;
-  }
-}
-
-__device__ __forceinline__ bool hash_contains(const int32_t* tab, int mask, int shift, int32_t key) {
-  uint32_t h = hash_slot(key, shift);
-  while (true) {
-    int32_t v = tab[h];
-    if (v == key) return true;
-    if (v == -1) return false;
-    h = (h + 1) & mask;
-  }
-}
 
 // Reduce per-thread counters over the block and add them to global memory.
 template <int N>
@@ -110,36 +88,66 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 }
 
-// compacted survivor of the geometric culls (phase A -> phase B)
-struct __align__(16) QEnt {
+// compacted survivor of the geometric culls (phase A -> phase B): 24 bytes
+struct __align__(8) QEnt {
   int32_t q;
-  int32_t j;     // position in mp_list
-  int32_t lvl;   // predicted level
-  int32_t pad;
+  uint32_t jl;   // (position in the block's query range) | (level << 27)
   double u, v;
 };
+
 // ---------------------------------------------------------------------------
 // MODE 0: fuse (already found = associated in the keyframe)
 // MODE 1: projection search (already found = pair_taken; taken features excluded)
 //
-// One CTA per (unit = keyframe/pair, query chunk); warps work independently
-// (no CTA barrier after staging). Staging: one elected thread issues three 1-D
-// TMA bulk copies (cell offsets, keypoints, octave/index words of the keyframe's
-// cell-major block) on an mbarrier while the CTA builds the already-found hash.
-// Phase A (per warp, 64 queries per batch, 2 per lane): list entry -> {flags,
-// first 32-B sector of the 64-B map-point record} -> fp64 SE3 projection, bounds /
-// distance / view-angle culls, level; survivors are ballot-compacted into the
-// warp's shared-memory ring. Phase B (whenever >= 32 survivors are queued): 4-lane
-// groups take one survivor each (8 per warp step) and stride over the cells of
-// each row of its window; per candidate 2 x uint4 descriptor loads + 8 POPC; the
-// group reduces (H << 16 | f) best and the second-best H with shuffles; the
-// proposal is a u64 atomicMin on (H << 32) | q.
+// One CTA per (unit = keyframe/pair, query chunk); warps work independently after
+// staging. Staging: one elected thread issues three 1-D TMA bulk copies (cell
+// offsets, keypoints, octave/index words of the keyframe's cell-major block) on an
+// mbarrier while the CTA builds the already-found hash (and, in sole mode,
+// initialises the unit's winner words).
+// Phase A (per warp, 64 queries per batch, 2 per lane): list entry -> {flags, first
+//   32-B sector of the 64-B map-point record} -> fp64 SE3 projection and culls.
+//   Division-free conservative pre-tests decide the bounds cull (pinhole) and the
+//   lower distance cull whenever the value is farther than a margin from the bound
+//   (margins >> fp64 rounding), so decisions equal the exact fp64 ones; the exact
+//   fp64 expression is evaluated otherwise. Survivors are ballot-compacted into
+//   the warp's shared-memory ring.
+// Phase B (per warp, whenever >= 32 survivors are queued; one survivor per lane):
+//   (1) the lane walks its window's cell rows in shared memory and records the
+//   candidate positions (octave + exact square-window test); (2) the warp computes
+//   the Hamming distance of ALL recorded candidates together (one 32-B descriptor
+//   sector per candidate, gathers issued by the whole warp; query descriptor words
+//   come from the owner lane by shuffle); (3) each lane reduces its own keys:
+//   best = min (H << 16 | f), second = min H of the rest; proposal = u64
+//   atomicMin on (H << 32) | q.
 // ---------------------------------------------------------------------------
 template <int MODE>
 __device__ void resolve_unit(const MatchArgs& a, int unit);
 
 constexpr int QW = 96;            // per-warp survivor ring (>= 31 + 64)
+constexpr int RMAX = 6;           // window cell rows per survivor in the flattened scan
 constexpr int NWARP = LC_NTHREADS / 32;
+constexpr int CPL = 6;            // candidate slots per survivor (more -> serial fallback)
+
+__device__ __forceinline__ uint32_t hslot(int32_t key, uint32_t size) {
+  return (uint32_t)(((uint64_t)((uint32_t)key * 2654435769u) * size) >> 32);
+}
+__device__ __forceinline__ void hins(int32_t* tab, uint32_t size, int32_t key) {
+  uint32_t h = hslot(key, size);
+  while (true) {
+    int32_t prev = atomicCAS(&tab[h], -1, key);
+    if (prev == -1 || prev == key) return;
+    h = (h + 1 == size) ? 0 : h + 1;
+  }
+}
+__device__ __forceinline__ bool hhas(const int32_t* tab, uint32_t size, int32_t key) {
+  uint32_t h = hslot(key, size);
+  while (true) {
+    int32_t v = tab[h];
+    if (v == key) return true;
+    if (v == -1) return false;
+    h = (h + 1 == size) ? 0 : h + 1;
+  }
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArgs a) {
@@ -151,19 +159,23 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArg
   __shared__ int s_next;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+  const unsigned ltmask = (1u << lane) - 1u;
   const int unit = a.blk_unit[blockIdx.x];
   const int k = a.unit_kf[unit];
   const int fb = a.kf_fbeg[k];
   const int F = a.kf_fbeg[k + 1] - fb;
   const int fp = a.kf_fpad[k];
-  const int H = a.hash_size;
-  const int hmask = H - 1;
-  const int hshift = 32 - __ffs(H) + 1;
+  const uint32_t HS = (uint32_t)a.hash_size;
   uint16_t* s_cell = (uint16_t*)smem;
   float2* s_uv = (float2*)(smem + a.off_uv);
   uint32_t* s_meta = (uint32_t*)(smem + a.off_meta);
   int32_t* s_hash = (int32_t*)(smem + a.off_hash);
-  QEnt* s_q = (QEnt*)(smem + a.off_queue) + warp * QW;
+  unsigned char* wbase = smem + a.off_queue + (size_t)warp * a.warp_bytes;
+  QEnt* s_q = (QEnt*)wbase;                                   // [QW]
+  uint32_t* s_key = (uint32_t*)(wbase + QW * sizeof(QEnt));   // [32][CPL] keys ...
+  uint32_t* s_rows = s_key;                                   // ... aliased by [32][RMAX] rows
+  uint16_t* s_cand = (uint16_t*)(s_key + 32 * (CPL > RMAX ? CPL : RMAX));  // [32][CPL]
+  int* s_nc = (int*)(s_cand + 32 * CPL);                      // [32] candidates per lane
   const int64_t toff = (MODE == 1 && a.taken) ? a.unit_toff[unit] : 0;
 
   // ---- stage the keyframe (TMA) + already-found hash ---------------------------
@@ -178,7 +190,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArg
     s_cam = a.cams[a.kf_cam[k]];
     s_next = 0;
   }
-  for (int i = tid; i < H; i += LC_NTHREADS) s_hash[i] = -1;
+  for (int i = tid; i < (int)HS; i += LC_NTHREADS) s_hash[i] = -1;
   __syncthreads();
   if (tid == 0) {
     const uint32_t b_cell = (uint32_t)a.Gs * 2u;
@@ -193,14 +205,16 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArg
   }
   for (int f = tid; f < F; f += LC_NTHREADS) {
     int32_t m = (MODE == 0) ? a.feat_mp[fb + f] : (a.taken ? a.taken[toff + f] : -1);
-    if (m >= 0) hash_insert(s_hash, hmask, hshift, m);
+    if (m >= 0) hins(s_hash, HS, m);
   }
   if (a.sole) {  // this CTA owns the unit's winner words: initialise them here
     unsigned long long* w0 = a.winner + a.unit_woff[unit];
     for (int f = tid; f < F; f += LC_NTHREADS) w0[f] = NONE;
   }
+  bool staged = false;
   if (MODE == 1 && a.taken) {  // taken features are not candidates (reading A19)
     mbar_wait(&s_bar, 0);
+    staged = true;
     __syncthreads();
     for (int p = tid; p < F; p += LC_NTHREADS)
       if (a.taken[toff + (s_meta[p] & 0xFFFFu)] >= 0) s_meta[p] |= 0x80000000u;
@@ -210,29 +224,44 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArg
   const lc_match_params prm = a.params[(MODE == 1 && a.unit_param) ? a.unit_param[unit] : 0];
   const int L = a.n_levels;
   const double sLm1 = a.scale[L - 1];
+  const double c08 = 0.8 / sLm1;            // for the division-free pre-test only
   const int cols = a.cols, rows = a.rows;
+  const bool pinhole = s_cam.model == 0;
+  const float fminx = (float)s_cam.min_x, fminy = (float)s_cam.min_y;
+  const float fsx = (float)s_cam.cell_sx, fsy = (float)s_cam.cell_sy;
   unsigned long long* win = a.winner + a.unit_woff[unit];
-  const int64_t lbeg = a.unit_lbeg[unit];
-  const int64_t qoff = a.unit_qoff[unit];
+  const int64_t q0 = a.blk_q0[blockIdx.x], q1 = a.blk_q1[blockIdx.x];
+  const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);   // debug index of q0
   uint32_t cnt[M_N];
 #pragma unroll
   for (int i = 0; i < M_N; ++i) cnt[i] = 0;
   int head = 0, tail = 0;  // warp-uniform ring indices (monotone; slot = idx % QW)
-  bool staged = (MODE == 1 && a.taken);
 
-  // ---- phase A: one query per call; true if it survived (entry written by caller)
+  // ---- phase A: one query; true if it survived (entry filled) ------------------
   auto phase_a = [&](int32_t q, int64_t j, bool in_range, uint8_t flag, uint4 r0, uint4 r1,
                      QEnt& ent) -> bool {
     int status = 0;
     double u = 0.0, v = 0.0;
     do {
       if (!in_range || (flag & 1u)) { status = LC_Q_BAD; cnt[M_BAD]++; break; }
-      if (hash_contains(s_hash, hmask, hshift, q)) { status = LC_Q_FOUND; cnt[M_FOUND]++; break; }
+      if (hhas(s_hash, HS, q)) { status = LC_Q_FOUND; cnt[M_FOUND]++; break; }
       const double p0 = __uint_as_float(r0.x), p1 = __uint_as_float(r0.y), p2 = __uint_as_float(r0.z);
       const double z = (s_T[6] * p0 + s_T[7] * p1) + s_T[8] * p2 + s_T[11];
       if (z <= 0.0) { status = LC_Q_DEPTH; cnt[M_DEPTH]++; break; }
       const double x = (s_T[0] * p0 + s_T[1] * p1) + s_T[2] * p2 + s_T[9];
       const double y = (s_T[3] * p0 + s_T[4] * p1) + s_T[5] * p2 + s_T[10];
+      if (pinhole && !a.dbg_uv) {
+        // conservative pre-test: |ua - u| <= 1e-6 |u| + tiny, margin 1e-2 px
+        const double rz = (double)__frcp_rn((float)z);
+        const double A = s_cam.fx * x, B = s_cam.fy * y;
+        const double e = 1e-6 * (fabs(A * rz) + fabs(B * rz)) + 1e-2;
+        const double ua = A * rz * (2.0 - z * rz) + s_cam.cx;   // one Newton step
+        const double va = B * rz * (2.0 - z * rz) + s_cam.cy;
+        if (ua < s_cam.min_x - e || ua >= s_cam.max_x + e || va < s_cam.min_y - e ||
+            va >= s_cam.max_y + e) {
+          status = LC_Q_BOUNDS; cnt[M_BOUNDS]++; break;
+        }
+      }
       lc_project(s_cam, x, y, z, u, v);
       if (!(u >= s_cam.min_x && u < s_cam.max_x && v >= s_cam.min_y && v < s_cam.max_y)) {
         status = LC_Q_BOUNDS; cnt[M_BOUNDS]++; break;
@@ -240,16 +269,22 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArg
       const double PO0 = p0 - s_Ow[0], PO1 = p1 - s_Ow[1], PO2 = p2 - s_Ow[2];
       const double d = sqrt((PO0 * PO0 + PO1 * PO1) + PO2 * PO2);
       const double dmax = __uint_as_float(r0.w);
-      if (d > 1.2 * dmax || d < 0.8 * (dmax / sLm1)) { status = LC_Q_DIST; cnt[M_DIST]++; break; }
+      bool dcull = d > 1.2 * dmax;
+      if (!dcull) {
+        const double t = dmax * c08;   // within a few ulp of 0.8 * (dmax / s_{L-1})
+        if (d < t * (1.0 - 1e-9)) dcull = true;
+        else if (!(d > t * (1.0 + 1e-9))) dcull = d < 0.8 * (dmax / sLm1);   // exact near the bound
+      }
+      if (dcull) { status = LC_Q_DIST; cnt[M_DIST]++; break; }
       const double n0 = __uint_as_float(r1.x), n1 = __uint_as_float(r1.y), n2 = __uint_as_float(r1.z);
       if ((PO0 * n0 + PO1 * n1) + PO2 * n2 < 0.5 * d) { status = LC_Q_ANGLE; cnt[M_ANGLE]++; break; }
       int lvl = L - 1;
       for (int n = 0; n < L; ++n)
         if (d * a.scale[n] >= dmax) { lvl = n; break; }
-      ent.q = q; ent.j = (int32_t)j; ent.lvl = lvl; ent.pad = 0; ent.u = u; ent.v = v;
+      ent.q = q; ent.jl = (uint32_t)(j - q0) | ((uint32_t)lvl << 27); ent.u = u; ent.v = v;
       return true;
     } while (0);
-    const int64_t qi = qoff + (j - lbeg);
+    const int64_t qi = qbase + (j - q0);
     if (a.dbg_best) a.dbg_best[qi] = status;
     if (a.dbg_uv) { a.dbg_uv[2 * qi] = u; a.dbg_uv[2 * qi + 1] = v; }
     if (a.dbg_ncand) a.dbg_ncand[qi] = 0;
@@ -258,91 +293,213 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArg
 
   auto enqueue = [&](bool surv, const QEnt& ent) {
     const unsigned m = __ballot_sync(0xffffffffu, surv);
-    if (surv) s_q[(tail + __popc(m & ((1u << lane) - 1u))) % QW] = ent;
+    if (surv) s_q[(tail + __popc(m & ltmask)) % QW] = ent;
     tail += __popc(m);
   };
 
-  // ---- phase B: 4-lane groups, one survivor per group, 8 per warp step --------
-  auto phase_b = [&](int navail) {
-    const int g = lane >> 2, t = lane & 3;
-    for (int s = 0; s < navail; s += 8) {
-      const bool act = s + g < navail;
-      QEnt e;
-      if (act) e = s_q[(head + s + g) % QW];
-      int ncand = 0;
-      uint32_t best = 0xFFFFFFFFu;  // (H << 16) | f
-      int second = 256;
-      if (act) {
-        const double u = e.u, v = e.v;
-        const int lvl = e.lvl;
-        const double r = (double)prm.th * a.scale[lvl];
-        const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + e.q);
-        const uint4 d0 = __ldg(rp + 2), d1 = __ldg(rp + 3);
-        const int cx0 = (int)fmax(0.0, floor(((u - r) - s_cam.min_x) * s_cam.cell_sx - 1e-6));
-        const int cx1 = (int)fmin((double)(cols - 1), floor(((u + r) - s_cam.min_x) * s_cam.cell_sx + 1e-6));
-        const int cy0 = (int)fmax(0.0, floor(((v - r) - s_cam.min_y) * s_cam.cell_sy - 1e-6));
-        const int cy1 = (int)fmin((double)(rows - 1), floor(((v + r) - s_cam.min_y) * s_cam.cell_sy + 1e-6));
-        const int lo = lvl - 1;
-        for (int cy = cy0; cy <= cy1; ++cy) {
-          const int pe = s_cell[cy * cols + cx1 + 1];
-          for (int p = s_cell[cy * cols + cx0] + t; p < pe; p += 4) {
-            const uint32_t meta = s_meta[p];
-            const int oct = (int)((meta >> 16) & 0xFFu);
-            if (oct < lo || oct > lvl) continue;
-            if (MODE == 1 && (meta & 0x80000000u)) continue;
-            const float2 fuv = s_uv[p];
-            const double du = fabs((double)fuv.x - u), dv = fabs((double)fuv.y - v);
-            if (!(du < r && dv < r)) continue;
-            ++ncand;
-            const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
-            const int h = popc_desc(d0, d1, __ldg(dp), __ldg(dp + 1));
-            const uint32_t key = ((uint32_t)h << 16) | (meta & 0xFFFFu);
-            if (key < best) {
-              if (best != 0xFFFFFFFFu) second = min(second, (int)(best >> 16));
-              best = key;
-            } else {
-              second = min(second, h);
-            }
-          }
+  // ---- phase B: n (<= 32) queued survivors, one per lane -----------------------
+  // Serial window scan of one survivor (fallback when its window has more than RMAX
+  // cell rows or more than CPL candidates): same arithmetic, evaluated in place.
+  auto scan_serial = [&](double u, double v, double r, int lvl, const uint4& d0, const uint4& d1,
+                         uint32_t& best, int& second) {
+    const float fu = (float)u, fv = (float)v, fr = (float)r;
+    const int cx0 = max(0, (int)floorf((fu - fr - 0.01f - fminx) * fsx));
+    const int cx1 = min(cols - 1, (int)floorf((fu + fr + 0.01f - fminx) * fsx));
+    const int cy0 = max(0, (int)floorf((fv - fr - 0.01f - fminy) * fsy));
+    const int cy1 = min(rows - 1, (int)floorf((fv + fr + 0.01f - fminy) * fsy));
+    for (int cy = cy0; cy <= cy1; ++cy) {
+      const int pe = s_cell[cy * cols + cx1 + 1];
+      for (int p = s_cell[cy * cols + cx0]; p < pe; ++p) {
+        const uint32_t meta = s_meta[p];
+        const int oct = (int)((meta >> 16) & 0xFFu);
+        if (oct < lvl - 1 || oct > lvl) continue;
+        if (MODE == 1 && (meta & 0x80000000u)) continue;
+        const float2 fuv = s_uv[p];
+        if (!(fabs((double)fuv.x - u) < r && fabs((double)fuv.y - v) < r)) continue;
+        const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
+        const int h = popc_desc(d0, d1, __ldg(dp), __ldg(dp + 1));
+        const uint32_t key = ((uint32_t)h << 16) | (meta & 0xFFFFu);
+        if (key < best) {
+          if (best != 0xFFFFFFFFu) second = min(second, (int)(best >> 16));
+          best = key;
+        } else {
+          second = min(second, h);
         }
-      }
-      // group reduction: best key, second H (exact: keys are unique per feature)
-      uint32_t gbest = best;
-      gbest = min(gbest, __shfl_xor_sync(0xffffffffu, gbest, 1, 4));
-      gbest = min(gbest, __shfl_xor_sync(0xffffffffu, gbest, 2, 4));
-      int sec = second;
-      if (best != gbest && best != 0xFFFFFFFFu) sec = min(sec, (int)(best >> 16));
-      sec = min(sec, __shfl_xor_sync(0xffffffffu, sec, 1, 4));
-      sec = min(sec, __shfl_xor_sync(0xffffffffu, sec, 2, 4));
-      ncand += __shfl_xor_sync(0xffffffffu, ncand, 1, 4);
-      ncand += __shfl_xor_sync(0xffffffffu, ncand, 2, 4);
-      if (act && t == 0) {
-        cnt[M_CAND] += ncand;
-        do {
-          if (ncand == 0) { cnt[M_NOCAND]++; break; }
-          const int hb = (int)(gbest >> 16);
-          if (hb > prm.max_hamming) { cnt[M_OVERTH]++; break; }
-          if (prm.ratio_den > 0 && (long long)prm.ratio_den * hb > (long long)prm.ratio_num * sec) {
-            cnt[M_RATIO]++; break;
-          }
-          cnt[M_PROP]++;
-          atomicMin(&win[gbest & 0xFFFFu], ((unsigned long long)hb << 32) | (unsigned int)e.q);
-        } while (0);
-        const int64_t qi = qoff + ((int64_t)e.j - lbeg);
-        if (a.dbg_best) {
-          long long val;
-          if (ncand == 0) val = (256LL << 48) | (256LL << 32) | 0xFFFFFFFFLL;
-          else val = ((long long)(gbest >> 16) << 48) | ((long long)sec << 32) | (long long)(gbest & 0xFFFFu);
-          a.dbg_best[qi] = val;
-        }
-        if (a.dbg_uv) { a.dbg_uv[2 * qi] = e.u; a.dbg_uv[2 * qi + 1] = e.v; }
-        if (a.dbg_ncand) a.dbg_ncand[qi] = ncand;
       }
     }
-    head += navail;
   };
 
-  const int64_t q0 = a.blk_q0[blockIdx.x], q1 = a.blk_q1[blockIdx.x];
+  auto phase_b = [&](int n) {
+    const bool act = lane < n;
+    const QEnt* my = s_q + (head + lane) % QW;
+    const QEnt e = act ? *my : QEnt{0, 0u, 0.0, 0.0};
+    const int lvl = (int)(e.jl >> 27);
+    const double r = (double)prm.th * a.scale[lvl];
+    uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
+    if (act) {
+      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + e.q);
+      d0 = __ldg(rp + 2); d1 = __ldg(rp + 3);
+    }
+    // (0) this lane's window rows -> (start, length) list; work size = sum of lengths
+    int nrow = 0, nfeat = 0;
+    if (act) {
+      const float fu = (float)e.u, fv = (float)e.v, fr = (float)r;
+      // conservative (0.01 px) superset of the exact square window
+      const int cx0 = max(0, (int)floorf((fu - fr - 0.01f - fminx) * fsx));
+      const int cx1 = min(cols - 1, (int)floorf((fu + fr + 0.01f - fminx) * fsx));
+      const int cy0 = max(0, (int)floorf((fv - fr - 0.01f - fminy) * fsy));
+      const int cy1 = min(rows - 1, (int)floorf((fv + fr + 0.01f - fminy) * fsy));
+      nrow = cy1 - cy0 + 1;
+      if (nrow <= RMAX) {
+        for (int i = 0; i < nrow; ++i) {
+          const int cy = cy0 + i;
+          const int pb = s_cell[cy * cols + cx0], pe = s_cell[cy * cols + cx1 + 1];
+          s_rows[lane * RMAX + i] = (uint32_t)pb | ((uint32_t)(pe - pb) << 16);
+          nfeat += pe - pb;
+        }
+      }
+    }
+    const bool serial = act && nrow > RMAX;
+    if (serial) nfeat = 0;
+    s_nc[lane] = 0;
+    __syncwarp();
+    // (1) flattened scan of all (survivor, feature) pairs of the warp
+    int incl = nfeat;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int excl = incl - nfeat;
+    for (int c0 = 0; c0 < total; c0 += 32) {
+      const int c = c0 + lane;
+      int own = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int ex = __shfl_sync(0xffffffffu, excl, own + step);
+        if (c < total && ex <= c) own += step;
+      }
+      const int oex = __shfl_sync(0xffffffffu, excl, own);
+      if (c < total) {
+        int t = c - oex, ri = 0;
+        uint32_t rw = s_rows[own * RMAX];
+        while (t >= (int)(rw >> 16)) { t -= (int)(rw >> 16); rw = s_rows[own * RMAX + (++ri)]; }
+        const int p = (int)(rw & 0xFFFFu) + t;
+        const QEnt oe = s_q[(head + own) % QW];
+        const int olvl = (int)(oe.jl >> 27);
+        const uint32_t meta = s_meta[p];
+        const int oct = (int)((meta >> 16) & 0xFFu);
+        bool cand = oct >= olvl - 1 && oct <= olvl;
+        if (MODE == 1) cand = cand && !(meta & 0x80000000u);
+        if (cand) {
+          const double orr = (double)prm.th * a.scale[olvl];
+          const float2 fuv = s_uv[p];
+          cand = fabs((double)fuv.x - oe.u) < orr && fabs((double)fuv.y - oe.v) < orr;
+        }
+        if (cand) {
+          const int slot = atomicAdd(&s_nc[own], 1);
+          if (slot < CPL) s_cand[own * CPL + slot] = (uint16_t)p;
+        }
+      }
+    }
+    __syncwarp();
+    // (2) Hamming of all slotted candidates, warp-wide
+    const int nc = s_nc[lane];
+    const bool over = act && !serial && nc > CPL;
+    const int ns = (act && !serial && !over) ? nc : 0;
+    incl = ns;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int tot2 = __shfl_sync(0xffffffffu, incl, 31);
+    const int ex2 = incl - ns;
+    for (int c0 = 0; c0 < tot2; c0 += 32) {
+      const int c = c0 + lane;
+      int own = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int ex = __shfl_sync(0xffffffffu, ex2, own + step);
+        if (c < tot2 && ex <= c) own += step;
+      }
+      const uint32_t w0 = __shfl_sync(0xffffffffu, d0.x, own), w1 = __shfl_sync(0xffffffffu, d0.y, own);
+      const uint32_t w2 = __shfl_sync(0xffffffffu, d0.z, own), w3 = __shfl_sync(0xffffffffu, d0.w, own);
+      const uint32_t w4 = __shfl_sync(0xffffffffu, d1.x, own), w5 = __shfl_sync(0xffffffffu, d1.y, own);
+      const uint32_t w6 = __shfl_sync(0xffffffffu, d1.z, own), w7 = __shfl_sync(0xffffffffu, d1.w, own);
+      const int oex = __shfl_sync(0xffffffffu, ex2, own);
+      if (c < tot2) {
+        const int slot = own * CPL + (c - oex);
+        const int p = s_cand[slot];
+        const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
+        const uint4 b0 = __ldg(dp), b1 = __ldg(dp + 1);
+        const int h = __popc(w0 ^ b0.x) + __popc(w1 ^ b0.y) + __popc(w2 ^ b0.z) + __popc(w3 ^ b0.w) +
+                      __popc(w4 ^ b1.x) + __popc(w5 ^ b1.y) + __popc(w6 ^ b1.z) + __popc(w7 ^ b1.w);
+        s_key[slot] = ((uint32_t)h << 16) | (s_meta[p] & 0xFFFFu);
+      }
+    }
+    __syncwarp();
+    // (3) per-lane reduction over its own keys (or the serial fallback)
+    if (act) {
+      uint32_t best = 0xFFFFFFFFu;  // (H << 16) | f
+      int second = 256;
+      int ncand = nc;
+      if (serial || over) {
+        scan_serial(e.u, e.v, r, lvl, d0, d1, best, second);
+        if (serial) {  // count the candidates of the serial scan
+          ncand = 0;
+          const float fu = (float)e.u, fv = (float)e.v, fr = (float)r;
+          const int cx0 = max(0, (int)floorf((fu - fr - 0.01f - fminx) * fsx));
+          const int cx1 = min(cols - 1, (int)floorf((fu + fr + 0.01f - fminx) * fsx));
+          const int cy0 = max(0, (int)floorf((fv - fr - 0.01f - fminy) * fsy));
+          const int cy1 = min(rows - 1, (int)floorf((fv + fr + 0.01f - fminy) * fsy));
+          for (int cy = cy0; cy <= cy1; ++cy)
+            for (int p = s_cell[cy * cols + cx0]; p < s_cell[cy * cols + cx1 + 1]; ++p) {
+              const uint32_t meta = s_meta[p];
+              const int oct = (int)((meta >> 16) & 0xFFu);
+              if (oct < lvl - 1 || oct > lvl) continue;
+              if (MODE == 1 && (meta & 0x80000000u)) continue;
+              const float2 fuv = s_uv[p];
+              if (fabs((double)fuv.x - e.u) < r && fabs((double)fuv.y - e.v) < r) ++ncand;
+            }
+        }
+      } else {
+        for (int i = 0; i < ns; ++i) {
+          const uint32_t key = s_key[lane * CPL + i];
+          if (key < best) {
+            if (best != 0xFFFFFFFFu) second = min(second, (int)(best >> 16));
+            best = key;
+          } else {
+            second = min(second, (int)(key >> 16));
+          }
+        }
+      }
+      cnt[M_CAND] += ncand;
+      do {
+        if (ncand == 0) { cnt[M_NOCAND]++; break; }
+        const int hb = (int)(best >> 16);
+        if (hb > prm.max_hamming) { cnt[M_OVERTH]++; break; }
+        if (prm.ratio_den > 0 && (long long)prm.ratio_den * hb > (long long)prm.ratio_num * second) {
+          cnt[M_RATIO]++; break;
+        }
+        cnt[M_PROP]++;
+        atomicMin(&win[best & 0xFFFFu], ((unsigned long long)hb << 32) | (unsigned int)e.q);
+      } while (0);
+      const int64_t qi = qbase + (int64_t)(e.jl & 0x07FFFFFFu);
+      if (a.dbg_best) {
+        long long val;
+        if (ncand == 0) val = (256LL << 48) | (256LL << 32) | 0xFFFFFFFFLL;
+        else val = ((long long)(best >> 16) << 48) | ((long long)second << 32) | (long long)(best & 0xFFFFu);
+        a.dbg_best[qi] = val;
+      }
+      if (a.dbg_uv) { a.dbg_uv[2 * qi] = e.u; a.dbg_uv[2 * qi + 1] = e.v; }
+      if (a.dbg_ncand) a.dbg_ncand[qi] = ncand;
+    }
+    __syncwarp();
+    head += n;
+  };
+
   while (true) {
     int bidx = 0;
     if (lane == 0) bidx = atomicAdd(&s_next, 1);
@@ -375,7 +532,6 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArg
     while (tail - head >= 32) {  // keeps the ring below 32 + 64 <= QW entries
       if (!staged) { mbar_wait(&s_bar, 0); staged = true; }
       phase_b(32);
-      __syncwarp();
     }
   }
   if (tail > head) {
@@ -540,30 +696,44 @@ __global__ void k_fuse_victims(int n_mp, const unsigned long long* __restrict__ 
 }
 
 // Apply pass 1: find the keyframes whose slots change (a victim to redirect or a
-// winner on an empty window slot) -> compact list.
+// winner on an empty window slot) -> compact list. One warp per keyframe, 16-B loads,
+// no shared memory (the victim bitmap stays L1-resident).
 __global__ void __launch_bounds__(LC_NTHREADS) k_apply_mark(
-    uint32_t epoch, const int32_t* __restrict__ kf_fbeg, const uint32_t* __restrict__ kf_win_ep,
+    int n_kf, uint32_t epoch, const int32_t* __restrict__ kf_fbeg, const uint32_t* __restrict__ kf_win_ep,
     const int32_t* __restrict__ kf_win_pos, const int64_t* __restrict__ woff_of_pos,
     const unsigned long long* __restrict__ winner, const uint32_t* __restrict__ vbits,
     const int32_t* __restrict__ feat_mp, int32_t* __restrict__ dirty_list) {
-  const int k = blockIdx.x;
-  const int fb = kf_fbeg[k], F = kf_fbeg[k + 1] - fb;
-  const int wpos = (kf_win_ep[k] == epoch) ? kf_win_pos[k] : -1;
-  const int64_t woff = wpos >= 0 ? woff_of_pos[wpos] : 0;
-  int dirty = 0;
-  for (int f = threadIdx.x; f < F; f += blockDim.x) {
-    const int32_t m = feat_mp[fb + f];
-    if (m >= 0) dirty |= (vbits[m >> 5] >> (m & 31)) & 1u;
-    else if (wpos >= 0) dirty |= winner[woff + f] != NONE;
-  }
-  if (__syncthreads_or(dirty) && threadIdx.x == 0) {
-    const int i = atomicAdd(&dirty_list[0], 1);
-    dirty_list[1 + i] = k;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int k = gw; k < n_kf; k += nw) {
+    const int fb = kf_fbeg[k], fe = kf_fbeg[k + 1];
+    const int wpos = (kf_win_ep[k] == epoch) ? kf_win_pos[k] : -1;
+    const int64_t wshift = wpos >= 0 ? woff_of_pos[wpos] - fb : 0;   // winner index = f + wshift
+    int dirty = 0;
+    // head (to a 16-B boundary), vector body, tail
+    const int vb = min(fe, (fb + 3) & ~3), ve = max(vb, fe & ~3);
+    auto test = [&](int f, int32_t m) {
+      if (m >= 0) dirty |= (__ldg(vbits + (m >> 5)) >> (m & 31)) & 1u;
+      else if (wpos >= 0) dirty |= winner[f + wshift] != NONE;
+    };
+    for (int f = fb + lane; f < vb; f += 32) test(f, feat_mp[f]);
+    for (int f = vb + 4 * lane; f < ve; f += 128) {
+      const int4 m4 = __ldg(reinterpret_cast<const int4*>(feat_mp + f));
+      test(f, m4.x); test(f + 1, m4.y); test(f + 2, m4.z); test(f + 3, m4.w);
+    }
+    for (int f = ve + lane; f < fe; f += 32) test(f, feat_mp[f]);
+    if (__any_sync(0xffffffffu, dirty) && lane == 0) {
+      const int i = atomicAdd(&dirty_list[0], 1);
+      dirty_list[1 + i] = k;
+    }
   }
 }
 
 // Apply pass 2 (dirty keyframes only): redirect victims, add winners to empty window
-// slots, per-keyframe duplicate cleanup by least (priority, f) (reading A22), n_obs deltas.
+// slots, per-keyframe duplicate cleanup by least (priority, f) (reading A22), n_obs
+// deltas. Only the NEW map points of changed slots are hashed: an unchanged slot can
+// only collide with a changed one (the input holds no map point twice in a keyframe).
 enum { A_REWIRED, A_DUP, A_ADDED, A_N };
 __device__ __constant__ int kApplySlot[A_N] = {LC_COUNT_REWIRED, LC_COUNT_DUP_CLEARED,
                                                LC_COUNT_ADDED};
@@ -578,21 +748,20 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t cnt[A_N] = {0, 0, 0};
   const int nd = dirty_list[0];
+  const uint32_t HS = (uint32_t)hash_size;
+  int32_t* s_key = (int32_t*)smem;
+  uint32_t* s_val = (uint32_t*)(s_key + hash_size);
+  int32_t* s_new = (int32_t*)(s_val + hash_size);
   for (int di = blockIdx.x; di < nd; di += gridDim.x) {
     const int k = dirty_list[1 + di];
     const int fb = kf_fbeg[k], F = kf_fbeg[k + 1] - fb;
     const int wpos = (kf_win_ep[k] == epoch) ? kf_win_pos[k] : -1;
     const int64_t woff = wpos >= 0 ? woff_of_pos[wpos] : 0;
-    int32_t* s_new = (int32_t*)smem;
-    int32_t* s_old = s_new + F;
-    int32_t* s_key = s_old + F;
-    uint32_t* s_val = (uint32_t*)(s_key + hash_size);
-    uint8_t* s_pr = (uint8_t*)(s_val + hash_size);
-    const int hmask = hash_size - 1;
-    const int hshift = 32 - __ffs(hash_size) + 1;
-    for (int i = threadIdx.x; i < hash_size; i += blockDim.x) { s_key[i] = -1; s_val[i] = 0xFFFFFFFFu; }
+    uint8_t* s_pr = (uint8_t*)(s_new + F);
+    for (int i = threadIdx.x; i < (int)HS; i += blockDim.x) { s_key[i] = -1; s_val[i] = 0xFFFFFFFFu; }
+    __syncthreads();
     for (int f = threadIdx.x; f < F; f += blockDim.x) {
-      int32_t m = feat_mp[fb + f];
+      const int32_t m = feat_mp[fb + f];
       int32_t nv = m;
       uint8_t pr = 0;
       if (m >= 0) {
@@ -600,39 +769,46 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
           nv = (int32_t)(victim[m] & 0xFFFFFFFFull); pr = 2; cnt[A_REWIRED]++;
         }
       } else if (wpos >= 0) {
-        unsigned long long w = winner[woff + f];
+        const unsigned long long w = winner[woff + f];
         if (w != NONE) { nv = (int32_t)(w & 0xFFFFFFFFull); pr = 1; }
       }
-      s_old[f] = m;
       s_new[f] = nv;
       s_pr[f] = pr;
+      if (pr) {  // hash the new map point of every changed slot
+        uint32_t h = hslot(nv, HS);
+        while (true) {
+          const int32_t prev = atomicCAS(&s_key[h], -1, nv);
+          if (prev == -1 || prev == nv) break;
+          h = (h + 1 == HS) ? 0 : h + 1;
+        }
+      }
     }
     __syncthreads();
+    // every slot holding a hashed map point competes for it with key (priority, f)
     for (int f = threadIdx.x; f < F; f += blockDim.x) {
-      int32_t nv = s_new[f];
+      const int32_t nv = s_new[f];
       if (nv < 0) continue;
-      uint32_t h = hash_slot(nv, hshift);
-      while (true) {
-        int32_t prev = atomicCAS(&s_key[h], -1, nv);
-        if (prev == -1 || prev == nv) break;
-        h = (h + 1) & hmask;
-      }
-      atomicMin(&s_val[h], ((uint32_t)s_pr[f] << 16) | (uint32_t)f);
+      uint32_t h = hslot(nv, HS);
+      while (s_key[h] != -1 && s_key[h] != nv) h = (h + 1 == HS) ? 0 : h + 1;
+      if (s_key[h] == nv) atomicMin(&s_val[h], ((uint32_t)s_pr[f] << 16) | (uint32_t)f);
     }
     __syncthreads();
     for (int f = threadIdx.x; f < F; f += blockDim.x) {
       int32_t nv = s_new[f];
-      const int32_t m = s_old[f];
+      const uint8_t pr = s_pr[f];
       if (nv >= 0) {
-        uint32_t h = hash_slot(nv, hshift);
-        while (s_key[h] != nv) h = (h + 1) & hmask;
-        if (s_val[h] != (((uint32_t)s_pr[f] << 16) | (uint32_t)f)) { nv = -1; cnt[A_DUP]++; }
-        else if (s_pr[f] == 1) cnt[A_ADDED]++;
+        uint32_t h = hslot(nv, HS);
+        while (s_key[h] != -1 && s_key[h] != nv) h = (h + 1 == HS) ? 0 : h + 1;
+        if (s_key[h] == nv && s_val[h] != (((uint32_t)pr << 16) | (uint32_t)f)) { nv = -1; cnt[A_DUP]++; }
+        else if (pr == 1) cnt[A_ADDED]++;
       }
-      if (nv != m) {
-        feat_mp[fb + f] = nv;
-        if (m >= 0) atomicSub(&nobs[m], 1);
-        if (nv >= 0) atomicAdd(&nobs[nv], 1);
+      if (pr != 0 || nv != s_new[f]) {
+        const int32_t m = feat_mp[fb + f];
+        if (nv != m) {
+          feat_mp[fb + f] = nv;
+          if (m >= 0) atomicSub(&nobs[m], 1);
+          if (nv >= 0) atomicAdd(&nobs[nv], 1);
+        }
       }
     }
     __syncthreads();
@@ -647,11 +823,6 @@ int grid_for(int64_t n) {
   return (int)b;
 }
 
-int pow2_at_least(int x) {
-  int h = 64;
-  while (h < x) h <<= 1;
-  return h;
-}
 
 }  // namespace
 
@@ -660,7 +831,8 @@ cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a_in, int n_block
   if (n_blocks <= 0) return cudaSuccess;
   MatchArgs a = a_in;
   const int Fm = F_max > 0 ? F_max : 1;
-  a.hash_size = pow2_at_least(2 * Fm);
+  // open-addressing table of >= 1.5 F slots (keys: the <= F associated map points)
+  a.hash_size = ((Fm + Fm / 2 + 1) + 31) & ~31;
   auto r16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
   size_t off = r16((size_t)a.Gs * 2);
   a.off_uv = (int)off;
@@ -670,7 +842,9 @@ cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a_in, int n_block
   a.off_hash = (int)off;
   off += r16((size_t)a.hash_size * 4);
   a.off_queue = (int)off;
-  off += (size_t)NWARP * QW * sizeof(QEnt);
+  a.warp_bytes = (int)r16(QW * sizeof(QEnt) + 32 * (CPL > RMAX ? CPL : RMAX) * sizeof(uint32_t) +
+                          32 * CPL * sizeof(uint16_t) + 32 * sizeof(int));
+  off += (size_t)NWARP * a.warp_bytes;
   const size_t smem = off;
   cudaError_t e;
   if (mode == 0) {
@@ -723,10 +897,12 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
     c->launches++;
   }
   if (st.n_kf > 0) {
-    k_apply_mark<<<st.n_kf, LC_NTHREADS, 0, s>>>(c->epoch, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos,
-                                                d_woff, winner, st.mp_vbits, st.feat_mp, st.kf_dirty);
-    int H = pow2_at_least(2 * (st.max_F > 0 ? st.max_F : 1));
-    size_t smem = (size_t)st.max_F * 9 + (size_t)H * 8;
+    k_apply_mark<<<std::min((st.n_kf + NWARP - 1) / NWARP, 148 * 8), LC_NTHREADS, 0, s>>>(
+        st.n_kf, c->epoch, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos, d_woff, winner, st.mp_vbits,
+        st.feat_mp, st.kf_dirty);
+    const int Fm = st.max_F > 0 ? st.max_F : 1;
+    const int H = ((Fm + Fm / 2 + 1) + 31) & ~31;
+    size_t smem = (size_t)H * 8 + (size_t)Fm * 5 + 16;
     smem = (smem + 15) & ~(size_t)15;
     cudaError_t e = cudaFuncSetAttribute(k_apply_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

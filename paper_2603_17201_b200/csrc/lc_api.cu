@@ -569,7 +569,7 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
       call.arg(window_kf, n_window, &d_win);
       call.arg((const double*)S_cw_corr, 13, &d_S);
       call.commit();
-      double* scr = (double*)call.scratch(sizeof(double) * 39 * (size_t)n_window);
+      double* scr = (double*)call.scratch(sizeof(double) * correct_window_scratch_stride() * (size_t)n_window);
       CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
       {
         Prof pr(c, LC_PROF_CORRECT_WINDOW, call.s);
@@ -577,10 +577,10 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
       }
       if (out_S_corr) {
         if (is_device_ptr(c, out_S_corr)) {
-          CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr, sizeof(double) * 39,
+          CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr + 28, sizeof(double) * correct_window_scratch_stride(),
                                sizeof(lc_sim3), n_window, cudaMemcpyDeviceToDevice, call.s));
         } else {
-          CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr, sizeof(double) * 39,
+          CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr + 28, sizeof(double) * correct_window_scratch_stride(),
                                sizeof(lc_sim3), n_window, cudaMemcpyDefault, call.s));
         }
       }
@@ -589,7 +589,7 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
     } else {
       REQUIRE(S_opt, LC_EINVAL, "null S_opt");
       const double* d_opt = call.in((const double*)S_opt, 13 * (size_t)st.n_kf);
-      double* scr = (double*)call.scratch(sizeof(double) * 26 * (size_t)std::max(st.n_kf, 1));
+      double* scr = (double*)call.scratch(sizeof(double) * correct_all_scratch_stride() * (size_t)std::max(st.n_kf, 1));
       CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
       {
         Prof pr(c, LC_PROF_CORRECT_ALL, call.s);

@@ -121,8 +121,9 @@ struct MatchArgs {
   int64_t* dbg_best;
   double* dbg_uv;
   int32_t* dbg_ncand;
-  int32_t hash_size;           // power of 2
+  int32_t hash_size;           // already-found table slots (>= 1.5 F_max)
   int32_t off_uv, off_meta, off_hash, off_queue;   // dynamic smem carve (bytes)
+  int32_t warp_bytes;                              // per-warp ring + candidate slots
   // resolve (orientation + actions / SBP output tables)
   const float* feat_angle;
   const uint32_t* loop_ep;
@@ -262,6 +263,8 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
 cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t* d_window,
                                   const double* d_Scw, double* d_scr, unsigned long long* counts,
                                   cudaStream_t s);
+int correct_window_scratch_stride();
+int correct_all_scratch_stride();
 cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
                                unsigned long long* counts, cudaStream_t s);
 cudaError_t launch_fill_u64(lc_ctx* c, unsigned long long* p, int64_t n, unsigned long long v,
