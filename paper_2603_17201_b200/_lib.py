@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblc.so")
+LIB_PATH = os.environ.get("LC_LIB_PATH") or os.path.join(PKG, "liblc.so")
 
 LC_OK, LC_EINVAL, LC_ESTATE, LC_ECUDA, LC_ENOMEM, LC_ERANGE, LC_ECAPACITY = 0, -1, -2, -3, -4, -5, -6
 STATUS_NAMES = {0: "LC_OK", -1: "LC_EINVAL", -2: "LC_ESTATE", -3: "LC_ECUDA", -4: "LC_ENOMEM",

@@ -8,17 +8,19 @@
 // applies two precomputed Sim3s in fp64 (loaded as 16-B vectors, L1-resident when
 // consecutive map points share their keyframe, as in creation order).
 //
-// WINDOW = 2 kernels (+2 memsets): [owner election || S^corr per window position]
-// then [point re-anchoring || pose write-back]; ALL = 2 kernels.
+// WINDOW = 3 kernels (+2 memsets): S^corr per window position, owner election, then
+// [point re-anchoring || pose write-back]; ALL = 2 kernels.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "lc_internal.cuh"
 
 namespace {
 
 // WINDOW scratch per window position i (16-B aligned rows of WSTR doubles):
-//   [0, 13) T_iw^old  |  [14, 27) inverse(S_i^corr)  |  [28, 41) S_i^corr
-constexpr int WSTR = 42;
+//   [0, 13) T_iw^old | [14, 27) inverse(S_i^corr) | [28, 41) S_i^corr | [42, 55) SE3(S_i^corr)
+constexpr int WSTR = 56;
 // ALL scratch per keyframe: [0, 13) S^pre | [14, 27) inverse(S^opt)
 constexpr int ASTR = 28;
 constexpr int32_t OWNER_NONE = 0x7F7F7F7F;  // memset byte pattern 0x7F
@@ -40,42 +42,67 @@ __device__ __forceinline__ void warp_count(uint32_t n, unsigned long long* dst) 
   if ((threadIdx.x & 31) == 0 && n) atomicAdd(dst, (unsigned long long)n);
 }
 
-// Block i = window position i: thread 0 computes S_i^corr = (T_iw * inverse(T_cw)) *
-// S_cw^corr from the OLD poses (S_c^corr = S_cw^corr) into scratch; all threads elect
-// owner(m) = min window position observing the non-bad map point m (atomicMin).
-__global__ void __launch_bounds__(LC_NTHREADS) k_win_a(
-    int cur_pos, const int32_t* __restrict__ window, const double* __restrict__ kf_pose,
-    const double* __restrict__ Scw, const int32_t* __restrict__ kf_fbeg,
-    const int32_t* __restrict__ feat_mp, const uint8_t* __restrict__ mp_flags,
-    int32_t* __restrict__ owner, double* __restrict__ scr, double* __restrict__ kf_S_corr,
-    int32_t* __restrict__ kf_in_win) {
-  const int i = blockIdx.x;
+// Thread i = window position i: S_i^corr = (T_iw * inverse(T_cw)) * S_cw^corr from the
+// OLD poses (S_c^corr = S_cw^corr) into scratch, with T_iw^old and inverse(S_i^corr).
+__global__ void k_win_sim3(int n_w, int cur_pos, const int32_t* __restrict__ window,
+                           const double* __restrict__ kf_pose, const double* __restrict__ Scw,
+                           double* __restrict__ scr, double* __restrict__ kf_S_corr,
+                           int32_t* __restrict__ kf_in_win) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_w) return;
   const int k = window[i];
-  if (threadIdx.x == 0) {
-    double T[13], S[13], Si[13];
-    for (int j = 0; j < 13; ++j) T[j] = kf_pose[13 * (size_t)k + j];
-    if (i == cur_pos) {
-      for (int j = 0; j < 13; ++j) S[j] = Scw[j];
-    } else {
-      double Tc[13], Tci[13], Sic[13];
-      const int c = window[cur_pos];
-      for (int j = 0; j < 13; ++j) Tc[j] = kf_pose[13 * (size_t)c + j];
-      lc_sim3_inverse(Tc, Tci);
-      lc_sim3_compose(T, Tci, Sic);   // S_ic = T_iw * inverse(T_cw)
-      lc_sim3_compose(Sic, Scw, S);   // S_iw^corr = S_ic * S_cw^corr
-    }
-    lc_sim3_inverse(S, Si);
-    double* o = scr + (size_t)WSTR * i;
-    for (int j = 0; j < 13; ++j) { o[j] = T[j]; o[14 + j] = Si[j]; o[28 + j] = S[j]; }
-    o[13] = o[27] = o[41] = 0.0;
-    for (int j = 0; j < 13; ++j) kf_S_corr[13 * (size_t)k + j] = S[j];
-    kf_in_win[k] = 1;
+  double T[13], S[13], Si[13];
+  for (int j = 0; j < 13; ++j) T[j] = kf_pose[13 * (size_t)k + j];
+  if (i == cur_pos) {
+    for (int j = 0; j < 13; ++j) S[j] = Scw[j];
+  } else {
+    double Tc[13], Tci[13], Sic[13];
+    const int c = window[cur_pos];
+    for (int j = 0; j < 13; ++j) Tc[j] = kf_pose[13 * (size_t)c + j];
+    lc_sim3_inverse(Tc, Tci);
+    lc_sim3_compose(T, Tci, Sic);   // S_ic = T_iw * inverse(T_cw)
+    lc_sim3_compose(Sic, Scw, S);   // S_iw^corr = S_ic * S_cw^corr
   }
-  const int f0 = kf_fbeg[k], f1 = kf_fbeg[k + 1];
-  for (int f = f0 + threadIdx.x; f < f1; f += blockDim.x) {
-    const int m = feat_mp[f];
-    if (m < 0 || (mp_flags[m] & 1u)) continue;
-    atomicMin(&owner[m], i);
+  lc_sim3_inverse(S, Si);
+  double* o = scr + (size_t)WSTR * i;
+  for (int j = 0; j < 13; ++j) { o[j] = T[j]; o[14 + j] = Si[j]; o[28 + j] = S[j]; }
+  lc_sim3_se3(S, T);
+  for (int j = 0; j < 13; ++j) o[42 + j] = T[j];
+  o[13] = o[27] = o[41] = o[55] = 0.0;
+  for (int j = 0; j < 13; ++j) kf_S_corr[13 * (size_t)k + j] = S[j];
+  kf_in_win[k] = 1;
+}
+
+// Warp per window position: owner(m) = min window position observing the non-bad map
+// point m (atomicMin), 16-B association loads, 4 slots per lane in flight.
+__global__ void __launch_bounds__(LC_NTHREADS) k_win_mark(
+    int n_w, const int32_t* __restrict__ window, const int32_t* __restrict__ kf_fbeg,
+    const int32_t* __restrict__ feat_mp, const uint8_t* __restrict__ mp_flags,
+    int32_t* __restrict__ owner) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = gw; i < n_w; i += nw) {
+    const int k = window[i];
+    const int fb = kf_fbeg[k], fe = kf_fbeg[k + 1];
+    const int vb = min(fe, (fb + 3) & ~3), ve = max(vb, fe & ~3);
+    for (int f = fb + lane; f < vb; f += 32) {
+      const int m = feat_mp[f];
+      if (m >= 0 && !(__ldg(mp_flags + m) & 1u)) atomicMin(&owner[m], i);
+    }
+    for (int f = vb + 4 * lane; f < ve; f += 128) {
+      const int4 m4 = __ldg(reinterpret_cast<const int4*>(feat_mp + f));
+      const uint8_t g0 = m4.x >= 0 ? __ldg(mp_flags + m4.x) : 1, g1 = m4.y >= 0 ? __ldg(mp_flags + m4.y) : 1;
+      const uint8_t g2 = m4.z >= 0 ? __ldg(mp_flags + m4.z) : 1, g3 = m4.w >= 0 ? __ldg(mp_flags + m4.w) : 1;
+      if (!(g0 & 1u)) atomicMin(&owner[m4.x], i);
+      if (!(g1 & 1u)) atomicMin(&owner[m4.y], i);
+      if (!(g2 & 1u)) atomicMin(&owner[m4.z], i);
+      if (!(g3 & 1u)) atomicMin(&owner[m4.w], i);
+    }
+    for (int f = ve + lane; f < fe; f += 32) {
+      const int m = feat_mp[f];
+      if (m >= 0 && !(__ldg(mp_flags + m) & 1u)) atomicMin(&owner[m], i);
+    }
   }
 }
 
@@ -116,8 +143,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_win_b(
   } else {
     const int i = (blockIdx.x - nb_mp) * blockDim.x + threadIdx.x;
     if (i < n_w) {
-      double T[13];
-      lc_sim3_se3(scr + (size_t)WSTR * i + 28, T);
+      const double* T = scr + (size_t)WSTR * i + 42;
       for (int j = 0; j < 13; ++j) kf_pose[13 * (size_t)window[i] + j] = T[j];
       n = 1;
     }
@@ -199,13 +225,15 @@ cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t
   if (st.n_mp > 0 && (e = cudaMemsetAsync(st.mp_owner, 0x7F, sizeof(int32_t) * st.n_mp, s)) != cudaSuccess)
     return e;
   if ((e = cudaMemsetAsync(st.kf_in_win, 0, sizeof(int32_t) * st.n_kf, s)) != cudaSuccess) return e;
-  k_win_a<<<n_w, LC_NTHREADS, 0, s>>>(cur_pos, d_window, st.kf_pose, d_Scw, st.kf_fbeg, st.feat_mp,
-                                      st.mp_flags, st.mp_owner, d_scr, st.kf_S_corr, st.kf_in_win);
+  k_win_sim3<<<(n_w + 63) / 64, 64, 0, s>>>(n_w, cur_pos, d_window, st.kf_pose, d_Scw, d_scr,
+                                            st.kf_S_corr, st.kf_in_win);
+  k_win_mark<<<std::min((n_w + 7) / 8, 148 * 8), LC_NTHREADS, 0, s>>>(n_w, d_window, st.kf_fbeg,
+                                                                    st.feat_mp, st.mp_flags, st.mp_owner);
   const int nb_mp = st.n_mp > 0 ? grid_for(st.n_mp) : 0;
   const int nb_w = (n_w + LC_NTHREADS - 1) / LC_NTHREADS;
   k_win_b<<<nb_mp + nb_w, LC_NTHREADS, 0, s>>>(st.n_mp, nb_mp, n_w, st.mp_owner, d_window, d_scr,
                                                st.mp_rec, st.mp_corr_ref, st.kf_pose, counts);
-  c->launches += 2;
+  c->launches += 3;
   return cudaGetLastError();
 }
 

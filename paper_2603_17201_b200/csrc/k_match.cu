@@ -24,10 +24,12 @@ constexpr unsigned long long NONE = 0x7FFFFFFFFFFFFFFFull;
 // local per-thread counters of the matching kernel (subset of LC_COUNT_*)
 enum { M_QUERIES, M_BAD, M_FOUND, M_DEPTH, M_BOUNDS, M_DIST, M_ANGLE, M_CAND, M_NOCAND,
        M_OVERTH, M_RATIO, M_PROP, M_N };
-__device__ __constant__ int kMatchSlot[M_N] = {
+__device__ __constant__ int kProjSlot[7] = {
     LC_COUNT_QUERIES, LC_COUNT_SKIP_BAD, LC_COUNT_SKIP_FOUND, LC_COUNT_CULL_DEPTH,
-    LC_COUNT_CULL_BOUNDS, LC_COUNT_CULL_DIST, LC_COUNT_CULL_ANGLE, LC_COUNT_CANDIDATES,
-    LC_COUNT_NO_CAND, LC_COUNT_OVER_TH, LC_COUNT_RATIO_REJ, LC_COUNT_PROPOSALS};
+    LC_COUNT_CULL_BOUNDS, LC_COUNT_CULL_DIST, LC_COUNT_CULL_ANGLE};
+__device__ __constant__ int kMatchSlot2[5] = {LC_COUNT_CANDIDATES, LC_COUNT_NO_CAND,
+                                              LC_COUNT_OVER_TH, LC_COUNT_RATIO_REJ,
+                                              LC_COUNT_PROPOSALS};
 
 
 // Reduce per-thread counters over the block and add them to global memory.
@@ -88,43 +90,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 }
 
-// compacted survivor of the geometric culls (phase A -> phase B): 24 bytes
-struct __align__(8) QEnt {
-  int32_t q;
-  uint32_t jl;   // (position in the block's query range) | (level << 27)
-  double u, v;
-};
 
 // ---------------------------------------------------------------------------
-// MODE 0: fuse (already found = associated in the keyframe)
-// MODE 1: projection search (already found = pair_taken; taken features excluded)
+// Loop fusion / projection search in two kernels over the same (unit, query chunk)
+// blocks (unit = keyframe for fuse, (keyframe, Sim3, params) pair for SBP):
 //
-// One CTA per (unit = keyframe/pair, query chunk); warps work independently after
-// staging. Staging: one elected thread issues three 1-D TMA bulk copies (cell
-// offsets, keypoints, octave/index words of the keyframe's cell-major block) on an
-// mbarrier while the CTA builds the already-found hash (and, in sole mode,
-// initialises the unit's winner words).
-// Phase A (per warp, 64 queries per batch, 2 per lane): list entry -> {flags, first
-//   32-B sector of the 64-B map-point record} -> fp64 SE3 projection and culls.
-//   Division-free conservative pre-tests decide the bounds cull (pinhole) and the
-//   lower distance cull whenever the value is farther than a margin from the bound
-//   (margins >> fp64 rounding), so decisions equal the exact fp64 ones; the exact
-//   fp64 expression is evaluated otherwise. Survivors are ballot-compacted into
-//   the warp's shared-memory ring.
-// Phase B (per warp, whenever >= 32 survivors are queued; one survivor per lane):
-//   (1) the lane walks its window's cell rows in shared memory and records the
-//   candidate positions (octave + exact square-window test); (2) the warp computes
-//   the Hamming distance of ALL recorded candidates together (one 32-B descriptor
-//   sector per candidate, gathers issued by the whole warp; query descriptor words
-//   come from the owner lane by shuffle); (3) each lane reduces its own keys:
-//   best = min (H << 16 | f), second = min H of the rest; proposal = u64
-//   atomicMin on (H << 32) | q.
+// k_project ("each GPU thread handles the projection ... for a single
+//   map point"): thread per query. List entry -> {flags, first 32-B sector of the
+//   64-B map-point record}; already-found test against a shared-memory hash of the
+//   keyframe's associations; fp64 SE3 projection and culls in the order of the
+//   definition (division-free conservative pre-tests decide the bounds and lower
+//   distance culls when the value is farther from the bound than a margin >> fp64
+//   rounding; the exact expression otherwise); level prediction (float guess,
+//   exact fp64 adjustment). Survivors are warp-aggregated into the block's region
+//   of a global survivor buffer (L2-resident between the two launches).
+// k_match: CTA per block; one elected thread stages the keyframe's cell offsets,
+//   keypoints and octave/index words with three 1-D TMA bulk copies on an mbarrier;
+//   each warp takes 32 survivors at a time: (1) lane-serial scan of the window's
+//   cells in shared memory (octave test + fp32-filtered exact square-window test)
+//   recording candidate positions; (2) warp-wide Hamming distances of all recorded
+//   candidates (one 32-B descriptor sector each, query words by shuffle);
+//   (3) per-lane best = min (H << 16 | f), second = min H of the rest, proposal =
+//   u64 atomicMin on (H << 32) | q. In sole mode (one block per unit) the CTA then
+//   resolves its unit (orientation + fuse actions) without another launch.
 // ---------------------------------------------------------------------------
 template <int MODE>
 __device__ void resolve_unit(const MatchArgs& a, int unit);
 
-constexpr int QW = 96;            // per-warp survivor ring (>= 31 + 64)
-constexpr int RMAX = 6;           // window cell rows per survivor in the flattened scan
 constexpr int NWARP = LC_NTHREADS / 32;
 constexpr int CPL = 6;            // candidate slots per survivor (more -> serial fallback)
 
@@ -149,38 +141,29 @@ __device__ __forceinline__ bool hhas(const int32_t* tab, uint32_t size, int32_t 
   }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArgs a) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t s_bar;
-  __shared__ double s_T[12];  // R row-major, tt = t / s
+template <int FCAP>
+struct HashSize {
+  static constexpr int HS = ((FCAP + FCAP / 8 + 1) + 31) & ~31;
+};
+
+// ---- k_project ---------------------------------------------------------------
+template <int MODE, int FCAP>
+__global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
+  constexpr uint32_t HS = (uint32_t)HashSize<FCAP>::HS;
+  __shared__ int32_t s_hash[HS];
+  __shared__ double s_T[12];
   __shared__ double s_Ow[3];
   __shared__ DevCam s_cam;
-  __shared__ int s_next;
+  __shared__ int s_cnt;
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
+  const int lane = tid & 31;
   const unsigned ltmask = (1u << lane) - 1u;
   const int unit = a.blk_unit[blockIdx.x];
   const int k = a.unit_kf[unit];
   const int fb = a.kf_fbeg[k];
   const int F = a.kf_fbeg[k + 1] - fb;
-  const int fp = a.kf_fpad[k];
-  const uint32_t HS = (uint32_t)a.hash_size;
-  uint16_t* s_cell = (uint16_t*)smem;
-  float2* s_uv = (float2*)(smem + a.off_uv);
-  uint32_t* s_meta = (uint32_t*)(smem + a.off_meta);
-  int32_t* s_hash = (int32_t*)(smem + a.off_hash);
-  unsigned char* wbase = smem + a.off_queue + (size_t)warp * a.warp_bytes;
-  QEnt* s_q = (QEnt*)wbase;                                   // [QW]
-  uint32_t* s_key = (uint32_t*)(wbase + QW * sizeof(QEnt));   // [32][CPL] keys ...
-  uint32_t* s_rows = s_key;                                   // ... aliased by [32][RMAX] rows
-  uint16_t* s_cand = (uint16_t*)(s_key + 32 * (CPL > RMAX ? CPL : RMAX));  // [32][CPL]
-  int* s_nc = (int*)(s_cand + 32 * CPL);                      // [32] candidates per lane
   const int64_t toff = (MODE == 1 && a.taken) ? a.unit_toff[unit] : 0;
-
-  // ---- stage the keyframe (TMA) + already-found hash ---------------------------
   if (tid == 0) {
-    mbar_init(&s_bar, 1);
     double S[13], T[13];
     const double* src = a.unit_S ? a.unit_S + 13 * (size_t)unit : a.kf_S_corr + 13 * (size_t)k;
     for (int i = 0; i < 13; ++i) S[i] = src[i];
@@ -188,11 +171,145 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArg
     for (int i = 0; i < 12; ++i) s_T[i] = T[i];
     for (int i = 0; i < 3; ++i) s_Ow[i] = -lc_col3(T, i, T + 9);
     s_cam = a.cams[a.kf_cam[k]];
-    s_next = 0;
+    s_cnt = 0;
   }
   for (int i = tid; i < (int)HS; i += LC_NTHREADS) s_hash[i] = -1;
   __syncthreads();
+  for (int f = tid; f < F; f += LC_NTHREADS) {
+    int32_t m = (MODE == 0) ? a.feat_mp[fb + f] : (a.taken ? a.taken[toff + f] : -1);
+    if (m >= 0) hins(s_hash, HS, m);
+  }
+  __syncthreads();
+  const int L = a.n_levels;
+  const double sLm1 = a.scale[L - 1];
+  const double c08 = 0.8 / sLm1;   // for the division-free pre-test only
+  const bool pinhole = s_cam.model == 0;
+  const float inv_lsf = 1.0f / logf((float)a.scale[1]);
+  const int64_t q0 = a.blk_q0[blockIdx.x], q1 = a.blk_q1[blockIdx.x];
+  const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
+  Surv* out = a.surv + a.surv_off[blockIdx.x];
+  uint32_t cA = 0, cB = 0, cQ = 0;   // packed 10-bit counters (<= 64 queries per thread per block)
+  for (int64_t jb = q0; jb < q1; jb += LC_NTHREADS) {
+    const int64_t j = jb + tid;
+    const bool valid = j < q1;
+    const int32_t q = valid ? a.mp_list[j] : -1;
+    const bool in_range = valid && (unsigned)q < (unsigned)a.n_mp;
+    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0;
+    uint8_t flag = 1;
+    if (in_range) {
+      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + q);
+      r0 = __ldg(rp); r1 = __ldg(rp + 1); flag = __ldg(a.mp_flags + q);
+    }
+    int status = 0;
+    double u = 0.0, v = 0.0;
+    int lvl = 0;
+    if (valid) {
+      cQ += 1u;
+      do {
+        if (!in_range || (flag & 1u)) { status = LC_Q_BAD; cA += 1u; break; }
+        if (hhas(s_hash, HS, q)) { status = LC_Q_FOUND; cA += 1u << 10; break; }
+        const double p0 = __uint_as_float(r0.x), p1 = __uint_as_float(r0.y), p2 = __uint_as_float(r0.z);
+        const double z = (s_T[6] * p0 + s_T[7] * p1) + s_T[8] * p2 + s_T[11];
+        if (z <= 0.0) { status = LC_Q_DEPTH; cA += 1u << 20; break; }
+        const double x = (s_T[0] * p0 + s_T[1] * p1) + s_T[2] * p2 + s_T[9];
+        const double y = (s_T[3] * p0 + s_T[4] * p1) + s_T[5] * p2 + s_T[10];
+        if (pinhole && !a.dbg_uv) {
+          // conservative pre-test: |ua - u| <= 1e-6 |u| + tiny, margin 1e-2 px
+          const double rz = (double)__frcp_rn((float)z);
+          const double A = s_cam.fx * x, B = s_cam.fy * y;
+          const double e = 1e-6 * (fabs(A * rz) + fabs(B * rz)) + 1e-2;
+          const double ua = A * rz * (2.0 - z * rz) + s_cam.cx;   // one Newton step
+          const double va = B * rz * (2.0 - z * rz) + s_cam.cy;
+          if (ua < s_cam.min_x - e || ua >= s_cam.max_x + e || va < s_cam.min_y - e ||
+              va >= s_cam.max_y + e) {
+            status = LC_Q_BOUNDS; cB += 1u; break;
+          }
+        }
+        lc_project(s_cam, x, y, z, u, v);
+        if (!(u >= s_cam.min_x && u < s_cam.max_x && v >= s_cam.min_y && v < s_cam.max_y)) {
+          status = LC_Q_BOUNDS; cB += 1u; break;
+        }
+        const double PO0 = p0 - s_Ow[0], PO1 = p1 - s_Ow[1], PO2 = p2 - s_Ow[2];
+        const double d = sqrt((PO0 * PO0 + PO1 * PO1) + PO2 * PO2);
+        const double dmax = __uint_as_float(r0.w);
+        bool dcull = d > 1.2 * dmax;
+        if (!dcull) {
+          const double t = dmax * c08;   // within a few ulp of 0.8 * (dmax / s_{L-1})
+          if (d < t * (1.0 - 1e-9)) dcull = true;
+          else if (!(d > t * (1.0 + 1e-9))) dcull = d < 0.8 * (dmax / sLm1);   // exact near the bound
+        }
+        if (dcull) { status = LC_Q_DIST; cB += 1u << 10; break; }
+        const double n0 = __uint_as_float(r1.x), n1 = __uint_as_float(r1.y), n2 = __uint_as_float(r1.z);
+        if ((PO0 * n0 + PO1 * n1) + PO2 * n2 < 0.5 * d) { status = LC_Q_ANGLE; cB += 1u << 20; break; }
+        // level: smallest n with d * s_n >= dmax (else L-1): float guess, exact adjustment
+        lvl = (int)ceilf(__logf((float)dmax / (float)d) * inv_lsf);
+        lvl = min(max(lvl, 0), L - 1);
+        while (lvl > 0 && d * a.scale[lvl - 1] >= dmax) --lvl;
+        while (lvl < L - 1 && !(d * a.scale[lvl] >= dmax)) ++lvl;
+        status = 1;
+      } while (0);
+    }
+    const bool surv = status == 1;
+    const unsigned m = __ballot_sync(0xffffffffu, surv);
+    int wbase = 0;
+    if (lane == 0 && m) wbase = atomicAdd(&s_cnt, __popc(m));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (surv) {
+      Surv e;
+      e.q = q; e.jl = (uint32_t)(j - q0) | ((uint32_t)lvl << 27); e.u = u; e.v = v;
+      out[wbase + __popc(m & ltmask)] = e;
+    } else if (valid) {
+      const int64_t qi = qbase + (j - q0);
+      if (a.dbg_best) a.dbg_best[qi] = status;
+      if (a.dbg_uv) {
+        if (status > LC_Q_BOUNDS) u = v = 0.0;
+        a.dbg_uv[2 * qi] = u; a.dbg_uv[2 * qi + 1] = v;
+      }
+      if (a.dbg_ncand) a.dbg_ncand[qi] = 0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) a.surv_cnt[blockIdx.x] = s_cnt;
+  uint32_t cnt[7];
+  cnt[0] = cQ; cnt[1] = cA & 1023u; cnt[2] = (cA >> 10) & 1023u; cnt[3] = (cA >> 20) & 1023u;
+  cnt[4] = cB & 1023u; cnt[5] = (cB >> 10) & 1023u; cnt[6] = (cB >> 20) & 1023u;
+  unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
+  block_add<7>(cnt, kProjSlot, cdst);
+}
+
+// ---- k_match ------------------------------------------------------------------
+template <int FCAP>
+struct MatchSmem {
+  static constexpr int WB = ((32 * CPL * 4 + 32 * CPL * 2) + 15) & ~15;
+  static constexpr int UV = 0;
+  static constexpr int META = UV + ((FCAP * 8 + 15) & ~15);
+  static constexpr int QUEUE = META + ((FCAP * 4 + 15) & ~15);
+  static constexpr int CELL = QUEUE + NWARP * WB;   // runtime-size cell table last
+};
+
+template <int MODE, int FCAP>
+__global__ void __launch_bounds__(LC_NTHREADS, 3) k_match(const MatchArgs a) {
+  using SM = MatchSmem<FCAP>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ double s_T[12];
+  __shared__ DevCam s_cam;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int unit = a.blk_unit[blockIdx.x];
+  const int k = a.unit_kf[unit];
+  const int fb = a.kf_fbeg[k];
+  const int F = a.kf_fbeg[k + 1] - fb;
+  const int fp = a.kf_fpad[k];
+  uint16_t* s_cell = (uint16_t*)(smem + SM::CELL);
+  float2* s_uv = (float2*)(smem + SM::UV);
+  uint32_t* s_meta = (uint32_t*)(smem + SM::META);
+  unsigned char* wb = smem + SM::QUEUE + warp * SM::WB;
+  uint32_t* s_key = (uint32_t*)wb;                  // [32][CPL] candidate keys
+  uint16_t* s_cand = (uint16_t*)(s_key + 32 * CPL); // [32][CPL] candidate positions
+  const int64_t toff = (MODE == 1 && a.taken) ? a.unit_toff[unit] : 0;
   if (tid == 0) {
+    mbar_init(&s_bar, 1);
     const uint32_t b_cell = (uint32_t)a.Gs * 2u;
     const uint32_t b_uv = (uint32_t)((F + 1) & ~1) * 8u;
     const uint32_t b_meta = (uint32_t)((F + 3) & ~3) * 4u;
@@ -202,213 +319,83 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArg
       tma_load_1d(s_uv, a.fc_uv + fp, b_uv, &s_bar);
       tma_load_1d(s_meta, a.fc_meta + fp, b_meta, &s_bar);
     }
-  }
-  for (int f = tid; f < F; f += LC_NTHREADS) {
-    int32_t m = (MODE == 0) ? a.feat_mp[fb + f] : (a.taken ? a.taken[toff + f] : -1);
-    if (m >= 0) hins(s_hash, HS, m);
+    double S[13], T[13];
+    const double* src = a.unit_S ? a.unit_S + 13 * (size_t)unit : a.kf_S_corr + 13 * (size_t)k;
+    for (int i = 0; i < 13; ++i) S[i] = src[i];
+    lc_sim3_se3(S, T);
+    for (int i = 0; i < 12; ++i) s_T[i] = T[i];
+    s_cam = a.cams[a.kf_cam[k]];
   }
   if (a.sole) {  // this CTA owns the unit's winner words: initialise them here
     unsigned long long* w0 = a.winner + a.unit_woff[unit];
     for (int f = tid; f < F; f += LC_NTHREADS) w0[f] = NONE;
   }
-  bool staged = false;
+  __syncthreads();
+  mbar_wait(&s_bar, 0);
   if (MODE == 1 && a.taken) {  // taken features are not candidates (reading A19)
-    mbar_wait(&s_bar, 0);
-    staged = true;
-    __syncthreads();
     for (int p = tid; p < F; p += LC_NTHREADS)
       if (a.taken[toff + (s_meta[p] & 0xFFFFu)] >= 0) s_meta[p] |= 0x80000000u;
   }
   __syncthreads();
 
   const lc_match_params prm = a.params[(MODE == 1 && a.unit_param) ? a.unit_param[unit] : 0];
-  const int L = a.n_levels;
-  const double sLm1 = a.scale[L - 1];
-  const double c08 = 0.8 / sLm1;            // for the division-free pre-test only
   const int cols = a.cols, rows = a.rows;
-  const bool pinhole = s_cam.model == 0;
+  const bool f32ok = fmax(fabs(s_cam.min_x), fabs(s_cam.max_x)) < 4096.0 &&
+                     fmax(fabs(s_cam.min_y), fabs(s_cam.max_y)) < 4096.0;
   const float fminx = (float)s_cam.min_x, fminy = (float)s_cam.min_y;
   const float fsx = (float)s_cam.cell_sx, fsy = (float)s_cam.cell_sy;
   unsigned long long* win = a.winner + a.unit_woff[unit];
-  const int64_t q0 = a.blk_q0[blockIdx.x], q1 = a.blk_q1[blockIdx.x];
-  const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);   // debug index of q0
-  uint32_t cnt[M_N];
-#pragma unroll
-  for (int i = 0; i < M_N; ++i) cnt[i] = 0;
-  int head = 0, tail = 0;  // warp-uniform ring indices (monotone; slot = idx % QW)
+  const int64_t q0 = a.blk_q0[blockIdx.x];
+  const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
+  const Surv* sv = a.surv + a.surv_off[blockIdx.x];
+  const int ns_tot = a.surv_cnt[blockIdx.x];
+  uint32_t cC = 0, cP = 0, cE = 0;   // NOCAND | OVERTH << 10 | RATIO << 20; PROP; CAND
 
-  // ---- phase A: one query; true if it survived (entry filled) ------------------
-  auto phase_a = [&](int32_t q, int64_t j, bool in_range, uint8_t flag, uint4 r0, uint4 r1,
-                     QEnt& ent) -> bool {
-    int status = 0;
-    double u = 0.0, v = 0.0;
-    do {
-      if (!in_range || (flag & 1u)) { status = LC_Q_BAD; cnt[M_BAD]++; break; }
-      if (hhas(s_hash, HS, q)) { status = LC_Q_FOUND; cnt[M_FOUND]++; break; }
-      const double p0 = __uint_as_float(r0.x), p1 = __uint_as_float(r0.y), p2 = __uint_as_float(r0.z);
-      const double z = (s_T[6] * p0 + s_T[7] * p1) + s_T[8] * p2 + s_T[11];
-      if (z <= 0.0) { status = LC_Q_DEPTH; cnt[M_DEPTH]++; break; }
-      const double x = (s_T[0] * p0 + s_T[1] * p1) + s_T[2] * p2 + s_T[9];
-      const double y = (s_T[3] * p0 + s_T[4] * p1) + s_T[5] * p2 + s_T[10];
-      if (pinhole && !a.dbg_uv) {
-        // conservative pre-test: |ua - u| <= 1e-6 |u| + tiny, margin 1e-2 px
-        const double rz = (double)__frcp_rn((float)z);
-        const double A = s_cam.fx * x, B = s_cam.fy * y;
-        const double e = 1e-6 * (fabs(A * rz) + fabs(B * rz)) + 1e-2;
-        const double ua = A * rz * (2.0 - z * rz) + s_cam.cx;   // one Newton step
-        const double va = B * rz * (2.0 - z * rz) + s_cam.cy;
-        if (ua < s_cam.min_x - e || ua >= s_cam.max_x + e || va < s_cam.min_y - e ||
-            va >= s_cam.max_y + e) {
-          status = LC_Q_BOUNDS; cnt[M_BOUNDS]++; break;
-        }
-      }
-      lc_project(s_cam, x, y, z, u, v);
-      if (!(u >= s_cam.min_x && u < s_cam.max_x && v >= s_cam.min_y && v < s_cam.max_y)) {
-        status = LC_Q_BOUNDS; cnt[M_BOUNDS]++; break;
-      }
-      const double PO0 = p0 - s_Ow[0], PO1 = p1 - s_Ow[1], PO2 = p2 - s_Ow[2];
-      const double d = sqrt((PO0 * PO0 + PO1 * PO1) + PO2 * PO2);
-      const double dmax = __uint_as_float(r0.w);
-      bool dcull = d > 1.2 * dmax;
-      if (!dcull) {
-        const double t = dmax * c08;   // within a few ulp of 0.8 * (dmax / s_{L-1})
-        if (d < t * (1.0 - 1e-9)) dcull = true;
-        else if (!(d > t * (1.0 + 1e-9))) dcull = d < 0.8 * (dmax / sLm1);   // exact near the bound
-      }
-      if (dcull) { status = LC_Q_DIST; cnt[M_DIST]++; break; }
-      const double n0 = __uint_as_float(r1.x), n1 = __uint_as_float(r1.y), n2 = __uint_as_float(r1.z);
-      if ((PO0 * n0 + PO1 * n1) + PO2 * n2 < 0.5 * d) { status = LC_Q_ANGLE; cnt[M_ANGLE]++; break; }
-      int lvl = L - 1;
-      for (int n = 0; n < L; ++n)
-        if (d * a.scale[n] >= dmax) { lvl = n; break; }
-      ent.q = q; ent.jl = (uint32_t)(j - q0) | ((uint32_t)lvl << 27); ent.u = u; ent.v = v;
-      return true;
-    } while (0);
-    const int64_t qi = qbase + (j - q0);
-    if (a.dbg_best) a.dbg_best[qi] = status;
-    if (a.dbg_uv) { a.dbg_uv[2 * qi] = u; a.dbg_uv[2 * qi + 1] = v; }
-    if (a.dbg_ncand) a.dbg_ncand[qi] = 0;
-    return false;
-  };
-
-  auto enqueue = [&](bool surv, const QEnt& ent) {
-    const unsigned m = __ballot_sync(0xffffffffu, surv);
-    if (surv) s_q[(tail + __popc(m & ltmask)) % QW] = ent;
-    tail += __popc(m);
-  };
-
-  // ---- phase B: n (<= 32) queued survivors, one per lane -----------------------
-  // Serial window scan of one survivor (fallback when its window has more than RMAX
-  // cell rows or more than CPL candidates): same arithmetic, evaluated in place.
-  auto scan_serial = [&](double u, double v, double r, int lvl, const uint4& d0, const uint4& d1,
-                         uint32_t& best, int& second) {
-    const float fu = (float)u, fv = (float)v, fr = (float)r;
-    const int cx0 = max(0, (int)floorf((fu - fr - 0.01f - fminx) * fsx));
-    const int cx1 = min(cols - 1, (int)floorf((fu + fr + 0.01f - fminx) * fsx));
-    const int cy0 = max(0, (int)floorf((fv - fr - 0.01f - fminy) * fsy));
-    const int cy1 = min(rows - 1, (int)floorf((fv + fr + 0.01f - fminy) * fsy));
-    for (int cy = cy0; cy <= cy1; ++cy) {
-      const int pe = s_cell[cy * cols + cx1 + 1];
-      for (int p = s_cell[cy * cols + cx0]; p < pe; ++p) {
-        const uint32_t meta = s_meta[p];
-        const int oct = (int)((meta >> 16) & 0xFFu);
-        if (oct < lvl - 1 || oct > lvl) continue;
-        if (MODE == 1 && (meta & 0x80000000u)) continue;
-        const float2 fuv = s_uv[p];
-        if (!(fabs((double)fuv.x - u) < r && fabs((double)fuv.y - v) < r)) continue;
-        const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
-        const int h = popc_desc(d0, d1, __ldg(dp), __ldg(dp + 1));
-        const uint32_t key = ((uint32_t)h << 16) | (meta & 0xFFFFu);
-        if (key < best) {
-          if (best != 0xFFFFFFFFu) second = min(second, (int)(best >> 16));
-          best = key;
-        } else {
-          second = min(second, h);
-        }
-      }
-    }
-  };
-
-  auto phase_b = [&](int n) {
-    const bool act = lane < n;
-    const QEnt* my = s_q + (head + lane) % QW;
-    const QEnt e = act ? *my : QEnt{0, 0u, 0.0, 0.0};
+  for (int i0 = warp * 32; i0 < ns_tot; i0 += NWARP * 32) {
+    const bool act = i0 + lane < ns_tot;
+    Surv e;
+    e.q = 0; e.jl = 0u; e.u = 0.0; e.v = 0.0;
+    if (act) e = sv[i0 + lane];
     const int lvl = (int)(e.jl >> 27);
     const double r = (double)prm.th * a.scale[lvl];
     uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
+    int cx0 = 0, cx1 = -1, cy0 = 0, cy1 = -1, nc = 0;
     if (act) {
       const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + e.q);
       d0 = __ldg(rp + 2); d1 = __ldg(rp + 3);
-    }
-    // (0) this lane's window rows -> (start, length) list; work size = sum of lengths
-    int nrow = 0, nfeat = 0;
-    if (act) {
       const float fu = (float)e.u, fv = (float)e.v, fr = (float)r;
-      // conservative (0.01 px) superset of the exact square window
-      const int cx0 = max(0, (int)floorf((fu - fr - 0.01f - fminx) * fsx));
-      const int cx1 = min(cols - 1, (int)floorf((fu + fr + 0.01f - fminx) * fsx));
-      const int cy0 = max(0, (int)floorf((fv - fr - 0.01f - fminy) * fsy));
-      const int cy1 = min(rows - 1, (int)floorf((fv + fr + 0.01f - fminy) * fsy));
-      nrow = cy1 - cy0 + 1;
-      if (nrow <= RMAX) {
-        for (int i = 0; i < nrow; ++i) {
-          const int cy = cy0 + i;
-          const int pb = s_cell[cy * cols + cx0], pe = s_cell[cy * cols + cx1 + 1];
-          s_rows[lane * RMAX + i] = (uint32_t)pb | ((uint32_t)(pe - pb) << 16);
-          nfeat += pe - pb;
-        }
-      }
-    }
-    const bool serial = act && nrow > RMAX;
-    if (serial) nfeat = 0;
-    s_nc[lane] = 0;
-    __syncwarp();
-    // (1) flattened scan of all (survivor, feature) pairs of the warp
-    int incl = nfeat;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    const int excl = incl - nfeat;
-    for (int c0 = 0; c0 < total; c0 += 32) {
-      const int c = c0 + lane;
-      int own = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int ex = __shfl_sync(0xffffffffu, excl, own + step);
-        if (c < total && ex <= c) own += step;
-      }
-      const int oex = __shfl_sync(0xffffffffu, excl, own);
-      if (c < total) {
-        int t = c - oex, ri = 0;
-        uint32_t rw = s_rows[own * RMAX];
-        while (t >= (int)(rw >> 16)) { t -= (int)(rw >> 16); rw = s_rows[own * RMAX + (++ri)]; }
-        const int p = (int)(rw & 0xFFFFu) + t;
-        const QEnt oe = s_q[(head + own) % QW];
-        const int olvl = (int)(oe.jl >> 27);
-        const uint32_t meta = s_meta[p];
-        const int oct = (int)((meta >> 16) & 0xFFu);
-        bool cand = oct >= olvl - 1 && oct <= olvl;
-        if (MODE == 1) cand = cand && !(meta & 0x80000000u);
-        if (cand) {
-          const double orr = (double)prm.th * a.scale[olvl];
+      // conservative (0.01 px) cell-range superset of the exact square window
+      cx0 = max(0, (int)floorf((fu - fr - 0.01f - fminx) * fsx));
+      cx1 = min(cols - 1, (int)floorf((fu + fr + 0.01f - fminx) * fsx));
+      cy0 = max(0, (int)floorf((fv - fr - 0.01f - fminy) * fsy));
+      cy1 = min(rows - 1, (int)floorf((fv + fr + 0.01f - fminy) * fsy));
+      const int lo = lvl - 1;
+      // (1) window scan. fp32 window test first: |fuv - (float)u| is within 2.5e-4 px
+      // of the exact |fuv - u| for |u| < 4096 px, so a decision farther than 1e-3 px
+      // from the edge is exact; otherwise (or for larger images) fp64.
+      for (int cy = cy0; cy <= cy1; ++cy) {
+        const int pe = s_cell[cy * cols + cx1 + 1];
+        for (int p = s_cell[cy * cols + cx0]; p < pe; ++p) {
+          const uint32_t meta = s_meta[p];
+          const int oct = (int)((meta >> 16) & 0xFFu);
+          if (oct < lo || oct > lvl) continue;
+          if (MODE == 1 && (meta & 0x80000000u)) continue;
           const float2 fuv = s_uv[p];
-          cand = fabs((double)fuv.x - oe.u) < orr && fabs((double)fuv.y - oe.v) < orr;
-        }
-        if (cand) {
-          const int slot = atomicAdd(&s_nc[own], 1);
-          if (slot < CPL) s_cand[own * CPL + slot] = (uint16_t)p;
+          const float du = fabsf(fuv.x - fu), dv = fabsf(fuv.y - fv);
+          if (f32ok && (du > fr + 1e-3f || dv > fr + 1e-3f)) continue;
+          if (!(f32ok && du < fr - 1e-3f && dv < fr - 1e-3f) &&
+              !(fabs((double)fuv.x - e.u) < r && fabs((double)fuv.y - e.v) < r))
+            continue;
+          if (nc < CPL) s_cand[lane * CPL + nc] = (uint16_t)p;
+          ++nc;
         }
       }
     }
     __syncwarp();
     // (2) Hamming of all slotted candidates, warp-wide
-    const int nc = s_nc[lane];
-    const bool over = act && !serial && nc > CPL;
-    const int ns = (act && !serial && !over) ? nc : 0;
-    incl = ns;
+    const bool over = act && nc > CPL;
+    const int ns = (act && !over) ? nc : 0;
+    int incl = ns;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -440,107 +427,62 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_project_match(const MatchArg
       }
     }
     __syncwarp();
-    // (3) per-lane reduction over its own keys (or the serial fallback)
+    // (3) per-lane reduction over its own keys (serial rescan when > CPL candidates)
     if (act) {
       uint32_t best = 0xFFFFFFFFu;  // (H << 16) | f
       int second = 256;
-      int ncand = nc;
-      if (serial || over) {
-        scan_serial(e.u, e.v, r, lvl, d0, d1, best, second);
-        if (serial) {  // count the candidates of the serial scan
-          ncand = 0;
-          const float fu = (float)e.u, fv = (float)e.v, fr = (float)r;
-          const int cx0 = max(0, (int)floorf((fu - fr - 0.01f - fminx) * fsx));
-          const int cx1 = min(cols - 1, (int)floorf((fu + fr + 0.01f - fminx) * fsx));
-          const int cy0 = max(0, (int)floorf((fv - fr - 0.01f - fminy) * fsy));
-          const int cy1 = min(rows - 1, (int)floorf((fv + fr + 0.01f - fminy) * fsy));
-          for (int cy = cy0; cy <= cy1; ++cy)
-            for (int p = s_cell[cy * cols + cx0]; p < s_cell[cy * cols + cx1 + 1]; ++p) {
-              const uint32_t meta = s_meta[p];
-              const int oct = (int)((meta >> 16) & 0xFFu);
-              if (oct < lvl - 1 || oct > lvl) continue;
-              if (MODE == 1 && (meta & 0x80000000u)) continue;
-              const float2 fuv = s_uv[p];
-              if (fabs((double)fuv.x - e.u) < r && fabs((double)fuv.y - e.v) < r) ++ncand;
-            }
+      auto take = [&](uint32_t key) {
+        if (key < best) {
+          if (best != 0xFFFFFFFFu) second = min(second, (int)(best >> 16));
+          best = key;
+        } else {
+          second = min(second, (int)(key >> 16));
         }
-      } else {
-        for (int i = 0; i < ns; ++i) {
-          const uint32_t key = s_key[lane * CPL + i];
-          if (key < best) {
-            if (best != 0xFFFFFFFFu) second = min(second, (int)(best >> 16));
-            best = key;
-          } else {
-            second = min(second, (int)(key >> 16));
+      };
+      if (over) {
+        for (int cy = cy0; cy <= cy1; ++cy) {
+          const int pe = s_cell[cy * cols + cx1 + 1];
+          for (int p = s_cell[cy * cols + cx0]; p < pe; ++p) {
+            const uint32_t meta = s_meta[p];
+            const int oct = (int)((meta >> 16) & 0xFFu);
+            if (oct < lvl - 1 || oct > lvl) continue;
+            if (MODE == 1 && (meta & 0x80000000u)) continue;
+            const float2 fuv = s_uv[p];
+            if (!(fabs((double)fuv.x - e.u) < r && fabs((double)fuv.y - e.v) < r)) continue;
+            const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
+            take(((uint32_t)popc_desc(d0, d1, __ldg(dp), __ldg(dp + 1)) << 16) | (meta & 0xFFFFu));
           }
         }
+      } else {
+        for (int i = 0; i < ns; ++i) take(s_key[lane * CPL + i]);
       }
-      cnt[M_CAND] += ncand;
+      cE += nc;
       do {
-        if (ncand == 0) { cnt[M_NOCAND]++; break; }
+        if (nc == 0) { cC += 1u; break; }
         const int hb = (int)(best >> 16);
-        if (hb > prm.max_hamming) { cnt[M_OVERTH]++; break; }
+        if (hb > prm.max_hamming) { cC += 1u << 10; break; }
         if (prm.ratio_den > 0 && (long long)prm.ratio_den * hb > (long long)prm.ratio_num * second) {
-          cnt[M_RATIO]++; break;
+          cC += 1u << 20; break;
         }
-        cnt[M_PROP]++;
+        cP += 1u;
         atomicMin(&win[best & 0xFFFFu], ((unsigned long long)hb << 32) | (unsigned int)e.q);
       } while (0);
       const int64_t qi = qbase + (int64_t)(e.jl & 0x07FFFFFFu);
       if (a.dbg_best) {
         long long val;
-        if (ncand == 0) val = (256LL << 48) | (256LL << 32) | 0xFFFFFFFFLL;
+        if (nc == 0) val = (256LL << 48) | (256LL << 32) | 0xFFFFFFFFLL;
         else val = ((long long)(best >> 16) << 48) | ((long long)second << 32) | (long long)(best & 0xFFFFu);
         a.dbg_best[qi] = val;
       }
       if (a.dbg_uv) { a.dbg_uv[2 * qi] = e.u; a.dbg_uv[2 * qi + 1] = e.v; }
-      if (a.dbg_ncand) a.dbg_ncand[qi] = ncand;
+      if (a.dbg_ncand) a.dbg_ncand[qi] = nc;
     }
     __syncwarp();
-    head += n;
-  };
-
-  while (true) {
-    int bidx = 0;
-    if (lane == 0) bidx = atomicAdd(&s_next, 1);
-    bidx = __shfl_sync(0xffffffffu, bidx, 0);
-    const int64_t base = q0 + (int64_t)bidx * 64;
-    if (base >= q1) break;
-    const int64_t ja = base + lane, jb = base + 32 + lane;
-    const bool va = ja < q1, vb = jb < q1;
-    const int32_t qa = va ? a.mp_list[ja] : -1;
-    const int32_t qb = vb ? a.mp_list[jb] : -1;
-    const bool ia = va && (unsigned)qa < (unsigned)a.n_mp;
-    const bool ib = vb && (unsigned)qb < (unsigned)a.n_mp;
-    uint4 ra0 = make_uint4(0, 0, 0, 0), ra1 = ra0, rb0 = ra0, rb1 = ra0;
-    uint8_t fla = 1, flb = 1;
-    if (ia) {
-      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + qa);
-      ra0 = __ldg(rp); ra1 = __ldg(rp + 1); fla = __ldg(a.mp_flags + qa);
-    }
-    if (ib) {
-      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + qb);
-      rb0 = __ldg(rp); rb1 = __ldg(rp + 1); flb = __ldg(a.mp_flags + qb);
-    }
-    QEnt ea, eb;
-    bool sa = false, sb = false;
-    if (va) { cnt[M_QUERIES]++; sa = phase_a(qa, ja, ia, fla, ra0, ra1, ea); }
-    enqueue(sa, ea);
-    if (vb) { cnt[M_QUERIES]++; sb = phase_a(qb, jb, ib, flb, rb0, rb1, eb); }
-    enqueue(sb, eb);
-    __syncwarp();
-    while (tail - head >= 32) {  // keeps the ring below 32 + 64 <= QW entries
-      if (!staged) { mbar_wait(&s_bar, 0); staged = true; }
-      phase_b(32);
-    }
   }
-  if (tail > head) {
-    if (!staged) { mbar_wait(&s_bar, 0); staged = true; }
-    phase_b(tail - head);
-  }
-  if (!staged) mbar_wait(&s_bar, 0);  // never leave the CTA with a bulk copy in flight
+  uint32_t cnt[5];
+  cnt[0] = cE; cnt[1] = cC & 1023u; cnt[2] = (cC >> 10) & 1023u; cnt[3] = (cC >> 20) & 1023u; cnt[4] = cP;
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
-  block_add<M_N>(cnt, kMatchSlot, cdst);
+  block_add<5>(cnt, kMatchSlot2, cdst);
   if (a.sole) {  // all proposals of this unit are in: resolve it here (no extra launch)
     __syncthreads();
     resolve_unit<MODE>(a, unit);
@@ -711,18 +653,28 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_mark(
     const int wpos = (kf_win_ep[k] == epoch) ? kf_win_pos[k] : -1;
     const int64_t wshift = wpos >= 0 ? woff_of_pos[wpos] - fb : 0;   // winner index = f + wshift
     int dirty = 0;
-    // head (to a 16-B boundary), vector body, tail
-    const int vb = min(fe, (fb + 3) & ~3), ve = max(vb, fe & ~3);
-    auto test = [&](int f, int32_t m) {
-      if (m >= 0) dirty |= (__ldg(vbits + (m >> 5)) >> (m & 31)) & 1u;
-      else if (wpos >= 0) dirty |= winner[f + wshift] != NONE;
-    };
-    for (int f = fb + lane; f < vb; f += 32) test(f, feat_mp[f]);
-    for (int f = vb + 4 * lane; f < ve; f += 128) {
-      const int4 m4 = __ldg(reinterpret_cast<const int4*>(feat_mp + f));
-      test(f, m4.x); test(f + 1, m4.y); test(f + 2, m4.z); test(f + 3, m4.w);
+    // 4 x 16-B association loads in flight per lane (512 slots per warp round)
+    for (int f0 = fb; f0 < fe && !__any_sync(0xffffffffu, dirty); f0 += 512) {
+      int32_t m[16];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int f = f0 + 128 * u + 4 * lane;
+        if (f + 3 < fe && !(f & 3)) {
+          const int4 m4 = __ldg(reinterpret_cast<const int4*>(feat_mp + f));
+          m[4 * u] = m4.x; m[4 * u + 1] = m4.y; m[4 * u + 2] = m4.z; m[4 * u + 3] = m4.w;
+        } else {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) m[4 * u + v] = (f + v < fe) ? feat_mp[f + v] : INT32_MIN;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int32_t mm = m[u];
+        if (mm >= 0) dirty |= (__ldg(vbits + (mm >> 5)) >> (mm & 31)) & 1u;
+        else if (mm != INT32_MIN && wpos >= 0)
+          dirty |= winner[f0 + 128 * (u >> 2) + 4 * lane + (u & 3) + wshift] != NONE;
+      }
     }
-    for (int f = ve + lane; f < fe; f += 32) test(f, feat_mp[f]);
     if (__any_sync(0xffffffffu, dirty) && lane == 0) {
       const int i = atomicAdd(&dirty_list[0], 1);
       dirty_list[1 + i] = k;
@@ -760,26 +712,42 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
     uint8_t* s_pr = (uint8_t*)(s_new + F);
     for (int i = threadIdx.x; i < (int)HS; i += blockDim.x) { s_key[i] = -1; s_val[i] = 0xFFFFFFFFu; }
     __syncthreads();
-    for (int f = threadIdx.x; f < F; f += blockDim.x) {
-      const int32_t m = feat_mp[fb + f];
-      int32_t nv = m;
-      uint8_t pr = 0;
-      if (m >= 0) {
-        if ((vbits[m >> 5] >> (m & 31)) & 1u) {
-          nv = (int32_t)(victim[m] & 0xFFFFFFFFull); pr = 2; cnt[A_REWIRED]++;
-        }
-      } else if (wpos >= 0) {
-        const unsigned long long w = winner[woff + f];
-        if (w != NONE) { nv = (int32_t)(w & 0xFFFFFFFFull); pr = 1; }
+    // new value per slot: 8 slots per thread with their loads in flight together
+    for (int base = 0; base < F; base += 8 * (int)blockDim.x) {
+      int32_t m[8];
+      unsigned long long w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = base + u * (int)blockDim.x + (int)threadIdx.x;
+        m[u] = f < F ? feat_mp[fb + f] : INT32_MIN;
       }
-      s_new[f] = nv;
-      s_pr[f] = pr;
-      if (pr) {  // hash the new map point of every changed slot
-        uint32_t h = hslot(nv, HS);
-        while (true) {
-          const int32_t prev = atomicCAS(&s_key[h], -1, nv);
-          if (prev == -1 || prev == nv) break;
-          h = (h + 1 == HS) ? 0 : h + 1;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = base + u * (int)blockDim.x + (int)threadIdx.x;
+        const bool isv = m[u] >= 0 && ((__ldg(vbits + (m[u] >> 5)) >> (m[u] & 31)) & 1u);
+        w[u] = isv ? victim[m[u]] : ((m[u] == -1 && wpos >= 0) ? winner[woff + f] : NONE);
+        if (!isv && m[u] >= 0) w[u] = NONE;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = base + u * (int)blockDim.x + (int)threadIdx.x;
+        if (f >= F) continue;
+        int32_t nv = m[u];
+        uint8_t pr = 0;
+        if (w[u] != NONE) {
+          nv = (int32_t)(w[u] & 0xFFFFFFFFull);
+          pr = m[u] >= 0 ? 2 : 1;
+          if (pr == 2) cnt[A_REWIRED]++;
+        }
+        s_new[f] = nv;
+        s_pr[f] = pr;
+        if (pr) {  // hash the new map point of every changed slot
+          uint32_t h = hslot(nv, HS);
+          while (true) {
+            const int32_t prev = atomicCAS(&s_key[h], -1, nv);
+            if (prev == -1 || prev == nv) break;
+            h = (h + 1 == HS) ? 0 : h + 1;
+          }
         }
       }
     }
@@ -826,38 +794,35 @@ int grid_for(int64_t n) {
 
 }  // namespace
 
-cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a_in, int n_blocks, int F_max,
+template <int MODE, int FCAP>
+cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, cudaStream_t s) {
+  using SM = MatchSmem<FCAP>;
+  k_project<MODE, FCAP><<<n_blocks, LC_NTHREADS, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const size_t smem = (size_t)SM::CELL + (((size_t)a.Gs * 2 + 15) & ~(size_t)15);
+  e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_match<MODE, FCAP><<<n_blocks, LC_NTHREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_match_m(const MatchArgs& a, int n_blocks, int F_max, cudaStream_t s) {
+  if (F_max <= 512) return launch_match_t<MODE, 512>(a, n_blocks, s);
+  if (F_max <= 1024) return launch_match_t<MODE, 1024>(a, n_blocks, s);
+  if (F_max <= 2048) return launch_match_t<MODE, 2048>(a, n_blocks, s);
+  if (F_max <= 4096) return launch_match_t<MODE, 4096>(a, n_blocks, s);
+  return launch_match_t<MODE, 8192>(a, n_blocks, s);
+}
+
+cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max,
                          cudaStream_t s) {
   if (n_blocks <= 0) return cudaSuccess;
-  MatchArgs a = a_in;
-  const int Fm = F_max > 0 ? F_max : 1;
-  // open-addressing table of >= 1.5 F slots (keys: the <= F associated map points)
-  a.hash_size = ((Fm + Fm / 2 + 1) + 31) & ~31;
-  auto r16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
-  size_t off = r16((size_t)a.Gs * 2);
-  a.off_uv = (int)off;
-  off += r16((size_t)((Fm + 1) & ~1) * 8);
-  a.off_meta = (int)off;
-  off += r16((size_t)((Fm + 3) & ~3) * 4);
-  a.off_hash = (int)off;
-  off += r16((size_t)a.hash_size * 4);
-  a.off_queue = (int)off;
-  a.warp_bytes = (int)r16(QW * sizeof(QEnt) + 32 * (CPL > RMAX ? CPL : RMAX) * sizeof(uint32_t) +
-                          32 * CPL * sizeof(uint16_t) + 32 * sizeof(int));
-  off += (size_t)NWARP * a.warp_bytes;
-  const size_t smem = off;
-  cudaError_t e;
-  if (mode == 0) {
-    e = cudaFuncSetAttribute(k_project_match<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_project_match<0><<<n_blocks, LC_NTHREADS, smem, s>>>(a);
-  } else {
-    e = cudaFuncSetAttribute(k_project_match<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_project_match<1><<<n_blocks, LC_NTHREADS, smem, s>>>(a);
-  }
-  c->launches++;
-  return cudaGetLastError();
+  cudaError_t e = mode == 0 ? launch_match_m<0>(a, n_blocks, F_max, s)
+                            : launch_match_m<1>(a, n_blocks, F_max, s);
+  c->launches += 2;
+  return e;
 }
 
 cudaError_t launch_resolve(lc_ctx* c, int mode, const MatchArgs& a, int n_units, cudaStream_t s) {

@@ -673,9 +673,12 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
         bq1.push_back(std::min<int64_t>(q + ch, e));
       }
     }
+    std::vector<int64_t> boff(bunit.size() + 1, 0);
+    for (size_t b = 0; b < bunit.size(); ++b) boff[b + 1] = boff[b] + (bq1[b] - bq0[b]);
     MatchArgs a;
     memset(&a, 0, sizeof(a));
     fill_match_store(c, a);
+    const int64_t* d_boff = nullptr;
     const int32_t* d_win = nullptr;
     const int64_t *d_woff = nullptr, *d_lbeg = nullptr, *d_qoff = nullptr, *d_bq0 = nullptr, *d_bq1 = nullptr;
     const int32_t* d_bunit = nullptr;
@@ -689,8 +692,11 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     call.arg(bq0.data(), bq0.size(), &d_bq0);
     call.arg(bq1.data(), bq1.size(), &d_bq1);
     call.arg(params, 1, &d_prm);
+    call.arg(boff.data(), boff.size(), &d_boff);
     if (window_S) call.arg((const double*)window_S, 13 * (size_t)n_window, &d_S);
     call.commit();
+    Surv* d_surv = (Surv*)call.scratch(sizeof(Surv) * std::max<int64_t>(boff.back(), 1));
+    int32_t* d_scnt = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(bunit.size(), 1));
     const int32_t* d_list = call.in(mp_list, (size_t)n_list);
     unsigned long long* win = (unsigned long long*)call.out(io_winner, (size_t)n_wfeat, phase == LC_FUSE_APPLY);
     if (!win) win = (unsigned long long*)call.scratch(sizeof(uint64_t) * std::max<int64_t>(n_wfeat, 1));
@@ -748,6 +754,9 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       a.action = act;
       a.sole = sole ? 1 : 0;
       a.unit_base = w_lo;
+      a.surv = d_surv;
+      a.surv_off = d_boff;
+      a.surv_cnt = d_scnt;
       {
         Prof pr(c, LC_PROF_MATCH, call.s);
         CK(launch_match(c, 0, a, (int)bunit.size(), F_max, call.s));
@@ -813,6 +822,9 @@ lc_status lc_search_by_projection(lc_ctx* c, int32_t n_pairs, const int32_t* pai
         bq0.push_back(q);
         bq1.push_back(std::min<int64_t>(q + ch, pair_list_begin[p + 1]));
       }
+    std::vector<int64_t> boff(bunit.size() + 1, 0);
+    for (size_t b = 0; b < bunit.size(); ++b) boff[b + 1] = boff[b] + (bq1[b] - bq0[b]);
+    const int64_t* d_boff = nullptr;
     Call call(c, stream);
     const int32_t *d_kf = nullptr, *d_param = nullptr, *d_bunit = nullptr;
     const int64_t *d_off = nullptr, *d_lbeg = nullptr, *d_bq0 = nullptr, *d_bq1 = nullptr;
@@ -827,7 +839,10 @@ lc_status lc_search_by_projection(lc_ctx* c, int32_t n_pairs, const int32_t* pai
     call.arg(bq1.data(), bq1.size(), &d_bq1);
     call.arg((const double*)pair_S, 13 * (size_t)n_pairs, &d_S);
     call.arg(params, n_params, &d_prm);
+    call.arg(boff.data(), boff.size(), &d_boff);
     call.commit();
+    Surv* d_surv = (Surv*)call.scratch(sizeof(Surv) * std::max<int64_t>(boff.back(), 1));
+    int32_t* d_scnt = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(bunit.size(), 1));
     const int32_t* d_list = call.in(mp_list, (size_t)n_list);
     const int32_t* d_taken = call.in(pair_taken, (size_t)n_tot);
     int32_t* o_mp = call.out(out_feat_mp, (size_t)n_tot);
@@ -858,6 +873,9 @@ lc_status lc_search_by_projection(lc_ctx* c, int32_t n_pairs, const int32_t* pai
     a.out_dist = o_dist;
     a.sole = 0;
     a.unit_base = 0;
+    a.surv = d_surv;
+    a.surv_off = d_boff;
+    a.surv_cnt = d_scnt;
     a.winner = win;
     a.counts = cnt;
     a.n_mp = st.n_mp;

@@ -84,6 +84,14 @@ struct Store {
 };
 
 // Parameters of one matching launch, passed by value.
+// compacted survivor of the geometric culls (k_project -> k_match): 24 bytes, exact
+// fp64 projection (u, v).
+struct __align__(8) Surv {
+  int32_t q;
+  uint32_t jl;   // (position in the block's query range) | (level << 27)
+  double u, v;
+};
+
 struct MatchArgs {
   // store
   const double* kf_pose;  // unused by the kernel (units carry S)
@@ -133,6 +141,9 @@ struct MatchArgs {
   int32_t* out_mp;
   int32_t* out_dist;
   int32_t sole;        // 1: one CTA per unit -> the match CTA initialises and resolves its unit
+  Surv* surv;          // survivor buffer (k_project -> k_match), per-block regions
+  const int64_t* surv_off;  // [n_blocks] region start (= block query offset)
+  int32_t* surv_cnt;        // [n_blocks] survivors written
   int32_t unit_base;   // k_resolve: unit = unit_base + blockIdx.x
 };
 

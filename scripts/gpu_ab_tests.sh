@@ -1,0 +1,3 @@
+set -x
+python -m pytest tests -m gpu -q -x 2>&1 | tail -5
+bash scripts/ab.sh
