@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", default="lc", choices=["lc", "reference"])
     ap.add_argument("--config", default="C5")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--grid", default=os.environ.get("LC_GRID", "64x48"),
+                    help="per-keyframe cell grid COLSxROWS (GPU acceleration structure only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -216,7 +218,8 @@ def main():
         tdist.init_process_group("nccl", device_id=dev)
     w = make_world(args.config, args.seed)
     ctx = Context(local)
-    ctx.upload_map(w.map_arrays(), [w.cam])
+    grid = tuple(int(x) for x in args.grid.lower().split("x"))
+    ctx.upload_map(w.map_arrays(), [w.cam], grid=grid)
     ctx.state_save()
     stream = torch.cuda.current_stream(dev)
 
@@ -350,7 +353,7 @@ def main():
                                    f"{int(np.diff(w.kf_feat_begin).max())} feats/KF, "
                                    f"{len(w.window)}-KF fusion window, {len(w.mp_list)} queries "
                                    f"(WINDOW correct + fuse + ALL correct)",
-                       "seed": args.seed, "candidates_per_step": cand_total,
+                       "seed": args.seed, "candidates_per_step": cand_total, "grid": args.grid,
                        "parallelism": f"keyframe-sharded x{ws}" if ws > 1 else "1 GPU",
                        "l2": "flushed between steps (512 MB write) after an untimed state restore"},
             "ms_per_loop": round(ms_step, 5),

@@ -189,17 +189,32 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
   const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
   Surv* out = a.surv + a.surv_off[blockIdx.x];
   uint32_t cA = 0, cB = 0, cQ = 0;   // packed 10-bit counters (<= 64 queries per thread per block)
+  // software pipeline: the record of the next query and the list entry of the one
+  // after are in flight while the current query is evaluated
+  auto list_at = [&](int64_t jj) -> int32_t { return jj < q1 ? __ldg(a.mp_list + jj) : -1; };
+  auto rec_at = [&](int32_t qq, uint4& x0, uint4& x1, uint8_t& fl) {
+    if ((unsigned)qq < (unsigned)a.n_mp) {
+      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + qq);
+      x0 = __ldg(rp); x1 = __ldg(rp + 1); fl = __ldg(a.mp_flags + qq);
+    } else {
+      x0 = make_uint4(0, 0, 0, 0); x1 = x0; fl = 1;
+    }
+  };
+  int32_t q_nx = list_at(q0 + tid);
+  int32_t q_nn = list_at(q0 + tid + LC_NTHREADS);
+  uint4 n0, n1;
+  uint8_t nfl;
+  rec_at(q_nx, n0, n1, nfl);
   for (int64_t jb = q0; jb < q1; jb += LC_NTHREADS) {
     const int64_t j = jb + tid;
     const bool valid = j < q1;
-    const int32_t q = valid ? a.mp_list[j] : -1;
+    const int32_t q = q_nx;
+    const uint4 r0 = n0, r1 = n1;
+    const uint8_t flag = nfl;
     const bool in_range = valid && (unsigned)q < (unsigned)a.n_mp;
-    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0;
-    uint8_t flag = 1;
-    if (in_range) {
-      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + q);
-      r0 = __ldg(rp); r1 = __ldg(rp + 1); flag = __ldg(a.mp_flags + q);
-    }
+    q_nx = q_nn;
+    q_nn = list_at(j + 2 * LC_NTHREADS);
+    rec_at(q_nx, n0, n1, nfl);
     int status = 0;
     double u = 0.0, v = 0.0;
     int lvl = 0;
@@ -351,11 +366,14 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_match(const MatchArgs a) {
   const int ns_tot = a.surv_cnt[blockIdx.x];
   uint32_t cC = 0, cP = 0, cE = 0;   // NOCAND | OVERTH << 10 | RATIO << 20; PROP; CAND
 
+  // the next step's survivor entries are in flight while the current step runs
+  Surv e_nx;
+  e_nx.q = 0; e_nx.jl = 0u; e_nx.u = 0.0; e_nx.v = 0.0;
+  if (warp * 32 + lane < ns_tot) e_nx = sv[warp * 32 + lane];
   for (int i0 = warp * 32; i0 < ns_tot; i0 += NWARP * 32) {
     const bool act = i0 + lane < ns_tot;
-    Surv e;
-    e.q = 0; e.jl = 0u; e.u = 0.0; e.v = 0.0;
-    if (act) e = sv[i0 + lane];
+    const Surv e = e_nx;
+    if (i0 + NWARP * 32 + lane < ns_tot) e_nx = sv[i0 + NWARP * 32 + lane];
     const int lvl = (int)(e.jl >> 27);
     const double r = (double)prm.th * a.scale[lvl];
     uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;

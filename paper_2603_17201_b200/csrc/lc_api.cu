@@ -110,27 +110,29 @@ struct Call {
   void commit() {
     if (args.empty()) return;
     size_t bytes = round_up(args.size(), 16);
-    if (c->pin_ev_pending) {
-      CK(cudaEventSynchronize(c->pin_ev));
-      c->pin_ev_pending = false;
+    const int r = c->pin_next;
+    c->pin_next = (r + 1) % lc_ctx::kPinRing;
+    if (c->pin_ev_pending[r]) {
+      CK(cudaEventSynchronize(c->pin_ev[r]));
+      c->pin_ev_pending[r] = false;
     }
-    if (c->pin_cap < bytes) {
-      if (c->pin) CK(cudaFreeHost(c->pin));
-      c->pin = nullptr;
-      c->pin_cap = 0;
+    if (c->pin_cap[r] < bytes) {
+      if (c->pin[r]) CK(cudaFreeHost(c->pin[r]));
+      c->pin[r] = nullptr;
+      c->pin_cap[r] = 0;
       size_t cap = std::max<size_t>(bytes * 2, 1 << 16);
-      if (cudaHostAlloc(&c->pin, cap, cudaHostAllocDefault) != cudaSuccess) {
+      if (cudaHostAlloc(&c->pin[r], cap, cudaHostAllocDefault) != cudaSuccess) {
         cudaGetLastError();
         set_err(c, "pinned staging allocation failed");
         throw Fail{LC_ENOMEM};
       }
-      c->pin_cap = cap;
+      c->pin_cap[r] = cap;
     }
-    memcpy(c->pin, args.data(), args.size());
+    memcpy(c->pin[r], args.data(), args.size());
     d_args = (char*)scratch(bytes);
-    CK(cudaMemcpyAsync(d_args, c->pin, bytes, cudaMemcpyHostToDevice, s));
-    CK(cudaEventRecord(c->pin_ev, s));
-    c->pin_ev_pending = true;
+    CK(cudaMemcpyAsync(d_args, c->pin[r], bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(c->pin_ev[r], s));
+    c->pin_ev_pending[r] = true;
     for (auto& f : arg_fix) *f.first = d_args + f.second;
   }
 
@@ -302,8 +304,12 @@ lc_status lc_create(lc_ctx** out, int32_t device) {
   lc_ctx* c = new (std::nothrow) lc_ctx();
   if (!c) return LC_ENOMEM;
   c->device = device;
-  if (cudaSetDevice(device) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->pin_ev, cudaEventDisableTiming) != cudaSuccess) {
+  bool ok = cudaSetDevice(device) == cudaSuccess;
+  for (int r = 0; ok && r < lc_ctx::kPinRing; ++r)
+    ok = cudaEventCreateWithFlags(&c->pin_ev[r], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    for (int r = 0; r < lc_ctx::kPinRing; ++r)
+      if (c->pin_ev[r]) cudaEventDestroy(c->pin_ev[r]);
     cudaGetLastError();
     g_create_err = "CUDA context setup failed";
     delete c;
@@ -320,9 +326,11 @@ lc_status lc_destroy(lc_ctx* c) {
   free_store(c->st);
   for (void* p : c->scr_ptr)
     if (p) cudaFree(p);
-  if (c->pin) cudaFreeHost(c->pin);
+  for (int r = 0; r < lc_ctx::kPinRing; ++r) {
+    if (c->pin[r]) cudaFreeHost(c->pin[r]);
+    if (c->pin_ev[r]) cudaEventDestroy(c->pin_ev[r]);
+  }
   if (c->sv) cudaFree(c->sv);
-  if (c->pin_ev) cudaEventDestroy(c->pin_ev);
   for (auto& r : c->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   cudaGetLastError();

@@ -159,12 +159,14 @@ struct lc_ctx {
   // scratch arena: named growable device buffers
   std::vector<void*> scr_ptr;
   std::vector<size_t> scr_cap;
-  // pinned staging ring
-  void* pin = nullptr;
-  size_t pin_cap = 0;
-  size_t pin_used = 0;
-  cudaEvent_t pin_ev = nullptr;  // recorded after the last H2D out of staging
-  bool pin_ev_pending = false;
+  // pinned staging ring: argument blocks of the last kPinRing calls may still be in
+  // flight, so the host only waits when it laps the ring (not on every call)
+  static constexpr int kPinRing = 8;
+  void* pin[kPinRing] = {};
+  size_t pin_cap[kPinRing] = {};
+  cudaEvent_t pin_ev[kPinRing] = {};   // recorded after the H2D out of that slot
+  bool pin_ev_pending[kPinRing] = {};
+  int pin_next = 0;
   // saved state (lc_state_save)
   void* sv = nullptr;
   size_t sv_cap = 0;
