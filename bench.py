@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--grid", default=os.environ.get("LC_GRID", "64x48"),
                     help="per-keyframe cell grid COLSxROWS (GPU acceleration structure only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="skip the secondary measurement of the step replayed as a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--profile-only", action="store_true",
@@ -106,12 +108,15 @@ class Clocks:
 
 
 def roofline_bytes(w, n_queries, n_proposals):
-    """Algorithmic bytes of one k_project_match<fuse> launch (SURVEY.md §8(d) per-unit
-    figures): 48 B per window-keyframe feature (the keyframe block:
-    uv 8 + octave/index 4 + descriptor 32 + association 4), 68 B per query (list entry 4 +
-    64-B map-point record), 8 B per proposal (winner word)."""
+    """Algorithmic bytes of the fuse matching stage (SURVEY.md §8(d) per-unit figures;
+    DESIGN.md "Roofline"), split by the kernel that moves them:
+      k_project: 68 B per query (list entry 4 + 64-B map-point record);
+      k_match:   48 B per window-keyframe feature (uv 8 + octave/index 4 + descriptor 32
+                 + association 4) + 8 B per proposal (winner word).
+    The survivor buffer between the two kernels is an L2-resident intermediate and is not
+    counted (it is not algorithmic traffic)."""
     n_wfeat = int(np.sum(np.diff(w.kf_feat_begin)[w.window]))
-    return 48 * n_wfeat + 68 * int(n_queries) + 8 * int(n_proposals)
+    return {"k_project": 68 * int(n_queries), "k_match": 48 * n_wfeat + 8 * int(n_proposals)}
 
 
 def load_peaks():
@@ -291,22 +296,32 @@ def main():
     cand_total = int(cand_t.item())
     value = cand_total / (ms_step / 1000.0)
 
-    # roofline of the dominant kernel (k_project_match<fuse>)
-    match_ms = prof["match"][0] / args.steps
+    # roofline of the dominant stage: fuse matching = k_project -> k_match (one launch each
+    # per step in this configuration), per-kernel device time from lc_profile events
     fam_ms = {k: v[0] / args.steps for k, v in prof.items() if v[1]}
-    B = roofline_bytes(w, q_rank, prop_rank) if ws == 1 else None
+    Bk = roofline_bytes(w, q_rank, prop_rank) if ws == 1 else None
     peaks = load_peaks()
     peak = peaks.get("hbm_gbs")
-    peak_src = "measured" if peak else "fallback"
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md)"
     peak = peak or 6650.0
-    traffic = load_traffic().get("k_project_match_fuse", {}).get(args.config)
+    traffic = load_traffic().get("match_stage", {}).get(args.config)
     roof = None
-    if B is not None and match_ms > 0:
-        ach = B / (match_ms / 1000.0) / 1e9
+    stage_ms = fam_ms.get("project", 0.0) + fam_ms.get("match", 0.0)
+    if Bk is not None and stage_ms > 0:
+        B = sum(Bk.values())
+        ach = B / (stage_ms / 1000.0) / 1e9
+        per = {}
+        for kname, fam in (("k_project", "project"), ("k_match", "match")):
+            kms = fam_ms.get(fam, 0.0)
+            if kms > 0:
+                a_k = Bk[kname] / (kms / 1000.0) / 1e9
+                per[kname] = {"ms": round(kms, 5), "bytes": Bk[kname], "achieved": round(a_k, 1),
+                              "frac": round(a_k / peak, 4)}
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": traffic, "kernel": "k_project_match<fuse>",
-                "algorithmic_bytes": B, "kernel_ms": round(match_ms, 5), "peak_source": peak_src,
-                "step_share": round(match_ms / ms_step, 4)}
+                "frac": round(ach / peak, 4), "traffic": traffic,
+                "kernel": "fuse matching stage: k_project -> k_match",
+                "algorithmic_bytes": B, "kernel_ms": round(stage_ms, 5), "peak_source": peak_src,
+                "step_share": round(stage_ms / ms_step, 4), "kernels": per}
 
     # e2e through the public API with host (pinned) buffers: H2D of the loop event's
     # inputs and D2H of its result (counts + victim table) inside the timed region
@@ -339,6 +354,32 @@ def main():
         e2e = {"value": cand_rank / (e_ms / 1000.0), "unit": UNIT, "ms_per_step": round(e_ms, 4),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
+    # secondary: the same step captured once (lc_graph_*) and replayed; host capture +
+    # instantiate time reported beside it (a new loop event needs a new capture)
+    graph = None
+    if ws == 1 and not args.no_graph and not args.profile_only:
+        reset()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with ctx.capture() as cap:
+            step()
+        torch.cuda.synchronize()
+        cap_ms = 1000.0 * (time.perf_counter() - t0)
+        gms = []
+        for i in range(args.warmup + args.steps):
+            reset()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            cap.graph.launch()
+            b.record(stream)
+            b.synchronize()
+            if i >= args.warmup:
+                gms.append(a.elapsed_time(b))
+        g_ms = float(np.mean(gms))
+        graph = {"ms_per_step": round(g_ms, 5), "value": round(cand_total / (g_ms / 1000.0), 1),
+                 "capture_instantiate_ms": round(cap_ms, 3)}
+        cap.graph.close()
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_only:
         cpu = cpu_baseline(w, args.cpu_seconds)
@@ -362,6 +403,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "graph": graph,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

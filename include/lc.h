@@ -222,9 +222,42 @@ int64_t lc_kernel_launches(const lc_ctx* ctx);
  * ------------------------------------------------------------------------- */
 enum { LC_PROF_UPLOAD = 0, LC_PROF_CORRECT_WINDOW, LC_PROF_CORRECT_ALL, LC_PROF_FUSE_PREP,
        LC_PROF_MATCH, LC_PROF_RESOLVE, LC_PROF_APPLY, LC_PROF_SBP_MATCH, LC_PROF_SBP_RESOLVE,
-       LC_PROF_STATE, LC_NPROF };
+       LC_PROF_STATE, LC_PROF_PROJECT, LC_NPROF };
 lc_status lc_profile_enable(lc_ctx* ctx, int32_t on);
 lc_status lc_profile_read(lc_ctx* ctx, double* ms, int64_t* launches);
+
+/* ---------------------------------------------------------------------------
+ * CUDA-graph capture: one loop event (lc_correct_sim3 WINDOW -> lc_fuse ->
+ * lc_correct_sim3 ALL, or any sequence of lc_correct_sim3 / lc_fuse /
+ * lc_search_by_projection calls) recorded once and replayed as a single graph
+ * launch, removing per-call host work and inter-kernel launch gaps.
+ *
+ * lc_graph_begin(ctx, stream): opens a capture on `stream` (non-NULL, owned by
+ *   the caller; relaxed capture mode). Until lc_graph_end, the calls above on
+ *   `stream` are validated and RECORDED, not executed. Their [host] control
+ *   arrays (window, window_S, parameters, ...) are copied at capture time into
+ *   graph-owned device memory and are constants of the graph. Their [host|dev]
+ *   data buffers must be device memory or page-locked host memory: they are
+ *   read/written at every replay (so a pinned input can be refreshed between
+ *   replays). Every other lc call, and any call on another stream, fails with
+ *   LC_ESTATE while a capture is open. A failing call aborts the capture.
+ * lc_graph_end(ctx, stream, out): closes the capture, instantiates the graph
+ *   and returns it in *out (owned by the caller; lc_graph_destroy).
+ * lc_graph_launch(ctx, graph, stream): replays the recorded calls on `stream`
+ *   (stream-ordered; any stream). Each replay of a fuse call takes a fresh
+ *   LoopSet epoch from a device counter, so replays are independent loop events.
+ *   Profiling families are not recorded for replays; lc_kernel_launches counts
+ *   the graph's kernels per replay. The host-side validation mirror of the
+ *   stored WINDOW corrections reflects the capture, not the replays.
+ * lc_graph_destroy(ctx, graph): synchronises the device and frees the graph and
+ *   its buffers. Errors: LC_EINVAL (NULL / foreign graph), LC_ESTATE (no map,
+ *   capture already open / not open), LC_ECUDA (capture or instantiate failed).
+ * ------------------------------------------------------------------------- */
+typedef struct lc_graph lc_graph;
+lc_status lc_graph_begin(lc_ctx* ctx, void* cuda_stream);
+lc_status lc_graph_end(lc_ctx* ctx, void* cuda_stream, lc_graph** out);
+lc_status lc_graph_launch(lc_ctx* ctx, lc_graph* graph, void* cuda_stream);
+lc_status lc_graph_destroy(lc_ctx* ctx, lc_graph* graph);
 
 /* ---------------------------------------------------------------------------
  * lc_upload_map -- GPU-resident keyframe storage.

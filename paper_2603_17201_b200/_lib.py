@@ -25,7 +25,7 @@ COUNTER_NAMES = [
 ]
 LC_NCOUNT = len(COUNTER_NAMES)
 PROF_NAMES = ["upload", "correct_window", "correct_all", "fuse_prep", "match", "resolve", "apply",
-              "sbp_match", "sbp_resolve", "state"]
+              "sbp_match", "sbp_resolve", "state", "project"]
 
 
 class lc_sim3(C.Structure):
@@ -102,6 +102,10 @@ def load():
                           vp, vp, vp, vp, vp]),
         "lc_search_by_projection": (i32, [vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp,
                                           vp, vp]),
+        "lc_graph_begin": (i32, [vp, vp]),
+        "lc_graph_end": (i32, [vp, vp, P(vp)]),
+        "lc_graph_launch": (i32, [vp, vp, vp]),
+        "lc_graph_destroy": (i32, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -115,4 +119,5 @@ def exported_symbols():
     return ["lc_create", "lc_destroy", "lc_last_error", "lc_kernel_launches", "lc_profile_enable",
             "lc_profile_read", "lc_upload_map",
             "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse",
-            "lc_search_by_projection"]
+            "lc_search_by_projection", "lc_graph_begin", "lc_graph_end", "lc_graph_launch",
+            "lc_graph_destroy"]

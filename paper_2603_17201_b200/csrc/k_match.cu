@@ -118,6 +118,12 @@ template <int MODE>
 __device__ void resolve_unit(const MatchArgs& a, int unit);
 
 constexpr int NWARP = LC_NTHREADS / 32;
+#ifndef LC_KM_MINB
+#define LC_KM_MINB 3      // k_match CTAs per SM the register budget is cut for
+#endif
+#ifndef LC_KM_PF
+#define LC_KM_PF 0        // L1 prefetch of a candidate's descriptor when it is recorded
+#endif
 constexpr int CPL = 6;            // candidate slots per survivor (more -> serial fallback)
 
 __device__ __forceinline__ uint32_t hslot(int32_t key, uint32_t size) {
@@ -143,14 +149,21 @@ __device__ __forceinline__ bool hhas(const int32_t* tab, uint32_t size, int32_t 
 
 template <int FCAP>
 struct HashSize {
-  static constexpr int HS = ((FCAP + FCAP / 8 + 1) + 31) & ~31;
+  static constexpr int HS = ((2 * FCAP + 1) + 31) & ~31;   // load factor <= 0.5
 };
+// membership pre-filter over the keyframe's associations: 2^15 bits, one hash
+// (a miss -- the common case -- costs one shared-memory load instead of a probe run)
+constexpr int FILT_LOG2 = 15;
+__device__ __forceinline__ uint32_t fslot(int32_t key) {
+  return ((uint32_t)key * 0x85EBCA6Bu) >> (32 - FILT_LOG2);
+}
 
 // ---- k_project ---------------------------------------------------------------
 template <int MODE, int FCAP>
 __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
   constexpr uint32_t HS = (uint32_t)HashSize<FCAP>::HS;
-  __shared__ int32_t s_hash[HS];
+  extern __shared__ __align__(16) int32_t s_hash[];   // [HS] (dynamic: up to 64 KB)
+  __shared__ uint32_t s_filt[1 << (FILT_LOG2 - 5)];
   __shared__ double s_T[12];
   __shared__ double s_Ow[3];
   __shared__ DevCam s_cam;
@@ -174,10 +187,15 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
     s_cnt = 0;
   }
   for (int i = tid; i < (int)HS; i += LC_NTHREADS) s_hash[i] = -1;
+  for (int i = tid; i < (1 << (FILT_LOG2 - 5)); i += LC_NTHREADS) s_filt[i] = 0u;
   __syncthreads();
   for (int f = tid; f < F; f += LC_NTHREADS) {
     int32_t m = (MODE == 0) ? a.feat_mp[fb + f] : (a.taken ? a.taken[toff + f] : -1);
-    if (m >= 0) hins(s_hash, HS, m);
+    if (m >= 0) {
+      const uint32_t b = fslot(m);
+      atomicOr(&s_filt[b >> 5], 1u << (b & 31));
+      hins(s_hash, HS, m);
+    }
   }
   __syncthreads();
   const int L = a.n_levels;
@@ -222,7 +240,10 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
       cQ += 1u;
       do {
         if (!in_range || (flag & 1u)) { status = LC_Q_BAD; cA += 1u; break; }
-        if (hhas(s_hash, HS, q)) { status = LC_Q_FOUND; cA += 1u << 10; break; }
+        const uint32_t fb2 = fslot(q);
+        if (((s_filt[fb2 >> 5] >> (fb2 & 31)) & 1u) && hhas(s_hash, HS, q)) {
+          status = LC_Q_FOUND; cA += 1u << 10; break;
+        }
         const double p0 = __uint_as_float(r0.x), p1 = __uint_as_float(r0.y), p2 = __uint_as_float(r0.z);
         const double z = (s_T[6] * p0 + s_T[7] * p1) + s_T[8] * p2 + s_T[11];
         if (z <= 0.0) { status = LC_Q_DEPTH; cA += 1u << 20; break; }
@@ -303,7 +324,7 @@ struct MatchSmem {
 };
 
 template <int MODE, int FCAP>
-__global__ void __launch_bounds__(LC_NTHREADS, 3) k_match(const MatchArgs a) {
+__global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchArgs a) {
   using SM = MatchSmem<FCAP>;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t s_bar;
@@ -404,7 +425,12 @@ __global__ void __launch_bounds__(LC_NTHREADS, 3) k_match(const MatchArgs a) {
           if (!(f32ok && du < fr - 1e-3f && dv < fr - 1e-3f) &&
               !(fabs((double)fuv.x - e.u) < r && fabs((double)fuv.y - e.v) < r))
             continue;
-          if (nc < CPL) s_cand[lane * CPL + nc] = (uint16_t)p;
+          if (nc < CPL) {
+            s_cand[lane * CPL + nc] = (uint16_t)p;
+#if LC_KM_PF
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.fc_desc + 2 * (size_t)(fp + p)));
+#endif
+          }
           ++nc;
         }
       }
@@ -535,6 +561,7 @@ __device__ void resolve_unit(const MatchArgs& a, int unit) {
   const int64_t toff = (MODE == 1 && a.taken) ? a.unit_toff[unit] : 0;
   const lc_match_params prm = a.params[(MODE == 1 && a.unit_param) ? a.unit_param[unit] : 0];
   unsigned long long* winner = a.winner;
+  const uint32_t epoch = MODE == 0 ? *a.epoch : 0u;
   uint32_t cnt[R_N];
 #pragma unroll
   for (int i = 0; i < R_N; ++i) cnt[i] = 0;
@@ -562,36 +589,69 @@ __device__ void resolve_unit(const MatchArgs& a, int unit) {
     }
     __syncthreads();
   }
-  for (int f = threadIdx.x; f < F; f += blockDim.x) {
-    unsigned long long w = winner[woff + f];
-    int8_t act = 0;
-    if (w != NONE) {
-      cnt[R_WINNERS]++;
-      int q = (int)(w & 0xFFFFFFFFull);
-      if (prm.check_orientation) {
-        int b = rot_bin(a.feat_angle[fb + f], a.mp_rec[q].angle);
+  // RB features per thread per pass with every load of a phase issued together:
+  // (winner, association) -> orientation -> (flags, LoopSet stamp) of held slots
+  constexpr int RB = 8;
+  const int nt = blockDim.x;
+  for (int f0 = threadIdx.x; f0 < F; f0 += RB * nt) {
+    unsigned long long w[RB];
+    int32_t slot[RB];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      const int f = f0 + i * nt;
+      w[i] = f < F ? winner[woff + f] : NONE;
+      slot[i] = (MODE == 0 && f < F) ? a.feat_mp[fb + f] : -1;
+    }
+    int8_t act[RB];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+      act[i] = 0;
+      if (w[i] != NONE) cnt[R_WINNERS]++;
+    }
+    if (prm.check_orientation) {
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        if (w[i] == NONE) continue;
+        const int f = f0 + i * nt;
+        const int b = rot_bin(a.feat_angle[fb + f], a.mp_rec[(int)(w[i] & 0xFFFFFFFFull)].angle);
         if (b != s_keep[0] && b != s_keep[1] && b != s_keep[2]) {
-          w = NONE;
+          w[i] = NONE;
           winner[woff + f] = NONE;
           cnt[R_ORIENT]++;
-          act = 4;
+          act[i] = 4;
         }
-      }
-      if (MODE == 0 && w != NONE) {
-        int slot = a.feat_mp[fb + f];
-        if (slot < 0) { act = 1; cnt[R_ADD]++; }
-        else if (a.mp_flags[slot] & 1u) { act = 5; cnt[R_BADSLOT]++; }
-        else if (a.loop_ep[slot] == a.epoch) { act = 3; cnt[R_LOOP]++; }
-        else { act = 2; cnt[R_VICTIM]++; atomicMin(&a.victim[slot], w); }
       }
     }
     if (MODE == 0) {
-      if (a.action) a.action[woff + f] = act;
+      uint8_t fl[RB];
+      uint32_t ep[RB];
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        const bool held = w[i] != NONE && slot[i] >= 0;
+        fl[i] = held ? a.mp_flags[slot[i]] : 0;
+        ep[i] = held ? a.loop_ep[slot[i]] : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        const int f = f0 + i * nt;
+        if (w[i] != NONE) {
+          if (slot[i] < 0) { act[i] = 1; cnt[R_ADD]++; }
+          else if (fl[i] & 1u) { act[i] = 5; cnt[R_BADSLOT]++; }
+          else if (ep[i] == epoch) { act[i] = 3; cnt[R_LOOP]++; }
+          else { act[i] = 2; cnt[R_VICTIM]++; atomicMin(&a.victim[slot[i]], w[i]); }
+        }
+        if (a.action && f < F) a.action[woff + f] = act[i];
+      }
     } else {
-      int t = a.taken ? a.taken[toff + f] : -1;
-      if (t >= 0) { a.out_mp[woff + f] = t; a.out_dist[woff + f] = -1; }
-      else if (w != NONE) { a.out_mp[woff + f] = (int)(w & 0xFFFFFFFFull); a.out_dist[woff + f] = (int)(w >> 32); }
-      else { a.out_mp[woff + f] = -1; a.out_dist[woff + f] = -1; }
+#pragma unroll
+      for (int i = 0; i < RB; ++i) {
+        const int f = f0 + i * nt;
+        if (f >= F) continue;
+        const int t = a.taken ? a.taken[toff + f] : -1;
+        if (t >= 0) { a.out_mp[woff + f] = t; a.out_dist[woff + f] = -1; }
+        else if (w[i] != NONE) { a.out_mp[woff + f] = (int)(w[i] & 0xFFFFFFFFull); a.out_dist[woff + f] = (int)(w[i] >> 32); }
+        else { a.out_mp[woff + f] = -1; a.out_dist[woff + f] = -1; }
+      }
     }
   }
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
@@ -603,14 +663,18 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_resolve(const MatchArgs a) {
   resolve_unit<MODE>(a, a.unit_base + blockIdx.x);
 }
 
-// Per-call setup: LoopSet stamps, winner/victim init, window membership.
-__global__ void k_fuse_prep(int phase, int init_winner, uint32_t epoch, int n_w,
+// Per-call setup: LoopSet stamps, winner/victim init, window membership. The call's
+// epoch is ep[0] + 1 (device counter, so that a replayed CUDA graph gets a fresh one);
+// the last block to finish publishes it in ep[0] for the kernels that follow.
+__global__ void k_fuse_prep(int phase, int init_winner, uint32_t* __restrict__ ep, int n_w,
                             const int32_t* __restrict__ window, int64_t n_wfeat,
                             const int32_t* __restrict__ mp_list, int64_t n_list, int n_mp,
                             unsigned long long* __restrict__ winner,
                             unsigned long long* __restrict__ victim, uint32_t* __restrict__ loop_ep,
                             uint32_t* __restrict__ kf_win_ep, int32_t* __restrict__ kf_win_pos,
                             uint32_t* __restrict__ vbits, int n_vbits, int32_t* __restrict__ dirty_n) {
+  uint32_t epoch = ep[0] + 1u;
+  if (epoch == 0u) epoch = 1u;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   for (int64_t i = t0; i < n_w; i += stride) {
@@ -619,14 +683,24 @@ __global__ void k_fuse_prep(int phase, int init_winner, uint32_t epoch, int n_w,
   }
   for (int64_t i = t0; i < n_vbits; i += stride) vbits[i] = 0u;
   if (t0 == 0) *dirty_n = 0;
-  if (!(phase & LC_FUSE_PLAN)) return;
-  for (int64_t i = t0; i < n_list; i += stride) {
-    const int32_t q = mp_list[i];
-    if ((unsigned)q < (unsigned)n_mp) loop_ep[q] = epoch;
+  if (phase & LC_FUSE_PLAN) {
+    for (int64_t i = t0; i < n_list; i += stride) {
+      const int32_t q = mp_list[i];
+      if ((unsigned)q < (unsigned)n_mp) loop_ep[q] = epoch;
+    }
+    if (init_winner)
+      for (int64_t i = t0; i < n_wfeat; i += stride) winner[i] = NONE;
+    for (int64_t i = t0; i < n_mp; i += stride) victim[i] = NONE;
   }
-  if (init_winner)
-    for (int64_t i = t0; i < n_wfeat; i += stride) winner[i] = NONE;
-  for (int64_t i = t0; i < n_mp; i += stride) victim[i] = NONE;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ep[1], 1u) == gridDim.x - 1) {
+      ep[0] = epoch;
+      ep[1] = 0u;
+      __threadfence();
+    }
+  }
 }
 
 // Victim marking: flags |= bad, replaced_by = survivor (reading O9 (iv)), victim bitmap.
@@ -659,10 +733,12 @@ __global__ void k_fuse_victims(int n_mp, const unsigned long long* __restrict__ 
 // winner on an empty window slot) -> compact list. One warp per keyframe, 16-B loads,
 // no shared memory (the victim bitmap stays L1-resident).
 __global__ void __launch_bounds__(LC_NTHREADS) k_apply_mark(
-    int n_kf, uint32_t epoch, const int32_t* __restrict__ kf_fbeg, const uint32_t* __restrict__ kf_win_ep,
-    const int32_t* __restrict__ kf_win_pos, const int64_t* __restrict__ woff_of_pos,
-    const unsigned long long* __restrict__ winner, const uint32_t* __restrict__ vbits,
-    const int32_t* __restrict__ feat_mp, int32_t* __restrict__ dirty_list) {
+    int n_kf, const uint32_t* __restrict__ ep, const int32_t* __restrict__ kf_fbeg,
+    const uint32_t* __restrict__ kf_win_ep, const int32_t* __restrict__ kf_win_pos,
+    const int64_t* __restrict__ woff_of_pos, const unsigned long long* __restrict__ winner,
+    const uint32_t* __restrict__ vbits, const int32_t* __restrict__ feat_mp,
+    int32_t* __restrict__ dirty_list) {
+  const uint32_t epoch = *ep;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -709,12 +785,13 @@ __device__ __constant__ int kApplySlot[A_N] = {LC_COUNT_REWIRED, LC_COUNT_DUP_CL
                                                LC_COUNT_ADDED};
 
 __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
-    uint32_t epoch, const int32_t* __restrict__ kf_fbeg, const uint32_t* __restrict__ kf_win_ep,
-    const int32_t* __restrict__ kf_win_pos, const int64_t* __restrict__ woff_of_pos,
-    const unsigned long long* __restrict__ winner, const unsigned long long* __restrict__ victim,
-    const uint32_t* __restrict__ vbits, const int32_t* __restrict__ dirty_list,
-    int32_t* __restrict__ feat_mp, int32_t* __restrict__ nobs, int hash_size,
-    unsigned long long* __restrict__ counts) {
+    const uint32_t* __restrict__ ep, const int32_t* __restrict__ kf_fbeg,
+    const uint32_t* __restrict__ kf_win_ep, const int32_t* __restrict__ kf_win_pos,
+    const int64_t* __restrict__ woff_of_pos, const unsigned long long* __restrict__ winner,
+    const unsigned long long* __restrict__ victim, const uint32_t* __restrict__ vbits,
+    const int32_t* __restrict__ dirty_list, int32_t* __restrict__ feat_mp, int32_t* __restrict__ nobs,
+    int hash_size, unsigned long long* __restrict__ counts) {
+  const uint32_t epoch = *ep;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t cnt[A_N] = {0, 0, 0};
   const int nd = dirty_list[0];
@@ -813,33 +890,40 @@ int grid_for(int64_t n) {
 }  // namespace
 
 template <int MODE, int FCAP>
-cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, cudaStream_t s) {
+cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, int part, cudaStream_t s) {
   using SM = MatchSmem<FCAP>;
-  k_project<MODE, FCAP><<<n_blocks, LC_NTHREADS, 0, s>>>(a);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (part == 0) {
+    const int hb = HashSize<FCAP>::HS * (int)sizeof(int32_t);
+    cudaError_t e = cudaFuncSetAttribute(k_project<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, hb);
+    if (e != cudaSuccess) return e;
+    k_project<MODE, FCAP><<<n_blocks, LC_NTHREADS, hb, s>>>(a);
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)SM::CELL + (((size_t)a.Gs * 2 + 15) & ~(size_t)15);
-  e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
   k_match<MODE, FCAP><<<n_blocks, LC_NTHREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int MODE>
-cudaError_t launch_match_m(const MatchArgs& a, int n_blocks, int F_max, cudaStream_t s) {
-  if (F_max <= 512) return launch_match_t<MODE, 512>(a, n_blocks, s);
-  if (F_max <= 1024) return launch_match_t<MODE, 1024>(a, n_blocks, s);
-  if (F_max <= 2048) return launch_match_t<MODE, 2048>(a, n_blocks, s);
-  if (F_max <= 4096) return launch_match_t<MODE, 4096>(a, n_blocks, s);
-  return launch_match_t<MODE, 8192>(a, n_blocks, s);
+cudaError_t launch_match_m(const MatchArgs& a, int n_blocks, int F_max, int part, cudaStream_t s) {
+  if (F_max <= 512) return launch_match_t<MODE, 512>(a, n_blocks, part, s);
+  if (F_max <= 1024) return launch_match_t<MODE, 1024>(a, n_blocks, part, s);
+  if (F_max <= 2048) return launch_match_t<MODE, 2048>(a, n_blocks, part, s);
+  if (F_max <= 4096) return launch_match_t<MODE, 4096>(a, n_blocks, part, s);
+  return launch_match_t<MODE, 8192>(a, n_blocks, part, s);
 }
 
-cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max,
+cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max, int part,
                          cudaStream_t s) {
   if (n_blocks <= 0) return cudaSuccess;
-  cudaError_t e = mode == 0 ? launch_match_m<0>(a, n_blocks, F_max, s)
-                            : launch_match_m<1>(a, n_blocks, F_max, s);
-  c->launches += 2;
+  cudaError_t e = mode == 0 ? launch_match_m<0>(a, n_blocks, F_max, part, s)
+                            : launch_match_m<1>(a, n_blocks, F_max, part, s);
+  c->launches += 1;
   return e;
 }
 
@@ -862,7 +946,7 @@ cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, con
     if (init_winner) n = std::max<int64_t>(n, n_wfeat);
     n = std::max<int64_t>(n, st.n_mp);
   }
-  k_fuse_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(phase, init_winner, c->epoch, n_w, d_window, n_wfeat,
+  k_fuse_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(phase, init_winner, st.ep, n_w, d_window, n_wfeat,
                                                  mp_list, n_list_total, st.n_mp, winner, victim,
                                                  st.mp_loop_ep, st.kf_win_ep, st.kf_win_pos,
                                                  st.mp_vbits, n_vbits, st.kf_dirty);
@@ -881,7 +965,7 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
   }
   if (st.n_kf > 0) {
     k_apply_mark<<<std::min((st.n_kf + NWARP - 1) / NWARP, 148 * 8), LC_NTHREADS, 0, s>>>(
-        st.n_kf, c->epoch, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos, d_woff, winner, st.mp_vbits,
+        st.n_kf, st.ep, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos, d_woff, winner, st.mp_vbits,
         st.feat_mp, st.kf_dirty);
     const int Fm = st.max_F > 0 ? st.max_F : 1;
     const int H = ((Fm + Fm / 2 + 1) + 31) & ~31;
@@ -890,7 +974,7 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
     cudaError_t e = cudaFuncSetAttribute(k_apply_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_apply_fix<<<std::min(st.n_kf, 148 * 4), LC_NTHREADS, smem, s>>>(
-        c->epoch, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos, d_woff, winner, victim, st.mp_vbits,
+        st.ep, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos, d_woff, winner, victim, st.mp_vbits,
         st.kf_dirty, st.feat_mp, st.mp_nobs, H, counts);
     c->launches += 2;
   }

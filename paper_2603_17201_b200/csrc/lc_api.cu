@@ -75,6 +75,7 @@ struct Call {
 
   void* scratch(size_t bytes) {
     bytes = std::max<size_t>(round_up(bytes, 256), 256);
+    if (c->cap) return graph_alloc(bytes);
     if ((int)c->scr_ptr.size() <= slot) {
       c->scr_ptr.push_back(nullptr);
       c->scr_cap.push_back(0);
@@ -97,6 +98,27 @@ struct Call {
     return c->scr_ptr[slot++];
   }
 
+  // capture: buffers the graph references are its own (freed with it)
+  void* graph_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      set_err(c, "graph scratch allocation failed");
+      throw Fail{LC_ENOMEM};
+    }
+    c->cap->dev.push_back(p);
+    return p;
+  }
+
+  // capture: a [host|dev] host pointer becomes a memcpy node read/written at every
+  // replay, so it must stay valid -> page-locked memory only
+  void require_pinned(const void* p) {
+    cudaPointerAttributes at;
+    const bool ok = cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    REQUIRE(ok, LC_EINVAL, "while capturing, host data buffers must be page-locked (pinned)");
+  }
+
   // small [host] control array -> device copy inside the argument block
   template <typename T>
   void arg(const T* host, size_t n, const T** dev_out) {
@@ -106,10 +128,18 @@ struct Call {
     arg_fix.push_back({(const void**)dev_out, off});
   }
 
-  // stage the argument block: one pinned memcpy + one H2D
+  // stage the argument block: one pinned memcpy + one H2D. While capturing, the block
+  // is uploaded once into graph-owned memory (its values are constants of the graph).
   void commit() {
     if (args.empty()) return;
     size_t bytes = round_up(args.size(), 16);
+    if (c->cap) {
+      d_args = (char*)graph_alloc(bytes);
+      CK(cudaMemcpyAsync(d_args, args.data(), args.size(), cudaMemcpyHostToDevice, c->side));
+      CK(cudaStreamSynchronize(c->side));
+      for (auto& f : arg_fix) *f.first = d_args + f.second;
+      return;
+    }
     const int r = c->pin_next;
     c->pin_next = (r + 1) % lc_ctx::kPinRing;
     if (c->pin_ev_pending[r]) {
@@ -141,6 +171,7 @@ struct Call {
   const T* in(const T* p, size_t n) {
     if (!p || n == 0) return p;
     if (is_device_ptr(c, p)) return p;
+    if (c->cap) require_pinned(p);
     T* d = (T*)scratch(sizeof(T) * n);
     CK(cudaMemcpyAsync(d, p, sizeof(T) * n, cudaMemcpyDefault, s));
     return d;
@@ -152,6 +183,7 @@ struct Call {
     if (!p) return nullptr;
     if (n == 0) return p;
     if (is_device_ptr(c, p)) return p;
+    if (c->cap) require_pinned(p);
     T* d = (T*)scratch(sizeof(T) * n);
     if (copy_in) CK(cudaMemcpyAsync(d, p, sizeof(T) * n, cudaMemcpyDefault, s));
     outs.push_back({p, d, sizeof(T) * n});
@@ -182,7 +214,7 @@ struct Prof {
     return e;
   }
   Prof(lc_ctx* ctx, int f, cudaStream_t st) : c(ctx), fam(f), s(st) {
-    if (!c->prof) return;
+    if (!c->prof || c->cap) return;
     a = get(c);
     if (a) cudaEventRecord(a, s);
     l0 = c->launches;
@@ -196,6 +228,28 @@ struct Prof {
   }
 };
 
+void free_graph(lc_graph* g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  for (void* p : g->dev) cudaFree(p);
+  cudaGetLastError();
+  delete g;
+}
+
+// A failed call inside a capture ends (and discards) the capture.
+void abort_capture(lc_ctx* c) {
+  if (!c->cap) return;
+  cudaGraph_t g = nullptr;
+  cudaStreamEndCapture(c->cap_stream, &g);
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();
+  cudaStreamSynchronize(c->side);
+  free_graph(c->cap);
+  c->cap = nullptr;
+  c->launches = c->cap_launch0;
+}
+
 template <typename F>
 lc_status guarded(lc_ctx* c, F&& f) {
   if (!c) return LC_EINVAL;
@@ -207,11 +261,39 @@ lc_status guarded(lc_ctx* c, F&& f) {
     f();
     return LC_OK;
   } catch (const Fail& e) {
+    if (c->cap) {
+      const std::string m = c->err;
+      abort_capture(c);
+      c->err = m + " (capture aborted)";
+    }
     return e.st;
   } catch (const std::bad_alloc&) {
+    abort_capture(c);
     set_err(c, "host allocation failed");
     return LC_ENOMEM;
   }
+}
+
+// Calls that may be recorded into a graph must use the capturing stream; the others
+// are refused while a capture is open.
+void capture_gate(lc_ctx* c, void* stream, bool allowed) {
+  if (!c->cap) return;
+  REQUIRE(allowed, LC_ESTATE, "call not allowed while a graph capture is open");
+  REQUIRE((cudaStream_t)stream == c->cap_stream, LC_ESTATE,
+          "while capturing, calls must use the capturing stream");
+}
+
+// Fuse epochs: the device counter restarts (and the stamps are cleared) long before
+// it could wrap; n = epochs about to be consumed (1 per fuse call, n_fuse per replay).
+void epoch_reserve(lc_ctx* c, int64_t n, cudaStream_t s) {
+  Store& st = c->st;
+  if (c->ep_used + (uint64_t)n >= 0xFFFFFF00ull) {
+    CK(cudaMemsetAsync(st.mp_loop_ep, 0, sizeof(uint32_t) * std::max(st.n_mp, 1), s));
+    CK(cudaMemsetAsync(st.kf_win_ep, 0, sizeof(uint32_t) * std::max(st.n_kf, 1), s));
+    CK(cudaMemsetAsync(st.ep, 0, sizeof(uint32_t) * 2, s));
+    c->ep_used = 0;
+  }
+  c->ep_used += (uint64_t)n;
 }
 
 bool params_ok(const lc_match_params& p) {
@@ -235,7 +317,7 @@ void free_store(Store& st) {
                   st.fc_desc, st.feat_mp, st.feat_angle, st.mp_rec, st.mp_flags, st.mp_ref_kf,
                   st.mp_replaced_by, st.mp_nobs, st.mp_corr_ref, st.mp_loop_ep, st.mp_owner,
                   st.kf_S_corr, st.kf_in_win, st.kf_win_ep, st.kf_win_pos, st.mp_vbits,
-                  st.kf_dirty, st.cams};
+                  st.kf_dirty, st.ep, st.cams};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   st = Store();
@@ -307,6 +389,7 @@ lc_status lc_create(lc_ctx** out, int32_t device) {
   bool ok = cudaSetDevice(device) == cudaSuccess;
   for (int r = 0; ok && r < lc_ctx::kPinRing; ++r)
     ok = cudaEventCreateWithFlags(&c->pin_ev[r], cudaEventDisableTiming) == cudaSuccess;
+  ok = ok && cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) == cudaSuccess;
   if (!ok) {
     for (int r = 0; r < lc_ctx::kPinRing; ++r)
       if (c->pin_ev[r]) cudaEventDestroy(c->pin_ev[r]);
@@ -322,6 +405,7 @@ lc_status lc_create(lc_ctx** out, int32_t device) {
 lc_status lc_destroy(lc_ctx* c) {
   if (!c) return LC_EINVAL;
   cudaSetDevice(c->device);
+  abort_capture(c);
   cudaDeviceSynchronize();
   free_store(c->st);
   for (void* p : c->scr_ptr)
@@ -331,6 +415,7 @@ lc_status lc_destroy(lc_ctx* c) {
     if (c->pin_ev[r]) cudaEventDestroy(c->pin_ev[r]);
   }
   if (c->sv) cudaFree(c->sv);
+  if (c->side) cudaStreamDestroy(c->side);
   for (auto& r : c->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   cudaGetLastError();
@@ -342,8 +427,71 @@ const char* lc_last_error(const lc_ctx* c) { return c ? c->err.c_str() : g_creat
 
 int64_t lc_kernel_launches(const lc_ctx* c) { return c ? c->launches : 0; }
 
+// ----------------------------------------------------------------------------
+// CUDA-graph capture of a sequence of calls
+lc_status lc_graph_begin(lc_ctx* c, void* stream) {
+  return guarded(c, [&] {
+    REQUIRE(!c->cap, LC_ESTATE, "a graph capture is already open");
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    REQUIRE(stream != nullptr, LC_EINVAL, "capture needs a non-default stream");
+    lc_graph* g = new lc_graph();
+    g->ctx = c;
+    cudaError_t e = cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      delete g;
+      set_err(c, std::string("cudaStreamBeginCapture failed: ") + cudaGetErrorString(e));
+      throw Fail{LC_ECUDA};
+    }
+    c->cap = g;
+    c->cap_stream = (cudaStream_t)stream;
+    c->cap_launch0 = c->launches;
+  });
+}
+
+lc_status lc_graph_end(lc_ctx* c, void* stream, lc_graph** out) {
+  return guarded(c, [&] {
+    REQUIRE(out, LC_EINVAL, "null out");
+    *out = nullptr;
+    REQUIRE(c->cap, LC_ESTATE, "no graph capture open");
+    REQUIRE((cudaStream_t)stream == c->cap_stream, LC_ESTATE, "end on a different stream");
+    lc_graph* g = c->cap;
+    c->cap = nullptr;
+    g->launches = c->launches - c->cap_launch0;
+    c->launches = c->cap_launch0;   // recorded, not executed
+    cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g->graph);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      free_graph(g);
+      set_err(c, std::string("graph capture failed: ") + cudaGetErrorString(e));
+      throw Fail{LC_ECUDA};
+    }
+    *out = g;
+  });
+}
+
+lc_status lc_graph_launch(lc_ctx* c, lc_graph* g, void* stream) {
+  return guarded(c, [&] {
+    REQUIRE(g && g->ctx == c, LC_EINVAL, "graph does not belong to this context");
+    capture_gate(c, stream, false);
+    if (g->n_fuse) epoch_reserve(c, g->n_fuse, (cudaStream_t)stream);
+    CK(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+    c->launches += g->launches;
+  });
+}
+
+lc_status lc_graph_destroy(lc_ctx* c, lc_graph* g) {
+  if (!c || !g || g->ctx != c) return LC_EINVAL;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  free_graph(g);
+  return LC_OK;
+}
+
 lc_status lc_profile_enable(lc_ctx* c, int32_t on) {
   return guarded(c, [&] {
+    capture_gate(c, nullptr, false);
     for (auto& r : c->prof_pending) { c->ev_pool.push_back(r.a); c->ev_pool.push_back(r.b); }
     c->prof_pending.clear();
     if (on) {
@@ -355,6 +503,7 @@ lc_status lc_profile_enable(lc_ctx* c, int32_t on) {
 
 lc_status lc_profile_read(lc_ctx* c, double* ms, int64_t* launches) {
   return guarded(c, [&] {
+    capture_gate(c, nullptr, false);
     for (auto& r : c->prof_pending) {
       CK(cudaEventSynchronize(r.b));
       float t = 0.f;
@@ -376,6 +525,7 @@ lc_status lc_profile_read(lc_ctx* c, double* ms, int64_t* launches) {
 lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, int32_t n_cams,
                         const lc_map_params* prm, void* stream) {
   return guarded(c, [&] {
+    capture_gate(c, stream, false);
     REQUIRE(m && cams && prm && n_cams >= 1, LC_EINVAL, "null map/camera/params");
     REQUIRE(m->n_kf >= 0 && m->n_feat >= 0 && m->n_mp >= 0, LC_EINVAL, "negative sizes");
     REQUIRE(prm->n_levels >= 1 && prm->n_levels <= LC_MAX_LEVELS, LC_EINVAL, "n_levels out of range");
@@ -459,6 +609,7 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
     dev_alloc(c, &st.kf_S_corr, 13 * NK);
     dev_alloc(c, &st.kf_in_win, NK);
     dev_alloc(c, &st.kf_win_ep, NK);
+    dev_alloc(c, &st.ep, 2);
     dev_alloc(c, &st.kf_win_pos, NK);
     dev_alloc(c, &st.mp_vbits, (NM + 31) / 32 + 1);
     dev_alloc(c, &st.kf_dirty, NK + 1);
@@ -489,7 +640,8 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
     CK(cudaMemsetAsync(st.kf_S_corr, 0, sizeof(double) * 13 * NK, s));
     CK(cudaMemsetAsync(st.kf_in_win, 0, sizeof(int32_t) * NK, s));
     CK(cudaMemsetAsync(st.kf_win_ep, 0, sizeof(uint32_t) * NK, s));
-    c->epoch = 0;
+    CK(cudaMemsetAsync(st.ep, 0, sizeof(uint32_t) * 2, s));
+    c->ep_used = 0;
     // raw SoA inputs the packing kernels read (device pointers used in place)
     const float* pos = call.in(m->mp_pos, 3 * NM);
     const float* nrm = call.in(m->mp_normal, 3 * NM);
@@ -518,6 +670,7 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
 
 lc_status lc_download_map(lc_ctx* c, const lc_map_state* o, void* stream) {
   return guarded(c, [&] {
+    capture_gate(c, stream, false);
     REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
     REQUIRE(o, LC_EINVAL, "null output struct");
     Call call(c, stream);
@@ -540,6 +693,7 @@ lc_status lc_download_map(lc_ctx* c, const lc_map_state* o, void* stream) {
 
 lc_status lc_state_save(lc_ctx* c, void* stream) {
   return guarded(c, [&] {
+    capture_gate(c, stream, false);
     REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
     Prof pr(c, LC_PROF_STATE, (cudaStream_t)stream);
     CK(launch_state_copy(c, true, (cudaStream_t)stream));
@@ -550,6 +704,7 @@ lc_status lc_state_save(lc_ctx* c, void* stream) {
 
 lc_status lc_state_restore(lc_ctx* c, void* stream) {
   return guarded(c, [&] {
+    capture_gate(c, stream, false);
     REQUIRE(c->has_map && c->has_saved, LC_ESTATE, "no saved state");
     Prof pr(c, LC_PROF_STATE, (cudaStream_t)stream);
     CK(launch_state_copy(c, false, (cudaStream_t)stream));
@@ -562,6 +717,7 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
                           int32_t n_window, const int32_t* window_kf, const lc_sim3* S_opt,
                           lc_sim3* out_S_corr, int64_t* out_counts, void* stream) {
   return guarded(c, [&] {
+    capture_gate(c, stream, true);
     REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
     REQUIRE(mode == LC_CORRECT_WINDOW || mode == LC_CORRECT_ALL, LC_EINVAL, "bad mode");
     Store& st = c->st;
@@ -620,6 +776,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
                   int64_t* io_winner, int64_t* io_victim, int8_t* out_action,
                   const lc_query_debug* dbg, int64_t* out_counts, void* stream) {
   return guarded(c, [&] {
+    capture_gate(c, stream, true);
     REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
     REQUIRE(phase == LC_FUSE_PLAN || phase == LC_FUSE_APPLY || phase == LC_FUSE_ALL, LC_EINVAL, "bad phase");
     REQUIRE(params && params_ok(*params), LC_EINVAL, "bad match params");
@@ -724,11 +881,8 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       dbg_nc = call.out(dbg->ncand, (size_t)n_q_all, true);
     }
     // ---- epoch (LoopSet stamp / window membership) ----
-    if (++c->epoch == 0) {
-      CK(cudaMemsetAsync(st.mp_loop_ep, 0, sizeof(uint32_t) * st.n_mp, call.s));
-      CK(cudaMemsetAsync(st.kf_win_ep, 0, sizeof(uint32_t) * st.n_kf, call.s));
-      c->epoch = 1;
-    }
+    if (c->cap) c->cap->n_fuse++;
+    else epoch_reserve(c, 1, call.s);
     {
       Prof pr(c, LC_PROF_FUSE_PREP, call.s);
       CK(launch_fuse_prep(c, phase, sole ? 0 : 1, n_window, d_win, n_wfeat, d_list, n_list, win, vic,
@@ -757,7 +911,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       a.dbg_ncand = dbg_nc;
       a.feat_angle = st.feat_angle;
       a.loop_ep = st.mp_loop_ep;
-      a.epoch = c->epoch;
+      a.epoch = st.ep;
       a.victim = vic;
       a.action = act;
       a.sole = sole ? 1 : 0;
@@ -766,8 +920,12 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       a.surv_off = d_boff;
       a.surv_cnt = d_scnt;
       {
+        Prof pr(c, LC_PROF_PROJECT, call.s);
+        CK(launch_match(c, 0, a, (int)bunit.size(), F_max, 0, call.s));
+      }
+      {
         Prof pr(c, LC_PROF_MATCH, call.s);
-        CK(launch_match(c, 0, a, (int)bunit.size(), F_max, call.s));
+        CK(launch_match(c, 0, a, (int)bunit.size(), F_max, 1, call.s));
       }
       if (!sole) {
         Prof pr(c, LC_PROF_RESOLVE, call.s);
@@ -795,6 +953,7 @@ lc_status lc_search_by_projection(lc_ctx* c, int32_t n_pairs, const int32_t* pai
                                   int32_t* out_feat_dist, const lc_query_debug* dbg,
                                   int64_t* out_counts, void* stream) {
   return guarded(c, [&] {
+    capture_gate(c, stream, true);
     REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
     REQUIRE(n_pairs >= 0, LC_EINVAL, "n_pairs < 0");
     if (n_pairs == 0) return;
@@ -894,7 +1053,8 @@ lc_status lc_search_by_projection(lc_ctx* c, int32_t n_pairs, const int32_t* pai
     }
     {
       Prof pr(c, LC_PROF_SBP_MATCH, call.s);
-      CK(launch_match(c, 1, a, (int)bunit.size(), F_max, call.s));
+      CK(launch_match(c, 1, a, (int)bunit.size(), F_max, 0, call.s));
+      CK(launch_match(c, 1, a, (int)bunit.size(), F_max, 1, call.s));
     }
     Prof pr(c, LC_PROF_SBP_RESOLVE, call.s);
     CK(launch_resolve(c, 1, a, n_pairs, call.s));

@@ -74,6 +74,7 @@ struct Store {
   double* kf_S_corr = nullptr;
   int32_t* kf_in_win = nullptr;
   uint32_t* kf_win_ep = nullptr;
+  uint32_t* ep = nullptr;        // [2]: current fuse epoch, k_fuse_prep block-done counter
   int32_t* kf_win_pos = nullptr;
   uint32_t* mp_vbits = nullptr;  // [(n_mp+31)/32] victim bitmap of the current fuse call
   int32_t* kf_dirty = nullptr;   // [1 + n_kf] count + keyframes changed by the apply
@@ -135,7 +136,7 @@ struct MatchArgs {
   // resolve (orientation + actions / SBP output tables)
   const float* feat_angle;
   const uint32_t* loop_ep;
-  uint32_t epoch;
+  const uint32_t* epoch;  // device word: the current fuse call's epoch (set by k_fuse_prep)
   unsigned long long* victim;
   int8_t* action;
   int32_t* out_mp;
@@ -147,6 +148,15 @@ struct MatchArgs {
   int32_t unit_base;   // k_resolve: unit = unit_base + blockIdx.x
 };
 
+struct lc_graph {
+  lc_ctx* ctx = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<void*> dev;     // graph-owned device buffers (argument blocks, scratch)
+  int64_t launches = 0;       // library kernels per replay
+  int64_t n_fuse = 0;         // fuse calls (epochs) per replay
+};
+
 struct lc_ctx {
   int device = 0;
   bool broken = false;
@@ -154,7 +164,13 @@ struct lc_ctx {
   Store st;
   bool has_map = false;
   bool has_saved = false;
-  uint32_t epoch = 0;
+  uint64_t ep_used = 0;   // fuse epochs consumed since the stamps were last cleared
+  // CUDA-graph capture (lc_graph_begin/end): calls on cap_stream are recorded; their
+  // argument blocks and scratch live in the graph's own arena
+  lc_graph* cap = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  int64_t cap_launch0 = 0;
+  cudaStream_t side = nullptr;   // private stream for capture-time uploads
   int64_t launches = 0;
   // scratch arena: named growable device buffers
   std::vector<void*> scr_ptr;
@@ -264,8 +280,8 @@ cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, co
                                const uint8_t* desc, const float* ang, const float* fuv,
                                const uint8_t* foct, const uint8_t* fdesc, uint32_t* d_errs,
                                cudaStream_t s);
-cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max,
-                         cudaStream_t s);
+cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max, int part,
+                         cudaStream_t s);  // part 0: k_project, 1: k_match
 cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, const int32_t* d_window,
                              int64_t n_wfeat, const int32_t* mp_list, int64_t n_list_total,
                              unsigned long long* winner, unsigned long long* victim, cudaStream_t s);

@@ -69,6 +69,70 @@ class _Keep:
         return a.ctypes.data
 
 
+class Graph:
+    """A captured sequence of liblc calls (lc_graph_*): launch() replays it on the
+    current stream. Holds every buffer the recorded calls reference."""
+
+    def __init__(self, ctx, handle, refs):
+        self.ctx, self.h, self.refs = ctx, handle, refs
+
+    def launch(self):
+        c = self.ctx
+        c._check("lc_graph_launch", c.lib.lc_graph_launch(c.h, self.h, c._stream()))
+
+    def close(self):
+        if getattr(self, "h", None) and self.ctx.h:
+            self.ctx.lib.lc_graph_destroy(self.ctx.h, self.h)
+        self.h = None
+        self.refs = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _Capture:
+    """`with ctx.capture() as cap: ...` records the liblc calls made inside (on a
+    private stream; outputs must be device tensors: host=False) into cap.graph."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+        self.graph = None
+
+    def __enter__(self):
+        c = self.ctx
+        self.stream = torch.cuda.Stream(device=c.device)
+        self.stream.wait_stream(torch.cuda.current_stream(c.device))
+        self._sc = torch.cuda.stream(self.stream)
+        self._sc.__enter__()
+        c._cap_refs = []
+        st = c.lib.lc_graph_begin(c.h, c._stream())
+        if st != 0:
+            c._cap_refs = None
+            self._sc.__exit__(None, None, None)
+            c._check("lc_graph_begin", st)
+        return self
+
+    def __exit__(self, et, ev, tb):
+        c = self.ctx
+        h = C.c_void_p()
+        st = c.lib.lc_graph_end(c.h, c._stream(), C.byref(h))
+        refs, c._cap_refs = c._cap_refs, None
+        self._sc.__exit__(et, ev, tb)
+        torch.cuda.current_stream(c.device).wait_stream(self.stream)
+        if et is None:
+            c._check("lc_graph_end", st)
+            self.graph = Graph(c, h, refs)
+        elif st == 0 and h.value:
+            c.lib.lc_graph_destroy(c.h, h)
+        return False
+
+    def launch(self):
+        self.graph.launch()
+
+
 class Context:
     """One liblc context on one CUDA device (lc_create / lc_destroy)."""
 
@@ -82,6 +146,7 @@ class Context:
         self.h = h
         self.n_kf = self.n_feat = self.n_mp = 0
         self.kf_feat_begin = None
+        self._cap_refs = None   # buffers referenced by an open capture
 
     def close(self):
         if getattr(self, "h", None):
@@ -103,7 +168,24 @@ class Context:
             raise LcError(fn, st, self.lib.lc_last_error(self.h).decode())
 
     def _dev(self, n, dtype):
-        return torch.empty(int(n), dtype=dtype, device=f"cuda:{self.device}")
+        t = torch.empty(int(n), dtype=dtype, device=f"cuda:{self.device}")
+        if self._cap_refs is not None:
+            self._cap_refs.append(t)
+        return t
+
+    def _keep(self, host):
+        """Per-call holder of converted arrays; while capturing, also kept by the graph."""
+        if self._cap_refs is not None and host:
+            raise LcError("capture", -1, "calls recorded into a graph need host=False")
+        k = _Keep()
+        if self._cap_refs is not None:
+            self._cap_refs.append(k)
+        return k
+
+    def capture(self):
+        """CUDA-graph capture (lc_graph_begin/end): `with ctx.capture() as cap: ...`,
+        then cap.graph.launch() replays the recorded calls."""
+        return _Capture(self)
 
     def kernel_launches(self) -> int:
         return int(self.lib.lc_kernel_launches(self.h))
@@ -176,7 +258,7 @@ class Context:
 
     # -- lc_correct_sim3 ----------------------------------------------------------
     def correct_window(self, cur_kf, S_cw_corr, window, host=True):
-        k = _Keep()
+        k = self._keep(host)
         window = np.ascontiguousarray(window, np.int32)
         S = np.ascontiguousarray(S_cw_corr, np.float64)
         if host:
@@ -194,7 +276,7 @@ class Context:
         return outS.view(-1, 13), cnt
 
     def correct_all(self, S_opt, host=True):
-        k = _Keep()
+        k = self._keep(host)
         cnt = np.zeros(LC_NCOUNT, np.int64) if host else self._dev(LC_NCOUNT, torch.int64)
         st = self.lib.lc_correct_sim3(self.h, LC_CORRECT_ALL, 0, None, 0, None,
                                       k.ptr(S_opt, np.float64), None, k.ptr(cnt), self._stream())
@@ -210,7 +292,7 @@ class Context:
              debug=False, host=True):
         """Returns dict(winner, victim, action, counts[, best, uv, ncand]).
         winner / victim: pass tensors to use them in place (PLAN -> NCCL -> APPLY)."""
-        k = _Keep()
+        k = self._keep(host)
         window = np.ascontiguousarray(window, np.int32)
         n_w = len(window)
         w_hi = n_w if w_hi is None else int(w_hi)
@@ -249,7 +331,7 @@ class Context:
     # -- lc_search_by_projection ----------------------------------------------------
     def search_by_projection(self, pair_kf, pair_S, pair_param, params, pair_list_begin, mp_list,
                              pair_taken=None, debug=False, host=True):
-        k = _Keep()
+        k = self._keep(host)
         pair_kf = np.ascontiguousarray(pair_kf, np.int32)
         n_pairs = len(pair_kf)
         plb = np.ascontiguousarray(pair_list_begin, np.int32)

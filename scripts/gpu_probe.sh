@@ -1,0 +1,2 @@
+set -x
+python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline  2>&1 | tail -3

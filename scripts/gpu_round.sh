@@ -1,6 +1,7 @@
 set -x
 TAG=${TAG:-r01}
 python -m pytest tests -m gpu -q -x 2>&1 | tail -30
-python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -3 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json
+python bench.py --steps 10 --warmup 3 --cpu-seconds 15 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; tail -3 gpurun_out/bench_$TAG.err; cat gpurun_out/bench_$TAG.json
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --profile-only --steps 2 --warmup 3 > /dev/null 2>&1; echo ncu1 $?
-ncu --set full --clock-control none --import-source on -k regex:k_project_match -s 3 -c 1 -o gpurun_out/match_$TAG python bench.py --profile-only --steps 1 --warmup 3 > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncu2 $?; tail -3 gpurun_out/ncu_full_$TAG.log
+ncu --set full --clock-control none --import-source on -k regex:'k_project|k_match' -s 6 -c 2 -o gpurun_out/match_$TAG python bench.py --profile-only --steps 1 --warmup 3 > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncu2 $?; tail -3 gpurun_out/ncu_full_$TAG.log
+python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2>&1; tail -1 gpurun_out/bench_ref_$TAG.json

@@ -102,7 +102,10 @@ def main():
         if args.update_traffic and summary["full"]:
             tpath = os.path.join(ROOT, "profiles", "traffic.json")
             t = json.load(open(tpath)) if os.path.exists(tpath) else {}
-            t.setdefault("k_project_match_fuse", {})[args.config] = summary["full"][0]["dram_bytes"]
+            # the capture holds one launch of each match-stage kernel (k_project, k_match)
+            t.setdefault("match_stage", {})[args.config] = sum(e["dram_bytes"] for e in summary["full"])
+            t.setdefault("per_kernel", {})[args.config] = {e["kernel"].split("(")[0]: e["dram_bytes"]
+                                                           for e in summary["full"]}
             t["source"] = f"ncu --set full capture {args.tag}"
             json.dump(t, open(tpath, "w"), indent=1)
     if args.launches:
