@@ -245,10 +245,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
           status = LC_Q_FOUND; cA += 1u << 10; break;
         }
         const double p0 = __uint_as_float(r0.x), p1 = __uint_as_float(r0.y), p2 = __uint_as_float(r0.z);
-        const double z = (s_T[6] * p0 + s_T[7] * p1) + s_T[8] * p2 + s_T[11];
+        double x, y, z;
+        lc_se3_xyz(s_T, p0, p1, p2, x, y, z);
         if (z <= 0.0) { status = LC_Q_DEPTH; cA += 1u << 20; break; }
-        const double x = (s_T[0] * p0 + s_T[1] * p1) + s_T[2] * p2 + s_T[9];
-        const double y = (s_T[3] * p0 + s_T[4] * p1) + s_T[5] * p2 + s_T[10];
         if (pinhole && !a.dbg_uv) {
           // conservative pre-test: |ua - u| <= 1e-6 |u| + tiny, margin 1e-2 px
           const double rz = (double)__frcp_rn((float)z);
@@ -292,7 +291,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
     wbase = __shfl_sync(0xffffffffu, wbase, 0);
     if (surv) {
       Surv e;
-      e.q = q; e.jl = (uint32_t)(j - q0) | ((uint32_t)lvl << 27); e.u = u; e.v = v;
+      e.q = q; e.jl = (uint32_t)(j - q0) | ((uint32_t)lvl << 27); e.fu = (float)u; e.fv = (float)v;
       out[wbase + __popc(m & ltmask)] = e;
     } else if (valid) {
       const int64_t qi = qbase + (j - q0);
@@ -316,12 +315,33 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
 // ---- k_match ------------------------------------------------------------------
 template <int FCAP>
 struct MatchSmem {
-  static constexpr int WB = ((32 * CPL * 4 + 32 * CPL * 2) + 15) & ~15;
+  // per warp: candidate keys [32][CPL] u32, candidate positions [32][CPL] u16,
+  // query descriptors [32][8] u32 (cp.async destination)
+  static constexpr int WKEY = 0;
+  static constexpr int WCAND = WKEY + 32 * CPL * 4;
+  static constexpr int WQD = (WCAND + 32 * CPL * 2 + 15) & ~15;
+  static constexpr int WB = WQD + 32 * 32;
   static constexpr int UV = 0;
   static constexpr int META = UV + ((FCAP * 8 + 15) & ~15);
   static constexpr int QUEUE = META + ((FCAP * 4 + 15) & ~15);
   static constexpr int CELL = QUEUE + NWARP * WB;   // runtime-size cell table last
 };
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
+}
+
+// exact fp64 (u, v) of a survivor: the same expressions as k_project (same bits)
+__device__ __noinline__ void exact_uv(const MatchArgs& a, const double* T, const DevCam& cam,
+                                         int q, double& u, double& v) {
+  const MpRec* r = a.mp_rec + q;
+  double x, y, z;
+  lc_se3_xyz(T, (double)__ldg(&r->pos[0]), (double)__ldg(&r->pos[1]), (double)__ldg(&r->pos[2]), x, y, z);
+  lc_project(cam, x, y, z, u, v);
+}
 
 template <int MODE, int FCAP>
 __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchArgs a) {
@@ -329,7 +349,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ double s_T[12];
-  __shared__ DevCam s_cam;
+  __shared__ __align__(16) DevCam s_cam;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int unit = a.blk_unit[blockIdx.x];
@@ -341,8 +361,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   float2* s_uv = (float2*)(smem + SM::UV);
   uint32_t* s_meta = (uint32_t*)(smem + SM::META);
   unsigned char* wb = smem + SM::QUEUE + warp * SM::WB;
-  uint32_t* s_key = (uint32_t*)wb;                  // [32][CPL] candidate keys
-  uint16_t* s_cand = (uint16_t*)(s_key + 32 * CPL); // [32][CPL] candidate positions
+  uint32_t* s_key = (uint32_t*)(wb + SM::WKEY);     // [32][CPL] candidate keys
+  uint16_t* s_cand = (uint16_t*)(wb + SM::WCAND);   // [32][CPL] candidate positions
+  uint32_t* s_qd = (uint32_t*)(wb + SM::WQD);       // [32][8] query descriptors
   const int64_t toff = (MODE == 1 && a.taken) ? a.unit_toff[unit] : 0;
   if (tid == 0) {
     mbar_init(&s_bar, 1);
@@ -355,12 +376,16 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
       tma_load_1d(s_uv, a.fc_uv + fp, b_uv, &s_bar);
       tma_load_1d(s_meta, a.fc_meta + fp, b_meta, &s_bar);
     }
-    double S[13], T[13];
+  }
+  if (tid >= 32 && tid < 44) {   // SE3 part (R, t/s) of the unit's Sim3 (reading A2)
     const double* src = a.unit_S ? a.unit_S + 13 * (size_t)unit : a.kf_S_corr + 13 * (size_t)k;
-    for (int i = 0; i < 13; ++i) S[i] = src[i];
-    lc_sim3_se3(S, T);
-    for (int i = 0; i < 12; ++i) s_T[i] = T[i];
-    s_cam = a.cams[a.kf_cam[k]];
+    const int i = tid - 32;
+    s_T[i] = i < 9 ? src[i] : src[i] / src[12];
+  }
+  if (tid >= 64 && tid < 64 + (int)(sizeof(DevCam) / 16)) {
+    static_assert(sizeof(DevCam) % 16 == 0, "DevCam copy granularity");
+    reinterpret_cast<uint4*>(&s_cam)[tid - 64] =
+        reinterpret_cast<const uint4*>(a.cams + a.kf_cam[k])[tid - 64];
   }
   if (a.sole) {  // this CTA owns the unit's winner words: initialise them here
     unsigned long long* w0 = a.winner + a.unit_woff[unit];
@@ -387,31 +412,42 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   const int ns_tot = a.surv_cnt[blockIdx.x];
   uint32_t cC = 0, cP = 0, cE = 0;   // NOCAND | OVERTH << 10 | RATIO << 20; PROP; CAND
 
+  // strict square window |fuv - uv| < r (reading A8). fp32 filter: |(float)a - fu| is
+  // within 2.5e-4 px of the exact |a - u| for |u| < 4096 px, so a decision farther
+  // than 1e-3 px from the edge is exact; -1 = ambiguous (decide in fp64)
+  auto win_f32 = [&](const float2 fuv, float fu, float fv, float fr) -> int {
+    if (!f32ok) return -1;
+    const float du = fabsf(fuv.x - fu), dv = fabsf(fuv.y - fv);
+    if (du > fr + 1e-3f || dv > fr + 1e-3f) return 0;
+    if (du < fr - 1e-3f && dv < fr - 1e-3f) return 1;
+    return -1;
+  };
+
   // the next step's survivor entries are in flight while the current step runs
   Surv e_nx;
-  e_nx.q = 0; e_nx.jl = 0u; e_nx.u = 0.0; e_nx.v = 0.0;
+  e_nx.q = 0; e_nx.jl = 0u; e_nx.fu = 0.f; e_nx.fv = 0.f;
   if (warp * 32 + lane < ns_tot) e_nx = sv[warp * 32 + lane];
   for (int i0 = warp * 32; i0 < ns_tot; i0 += NWARP * 32) {
     const bool act = i0 + lane < ns_tot;
     const Surv e = e_nx;
     if (i0 + NWARP * 32 + lane < ns_tot) e_nx = sv[i0 + NWARP * 32 + lane];
     const int lvl = (int)(e.jl >> 27);
-    const double r = (double)prm.th * a.scale[lvl];
-    uint4 d0 = make_uint4(0, 0, 0, 0), d1 = d0;
     int cx0 = 0, cx1 = -1, cy0 = 0, cy1 = -1, nc = 0;
+    const float fr = (float)((double)prm.th * a.scale[lvl]);
     if (act) {
+      // query descriptor -> shared memory, asynchronously, during the scan
       const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + e.q);
-      d0 = __ldg(rp + 2); d1 = __ldg(rp + 3);
-      const float fu = (float)e.u, fv = (float)e.v, fr = (float)r;
+      cp_async16(s_qd + lane * 8, rp + 2);
+      cp_async16(s_qd + lane * 8 + 4, rp + 3);
       // conservative (0.01 px) cell-range superset of the exact square window
-      cx0 = max(0, (int)floorf((fu - fr - 0.01f - fminx) * fsx));
-      cx1 = min(cols - 1, (int)floorf((fu + fr + 0.01f - fminx) * fsx));
-      cy0 = max(0, (int)floorf((fv - fr - 0.01f - fminy) * fsy));
-      cy1 = min(rows - 1, (int)floorf((fv + fr + 0.01f - fminy) * fsy));
+      cx0 = max(0, (int)floorf((e.fu - fr - 0.01f - fminx) * fsx));
+      cx1 = min(cols - 1, (int)floorf((e.fu + fr + 0.01f - fminx) * fsx));
+      cy0 = max(0, (int)floorf((e.fv - fr - 0.01f - fminy) * fsy));
+      cy1 = min(rows - 1, (int)floorf((e.fv + fr + 0.01f - fminy) * fsy));
       const int lo = lvl - 1;
-      // (1) window scan. fp32 window test first: |fuv - (float)u| is within 2.5e-4 px
-      // of the exact |fuv - u| for |u| < 4096 px, so a decision farther than 1e-3 px
-      // from the edge is exact; otherwise (or for larger images) fp64.
+      // (1) window scan over the staged cells, octave filter (A9) first; slots whose
+      // fp32 window test is ambiguous are marked and settled in fp64 after the scan
+      uint32_t amb = 0u;
       for (int cy = cy0; cy <= cy1; ++cy) {
         const int pe = s_cell[cy * cols + cx1 + 1];
         for (int p = s_cell[cy * cols + cx0]; p < pe; ++p) {
@@ -419,22 +455,32 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
           const int oct = (int)((meta >> 16) & 0xFFu);
           if (oct < lo || oct > lvl) continue;
           if (MODE == 1 && (meta & 0x80000000u)) continue;
-          const float2 fuv = s_uv[p];
-          const float du = fabsf(fuv.x - fu), dv = fabsf(fuv.y - fv);
-          if (f32ok && (du > fr + 1e-3f || dv > fr + 1e-3f)) continue;
-          if (!(f32ok && du < fr - 1e-3f && dv < fr - 1e-3f) &&
-              !(fabs((double)fuv.x - e.u) < r && fabs((double)fuv.y - e.v) < r))
-            continue;
+          const int w = win_f32(s_uv[p], e.fu, e.fv, fr);
+          if (w == 0) continue;
           if (nc < CPL) {
             s_cand[lane * CPL + nc] = (uint16_t)p;
-#if LC_KM_PF
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(a.fc_desc + 2 * (size_t)(fp + p)));
-#endif
+            if (w < 0) amb |= 1u << nc;
           }
           ++nc;
         }
       }
+      if (amb && nc <= CPL) {   // rare: one exact projection, drop slots outside the window
+        double u, v;
+        exact_uv(a, s_T, s_cam, e.q, u, v);
+        const double r = (double)prm.th * a.scale[lvl];
+        int m = 0;
+        for (int i = 0; i < nc; ++i) {
+          const int p = s_cand[lane * CPL + i];
+          const float2 fuv = s_uv[p];
+          if ((amb >> i) & 1u) {
+            if (!(fabs((double)fuv.x - u) < r && fabs((double)fuv.y - v) < r)) continue;
+          }
+          s_cand[lane * CPL + m++] = (uint16_t)p;
+        }
+        nc = m;
+      }
     }
+    cp_async_wait_all();
     __syncwarp();
     // (2) Hamming of all slotted candidates, warp-wide
     const bool over = act && nc > CPL;
@@ -455,19 +501,14 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         const int ex = __shfl_sync(0xffffffffu, ex2, own + step);
         if (c < tot2 && ex <= c) own += step;
       }
-      const uint32_t w0 = __shfl_sync(0xffffffffu, d0.x, own), w1 = __shfl_sync(0xffffffffu, d0.y, own);
-      const uint32_t w2 = __shfl_sync(0xffffffffu, d0.z, own), w3 = __shfl_sync(0xffffffffu, d0.w, own);
-      const uint32_t w4 = __shfl_sync(0xffffffffu, d1.x, own), w5 = __shfl_sync(0xffffffffu, d1.y, own);
-      const uint32_t w6 = __shfl_sync(0xffffffffu, d1.z, own), w7 = __shfl_sync(0xffffffffu, d1.w, own);
       const int oex = __shfl_sync(0xffffffffu, ex2, own);
       if (c < tot2) {
         const int slot = own * CPL + (c - oex);
         const int p = s_cand[slot];
         const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
         const uint4 b0 = __ldg(dp), b1 = __ldg(dp + 1);
-        const int h = __popc(w0 ^ b0.x) + __popc(w1 ^ b0.y) + __popc(w2 ^ b0.z) + __popc(w3 ^ b0.w) +
-                      __popc(w4 ^ b1.x) + __popc(w5 ^ b1.y) + __popc(w6 ^ b1.z) + __popc(w7 ^ b1.w);
-        s_key[slot] = ((uint32_t)h << 16) | (s_meta[p] & 0xFFFFu);
+        const uint4* qd = reinterpret_cast<const uint4*>(s_qd + own * 8);
+        s_key[slot] = ((uint32_t)popc_desc(qd[0], qd[1], b0, b1) << 16) | (s_meta[p] & 0xFFFFu);
       }
     }
     __syncwarp();
@@ -483,7 +524,13 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
           second = min(second, (int)(key >> 16));
         }
       };
-      if (over) {
+      if (over) {   // > CPL fp32 candidates: serial rescan with the exact window test
+        const uint4* qd = reinterpret_cast<const uint4*>(s_qd + lane * 8);
+        const uint4 d0 = qd[0], d1 = qd[1];
+        double u, v;
+        exact_uv(a, s_T, s_cam, e.q, u, v);
+        const double r = (double)prm.th * a.scale[lvl];
+        nc = 0;
         for (int cy = cy0; cy <= cy1; ++cy) {
           const int pe = s_cell[cy * cols + cx1 + 1];
           for (int p = s_cell[cy * cols + cx0]; p < pe; ++p) {
@@ -492,9 +539,10 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
             if (oct < lvl - 1 || oct > lvl) continue;
             if (MODE == 1 && (meta & 0x80000000u)) continue;
             const float2 fuv = s_uv[p];
-            if (!(fabs((double)fuv.x - e.u) < r && fabs((double)fuv.y - e.v) < r)) continue;
+            if (!(fabs((double)fuv.x - u) < r && fabs((double)fuv.y - v) < r)) continue;
             const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
             take(((uint32_t)popc_desc(d0, d1, __ldg(dp), __ldg(dp + 1)) << 16) | (meta & 0xFFFFu));
+            ++nc;
           }
         }
       } else {
@@ -518,7 +566,11 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         else val = ((long long)(best >> 16) << 48) | ((long long)second << 32) | (long long)(best & 0xFFFFu);
         a.dbg_best[qi] = val;
       }
-      if (a.dbg_uv) { a.dbg_uv[2 * qi] = e.u; a.dbg_uv[2 * qi + 1] = e.v; }
+      if (a.dbg_uv) {
+        double u, v;
+        exact_uv(a, s_T, s_cam, e.q, u, v);
+        a.dbg_uv[2 * qi] = u; a.dbg_uv[2 * qi + 1] = v;
+      }
       if (a.dbg_ncand) a.dbg_ncand[qi] = nc;
     }
     __syncwarp();
@@ -591,7 +643,7 @@ __device__ void resolve_unit(const MatchArgs& a, int unit) {
   }
   // RB features per thread per pass with every load of a phase issued together:
   // (winner, association) -> orientation -> (flags, LoopSet stamp) of held slots
-  constexpr int RB = 8;
+  constexpr int RB = 4;
   const int nt = blockDim.x;
   for (int f0 = threadIdx.x; f0 < F; f0 += RB * nt) {
     unsigned long long w[RB];

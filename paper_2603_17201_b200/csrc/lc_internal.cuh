@@ -85,12 +85,14 @@ struct Store {
 };
 
 // Parameters of one matching launch, passed by value.
-// compacted survivor of the geometric culls (k_project -> k_match): 24 bytes, exact
-// fp64 projection (u, v).
-struct __align__(8) Surv {
+// compacted survivor of the geometric culls (k_project -> k_match): 16 bytes, the
+// projection rounded to fp32 (the exact fp64 (u, v) is recomputed with lc_se3_xyz +
+// lc_project -- the same expressions, hence the same bits -- where a window decision
+// needs it).
+struct __align__(16) Surv {
   int32_t q;
   uint32_t jl;   // (position in the block's query range) | (level << 27)
-  double u, v;
+  float fu, fv;  // (float)u, (float)v
 };
 
 struct MatchArgs {
@@ -252,6 +254,15 @@ __host__ __device__ __forceinline__ void lc_sim3_se3(const double* S, double* o)
 }
 
 // Projection (reading A29). Returns u, v in fp64.
+// camera coordinates of a map point under the SE3 part T = (R row-major, t) of a
+// unit's Sim3 (reading A2), in the order of DESIGN.md "Sim3 arithmetic"
+__device__ __forceinline__ void lc_se3_xyz(const double* T, double p0, double p1, double p2,
+                                           double& x, double& y, double& z) {
+  z = (T[6] * p0 + T[7] * p1) + T[8] * p2 + T[11];
+  x = (T[0] * p0 + T[1] * p1) + T[2] * p2 + T[9];
+  y = (T[3] * p0 + T[4] * p1) + T[5] * p2 + T[10];
+}
+
 __device__ __forceinline__ void lc_project(const DevCam& c, double x, double y, double z,
                                            double& u, double& v) {
   if (c.model == 0) {
