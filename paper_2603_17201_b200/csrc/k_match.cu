@@ -850,16 +850,34 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
   const uint32_t HS = (uint32_t)hash_size;
   int32_t* s_key = (int32_t*)smem;
   uint32_t* s_val = (uint32_t*)(s_key + hash_size);
-  int32_t* s_new = (int32_t*)(s_val + hash_size);
+  uint32_t* s_filt = s_val + hash_size;                          // 2^15-bit pre-filter
+  int32_t* s_new = (int32_t*)(s_filt + (1 << (FILT_LOG2 - 5)));   // [F] new association per slot
+  auto probe = [&](int32_t key) -> int {   // slot of key in the hash, -1 if absent
+    uint32_t h = hslot(key, HS);
+    while (true) {
+      const int32_t v = s_key[h];
+      if (v == key) return (int)h;
+      if (v == -1) return -1;
+      h = (h + 1 == HS) ? 0 : h + 1;
+    }
+  };
+  auto filt_has = [&](int32_t key) -> bool {
+    const uint32_t b = fslot(key);
+    return (s_filt[b >> 5] >> (b & 31)) & 1u;
+  };
   for (int di = blockIdx.x; di < nd; di += gridDim.x) {
     const int k = dirty_list[1 + di];
     const int fb = kf_fbeg[k], F = kf_fbeg[k + 1] - fb;
     const int wpos = (kf_win_ep[k] == epoch) ? kf_win_pos[k] : -1;
     const int64_t woff = wpos >= 0 ? woff_of_pos[wpos] : 0;
-    uint8_t* s_pr = (uint8_t*)(s_new + F);
+    int32_t* s_old = s_new + F;                // [F] association before the apply
+    uint8_t* s_pr = (uint8_t*)(s_old + F);     // [F] priority: 0 unchanged, 1 ADD, 2 rewired
     for (int i = threadIdx.x; i < (int)HS; i += blockDim.x) { s_key[i] = -1; s_val[i] = 0xFFFFFFFFu; }
+    for (int i = threadIdx.x; i < (1 << (FILT_LOG2 - 5)); i += blockDim.x) s_filt[i] = 0u;
     __syncthreads();
-    // new value per slot: 8 slots per thread with their loads in flight together
+    // (1) new value per slot (8 slots per thread, their loads in flight together); the
+    // new map point of every changed slot is hashed and competes at once with key
+    // (priority, f) (reading A22)
     for (int base = 0; base < F; base += 8 * (int)blockDim.x) {
       int32_t m[8];
       unsigned long long w[8];
@@ -887,43 +905,43 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
           if (pr == 2) cnt[A_REWIRED]++;
         }
         s_new[f] = nv;
+        s_old[f] = m[u];
         s_pr[f] = pr;
-        if (pr) {  // hash the new map point of every changed slot
+        if (pr) {
           uint32_t h = hslot(nv, HS);
           while (true) {
             const int32_t prev = atomicCAS(&s_key[h], -1, nv);
             if (prev == -1 || prev == nv) break;
             h = (h + 1 == HS) ? 0 : h + 1;
           }
+          atomicMin(&s_val[h], ((uint32_t)pr << 16) | (uint32_t)f);
+          const uint32_t b = fslot(nv);
+          atomicOr(&s_filt[b >> 5], 1u << (b & 31));
         }
       }
     }
     __syncthreads();
-    // every slot holding a hashed map point competes for it with key (priority, f)
+    // (2) unchanged slots holding a hashed map point compete too (priority 0 wins)
     for (int f = threadIdx.x; f < F; f += blockDim.x) {
       const int32_t nv = s_new[f];
-      if (nv < 0) continue;
-      uint32_t h = hslot(nv, HS);
-      while (s_key[h] != -1 && s_key[h] != nv) h = (h + 1 == HS) ? 0 : h + 1;
-      if (s_key[h] == nv) atomicMin(&s_val[h], ((uint32_t)s_pr[f] << 16) | (uint32_t)f);
+      if (nv < 0 || s_pr[f] != 0 || !filt_has(nv)) continue;
+      const int h = probe(nv);
+      if (h >= 0) atomicMin(&s_val[h], (uint32_t)f);
     }
     __syncthreads();
+    // (3) losers of a hashed map point are cleared; write changed slots, n_obs deltas
     for (int f = threadIdx.x; f < F; f += blockDim.x) {
       int32_t nv = s_new[f];
       const uint8_t pr = s_pr[f];
-      if (nv >= 0) {
-        uint32_t h = hslot(nv, HS);
-        while (s_key[h] != -1 && s_key[h] != nv) h = (h + 1 == HS) ? 0 : h + 1;
-        if (s_key[h] == nv && s_val[h] != (((uint32_t)pr << 16) | (uint32_t)f)) { nv = -1; cnt[A_DUP]++; }
-        else if (pr == 1) cnt[A_ADDED]++;
-      }
-      if (pr != 0 || nv != s_new[f]) {
-        const int32_t m = feat_mp[fb + f];
-        if (nv != m) {
-          feat_mp[fb + f] = nv;
-          if (m >= 0) atomicSub(&nobs[m], 1);
-          if (nv >= 0) atomicAdd(&nobs[nv], 1);
-        }
+      if (nv < 0 || (pr == 0 && !filt_has(nv))) continue;
+      const int h = probe(nv);
+      if (h >= 0 && s_val[h] != (((uint32_t)pr << 16) | (uint32_t)f)) { nv = -1; cnt[A_DUP]++; }
+      else if (pr == 1) cnt[A_ADDED]++;
+      const int32_t m = s_old[f];
+      if (nv != m) {
+        feat_mp[fb + f] = nv;
+        if (m >= 0) atomicSub(&nobs[m], 1);
+        if (nv >= 0) atomicAdd(&nobs[nv], 1);
       }
     }
     __syncthreads();
@@ -1021,7 +1039,7 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
         st.feat_mp, st.kf_dirty);
     const int Fm = st.max_F > 0 ? st.max_F : 1;
     const int H = ((Fm + Fm / 2 + 1) + 31) & ~31;
-    size_t smem = (size_t)H * 8 + (size_t)Fm * 5 + 16;
+    size_t smem = (size_t)H * 8 + (size_t)(1 << (FILT_LOG2 - 3)) + (size_t)Fm * 9 + 16;
     smem = (smem + 15) & ~(size_t)15;
     cudaError_t e = cudaFuncSetAttribute(k_apply_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
