@@ -260,6 +260,7 @@ def main():
     torch.cuda.synchronize()
     counts = _lib.COUNTER_NAMES
     cf = cnt_fuse.cpu().numpy() if hasattr(cnt_fuse, "cpu") else np.asarray(list(cnt_fuse.values()))
+    fuse_counts = {n: int(v) for n, v in zip(counts, cf)}
     cand_rank = int(cf[counts.index("candidates")])
     q_rank = int(cf[counts.index("queries")])
     prop_rank = int(cf[counts.index("proposals")])
@@ -399,6 +400,7 @@ def main():
                        "l2": "flushed between steps (512 MB write) after an untimed state restore"},
             "ms_per_loop": round(ms_step, 5),
             "kernel_ms_per_step": {k: round(v, 5) for k, v in fam_ms.items()},
+            "fuse_counts": fuse_counts if ws == 1 else None,
             "gpu_launches": int(launches_timed),
             "roofline": roof,
             "cpu_baseline": cpu,
