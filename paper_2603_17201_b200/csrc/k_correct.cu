@@ -48,6 +48,7 @@ __global__ void k_win_sim3(int n_w, int cur_pos, const int32_t* __restrict__ win
                            const double* __restrict__ kf_pose, const double* __restrict__ Scw,
                            double* __restrict__ scr, double* __restrict__ kf_S_corr,
                            int32_t* __restrict__ kf_in_win) {
+  pdl_trigger();   // k_win_mark reads none of this kernel's outputs
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_w) return;
   const int k = window[i];
@@ -73,12 +74,12 @@ __global__ void k_win_sim3(int n_w, int cur_pos, const int32_t* __restrict__ win
   kf_in_win[k] = 1;
 }
 
-// Warp per window position: owner(m) = min window position observing the non-bad map
-// point m (atomicMin), 16-B association loads, 4 slots per lane in flight.
+// Warp per window position: owner(m) = min window position observing map point m
+// (fire-and-forget atomicMin reductions), 16-B association loads. Bad map points get an
+// owner too; k_win_b ignores them (it reads the flags coalesced, per point).
 __global__ void __launch_bounds__(LC_NTHREADS) k_win_mark(
     int n_w, const int32_t* __restrict__ window, const int32_t* __restrict__ kf_fbeg,
-    const int32_t* __restrict__ feat_mp, const uint8_t* __restrict__ mp_flags,
-    int32_t* __restrict__ owner) {
+    const int32_t* __restrict__ feat_mp, int32_t* __restrict__ owner) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -88,59 +89,63 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_win_mark(
     const int vb = min(fe, (fb + 3) & ~3), ve = max(vb, fe & ~3);
     for (int f = fb + lane; f < vb; f += 32) {
       const int m = feat_mp[f];
-      if (m >= 0 && !(__ldg(mp_flags + m) & 1u)) atomicMin(&owner[m], i);
+      if (m >= 0) atomicMin(&owner[m], i);
     }
     for (int f = vb + 4 * lane; f < ve; f += 128) {
       const int4 m4 = __ldg(reinterpret_cast<const int4*>(feat_mp + f));
-      const uint8_t g0 = m4.x >= 0 ? __ldg(mp_flags + m4.x) : 1, g1 = m4.y >= 0 ? __ldg(mp_flags + m4.y) : 1;
-      const uint8_t g2 = m4.z >= 0 ? __ldg(mp_flags + m4.z) : 1, g3 = m4.w >= 0 ? __ldg(mp_flags + m4.w) : 1;
-      if (!(g0 & 1u)) atomicMin(&owner[m4.x], i);
-      if (!(g1 & 1u)) atomicMin(&owner[m4.y], i);
-      if (!(g2 & 1u)) atomicMin(&owner[m4.z], i);
-      if (!(g3 & 1u)) atomicMin(&owner[m4.w], i);
+      if (m4.x >= 0) atomicMin(&owner[m4.x], i);
+      if (m4.y >= 0) atomicMin(&owner[m4.y], i);
+      if (m4.z >= 0) atomicMin(&owner[m4.z], i);
+      if (m4.w >= 0) atomicMin(&owner[m4.w], i);
     }
     for (int f = ve + lane; f < fe; f += 32) {
       const int m = feat_mp[f];
-      if (m >= 0 && !(__ldg(mp_flags + m) & 1u)) atomicMin(&owner[m], i);
+      if (m >= 0) atomicMin(&owner[m], i);
     }
   }
+  pdl_wait();   // (PDL) independent of k_win_sim3; completes after it
 }
 
 // Blocks [0, nb_mp): p <- fl32( inverse(S_o^corr)( T_o,w^old(p) ) ), corr_ref <- window[o]
 // (or -1); blocks [nb_mp, ...): window pose write-back T_iw <- SE3(S_i^corr).
 __global__ void __launch_bounds__(LC_NTHREADS) k_win_b(
-    int n_mp, int nb_mp, int n_w, const int32_t* __restrict__ owner,
+    int n_mp, int nb_mp, int n_w, const int32_t* __restrict__ owner, const uint8_t* __restrict__ flags,
     const int32_t* __restrict__ window, const double* __restrict__ scr, MpRec* __restrict__ rec,
     int32_t* __restrict__ corr_ref, double* __restrict__ kf_pose,
     unsigned long long* __restrict__ counts) {
   uint32_t n = 0;
-  if ((int)blockIdx.x < nb_mp) {
-    const int stride = nb_mp * blockDim.x;
-    for (int q0 = blockIdx.x * blockDim.x; q0 < n_mp; q0 += stride) {
-      const int q = q0 + threadIdx.x;
-      if (q < n_mp) {
-        const int o = owner[q];
-        if (o == OWNER_NONE) {
-          corr_ref[q] = -1;
-        } else {
-          const double* S = scr + (size_t)WSTR * o;
-          double T[13], Si[13];
-          load13(S, T);
-          load13(S + 14, Si);
-          const float4 pf = *reinterpret_cast<const float4*>(rec + q);
-          double p[3] = {pf.x, pf.y, pf.z}, pc[3], pw[3];
-          lc_sim3_apply(T, p, pc);
-          lc_sim3_apply(Si, pc, pw);
-          rec[q].pos[0] = __double2float_rn(pw[0]);
-          rec[q].pos[1] = __double2float_rn(pw[1]);
-          rec[q].pos[2] = __double2float_rn(pw[2]);
-          corr_ref[q] = window[o];
-          ++n;
-        }
+  if ((int)blockIdx.x < nb_mp) {   // one point per thread (nb_mp * blockDim.x >= n_mp)
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    uint8_t fl = 1;
+    float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q < n_mp) {   // independent of the predecessors: before the PDL wait
+      fl = flags[q];
+      pf = *reinterpret_cast<const float4*>(rec + q);
+    }
+    pdl_wait();
+    if (q < n_mp) {
+      const int o = owner[q];
+      if (o == OWNER_NONE || (fl & 1u)) {   // unobserved by the window, or bad
+        corr_ref[q] = -1;
+      } else {
+        const double* S = scr + (size_t)WSTR * o;
+        double T[13], Si[13];
+        load13(S, T);
+        load13(S + 14, Si);
+        const int ko = window[o];
+        double p[3] = {pf.x, pf.y, pf.z}, pc[3], pw[3];
+        lc_sim3_apply(T, p, pc);
+        lc_sim3_apply(Si, pc, pw);
+        rec[q].pos[0] = __double2float_rn(pw[0]);
+        rec[q].pos[1] = __double2float_rn(pw[1]);
+        rec[q].pos[2] = __double2float_rn(pw[2]);
+        corr_ref[q] = ko;
+        ++n;
       }
     }
     warp_count(n, &counts[LC_COUNT_CORR_MP]);
   } else {
+    pdl_wait();
     const int i = (blockIdx.x - nb_mp) * blockDim.x + threadIdx.x;
     if (i < n_w) {
       const double* T = scr + (size_t)WSTR * i + 42;
@@ -155,6 +160,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_win_b(
 __global__ void k_all_kf(int n_kf, const double* __restrict__ Sopt, double* __restrict__ kf_pose,
                          const double* __restrict__ kf_S_corr, int32_t* __restrict__ kf_in_win,
                          double* __restrict__ scr, unsigned long long* __restrict__ counts) {
+  pdl_trigger();   // k_all_points' prologue reads none of this kernel's outputs
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t n = 0;
   if (k < n_kf) {
@@ -179,37 +185,35 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_all_points(
     const uint8_t* __restrict__ flags, MpRec* __restrict__ rec, int32_t* __restrict__ corr_ref,
     unsigned long long* __restrict__ counts) {
   uint32_t n = 0;
-  const int stride = gridDim.x * blockDim.x;
-  for (int q0 = blockIdx.x * blockDim.x; q0 < n_mp; q0 += stride) {
-    const int q = q0 + threadIdx.x;
-    if (q < n_mp) {
-      const int cr = corr_ref[q];
-      if (cr >= 0) corr_ref[q] = -1;
-      if (!(flags[q] & 1u)) {
-        const int r = cr >= 0 ? cr : ref_kf[q];
-        const double* S = scr + (size_t)ASTR * r;
-        double pre[13], inv[13];
-        load13(S, pre);
-        load13(S + 14, inv);
-        const float4 pf = *reinterpret_cast<const float4*>(rec + q);
-        double p[3] = {pf.x, pf.y, pf.z}, pc[3], pw[3];
-        lc_sim3_apply(pre, p, pc);
-        lc_sim3_apply(inv, pc, pw);
-        rec[q].pos[0] = __double2float_rn(pw[0]);
-        rec[q].pos[1] = __double2float_rn(pw[1]);
-        rec[q].pos[2] = __double2float_rn(pw[2]);
-        ++n;
-      }
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;   // one point per thread
+  int cr = -1, rk = 0;
+  uint8_t fl = 1;
+  float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (q < n_mp) {   // per-point loads: independent of k_all_kf, before the PDL wait
+    cr = corr_ref[q];
+    rk = ref_kf[q];
+    fl = flags[q];
+    pf = *reinterpret_cast<const float4*>(rec + q);
+  }
+  pdl_wait();
+  if (q < n_mp) {
+    if (cr >= 0) corr_ref[q] = -1;
+    if (!(fl & 1u)) {
+      const int r = cr >= 0 ? cr : rk;
+      const double* S = scr + (size_t)ASTR * r;
+      double pre[13], inv[13];
+      load13(S, pre);
+      load13(S + 14, inv);
+      double p[3] = {pf.x, pf.y, pf.z}, pc[3], pw[3];
+      lc_sim3_apply(pre, p, pc);
+      lc_sim3_apply(inv, pc, pw);
+      rec[q].pos[0] = __double2float_rn(pw[0]);
+      rec[q].pos[1] = __double2float_rn(pw[1]);
+      rec[q].pos[2] = __double2float_rn(pw[2]);
+      ++n;
     }
   }
   warp_count(n, &counts[LC_COUNT_CORR_MP]);
-}
-
-int grid_for(int64_t n) {
-  int64_t b = (n + LC_NTHREADS - 1) / LC_NTHREADS;
-  if (b < 1) b = 1;
-  if (b > 148 * 16) b = 148 * 16;
-  return (int)b;
 }
 
 }  // namespace
@@ -227,12 +231,15 @@ cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t
   if ((e = cudaMemsetAsync(st.kf_in_win, 0, sizeof(int32_t) * st.n_kf, s)) != cudaSuccess) return e;
   k_win_sim3<<<(n_w + 63) / 64, 64, 0, s>>>(n_w, cur_pos, d_window, st.kf_pose, d_Scw, d_scr,
                                             st.kf_S_corr, st.kf_in_win);
-  k_win_mark<<<std::min((n_w + 7) / 8, 148 * 8), LC_NTHREADS, 0, s>>>(n_w, d_window, st.kf_fbeg,
-                                                                    st.feat_mp, st.mp_flags, st.mp_owner);
-  const int nb_mp = st.n_mp > 0 ? grid_for(st.n_mp) : 0;
+  if ((e = launch_pdl(k_win_mark, dim3(std::min((n_w + 7) / 8, 148 * 8)), dim3(LC_NTHREADS), 0, s, n_w,
+                      d_window, st.kf_fbeg, st.feat_mp, st.mp_owner)) != cudaSuccess)
+    return e;
+  const int nb_mp = st.n_mp > 0 ? (st.n_mp + LC_NTHREADS - 1) / LC_NTHREADS : 0;
   const int nb_w = (n_w + LC_NTHREADS - 1) / LC_NTHREADS;
-  k_win_b<<<nb_mp + nb_w, LC_NTHREADS, 0, s>>>(st.n_mp, nb_mp, n_w, st.mp_owner, d_window, d_scr,
-                                               st.mp_rec, st.mp_corr_ref, st.kf_pose, counts);
+  if ((e = launch_pdl(k_win_b, dim3(nb_mp + nb_w), dim3(LC_NTHREADS), 0, s, st.n_mp, nb_mp, n_w,
+                      st.mp_owner, st.mp_flags, d_window, d_scr, st.mp_rec, st.mp_corr_ref, st.kf_pose,
+                      counts)) != cudaSuccess)
+    return e;
   c->launches += 3;
   return cudaGetLastError();
 }
@@ -244,9 +251,11 @@ cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
                                                 st.kf_in_win, d_scr, counts);
   c->launches++;
   if (st.n_mp > 0) {
-    k_all_points<<<grid_for(st.n_mp), LC_NTHREADS, 0, s>>>(st.n_mp, d_scr, st.mp_ref_kf,
-                                                          st.mp_flags, st.mp_rec, st.mp_corr_ref,
-                                                          counts);
+    cudaError_t e = launch_pdl(k_all_points, dim3((st.n_mp + LC_NTHREADS - 1) / LC_NTHREADS),
+                               dim3(LC_NTHREADS), 0, s, st.n_mp, (const double*)d_scr,
+                               (const int32_t*)st.mp_ref_kf, (const uint8_t*)st.mp_flags, st.mp_rec,
+                               st.mp_corr_ref, counts);
+    if (e != cudaSuccess) return e;
     c->launches++;
   }
   return cudaGetLastError();

@@ -305,11 +305,13 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
   }
   __syncthreads();
   if (tid == 0) a.surv_cnt[blockIdx.x] = s_cnt;
+  pdl_trigger();
   uint32_t cnt[7];
   cnt[0] = cQ; cnt[1] = cA & 1023u; cnt[2] = (cA >> 10) & 1023u; cnt[3] = (cA >> 20) & 1023u;
   cnt[4] = cB & 1023u; cnt[5] = (cB >> 10) & 1023u; cnt[6] = (cB >> 20) & 1023u;
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
   block_add<7>(cnt, kProjSlot, cdst);
+  pdl_wait();   // (PDL) reads nothing k_fuse_prep writes; completes after it
 }
 
 // ---- k_match ------------------------------------------------------------------
@@ -408,6 +410,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   unsigned long long* win = a.winner + a.unit_woff[unit];
   const int64_t q0 = a.blk_q0[blockIdx.x];
   const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
+  pdl_wait();   // survivors of k_project from here on
   const Surv* sv = a.surv + a.surv_off[blockIdx.x];
   const int ns_tot = a.surv_cnt[blockIdx.x];
   uint32_t cC = 0, cP = 0, cE = 0;   // NOCAND | OVERTH << 10 | RATIO << 20; PROP; CAND
@@ -575,6 +578,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
     }
     __syncwarp();
   }
+  pdl_trigger();
   uint32_t cnt[5];
   cnt[0] = cE; cnt[1] = cC & 1023u; cnt[2] = (cC >> 10) & 1023u; cnt[3] = (cC >> 20) & 1023u; cnt[4] = cP;
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
@@ -725,6 +729,7 @@ __global__ void k_fuse_prep(int phase, int init_winner, uint32_t* __restrict__ e
                             unsigned long long* __restrict__ victim, uint32_t* __restrict__ loop_ep,
                             uint32_t* __restrict__ kf_win_ep, int32_t* __restrict__ kf_win_pos,
                             uint32_t* __restrict__ vbits, int n_vbits, int32_t* __restrict__ dirty_n) {
+  pdl_trigger();   // k_project reads none of this kernel's outputs
   uint32_t epoch = ep[0] + 1u;
   if (epoch == 0u) epoch = 1u;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -759,6 +764,7 @@ __global__ void k_fuse_prep(int phase, int init_winner, uint32_t* __restrict__ e
 __global__ void k_fuse_victims(int n_mp, const unsigned long long* __restrict__ victim,
                                uint8_t* __restrict__ flags, int32_t* __restrict__ replaced_by,
                                uint32_t* __restrict__ vbits, unsigned long long* __restrict__ counts) {
+  pdl_wait();
   uint32_t n = 0;
   const int stride = gridDim.x * blockDim.x;
   for (int q0 = blockIdx.x * blockDim.x; q0 < n_mp; q0 += stride) {
@@ -776,6 +782,7 @@ __global__ void k_fuse_victims(int n_mp, const unsigned long long* __restrict__ 
     const unsigned m = __ballot_sync(0xffffffffu, isv);   // q0 is a multiple of 32
     if ((threadIdx.x & 31) == 0 && m) vbits[(q0 + threadIdx.x) >> 5] = m;
   }
+  pdl_trigger();
   const int slot[1] = {LC_COUNT_VICTIMS};
   uint32_t loc[1] = {n};
   block_add<1>(loc, slot, counts);
@@ -790,6 +797,8 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_mark(
     const int64_t* __restrict__ woff_of_pos, const unsigned long long* __restrict__ winner,
     const uint32_t* __restrict__ vbits, const int32_t* __restrict__ feat_mp,
     int32_t* __restrict__ dirty_list) {
+  pdl_wait();
+  pdl_trigger();   // one wave: k_apply_fix may take the remaining slots now
   const uint32_t epoch = *ep;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -843,6 +852,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
     const unsigned long long* __restrict__ victim, const uint32_t* __restrict__ vbits,
     const int32_t* __restrict__ dirty_list, int32_t* __restrict__ feat_mp, int32_t* __restrict__ nobs,
     int hash_size, unsigned long long* __restrict__ counts) {
+  pdl_wait();
   const uint32_t epoch = *ep;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t cnt[A_N] = {0, 0, 0};
@@ -966,8 +976,7 @@ cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, int part, cudaStrea
     const int hb = HashSize<FCAP>::HS * (int)sizeof(int32_t);
     cudaError_t e = cudaFuncSetAttribute(k_project<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, hb);
     if (e != cudaSuccess) return e;
-    k_project<MODE, FCAP><<<n_blocks, LC_NTHREADS, hb, s>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(k_project<MODE, FCAP>, dim3(n_blocks), dim3(LC_NTHREADS), hb, s, a);
   }
   const size_t smem = (size_t)SM::CELL + (((size_t)a.Gs * 2 + 15) & ~(size_t)15);
   cudaError_t e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -975,8 +984,7 @@ cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, int part, cudaStrea
   e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
-  k_match<MODE, FCAP><<<n_blocks, LC_NTHREADS, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_match<MODE, FCAP>, dim3(n_blocks), dim3(LC_NTHREADS), smem, s, a);
 }
 
 template <int MODE>
@@ -1029,23 +1037,29 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
                               cudaStream_t s) {
   Store& st = c->st;
   if (st.n_mp > 0) {
-    k_fuse_victims<<<grid_for(st.n_mp), LC_NTHREADS, 0, s>>>(st.n_mp, victim, st.mp_flags,
-                                                             st.mp_replaced_by, st.mp_vbits, counts);
+    cudaError_t e = launch_pdl(k_fuse_victims, dim3(grid_for(st.n_mp)), dim3(LC_NTHREADS), 0, s, st.n_mp,
+                               victim, st.mp_flags, st.mp_replaced_by, st.mp_vbits, counts);
+    if (e != cudaSuccess) return e;
     c->launches++;
   }
   if (st.n_kf > 0) {
-    k_apply_mark<<<std::min((st.n_kf + NWARP - 1) / NWARP, 148 * 8), LC_NTHREADS, 0, s>>>(
-        st.n_kf, st.ep, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos, d_woff, winner, st.mp_vbits,
-        st.feat_mp, st.kf_dirty);
+    cudaError_t e = launch_pdl(k_apply_mark, dim3(std::min((st.n_kf + NWARP - 1) / NWARP, 148 * 8)),
+                               dim3(LC_NTHREADS), 0, s, st.n_kf, (const uint32_t*)st.ep,
+                               (const int32_t*)st.kf_fbeg, (const uint32_t*)st.kf_win_ep,
+                               (const int32_t*)st.kf_win_pos, d_woff, winner, (const uint32_t*)st.mp_vbits,
+                               (const int32_t*)st.feat_mp, st.kf_dirty);
+    if (e != cudaSuccess) return e;
     const int Fm = st.max_F > 0 ? st.max_F : 1;
     const int H = ((Fm + Fm / 2 + 1) + 31) & ~31;
     size_t smem = (size_t)H * 8 + (size_t)(1 << (FILT_LOG2 - 3)) + (size_t)Fm * 9 + 16;
     smem = (smem + 15) & ~(size_t)15;
-    cudaError_t e = cudaFuncSetAttribute(k_apply_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(k_apply_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_apply_fix<<<std::min(st.n_kf, 148 * 4), LC_NTHREADS, smem, s>>>(
-        st.ep, st.kf_fbeg, st.kf_win_ep, st.kf_win_pos, d_woff, winner, victim, st.mp_vbits,
-        st.kf_dirty, st.feat_mp, st.mp_nobs, H, counts);
+    e = launch_pdl(k_apply_fix, dim3(std::min(st.n_kf, 148 * 4)), dim3(LC_NTHREADS), smem, s,
+                   (const uint32_t*)st.ep, (const int32_t*)st.kf_fbeg, (const uint32_t*)st.kf_win_ep,
+                   (const int32_t*)st.kf_win_pos, d_woff, winner, victim, (const uint32_t*)st.mp_vbits,
+                   (const int32_t*)st.kf_dirty, st.feat_mp, st.mp_nobs, H, counts);
+    if (e != cudaSuccess) return e;
     c->launches += 2;
   }
   return cudaGetLastError();

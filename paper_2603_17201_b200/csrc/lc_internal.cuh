@@ -285,6 +285,32 @@ __device__ __forceinline__ void lc_project(const DevCam& c, double x, double y, 
 }
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL). A kernel launched with launch_pdl may start
+// while its stream predecessor is still running; it must (1) touch only data no
+// unfinished predecessor writes before pdl_wait(), and (2) execute pdl_wait() before
+// it exits (so "predecessor complete" stays transitive along the stream). pdl_trigger()
+// lets the next PDL kernel launch once every CTA has triggered or exited.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// ---------------------------------------------------------------------------
 // kernel launchers (defined in the .cu files)
 // ---------------------------------------------------------------------------
 cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, const float* dmax,
