@@ -147,6 +147,10 @@ __device__ __forceinline__ bool hhas(const int32_t* tab, uint32_t size, int32_t 
   }
 }
 
+// fp32 window-filter margin (px): |fuv - fu| in fp32 is within 2.5e-4 (rounding of the
+// exact u to fp32) + 4.9e-4 (fp32 subtraction at |u| < 4096) px of the exact distance
+constexpr float kWinTol = 1e-3f;
+
 template <int FCAP>
 struct HashSize {
   static constexpr int HS = ((2 * FCAP + 1) + 31) & ~31;   // load factor <= 0.5
@@ -189,12 +193,24 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
   for (int i = tid; i < (int)HS; i += LC_NTHREADS) s_hash[i] = -1;
   for (int i = tid; i < (1 << (FILT_LOG2 - 5)); i += LC_NTHREADS) s_filt[i] = 0u;
   __syncthreads();
-  for (int f = tid; f < F; f += LC_NTHREADS) {
-    int32_t m = (MODE == 0) ? a.feat_mp[fb + f] : (a.taken ? a.taken[toff + f] : -1);
-    if (m >= 0) {
-      const uint32_t b = fslot(m);
-      atomicOr(&s_filt[b >> 5], 1u << (b & 31));
-      hins(s_hash, HS, m);
+  // the keyframe's associations: 8 loads per thread in flight, then the inserts
+  const int32_t* assoc = (MODE == 0) ? a.feat_mp + fb : (a.taken ? a.taken + toff : nullptr);
+  if (assoc) {
+    for (int f0 = tid; f0 < F; f0 += 8 * LC_NTHREADS) {
+      int32_t m[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = f0 + u * LC_NTHREADS;
+        m[u] = f < F ? __ldg(assoc + f) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (m[u] >= 0) {
+          const uint32_t b = fslot(m[u]);
+          atomicOr(&s_filt[b >> 5], 1u << (b & 31));
+          hins(s_hash, HS, m[u]);
+        }
+      }
     }
   }
   __syncthreads();
@@ -421,8 +437,8 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   auto win_f32 = [&](const float2 fuv, float fu, float fv, float fr) -> int {
     if (!f32ok) return -1;
     const float du = fabsf(fuv.x - fu), dv = fabsf(fuv.y - fv);
-    if (du > fr + 1e-3f || dv > fr + 1e-3f) return 0;
-    if (du < fr - 1e-3f && dv < fr - 1e-3f) return 1;
+    if (du > fr + kWinTol || dv > fr + kWinTol) return 0;
+    if (du < fr - kWinTol && dv < fr - kWinTol) return 1;
     return -1;
   };
 
