@@ -467,20 +467,43 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
       // (1) window scan over the staged cells, octave filter (A9) first; slots whose
       // fp32 window test is ambiguous are marked and settled in fp64 after the scan
       uint32_t amb = 0u;
-      for (int cy = cy0; cy <= cy1; ++cy) {
-        const int pe = s_cell[cy * cols + cx1 + 1];
-        for (int p = s_cell[cy * cols + cx0]; p < pe; ++p) {
-          const uint32_t meta = s_meta[p];
-          const int oct = (int)((meta >> 16) & 0xFFu);
-          if (oct < lo || oct > lvl) continue;
-          if (MODE == 1 && (meta & 0x80000000u)) continue;
-          const int w = win_f32(s_uv[p], e.fu, e.fv, fr);
-          if (w == 0) continue;
-          if (nc < CPL) {
-            s_cand[lane * CPL + nc] = (uint16_t)p;
-            if (w < 0) amb |= 1u << nc;
+      // the lane's rows are visited 4 at a time and each row's features 4 at a time:
+      // all shared-memory loads of a batch are issued together, then the tests run on
+      // registers (the scan is latency-bound on dependent shared loads otherwise)
+      for (int cb = cy0; cb <= cy1; cb += 4) {
+        int ps[4], pe[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int cy = min(cb + u, cy1);
+          ps[u] = s_cell[cy * cols + cx0];
+          pe[u] = cb + u <= cy1 ? (int)s_cell[cy * cols + cx1 + 1] : ps[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          for (int p0 = ps[u]; p0 < pe[u]; p0 += 4) {
+            uint32_t mt[4];
+            float2 fuv[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int pp = min(p0 + t, pe[u] - 1);
+              mt[t] = s_meta[pp];
+              fuv[t] = s_uv[pp];
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              if (p0 + t >= pe[u]) break;
+              const int oct = (int)((mt[t] >> 16) & 0xFFu);
+              if (oct < lo || oct > lvl) continue;
+              if (MODE == 1 && (mt[t] & 0x80000000u)) continue;
+              const int w = win_f32(fuv[t], e.fu, e.fv, fr);
+              if (w == 0) continue;
+              if (nc < CPL) {
+                s_cand[lane * CPL + nc] = (uint16_t)(p0 + t);
+                if (w < 0) amb |= 1u << nc;
+              }
+              ++nc;
+            }
           }
-          ++nc;
         }
       }
       if (amb && nc <= CPL) {   // rare: one exact projection, drop slots outside the window
