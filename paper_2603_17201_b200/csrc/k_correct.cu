@@ -24,6 +24,21 @@ constexpr int WSTR = 56;
 // ALL scratch per keyframe: [0, 13) S^pre | [14, 27) inverse(S^opt)
 constexpr int ASTR = 28;
 constexpr int32_t OWNER_NONE = 0x7F7F7F7F;  // memset byte pattern 0x7F
+#ifndef LC_PT_MINB
+#define LC_PT_MINB 2   // point kernels: CTAs per SM the register budget is cut for
+#endif
+#ifndef LC_OWN_PRECHECK
+#define LC_OWN_PRECHECK 0
+#endif
+
+// owner election step: a plain (possibly stale) read can only over-estimate the
+// current owner, so skipping the reduction when it is already <= i is exact
+__device__ __forceinline__ void own_min(int32_t* owner, int m, int i) {
+#if LC_OWN_PRECHECK
+  if (owner[m] <= i) return;
+#endif
+  atomicMin(&owner[m], i);
+}
 
 __device__ __forceinline__ void load13(const double* __restrict__ src, double* d) {
   const double2* s2 = reinterpret_cast<const double2*>(src);
@@ -79,7 +94,7 @@ __global__ void k_win_sim3(int n_w, int cur_pos, const int32_t* __restrict__ win
 // owner too; k_win_b ignores them (it reads the flags coalesced, per point).
 __global__ void __launch_bounds__(LC_NTHREADS) k_win_mark(
     int n_w, const int32_t* __restrict__ window, const int32_t* __restrict__ kf_fbeg,
-    const int32_t* __restrict__ feat_mp, int32_t* __restrict__ owner) {
+    const int32_t* __restrict__ feat_mp, int32_t* owner) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -89,18 +104,18 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_win_mark(
     const int vb = min(fe, (fb + 3) & ~3), ve = max(vb, fe & ~3);
     for (int f = fb + lane; f < vb; f += 32) {
       const int m = feat_mp[f];
-      if (m >= 0) atomicMin(&owner[m], i);
+      if (m >= 0) own_min(owner, m, i);
     }
     for (int f = vb + 4 * lane; f < ve; f += 128) {
       const int4 m4 = __ldg(reinterpret_cast<const int4*>(feat_mp + f));
-      if (m4.x >= 0) atomicMin(&owner[m4.x], i);
-      if (m4.y >= 0) atomicMin(&owner[m4.y], i);
-      if (m4.z >= 0) atomicMin(&owner[m4.z], i);
-      if (m4.w >= 0) atomicMin(&owner[m4.w], i);
+      if (m4.x >= 0) own_min(owner, m4.x, i);
+      if (m4.y >= 0) own_min(owner, m4.y, i);
+      if (m4.z >= 0) own_min(owner, m4.z, i);
+      if (m4.w >= 0) own_min(owner, m4.w, i);
     }
     for (int f = ve + lane; f < fe; f += 32) {
       const int m = feat_mp[f];
-      if (m >= 0) atomicMin(&owner[m], i);
+      if (m >= 0) own_min(owner, m, i);
     }
   }
   pdl_wait();   // (PDL) independent of k_win_sim3; completes after it
@@ -108,40 +123,53 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_win_mark(
 
 // Blocks [0, nb_mp): p <- fl32( inverse(S_o^corr)( T_o,w^old(p) ) ), corr_ref <- window[o]
 // (or -1); blocks [nb_mp, ...): window pose write-back T_iw <- SE3(S_i^corr).
-__global__ void __launch_bounds__(LC_NTHREADS) k_win_b(
+__global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_win_b(
     int n_mp, int nb_mp, int n_w, const int32_t* __restrict__ owner, const uint8_t* __restrict__ flags,
     const int32_t* __restrict__ window, const double* __restrict__ scr, MpRec* __restrict__ rec,
     int32_t* __restrict__ corr_ref, double* __restrict__ kf_pose,
     unsigned long long* __restrict__ counts) {
   uint32_t n = 0;
-  if ((int)blockIdx.x < nb_mp) {   // one point per thread (nb_mp * blockDim.x >= n_mp)
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    uint8_t fl = 1;
-    float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (q < n_mp) {   // independent of the predecessors: before the PDL wait
-      fl = flags[q];
-      pf = *reinterpret_cast<const float4*>(rec + q);
+  if ((int)blockIdx.x < nb_mp) {   // two adjacent points per thread (2 nb_mp blockDim.x >= n_mp)
+    const int q0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    uint8_t fl[2] = {1, 1};
+    float4 pf[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {   // independent of the predecessors: before the PDL wait
+      pf[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (q0 + u < n_mp) {
+        fl[u] = flags[q0 + u];
+        pf[u] = *reinterpret_cast<const float4*>(rec + q0 + u);
+      }
     }
     pdl_wait();
-    if (q < n_mp) {
-      const int o = owner[q];
-      if (o == OWNER_NONE || (fl & 1u)) {   // unobserved by the window, or bad
+    int o[2] = {OWNER_NONE, OWNER_NONE};
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (q0 + u < n_mp) o[u] = owner[q0 + u];
+    double T[13], Si[13];
+    int have = -1;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int q = q0 + u;
+      if (q >= n_mp) break;
+      if (o[u] == OWNER_NONE || (fl[u] & 1u)) {   // unobserved by the window, or bad
         corr_ref[q] = -1;
-      } else {
-        const double* S = scr + (size_t)WSTR * o;
-        double T[13], Si[13];
+        continue;
+      }
+      if (o[u] != have) {
+        const double* S = scr + (size_t)WSTR * o[u];
         load13(S, T);
         load13(S + 14, Si);
-        const int ko = window[o];
-        double p[3] = {pf.x, pf.y, pf.z}, pc[3], pw[3];
-        lc_sim3_apply(T, p, pc);
-        lc_sim3_apply(Si, pc, pw);
-        rec[q].pos[0] = __double2float_rn(pw[0]);
-        rec[q].pos[1] = __double2float_rn(pw[1]);
-        rec[q].pos[2] = __double2float_rn(pw[2]);
-        corr_ref[q] = ko;
-        ++n;
+        have = o[u];
       }
+      double p[3] = {pf[u].x, pf[u].y, pf[u].z}, pc[3], pw[3];
+      lc_sim3_apply(T, p, pc);
+      lc_sim3_apply(Si, pc, pw);
+      rec[q].pos[0] = __double2float_rn(pw[0]);
+      rec[q].pos[1] = __double2float_rn(pw[1]);
+      rec[q].pos[2] = __double2float_rn(pw[2]);
+      corr_ref[q] = window[o[u]];
+      ++n;
     }
     warp_count(n, &counts[LC_COUNT_CORR_MP]);
   } else {
@@ -180,38 +208,51 @@ __global__ void k_all_kf(int n_kf, const double* __restrict__ Sopt, double* __re
   warp_count(n, &counts[LC_COUNT_CORR_KF]);
 }
 
-__global__ void __launch_bounds__(LC_NTHREADS) k_all_points(
+// Two adjacent points per thread (they share their reference keyframe in creation
+// order, so the two 13-double transforms are loaded once): every per-point load is
+// issued before the PDL wait, the transform gather after it.
+__global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_all_points(
     int n_mp, const double* __restrict__ scr, const int32_t* __restrict__ ref_kf,
     const uint8_t* __restrict__ flags, MpRec* __restrict__ rec, int32_t* __restrict__ corr_ref,
     unsigned long long* __restrict__ counts) {
   uint32_t n = 0;
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;   // one point per thread
-  int cr = -1, rk = 0;
-  uint8_t fl = 1;
-  float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (q < n_mp) {   // per-point loads: independent of k_all_kf, before the PDL wait
-    cr = corr_ref[q];
-    rk = ref_kf[q];
-    fl = flags[q];
-    pf = *reinterpret_cast<const float4*>(rec + q);
+  const int q0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  int cr[2] = {-1, -1}, rk[2] = {0, 0};
+  uint8_t fl[2] = {1, 1};
+  float4 pf[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    pf[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q0 + u < n_mp) {
+      cr[u] = corr_ref[q0 + u];
+      rk[u] = ref_kf[q0 + u];
+      fl[u] = flags[q0 + u];
+      pf[u] = *reinterpret_cast<const float4*>(rec + q0 + u);
+    }
   }
   pdl_wait();
-  if (q < n_mp) {
-    if (cr >= 0) corr_ref[q] = -1;
-    if (!(fl & 1u)) {
-      const int r = cr >= 0 ? cr : rk;
+  double pre[13], inv[13];
+  int have = -1;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int q = q0 + u;
+    if (q >= n_mp) break;
+    if (cr[u] >= 0) corr_ref[q] = -1;
+    if (fl[u] & 1u) continue;
+    const int r = cr[u] >= 0 ? cr[u] : rk[u];
+    if (r != have) {
       const double* S = scr + (size_t)ASTR * r;
-      double pre[13], inv[13];
       load13(S, pre);
       load13(S + 14, inv);
-      double p[3] = {pf.x, pf.y, pf.z}, pc[3], pw[3];
-      lc_sim3_apply(pre, p, pc);
-      lc_sim3_apply(inv, pc, pw);
-      rec[q].pos[0] = __double2float_rn(pw[0]);
-      rec[q].pos[1] = __double2float_rn(pw[1]);
-      rec[q].pos[2] = __double2float_rn(pw[2]);
-      ++n;
+      have = r;
     }
+    double p[3] = {pf[u].x, pf[u].y, pf[u].z}, pc[3], pw[3];
+    lc_sim3_apply(pre, p, pc);
+    lc_sim3_apply(inv, pc, pw);
+    rec[q].pos[0] = __double2float_rn(pw[0]);
+    rec[q].pos[1] = __double2float_rn(pw[1]);
+    rec[q].pos[2] = __double2float_rn(pw[2]);
+    ++n;
   }
   warp_count(n, &counts[LC_COUNT_CORR_MP]);
 }
@@ -234,7 +275,7 @@ cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t
   if ((e = launch_pdl(k_win_mark, dim3(std::min((n_w + 7) / 8, 148 * 8)), dim3(LC_NTHREADS), 0, s, n_w,
                       d_window, st.kf_fbeg, st.feat_mp, st.mp_owner)) != cudaSuccess)
     return e;
-  const int nb_mp = st.n_mp > 0 ? (st.n_mp + LC_NTHREADS - 1) / LC_NTHREADS : 0;
+  const int nb_mp = st.n_mp > 0 ? (st.n_mp + 2 * LC_NTHREADS - 1) / (2 * LC_NTHREADS) : 0;
   const int nb_w = (n_w + LC_NTHREADS - 1) / LC_NTHREADS;
   if ((e = launch_pdl(k_win_b, dim3(nb_mp + nb_w), dim3(LC_NTHREADS), 0, s, st.n_mp, nb_mp, n_w,
                       st.mp_owner, st.mp_flags, d_window, d_scr, st.mp_rec, st.mp_corr_ref, st.kf_pose,
@@ -251,7 +292,7 @@ cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
                                                 st.kf_in_win, d_scr, counts);
   c->launches++;
   if (st.n_mp > 0) {
-    cudaError_t e = launch_pdl(k_all_points, dim3((st.n_mp + LC_NTHREADS - 1) / LC_NTHREADS),
+    cudaError_t e = launch_pdl(k_all_points, dim3((st.n_mp + 2 * LC_NTHREADS - 1) / (2 * LC_NTHREADS)),
                                dim3(LC_NTHREADS), 0, s, st.n_mp, (const double*)d_scr,
                                (const int32_t*)st.mp_ref_kf, (const uint8_t*)st.mp_flags, st.mp_rec,
                                st.mp_corr_ref, counts);
