@@ -349,6 +349,10 @@ lc_status lc_correct_sim3(lc_ctx* ctx, int32_t mode, int32_t cur_kf, const lc_si
  *   window_kf, window_S (nullable), win_list_begin (nullable) [host], n_window >= 1
  *   distinct keyframes; mp_list [host|dev] n_list entries, each list ascending
  *   and unique (not checked on device; duplicates give duplicate queries).
+ *   A host mp_list with per-keyframe lists (win_list_begin) on a full-range PLAN
+ *   (>= 2^18 entries, no dbg, not capturing) is uploaded in 4 chunks on a private
+ *   stream while the matching of the chunks already resident runs (same results;
+ *   the buffer must stay unchanged until the call stream has passed the call).
  *   io_winner [host|dev] nullable (internal), [sum_i F(window_kf[i])] window-major,
  *     local feature order: the surviving winner word per window feature.
  *   io_victim [host|dev] nullable (internal), [n_mp].

@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const unsigned ltmask = (1u << lane) - 1u;
-  const int unit = a.blk_unit[blockIdx.x];
+  const int blk = a.blk_base + (int)blockIdx.x;
+  const int unit = a.blk_unit[blk];
   const int k = a.unit_kf[unit];
   const int fb = a.kf_fbeg[k];
   const int F = a.kf_fbeg[k + 1] - fb;
@@ -219,9 +220,10 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
   const double c08 = 0.8 / sLm1;   // for the division-free pre-test only
   const bool pinhole = s_cam.model == 0;
   const float inv_lsf = 1.0f / logf((float)a.scale[1]);
-  const int64_t q0 = a.blk_q0[blockIdx.x], q1 = a.blk_q1[blockIdx.x];
+  const int64_t q0 = a.blk_q0[blk], q1 = a.blk_q1[blk];
+  const uint32_t epoch = a.loop_ep_w ? *a.epoch : 0u;
   const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
-  Surv* out = a.surv + a.surv_off[blockIdx.x];
+  Surv* out = a.surv + a.surv_off[blk];
   uint32_t cA = 0, cB = 0, cQ = 0;   // packed 10-bit counters (<= 64 queries per thread per block)
   // software pipeline: the record of the next query and the list entry of the one
   // after are in flight while the current query is evaluated
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
     const uint4 r0 = n0, r1 = n1;
     const uint8_t flag = nfl;
     const bool in_range = valid && (unsigned)q < (unsigned)a.n_mp;
+    if (a.loop_ep_w && in_range) a.loop_ep_w[q] = epoch;   // LoopSet stamp (pipelined mode)
     q_nx = q_nn;
     q_nn = list_at(j + 2 * LC_NTHREADS);
     rec_at(q_nx, n0, n1, nfl);
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
     }
   }
   __syncthreads();
-  if (tid == 0) a.surv_cnt[blockIdx.x] = s_cnt;
+  if (tid == 0) a.surv_cnt[blk] = s_cnt;
   pdl_trigger();
   uint32_t cnt[7];
   cnt[0] = cQ; cnt[1] = cA & 1023u; cnt[2] = (cA >> 10) & 1023u; cnt[3] = (cA >> 20) & 1023u;
@@ -370,7 +373,8 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   __shared__ __align__(16) DevCam s_cam;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int unit = a.blk_unit[blockIdx.x];
+  const int blk = a.blk_base + (int)blockIdx.x;
+  const int unit = a.blk_unit[blk];
   const int k = a.unit_kf[unit];
   const int fb = a.kf_fbeg[k];
   const int F = a.kf_fbeg[k + 1] - fb;
@@ -424,11 +428,11 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   const float fminx = (float)s_cam.min_x, fminy = (float)s_cam.min_y;
   const float fsx = (float)s_cam.cell_sx, fsy = (float)s_cam.cell_sy;
   unsigned long long* win = a.winner + a.unit_woff[unit];
-  const int64_t q0 = a.blk_q0[blockIdx.x];
+  const int64_t q0 = a.blk_q0[blk];
   const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
   pdl_wait();   // survivors of k_project from here on
-  const Surv* sv = a.surv + a.surv_off[blockIdx.x];
-  const int ns_tot = a.surv_cnt[blockIdx.x];
+  const Surv* sv = a.surv + a.surv_off[blk];
+  const int ns_tot = a.surv_cnt[blk];
   uint32_t cC = 0, cP = 0, cE = 0;   // NOCAND | OVERTH << 10 | RATIO << 20; PROP; CAND
 
   // strict square window |fuv - uv| < r (reading A8). fp32 filter: |(float)a - fu| is
@@ -1009,13 +1013,18 @@ int grid_for(int64_t n) {
 }  // namespace
 
 template <int MODE, int FCAP>
-cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, int part, cudaStream_t s) {
+cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, int part, bool pdl, cudaStream_t s) {
   using SM = MatchSmem<FCAP>;
+  auto go = [&](auto kernel, size_t smem) -> cudaError_t {
+    if (pdl) return launch_pdl(kernel, dim3(n_blocks), dim3(LC_NTHREADS), smem, s, a);
+    kernel<<<n_blocks, LC_NTHREADS, smem, s>>>(a);
+    return cudaGetLastError();
+  };
   if (part == 0) {
     const int hb = HashSize<FCAP>::HS * (int)sizeof(int32_t);
     cudaError_t e = cudaFuncSetAttribute(k_project<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, hb);
     if (e != cudaSuccess) return e;
-    return launch_pdl(k_project<MODE, FCAP>, dim3(n_blocks), dim3(LC_NTHREADS), hb, s, a);
+    return go(k_project<MODE, FCAP>, (size_t)hb);
   }
   const size_t smem = (size_t)SM::CELL + (((size_t)a.Gs * 2 + 15) & ~(size_t)15);
   cudaError_t e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1023,23 +1032,23 @@ cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, int part, cudaStrea
   e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            cudaSharedmemCarveoutMaxShared);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k_match<MODE, FCAP>, dim3(n_blocks), dim3(LC_NTHREADS), smem, s, a);
+  return go(k_match<MODE, FCAP>, smem);
 }
 
 template <int MODE>
-cudaError_t launch_match_m(const MatchArgs& a, int n_blocks, int F_max, int part, cudaStream_t s) {
-  if (F_max <= 512) return launch_match_t<MODE, 512>(a, n_blocks, part, s);
-  if (F_max <= 1024) return launch_match_t<MODE, 1024>(a, n_blocks, part, s);
-  if (F_max <= 2048) return launch_match_t<MODE, 2048>(a, n_blocks, part, s);
-  if (F_max <= 4096) return launch_match_t<MODE, 4096>(a, n_blocks, part, s);
-  return launch_match_t<MODE, 8192>(a, n_blocks, part, s);
+cudaError_t launch_match_m(const MatchArgs& a, int n_blocks, int F_max, int part, bool pdl, cudaStream_t s) {
+  if (F_max <= 512) return launch_match_t<MODE, 512>(a, n_blocks, part, pdl, s);
+  if (F_max <= 1024) return launch_match_t<MODE, 1024>(a, n_blocks, part, pdl, s);
+  if (F_max <= 2048) return launch_match_t<MODE, 2048>(a, n_blocks, part, pdl, s);
+  if (F_max <= 4096) return launch_match_t<MODE, 4096>(a, n_blocks, part, pdl, s);
+  return launch_match_t<MODE, 8192>(a, n_blocks, part, pdl, s);
 }
 
 cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max, int part,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool pdl) {
   if (n_blocks <= 0) return cudaSuccess;
-  cudaError_t e = mode == 0 ? launch_match_m<0>(a, n_blocks, F_max, part, s)
-                            : launch_match_m<1>(a, n_blocks, F_max, part, s);
+  cudaError_t e = mode == 0 ? launch_match_m<0>(a, n_blocks, F_max, part, pdl, s)
+                            : launch_match_m<1>(a, n_blocks, F_max, part, pdl, s);
   c->launches += 1;
   return e;
 }

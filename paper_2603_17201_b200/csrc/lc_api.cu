@@ -390,6 +390,8 @@ lc_status lc_create(lc_ctx** out, int32_t device) {
   for (int r = 0; ok && r < lc_ctx::kPinRing; ++r)
     ok = cudaEventCreateWithFlags(&c->pin_ev[r], cudaEventDisableTiming) == cudaSuccess;
   ok = ok && cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) == cudaSuccess;
+  for (int r = 0; ok && r <= lc_ctx::kPipe; ++r)
+    ok = cudaEventCreateWithFlags(&c->pipe_ev[r], cudaEventDisableTiming) == cudaSuccess;
   if (!ok) {
     for (int r = 0; r < lc_ctx::kPinRing; ++r)
       if (c->pin_ev[r]) cudaEventDestroy(c->pin_ev[r]);
@@ -416,6 +418,8 @@ lc_status lc_destroy(lc_ctx* c) {
   }
   if (c->sv) cudaFree(c->sv);
   if (c->side) cudaStreamDestroy(c->side);
+  for (int r = 0; r <= lc_ctx::kPipe; ++r)
+    if (c->pipe_ev[r]) cudaEventDestroy(c->pipe_ev[r]);
   for (auto& r : c->prof_pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   cudaGetLastError();
@@ -819,7 +823,13 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     int64_t max_len = 0;
     for (int i = w_lo; i < w_hi; ++i)
       max_len = std::max<int64_t>(max_len, win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list);
-    const bool sole = (w_hi - w_lo) >= 2 * 148 && max_len <= 16384;
+    // pipelined host list: a full-range PLAN whose per-keyframe lists are in host
+    // memory uploads them in kPipe chunks on a side stream; k_project / k_match run
+    // on each chunk's blocks as it lands (k_project stamps the LoopSet), the resolve
+    // after all of them
+    const bool pipe = (phase & LC_FUSE_PLAN) && win_list_begin && n_list >= (1 << 18) && !dbg &&
+                      !c->cap && w_lo == 0 && w_hi == n_window && !is_device_ptr(c, mp_list);
+    const bool sole = !pipe && (w_hi - w_lo) >= 2 * 148 && max_len <= 16384;
     const int64_t ch = sole ? std::max<int64_t>(max_len, 1) : pick_chunk(total_q);
     std::vector<int32_t> bunit;
     std::vector<int64_t> bq0, bq1;
@@ -862,7 +872,36 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     call.commit();
     Surv* d_surv = (Surv*)call.scratch(sizeof(Surv) * std::max<int64_t>(boff.back(), 1));
     int32_t* d_scnt = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(bunit.size(), 1));
-    const int32_t* d_list = call.in(mp_list, (size_t)n_list);
+    const int32_t* d_list = nullptr;
+    int pipe_b[lc_ctx::kPipe + 1] = {};   // block boundaries of the chunks
+    if (pipe) {
+      int32_t* dl = (int32_t*)call.scratch(sizeof(int32_t) * (size_t)n_list);
+      const int nb = (int)bunit.size();
+      const int64_t tot = boff[nb];
+      pipe_b[0] = 0;
+      for (int k = 1; k < lc_ctx::kPipe; ++k) {
+        int b = pipe_b[k - 1];
+        while (b < nb && boff[b] < tot * k / lc_ctx::kPipe) ++b;
+        pipe_b[k] = b;
+      }
+      pipe_b[lc_ctx::kPipe] = nb;
+      // the side stream first waits for the work already on the call stream (the list
+      // buffer may still be read by an earlier call)
+      CK(cudaEventRecord(c->pipe_ev[lc_ctx::kPipe], call.s));
+      CK(cudaStreamWaitEvent(c->side, c->pipe_ev[lc_ctx::kPipe], 0));
+      for (int k = 0; k < lc_ctx::kPipe; ++k) {
+        const int b0 = pipe_b[k], b1 = pipe_b[k + 1];
+        if (b1 > b0) {
+          const int64_t l0 = bq0[b0], l1 = bq1[b1 - 1];
+          CK(cudaMemcpyAsync(dl + l0, mp_list + l0, sizeof(int32_t) * (size_t)(l1 - l0),
+                             cudaMemcpyHostToDevice, c->side));
+        }
+        CK(cudaEventRecord(c->pipe_ev[k], c->side));
+      }
+      d_list = dl;
+    } else {
+      d_list = call.in(mp_list, (size_t)n_list);
+    }
     unsigned long long* win = (unsigned long long*)call.out(io_winner, (size_t)n_wfeat, phase == LC_FUSE_APPLY);
     if (!win) win = (unsigned long long*)call.scratch(sizeof(uint64_t) * std::max<int64_t>(n_wfeat, 1));
     unsigned long long* vic = (unsigned long long*)call.out(io_victim, (size_t)st.n_mp, phase == LC_FUSE_APPLY);
@@ -885,8 +924,8 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     else epoch_reserve(c, 1, call.s);
     {
       Prof pr(c, LC_PROF_FUSE_PREP, call.s);
-      CK(launch_fuse_prep(c, phase, sole ? 0 : 1, n_window, d_win, n_wfeat, d_list, n_list, win, vic,
-                          call.s));
+      CK(launch_fuse_prep(c, phase, sole ? 0 : 1, n_window, d_win, n_wfeat, d_list, pipe ? 0 : n_list,
+                          win, vic, call.s));
     }
     if (phase & LC_FUSE_PLAN) {
       a.unit_kf = d_win;
@@ -919,11 +958,26 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       a.surv = d_surv;
       a.surv_off = d_boff;
       a.surv_cnt = d_scnt;
-      {
-        Prof pr(c, LC_PROF_PROJECT, call.s);
-        CK(launch_match(c, 0, a, (int)bunit.size(), F_max, 0, call.s));
-      }
-      {
+      if (pipe) {
+        a.loop_ep_w = st.mp_loop_ep;
+        for (int k = 0; k < lc_ctx::kPipe; ++k) {
+          const int b0 = pipe_b[k], nbk = pipe_b[k + 1] - pipe_b[k];
+          CK(cudaStreamWaitEvent(call.s, c->pipe_ev[k], 0));
+          if (nbk == 0) continue;
+          a.blk_base = b0;
+          {
+            Prof pr(c, LC_PROF_PROJECT, call.s);
+            CK(launch_match(c, 0, a, nbk, F_max, 0, call.s, false));
+          }
+          Prof pr(c, LC_PROF_MATCH, call.s);
+          CK(launch_match(c, 0, a, nbk, F_max, 1, call.s));
+        }
+        a.blk_base = 0;
+      } else {
+        {
+          Prof pr(c, LC_PROF_PROJECT, call.s);
+          CK(launch_match(c, 0, a, (int)bunit.size(), F_max, 0, call.s));
+        }
         Prof pr(c, LC_PROF_MATCH, call.s);
         CK(launch_match(c, 0, a, (int)bunit.size(), F_max, 1, call.s));
       }

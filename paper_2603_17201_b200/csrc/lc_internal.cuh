@@ -148,6 +148,8 @@ struct MatchArgs {
   const int64_t* surv_off;  // [n_blocks] region start (= block query offset)
   int32_t* surv_cnt;        // [n_blocks] survivors written
   int32_t unit_base;   // k_resolve: unit = unit_base + blockIdx.x
+  int32_t blk_base;    // k_project / k_match: block = blk_base + blockIdx.x (pipelined chunks)
+  uint32_t* loop_ep_w; // non-null: k_project stamps the LoopSet (pipelined host-list mode)
 };
 
 struct lc_graph {
@@ -172,7 +174,9 @@ struct lc_ctx {
   lc_graph* cap = nullptr;
   cudaStream_t cap_stream = nullptr;
   int64_t cap_launch0 = 0;
-  cudaStream_t side = nullptr;   // private stream for capture-time uploads
+  cudaStream_t side = nullptr;   // private stream: capture-time uploads, pipelined list copies
+  static constexpr int kPipe = 4;              // chunks of a pipelined host-list fuse
+  cudaEvent_t pipe_ev[kPipe + 1] = {};          // [kPipe]: start (side waits on the call stream)
   int64_t launches = 0;
   // scratch arena: named growable device buffers
   std::vector<void*> scr_ptr;
@@ -318,7 +322,7 @@ cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, co
                                const uint8_t* foct, const uint8_t* fdesc, uint32_t* d_errs,
                                cudaStream_t s);
 cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max, int part,
-                         cudaStream_t s);  // part 0: k_project, 1: k_match
+                         cudaStream_t s, bool pdl = true);  // part 0: k_project, 1: k_match; blocks [a.blk_base, +n_blocks)  // part 0: k_project, 1: k_match
 cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, const int32_t* d_window,
                              int64_t n_wfeat, const int32_t* mp_list, int64_t n_list_total,
                              unsigned long long* winner, unsigned long long* victim, cudaStream_t s);

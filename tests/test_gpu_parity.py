@@ -284,3 +284,31 @@ def test_C5_full_size_sampled_parity(Ctx):
     vic = np.nonzero(g["victim"] != NONE)[0]
     assert len(vic) > 10000 and np.all(m["mp_nobs"][vic] == 0)
     assert np.all(m["mp_replaced_by"][vic] == (g["victim"][vic] & 0xFFFFFFFF))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("pinned", [False, True])
+def test_C5_pipelined_host_list_equals_device_list(Ctx, pinned):
+    """A full-range fuse whose per-keyframe lists are in host memory takes the pipelined
+    path (chunked upload on a side stream, k_project stamping the LoopSet, separate
+    resolve); it must equal, table for table, the sole-mode path a device-resident list
+    takes (itself pinned to the oracle above)."""
+    w = world("C5")
+    out = []
+    for mode in ("device", "host"):
+        ctx = Ctx(0)
+        ctx.upload_map(w.map_arrays(), [w.cam])
+        ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+        if mode == "device":
+            lst = torch.from_numpy(w.mp_list).cuda()
+        else:
+            lst = torch.from_numpy(w.mp_list).pin_memory() if pinned else w.mp_list
+        g = ctx.fuse(w.window, lst, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+        out.append((g, ctx.download_map()))
+        ctx.close()
+    (gd, md), (gh, mh) = out
+    for key in ("winner", "victim", "action"):
+        assert np.array_equal(gd[key], gh[key]), key
+    assert gd["counts"] == gh["counts"]
+    for key in md:
+        assert np.array_equal(md[key], mh[key]), key
