@@ -100,6 +100,16 @@ def test_loop_parity_small(Ctx, name, params):
     assert g["counts"]["candidates"] > 0 and g["counts"]["proposals"] > 0
 
 
+@pytest.mark.parametrize("name", ["T3K", "T6K"])
+def test_loop_parity_dense_keyframes(Ctx, name):
+    """3000 / 6000 features per keyframe: the FCAP 4096 / 8192 instantiations of
+    k_project / k_match (64-KB dynamic hash, 120-KB staged keyframe) and the larger
+    k_apply_fix shared-memory layout."""
+    w, g, o, ctx = _run_loop(Ctx, name, FUSE_PARAMS_CHECKS)
+    assert np.diff(w.kf_feat_begin).max() > {"T3K": 2048, "T6K": 4096}[name]
+    assert g["counts"]["candidates"] > 0 and g["counts"]["proposals"] > 0
+
+
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_loop_parity_euroc_tumvi(Ctx, name):
     w, g, o, ctx = _run_loop(Ctx, name, FUSE_PARAMS_CHECKS)
