@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--grid", default=os.environ.get("LC_GRID", "64x48"),
                     help="per-keyframe cell grid COLSxROWS (GPU acceleration structure only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sbp", action="store_true", help="skip the C4 batched-search line")
     ap.add_argument("--no-graph", action="store_true",
                     help="skip the secondary measurement of the step replayed as a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -224,9 +225,18 @@ def main():
     w = make_world(args.config, args.seed)
     ctx = Context(local)
     grid = tuple(int(x) for x in args.grid.lower().split("x"))
-    ctx.upload_map(w.map_arrays(), [w.cam], grid=grid)
-    ctx.state_save()
+    arrays = w.map_arrays()
     stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize()
+    u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    u0.record(stream)
+    ctx.upload_map(arrays, [w.cam], grid=grid)   # SURVEY §8 a1 + a2 (once per map)
+    u1.record(stream)
+    u1.synchronize()
+    upload = {"ms": round(u0.elapsed_time(u1), 3), "note": "lc_upload_map incl. H2D of the host "
+              "SoA map (pageable) + SoA pack + per-keyframe grid build; once per map, not per step",
+              "bytes": int(sum(np.asarray(v).nbytes for v in arrays.values()))}
+    ctx.state_save()
 
     mp_list_d = torch.from_numpy(w.mp_list).to(dev)
     S_opt_d = torch.from_numpy(w.S_opt).to(dev)
@@ -381,6 +391,40 @@ def main():
                  "capture_instantiate_ms": round(cap_ms, 3)}
         cap.graph.close()
 
+    # secondary: SURVEY §8 a9, batched read-only guided search on C4 (32 hypotheses x
+    # (current KF + 3 covisible) pairs, PS2a / PS2b / PS1-3 parameter sets)
+    sbp = None
+    if ws == 1 and not args.profile_only and not args.no_sbp:
+        from lcsynth.world import SBP_PARAMS
+        w4 = make_world("C4", args.seed)
+        c4 = Context(local)
+        c4.upload_map(w4.map_arrays(), [w4.cam])
+        args4 = dict(pair_taken=torch.from_numpy(w4.pair_taken).to(dev), host=False)
+        lst4 = torch.from_numpy(w4.pair_mp_list).to(dev)
+        for _ in range(args.warmup):
+            r4 = c4.search_by_projection(w4.pair_kf, w4.pair_S, w4.pair_param, SBP_PARAMS,
+                                         w4.pair_list_begin, lst4, **args4)
+        torch.cuda.synchronize()
+        sms = []
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            r4 = c4.search_by_projection(w4.pair_kf, w4.pair_S, w4.pair_param, SBP_PARAMS,
+                                         w4.pair_list_begin, lst4, **args4)
+            b.record(stream)
+            b.synchronize()
+            sms.append(a.elapsed_time(b))
+        c4cnt = r4["counts"].sum(0).cpu().numpy()
+        cand4 = int(c4cnt[counts.index("candidates")])
+        s_ms = float(np.mean(sms))
+        sbp = {"config": f"C4: {len(w4.pair_kf)} (hypothesis, keyframe) pairs, "
+                         f"{len(w4.pair_mp_list)} queries, 3 parameter sets",
+               "ms_per_call": round(s_ms, 5), "candidates": cand4,
+               "value": round(cand4 / (s_ms / 1000.0), 1), "unit": UNIT,
+               "proposals": int(c4cnt[counts.index("proposals")])}
+        c4.close()
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile_only:
         cpu = cpu_baseline(w, args.cpu_seconds)
@@ -406,6 +450,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "graph": graph,
+            "upload": upload,
+            "sbp": sbp,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
