@@ -22,6 +22,7 @@ COUNTER_NAMES = [
     "cull_angle", "candidates", "no_cand", "over_th", "ratio_rej", "proposals",
     "winners", "orient_rej", "add", "victim_prop", "loop_skip", "bad_slot",
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
+    "refresh_mp", "refresh_obs",
 ]
 NONE64 = np.iinfo(np.int64).max
 
@@ -79,7 +80,8 @@ def lib():
         _lib.orc_hamming.restype = C.c_int
         _lib.orc_predict_level.restype = C.c_int
         _lib.orc_predict_level.argtypes = [C.c_double, C.c_double, C.c_void_p, C.c_int32]
-        for fn in ("orc_correct_window", "orc_correct_all", "orc_fuse", "orc_search_by_projection"):
+        for fn in ("orc_correct_window", "orc_correct_all", "orc_fuse", "orc_search_by_projection",
+                   "orc_refresh"):
             getattr(_lib, fn).restype = C.c_int
     return _lib
 
@@ -173,9 +175,9 @@ class OracleMap:
         self.feat_desc = np.ascontiguousarray(a["feat_desc"], np.uint8).reshape(-1, 32)
         self.feat_mp = np.array(a["feat_mp"], np.int32)
         self.mp_pos = np.array(a["mp_pos"], np.float32).reshape(-1, 3)
-        self.mp_normal = np.ascontiguousarray(a["mp_normal"], np.float32).reshape(-1, 3)
-        self.mp_max_dist = np.ascontiguousarray(a["mp_max_dist"], np.float32)
-        self.mp_desc = np.ascontiguousarray(a["mp_desc"], np.uint8).reshape(-1, 32)
+        self.mp_normal = np.array(a["mp_normal"], np.float32).reshape(-1, 3)      # mutable copies
+        self.mp_max_dist = np.array(a["mp_max_dist"], np.float32)
+        self.mp_desc = np.array(a["mp_desc"], np.uint8).reshape(-1, 32)
         self.mp_angle = np.ascontiguousarray(a["mp_angle"], np.float32)
         self.mp_ref_kf = np.ascontiguousarray(a["mp_ref_kf"], np.int32)
         self.mp_flags = np.array(a["mp_flags"], np.uint8)
@@ -297,3 +299,14 @@ class OracleMap:
                                        _p(dbg.get("uv")), _p(dbg.get("ncand")),
                                        _p(dbg.get("edge")), _p(cnt))
         return dict(feat_mp=out_mp, feat_dist=out_dist, counts=cnt, **dbg)
+
+    # -- O11 -----------------------------------------------------------------
+    def refresh(self, mp_idx=None, what=3):
+        """Map-point refresh (descriptor: what & 1, normal + depth range: what & 2)."""
+        idx = None if mp_idx is None else np.ascontiguousarray(mp_idx, np.int32)
+        n = self.n_mp if idx is None else len(idx)
+        cnt = np.zeros(len(COUNTER_NAMES), np.int64)
+        rc = lib().orc_refresh(C.byref(self._m), C.c_int32(n), _p(idx), C.c_int32(what), _p(cnt))
+        if rc != 0:
+            raise ValueError("orc_refresh: invalid arguments")
+        return dict(zip(COUNTER_NAMES, cnt.tolist()))

@@ -20,6 +20,10 @@
  *   - Propagation of the optimised Sim3 of every keyframe to the whole map
  *     ("propagates the loop correction to the rest of the map")
  *                                                               -> orc_correct_all   (O10)
+ *   - Map-point refresh after a merge: distinctive descriptor + normal and depth
+ *     range ("merge duplicate map points"; the
+ *     refresh itself is inherited ORB-SLAM3 behaviour, readings A33-A37)
+ *                                                               -> orc_refresh       (O11)
  * The paper gives no matching math (SURVEY.md §0 "Key finding"); every
  * constant and tie-break is a DESIGN.md reading (A1-A32), noted inline.
  *
@@ -43,7 +47,8 @@ enum {
   C_QUERIES = 0, C_SKIP_BAD, C_SKIP_FOUND, C_CULL_DEPTH, C_CULL_BOUNDS, C_CULL_DIST,
   C_CULL_ANGLE, C_CANDIDATES, C_NO_CAND, C_OVER_TH, C_RATIO_REJ, C_PROPOSALS,
   C_WINNERS, C_ORIENT_REJ, C_ADD, C_VICTIM_PROP, C_LOOP_SKIP, C_BAD_SLOT,
-  C_VICTIMS, C_REWIRED, C_DUP_CLEARED, C_ADDED, C_CORR_KF, C_CORR_MP, C_N
+  C_VICTIMS, C_REWIRED, C_DUP_CLEARED, C_ADDED, C_CORR_KF, C_CORR_MP,
+  C_REFRESH_MP, C_REFRESH_OBS, C_N
 };
 
 /* query status codes written to out_status (negative = culled/skipped) */
@@ -73,9 +78,9 @@ typedef struct {
   const uint8_t *feat_desc; /* [n_feat][32] */
   int32_t *feat_mp;         /* mutable (fusion) */
   float *mp_pos;            /* [n_mp][3] mutable (corrections) */
-  const float *mp_normal;
-  const float *mp_max_dist;
-  const uint8_t *mp_desc;   /* [n_mp][32] */
+  float *mp_normal;         /* [n_mp][3] mutable (refresh) */
+  float *mp_max_dist;       /* mutable (refresh) */
+  uint8_t *mp_desc;         /* [n_mp][32] mutable (refresh) */
   const float *mp_angle;
   const int32_t *mp_ref_kf;
   uint8_t *mp_flags;        /* bit0 = bad */
@@ -630,6 +635,105 @@ int orc_search_by_projection(const orc_map *m, int32_t n_pairs, const int32_t *p
     free(win);
     off += nf;
   }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O11 map-point refresh (readings A33-A37).              */
+/*  what & 1: distinctive descriptor (EXT ComputeDistinctiveDescriptors)      */
+/*  what & 2: normal + depth range   (EXT UpdateNormalAndDepth)               */
+/* ------------------------------------------------------------------------- */
+static int cmp_int(const void *a, const void *b) {
+  int x = *(const int *)a, y = *(const int *)b;
+  return (x > y) - (x < y);
+}
+
+/* camera centre of keyframe k: Ow = -R^T (t/s) of its pose (reading A2) */
+static void kf_centre(const orc_map *m, int32_t k, double *O) {
+  double T[13];
+  orc_sim3_se3(m->kf_pose + 13 * (size_t)k, T);
+  for (int i = 0; i < 3; ++i) O[i] = -col3(T, i, T + 9);
+}
+
+int orc_refresh(orc_map *m, int32_t n, const int32_t *idx, int32_t what, int64_t *cnt) {
+  if (n < 0) return -1;
+  /* A34: observations of every map point in ascending global feature order
+   * (one counting pass over the associations, then an ordered fill) */
+  int32_t *kf_of = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_feat > 0 ? m->n_feat : 1));
+  int64_t *obeg = (int64_t *)calloc((size_t)m->n_mp + 1, sizeof(int64_t));
+  for (int32_t k = 0; k < m->n_kf; ++k)
+    for (int32_t f = m->kf_feat_begin[k]; f < m->kf_feat_begin[k + 1]; ++f) kf_of[f] = k;
+  for (int32_t f = 0; f < m->n_feat; ++f)
+    if (m->feat_mp[f] >= 0) obeg[m->feat_mp[f] + 1]++;
+  for (int32_t q = 0; q < m->n_mp; ++q) obeg[q + 1] += obeg[q];
+  int32_t *obs = (int32_t *)malloc(sizeof(int32_t) * (size_t)(obeg[m->n_mp] > 0 ? obeg[m->n_mp] : 1));
+  int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(m->n_mp > 0 ? m->n_mp : 1));
+  for (int32_t q = 0; q < m->n_mp; ++q) fill[q] = obeg[q];
+  for (int32_t f = 0; f < m->n_feat; ++f)
+    if (m->feat_mp[f] >= 0) obs[fill[m->feat_mp[f]]++] = f;
+  double scale[64];
+  orc_scale_table(m->n_levels, m->scale_factor, scale);
+  int64_t *c = cnt;
+  const int32_t total = idx ? n : m->n_mp;
+  for (int32_t t = 0; t < total; ++t) {
+    const int32_t q = idx ? idx[t] : t;
+    if (q < 0 || q >= m->n_mp) continue;
+    if (m->mp_flags[q] & 1u) continue;                      /* A33: bad points are skipped */
+    const int32_t *o = obs + obeg[q];
+    const int32_t N = (int32_t)(obeg[q + 1] - obeg[q]);
+    if (N == 0) continue;
+    c[C_REFRESH_MP]++;
+    c[C_REFRESH_OBS] += N;
+    if (what & 1) {
+      /* A35: least median Hamming distance to the other observation descriptors;
+       * median = sorted row [floor((N-1)/2)]; the first such observation wins */
+      int *row = (int *)malloc(sizeof(int) * (size_t)N);
+      int best_med = 1 << 30, best_i = 0;
+      for (int32_t i = 0; i < N; ++i) {
+        for (int32_t j = 0; j < N; ++j)
+          row[j] = orc_hamming(m->feat_desc + 32 * (size_t)o[i], m->feat_desc + 32 * (size_t)o[j]);
+        qsort(row, (size_t)N, sizeof(int), cmp_int);
+        const int med = row[(N - 1) / 2];
+        if (med < best_med) { best_med = med; best_i = i; }
+      }
+      memcpy(m->mp_desc + 32 * (size_t)q, m->feat_desc + 32 * (size_t)o[best_i], 32);
+      free(row);
+    }
+    if (what & 2) {
+      /* A36: normal = (sum of unit vectors from the observing cameras) / N, in
+       * observation order; zero-length vectors are skipped and not counted */
+      const double p[3] = {(double)m->mp_pos[3 * (size_t)q], (double)m->mp_pos[3 * (size_t)q + 1],
+                           (double)m->mp_pos[3 * (size_t)q + 2]};
+      double acc[3] = {0.0, 0.0, 0.0};
+      int32_t nn = 0;
+      for (int32_t i = 0; i < N; ++i) {
+        double O[3], v[3];
+        kf_centre(m, kf_of[o[i]], O);
+        for (int j = 0; j < 3; ++j) v[j] = p[j] - O[j];
+        const double len = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+        if (len == 0.0) continue;
+        for (int j = 0; j < 3; ++j) acc[j] = acc[j] + v[j] / len;
+        ++nn;
+      }
+      if (nn > 0)
+        for (int j = 0; j < 3; ++j) m->mp_normal[3 * (size_t)q + j] = (float)(acc[j] / (double)nn);
+      /* A37: dmax = |p - O_ref| * s_level, level = octave of the reference
+       * keyframe's (first) observation; unchanged if it does not observe q */
+      const int32_t ref = m->mp_ref_kf[q];
+      for (int32_t i = 0; i < N; ++i) {
+        if (kf_of[o[i]] != ref) continue;
+        double O[3], v[3];
+        kf_centre(m, ref, O);
+        for (int j = 0; j < 3; ++j) v[j] = p[j] - O[j];
+        const double dist = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+        int lvl = m->feat_octave[o[i]];
+        if (lvl >= m->n_levels) lvl = m->n_levels - 1;
+        m->mp_max_dist[q] = (float)(dist * scale[lvl]);
+        break;
+      }
+    }
+  }
+  free(kf_of); free(obeg); free(obs); free(fill);
   return 0;
 }
 

@@ -459,3 +459,114 @@ def test_sbp_taken_features_and_points():
     r = om.search_by_projection([0], tm.IDENT[None], [0], prm, [0, 2], [0, 1], pair_taken=[1, -1])
     assert r["feat_mp"].tolist() == [1, 0] and r["feat_dist"].tolist() == [-1, 3]
     assert r["counts"][0][oracle.COUNTER_NAMES.index("skip_found")] == 1
+
+
+# ----------------------------------------------------------------------------
+# O11 map-point refresh (readings A33-A37)
+# ----------------------------------------------------------------------------
+def _pose_at(O):
+    """SE3 world->camera pose with identity rotation and camera centre O."""
+    S = tm.IDENT.copy()
+    S[9:12] = -np.asarray(O, np.float64)
+    return S
+
+
+def _refresh_map(descs, centres, octs, pos, ref_kf=0, flags=0, extra_feats=0):
+    """One map point observed once by each of len(descs) keyframes (centres[i],
+    octave octs[i]), plus optional unassociated clutter features."""
+    base = tm.desc_from_bits([])
+    kfs = []
+    for i, d in enumerate(descs):
+        feats = [dict(u=1.0, v=1.0, desc=base) for _ in range(extra_feats)]
+        feats.append(dict(u=10.0, v=10.0, oct=int(octs[i]), desc=d, mp=0))
+        kfs.append(dict(pose=_pose_at(centres[i]), feats=feats))
+    mps = [dict(pos=tuple(pos), desc=base, normal=(0.0, 0.0, 1.0), dmax=1.0, ref_kf=ref_kf, flags=flags)]
+    return oracle.OracleMap(arrays=tm.build(kfs, mps), cams=[tm.PIN])
+
+
+def test_refresh_descriptor_special_cases():
+    rng = np.random.default_rng(11)
+    d = [rng.integers(0, 256, 32, dtype=np.uint8) for _ in range(3)]
+    # N = 1: the only observation
+    om = _refresh_map(d[:1], [(0, 0, -5)], [0], (0, 0, 0))
+    om.refresh(what=1)
+    assert np.array_equal(om.mp_desc[0], d[0])
+    # N = 2: both medians are 0 (sorted row [0, h], index floor(1/2) = 0) -> the first
+    om = _refresh_map(d[:2], [(0, 0, -5), (1, 0, -5)], [0, 0], (0, 0, 0))
+    om.refresh(what=1)
+    assert np.array_equal(om.mp_desc[0], d[0])
+    # N = 3: A, B = A^1 bit, C = A^100 bits -> medians 1, 1, 99 -> A (first of the tie)
+    A = d[0]
+    B = tm.desc_with_h(A, 1, offset=200)
+    Cd = tm.desc_with_h(A, 100, offset=0)
+    om = _refresh_map([Cd, A, B], [(0, 0, -5), (1, 0, -5), (2, 0, -5)], [0, 0, 0], (0, 0, 0))
+    om.refresh(what=1)
+    assert np.array_equal(om.mp_desc[0], A)
+
+
+def test_refresh_descriptor_planted_medoid():
+    """Disjoint bit flips around a centre: d(i, j) = w_i + w_j (i != j). With the weights
+    sorted a_1 < a_2 < ... and m = floor((N-1)/2), the k-th smallest has median
+    a_k + a_m (k > m) or a_k + a_{m+1} (k <= m): the minimum a_1 + a_{m+1} is unique for
+    N >= 5 and shared by a_1 and a_2 for N in {3, 4} (then the earlier observation)."""
+    rng = np.random.default_rng(12)
+    for trial in range(20):
+        N = int(rng.integers(3, 12))
+        w = rng.permutation(np.arange(1, 60))[:N]
+        centre = rng.integers(0, 256, 32, dtype=np.uint8)
+        descs, off = [], 0
+        for wi in w:
+            descs.append(tm.desc_with_h(centre, int(wi), offset=off))
+            off += int(wi)
+        if off > 256:
+            continue
+        om = _refresh_map(descs, [(i, 0, -5) for i in range(N)], [0] * N, (0, 0, 0))
+        om.refresh(what=1)
+        order = np.argsort(w)
+        exp = int(order[0]) if N >= 5 else int(min(order[0], order[1]))
+        assert np.array_equal(om.mp_desc[0], descs[exp]), (trial, w)
+
+
+def test_refresh_normal_and_depth_closed_forms():
+    d = [tm.desc_from_bits([i]) for i in range(4)]
+    # cameras along +x and +y of the point: unit vectors (-1,0,0), (0,-1,0) -> mean (-0.5,-0.5,0)
+    om = _refresh_map(d[:2], [(4, 0, 0), (0, 3, 0)], [2, 0], (0, 0, 0), ref_kf=0)
+    om.refresh(what=2)
+    assert np.array_equal(om.mp_normal[0], np.float32([-0.5, -0.5, 0.0]))
+    # dmax = |p - O_ref| * 1.2^octave(ref observation) = 4 * 1.44
+    assert om.mp_max_dist[0] == np.float32(4.0 * 1.2 * 1.2)
+    # symmetric cameras: the unit vectors cancel
+    om = _refresh_map(d[:2], [(2, 0, 0), (-7, 0, 0)], [0, 0], (0, 0, 0), ref_kf=1)
+    om.refresh(what=2)
+    assert np.array_equal(om.mp_normal[0], np.float32([0, 0, 0]))
+    assert om.mp_max_dist[0] == np.float32(7.0)
+    # translation invariance: moving point and cameras together changes nothing
+    om2 = _refresh_map(d[:3], [(1, 2, 3), (4, -1, 0), (0, 0, 9)], [1, 3, 0], (0.5, 0.25, 0.125), ref_kf=2)
+    om3 = _refresh_map(d[:3], [(11, 12, 13), (14, 9, 10), (10, 10, 19)], [1, 3, 0], (10.5, 10.25, 10.125),
+                       ref_kf=2)
+    om2.refresh(what=2)
+    om3.refresh(what=2)
+    assert np.allclose(om2.mp_normal, om3.mp_normal, atol=1e-6)
+    assert abs(om2.mp_max_dist[0] - om3.mp_max_dist[0]) < 1e-5
+    # the normal is the mean of unit vectors: its norm is <= 1, == 1 iff all agree
+    assert np.linalg.norm(om2.mp_normal[0]) < 1.0
+    om4 = _refresh_map(d[:3], [(0, 0, -1), (0, 0, -2), (0, 0, -8)], [0, 0, 0], (0, 0, 0))
+    om4.refresh(what=2)
+    assert np.array_equal(om4.mp_normal[0], np.float32([0, 0, 1]))
+
+
+def test_refresh_skips_bad_unobserved_and_foreign_ref():
+    d = [tm.desc_from_bits([i]) for i in range(2)]
+    om = _refresh_map(d, [(4, 0, 0), (0, 3, 0)], [0, 0], (0, 0, 0), flags=1)
+    before = (om.mp_desc.copy(), om.mp_normal.copy(), om.mp_max_dist.copy())
+    c = om.refresh(what=3)
+    assert c["refresh_mp"] == 0
+    assert np.array_equal(om.mp_desc, before[0]) and np.array_equal(om.mp_normal, before[1])
+    # reference keyframe that does not observe the point: depth range unchanged
+    om = _refresh_map(d, [(4, 0, 0), (0, 3, 0)], [0, 0], (0, 0, 0), ref_kf=5)
+    om.refresh(what=2)
+    assert om.mp_max_dist[0] == np.float32(1.0)
+    # an index list selects the points; counters count points and observations
+    om = _refresh_map(d, [(4, 0, 0), (0, 3, 0)], [0, 0], (0, 0, 0), extra_feats=3)
+    c = om.refresh(mp_idx=[0], what=3)
+    assert c["refresh_mp"] == 1 and c["refresh_obs"] == 2
