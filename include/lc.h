@@ -128,6 +128,9 @@ typedef struct {
   uint8_t* mp_flags;             /* [n_mp]                                          */
   int32_t* mp_replaced_by;       /* [n_mp] survivor of a fused victim, -1 = none    */
   int32_t* mp_nobs;              /* [n_mp] number of slots holding the map point    */
+  float* mp_normal;              /* [n_mp][3] viewing direction (lc_refresh_mappoints) */
+  float* mp_max_dist;            /* [n_mp] depth-range bound                        */
+  uint8_t* mp_desc;              /* [n_mp][32] distinctive descriptor               */
 } lc_map_state;
 
 /* Matching parameters (readings A8-A15). th: window half-size at level 0 in px
@@ -183,6 +186,8 @@ enum {
   LC_COUNT_ADDED,          /* fuse apply: new associations kept                      */
   LC_COUNT_CORR_KF,        /* correction: keyframe poses written                     */
   LC_COUNT_CORR_MP,        /* correction: map points moved                           */
+  LC_COUNT_REFRESH_MP,     /* refresh: map points refreshed (not bad, >= 1 observation) */
+  LC_COUNT_REFRESH_OBS,    /* refresh: observations visited                           */
   LC_NCOUNT
 };
 
@@ -222,9 +227,33 @@ int64_t lc_kernel_launches(const lc_ctx* ctx);
  * ------------------------------------------------------------------------- */
 enum { LC_PROF_UPLOAD = 0, LC_PROF_CORRECT_WINDOW, LC_PROF_CORRECT_ALL, LC_PROF_FUSE_PREP,
        LC_PROF_MATCH, LC_PROF_RESOLVE, LC_PROF_APPLY, LC_PROF_SBP_MATCH, LC_PROF_SBP_RESOLVE,
-       LC_PROF_STATE, LC_PROF_PROJECT, LC_NPROF };
+       LC_PROF_STATE, LC_PROF_PROJECT, LC_PROF_REFRESH, LC_NPROF };
 lc_status lc_profile_enable(lc_ctx* ctx, int32_t on);
 lc_status lc_profile_read(lc_ctx* ctx, double* ms, int64_t* launches);
+
+/* ---------------------------------------------------------------------------
+ * lc_refresh_mappoints -- map-point refresh after a merge (
+ * PAPER.md:95 "identify and merge duplicate map points" -- the refresh of the
+ * merged points is inherited ORB-SLAM3 behaviour, readings A33-A37).
+ *
+ * For each selected map point that is not bad and has >= 1 observation (the
+ * (keyframe, feature) slots holding it, in ascending global feature order, A34):
+ *   what & LC_REFRESH_DESC  : descriptor <- the observation descriptor with the
+ *     least median Hamming distance to all observation descriptors (median =
+ *     element floor((N-1)/2) of the sorted row, first observation on ties, A35);
+ *   what & LC_REFRESH_NORMAL: normal <- fl32((sum_i (p - O_i) / |p - O_i|) / N) in
+ *     fp64, observation order, O_i the camera centre of the observing keyframe
+ *     (zero-length terms skipped and not counted, A36); depth bound dmax <-
+ *     fl32(|p - O_ref| * s_level), level = octave of the reference keyframe's first
+ *     observation; unchanged when the reference keyframe does not observe it (A37).
+ *   n, mp_idx [host|dev] nullable: the points to refresh (NULL: all n_mp, n ignored);
+ *     out-of-range indices are skipped.
+ *   out_counts [host|dev] nullable, [LC_NCOUNT] (REFRESH_MP, REFRESH_OBS).
+ * Errors: LC_EINVAL (bad what / n < 0), LC_ESTATE (no map).
+ * ------------------------------------------------------------------------- */
+enum { LC_REFRESH_DESC = 1, LC_REFRESH_NORMAL = 2 };
+lc_status lc_refresh_mappoints(lc_ctx* ctx, int32_t n, const int32_t* mp_idx, int32_t what,
+                               int64_t* out_counts, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * CUDA-graph capture: one loop event (lc_correct_sim3 WINDOW -> lc_fuse ->

@@ -17,15 +17,17 @@ STATUS_NAMES = {0: "LC_OK", -1: "LC_EINVAL", -2: "LC_ESTATE", -3: "LC_ECUDA", -4
 LC_NONE = (1 << 63) - 1
 LC_CORRECT_WINDOW, LC_CORRECT_ALL = 1, 2
 LC_FUSE_PLAN, LC_FUSE_APPLY, LC_FUSE_ALL = 1, 2, 3
+LC_REFRESH_DESC, LC_REFRESH_NORMAL = 1, 2
 COUNTER_NAMES = [
     "queries", "skip_bad", "skip_found", "cull_depth", "cull_bounds", "cull_dist",
     "cull_angle", "candidates", "no_cand", "over_th", "ratio_rej", "proposals",
     "winners", "orient_rej", "add", "victim_prop", "loop_skip", "bad_slot",
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
+    "refresh_mp", "refresh_obs",
 ]
 LC_NCOUNT = len(COUNTER_NAMES)
 PROF_NAMES = ["upload", "correct_window", "correct_all", "fuse_prep", "match", "resolve", "apply",
-              "sbp_match", "sbp_resolve", "state", "project"]
+              "sbp_match", "sbp_resolve", "state", "project", "refresh"]
 
 
 class lc_sim3(C.Structure):
@@ -54,7 +56,8 @@ class lc_map_view(C.Structure):
 
 class lc_map_state(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("kf_pose", "feat_mp", "mp_pos", "mp_flags",
-                                          "mp_replaced_by", "mp_nobs")]
+                                          "mp_replaced_by", "mp_nobs", "mp_normal",
+                                          "mp_max_dist", "mp_desc")]
 
 
 class lc_match_params(C.Structure):
@@ -102,6 +105,7 @@ def load():
                           vp, vp, vp, vp, vp]),
         "lc_search_by_projection": (i32, [vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp,
                                           vp, vp]),
+        "lc_refresh_mappoints": (i32, [vp, i32, vp, i32, vp, vp]),
         "lc_graph_begin": (i32, [vp, vp]),
         "lc_graph_end": (i32, [vp, vp, P(vp)]),
         "lc_graph_launch": (i32, [vp, vp, vp]),
@@ -119,5 +123,5 @@ def exported_symbols():
     return ["lc_create", "lc_destroy", "lc_last_error", "lc_kernel_launches", "lc_profile_enable",
             "lc_profile_read", "lc_upload_map",
             "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse",
-            "lc_search_by_projection", "lc_graph_begin", "lc_graph_end", "lc_graph_launch",
+            "lc_search_by_projection", "lc_refresh_mappoints", "lc_graph_begin", "lc_graph_end", "lc_graph_launch",
             "lc_graph_destroy"]

@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
     const int32_t* __restrict__ fpad, const int32_t* __restrict__ kf_cam,
     const DevCam* __restrict__ cams, const float* __restrict__ fuv, const uint8_t* __restrict__ foct,
     const uint8_t* __restrict__ fdesc, uint16_t* __restrict__ kf_cell, float2* __restrict__ fc_uv,
-    uint32_t* __restrict__ fc_meta, uint4* __restrict__ fc_desc, uint32_t* __restrict__ errs) {
+    uint32_t* __restrict__ fc_meta, uint4* __restrict__ fc_desc, int32_t* __restrict__ feat_cpos,
+    uint32_t* __restrict__ errs) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int k = blockIdx.x;
   const int fb = fbeg[k];
@@ -129,6 +130,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
     int f = s_perm[p];
     fc_uv[fp + p] = make_float2(fuv[2 * (fb + f)], fuv[2 * (fb + f) + 1]);
     fc_meta[fp + p] = (uint32_t)f | ((uint32_t)foct[fb + f] << 16);
+    feat_cpos[fb + f] = fp + p;   // original order -> cell-major position
     const uint8_t* d = fdesc + 32 * (size_t)(fb + f);
     uint32_t w[8];
 #pragma unroll
@@ -145,14 +147,6 @@ __global__ void k_pos_gather(int n_mp, const MpRec* __restrict__ rec, float* __r
     out[3 * q + 0] = rec[q].pos[0];
     out[3 * q + 1] = rec[q].pos[1];
     out[3 * q + 2] = rec[q].pos[2];
-  }
-}
-
-__global__ void k_pos_scatter(int n_mp, const float* __restrict__ in, MpRec* __restrict__ rec) {
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_mp; q += gridDim.x * blockDim.x) {
-    rec[q].pos[0] = in[3 * q + 0];
-    rec[q].pos[1] = in[3 * q + 1];
-    rec[q].pos[2] = in[3 * q + 2];
   }
 }
 
@@ -204,14 +198,14 @@ cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, co
     k_grid_build<<<st.n_kf, LC_NTHREADS, smem, s>>>(st.n_levels, st.n_cams, st.Gs, st.kf_fbeg,
                                                     st.kf_fpad, st.kf_cam,
                                                     st.cams, fuv, foct, fdesc, st.kf_cell,
-                                                    st.fc_uv, st.fc_meta, st.fc_desc, d_errs);
+                                                    st.fc_uv, st.fc_meta, st.fc_desc, st.feat_cpos, d_errs);
     c->launches++;
   }
   return cudaGetLastError();
 }
 
-// Saved-state layout (bytes): kf_pose | kf_S_corr | kf_in_win | feat_mp | pos | flags |
-// replaced_by | nobs | corr_ref
+// Saved-state layout (bytes): kf_pose | kf_S_corr | kf_in_win | feat_mp | mp_rec (64-B
+// records) | flags | replaced_by | nobs | corr_ref
 static size_t state_bytes(const Store& st, size_t off[10]) {
   size_t o = 0;
   auto add = [&](int i, size_t b) { off[i] = o; o += (b + 255) & ~(size_t)255; };
@@ -219,7 +213,7 @@ static size_t state_bytes(const Store& st, size_t off[10]) {
   add(1, sizeof(double) * 13 * st.n_kf);
   add(2, sizeof(int32_t) * st.n_kf);
   add(3, sizeof(int32_t) * st.n_feat);
-  add(4, sizeof(float) * 3 * st.n_mp);
+  add(4, sizeof(MpRec) * st.n_mp);
   add(5, sizeof(uint8_t) * st.n_mp);
   add(6, sizeof(int32_t) * st.n_mp);
   add(7, sizeof(int32_t) * st.n_mp);
@@ -246,6 +240,7 @@ cudaError_t launch_state_copy(lc_ctx* c, bool save, cudaStream_t s) {
       {st.kf_S_corr, off[1], sizeof(double) * 13 * st.n_kf},
       {st.kf_in_win, off[2], sizeof(int32_t) * st.n_kf},
       {st.feat_mp, off[3], sizeof(int32_t) * st.n_feat},
+      {st.mp_rec, off[4], sizeof(MpRec) * st.n_mp},   // positions, normals, depth bounds, descriptors
       {st.mp_flags, off[5], sizeof(uint8_t) * st.n_mp},
       {st.mp_replaced_by, off[6], sizeof(int32_t) * st.n_mp},
       {st.mp_nobs, off[7], sizeof(int32_t) * st.n_mp},
@@ -256,13 +251,6 @@ cudaError_t launch_state_copy(lc_ctx* c, bool save, cudaStream_t s) {
     cudaError_t e = save ? cudaMemcpyAsync(b + it.o, it.dev, it.bytes, cudaMemcpyDeviceToDevice, s)
                          : cudaMemcpyAsync(it.dev, b + it.o, it.bytes, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return e;
-  }
-  if (st.n_mp > 0) {
-    if (save)
-      k_pos_gather<<<grid_for(st.n_mp), LC_NTHREADS, 0, s>>>(st.n_mp, st.mp_rec, (float*)(b + off[4]));
-    else
-      k_pos_scatter<<<grid_for(st.n_mp), LC_NTHREADS, 0, s>>>(st.n_mp, (const float*)(b + off[4]), st.mp_rec);
-    c->launches++;
   }
   return cudaGetLastError();
 }

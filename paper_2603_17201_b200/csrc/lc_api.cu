@@ -314,7 +314,7 @@ void dev_alloc(lc_ctx* c, T** p, size_t n) {
 
 void free_store(Store& st) {
   void* ptrs[] = {st.kf_pose, st.kf_cam, st.kf_fbeg, st.kf_fpad, st.kf_cell, st.fc_uv, st.fc_meta,
-                  st.fc_desc, st.feat_mp, st.feat_angle, st.mp_rec, st.mp_flags, st.mp_ref_kf,
+                  st.fc_desc, st.feat_mp, st.feat_angle, st.feat_cpos, st.mp_rec, st.mp_flags, st.mp_ref_kf,
                   st.mp_replaced_by, st.mp_nobs, st.mp_corr_ref, st.mp_loop_ep, st.mp_owner,
                   st.kf_S_corr, st.kf_in_win, st.kf_win_ep, st.kf_win_pos, st.mp_vbits,
                   st.kf_dirty, st.ep, st.cams};
@@ -602,6 +602,7 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
     CK(cudaMemcpyAsync(st.kf_fpad, fpad.data(), sizeof(int32_t) * (NK + 1), cudaMemcpyHostToDevice, s));
     dev_alloc(c, &st.feat_mp, NF);
     dev_alloc(c, &st.feat_angle, NF);
+    dev_alloc(c, &st.feat_cpos, NF);
     dev_alloc(c, &st.mp_rec, NM);
     dev_alloc(c, &st.mp_flags, NM);
     dev_alloc(c, &st.mp_ref_kf, NM);
@@ -690,6 +691,42 @@ lc_status lc_download_map(lc_ctx* c, const lc_map_state* o, void* stream) {
     if (o->mp_pos && st.n_mp) {
       float* d = call.out(o->mp_pos, 3 * (size_t)st.n_mp);
       CK(launch_download_pos(c, d, call.s));
+    }
+    if ((o->mp_normal || o->mp_max_dist || o->mp_desc) && st.n_mp) {
+      float* dn = call.out(o->mp_normal, 3 * (size_t)st.n_mp);
+      float* dd = call.out(o->mp_max_dist, (size_t)st.n_mp);
+      uint8_t* de = call.out(o->mp_desc, 32 * (size_t)st.n_mp);
+      CK(launch_download_rec(c, dn, dd, de, call.s));
+    }
+    call.finish();
+  });
+}
+
+lc_status lc_refresh_mappoints(lc_ctx* c, int32_t n, const int32_t* mp_idx, int32_t what,
+                               int64_t* out_counts, void* stream) {
+  return guarded(c, [&] {
+    capture_gate(c, stream, true);
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    REQUIRE(what >= 1 && what <= (LC_REFRESH_DESC | LC_REFRESH_NORMAL), LC_EINVAL, "bad what");
+    REQUIRE(mp_idx == nullptr || n >= 0, LC_EINVAL, "n < 0");
+    Store& st = c->st;
+    Call call(c, stream);
+    const int n_sel = mp_idx ? n : st.n_mp;
+    const int32_t* d_idx = mp_idx ? call.in(mp_idx, (size_t)n_sel) : nullptr;
+    const int nb = (st.n_mp + LC_NTHREADS * 8 - 1) / (LC_NTHREADS * 8);
+    int32_t* d_obeg = (int32_t*)call.scratch(sizeof(int32_t) * ((size_t)st.n_mp + 1));
+    int32_t* d_cursor = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(st.n_mp, 1));
+    int32_t* d_bsum = (int32_t*)call.scratch(sizeof(int32_t) * std::max(nb, 1));
+    int32_t* d_obs = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(st.n_feat, 1));
+    unsigned long long* cnt = (unsigned long long*)call.scratch(sizeof(uint64_t) * LC_NCOUNT);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
+    {
+      Prof pr(c, LC_PROF_REFRESH, call.s);
+      CK(launch_refresh(c, n_sel, d_idx, what, d_obeg, d_cursor, d_bsum, d_obs, cnt, call.s));
+    }
+    if (out_counts) {
+      int64_t* d = call.out(out_counts, LC_NCOUNT);
+      CK(cudaMemcpyAsync(d, cnt, sizeof(uint64_t) * LC_NCOUNT, cudaMemcpyDeviceToDevice, call.s));
     }
     call.finish();
   });

@@ -63,6 +63,7 @@ struct Store {
   uint4* fc_desc = nullptr;
   int32_t* feat_mp = nullptr;
   float* feat_angle = nullptr;
+  int32_t* feat_cpos = nullptr;   // [n_feat] cell-major position of each original-order feature
   MpRec* mp_rec = nullptr;
   uint8_t* mp_flags = nullptr;
   int32_t* mp_ref_kf = nullptr;
@@ -341,3 +342,7 @@ cudaError_t launch_fill_u64(lc_ctx* c, unsigned long long* p, int64_t n, unsigne
                             cudaStream_t s);
 cudaError_t launch_state_copy(lc_ctx* c, bool save, cudaStream_t s);
 cudaError_t launch_download_pos(lc_ctx* c, float* out, cudaStream_t s);
+cudaError_t launch_download_rec(lc_ctx* c, float* normal, float* dmax, uint8_t* desc, cudaStream_t s);
+cudaError_t launch_refresh(lc_ctx* c, int n_sel, const int32_t* d_idx, int what, int32_t* d_obeg,
+                           int32_t* d_cursor, int32_t* d_bsum, int32_t* d_obs,
+                           unsigned long long* counts, cudaStream_t s);

@@ -243,9 +243,11 @@ class Context:
                    mp_pos=np.zeros((self.n_mp, 3), np.float32),
                    mp_flags=np.zeros(self.n_mp, np.uint8),
                    mp_replaced_by=np.zeros(self.n_mp, np.int32),
-                   mp_nobs=np.zeros(self.n_mp, np.int32))
-        s = _lib.lc_map_state(*[out[n].ctypes.data for n in ("kf_pose", "feat_mp", "mp_pos",
-                                                              "mp_flags", "mp_replaced_by", "mp_nobs")])
+                   mp_nobs=np.zeros(self.n_mp, np.int32),
+                   mp_normal=np.zeros((self.n_mp, 3), np.float32),
+                   mp_max_dist=np.zeros(self.n_mp, np.float32),
+                   mp_desc=np.zeros((self.n_mp, 32), np.uint8))
+        s = _lib.lc_map_state(*[out[n].ctypes.data for n, _ in _lib.lc_map_state._fields_])
         self._check("lc_download_map", self.lib.lc_download_map(self.h, C.byref(s), self._stream()))
         self.synchronize()
         return out
@@ -255,6 +257,21 @@ class Context:
 
     def state_restore(self):
         self._check("lc_state_restore", self.lib.lc_state_restore(self.h, self._stream()))
+
+    # -- lc_refresh_mappoints -------------------------------------------------------
+    def refresh_mappoints(self, mp_idx=None, what=3, host=True):
+        """Distinctive descriptor (what & 1) and normal + depth range (what & 2) of the
+        given map points (None: all). Returns the counters."""
+        k = self._keep(host)
+        n = 0 if mp_idx is None else (int(mp_idx.shape[0]) if hasattr(mp_idx, "shape") else len(mp_idx))
+        cnt = np.zeros(LC_NCOUNT, np.int64) if host else self._dev(LC_NCOUNT, torch.int64)
+        st = self.lib.lc_refresh_mappoints(self.h, n, k.ptr(mp_idx, np.int32), int(what), k.ptr(cnt),
+                                           self._stream())
+        self._check("lc_refresh_mappoints", st)
+        if host:
+            self.synchronize()
+            return counts_dict(cnt)
+        return cnt
 
     # -- lc_correct_sim3 ----------------------------------------------------------
     def correct_window(self, cur_kf, S_cw_corr, window, host=True):

@@ -1,0 +1,82 @@
+"""GPU map-point refresh (lc_refresh_mappoints) against the oracle
+(O11): after a full loop event, descriptors, normals and depth bounds are compared
+bit for bit (fp64 in the same order on both sides, stored fp32), with the counters."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from lcsynth import make_world  # noqa: E402
+from lcsynth.world import FUSE_PARAMS  # noqa: E402
+from tests import tinymap as tm  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def Ctx():
+    from paper_2603_17201_b200 import Context, build
+    build.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return Context
+
+
+def _compare(ctx, om):
+    st = ctx.download_map()
+    assert np.array_equal(st["mp_desc"], om.mp_desc), "descriptors"
+    assert np.array_equal(st["mp_normal"], om.mp_normal), "normals"
+    assert np.array_equal(st["mp_max_dist"], om.mp_max_dist), "depth bounds"
+
+
+@pytest.mark.parametrize("name", ["T1", "T2", "C2"])
+def test_refresh_after_loop_event_matches_oracle(Ctx, name):
+    w = make_world(name, 0)
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    om = oracle.OracleMap(w)
+    for side in (ctx, om):
+        side.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+        side.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+        side.correct_all(w.S_opt)
+    # the loop's points first (the survivors of the merge), then everything
+    sel = np.unique(w.mp_list).astype(np.int32)
+    cg = ctx.refresh_mappoints(sel, what=3)
+    co = om.refresh(sel, what=3)
+    assert cg["refresh_mp"] == co["refresh_mp"] > 0 and cg["refresh_obs"] == co["refresh_obs"]
+    _compare(ctx, om)
+    cg = ctx.refresh_mappoints(None, what=1)
+    co = om.refresh(None, what=1)
+    assert cg["refresh_mp"] == co["refresh_mp"] and cg["refresh_obs"] == co["refresh_obs"]
+    _compare(ctx, om)
+    cg = ctx.refresh_mappoints(None, what=2)
+    co = om.refresh(None, what=2)
+    _compare(ctx, om)
+
+
+def test_refresh_many_observations_and_skips(Ctx):
+    """80 observations of one point (the global-memory path), a bad point and an
+    unobserved point (both unchanged)."""
+    rng = np.random.default_rng(5)
+    base = rng.integers(0, 256, 32, dtype=np.uint8)
+    kfs = []
+    for k in range(10):
+        S = tm.IDENT.copy()
+        S[9:12] = -np.array([rng.uniform(-3, 3), rng.uniform(-3, 3), -5.0 - k])
+        feats = [dict(u=10.0 + i, v=10.0, oct=int(rng.integers(0, 8)),
+                      desc=tm.desc_with_h(base, int(rng.integers(0, 40)), offset=int(rng.integers(0, 200))),
+                      mp=0 if i < 8 else (1 if i == 8 else -1)) for i in range(10)]
+        kfs.append(dict(pose=S, feats=feats))
+    mps = [dict(pos=(0.1, -0.2, 0.3), desc=base, ref_kf=3), dict(pos=(1.0, 1.0, 1.0), desc=base, flags=1),
+           dict(pos=(2.0, 0.0, 0.0), desc=~base)]
+    arrays = tm.build(kfs, mps)
+    arrays["feat_mp"][arrays["feat_mp"] == 1] = 1   # point 1 is observed but bad
+    ctx = Ctx(0)
+    ctx.upload_map(arrays, [tm.PIN])
+    om = oracle.OracleMap(arrays=arrays, cams=[tm.PIN])
+    cg = ctx.refresh_mappoints(None, what=3)
+    co = om.refresh(None, what=3)
+    assert cg["refresh_mp"] == co["refresh_mp"] == 1 and cg["refresh_obs"] == co["refresh_obs"] == 80
+    _compare(ctx, om)
+    st = ctx.download_map()
+    assert np.array_equal(st["mp_desc"][1], base) and np.array_equal(st["mp_desc"][2], ~base)
