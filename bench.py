@@ -391,6 +391,28 @@ def main():
                  "capture_instantiate_ms": round(cap_ms, 3)}
         cap.graph.close()
 
+    # secondary: SURVEY §8(f) f2, refresh of the loop's map points after the event
+    # (observation transpose + medoid descriptor + normal / depth range)
+    refresh = None
+    if ws == 1 and not args.profile_only and not args.no_sbp:
+        sel = torch.from_numpy(np.unique(w.mp_list).astype(np.int32)).to(dev)
+        rms = []
+        for i in range(args.warmup + args.steps):
+            reset()
+            step()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            rc = ctx.refresh_mappoints(sel, what=3, host=False)
+            b.record(stream)
+            b.synchronize()
+            if i >= args.warmup:
+                rms.append(a.elapsed_time(b))
+        rcnt = rc.cpu().numpy()
+        refresh = {"points": int(rcnt[counts.index("refresh_mp")]),
+                   "observations": int(rcnt[counts.index("refresh_obs")]),
+                   "ms_per_call": round(float(np.mean(rms)), 5),
+                   "note": "after one loop event; the loop's unique map points, what = descriptor | normal"}
+
     # secondary: SURVEY §8 a9, batched read-only guided search on C4 (32 hypotheses x
     # (current KF + 3 covisible) pairs, PS2a / PS2b / PS1-3 parameter sets)
     sbp = None
@@ -452,6 +474,7 @@ def main():
             "graph": graph,
             "upload": upload,
             "sbp": sbp,
+            "refresh": refresh,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
