@@ -205,6 +205,9 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_refresh(const RefreshArgs a) {
   __shared__ int32_t s_tmp[RWARPS][OBS_CAP];
   __shared__ int32_t s_ord[RWARPS][OBS_CAP];
   __shared__ uint4 s_d[RWARPS][OBS_CAP][2];
+  __shared__ double s_u[RWARPS][OBS_CAP][3];
+  __shared__ double s_len[RWARPS][OBS_CAP];
+  __shared__ int32_t s_kf[RWARPS][OBS_CAP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t c_mp = 0, c_obs = 0;
   for (int t = blockIdx.x * RWARPS + warp; t < a.n_sel; t += gridDim.x * RWARPS) {
@@ -235,9 +238,9 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_refresh(const RefreshArgs a) {
         uint32_t best = 0xFFFFFFFFu;   // (median << 16) | rank
         for (int i = lane; i < N; i += 32) {
           const uint4 x0 = s_d[warp][i][0], x1 = s_d[warp][i][1];
-          const int med = row_median(N, [&](int j) {
-            return hamming32(x0, x1, s_d[warp][j][0], s_d[warp][j][1]);
-          });
+          uint16_t row[OBS_CAP];   // the row once; the median search then only compares
+          for (int j = 0; j < N; ++j) row[j] = (uint16_t)hamming32(x0, x1, s_d[warp][j][0], s_d[warp][j][1]);
+          const int med = row_median(N, [&](int j) { return (int)row[j]; });
           best = min(best, ((uint32_t)med << 16) | (uint32_t)i);
         }
 #pragma unroll
@@ -249,7 +252,43 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_refresh(const RefreshArgs a) {
           d[1] = s_d[warp][i][1];
         }
       }
-      if ((a.what & LC_REFRESH_NORMAL) && lane == 0) refresh_geometry(a, q, N, s_ord[warp], nullptr);
+      if (a.what & LC_REFRESH_NORMAL) {
+        // per observation (one lane each): keyframe, unit viewing vector, length; then
+        // lane 0 sums in observation order (A36) -- the oracle's expressions and order
+        MpRec& r = a.rec[q];
+        const double p[3] = {(double)r.pos[0], (double)r.pos[1], (double)r.pos[2]};
+        for (int i = lane; i < N; i += 32) {
+          const int32_t f = s_ord[warp][i];
+          const int k = kf_of_feature(a.kf_fbeg, a.n_kf, f);
+          double O[3], v[3];
+          kf_centre(a.kf_pose, k, O);
+          for (int j = 0; j < 3; ++j) v[j] = p[j] - O[j];
+          const double len = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+          for (int j = 0; j < 3; ++j) s_u[warp][i][j] = len == 0.0 ? 0.0 : v[j] / len;
+          s_len[warp][i] = len;
+          s_kf[warp][i] = k;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          double acc[3] = {0.0, 0.0, 0.0};
+          int nn = 0;
+          for (int i = 0; i < N; ++i) {
+            if (s_len[warp][i] == 0.0) continue;
+            for (int j = 0; j < 3; ++j) acc[j] = acc[j] + s_u[warp][i][j];
+            ++nn;
+          }
+          if (nn > 0)
+            for (int j = 0; j < 3; ++j) r.normal[j] = (float)(acc[j] / (double)nn);
+          const int ref = a.ref_kf[q];
+          for (int i = 0; i < N; ++i) {
+            if (s_kf[warp][i] != ref) continue;
+            int lvl = (int)((a.fc_meta[a.feat_cpos[s_ord[warp][i]]] >> 16) & 0xFFu);
+            if (lvl >= a.n_levels) lvl = a.n_levels - 1;
+            r.dmax = (float)(s_len[warp][i] * a.scale[lvl]);   // A37: |p - O_ref| of that observation
+            break;
+          }
+        }
+      }
     } else {
       // many observations: same arithmetic from global memory
       if (a.what & LC_REFRESH_DESC) {
