@@ -61,9 +61,11 @@ __device__ __forceinline__ void warp_count(uint32_t n, unsigned long long* dst) 
 // OLD poses (S_c^corr = S_cw^corr) into scratch, with T_iw^old and inverse(S_i^corr).
 __global__ void k_win_sim3(int n_w, int cur_pos, const int32_t* __restrict__ window,
                            const double* __restrict__ kf_pose, const double* __restrict__ Scw,
-                           double* __restrict__ scr, double* __restrict__ kf_S_corr,
-                           int32_t* __restrict__ kf_in_win) {
+                           double* __restrict__ scr,
+                           double* __restrict__ kf_S_corr, int32_t* __restrict__ kf_in_win,
+                           double* __restrict__ out_S, unsigned long long* __restrict__ counts) {
   pdl_trigger();   // k_win_mark reads none of this kernel's outputs
+  if (blockIdx.x == 0 && threadIdx.x < LC_NCOUNT) counts[threadIdx.x] = 0;   // the call's counters
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_w) return;
   const int k = window[i];
@@ -86,6 +88,8 @@ __global__ void k_win_sim3(int n_w, int cur_pos, const int32_t* __restrict__ win
   for (int j = 0; j < 13; ++j) o[42 + j] = T[j];
   o[13] = o[27] = o[41] = o[55] = 0.0;
   for (int j = 0; j < 13; ++j) kf_S_corr[13 * (size_t)k + j] = S[j];
+  if (out_S)
+    for (int j = 0; j < 13; ++j) out_S[13 * (size_t)i + j] = S[j];
   kf_in_win[k] = 1;
 }
 
@@ -189,8 +193,9 @@ __global__ void k_all_kf(int n_kf, const double* __restrict__ Sopt, double* __re
                          const double* __restrict__ kf_S_corr, int32_t* __restrict__ kf_in_win,
                          double* __restrict__ scr, unsigned long long* __restrict__ counts) {
   pdl_trigger();   // k_all_points' prologue reads none of this kernel's outputs
+  if (blockIdx.x == 0 && threadIdx.x < LC_NCOUNT)   // the call's counters (k_all_points adds later)
+    counts[threadIdx.x] = threadIdx.x == LC_COUNT_CORR_KF ? (unsigned long long)n_kf : 0ull;
   int k = blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t n = 0;
   if (k < n_kf) {
     double pre[13], opt[13], inv[13], T[13];
     const double* src = kf_in_win[k] ? kf_S_corr + 13 * (size_t)k : kf_pose + 13 * (size_t)k;
@@ -203,9 +208,7 @@ __global__ void k_all_kf(int n_kf, const double* __restrict__ Sopt, double* __re
     o[13] = o[27] = 0.0;
     for (int j = 0; j < 13; ++j) kf_pose[13 * (size_t)k + j] = T[j];
     kf_in_win[k] = 0;
-    n = 1;
   }
-  warp_count(n, &counts[LC_COUNT_CORR_KF]);
 }
 
 // Two adjacent points per thread (they share their reference keyframe in creation
@@ -263,15 +266,15 @@ int correct_window_scratch_stride() { return WSTR; }
 int correct_all_scratch_stride() { return ASTR; }
 
 cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t* d_window,
-                                  const double* d_Scw, double* d_scr, unsigned long long* counts,
-                                  cudaStream_t s) {
+                                  const double* d_Scw, double* d_scr, double* d_outS,
+                                  unsigned long long* counts, cudaStream_t s) {
   Store& st = c->st;
   cudaError_t e;
   if (st.n_mp > 0 && (e = cudaMemsetAsync(st.mp_owner, 0x7F, sizeof(int32_t) * st.n_mp, s)) != cudaSuccess)
     return e;
   if ((e = cudaMemsetAsync(st.kf_in_win, 0, sizeof(int32_t) * st.n_kf, s)) != cudaSuccess) return e;
   k_win_sim3<<<(n_w + 63) / 64, 64, 0, s>>>(n_w, cur_pos, d_window, st.kf_pose, d_Scw, d_scr,
-                                            st.kf_S_corr, st.kf_in_win);
+                                            st.kf_S_corr, st.kf_in_win, d_outS, counts);
   if ((e = launch_pdl(k_win_mark, dim3(std::min((n_w + 7) / 8, 148 * 8)), dim3(LC_NTHREADS), 0, s, n_w,
                       d_window, st.kf_fbeg, st.feat_mp, st.mp_owner)) != cudaSuccess)
     return e;
@@ -288,7 +291,7 @@ cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t
 cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
                                unsigned long long* counts, cudaStream_t s) {
   Store& st = c->st;
-  k_all_kf<<<(st.n_kf + 127) / 128, 128, 0, s>>>(st.n_kf, d_Sopt, st.kf_pose, st.kf_S_corr,
+  k_all_kf<<<std::max(1, (st.n_kf + 127) / 128), 128, 0, s>>>(st.n_kf, d_Sopt, st.kf_pose, st.kf_S_corr,
                                                 st.kf_in_win, d_scr, counts);
   c->launches++;
   if (st.n_mp > 0) {

@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
   cnt[0] = cQ; cnt[1] = cA & 1023u; cnt[2] = (cA >> 10) & 1023u; cnt[3] = (cA >> 20) & 1023u;
   cnt[4] = cB & 1023u; cnt[5] = (cB >> 10) & 1023u; cnt[6] = (cB >> 20) & 1023u;
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
+  pdl_wait();   // (PDL) k_fuse_prep zeroes the counters: add after it completed
   block_add<7>(cnt, kProjSlot, cdst);
-  pdl_wait();   // (PDL) reads nothing k_fuse_prep writes; completes after it
 }
 
 // ---- k_match ------------------------------------------------------------------
@@ -771,8 +771,10 @@ __global__ void k_fuse_prep(int phase, int init_winner, uint32_t* __restrict__ e
                             unsigned long long* __restrict__ winner,
                             unsigned long long* __restrict__ victim, uint32_t* __restrict__ loop_ep,
                             uint32_t* __restrict__ kf_win_ep, int32_t* __restrict__ kf_win_pos,
-                            uint32_t* __restrict__ vbits, int n_vbits, int32_t* __restrict__ dirty_n) {
+                            uint32_t* __restrict__ vbits, int n_vbits, int32_t* __restrict__ dirty_n,
+                            unsigned long long* __restrict__ counts) {
   pdl_trigger();   // k_project reads none of this kernel's outputs
+  if (blockIdx.x == 0 && threadIdx.x < LC_NCOUNT) counts[threadIdx.x] = 0;   // the call's counters
   uint32_t epoch = ep[0] + 1u;
   if (epoch == 0u) epoch = 1u;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1063,7 +1065,8 @@ cudaError_t launch_resolve(lc_ctx* c, int mode, const MatchArgs& a, int n_units,
 
 cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, const int32_t* d_window,
                              int64_t n_wfeat, const int32_t* mp_list, int64_t n_list_total,
-                             unsigned long long* winner, unsigned long long* victim, cudaStream_t s) {
+                             unsigned long long* winner, unsigned long long* victim,
+                             unsigned long long* counts, cudaStream_t s) {
   Store& st = c->st;
   const int n_vbits = (st.n_mp + 31) / 32;
   int64_t n = std::max<int64_t>(n_w, n_vbits);
@@ -1075,7 +1078,7 @@ cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, con
   k_fuse_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(phase, init_winner, st.ep, n_w, d_window, n_wfeat,
                                                  mp_list, n_list_total, st.n_mp, winner, victim,
                                                  st.mp_loop_ep, st.kf_win_ep, st.kf_win_pos,
-                                                 st.mp_vbits, n_vbits, st.kf_dirty);
+                                                 st.mp_vbits, n_vbits, st.kf_dirty, counts);
   c->launches++;
   return cudaGetLastError();
 }

@@ -190,6 +190,18 @@ struct Call {
     return d;
   }
 
+  // counters: accumulated in the caller's buffer when it is device memory (no copy),
+  // else in scratch with a copy-out at finish; zeroed by the call's first kernel
+  unsigned long long* counts(int64_t* user, size_t n) {
+    if (user && is_device_ptr(c, user)) return (unsigned long long*)user;
+    unsigned long long* d = (unsigned long long*)scratch(sizeof(uint64_t) * n);
+    if (user) {
+      if (c->cap) require_pinned(user);
+      outs.push_back({user, d, sizeof(uint64_t) * n});
+    }
+    return d;
+  }
+
   void finish() {
     for (auto& o : outs) CK(cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDefault, s));
     CK(cudaGetLastError());
@@ -763,7 +775,7 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
     REQUIRE(mode == LC_CORRECT_WINDOW || mode == LC_CORRECT_ALL, LC_EINVAL, "bad mode");
     Store& st = c->st;
     Call call(c, stream);
-    unsigned long long* cnt = (unsigned long long*)call.scratch(sizeof(uint64_t) * LC_NCOUNT);
+    unsigned long long* cnt = call.counts(out_counts, LC_NCOUNT);   // zeroed by the first kernel
     if (mode == LC_CORRECT_WINDOW) {
       REQUIRE(S_cw_corr, LC_EINVAL, "null S_cw_corr");
       REQUIRE(cur_kf >= 0 && cur_kf < st.n_kf, LC_ERANGE, "cur_kf out of range");
@@ -775,16 +787,13 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
       call.arg((const double*)S_cw_corr, 13, &d_S);
       call.commit();
       double* scr = (double*)call.scratch(sizeof(double) * correct_window_scratch_stride() * (size_t)n_window);
-      CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
+      double* d_outS = (out_S_corr && is_device_ptr(c, out_S_corr)) ? (double*)out_S_corr : nullptr;
       {
         Prof pr(c, LC_PROF_CORRECT_WINDOW, call.s);
-        CK(launch_correct_window(c, 0, n_window, d_win, d_S, scr, cnt, call.s));
+        CK(launch_correct_window(c, 0, n_window, d_win, d_S, scr, d_outS, cnt, call.s));
       }
-      if (out_S_corr) {
-        if (is_device_ptr(c, out_S_corr)) {
-          CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr + 28, sizeof(double) * correct_window_scratch_stride(),
-                               sizeof(lc_sim3), n_window, cudaMemcpyDeviceToDevice, call.s));
-        } else {
+      if (out_S_corr && !d_outS) {
+        {
           CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr + 28, sizeof(double) * correct_window_scratch_stride(),
                                sizeof(lc_sim3), n_window, cudaMemcpyDefault, call.s));
         }
@@ -795,16 +804,11 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
       REQUIRE(S_opt, LC_EINVAL, "null S_opt");
       const double* d_opt = call.in((const double*)S_opt, 13 * (size_t)st.n_kf);
       double* scr = (double*)call.scratch(sizeof(double) * correct_all_scratch_stride() * (size_t)std::max(st.n_kf, 1));
-      CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
       {
         Prof pr(c, LC_PROF_CORRECT_ALL, call.s);
         CK(launch_correct_all(c, d_opt, scr, cnt, call.s));
       }
       std::fill(st.h_in_win.begin(), st.h_in_win.end(), 0);
-    }
-    if (out_counts) {
-      int64_t* d = call.out(out_counts, LC_NCOUNT);
-      CK(cudaMemcpyAsync(d, cnt, sizeof(uint64_t) * LC_NCOUNT, cudaMemcpyDeviceToDevice, call.s));
     }
     call.finish();
   });
@@ -945,8 +949,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     if (!vic) vic = (unsigned long long*)call.scratch(sizeof(uint64_t) * std::max(st.n_mp, 1));
     int8_t* act = call.out(out_action, (size_t)n_wfeat);
     if (act && (phase & LC_FUSE_PLAN)) CK(cudaMemsetAsync(act, 0, (size_t)n_wfeat, call.s));
-    unsigned long long* cnt = (unsigned long long*)call.scratch(sizeof(uint64_t) * LC_NCOUNT);
-    CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
+    unsigned long long* cnt = call.counts(out_counts, LC_NCOUNT);   // zeroed by k_fuse_prep
     const int64_t n_q_all = win_list_begin ? n_list : (int64_t)n_window * n_list;
     int64_t* dbg_best = nullptr;
     double* dbg_uv = nullptr;
@@ -962,7 +965,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     {
       Prof pr(c, LC_PROF_FUSE_PREP, call.s);
       CK(launch_fuse_prep(c, phase, sole ? 0 : 1, n_window, d_win, n_wfeat, d_list, pipe ? 0 : n_list,
-                          win, vic, call.s));
+                          win, vic, cnt, call.s));
     }
     if (phase & LC_FUSE_PLAN) {
       a.unit_kf = d_win;
@@ -1027,10 +1030,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       Prof pr(c, LC_PROF_APPLY, call.s);
       CK(launch_fuse_apply(c, d_woff, win, vic, cnt, call.s));
     }
-    if (out_counts) {
-      int64_t* d = call.out(out_counts, LC_NCOUNT);
-      CK(cudaMemcpyAsync(d, cnt, sizeof(uint64_t) * LC_NCOUNT, cudaMemcpyDeviceToDevice, call.s));
-    }
+
     call.finish();
   });
 }

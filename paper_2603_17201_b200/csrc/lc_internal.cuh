@@ -323,21 +323,22 @@ cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, co
                                const uint8_t* foct, const uint8_t* fdesc, uint32_t* d_errs,
                                cudaStream_t s);
 cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max, int part,
-                         cudaStream_t s, bool pdl = true);  // part 0: k_project, 1: k_match; blocks [a.blk_base, +n_blocks)  // part 0: k_project, 1: k_match
+                         cudaStream_t s, bool pdl = true);  // part 0: k_project, 1: k_match; blocks [a.blk_base, +n_blocks)
 cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, const int32_t* d_window,
                              int64_t n_wfeat, const int32_t* mp_list, int64_t n_list_total,
-                             unsigned long long* winner, unsigned long long* victim, cudaStream_t s);
+                             unsigned long long* winner, unsigned long long* victim,
+                             unsigned long long* counts, cudaStream_t s);   // zeroes counts
 cudaError_t launch_resolve(lc_ctx* c, int mode, const MatchArgs& a, int n_units, cudaStream_t s);
 cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned long long* winner,
                               const unsigned long long* victim, unsigned long long* counts,
                               cudaStream_t s);
 cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t* d_window,
-                                  const double* d_Scw, double* d_scr, unsigned long long* counts,
-                                  cudaStream_t s);
+                                  const double* d_Scw, double* d_scr, double* d_outS,
+                                  unsigned long long* counts, cudaStream_t s);   // zeroes counts
 int correct_window_scratch_stride();
 int correct_all_scratch_stride();
 cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
-                               unsigned long long* counts, cudaStream_t s);
+                               unsigned long long* counts, cudaStream_t s);   // zeroes counts
 cudaError_t launch_fill_u64(lc_ctx* c, unsigned long long* p, int64_t n, unsigned long long v,
                             cudaStream_t s);
 cudaError_t launch_state_copy(lc_ctx* c, bool save, cudaStream_t s);
