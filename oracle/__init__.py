@@ -22,7 +22,7 @@ COUNTER_NAMES = [
     "cull_angle", "candidates", "no_cand", "over_th", "ratio_rej", "proposals",
     "winners", "orient_rej", "add", "victim_prop", "loop_skip", "bad_slot",
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
-    "refresh_mp", "refresh_obs",
+    "refresh_mp", "refresh_obs", "conn_kf", "conn_edges",
 ]
 NONE64 = np.iinfo(np.int64).max
 
@@ -81,7 +81,7 @@ def lib():
         _lib.orc_predict_level.restype = C.c_int
         _lib.orc_predict_level.argtypes = [C.c_double, C.c_double, C.c_void_p, C.c_int32]
         for fn in ("orc_correct_window", "orc_correct_all", "orc_fuse", "orc_search_by_projection",
-                   "orc_refresh"):
+                   "orc_refresh", "orc_update_connections"):
             getattr(_lib, fn).restype = C.c_int
     return _lib
 
@@ -310,3 +310,19 @@ class OracleMap:
         if rc != 0:
             raise ValueError("orc_refresh: invalid arguments")
         return dict(zip(COUNTER_NAMES, cnt.tolist()))
+
+    # -- O12 -----------------------------------------------------------------
+    def update_connections(self, kf_idx=None, th=15, max_edges=64):
+        """Covisibility edges of the given keyframes (None: all): (n_edges, kf, weight)
+        with kf / weight [n, max_edges] (rows valid up to min(n_edges, max_edges))."""
+        idx = None if kf_idx is None else np.ascontiguousarray(kf_idx, np.int32)
+        n = self.n_kf if idx is None else len(idx)
+        out_n = np.zeros(n, np.int32)
+        out_kf = np.full((n, max_edges), -1, np.int32)
+        out_w = np.zeros((n, max_edges), np.int32)
+        cnt = np.zeros(len(COUNTER_NAMES), np.int64)
+        rc = lib().orc_update_connections(C.byref(self._m), C.c_int32(n), _p(idx), C.c_int32(th),
+                                          C.c_int32(max_edges), _p(out_n), _p(out_kf), _p(out_w), _p(cnt))
+        if rc != 0:
+            raise ValueError("orc_update_connections: invalid arguments")
+        return out_n, out_kf, out_w, dict(zip(COUNTER_NAMES, cnt.tolist()))

@@ -24,6 +24,9 @@
  *     range ("merge duplicate map points"; the
  *     refresh itself is inherited ORB-SLAM3 behaviour, readings A33-A37)
  *                                                               -> orc_refresh       (O11)
+ *   - Covisibility recount after the merge ("creates new connections in the
+ *     covisibility and essential graphs"; SURVEY.md
+ *     §8(f) f4, readings A38-A40)                               -> orc_update_connections (O12)
  * The paper gives no matching math (SURVEY.md §0 "Key finding"); every
  * constant and tie-break is a DESIGN.md reading (A1-A32), noted inline.
  *
@@ -48,7 +51,7 @@ enum {
   C_CULL_ANGLE, C_CANDIDATES, C_NO_CAND, C_OVER_TH, C_RATIO_REJ, C_PROPOSALS,
   C_WINNERS, C_ORIENT_REJ, C_ADD, C_VICTIM_PROP, C_LOOP_SKIP, C_BAD_SLOT,
   C_VICTIMS, C_REWIRED, C_DUP_CLEARED, C_ADDED, C_CORR_KF, C_CORR_MP,
-  C_REFRESH_MP, C_REFRESH_OBS, C_N
+  C_REFRESH_MP, C_REFRESH_OBS, C_CONN_KF, C_CONN_EDGES, C_N
 };
 
 /* query status codes written to out_status (negative = culled/skipped) */
@@ -734,6 +737,89 @@ int orc_refresh(orc_map *m, int32_t n, const int32_t *idx, int32_t what, int64_t
     }
   }
   free(kf_of); free(obeg); free(obs); free(fill);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O12 covisibility recount (readings A38-A40).           */
+/* For each selected keyframe k: weight(k, k2) = number of distinct non-bad   */
+/* map points held by k that k2 (!= k) also holds; edges with weight >= th,   */
+/* or the single strongest one if none reaches th; ordered by weight desc,   */
+/* then keyframe id asc. out_n[i] = number of edges (may exceed max_edges;    */
+/* only the first max_edges are written to out_kf / out_w [i*max_edges...]).  */
+/* ------------------------------------------------------------------------- */
+int orc_update_connections(orc_map *m, int32_t n, const int32_t *idx, int32_t th, int32_t max_edges,
+                           int32_t *out_n, int32_t *out_kf, int32_t *out_w, int64_t *cnt) {
+  if (n < 0 || max_edges < 0) return -1;
+  int32_t *kf_of = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_feat > 0 ? m->n_feat : 1));
+  for (int32_t k = 0; k < m->n_kf; ++k)
+    for (int32_t f = m->kf_feat_begin[k]; f < m->kf_feat_begin[k + 1]; ++f) kf_of[f] = k;
+  /* holds[q] lists, per map point, the keyframes holding it (ascending, distinct) */
+  int64_t *hbeg = (int64_t *)calloc((size_t)m->n_mp + 1, sizeof(int64_t));
+  for (int32_t f = 0; f < m->n_feat; ++f)
+    if (m->feat_mp[f] >= 0) hbeg[m->feat_mp[f] + 1]++;
+  for (int32_t q = 0; q < m->n_mp; ++q) hbeg[q + 1] += hbeg[q];
+  int32_t *holds = (int32_t *)malloc(sizeof(int32_t) * (size_t)(hbeg[m->n_mp] > 0 ? hbeg[m->n_mp] : 1));
+  int64_t *hn = (int64_t *)calloc((size_t)(m->n_mp > 0 ? m->n_mp : 1), sizeof(int64_t));
+  for (int32_t f = 0; f < m->n_feat; ++f) {   /* features ascending -> keyframes ascending */
+    const int32_t q = m->feat_mp[f];
+    if (q < 0) continue;
+    const int32_t k = kf_of[f];
+    if (hn[q] > 0 && holds[hbeg[q] + hn[q] - 1] == k) continue;   /* k holds q twice: once */
+    holds[hbeg[q] + hn[q]++] = k;
+  }
+  int32_t *w = (int32_t *)calloc((size_t)(m->n_kf > 0 ? m->n_kf : 1), sizeof(int32_t));
+  uint8_t *seen = (uint8_t *)calloc((size_t)(m->n_mp > 0 ? m->n_mp : 1), 1);
+  const int32_t total = idx ? n : m->n_kf;
+  for (int32_t t = 0; t < total; ++t) {
+    const int32_t k = idx ? idx[t] : t;
+    if (out_n) out_n[t] = 0;
+    if (k < 0 || k >= m->n_kf) continue;
+    memset(w, 0, sizeof(int32_t) * (size_t)m->n_kf);
+    for (int32_t f = m->kf_feat_begin[k]; f < m->kf_feat_begin[k + 1]; ++f) {
+      const int32_t q = m->feat_mp[f];
+      if (q < 0 || (m->mp_flags[q] & 1u) || seen[q]) continue;   /* A38: distinct, not bad */
+      seen[q] = 1;
+      for (int64_t h = hbeg[q]; h < hbeg[q] + hn[q]; ++h)
+        if (holds[h] != k) w[holds[h]]++;
+    }
+    for (int32_t f = m->kf_feat_begin[k]; f < m->kf_feat_begin[k + 1]; ++f)
+      if (m->feat_mp[f] >= 0) seen[m->feat_mp[f]] = 0;
+    /* A39 + A40: edges >= th by (weight desc, id asc); else the strongest one */
+    int32_t ne = 0;
+    for (int32_t k2 = 0; k2 < m->n_kf; ++k2) ne += w[k2] >= th && w[k2] > 0;
+    int32_t wr = 0;
+    if (ne == 0) {
+      int32_t best = -1;
+      for (int32_t k2 = 0; k2 < m->n_kf; ++k2)
+        if (w[k2] > 0 && (best < 0 || w[k2] > w[best])) best = k2;
+      if (best >= 0) {
+        ne = 1;
+        if (max_edges > 0 && out_kf) { out_kf[(size_t)t * max_edges] = best; out_w[(size_t)t * max_edges] = w[best]; }
+      }
+    } else {
+      int32_t last_w = 1 << 30, last_k = -1;   /* selection in (weight desc, id asc) order */
+      for (int32_t e = 0; e < ne; ++e) {
+        int32_t bk = -1;
+        for (int32_t k2 = 0; k2 < m->n_kf; ++k2) {
+          if (!(w[k2] >= th && w[k2] > 0)) continue;
+          const int after = w[k2] < last_w || (w[k2] == last_w && k2 > last_k);
+          if (!after) continue;
+          if (bk < 0 || w[k2] > w[bk] || (w[k2] == w[bk] && k2 < bk)) bk = k2;
+        }
+        last_w = w[bk]; last_k = bk;
+        if (wr < max_edges && out_kf) {
+          out_kf[(size_t)t * max_edges + wr] = bk;
+          out_w[(size_t)t * max_edges + wr] = w[bk];
+          ++wr;
+        }
+      }
+    }
+    if (out_n) out_n[t] = ne;
+    cnt[C_CONN_KF]++;
+    cnt[C_CONN_EDGES] += ne;
+  }
+  free(kf_of); free(hbeg); free(holds); free(hn); free(w); free(seen);
   return 0;
 }
 

@@ -570,3 +570,67 @@ def test_refresh_skips_bad_unobserved_and_foreign_ref():
     om = _refresh_map(d, [(4, 0, 0), (0, 3, 0)], [0, 0], (0, 0, 0), extra_feats=3)
     c = om.refresh(mp_idx=[0], what=3)
     assert c["refresh_mp"] == 1 and c["refresh_obs"] == 2
+
+
+# ----------------------------------------------------------------------------
+# O12 covisibility recount (SPEC.md update_connections examples;
+# DESIGN.md readings A38-A40)
+# ----------------------------------------------------------------------------
+def _conn_map(holdings, bad=()):
+    """holdings[k] = list of map-point ids held by keyframe k (one slot each)."""
+    n_mp = max([q for h in holdings for q in h] + [0]) + 1
+    base = tm.desc_from_bits([])
+    kfs = [dict(feats=[dict(u=1.0 + i, v=1.0, desc=base, mp=int(q)) for i, q in enumerate(h)] or
+                [dict(u=1.0, v=1.0, desc=base)]) for h in holdings]
+    mps = [dict(pos=(0.0, 0.0, 1.0), desc=base, flags=1 if q in bad else 0) for q in range(n_mp)]
+    return oracle.OracleMap(arrays=tm.build(kfs, mps), cams=[tm.PIN])
+
+
+def test_connections_spec_examples():
+    # "keyframe sharing 20 points with kf A and 5 with kf B -> weights {A:20, B:5}"
+    om = _conn_map([list(range(30)), list(range(20)) + [40, 41], list(range(25, 30))])
+    n, kf, w, c = om.update_connections([0], th=5)
+    assert n[0] == 2 and list(kf[0, :2]) == [1, 2] and list(w[0, :2]) == [20, 5]
+    n, kf, w, c = om.update_connections([0], th=15)    # B below the threshold: dropped
+    assert n[0] == 1 and kf[0, 0] == 1 and w[0, 0] == 20
+    # "keyframe whose every weight < 15 -> retains exactly one edge (max, tie -> lowest id)"
+    om = _conn_map([list(range(10)), list(range(7)), list(range(3, 10)), [0]])
+    n, kf, w, c = om.update_connections([0], th=15)
+    assert n[0] == 1 and kf[0, 0] == 1 and w[0, 0] == 7
+    # no shared points at all: no edge
+    om = _conn_map([[0, 1], [2, 3]])
+    n, kf, w, c = om.update_connections(None, th=15)
+    assert list(n) == [0, 0] and c["conn_kf"] == 2 and c["conn_edges"] == 0
+
+
+def test_connections_order_bad_points_and_duplicates():
+    # equal weights: ascending keyframe id; larger weight first
+    om = _conn_map([list(range(40)), list(range(16)), list(range(20, 40)), list(range(16)), [0, 1]])
+    n, kf, w, c = om.update_connections([0], th=15)
+    assert n[0] == 3 and list(kf[0, :3]) == [2, 1, 3] and list(w[0, :3]) == [20, 16, 16]
+    # bad points do not count; a keyframe holding a point twice counts it once
+    om = _conn_map([list(range(20)), list(range(20)) + [3], list(range(20))], bad=(0, 1))
+    n, kf, w, c = om.update_connections(None, th=15)
+    assert list(w[0, :2]) == [18, 18] and list(kf[0, :2]) == [1, 2]
+    assert w[1, 0] == 18 and w[2, 0] == 18
+
+
+def test_connections_symmetric_and_truncated():
+    rng = np.random.default_rng(3)
+    holdings = [sorted(rng.choice(300, size=int(rng.integers(20, 120)), replace=False).tolist())
+                for _ in range(12)]
+    om = _conn_map(holdings)
+    n, kf, w, c = om.update_connections(None, th=1, max_edges=16)
+    W = np.zeros((12, 12), np.int64)
+    for a in range(12):
+        for e in range(min(n[a], 16)):
+            W[a, kf[a, e]] = w[a, e]
+    # with th = 1 every shared keyframe is an edge; the weight matrix is symmetric and
+    # equals the size of the intersection of the held sets
+    for a in range(12):
+        for b in range(12):
+            if a != b:
+                assert W[a, b] == len(set(holdings[a]) & set(holdings[b])) or n[a] > 16
+    assert np.array_equal(W, W.T)
+    n2, kf2, w2, _ = om.update_connections(None, th=1, max_edges=3)   # truncated rows
+    assert np.array_equal(n2, n) and np.array_equal(kf2[:, :3], kf[:, :3])
