@@ -188,6 +188,8 @@ enum {
   LC_COUNT_CORR_MP,        /* correction: map points moved                           */
   LC_COUNT_REFRESH_MP,     /* refresh: map points refreshed (not bad, >= 1 observation) */
   LC_COUNT_REFRESH_OBS,    /* refresh: observations visited                           */
+  LC_COUNT_CONN_KF,        /* connections: keyframes recounted                        */
+  LC_COUNT_CONN_EDGES,     /* connections: edges kept (before max_edges truncation)   */
   LC_NCOUNT
 };
 
@@ -227,7 +229,7 @@ int64_t lc_kernel_launches(const lc_ctx* ctx);
  * ------------------------------------------------------------------------- */
 enum { LC_PROF_UPLOAD = 0, LC_PROF_CORRECT_WINDOW, LC_PROF_CORRECT_ALL, LC_PROF_FUSE_PREP,
        LC_PROF_MATCH, LC_PROF_RESOLVE, LC_PROF_APPLY, LC_PROF_SBP_MATCH, LC_PROF_SBP_RESOLVE,
-       LC_PROF_STATE, LC_PROF_PROJECT, LC_PROF_REFRESH, LC_NPROF };
+       LC_PROF_STATE, LC_PROF_PROJECT, LC_PROF_REFRESH, LC_PROF_CONN, LC_NPROF };
 lc_status lc_profile_enable(lc_ctx* ctx, int32_t on);
 lc_status lc_profile_read(lc_ctx* ctx, double* ms, int64_t* launches);
 
@@ -254,6 +256,26 @@ lc_status lc_profile_read(lc_ctx* ctx, double* ms, int64_t* launches);
 enum { LC_REFRESH_DESC = 1, LC_REFRESH_NORMAL = 2 };
 lc_status lc_refresh_mappoints(lc_ctx* ctx, int32_t n, const int32_t* mp_idx, int32_t what,
                                int64_t* out_counts, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * lc_update_connections -- covisibility recount after the merge (SURVEY.md §8(f)
+ * f4; "creates new connections in the covisibility and essential
+ * graphs"; readings A38-A40). The paper keeps this step on
+ * the CPU; here it runs on the device observation lists.
+ *
+ * For each selected keyframe k (kf_idx [host|dev] nullable: all n_kf, n ignored):
+ *   weight(k, k2) = number of distinct non-bad map points held by both k and k2 != k;
+ *   edges: every k2 with weight >= th, or, if there is none, the single strongest
+ *   (max weight, lowest id); ordered by weight descending, then keyframe id.
+ *   out_n [host|dev] [n]: number of edges of row i (may exceed max_edges);
+ *   out_kf, out_w [host|dev] nullable, [n][max_edges]: the first min(out_n[i],
+ *   max_edges) edges of row i (the rest of the row is left unchanged).
+ *   out_counts [host|dev] nullable, [LC_NCOUNT] (CONN_KF, CONN_EDGES).
+ * Errors: LC_EINVAL (n < 0, max_edges < 0, th < 1, n_kf > 40000), LC_ESTATE (no map).
+ * ------------------------------------------------------------------------- */
+lc_status lc_update_connections(lc_ctx* ctx, int32_t n, const int32_t* kf_idx, int32_t th,
+                                int32_t max_edges, int32_t* out_n, int32_t* out_kf,
+                                int32_t* out_w, int64_t* out_counts, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * CUDA-graph capture: one loop event (lc_correct_sim3 WINDOW -> lc_fuse ->

@@ -355,9 +355,8 @@ int grid_of(int64_t n, int per_block) {
 
 }  // namespace
 
-cudaError_t launch_refresh(lc_ctx* c, int n_sel, const int32_t* d_idx, int what, int32_t* d_obeg,
-                           int32_t* d_cursor, int32_t* d_bsum, int32_t* d_obs,
-                           unsigned long long* counts, cudaStream_t s) {
+cudaError_t launch_obs_lists(lc_ctx* c, int32_t* d_obeg, int32_t* d_cursor, int32_t* d_bsum,
+                             int32_t* d_obs, cudaStream_t s) {
   Store& st = c->st;
   if (st.n_mp <= 0) return cudaSuccess;
   const int nb = (st.n_mp + SCAN_SEG - 1) / SCAN_SEG;
@@ -367,6 +366,18 @@ cudaError_t launch_refresh(lc_ctx* c, int n_sel, const int32_t* d_idx, int what,
   k_obs_fill<<<grid_of(st.n_feat, LC_NTHREADS), LC_NTHREADS, 0, s>>>(st.n_feat, st.n_mp, st.feat_mp, d_obeg,
                                                                     d_cursor, d_obs);
   c->launches += 4;
+  return cudaGetLastError();
+}
+
+int obs_scan_blocks(int n_mp) { return (n_mp + SCAN_SEG - 1) / SCAN_SEG; }
+
+cudaError_t launch_refresh(lc_ctx* c, int n_sel, const int32_t* d_idx, int what, int32_t* d_obeg,
+                           int32_t* d_cursor, int32_t* d_bsum, int32_t* d_obs,
+                           unsigned long long* counts, cudaStream_t s) {
+  Store& st = c->st;
+  if (st.n_mp <= 0) return cudaSuccess;
+  cudaError_t e = launch_obs_lists(c, d_obeg, d_cursor, d_bsum, d_obs, s);
+  if (e != cudaSuccess) return e;
   if (n_sel > 0) {
     RefreshArgs a;
     a.n_sel = n_sel; a.n_mp = st.n_mp; a.n_kf = st.n_kf; a.n_levels = st.n_levels; a.what = what;

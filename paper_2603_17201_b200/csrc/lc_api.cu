@@ -744,6 +744,39 @@ lc_status lc_refresh_mappoints(lc_ctx* c, int32_t n, const int32_t* mp_idx, int3
   });
 }
 
+lc_status lc_update_connections(lc_ctx* c, int32_t n, const int32_t* kf_idx, int32_t th,
+                                int32_t max_edges, int32_t* out_n, int32_t* out_kf, int32_t* out_w,
+                                int64_t* out_counts, void* stream) {
+  return guarded(c, [&] {
+    capture_gate(c, stream, true);
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    REQUIRE(kf_idx == nullptr || n >= 0, LC_EINVAL, "n < 0");
+    REQUIRE(max_edges >= 0 && th >= 1, LC_EINVAL, "bad max_edges / th");
+    REQUIRE(c->st.n_kf <= connections_max_kf(), LC_EINVAL, "too many keyframes for the shared weight array");
+    REQUIRE(out_n, LC_EINVAL, "null out_n");
+    REQUIRE(max_edges == 0 || (out_kf && out_w), LC_EINVAL, "null out_kf / out_w");
+    Store& st = c->st;
+    Call call(c, stream);
+    const int n_sel = kf_idx ? n : st.n_kf;
+    const int32_t* d_idx = kf_idx ? call.in(kf_idx, (size_t)n_sel) : nullptr;
+    int32_t* d_n = call.out(out_n, (size_t)n_sel);
+    int32_t* d_kf = max_edges ? call.out(out_kf, (size_t)n_sel * max_edges, true) : nullptr;
+    int32_t* d_w = max_edges ? call.out(out_w, (size_t)n_sel * max_edges, true) : nullptr;
+    int32_t* d_obeg = (int32_t*)call.scratch(sizeof(int32_t) * ((size_t)st.n_mp + 1));
+    int32_t* d_cursor = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(st.n_mp, 1));
+    int32_t* d_bsum = (int32_t*)call.scratch(sizeof(int32_t) * std::max(obs_scan_blocks(st.n_mp), 1));
+    int32_t* d_obs = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(st.n_feat, 1));
+    unsigned long long* cnt = call.counts(out_counts, LC_NCOUNT);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
+    {
+      Prof pr(c, LC_PROF_CONN, call.s);
+      CK(launch_obs_lists(c, d_obeg, d_cursor, d_bsum, d_obs, call.s));
+      CK(launch_connections(c, n_sel, d_idx, th, max_edges, d_obeg, d_obs, d_n, d_kf, d_w, cnt, call.s));
+    }
+    call.finish();
+  });
+}
+
 lc_status lc_state_save(lc_ctx* c, void* stream) {
   return guarded(c, [&] {
     capture_gate(c, stream, false);

@@ -273,6 +273,31 @@ class Context:
             return counts_dict(cnt)
         return cnt
 
+    # -- lc_update_connections -----------------------------------------------------
+    def update_connections(self, kf_idx=None, th=15, max_edges=64, host=True):
+        """Covisibility edges (n_edges [n], kf [n, max_edges], weight [n, max_edges], counts);
+        row i is valid up to min(n_edges[i], max_edges), -1 / 0 elsewhere."""
+        k = self._keep(host)
+        n = self.n_kf if kf_idx is None else (int(kf_idx.shape[0]) if hasattr(kf_idx, "shape") else len(kf_idx))
+        if host:
+            o_n = np.zeros(n, np.int32)
+            o_kf = np.full((n, max_edges), -1, np.int32)
+            o_w = np.zeros((n, max_edges), np.int32)
+            cnt = np.zeros(LC_NCOUNT, np.int64)
+        else:
+            o_n = self._dev(n, torch.int32)
+            o_kf = self._dev(n * max_edges, torch.int32).fill_(-1)
+            o_w = self._dev(n * max_edges, torch.int32).zero_()
+            cnt = self._dev(LC_NCOUNT, torch.int64)
+        st = self.lib.lc_update_connections(self.h, n if kf_idx is not None else 0, k.ptr(kf_idx, np.int32),
+                                            int(th), int(max_edges), k.ptr(o_n), k.ptr(o_kf), k.ptr(o_w),
+                                            k.ptr(cnt), self._stream())
+        self._check("lc_update_connections", st)
+        if host:
+            self.synchronize()
+            return o_n, o_kf, o_w, counts_dict(cnt)
+        return o_n, o_kf.view(n, max_edges), o_w.view(n, max_edges), cnt
+
     # -- lc_correct_sim3 ----------------------------------------------------------
     def correct_window(self, cur_kf, S_cw_corr, window, host=True):
         k = self._keep(host)

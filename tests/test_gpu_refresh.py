@@ -80,3 +80,45 @@ def test_refresh_many_observations_and_skips(Ctx):
     _compare(ctx, om)
     st = ctx.download_map()
     assert np.array_equal(st["mp_desc"][1], base) and np.array_equal(st["mp_desc"][2], ~base)
+
+
+def _cmp_conn(g, o, max_edges):
+    gn, gk, gw = g[0], g[1], g[2]
+    on, ok, ow = o[0], o[1], o[2]
+    assert np.array_equal(gn, on), np.nonzero(gn != on)[0][:5]
+    for i in range(len(on)):
+        m = min(int(on[i]), max_edges)
+        assert np.array_equal(gk[i, :m], ok[i, :m]) and np.array_equal(gw[i, :m], ow[i, :m]), i
+
+
+@pytest.mark.parametrize("name", ["T1", "T2", "C2"])
+def test_connections_after_loop_event_match_oracle(Ctx, name):
+    """Covisibility recount (lc_update_connections) after the merge:
+    edge counts, keyframes and weights equal the oracle's (O12) for every keyframe."""
+    w = make_world(name, 0)
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    om = oracle.OracleMap(w)
+    for side in (ctx, om):
+        side.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+        side.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+    for th, me in ((15, 64), (1, 8)):
+        g = ctx.update_connections(None, th=th, max_edges=me)
+        o = om.update_connections(None, th=th, max_edges=me)
+        _cmp_conn(g, o, me)
+        assert g[3]["conn_kf"] == o[3]["conn_kf"] == w.n_kf and g[3]["conn_edges"] == o[3]["conn_edges"]
+    sel = np.asarray(w.window, np.int32)
+    _cmp_conn(ctx.update_connections(sel, th=15, max_edges=32), om.update_connections(sel, th=15, max_edges=32), 32)
+
+
+def test_connections_spec_example_on_gpu(Ctx):
+    base = tm.desc_from_bits([])
+    holdings = [list(range(30)), list(range(20)) + [40, 41], list(range(25, 30)), [50]]
+    kfs = [dict(feats=[dict(u=1.0 + i, v=1.0, desc=base, mp=int(q)) for i, q in enumerate(h)]) for h in holdings]
+    mps = [dict(pos=(0.0, 0.0, 1.0), desc=base) for _ in range(51)]
+    arrays = tm.build(kfs, mps)
+    ctx = Ctx(0)
+    ctx.upload_map(arrays, [tm.PIN])
+    n, kf, wt, c = ctx.update_connections(None, th=5, max_edges=4)
+    assert list(n) == [2, 1, 1, 0]
+    assert list(kf[0, :2]) == [1, 2] and list(wt[0, :2]) == [20, 5]
