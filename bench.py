@@ -393,7 +393,7 @@ def main():
 
     # secondary: SURVEY §8(f) f2, refresh of the loop's map points after the event
     # (observation transpose + medoid descriptor + normal / depth range)
-    refresh = None
+    refresh = connections = None
     if ws == 1 and not args.profile_only and not args.no_sbp:
         sel = torch.from_numpy(np.unique(w.mp_list).astype(np.int32)).to(dev)
         rms = []
@@ -408,6 +408,20 @@ def main():
             if i >= args.warmup:
                 rms.append(a.elapsed_time(b))
         rcnt = rc.cpu().numpy()
+        # covisibility recount of every keyframe after the event
+        cms = []
+        for i in range(args.warmup + args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            cn = ctx.update_connections(None, th=15, max_edges=64, host=False)
+            b.record(stream)
+            b.synchronize()
+            if i >= args.warmup:
+                cms.append(a.elapsed_time(b))
+        ccnt = cn[3].cpu().numpy()
+        connections = {"keyframes": int(ccnt[counts.index("conn_kf")]),
+                       "edges": int(ccnt[counts.index("conn_edges")]), "th": 15,
+                       "ms_per_call": round(float(np.mean(cms)), 5)}
         refresh = {"points": int(rcnt[counts.index("refresh_mp")]),
                    "observations": int(rcnt[counts.index("refresh_obs")]),
                    "ms_per_call": round(float(np.mean(rms)), 5),
@@ -475,6 +489,7 @@ def main():
             "upload": upload,
             "sbp": sbp,
             "refresh": refresh,
+            "connections": connections,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
