@@ -17,23 +17,22 @@ namespace {
 
 constexpr int EDGE_CAP = 2048;   // edges ranked per keyframe in shared memory
 
-__device__ __forceinline__ int kf_of_f(const int32_t* __restrict__ kf_fbeg, int n_kf, int f) {
-  int lo = 0, hi = n_kf - 1;   // largest k with kf_fbeg[k] <= f
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (kf_fbeg[mid] <= f) lo = mid; else hi = mid - 1;
+// feat_first[f] = 1 iff feature f is the smallest slot of its keyframe holding its map
+// point (A38: a keyframe counts a point once). Thread per observation position.
+__global__ void k_feat_first(int n_mp, const int32_t* __restrict__ feat_mp,
+                             const int32_t* __restrict__ obeg, const int32_t* __restrict__ obs,
+                             const int32_t* __restrict__ obs_kf, uint8_t* __restrict__ feat_first) {
+  const int n_obs_total = obeg[n_mp];   // the lists' length (associations)
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n_obs_total; p += gridDim.x * blockDim.x) {
+    const int f = obs[p], k = obs_kf[p];
+    const int q = feat_mp[f];
+    if ((unsigned)q >= (unsigned)n_mp) continue;
+    const int b = obeg[q], e = obeg[q + 1];
+    bool first = true;
+    for (int i = b; i < e; ++i)
+      if (obs_kf[i] == k && obs[i] < f) { first = false; break; }
+    feat_first[f] = first ? 1 : 0;
   }
-  return lo;
-}
-
-// does feature g hold its map point for the first time inside [lo, hi)? (the smallest
-// observation of the point within that feature range)
-__device__ __forceinline__ bool first_in(const int32_t* __restrict__ ob, int no, int g, int lo, int hi) {
-  for (int j = 0; j < no; ++j) {
-    const int h = ob[j];
-    if (h >= lo && h < hi && h < g) return false;
-  }
-  return true;
 }
 
 struct ConnArgs {
@@ -44,6 +43,8 @@ struct ConnArgs {
   const uint8_t* flags;
   const int32_t* obeg;
   const int32_t* obs;
+  const int32_t* obs_kf;
+  const uint8_t* feat_first;
   int32_t* out_n;
   int32_t* out_kf;
   int32_t* out_w;
@@ -68,14 +69,13 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_connections(const ConnArgs a) {
     for (int f = fb + threadIdx.x; f < fe; f += blockDim.x) {
       const int q = a.feat_mp[f];
       if ((unsigned)q >= (unsigned)a.n_mp || (a.flags[q] & 1u)) continue;   // A38: not bad
+      if (!a.feat_first[f]) continue;                   // distinct in k
       const int32_t* ob = a.obs + a.obeg[q];
+      const int32_t* okf = a.obs_kf + a.obeg[q];
       const int no = a.obeg[q + 1] - a.obeg[q];
-      if (!first_in(ob, no, f, fb, fe)) continue;                          // distinct in k
       for (int j = 0; j < no; ++j) {
-        const int g = ob[j];
-        const int k2 = kf_of_f(a.kf_fbeg, a.n_kf, g);
-        if (k2 == k) continue;
-        if (!first_in(ob, no, g, a.kf_fbeg[k2], a.kf_fbeg[k2 + 1])) continue;   // once per k2
+        const int k2 = okf[j];
+        if (k2 == k || !a.feat_first[ob[j]]) continue;   // once per k2
         atomicAdd(&s_w[k2], 1);
       }
     }
@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_connections(const ConnArgs a) {
 int connections_max_kf() { return 40000; }
 
 cudaError_t launch_connections(lc_ctx* c, int n_sel, const int32_t* d_idx, int th, int max_edges,
-                               const int32_t* d_obeg, const int32_t* d_obs, int32_t* out_n,
+                               const int32_t* d_obeg, const int32_t* d_obs, const int32_t* d_obs_kf,
+                               uint8_t* d_first, int32_t* out_n,
                                int32_t* out_kf, int32_t* out_w, unsigned long long* counts,
                                cudaStream_t s) {
   Store& st = c->st;
@@ -139,7 +140,12 @@ cudaError_t launch_connections(lc_ctx* c, int n_sel, const int32_t* d_idx, int t
   ConnArgs a;
   a.n_sel = n_sel; a.n_kf = st.n_kf; a.n_mp = st.n_mp; a.th = th; a.max_edges = max_edges;
   a.idx = d_idx; a.kf_fbeg = st.kf_fbeg; a.feat_mp = st.feat_mp; a.flags = st.mp_flags;
-  a.obeg = d_obeg; a.obs = d_obs; a.out_n = out_n; a.out_kf = out_kf; a.out_w = out_w; a.counts = counts;
+  a.obeg = d_obeg; a.obs = d_obs; a.obs_kf = d_obs_kf; a.feat_first = d_first; a.out_n = out_n; a.out_kf = out_kf; a.out_w = out_w; a.counts = counts;
+  if (st.n_feat > 0) {   // first-slot flags over every observation
+    k_feat_first<<<std::min<int64_t>(((int64_t)st.n_feat + LC_NTHREADS - 1) / LC_NTHREADS, 148 * 32),
+                   LC_NTHREADS, 0, s>>>(st.n_mp, st.feat_mp, d_obeg, d_obs, d_obs_kf, d_first);
+    c->launches++;
+  }
   const size_t smem = sizeof(int32_t) * (size_t)std::max(st.n_kf, 1);
   cudaError_t e = cudaFuncSetAttribute(k_connections, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

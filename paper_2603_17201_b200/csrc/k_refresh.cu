@@ -91,15 +91,20 @@ __global__ void k_scan_c(int32_t* __restrict__ out, int n, const int32_t* __rest
   }
 }
 
-// (1) scatter feature indices into their point's observation segment
-__global__ void k_obs_fill(int n_feat, int n_mp, const int32_t* __restrict__ feat_mp,
-                           const int32_t* __restrict__ obeg, int32_t* __restrict__ cursor,
-                           int32_t* __restrict__ obs) {
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < n_feat; f += gridDim.x * blockDim.x) {
-    const int32_t q = feat_mp[f];
-    if ((unsigned)q >= (unsigned)n_mp) continue;
-    const int32_t p = atomicAdd(&cursor[q], 1);
-    if (p < obeg[q + 1]) obs[p] = f;
+// (1) scatter (feature, keyframe) into their point's observation segment: a CTA per
+// keyframe, so the keyframe of each observation is known without a search
+__global__ void k_obs_fill(int n_kf, int n_mp, const int32_t* __restrict__ kf_fbeg,
+                           const int32_t* __restrict__ feat_mp, const int32_t* __restrict__ obeg,
+                           int32_t* __restrict__ cursor, int32_t* __restrict__ obs,
+                           int32_t* __restrict__ obs_kf) {
+  for (int k = blockIdx.x; k < n_kf; k += gridDim.x) {
+    const int fe = kf_fbeg[k + 1];
+    for (int f = kf_fbeg[k] + threadIdx.x; f < fe; f += blockDim.x) {
+      const int32_t q = feat_mp[f];
+      if ((unsigned)q >= (unsigned)n_mp) continue;
+      const int32_t p = atomicAdd(&cursor[q], 1);
+      if (p < obeg[q + 1]) { obs[p] = f; obs_kf[p] = k; }
+    }
   }
 }
 
@@ -130,6 +135,7 @@ struct RefreshArgs {
   const int32_t* idx;
   const int32_t* obeg;
   const int32_t* obs;
+  const int32_t* obs_kf;   // keyframe of each observation (same layout as obs)
   const int32_t* feat_cpos;
   const uint32_t* fc_meta;
   const uint4* fc_desc;
@@ -226,6 +232,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_refresh(const RefreshArgs a) {
         int r = 0;
         for (int j = 0; j < N; ++j) r += s_tmp[warp][j] < f;
         s_ord[warp][r] = f;
+        s_kf[warp][r] = a.obs_kf[b + i];
       }
       __syncwarp();
       for (int i = lane; i < N; i += 32) {
@@ -258,15 +265,13 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_refresh(const RefreshArgs a) {
         MpRec& r = a.rec[q];
         const double p[3] = {(double)r.pos[0], (double)r.pos[1], (double)r.pos[2]};
         for (int i = lane; i < N; i += 32) {
-          const int32_t f = s_ord[warp][i];
-          const int k = kf_of_feature(a.kf_fbeg, a.n_kf, f);
+          const int k = s_kf[warp][i];
           double O[3], v[3];
           kf_centre(a.kf_pose, k, O);
           for (int j = 0; j < 3; ++j) v[j] = p[j] - O[j];
           const double len = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
           for (int j = 0; j < 3; ++j) s_u[warp][i][j] = len == 0.0 ? 0.0 : v[j] / len;
           s_len[warp][i] = len;
-          s_kf[warp][i] = k;
         }
         __syncwarp();
         if (lane == 0) {
@@ -356,15 +361,15 @@ int grid_of(int64_t n, int per_block) {
 }  // namespace
 
 cudaError_t launch_obs_lists(lc_ctx* c, int32_t* d_obeg, int32_t* d_cursor, int32_t* d_bsum,
-                             int32_t* d_obs, cudaStream_t s) {
+                             int32_t* d_obs, int32_t* d_obs_kf, cudaStream_t s) {
   Store& st = c->st;
   if (st.n_mp <= 0) return cudaSuccess;
   const int nb = (st.n_mp + SCAN_SEG - 1) / SCAN_SEG;
   k_scan_a<<<nb, LC_NTHREADS, 0, s>>>(st.mp_nobs, st.n_mp, d_obeg, d_bsum);
   k_scan_b<<<1, LC_NTHREADS, 0, s>>>(d_bsum, nb, d_obeg + st.n_mp);
   k_scan_c<<<(st.n_mp + LC_NTHREADS - 1) / LC_NTHREADS, LC_NTHREADS, 0, s>>>(d_obeg, st.n_mp, d_bsum, d_cursor);
-  k_obs_fill<<<grid_of(st.n_feat, LC_NTHREADS), LC_NTHREADS, 0, s>>>(st.n_feat, st.n_mp, st.feat_mp, d_obeg,
-                                                                    d_cursor, d_obs);
+  k_obs_fill<<<std::max(1, std::min(st.n_kf, 148 * 16)), LC_NTHREADS, 0, s>>>(
+      st.n_kf, st.n_mp, st.kf_fbeg, st.feat_mp, d_obeg, d_cursor, d_obs, d_obs_kf);
   c->launches += 4;
   return cudaGetLastError();
 }
@@ -372,16 +377,16 @@ cudaError_t launch_obs_lists(lc_ctx* c, int32_t* d_obeg, int32_t* d_cursor, int3
 int obs_scan_blocks(int n_mp) { return (n_mp + SCAN_SEG - 1) / SCAN_SEG; }
 
 cudaError_t launch_refresh(lc_ctx* c, int n_sel, const int32_t* d_idx, int what, int32_t* d_obeg,
-                           int32_t* d_cursor, int32_t* d_bsum, int32_t* d_obs,
+                           int32_t* d_cursor, int32_t* d_bsum, int32_t* d_obs, int32_t* d_obs_kf,
                            unsigned long long* counts, cudaStream_t s) {
   Store& st = c->st;
   if (st.n_mp <= 0) return cudaSuccess;
-  cudaError_t e = launch_obs_lists(c, d_obeg, d_cursor, d_bsum, d_obs, s);
+  cudaError_t e = launch_obs_lists(c, d_obeg, d_cursor, d_bsum, d_obs, d_obs_kf, s);
   if (e != cudaSuccess) return e;
   if (n_sel > 0) {
     RefreshArgs a;
     a.n_sel = n_sel; a.n_mp = st.n_mp; a.n_kf = st.n_kf; a.n_levels = st.n_levels; a.what = what;
-    a.idx = d_idx; a.obeg = d_obeg; a.obs = d_obs; a.feat_cpos = st.feat_cpos; a.fc_meta = st.fc_meta;
+    a.idx = d_idx; a.obeg = d_obeg; a.obs = d_obs; a.obs_kf = d_obs_kf; a.feat_cpos = st.feat_cpos; a.fc_meta = st.fc_meta;
     a.fc_desc = st.fc_desc; a.kf_fbeg = st.kf_fbeg; a.kf_pose = st.kf_pose; a.flags = st.mp_flags;
     a.ref_kf = st.mp_ref_kf; a.rec = st.mp_rec; a.counts = counts;
     for (int i = 0; i < LC_MAX_LEVELS; ++i) a.scale[i] = st.scale[i];

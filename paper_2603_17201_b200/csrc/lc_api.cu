@@ -730,11 +730,12 @@ lc_status lc_refresh_mappoints(lc_ctx* c, int32_t n, const int32_t* mp_idx, int3
     int32_t* d_cursor = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(st.n_mp, 1));
     int32_t* d_bsum = (int32_t*)call.scratch(sizeof(int32_t) * std::max(nb, 1));
     int32_t* d_obs = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(st.n_feat, 1));
+    int32_t* d_obs_kf = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(st.n_feat, 1));
     unsigned long long* cnt = (unsigned long long*)call.scratch(sizeof(uint64_t) * LC_NCOUNT);
     CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
     {
       Prof pr(c, LC_PROF_REFRESH, call.s);
-      CK(launch_refresh(c, n_sel, d_idx, what, d_obeg, d_cursor, d_bsum, d_obs, cnt, call.s));
+      CK(launch_refresh(c, n_sel, d_idx, what, d_obeg, d_cursor, d_bsum, d_obs, d_obs_kf, cnt, call.s));
     }
     if (out_counts) {
       int64_t* d = call.out(out_counts, LC_NCOUNT);
@@ -766,12 +767,15 @@ lc_status lc_update_connections(lc_ctx* c, int32_t n, const int32_t* kf_idx, int
     int32_t* d_cursor = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(st.n_mp, 1));
     int32_t* d_bsum = (int32_t*)call.scratch(sizeof(int32_t) * std::max(obs_scan_blocks(st.n_mp), 1));
     int32_t* d_obs = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(st.n_feat, 1));
+    int32_t* d_obs_kf = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(st.n_feat, 1));
+    uint8_t* d_first = (uint8_t*)call.scratch(std::max<size_t>(st.n_feat, 1));
     unsigned long long* cnt = call.counts(out_counts, LC_NCOUNT);
     CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
     {
       Prof pr(c, LC_PROF_CONN, call.s);
-      CK(launch_obs_lists(c, d_obeg, d_cursor, d_bsum, d_obs, call.s));
-      CK(launch_connections(c, n_sel, d_idx, th, max_edges, d_obeg, d_obs, d_n, d_kf, d_w, cnt, call.s));
+      CK(launch_obs_lists(c, d_obeg, d_cursor, d_bsum, d_obs, d_obs_kf, call.s));
+      CK(launch_connections(c, n_sel, d_idx, th, max_edges, d_obeg, d_obs, d_obs_kf, d_first, d_n, d_kf,
+                            d_w, cnt, call.s));
     }
     call.finish();
   });

@@ -345,13 +345,14 @@ cudaError_t launch_state_copy(lc_ctx* c, bool save, cudaStream_t s);
 cudaError_t launch_download_pos(lc_ctx* c, float* out, cudaStream_t s);
 cudaError_t launch_download_rec(lc_ctx* c, float* normal, float* dmax, uint8_t* desc, cudaStream_t s);
 cudaError_t launch_obs_lists(lc_ctx* c, int32_t* d_obeg, int32_t* d_cursor, int32_t* d_bsum,
-                             int32_t* d_obs, cudaStream_t s);   // per-point observation lists
+                             int32_t* d_obs, int32_t* d_obs_kf, cudaStream_t s);   // per-point observation lists
 int obs_scan_blocks(int n_mp);
 int connections_max_kf();
 cudaError_t launch_connections(lc_ctx* c, int n_sel, const int32_t* d_idx, int th, int max_edges,
-                               const int32_t* d_obeg, const int32_t* d_obs, int32_t* out_n,
+                               const int32_t* d_obeg, const int32_t* d_obs, const int32_t* d_obs_kf,
+                               uint8_t* d_first, int32_t* out_n,
                                int32_t* out_kf, int32_t* out_w, unsigned long long* counts,
                                cudaStream_t s);
 cudaError_t launch_refresh(lc_ctx* c, int n_sel, const int32_t* d_idx, int what, int32_t* d_obeg,
-                           int32_t* d_cursor, int32_t* d_bsum, int32_t* d_obs,
+                           int32_t* d_cursor, int32_t* d_bsum, int32_t* d_obs, int32_t* d_obs_kf,
                            unsigned long long* counts, cudaStream_t s);

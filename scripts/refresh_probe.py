@@ -15,3 +15,5 @@ ctx.fuse(w.window, torch.from_numpy(w.mp_list).cuda(), FUSE_PARAMS, window_S=w.w
          win_list_begin=w.win_list_begin)
 sel = torch.from_numpy(np.unique(w.mp_list).astype(np.int32)).cuda()
 print(ctx.refresh_mappoints(sel, what=3))
+n, kf, w, c = ctx.update_connections(None, th=15, max_edges=64)
+print(c["conn_kf"], c["conn_edges"], int(n.max()))
