@@ -1,0 +1,73 @@
+"""Keyframe-sharded fusion (paper_2603_17201_b200/dist.py) with real liblc contexts:
+two ranks (gloo, both on cuda:0 -- the GPU box has one device) run PLAN on their shard,
+merge [winner | victim] by all_reduce(MIN) and APPLY; the merged tables and the final
+map store must equal single-GPU FUSE_ALL bit for bit (readings A17, A21). The NCCL
+launch of bench.py runs the same code with one device per rank."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from lcsynth import make_world  # noqa: E402
+from lcsynth.world import FUSE_PARAMS  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, name, on_device, out_path):
+    import torch.distributed as dist
+    from paper_2603_17201_b200 import Context
+    from paper_2603_17201_b200.dist import fuse_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    w = make_world(name, 0)
+    ctx = Context(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    dev = torch.device("cuda:0") if on_device else None
+    lst = torch.from_numpy(w.mp_list).cuda() if on_device else w.mp_list
+    pc, ac, tables = fuse_sharded(ctx, w.window, lst, FUSE_PARAMS, window_S=w.win_S,
+                                  win_list_begin=w.win_list_begin, device=dev)
+    torch.cuda.synchronize()
+    st = ctx.download_map()
+    np.savez(f"{out_path}.{rank}.npz", tables=tables.cpu().numpy(), feat_mp=st["feat_mp"],
+             mp_flags=st["mp_flags"], mp_replaced_by=st["mp_replaced_by"], mp_nobs=st["mp_nobs"])
+    ctx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["T5", "C2"])
+@pytest.mark.parametrize("on_device", [False, True], ids=["host-tables", "device-tables"])
+def test_sharded_fuse_two_ranks_equals_single_gpu(tmp_path, name, on_device):
+    import torch.multiprocessing as mp
+    from paper_2603_17201_b200 import Context, build
+    build.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    out = str(tmp_path / "r")
+    mp.start_processes(_worker, args=(2, _free_port(), name, on_device, out), nprocs=2, join=True,
+                       start_method="spawn")
+    w = make_world(name, 0)
+    ctx = Context(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    g = ctx.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+    st = ctx.download_map()
+    ref_tables = np.concatenate([g["winner"], g["victim"]])
+    for r in range(2):
+        d = np.load(f"{out}.{r}.npz")
+        assert np.array_equal(d["tables"], ref_tables), f"rank {r}: merged tables"
+        for key in ("feat_mp", "mp_flags", "mp_replaced_by", "mp_nobs"):
+            assert np.array_equal(d[key], st[key]), f"rank {r}: {key}"
