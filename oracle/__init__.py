@@ -22,7 +22,7 @@ COUNTER_NAMES = [
     "cull_angle", "candidates", "no_cand", "over_th", "ratio_rej", "proposals",
     "winners", "orient_rej", "add", "victim_prop", "loop_skip", "bad_slot",
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
-    "refresh_mp", "refresh_obs", "conn_kf", "conn_edges",
+    "refresh_mp", "refresh_obs", "conn_kf", "conn_edges", "ransac_hyp", "ransac_inliers",
 ]
 NONE64 = np.iinfo(np.int64).max
 
@@ -81,7 +81,7 @@ def lib():
         _lib.orc_predict_level.restype = C.c_int
         _lib.orc_predict_level.argtypes = [C.c_double, C.c_double, C.c_void_p, C.c_int32]
         for fn in ("orc_correct_window", "orc_correct_all", "orc_fuse", "orc_search_by_projection",
-                   "orc_refresh", "orc_update_connections"):
+                   "orc_refresh", "orc_update_connections", "orc_sim3_ransac"):
             getattr(_lib, fn).restype = C.c_int
     return _lib
 
@@ -144,6 +144,25 @@ def project(cam, pc):
     uv = np.zeros(2, np.float64)
     lib().orc_project(C.byref(c), _p(pc), _p(uv))
     return uv
+
+
+def jacobi4(A):
+    """Eigenvalues / eigenvector columns of a symmetric 4x4 (oracle's Jacobi, A42)."""
+    A = np.ascontiguousarray(A, np.float64).reshape(4, 4)
+    ev = np.zeros(4, np.float64)
+    V = np.zeros((4, 4), np.float64)
+    lib().orc_jacobi4(_p(A), _p(ev), _p(V))
+    return ev, V
+
+
+def horn(P1, P2, fix_scale=False):
+    """Closed-form similarity S12 (p1 ~ s R p2 + t) of all correspondences (A42)."""
+    P1 = np.ascontiguousarray(P1, np.float64).reshape(-1, 3)
+    P2 = np.ascontiguousarray(P2, np.float64).reshape(-1, 3)
+    sel = np.arange(len(P1), dtype=np.int32)
+    S = np.zeros(13, np.float64)
+    lib().orc_horn(C.c_int32(len(P1)), _p(sel), _p(P1), _p(P2), C.c_int32(int(fix_scale)), _p(S))
+    return S
 
 
 def scale_table(L=8, f=1.2):
@@ -326,3 +345,29 @@ class OracleMap:
         if rc != 0:
             raise ValueError("orc_update_connections: invalid arguments")
         return out_n, out_kf, out_w, dict(zip(COUNTER_NAMES, cnt.tolist()))
+
+    # -- O13 -----------------------------------------------------------------
+    def sim3_ransac(self, prob_begin, P1, P2, uv1, uv2, sig1, sig2, cam1, cam2, samples,
+                    chi2=9.210, fix_scale=False, refit=True):
+        """Batched Sim3 RANSAC: returns (S [n_prob, 13], inliers [n_prob], mask [n_corr], counts)."""
+        pb = np.ascontiguousarray(prob_begin, np.int32)
+        n_prob = len(pb) - 1
+        P1 = np.ascontiguousarray(P1, np.float64).reshape(-1, 3)
+        P2 = np.ascontiguousarray(P2, np.float64).reshape(-1, 3)
+        uv1 = np.ascontiguousarray(uv1, np.float32).reshape(-1, 2)
+        uv2 = np.ascontiguousarray(uv2, np.float32).reshape(-1, 2)
+        sig1 = np.ascontiguousarray(sig1, np.float32)
+        sig2 = np.ascontiguousarray(sig2, np.float32)
+        cam1 = np.ascontiguousarray(cam1, np.int32)
+        cam2 = np.ascontiguousarray(cam2, np.int32)
+        smp = np.ascontiguousarray(samples, np.int32).reshape(n_prob, -1, 3)
+        n_iter = smp.shape[1]
+        S = np.zeros((n_prob, 13), np.float64)
+        inl = np.zeros(n_prob, np.int32)
+        mask = np.zeros(len(P1), np.uint8)
+        cnt = np.zeros(len(COUNTER_NAMES), np.int64)
+        lib().orc_sim3_ransac(C.byref(self._m), C.c_int32(n_prob), _p(pb), _p(P1), _p(P2), _p(uv1),
+                              _p(uv2), _p(sig1), _p(sig2), _p(cam1), _p(cam2), _p(smp), C.c_int32(n_iter),
+                              C.c_double(chi2), C.c_int32(int(fix_scale)), C.c_int32(int(refit)), _p(S),
+                              _p(inl), _p(mask), _p(cnt))
+        return S, inl, mask, dict(zip(COUNTER_NAMES, cnt.tolist()))

@@ -27,6 +27,10 @@
  *   - Covisibility recount after the merge ("creates new connections in the
  *     covisibility and essential graphs"; SURVEY.md
  *     §8(f) f4, readings A38-A40)                               -> orc_update_connections (O12)
+ *   - Region-detection Sim3 estimation: RANSAC over minimal 3-point samples,
+ *     closed-form Horn similarity, symmetric reprojection inlier test ("estimating
+ *     the relative pose between the new keyframe and the matched one", PAPER.md:89;
+ *     SURVEY.md §8(f) f3, readings A41-A44)                     -> orc_sim3_ransac (O13)
  * The paper gives no matching math (SURVEY.md §0 "Key finding"); every
  * constant and tie-break is a DESIGN.md reading (A1-A32), noted inline.
  *
@@ -51,7 +55,7 @@ enum {
   C_CULL_ANGLE, C_CANDIDATES, C_NO_CAND, C_OVER_TH, C_RATIO_REJ, C_PROPOSALS,
   C_WINNERS, C_ORIENT_REJ, C_ADD, C_VICTIM_PROP, C_LOOP_SKIP, C_BAD_SLOT,
   C_VICTIMS, C_REWIRED, C_DUP_CLEARED, C_ADDED, C_CORR_KF, C_CORR_MP,
-  C_REFRESH_MP, C_REFRESH_OBS, C_CONN_KF, C_CONN_EDGES, C_N
+  C_REFRESH_MP, C_REFRESH_OBS, C_CONN_KF, C_CONN_EDGES, C_RANSAC_HYP, C_RANSAC_INLIERS, C_N
 };
 
 /* query status codes written to out_status (negative = culled/skipped) */
@@ -820,6 +824,172 @@ int orc_update_connections(orc_map *m, int32_t n, const int32_t *idx, int32_t th
     cnt[C_CONN_EDGES] += ne;
   }
   free(kf_of); free(hbeg); free(holds); free(hn); free(w); free(seen);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O13 Sim3 RANSAC (readings A41-A44).                    */
+/* ------------------------------------------------------------------------- */
+/* A42: eigen-decomposition of a symmetric 4x4 by cyclic Jacobi rotations in  */
+/* the fixed order (0,1),(0,2),(0,3),(1,2),(1,3),(2,3); at most 50 sweeps,    */
+/* stop when the off-diagonal sum of squares is 0 or <= 1e-300.               */
+void orc_jacobi4(const double *A_in, double *evals, double *evecs /* [4][4] columns */) {
+  double A[16], V[16];
+  memcpy(A, A_in, sizeof(A));
+  for (int i = 0; i < 16; ++i) V[i] = (i % 5 == 0) ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 50; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < 4; ++p)
+      for (int q = p + 1; q < 4; ++q) off = off + A[4 * p + q] * A[4 * p + q];
+    if (off <= 1e-300) break;
+    for (int p = 0; p < 4; ++p)
+      for (int q = p + 1; q < 4; ++q) {
+        const double apq = A[4 * p + q];
+        if (apq == 0.0) continue;
+        const double theta = (A[4 * q + q] - A[4 * p + p]) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < 4; ++k) {   /* columns p, q of A */
+          const double akp = A[4 * k + p], akq = A[4 * k + q];
+          A[4 * k + p] = c * akp - sn * akq;
+          A[4 * k + q] = sn * akp + c * akq;
+        }
+        for (int k = 0; k < 4; ++k) {   /* rows p, q of A */
+          const double apk = A[4 * p + k], aqk = A[4 * q + k];
+          A[4 * p + k] = c * apk - sn * aqk;
+          A[4 * q + k] = sn * apk + c * aqk;
+        }
+        for (int k = 0; k < 4; ++k) {   /* eigenvector columns */
+          const double vkp = V[4 * k + p], vkq = V[4 * k + q];
+          V[4 * k + p] = c * vkp - sn * vkq;
+          V[4 * k + q] = sn * vkp + c * vkq;
+        }
+      }
+  }
+  for (int i = 0; i < 4; ++i) evals[i] = A[4 * i + i];
+  memcpy(evecs, V, sizeof(V));
+}
+
+/* A42: closed-form similarity S12 (p1 ~ s R p2 + t) from n >= 3 correspondences:
+ * centroids, M = sum (p2-c2)(p1-c1)^T (EXT M = Pr2 Pr1^T), Horn's N, quaternion = eigenvector of the
+ * largest eigenvalue (first on ties; sign so that w > 0, else the first non-zero
+ * component > 0), R from the quaternion, s = sum (p1-c1).(R(p2-c2)) / sum |R(p2-c2)|^2
+ * (1 when fix_scale), t = c1 - s R c2. Sums run in index order. Output 13-vector. */
+void orc_horn(int32_t n, const int32_t *sel, const double *P1, const double *P2, int32_t fix_scale,
+              double *S) {
+  double c1[3] = {0, 0, 0}, c2[3] = {0, 0, 0};
+  for (int32_t i = 0; i < n; ++i)
+    for (int j = 0; j < 3; ++j) {
+      c1[j] = c1[j] + P1[3 * (size_t)sel[i] + j];
+      c2[j] = c2[j] + P2[3 * (size_t)sel[i] + j];
+    }
+  for (int j = 0; j < 3; ++j) { c1[j] = c1[j] / (double)n; c2[j] = c2[j] / (double)n; }
+  double M[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int32_t i = 0; i < n; ++i) {
+    double a[3], b[3];
+    for (int j = 0; j < 3; ++j) { a[j] = P1[3 * (size_t)sel[i] + j] - c1[j]; b[j] = P2[3 * (size_t)sel[i] + j] - c2[j]; }
+    for (int r = 0; r < 3; ++r)   /* M = sum (p2 - c2)(p1 - c1)^T: R maps frame 2 into 1 */
+      for (int cc = 0; cc < 3; ++cc) M[3 * r + cc] = M[3 * r + cc] + b[r] * a[cc];
+  }
+  double N[16];
+  N[0] = (M[0] + M[4]) + M[8];  N[1] = M[5] - M[7];          N[2] = M[6] - M[2];          N[3] = M[1] - M[3];
+  N[5] = (M[0] - M[4]) - M[8];  N[6] = M[1] + M[3];          N[7] = M[6] + M[2];
+  N[10] = (-M[0] + M[4]) - M[8]; N[11] = M[5] + M[7];
+  N[15] = (-M[0] - M[4]) + M[8];
+  N[4] = N[1]; N[8] = N[2]; N[12] = N[3]; N[9] = N[6]; N[13] = N[7]; N[14] = N[11];
+  double ev[4], V[16];
+  orc_jacobi4(N, ev, V);
+  int best = 0;
+  for (int i = 1; i < 4; ++i) if (ev[i] > ev[best]) best = i;
+  double q[4] = {V[best], V[4 + best], V[8 + best], V[12 + best]};   /* (w, x, y, z) */
+  int lead = 0;
+  while (lead < 3 && q[lead] == 0.0) ++lead;
+  if (q[lead] < 0.0) for (int i = 0; i < 4; ++i) q[i] = -q[i];
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  double R[9];
+  R[0] = ((w * w + x * x) - y * y) - z * z; R[1] = 2.0 * (x * y - w * z);         R[2] = 2.0 * (x * z + w * y);
+  R[3] = 2.0 * (x * y + w * z);         R[4] = ((w * w - x * x) + y * y) - z * z; R[5] = 2.0 * (y * z - w * x);
+  R[6] = 2.0 * (x * z - w * y);         R[7] = 2.0 * (y * z + w * x);         R[8] = ((w * w - x * x) - y * y) + z * z;
+  double nom = 0.0, den = 0.0;
+  for (int32_t i = 0; i < n; ++i) {
+    double a[3], b[3], rb[3];
+    for (int j = 0; j < 3; ++j) { a[j] = P1[3 * (size_t)sel[i] + j] - c1[j]; b[j] = P2[3 * (size_t)sel[i] + j] - c2[j]; }
+    for (int j = 0; j < 3; ++j) rb[j] = row3(R + 3 * j, b);
+    nom = nom + ((a[0] * rb[0] + a[1] * rb[1]) + a[2] * rb[2]);
+    den = den + ((rb[0] * rb[0] + rb[1] * rb[1]) + rb[2] * rb[2]);
+  }
+  const double sc = fix_scale ? 1.0 : nom / den;
+  memcpy(S, R, sizeof(R));
+  for (int j = 0; j < 3; ++j) S[9 + j] = c1[j] - sc * row3(R + 3 * j, c2);
+  S[12] = sc;
+}
+
+/* A43: both reprojection errors below chi2 * sigma^2; behind a camera = outlier */
+static int ransac_inlier(const orc_camera *cam1, const orc_camera *cam2, const double *S12,
+                         const double *S21, const double *p1, const double *p2, const float *uv1,
+                         const float *uv2, float s1, float s2, double chi2) {
+  double a[3], b[3], uv[2];
+  orc_sim3_apply(S12, p2, a);                 /* P2 in camera 1 */
+  if (a[2] <= 0.0) return 0;
+  orc_project(cam1, a, uv);
+  double du = uv[0] - (double)uv1[0], dv = uv[1] - (double)uv1[1];
+  if (!(du * du + dv * dv < chi2 * (double)s1)) return 0;
+  orc_sim3_apply(S21, p1, b);                 /* P1 in camera 2 */
+  if (b[2] <= 0.0) return 0;
+  orc_project(cam2, b, uv);
+  du = uv[0] - (double)uv2[0]; dv = uv[1] - (double)uv2[1];
+  return du * du + dv * dv < chi2 * (double)s2;
+}
+
+int orc_sim3_ransac(const orc_map *m, int32_t n_prob, const int32_t *pbeg, const double *P1,
+                    const double *P2, const float *uv1, const float *uv2, const float *sig1,
+                    const float *sig2, const int32_t *cam1, const int32_t *cam2, const int32_t *samples,
+                    int32_t n_iter, double chi2, int32_t fix_scale, int32_t refit, double *out_S,
+                    int32_t *out_inl, uint8_t *out_mask, int64_t *cnt) {
+  for (int32_t b = 0; b < n_prob; ++b) {
+    const int32_t c0 = pbeg[b], nc = pbeg[b + 1] - pbeg[b];
+    const orc_camera *k1 = m->cams + cam1[b], *k2 = m->cams + cam2[b];
+    int32_t best_inl = -1, best_it = -1;
+    double bestS[13];
+    for (int32_t it = 0; it < n_iter; ++it) {
+      const int32_t *t = samples + 3 * ((size_t)b * n_iter + it);
+      if (t[0] < 0 || t[1] < 0 || t[2] < 0 || t[0] >= nc || t[1] >= nc || t[2] >= nc ||
+          t[0] == t[1] || t[0] == t[2] || t[1] == t[2]) continue;   /* A41 */
+      int32_t sel[3] = {c0 + t[0], c0 + t[1], c0 + t[2]};
+      double S[13], Si[13];
+      orc_horn(3, sel, P1, P2, fix_scale, S);
+      orc_sim3_inverse(S, Si);
+      cnt[C_RANSAC_HYP]++;
+      int32_t ninl = 0;
+      for (int32_t i = 0; i < nc; ++i)
+        ninl += ransac_inlier(k1, k2, S, Si, P1 + 3 * (size_t)(c0 + i), P2 + 3 * (size_t)(c0 + i),
+                              uv1 + 2 * (size_t)(c0 + i), uv2 + 2 * (size_t)(c0 + i), sig1[c0 + i],
+                              sig2[c0 + i], chi2);
+      if (ninl > best_inl) { best_inl = ninl; best_it = it; memcpy(bestS, S, sizeof(S)); }   /* A44 */
+    }
+    if (best_it < 0) {   /* no valid sample */
+      for (int i = 0; i < 13; ++i) out_S[13 * (size_t)b + i] = 0.0;
+      out_inl[b] = 0;
+      for (int32_t i = 0; i < nc; ++i) out_mask[c0 + i] = 0;
+      continue;
+    }
+    double Si[13];
+    orc_sim3_inverse(bestS, Si);
+    int32_t *sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nc > 0 ? nc : 1));
+    int32_t ns = 0;
+    for (int32_t i = 0; i < nc; ++i) {
+      const int in = ransac_inlier(k1, k2, bestS, Si, P1 + 3 * (size_t)(c0 + i), P2 + 3 * (size_t)(c0 + i),
+                                   uv1 + 2 * (size_t)(c0 + i), uv2 + 2 * (size_t)(c0 + i), sig1[c0 + i],
+                                   sig2[c0 + i], chi2);
+      out_mask[c0 + i] = (uint8_t)in;
+      if (in) sel[ns++] = c0 + i;
+    }
+    out_inl[b] = ns;
+    cnt[C_RANSAC_INLIERS] += ns;
+    if (refit && ns >= 3) orc_horn(ns, sel, P1, P2, fix_scale, bestS);   /* A44 */
+    memcpy(out_S + 13 * (size_t)b, bestS, sizeof(bestS));
+    free(sel);
+  }
   return 0;
 }
 

@@ -634,3 +634,95 @@ def test_connections_symmetric_and_truncated():
     assert np.array_equal(W, W.T)
     n2, kf2, w2, _ = om.update_connections(None, th=1, max_edges=3)   # truncated rows
     assert np.array_equal(n2, n) and np.array_equal(kf2[:, :3], kf[:, :3])
+
+
+# ----------------------------------------------------------------------------
+# O13 Sim3 RANSAC (SPEC.md estimate_sim3_ransac examples;
+# DESIGN.md readings A41-A44)
+# ----------------------------------------------------------------------------
+def _sim3_yaw(s, yaw_deg, t):
+    a = np.deg2rad(yaw_deg)
+    R = np.array([[np.cos(a), -np.sin(a), 0], [np.sin(a), np.cos(a), 0], [0, 0, 1.0]])
+    return np.r_[R.reshape(-1), np.asarray(t, np.float64), s]
+
+
+def test_jacobi4_matches_library_eigh():
+    rng = np.random.default_rng(21)
+    for _ in range(200):
+        A = rng.standard_normal((4, 4))
+        A = A + A.T
+        ev, V = oracle.jacobi4(A)
+        ref = np.linalg.eigh(A)[0]
+        assert np.allclose(np.sort(ev), ref, rtol=1e-12, atol=1e-12)
+        assert np.allclose(A @ V, V * ev, atol=1e-10)            # columns are eigenvectors
+        assert np.allclose(V.T @ V, np.eye(4), atol=1e-12)
+
+
+def test_horn_closed_form_cases():
+    rng = np.random.default_rng(22)
+    P = rng.uniform(-2, 2, (50, 3)) + [0, 0, 5]
+    S = oracle.horn(P, P)                                          # identity
+    assert np.allclose(S, tm.IDENT, atol=1e-12)
+    T = _sim3_yaw(1.3, 10.0, (1, 2, 3))                            # SPEC: s=1.3, 10° yaw, t=(1,2,3)
+    P1 = np.array([oracle.sim3_apply(T, p) for p in P])
+    for n in (3, 50):
+        S = oracle.horn(P1[:n], P[:n])
+        assert np.allclose(S, T, atol=1e-9), (n, S - T)
+    T1 = _sim3_yaw(1.0, -35.0, (0.5, -1, 2))                       # rigid: fixed scale exact
+    P1 = np.array([oracle.sim3_apply(T1, p) for p in P])
+    assert np.allclose(oracle.horn(P1, P, fix_scale=True), T1, atol=1e-9)
+
+
+def _ransac_scene(rng, n=60, out_frac=0.3, T=None):
+    T = _sim3_yaw(1.3, 10.0, (0.3, -0.2, 0.1)) if T is None else T
+    Ti = oracle.sim3_inverse(T)
+    P1 = rng.uniform([-2, -2, 3], [2, 2, 8], (n, 3))               # camera-1 frame
+    P2 = np.array([oracle.sim3_apply(Ti, p) for p in P1])          # camera-2 frame
+    inl = np.ones(n, bool)
+    out = rng.choice(n, int(out_frac * n), replace=False)
+    inl[out] = False
+    P2[out] = rng.uniform([-2, -2, 3], [2, 2, 8], (len(out), 3))   # wrong partner
+    uv1 = np.array([oracle.project(tm.PIN, p) for p in P1])
+    uv2 = np.array([oracle.project(tm.PIN, p) for p in np.array([oracle.sim3_apply(Ti, p) for p in P1])])
+    return T, P1, P2, uv1.astype(np.float32), uv2.astype(np.float32), inl
+
+
+def _empty_map():
+    base = tm.desc_from_bits([])
+    return oracle.OracleMap(arrays=tm.build([dict(feats=[dict(u=1.0, v=1.0, desc=base)])],
+                                            [dict(pos=(0, 0, 1), desc=base)]), cams=[tm.PIN])
+
+
+def test_ransac_recovers_planted_model_and_inliers():
+    rng = np.random.default_rng(23)
+    om = _empty_map()
+    T, P1, P2, uv1, uv2, inl = _ransac_scene(rng)
+    n = len(P1)
+    samples = np.array([rng.choice(n, 3, replace=False) for _ in range(200)], np.int32)
+    S, ninl, mask, c = om.sim3_ransac([0, n], P1, P2, uv1, uv2, np.ones(n), np.ones(n), [0], [0],
+                                      samples[None], chi2=9.210)
+    assert np.array_equal(mask.astype(bool), inl)                  # exactly the constructed inliers
+    assert ninl[0] == inl.sum() and c["ransac_hyp"] == 200
+    assert np.allclose(S[0], T, atol=1e-6)
+    # outlier-free: every sample is exact, the first one wins
+    T, P1, P2, uv1, uv2, inl = _ransac_scene(rng, n=20, out_frac=0.0)
+    S, ninl, mask, c = om.sim3_ransac([0, 20], P1, P2, uv1, uv2, np.ones(20), np.ones(20), [0], [0],
+                                      np.array([[[0, 1, 2], [3, 4, 5]]], np.int32), refit=False)
+    assert ninl[0] == 20 and np.allclose(S[0], T, atol=1e-9)
+
+
+def test_ransac_degenerate_samples_and_batches():
+    rng = np.random.default_rng(24)
+    om = _empty_map()
+    T, P1, P2, uv1, uv2, inl = _ransac_scene(rng, n=12)
+    S, ninl, mask, c = om.sim3_ransac([0, 12], P1, P2, uv1, uv2, np.ones(12), np.ones(12), [0], [0],
+                                      np.array([[[1, 1, 2], [4, 5, 5]]], np.int32))
+    assert ninl[0] == 0 and c["ransac_hyp"] == 0 and not mask.any()   # A41: skipped
+    # two problems in one batch: each solved independently
+    T2, Q1, Q2, w1, w2, inl2 = _ransac_scene(rng, n=30, T=_sim3_yaw(0.8, -20.0, (1, 0, 0)))
+    smp = np.array([[rng.choice(12, 3, replace=False) for _ in range(50)],
+                    [rng.choice(30, 3, replace=False) for _ in range(50)]], np.int32)
+    S, ninl, mask, c = om.sim3_ransac([0, 12, 42], np.r_[P1, Q1], np.r_[P2, Q2], np.r_[uv1, w1],
+                                      np.r_[uv2, w2], np.ones(42), np.ones(42), [0, 0], [0, 0], smp)
+    assert np.array_equal(mask.astype(bool), np.r_[inl, inl2])
+    assert np.allclose(S[1], T2, atol=1e-6)
