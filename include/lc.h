@@ -190,6 +190,8 @@ enum {
   LC_COUNT_REFRESH_OBS,    /* refresh: observations visited                           */
   LC_COUNT_CONN_KF,        /* connections: keyframes recounted                        */
   LC_COUNT_CONN_EDGES,     /* connections: edges kept (before max_edges truncation)   */
+  LC_COUNT_RANSAC_HYP,     /* Sim3 RANSAC: hypotheses evaluated (valid samples)       */
+  LC_COUNT_RANSAC_INLIERS, /* Sim3 RANSAC: inliers of the selected models             */
   LC_NCOUNT
 };
 
@@ -229,7 +231,7 @@ int64_t lc_kernel_launches(const lc_ctx* ctx);
  * ------------------------------------------------------------------------- */
 enum { LC_PROF_UPLOAD = 0, LC_PROF_CORRECT_WINDOW, LC_PROF_CORRECT_ALL, LC_PROF_FUSE_PREP,
        LC_PROF_MATCH, LC_PROF_RESOLVE, LC_PROF_APPLY, LC_PROF_SBP_MATCH, LC_PROF_SBP_RESOLVE,
-       LC_PROF_STATE, LC_PROF_PROJECT, LC_PROF_REFRESH, LC_PROF_CONN, LC_NPROF };
+       LC_PROF_STATE, LC_PROF_PROJECT, LC_PROF_REFRESH, LC_PROF_CONN, LC_PROF_RANSAC, LC_NPROF };
 lc_status lc_profile_enable(lc_ctx* ctx, int32_t on);
 lc_status lc_profile_read(lc_ctx* ctx, double* ms, int64_t* launches);
 
@@ -276,6 +278,35 @@ lc_status lc_refresh_mappoints(lc_ctx* ctx, int32_t n, const int32_t* mp_idx, in
 lc_status lc_update_connections(lc_ctx* ctx, int32_t n, const int32_t* kf_idx, int32_t th,
                                 int32_t max_edges, int32_t* out_n, int32_t* out_kf,
                                 int32_t* out_w, int64_t* out_counts, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * lc_sim3_ransac -- batched Sim3 estimation of region detection (SURVEY.md §8(f)
+ * f3; "estimating the relative pose between the new keyframe and the
+ * matched one"; PAPER.md:200 hypotheses evaluated in parallel; DESIGN.md readings
+ * A41-A44). One problem per candidate keyframe pair b, correspondences
+ * [prob_begin[b], prob_begin[b+1]) (CSR):
+ *   P1, P2 [host|dev] [n_corr][3] fp64: the matched map points in camera-1 / camera-2
+ *     coordinates; uv1, uv2 [host|dev] [n_corr][2]: their keypoints; sigma2_1,
+ *     sigma2_2 [host|dev] [n_corr]: level variances; cam1, cam2 [host] [n_prob]:
+ *     camera indices of the uploaded cameras.
+ *   samples [host|dev] [n_prob][n_iter][3]: the RANSAC draws (indices local to the
+ *     problem; random numbers are inputs, A41); a sample with a repeated or
+ *     out-of-range index is skipped.
+ *   Per valid sample: S12 (p1 ~ s R p2 + t) by Horn's closed form (A42, fix_scale:
+ *   s = 1); inliers = correspondences whose reprojection errors in both images are
+ *   below chi2 * sigma^2 (A43). The selected model has the most inliers (first
+ *   iteration on ties); with refit != 0 it is re-estimated on all its inliers (A44).
+ *   out_S12 [host|dev] [n_prob] (all zero if no valid sample), out_inliers
+ *   [host|dev] [n_prob], out_mask [host|dev] [n_corr] (inliers of the selected
+ *   sample model); out_counts [LC_NCOUNT] (RANSAC_HYP, RANSAC_INLIERS).
+ * Errors: LC_EINVAL (bad sizes, camera index), LC_ESTATE (no map: cameras).
+ * ------------------------------------------------------------------------- */
+lc_status lc_sim3_ransac(lc_ctx* ctx, int32_t n_prob, const int32_t* prob_begin, const double* P1,
+                         const double* P2, const float* uv1, const float* uv2, const float* sigma2_1,
+                         const float* sigma2_2, const int32_t* cam1, const int32_t* cam2,
+                         const int32_t* samples, int32_t n_iter, double chi2, int32_t fix_scale,
+                         int32_t refit, lc_sim3* out_S12, int32_t* out_inliers, uint8_t* out_mask,
+                         int64_t* out_counts, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * CUDA-graph capture: one loop event (lc_correct_sim3 WINDOW -> lc_fuse ->

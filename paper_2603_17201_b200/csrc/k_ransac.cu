@@ -1,0 +1,277 @@
+// k_ransac.cu -- batched Sim3 RANSAC of region detection (
+// PAPER.md:89 "estimating the relative pose between the new keyframe and the matched
+// one", PAPER.md:200 (hypotheses evaluated in parallel); readings A41-A44;
+// include/lc.h lc_sim3_ransac).
+//
+// CTA per problem (hypothesis pair of keyframes), thread per RANSAC iteration: Horn's
+// closed-form similarity of the iteration's 3-point sample (centroids, cross-covariance,
+// Horn's 4x4 N, max-eigenvalue eigenvector by cyclic Jacobi, quaternion -> R, scale,
+// translation), then the symmetric reprojection inlier count over the problem's
+// correspondences (staged in shared memory). Block argmax of (inliers, -iteration),
+// inlier mask of the winner, optional refit on all inliers. Every fp64 expression is
+// written in the oracle's order (the build uses -fmad=false), so the models, counts
+// and masks are identical to oracle O13.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "lc_internal.cuh"
+
+namespace {
+
+constexpr int RCAP = 512;   // correspondences staged per problem
+
+__device__ void jacobi4(const double* A_in, double* ev, double* V) {
+  double A[16];
+  for (int i = 0; i < 16; ++i) { A[i] = A_in[i]; V[i] = (i % 5 == 0) ? 1.0 : 0.0; }
+  for (int sweep = 0; sweep < 50; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < 4; ++p)
+      for (int q = p + 1; q < 4; ++q) off = off + A[4 * p + q] * A[4 * p + q];
+    if (off <= 1e-300) break;
+    for (int p = 0; p < 4; ++p)
+      for (int q = p + 1; q < 4; ++q) {
+        const double apq = A[4 * p + q];
+        if (apq == 0.0) continue;
+        const double theta = (A[4 * q + q] - A[4 * p + p]) / (2.0 * apq);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < 4; ++k) {
+          const double akp = A[4 * k + p], akq = A[4 * k + q];
+          A[4 * k + p] = c * akp - sn * akq;
+          A[4 * k + q] = sn * akp + c * akq;
+        }
+        for (int k = 0; k < 4; ++k) {
+          const double apk = A[4 * p + k], aqk = A[4 * q + k];
+          A[4 * p + k] = c * apk - sn * aqk;
+          A[4 * q + k] = sn * apk + c * aqk;
+        }
+        for (int k = 0; k < 4; ++k) {
+          const double vkp = V[4 * k + p], vkq = V[4 * k + q];
+          V[4 * k + p] = c * vkp - sn * vkq;
+          V[4 * k + q] = sn * vkp + c * vkq;
+        }
+      }
+  }
+  for (int i = 0; i < 4; ++i) ev[i] = A[4 * i + i];
+}
+
+// Horn's similarity S12 (p1 ~ s R p2 + t) of the n correspondences idx[0..n) (A42)
+template <typename PtAt>
+__device__ void horn(int n, PtAt pt, int fix_scale, double* S) {
+  double c1[3] = {0, 0, 0}, c2[3] = {0, 0, 0};
+  for (int i = 0; i < n; ++i) {
+    const double* a = pt(i, 1);
+    const double* b = pt(i, 2);
+    for (int j = 0; j < 3; ++j) { c1[j] = c1[j] + a[j]; c2[j] = c2[j] + b[j]; }
+  }
+  for (int j = 0; j < 3; ++j) { c1[j] = c1[j] / (double)n; c2[j] = c2[j] / (double)n; }
+  double M[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < n; ++i) {
+    const double* pa = pt(i, 1);
+    const double* pb = pt(i, 2);
+    double a[3], b[3];
+    for (int j = 0; j < 3; ++j) { a[j] = pa[j] - c1[j]; b[j] = pb[j] - c2[j]; }
+    for (int r = 0; r < 3; ++r)
+      for (int cc = 0; cc < 3; ++cc) M[3 * r + cc] = M[3 * r + cc] + b[r] * a[cc];
+  }
+  double N[16];
+  N[0] = (M[0] + M[4]) + M[8];  N[1] = M[5] - M[7];          N[2] = M[6] - M[2];          N[3] = M[1] - M[3];
+  N[5] = (M[0] - M[4]) - M[8];  N[6] = M[1] + M[3];          N[7] = M[6] + M[2];
+  N[10] = (-M[0] + M[4]) - M[8]; N[11] = M[5] + M[7];
+  N[15] = (-M[0] - M[4]) + M[8];
+  N[4] = N[1]; N[8] = N[2]; N[12] = N[3]; N[9] = N[6]; N[13] = N[7]; N[14] = N[11];
+  double ev[4], V[16];
+  jacobi4(N, ev, V);
+  int best = 0;
+  for (int i = 1; i < 4; ++i) if (ev[i] > ev[best]) best = i;
+  double q[4] = {V[best], V[4 + best], V[8 + best], V[12 + best]};
+  int lead = 0;
+  while (lead < 3 && q[lead] == 0.0) ++lead;
+  if (q[lead] < 0.0) for (int i = 0; i < 4; ++i) q[i] = -q[i];
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  double R[9];
+  R[0] = ((w * w + x * x) - y * y) - z * z; R[1] = 2.0 * (x * y - w * z);         R[2] = 2.0 * (x * z + w * y);
+  R[3] = 2.0 * (x * y + w * z);         R[4] = ((w * w - x * x) + y * y) - z * z; R[5] = 2.0 * (y * z - w * x);
+  R[6] = 2.0 * (x * z - w * y);         R[7] = 2.0 * (y * z + w * x);         R[8] = ((w * w - x * x) - y * y) + z * z;
+  double nom = 0.0, den = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double* pa = pt(i, 1);
+    const double* pb = pt(i, 2);
+    double a[3], b[3], rb[3];
+    for (int j = 0; j < 3; ++j) { a[j] = pa[j] - c1[j]; b[j] = pb[j] - c2[j]; }
+    for (int j = 0; j < 3; ++j) rb[j] = lc_row3(R + 3 * j, b);
+    nom = nom + ((a[0] * rb[0] + a[1] * rb[1]) + a[2] * rb[2]);
+    den = den + ((rb[0] * rb[0] + rb[1] * rb[1]) + rb[2] * rb[2]);
+  }
+  const double sc = fix_scale ? 1.0 : nom / den;
+  for (int i = 0; i < 9; ++i) S[i] = R[i];
+  for (int j = 0; j < 3; ++j) S[9 + j] = c1[j] - sc * lc_row3(R + 3 * j, c2);
+  S[12] = sc;
+}
+
+struct RansacArgs {
+  int n_prob, n_iter, fix_scale, refit;
+  double chi2;
+  const int32_t* pbeg;
+  const double* P1;
+  const double* P2;
+  const float* uv1;
+  const float* uv2;
+  const float* sig1;
+  const float* sig2;
+  const int32_t* cam1;
+  const int32_t* cam2;
+  const int32_t* samples;
+  const DevCam* cams;
+  double* out_S;
+  int32_t* out_inl;
+  uint8_t* out_mask;
+  unsigned long long* counts;
+};
+
+// A43: both reprojection errors below chi2 * sigma^2; behind a camera = outlier
+__device__ __forceinline__ bool inlier(const DevCam& k1, const DevCam& k2, const double* S12,
+                                       const double* S21, const double* p1, const double* p2,
+                                       float2 u1, float2 u2, float s1, float s2, double chi2) {
+  double a[3], b[3], u, v;
+  lc_sim3_apply(S12, p2, a);
+  if (a[2] <= 0.0) return false;
+  lc_project(k1, a[0], a[1], a[2], u, v);
+  double du = u - (double)u1.x, dv = v - (double)u1.y;
+  if (!(du * du + dv * dv < chi2 * (double)s1)) return false;
+  lc_sim3_apply(S21, p1, b);
+  if (b[2] <= 0.0) return false;
+  lc_project(k2, b[0], b[1], b[2], u, v);
+  du = u - (double)u2.x; dv = v - (double)u2.y;
+  return du * du + dv * dv < chi2 * (double)s2;
+}
+
+__global__ void __launch_bounds__(LC_NTHREADS) k_ransac(const RansacArgs a) {
+  __shared__ double s_p1[RCAP][3], s_p2[RCAP][3];
+  __shared__ float2 s_u1[RCAP], s_u2[RCAP];
+  __shared__ float s_s1[RCAP], s_s2[RCAP];
+  __shared__ unsigned long long s_best;   // (inliers << 32) | (0xFFFFFFFF - iteration)
+  __shared__ double s_S[13];
+  __shared__ int32_t s_sel[RCAP];
+  __shared__ int s_ns;
+  __shared__ DevCam s_k1, s_k2;
+  const int tid = threadIdx.x;
+  uint32_t c_hyp = 0;
+  for (int b = blockIdx.x; b < a.n_prob; b += gridDim.x) {
+    const int c0 = a.pbeg[b], nc = a.pbeg[b + 1] - c0;
+    const bool staged = nc <= RCAP;
+    if (tid == 0) { s_best = 0ull; s_ns = 0; s_k1 = a.cams[a.cam1[b]]; s_k2 = a.cams[a.cam2[b]]; }
+    if (staged)
+      for (int i = tid; i < nc; i += blockDim.x) {
+        for (int j = 0; j < 3; ++j) { s_p1[i][j] = a.P1[3 * (size_t)(c0 + i) + j]; s_p2[i][j] = a.P2[3 * (size_t)(c0 + i) + j]; }
+        s_u1[i] = reinterpret_cast<const float2*>(a.uv1)[c0 + i];
+        s_u2[i] = reinterpret_cast<const float2*>(a.uv2)[c0 + i];
+        s_s1[i] = a.sig1[c0 + i];
+        s_s2[i] = a.sig2[c0 + i];
+      }
+    __syncthreads();
+    auto P = [&](int i, int side) -> const double* {
+      if (staged) return side == 1 ? s_p1[i] : s_p2[i];
+      return (side == 1 ? a.P1 : a.P2) + 3 * (size_t)(c0 + i);
+    };
+    auto U = [&](int i, int side) -> float2 {
+      if (staged) return side == 1 ? s_u1[i] : s_u2[i];
+      return reinterpret_cast<const float2*>(side == 1 ? a.uv1 : a.uv2)[c0 + i];
+    };
+    auto SG = [&](int i, int side) -> float {
+      if (staged) return side == 1 ? s_s1[i] : s_s2[i];
+      return (side == 1 ? a.sig1 : a.sig2)[c0 + i];
+    };
+    auto count = [&](const double* S, const double* Si) {
+      int n = 0;
+      for (int i = 0; i < nc; ++i)
+        n += inlier(s_k1, s_k2, S, Si, P(i, 1), P(i, 2), U(i, 1), U(i, 2), SG(i, 1), SG(i, 2), a.chi2);
+      return n;
+    };
+    // (1) hypotheses
+    for (int it = tid; it < a.n_iter; it += blockDim.x) {
+      const int32_t* t = a.samples + 3 * ((size_t)b * a.n_iter + it);
+      const int i0 = t[0], i1 = t[1], i2 = t[2];
+      if (i0 < 0 || i1 < 0 || i2 < 0 || i0 >= nc || i1 >= nc || i2 >= nc || i0 == i1 || i0 == i2 || i1 == i2)
+        continue;   // A41
+      const int sel[3] = {i0, i1, i2};
+      double S[13], Si[13];
+      horn(3, [&](int i, int side) { return P(sel[i], side); }, a.fix_scale, S);
+      lc_sim3_inverse(S, Si);
+      ++c_hyp;
+      const int n = count(S, Si);
+      atomicMax(&s_best, ((unsigned long long)(uint32_t)n << 32) | (0xFFFFFFFFull - (uint32_t)it));
+    }
+    __syncthreads();
+    const unsigned long long best = s_best;
+    const bool any = best != 0ull;
+    const int best_it = any ? (int)(0xFFFFFFFFull - (best & 0xFFFFFFFFull)) : -1;
+    // (2) the winner's model (recomputed by thread 0: the same expressions), mask, refit
+    if (tid == 0 && any) {
+      const int32_t* t = a.samples + 3 * ((size_t)b * a.n_iter + best_it);
+      const int sel[3] = {t[0], t[1], t[2]};
+      double S[13];
+      horn(3, [&](int i, int side) { return P(sel[i], side); }, a.fix_scale, S);
+      for (int i = 0; i < 13; ++i) s_S[i] = S[i];
+    }
+    __syncthreads();
+    if (!any) {
+      for (int i = tid; i < nc; i += blockDim.x) a.out_mask[c0 + i] = 0;
+      if (tid == 0) {
+        for (int i = 0; i < 13; ++i) a.out_S[13 * (size_t)b + i] = 0.0;
+        a.out_inl[b] = 0;
+      }
+      __syncthreads();
+      continue;
+    }
+    double S[13], Si[13];
+    for (int i = 0; i < 13; ++i) S[i] = s_S[i];
+    lc_sim3_inverse(S, Si);
+    for (int i = tid; i < nc; i += blockDim.x) {
+      const bool in = inlier(s_k1, s_k2, S, Si, P(i, 1), P(i, 2), U(i, 1), U(i, 2), SG(i, 1), SG(i, 2), a.chi2);
+      a.out_mask[c0 + i] = in ? 1 : 0;
+      if (in) atomicAdd(&s_ns, 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int ns = s_ns;
+      a.out_inl[b] = ns;
+      atomicAdd(&a.counts[LC_COUNT_RANSAC_INLIERS], (unsigned long long)ns);
+      if (a.refit && ns >= 3) {   // A44: Horn on all inliers, in index order
+        if (ns <= RCAP) {
+          int k = 0;
+          for (int i = 0; i < nc; ++i) if (a.out_mask[c0 + i]) s_sel[k++] = i;
+          horn(ns, [&](int i, int side) { return P(s_sel[i], side); }, a.fix_scale, S);
+        } else {   // many inliers: walk the mask for every access (same order, slower)
+          auto nth = [&](int r) { int k = -1; for (int i = 0; i < nc; ++i) if (a.out_mask[c0 + i] && ++k == r) return i; return 0; };
+          horn(ns, [&](int i, int side) { return P(nth(i), side); }, a.fix_scale, S);
+        }
+      }
+      for (int i = 0; i < 13; ++i) a.out_S[13 * (size_t)b + i] = S[i];
+    }
+    __syncthreads();
+  }
+  // hypotheses evaluated
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c_hyp += __shfl_down_sync(0xffffffffu, c_hyp, o);
+  if ((tid & 31) == 0 && c_hyp) atomicAdd(&a.counts[LC_COUNT_RANSAC_HYP], (unsigned long long)c_hyp);
+}
+
+}  // namespace
+
+cudaError_t launch_ransac(lc_ctx* c, int n_prob, const int32_t* d_pbeg, const double* P1, const double* P2,
+                          const float* uv1, const float* uv2, const float* sig1, const float* sig2,
+                          const int32_t* d_cam1, const int32_t* d_cam2, const int32_t* samples, int n_iter,
+                          double chi2, int fix_scale, int refit, double* out_S, int32_t* out_inl,
+                          uint8_t* out_mask, unsigned long long* counts, cudaStream_t s) {
+  if (n_prob <= 0) return cudaSuccess;
+  RansacArgs a;
+  a.n_prob = n_prob; a.n_iter = n_iter; a.fix_scale = fix_scale; a.refit = refit; a.chi2 = chi2;
+  a.pbeg = d_pbeg; a.P1 = P1; a.P2 = P2; a.uv1 = uv1; a.uv2 = uv2; a.sig1 = sig1; a.sig2 = sig2;
+  a.cam1 = d_cam1; a.cam2 = d_cam2; a.samples = samples; a.cams = c->st.cams;
+  a.out_S = out_S; a.out_inl = out_inl; a.out_mask = out_mask; a.counts = counts;
+  k_ransac<<<std::min(n_prob, 148 * 8), LC_NTHREADS, 0, s>>>(a);
+  c->launches++;
+  return cudaGetLastError();
+}
