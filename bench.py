@@ -429,7 +429,7 @@ def main():
 
     # secondary: SURVEY §8 a9, batched read-only guided search on C4 (32 hypotheses x
     # (current KF + 3 covisible) pairs, PS2a / PS2b / PS1-3 parameter sets)
-    sbp = None
+    sbp = ransac = None
     if ws == 1 and not args.profile_only and not args.no_sbp:
         from lcsynth.world import SBP_PARAMS
         w4 = make_world("C4", args.seed)
@@ -454,6 +454,36 @@ def main():
         c4cnt = r4["counts"].sum(0).cpu().numpy()
         cand4 = int(c4cnt[counts.index("candidates")])
         s_ms = float(np.mean(sms))
+        # batched Sim3 RANSAC of the 32 hypotheses (150 3D-3D
+        # correspondences each, 30% outliers, 300 iterations, chi2 9.21)
+        rng = np.random.default_rng(args.seed)
+        nb, nper, nit = 32, 150, 300
+        P1 = rng.uniform([-1.5, -1.5, 3], [1.5, 1.5, 8], (nb * nper, 3))
+        P2 = P1 + rng.normal(0, 0.002, P1.shape)
+        out = rng.random(nb * nper) < 0.3
+        P2[out] = rng.uniform([-1.5, -1.5, 3], [1.5, 1.5, 8], (int(out.sum()), 3))
+        cam = w4.cam.as_dict() if hasattr(w4.cam, "as_dict") else dict(w4.cam)
+        U1 = np.stack([cam["fx"] * P1[:, 0] / P1[:, 2] + cam["cx"], cam["fy"] * P1[:, 1] / P1[:, 2] + cam["cy"]], 1)
+        U2 = U1.copy()
+        pbeg = (np.arange(nb + 1) * nper).astype(np.int32)
+        smp = rng.integers(0, nper, (nb, nit, 3)).astype(np.int32)
+        ones = np.ones(nb * nper, np.float32)
+        cz = np.zeros(nb, np.int32)
+        rt = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in
+              (P1, P2, U1.astype(np.float32), U2.astype(np.float32), ones, ones, smp)]
+        rms = []
+        for i in range(args.warmup + args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            rr = c4.sim3_ransac(pbeg, *rt[:6], cz, cz, rt[6], host=False)
+            b.record(stream)
+            b.synchronize()
+            if i >= args.warmup:
+                rms.append(a.elapsed_time(b))
+        rc4 = rr[3].cpu().numpy()
+        ransac = {"problems": nb, "correspondences": nb * nper, "iterations": nit,
+                  "hypotheses": int(rc4[counts.index("ransac_hyp")]),
+                  "ms_per_call": round(float(np.mean(rms)), 5)}
         sbp = {"config": f"C4: {len(w4.pair_kf)} (hypothesis, keyframe) pairs, "
                          f"{len(w4.pair_mp_list)} queries, 3 parameter sets",
                "ms_per_call": round(s_ms, 5), "candidates": cand4,
@@ -490,6 +520,7 @@ def main():
             "sbp": sbp,
             "refresh": refresh,
             "connections": connections,
+            "ransac": ransac,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
