@@ -78,6 +78,17 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait2() {   // all but the 2 newest groups
+  asm volatile("cp.async.wait_group 2;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t done = 0;
   while (!done) {
@@ -225,33 +236,43 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
   const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
   Surv* out = a.surv + a.surv_off[blk];
   uint32_t cA = 0, cB = 0, cQ = 0;   // packed 10-bit counters (<= 64 queries per thread per block)
-  // software pipeline: the record of the next query and the list entry of the one
-  // after are in flight while the current query is evaluated
+  // software pipeline: the 32-B record (geometry sector) of the query two steps ahead
+  // is copied by cp.async into a per-thread 3-slot ring behind the hash (no registers
+  // held), its flag and the list entry three steps ahead are in flight in registers
+  uint4* s_rec = reinterpret_cast<uint4*>(s_hash + HS);   // [3][LC_NTHREADS][2]
   auto list_at = [&](int64_t jj) -> int32_t { return jj < q1 ? __ldg(a.mp_list + jj) : -1; };
-  auto rec_at = [&](int32_t qq, uint4& x0, uint4& x1, uint8_t& fl) {
+  auto flag_at = [&](int32_t qq) -> uint8_t {
+    return (unsigned)qq < (unsigned)a.n_mp ? __ldg(a.mp_flags + qq) : (uint8_t)1;
+  };
+  auto issue = [&](int32_t qq, int slot) {
     if ((unsigned)qq < (unsigned)a.n_mp) {
       const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + qq);
-      x0 = __ldg(rp); x1 = __ldg(rp + 1); fl = __ldg(a.mp_flags + qq);
-    } else {
-      x0 = make_uint4(0, 0, 0, 0); x1 = x0; fl = 1;
+      uint4* d = s_rec + 2 * (slot * LC_NTHREADS + tid);
+      cp_async16(d, rp);
+      cp_async16(d + 1, rp + 1);
     }
+    cp_async_commit();   // one group per step, empty or not
   };
-  int32_t q_nx = list_at(q0 + tid);
-  int32_t q_nn = list_at(q0 + tid + LC_NTHREADS);
-  uint4 n0, n1;
-  uint8_t nfl;
-  rec_at(q_nx, n0, n1, nfl);
-  for (int64_t jb = q0; jb < q1; jb += LC_NTHREADS) {
+  int32_t qa = list_at(q0 + tid), qb = list_at(q0 + tid + LC_NTHREADS);
+  int32_t qc = list_at(q0 + tid + 2 * LC_NTHREADS);
+  uint8_t fa = flag_at(qa), fbl = flag_at(qb);
+  issue(qa, 0);
+  issue(qb, 1);
+  int slot = 0;
+  for (int64_t jb = q0; jb < q1; jb += LC_NTHREADS, slot = slot == 2 ? 0 : slot + 1) {
     const int64_t j = jb + tid;
     const bool valid = j < q1;
-    const int32_t q = q_nx;
-    const uint4 r0 = n0, r1 = n1;
-    const uint8_t flag = nfl;
+    const int32_t q = qa;
+    const uint8_t flag = fa;
+    issue(qc, slot == 0 ? 2 : slot - 1);   // slot of step + 2
+    const uint8_t fc = flag_at(qc);
+    const int32_t qd = list_at(j + 3 * LC_NTHREADS);
+    cp_async_wait2();                      // this step's record is in
+    const uint4 r0 = s_rec[2 * (slot * LC_NTHREADS + tid)];
+    const uint4 r1 = s_rec[2 * (slot * LC_NTHREADS + tid) + 1];
+    qa = qb; fa = fbl; qb = qc; fbl = fc; qc = qd;
     const bool in_range = valid && (unsigned)q < (unsigned)a.n_mp;
     if (a.loop_ep_w && in_range) a.loop_ep_w[q] = epoch;   // LoopSet stamp (pipelined mode)
-    q_nx = q_nn;
-    q_nn = list_at(j + 2 * LC_NTHREADS);
-    rec_at(q_nx, n0, n1, nfl);
     int status = 0;
     double u = 0.0, v = 0.0;
     int lvl = 0;
@@ -347,13 +368,6 @@ struct MatchSmem {
   static constexpr int QUEUE = META + ((FCAP * 4 + 15) & ~15);
   static constexpr int CELL = QUEUE + NWARP * WB;   // runtime-size cell table last
 };
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
-}
 
 // exact fp64 (u, v) of a survivor: the same expressions as k_project (same bits)
 __device__ __noinline__ void exact_uv(const MatchArgs& a, const double* T, const DevCam& cam,
@@ -1023,7 +1037,7 @@ cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, int part, bool pdl,
     return cudaGetLastError();
   };
   if (part == 0) {
-    const int hb = HashSize<FCAP>::HS * (int)sizeof(int32_t);
+    const int hb = HashSize<FCAP>::HS * (int)sizeof(int32_t) + 3 * LC_NTHREADS * 32;   // hash + record ring
     cudaError_t e = cudaFuncSetAttribute(k_project<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, hb);
     if (e != cudaSuccess) return e;
     return go(k_project<MODE, FCAP>, (size_t)hb);
