@@ -23,6 +23,7 @@ COUNTER_NAMES = [
     "winners", "orient_rej", "add", "victim_prop", "loop_skip", "bad_slot",
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
     "refresh_mp", "refresh_obs", "conn_kf", "conn_edges", "ransac_hyp", "ransac_inliers",
+    "refine_iters", "refine_inliers",
 ]
 NONE64 = np.iinfo(np.int64).max
 
@@ -81,7 +82,7 @@ def lib():
         _lib.orc_predict_level.restype = C.c_int
         _lib.orc_predict_level.argtypes = [C.c_double, C.c_double, C.c_void_p, C.c_int32]
         for fn in ("orc_correct_window", "orc_correct_all", "orc_fuse", "orc_search_by_projection",
-                   "orc_refresh", "orc_update_connections", "orc_sim3_ransac"):
+                   "orc_refresh", "orc_update_connections", "orc_sim3_ransac", "orc_sim3_refine"):
             getattr(_lib, fn).restype = C.c_int
     return _lib
 
@@ -163,6 +164,14 @@ def horn(P1, P2, fix_scale=False):
     S = np.zeros(13, np.float64)
     lib().orc_horn(C.c_int32(len(P1)), _p(sel), _p(P1), _p(P2), C.c_int32(int(fix_scale)), _p(S))
     return S
+
+
+def sim3_retract(d, S):
+    """S <- (Cayley(w), tau, 1 + sig) o S for d = (w, tau, sig) (A45)."""
+    out = np.zeros(13, np.float64)
+    lib().orc_sim3_retract(_p(np.ascontiguousarray(d, np.float64)), _p(np.ascontiguousarray(S, np.float64)),
+                           _p(out))
+    return out
 
 
 def scale_table(L=8, f=1.2):
@@ -370,4 +379,28 @@ class OracleMap:
                               _p(uv2), _p(sig1), _p(sig2), _p(cam1), _p(cam2), _p(smp), C.c_int32(n_iter),
                               C.c_double(chi2), C.c_int32(int(fix_scale)), C.c_int32(int(refit)), _p(S),
                               _p(inl), _p(mask), _p(cnt))
+        return S, inl, mask, dict(zip(COUNTER_NAMES, cnt.tolist()))
+
+    # -- O14 -----------------------------------------------------------------
+    def sim3_refine(self, prob_begin, P1, P2, uv1, uv2, sig1, sig2, cam1, cam2, S_init, max_iter=10,
+                    th2=10.0, lam=1e-6):
+        """Gauss-Newton Sim3 refinement: (S [n_prob, 13], inliers [n_prob], mask [n_corr], counts)."""
+        pb = np.ascontiguousarray(prob_begin, np.int32)
+        n_prob = len(pb) - 1
+        P1 = np.ascontiguousarray(P1, np.float64).reshape(-1, 3)
+        P2 = np.ascontiguousarray(P2, np.float64).reshape(-1, 3)
+        uv1 = np.ascontiguousarray(uv1, np.float32).reshape(-1, 2)
+        uv2 = np.ascontiguousarray(uv2, np.float32).reshape(-1, 2)
+        sig1 = np.ascontiguousarray(sig1, np.float32)
+        sig2 = np.ascontiguousarray(sig2, np.float32)
+        cam1 = np.ascontiguousarray(cam1, np.int32)
+        cam2 = np.ascontiguousarray(cam2, np.int32)
+        S0 = np.ascontiguousarray(S_init, np.float64).reshape(n_prob, 13)
+        S = np.zeros((n_prob, 13), np.float64)
+        inl = np.zeros(n_prob, np.int32)
+        mask = np.zeros(len(P1), np.uint8)
+        cnt = np.zeros(len(COUNTER_NAMES), np.int64)
+        lib().orc_sim3_refine(C.byref(self._m), C.c_int32(n_prob), _p(pb), _p(P1), _p(P2), _p(uv1), _p(uv2),
+                              _p(sig1), _p(sig2), _p(cam1), _p(cam2), _p(S0), C.c_int32(max_iter),
+                              C.c_double(th2), C.c_double(lam), _p(S), _p(inl), _p(mask), _p(cnt))
         return S, inl, mask, dict(zip(COUNTER_NAMES, cnt.tolist()))

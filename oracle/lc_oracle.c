@@ -31,6 +31,8 @@
  *     closed-form Horn similarity, symmetric reprojection inlier test ("estimating
  *     the relative pose between the new keyframe and the matched one", PAPER.md:89;
  *     SURVEY.md §8(f) f3, readings A41-A44)                     -> orc_sim3_ransac (O13)
+ *   - its Gauss-Newton Sim3 refinement with a Huber kernel (SPEC.md refine_sim3;
+ *     readings A45-A48)                                        -> orc_sim3_refine (O14)
  * The paper gives no matching math (SURVEY.md §0 "Key finding"); every
  * constant and tie-break is a DESIGN.md reading (A1-A32), noted inline.
  *
@@ -55,7 +57,8 @@ enum {
   C_CULL_ANGLE, C_CANDIDATES, C_NO_CAND, C_OVER_TH, C_RATIO_REJ, C_PROPOSALS,
   C_WINNERS, C_ORIENT_REJ, C_ADD, C_VICTIM_PROP, C_LOOP_SKIP, C_BAD_SLOT,
   C_VICTIMS, C_REWIRED, C_DUP_CLEARED, C_ADDED, C_CORR_KF, C_CORR_MP,
-  C_REFRESH_MP, C_REFRESH_OBS, C_CONN_KF, C_CONN_EDGES, C_RANSAC_HYP, C_RANSAC_INLIERS, C_N
+  C_REFRESH_MP, C_REFRESH_OBS, C_CONN_KF, C_CONN_EDGES, C_RANSAC_HYP, C_RANSAC_INLIERS,
+  C_REFINE_ITERS, C_REFINE_INLIERS, C_N
 };
 
 /* query status codes written to out_status (negative = culled/skipped) */
@@ -989,6 +992,187 @@ int orc_sim3_ransac(const orc_map *m, int32_t n_prob, const int32_t *pbeg, const
     if (refit && ns >= 3) orc_horn(ns, sel, P1, P2, fix_scale, bestS);   /* A44 */
     memcpy(out_S + 13 * (size_t)b, bestS, sizeof(bestS));
     free(sel);
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O14 Sim3 refinement (readings A45-A48).                */
+/* ------------------------------------------------------------------------- */
+/* A45: retraction S <- D(d) o S, D(d) = (Cayley(w), tau, 1 + sig) for the      */
+/* 7-vector d = (w0..2, tau0..2, sig): Cayley(w) = (I - [w]x)^-1 (I + [w]x) in  */
+/* closed form (rational: identical in any IEEE implementation).              */
+void orc_sim3_retract(const double *d, const double *S, double *out) {
+  const double a = d[0], b = d[1], c = d[2];
+  const double n2 = (a * a + b * b) + c * c;
+  const double k = 1.0 / (1.0 + n2);
+  double D[13];
+  D[0] = ((1.0 + a * a) - b * b - c * c) * k;  D[1] = 2.0 * (a * b - c) * k;          D[2] = 2.0 * (a * c + b) * k;
+  D[3] = 2.0 * (a * b + c) * k;          D[4] = ((1.0 - a * a) + b * b - c * c) * k;  D[5] = 2.0 * (b * c - a) * k;
+  D[6] = 2.0 * (a * c - b) * k;          D[7] = 2.0 * (b * c + a) * k;          D[8] = ((1.0 - a * a) - b * b + c * c) * k;
+  D[9] = d[3]; D[10] = d[4]; D[11] = d[5]; D[12] = 1.0 + d[6];
+  orc_sim3_compose(D, S, out);
+}
+
+/* residuals of correspondence i under S (S21 = inverse(S)): r[0..1] = pi1(S p2) - uv1,
+ * r[2..3] = pi2(S21 p1) - uv2; returns 0 if a point is behind a camera */
+static int refine_res(const orc_camera *k1, const orc_camera *k2, const double *S, const double *p1,
+                      const double *p2, const float *uv1, const float *uv2, double *r) {
+  double Si[13], a[3], b[3], uv[2];
+  orc_sim3_inverse(S, Si);
+  orc_sim3_apply(S, p2, a);
+  orc_sim3_apply(Si, p1, b);
+  if (a[2] <= 0.0 || b[2] <= 0.0) return 0;
+  orc_project(k1, a, uv);
+  r[0] = uv[0] - (double)uv1[0]; r[1] = uv[1] - (double)uv1[1];
+  orc_project(k2, b, uv);
+  r[2] = uv[0] - (double)uv2[0]; r[3] = uv[1] - (double)uv2[1];
+  return 1;
+}
+
+/* Huber weight of a chi2 value e2 = |r|^2 / sigma2 (A47): 1 if sqrt(e2) <= delta,
+ * else delta / sqrt(e2) */
+static double huber_w(double e2, double delta) {
+  const double e = sqrt(e2);
+  return e <= delta ? 1.0 : delta / e;
+}
+
+/* A46/A47: Gauss-Newton with central-difference Jacobians (h = 1e-6), Huber-weighted
+ * normal equations accumulated in correspondence order, H + lambda*diag(H) solved by
+ * the 7x7 Cholesky in fixed order; stop when |d|^2 < 1e-20 or after max_iter; A48:
+ * inliers = both chi2 < th2 under the final model. Correspondences behind a camera
+ * at the current model contribute nothing. */
+/* chi2 of both residuals of correspondence i under S; 0 if behind a camera */
+static int refine_chi2(const orc_camera *k1, const orc_camera *k2, const double *S, const double *p1,
+                       const double *p2, const float *u1, const float *u2, float s1, float s2,
+                       double *e1, double *e2) {
+  double r[4];
+  if (!refine_res(k1, k2, S, p1, p2, u1, u2, r)) return 0;
+  *e1 = (r[0] * r[0] + r[1] * r[1]) / (double)s1;
+  *e2 = (r[2] * r[2] + r[3] * r[3]) / (double)s2;
+  return 1;
+}
+
+/* one Gauss-Newton step over the active correspondences; returns 0 if H is not SPD */
+static int refine_step(const orc_camera *k1, const orc_camera *k2, int32_t c0, int32_t nc,
+                       const uint8_t *act, const double *P1, const double *P2, const float *uv1,
+                       const float *uv2, const float *sig1, const float *sig2, double delta,
+                       double lambda, double *S, double *dn_out) {
+  const double h = 1e-6;
+  double H[49], g[7];
+  for (int i = 0; i < 49; ++i) H[i] = 0.0;
+  for (int i = 0; i < 7; ++i) g[i] = 0.0;
+  for (int32_t i = 0; i < nc; ++i) {
+    if (!act[i]) continue;
+    const double *p1 = P1 + 3 * (size_t)(c0 + i), *p2 = P2 + 3 * (size_t)(c0 + i);
+    const float *u1 = uv1 + 2 * (size_t)(c0 + i), *u2 = uv2 + 2 * (size_t)(c0 + i);
+    double r[4], J[4][7];
+    if (!refine_res(k1, k2, S, p1, p2, u1, u2, r)) continue;
+    int ok = 1;
+    for (int j = 0; j < 7 && ok; ++j) {
+      double dp[7] = {0, 0, 0, 0, 0, 0, 0}, dm[7] = {0, 0, 0, 0, 0, 0, 0};
+      dp[j] = h; dm[j] = -h;
+      double Sp[13], Sm[13], rp[4], rm[4];
+      orc_sim3_retract(dp, S, Sp);
+      orc_sim3_retract(dm, S, Sm);
+      ok = refine_res(k1, k2, Sp, p1, p2, u1, u2, rp) && refine_res(k1, k2, Sm, p1, p2, u1, u2, rm);
+      for (int q = 0; q < 4; ++q) J[q][j] = (rp[q] - rm[q]) / (2.0 * h);
+    }
+    if (!ok) continue;
+    const double s1 = (double)sig1[c0 + i], s2 = (double)sig2[c0 + i];
+    const double e1 = (r[0] * r[0] + r[1] * r[1]) / s1, e2 = (r[2] * r[2] + r[3] * r[3]) / s2;
+    const double w1 = huber_w(e1, delta) / s1, w2 = huber_w(e2, delta) / s2;
+    for (int q = 0; q < 4; ++q) {
+      const double wq = q < 2 ? w1 : w2;
+      for (int x = 0; x < 7; ++x) {
+        g[x] = g[x] + wq * J[q][x] * r[q];
+        for (int y = 0; y <= x; ++y) H[7 * x + y] = H[7 * x + y] + wq * J[q][x] * J[q][y];
+      }
+    }
+  }
+  double L[49];   /* Cholesky of H + lambda * diag(H) (lower), then H d = -g */
+  for (int x = 0; x < 7; ++x)
+    for (int y = 0; y <= x; ++y) L[7 * x + y] = H[7 * x + y] + (x == y ? lambda * H[7 * x + x] : 0.0);
+  for (int x = 0; x < 7; ++x)
+    for (int y = 0; y <= x; ++y) {
+      double acc = L[7 * x + y];
+      for (int k = 0; k < y; ++k) acc = acc - L[7 * x + k] * L[7 * y + k];
+      if (x == y) {
+        if (!(acc > 0.0)) return 0;
+        L[7 * x + x] = sqrt(acc);
+      } else {
+        L[7 * x + y] = acc / L[7 * y + y];
+      }
+    }
+  double z[7], d[7];
+  for (int x = 0; x < 7; ++x) {
+    double acc = -g[x];
+    for (int k = 0; k < x; ++k) acc = acc - L[7 * x + k] * z[k];
+    z[x] = acc / L[7 * x + x];
+  }
+  for (int x = 6; x >= 0; --x) {
+    double acc = z[x];
+    for (int k = x + 1; k < 7; ++k) acc = acc - L[7 * k + x] * d[k];
+    d[x] = acc / L[7 * x + x];
+  }
+  double S2[13];
+  orc_sim3_retract(d, S, S2);
+  memcpy(S, S2, sizeof(S2));
+  double dn = 0.0;
+  for (int x = 0; x < 7; ++x) dn = dn + d[x] * d[x];
+  *dn_out = dn;
+  return 1;
+}
+
+/* A46-A48: Gauss-Newton with central-difference Jacobians (h = 1e-6) and Huber
+ * weights (delta = sqrt(th2)), normal equations accumulated in correspondence order,
+ * H + lambda diag(H) solved by the fixed-order 7x7 Cholesky; phase 1 (<= 5 steps) on
+ * all correspondences, then those with a chi2 >= th2 (or behind a camera) are dropped
+ * (EXT OptimizeSim3), phase 2 (<= max_iter steps) on the rest; a phase stops when
+ * |d|^2 < 1e-20 or H is not positive definite. Inliers: both chi2 < th2 under the
+ * final model. */
+int orc_sim3_refine(const orc_map *m, int32_t n_prob, const int32_t *pbeg, const double *P1,
+                    const double *P2, const float *uv1, const float *uv2, const float *sig1,
+                    const float *sig2, const int32_t *cam1, const int32_t *cam2, const double *S_in,
+                    int32_t max_iter, double th2, double lambda, double *out_S, int32_t *out_inl,
+                    uint8_t *out_mask, int64_t *cnt) {
+  const double delta = sqrt(th2);
+  for (int32_t b = 0; b < n_prob; ++b) {
+    const int32_t c0 = pbeg[b], nc = pbeg[b + 1] - pbeg[b];
+    const orc_camera *k1 = m->cams + cam1[b], *k2 = m->cams + cam2[b];
+    double S[13];
+    memcpy(S, S_in + 13 * (size_t)b, sizeof(S));
+    uint8_t *act = (uint8_t *)malloc((size_t)(nc > 0 ? nc : 1));
+    for (int32_t i = 0; i < nc; ++i) act[i] = 1;
+    for (int phase = 0; phase < 2; ++phase) {
+      const int32_t n_it = phase == 0 ? (max_iter < 5 ? max_iter : 5) : max_iter;
+      for (int32_t it = 0; it < n_it; ++it) {
+        double dn = 0.0;
+        if (!refine_step(k1, k2, c0, nc, act, P1, P2, uv1, uv2, sig1, sig2, delta, lambda, S, &dn)) break;
+        cnt[C_REFINE_ITERS]++;
+        if (dn < 1e-20) break;
+      }
+      if (phase == 0)
+        for (int32_t i = 0; i < nc; ++i) {
+          double e1, e2;
+          act[i] = refine_chi2(k1, k2, S, P1 + 3 * (size_t)(c0 + i), P2 + 3 * (size_t)(c0 + i),
+                               uv1 + 2 * (size_t)(c0 + i), uv2 + 2 * (size_t)(c0 + i), sig1[c0 + i],
+                               sig2[c0 + i], &e1, &e2) && e1 < th2 && e2 < th2;
+        }
+    }
+    int32_t ninl = 0;
+    for (int32_t i = 0; i < nc; ++i) {
+      double e1, e2;
+      const int in = refine_chi2(k1, k2, S, P1 + 3 * (size_t)(c0 + i), P2 + 3 * (size_t)(c0 + i),
+                                 uv1 + 2 * (size_t)(c0 + i), uv2 + 2 * (size_t)(c0 + i), sig1[c0 + i],
+                                 sig2[c0 + i], &e1, &e2) && e1 < th2 && e2 < th2;
+      out_mask[c0 + i] = (uint8_t)in;
+      ninl += in;
+    }
+    out_inl[b] = ninl;
+    cnt[C_REFINE_INLIERS] += ninl;
+    memcpy(out_S + 13 * (size_t)b, S, sizeof(S));
+    free(act);
   }
   return 0;
 }

@@ -726,3 +726,41 @@ def test_ransac_degenerate_samples_and_batches():
                                       np.r_[uv2, w2], np.ones(42), np.ones(42), [0, 0], [0, 0], smp)
     assert np.array_equal(mask.astype(bool), np.r_[inl, inl2])
     assert np.allclose(S[1], T2, atol=1e-6)
+
+
+# ----------------------------------------------------------------------------
+# O14 Sim3 refinement (SPEC.md refine_sim3; readings A45-A48)
+# ----------------------------------------------------------------------------
+def test_retraction_closed_forms():
+    rng = np.random.default_rng(41)
+    S = tm.random_sim3(rng)
+    assert np.array_equal(oracle.sim3_retract(np.zeros(7), S), oracle.sim3_compose(tm.IDENT, S))
+    for _ in range(50):
+        w = rng.normal(0, 0.5, 3)
+        d = np.r_[w, rng.normal(0, 1, 3), rng.uniform(-0.5, 0.5)]
+        D = oracle.sim3_retract(d, tm.IDENT)
+        R = D[:9].reshape(3, 3)
+        assert np.allclose(R @ R.T, np.eye(3), atol=1e-14) and np.linalg.det(R) > 0
+        ang = np.arccos(np.clip((np.trace(R) - 1) / 2, -1, 1))     # Cayley: angle = 2 atan |w|
+        assert abs(ang - 2 * np.arctan(np.linalg.norm(w))) < 1e-12
+        assert np.allclose(R @ w, w, atol=1e-14)                     # about the axis w
+        assert np.allclose(D[9:12], d[3:6]) and D[12] == 1.0 + d[6]
+
+
+def test_refine_fixed_point_convergence_and_outliers():
+    rng = np.random.default_rng(42)
+    om = _empty_map()
+    T, P1, P2, uv1, uv2, inl = _ransac_scene(rng, n=80, out_frac=0.0)
+    ones = np.ones(80)
+    S, ninl, mask, c = om.sim3_refine([0, 80], P1, P2, uv1, uv2, ones, ones, [0], [0], T[None])
+    # the truth is a fixed point up to the fp32 rounding of the keypoints (~1e-7)
+    assert np.allclose(S[0], T, atol=1e-6) and ninl[0] == 80
+    S0 = oracle.sim3_retract(np.r_[0.01, -0.02, 0.005, 0.05, -0.03, 0.02, 0.02], T)
+    S, ninl, mask, c = om.sim3_refine([0, 80], P1, P2, uv1, uv2, ones, ones, [0], [0], S0[None], max_iter=30)
+    assert np.allclose(S[0], T, atol=1e-6) and ninl[0] == 80 and c["refine_iters"] >= 2
+    # 25% far outliers: Huber keeps the estimate at the truth, the mask is the planted one
+    T, P1, P2, uv1, uv2, inl = _ransac_scene(rng, n=80, out_frac=0.25)
+    S0 = oracle.sim3_retract(np.r_[0.005, 0.0, -0.005, 0.02, 0.0, 0.01, 0.01], T)
+    S, ninl, mask, c = om.sim3_refine([0, 80], P1, P2, uv1, uv2, ones, ones, [0], [0], S0[None], max_iter=30)
+    assert np.allclose(S[0], T, atol=1e-5), S[0] - T
+    assert np.array_equal(mask.astype(bool), inl)
