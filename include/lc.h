@@ -192,6 +192,8 @@ enum {
   LC_COUNT_CONN_EDGES,     /* connections: edges kept (before max_edges truncation)   */
   LC_COUNT_RANSAC_HYP,     /* Sim3 RANSAC: hypotheses evaluated (valid samples)       */
   LC_COUNT_RANSAC_INLIERS, /* Sim3 RANSAC: inliers of the selected models             */
+  LC_COUNT_REFINE_ITERS,   /* Sim3 refinement: Gauss-Newton steps taken              */
+  LC_COUNT_REFINE_INLIERS, /* Sim3 refinement: inliers under the refined models      */
   LC_NCOUNT
 };
 
@@ -231,7 +233,8 @@ int64_t lc_kernel_launches(const lc_ctx* ctx);
  * ------------------------------------------------------------------------- */
 enum { LC_PROF_UPLOAD = 0, LC_PROF_CORRECT_WINDOW, LC_PROF_CORRECT_ALL, LC_PROF_FUSE_PREP,
        LC_PROF_MATCH, LC_PROF_RESOLVE, LC_PROF_APPLY, LC_PROF_SBP_MATCH, LC_PROF_SBP_RESOLVE,
-       LC_PROF_STATE, LC_PROF_PROJECT, LC_PROF_REFRESH, LC_PROF_CONN, LC_PROF_RANSAC, LC_NPROF };
+       LC_PROF_STATE, LC_PROF_PROJECT, LC_PROF_REFRESH, LC_PROF_CONN, LC_PROF_RANSAC, LC_PROF_REFINE,
+       LC_NPROF };
 lc_status lc_profile_enable(lc_ctx* ctx, int32_t on);
 lc_status lc_profile_read(lc_ctx* ctx, double* ms, int64_t* launches);
 
@@ -307,6 +310,26 @@ lc_status lc_sim3_ransac(lc_ctx* ctx, int32_t n_prob, const int32_t* prob_begin,
                          const int32_t* samples, int32_t n_iter, double chi2, int32_t fix_scale,
                          int32_t refit, lc_sim3* out_S12, int32_t* out_inliers, uint8_t* out_mask,
                          int64_t* out_counts, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * lc_sim3_refine -- Sim3 refinement of region detection (
+ * SPEC.md refine_sim3; readings A45-A48): Gauss-Newton on the same
+ * problems and correspondence arrays as lc_sim3_ransac, from S_init [host|dev]
+ * [n_prob] (e.g. its output). Update S <- (Cayley(w), tau, 1 + sig) o S (A45),
+ * central-difference Jacobians (h = 1e-6, A46), Huber weights with delta =
+ * sqrt(th2) on each image's chi2, H + lambda diag(H) solved by Cholesky (A47);
+ * phase 1 (<= 5 steps) on all correspondences, then those with a chi2 >= th2 are
+ * dropped, phase 2 (<= max_iter steps) on the rest (EXT OptimizeSim3); a phase ends
+ * when |d|^2 < 1e-20 or H is not positive definite. out_S [n_prob], out_inliers,
+ * out_mask: both chi2 < th2 under the final model (A48). out_counts (REFINE_ITERS,
+ * REFINE_INLIERS). Errors as lc_sim3_ransac.
+ * ------------------------------------------------------------------------- */
+lc_status lc_sim3_refine(lc_ctx* ctx, int32_t n_prob, const int32_t* prob_begin, const double* P1,
+                         const double* P2, const float* uv1, const float* uv2, const float* sigma2_1,
+                         const float* sigma2_2, const int32_t* cam1, const int32_t* cam2,
+                         const lc_sim3* S_init, int32_t max_iter, double th2, double lambda,
+                         lc_sim3* out_S, int32_t* out_inliers, uint8_t* out_mask, int64_t* out_counts,
+                         void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * CUDA-graph capture: one loop event (lc_correct_sim3 WINDOW -> lc_fuse ->

@@ -24,10 +24,11 @@ COUNTER_NAMES = [
     "winners", "orient_rej", "add", "victim_prop", "loop_skip", "bad_slot",
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
     "refresh_mp", "refresh_obs", "conn_kf", "conn_edges", "ransac_hyp", "ransac_inliers",
+    "refine_iters", "refine_inliers",
 ]
 LC_NCOUNT = len(COUNTER_NAMES)
 PROF_NAMES = ["upload", "correct_window", "correct_all", "fuse_prep", "match", "resolve", "apply",
-              "sbp_match", "sbp_resolve", "state", "project", "refresh", "conn", "ransac"]
+              "sbp_match", "sbp_resolve", "state", "project", "refresh", "conn", "ransac", "refine"]
 
 
 class lc_sim3(C.Structure):
@@ -109,6 +110,8 @@ def load():
         "lc_update_connections": (i32, [vp, i32, vp, i32, i32, vp, vp, vp, vp, vp]),
         "lc_sim3_ransac": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, C.c_double, i32,
                                  i32, vp, vp, vp, vp, vp]),
+        "lc_sim3_refine": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, C.c_double,
+                                 C.c_double, vp, vp, vp, vp, vp]),
         "lc_graph_begin": (i32, [vp, vp]),
         "lc_graph_end": (i32, [vp, vp, P(vp)]),
         "lc_graph_launch": (i32, [vp, vp, vp]),
@@ -126,5 +129,5 @@ def exported_symbols():
     return ["lc_create", "lc_destroy", "lc_last_error", "lc_kernel_launches", "lc_profile_enable",
             "lc_profile_read", "lc_upload_map",
             "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse",
-            "lc_search_by_projection", "lc_refresh_mappoints", "lc_update_connections", "lc_sim3_ransac", "lc_graph_begin", "lc_graph_end", "lc_graph_launch",
+            "lc_search_by_projection", "lc_refresh_mappoints", "lc_update_connections", "lc_sim3_ransac", "lc_sim3_refine", "lc_graph_begin", "lc_graph_end", "lc_graph_launch",
             "lc_graph_destroy"]

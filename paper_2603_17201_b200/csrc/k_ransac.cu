@@ -258,7 +258,238 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_ransac(const RansacArgs a) {
   if ((tid & 31) == 0 && c_hyp) atomicAdd(&a.counts[LC_COUNT_RANSAC_HYP], (unsigned long long)c_hyp);
 }
 
+// ---------------------------------------------------------------------------
+// Sim3 refinement (readings A45-A48): Gauss-Newton with central-difference Jacobians,
+// Huber weights, outlier removal between the two phases. Per step: threads compute
+// each correspondence's residuals / Jacobians / weights into shared memory (chunks
+// of RCH), then 35 threads -- one per entry of H (lower 28) and g (7) -- accumulate in
+// the oracle's (correspondence, residual) order, so every sum, the fixed-order 7x7
+// Cholesky (thread 0) and the retraction are the oracle's bits.
+// ---------------------------------------------------------------------------
+constexpr int RCH = 64;
+
+__device__ __forceinline__ void retract(const double* d, const double* S, double* out) {   // A45
+  const double a = d[0], b = d[1], c = d[2];
+  const double n2 = (a * a + b * b) + c * c;
+  const double k = 1.0 / (1.0 + n2);
+  double D[13];
+  D[0] = ((1.0 + a * a) - b * b - c * c) * k;  D[1] = 2.0 * (a * b - c) * k;          D[2] = 2.0 * (a * c + b) * k;
+  D[3] = 2.0 * (a * b + c) * k;          D[4] = ((1.0 - a * a) + b * b - c * c) * k;  D[5] = 2.0 * (b * c - a) * k;
+  D[6] = 2.0 * (a * c - b) * k;          D[7] = 2.0 * (b * c + a) * k;          D[8] = ((1.0 - a * a) - b * b + c * c) * k;
+  D[9] = d[3]; D[10] = d[4]; D[11] = d[5]; D[12] = 1.0 + d[6];
+  lc_sim3_compose(D, S, out);
+}
+
+__device__ __forceinline__ bool residuals(const DevCam& k1, const DevCam& k2, const double* S, const double* p1,
+                                          const double* p2, float2 u1, float2 u2, double* r) {
+  double Si[13], a[3], b[3], u, v;
+  lc_sim3_inverse(S, Si);
+  lc_sim3_apply(S, p2, a);
+  lc_sim3_apply(Si, p1, b);
+  if (a[2] <= 0.0 || b[2] <= 0.0) return false;
+  lc_project(k1, a[0], a[1], a[2], u, v);
+  r[0] = u - (double)u1.x; r[1] = v - (double)u1.y;
+  lc_project(k2, b[0], b[1], b[2], u, v);
+  r[2] = u - (double)u2.x; r[3] = v - (double)u2.y;
+  return true;
+}
+
+__device__ __forceinline__ double huber_w(double e2, double delta) {
+  const double e = sqrt(e2);
+  return e <= delta ? 1.0 : delta / e;
+}
+
+struct RefineArgs {
+  int n_prob, max_iter;
+  double th2, lambda;
+  const int32_t* pbeg;
+  const double* P1;
+  const double* P2;
+  const float* uv1;
+  const float* uv2;
+  const float* sig1;
+  const float* sig2;
+  const int32_t* cam1;
+  const int32_t* cam2;
+  const double* S_in;
+  const DevCam* cams;
+  double* out_S;
+  int32_t* out_inl;
+  uint8_t* out_mask;   // also the active flags during the refinement
+  unsigned long long* counts;
+};
+
+__global__ void __launch_bounds__(LC_NTHREADS) k_refine(const RefineArgs a) {
+  __shared__ double s_J[RCH][4][7], s_r[RCH][4], s_w[RCH][2];
+  __shared__ uint8_t s_ok[RCH];
+  __shared__ double s_H[49], s_g[7], s_S[13], s_dn;
+  __shared__ int s_spd, s_ninl;
+  __shared__ DevCam s_k1, s_k2;
+  const int tid = threadIdx.x;
+  const double delta = sqrt(a.th2), h = 1e-6;
+  uint32_t c_it = 0, c_inl = 0;
+  for (int b = blockIdx.x; b < a.n_prob; b += gridDim.x) {
+    const int c0 = a.pbeg[b], nc = a.pbeg[b + 1] - c0;
+    if (tid == 0) {
+      for (int i = 0; i < 13; ++i) s_S[i] = a.S_in[13 * (size_t)b + i];
+      s_k1 = a.cams[a.cam1[b]];
+      s_k2 = a.cams[a.cam2[b]];
+      s_ninl = 0;
+    }
+    for (int i = tid; i < nc; i += blockDim.x) a.out_mask[c0 + i] = 1;   // active
+    __syncthreads();
+    auto P = [&](int i, int side) { return (side == 1 ? a.P1 : a.P2) + 3 * (size_t)(c0 + i); };
+    auto U = [&](int i, int side) { return reinterpret_cast<const float2*>(side == 1 ? a.uv1 : a.uv2)[c0 + i]; };
+    auto chi2 = [&](const double* S, int i, double& e1, double& e2) -> bool {
+      double r[4];
+      if (!residuals(s_k1, s_k2, S, P(i, 1), P(i, 2), U(i, 1), U(i, 2), r)) return false;
+      e1 = (r[0] * r[0] + r[1] * r[1]) / (double)a.sig1[c0 + i];
+      e2 = (r[2] * r[2] + r[3] * r[3]) / (double)a.sig2[c0 + i];
+      return true;
+    };
+    for (int phase = 0; phase < 2; ++phase) {
+      const int n_it = phase == 0 ? min(a.max_iter, 5) : a.max_iter;
+      for (int it = 0; it < n_it; ++it) {
+        double S[13];
+        for (int i = 0; i < 13; ++i) S[i] = s_S[i];
+        if (tid < 49) s_H[tid] = 0.0;
+        if (tid < 7) s_g[tid] = 0.0;
+        __syncthreads();
+        for (int ch = 0; ch < nc; ch += RCH) {
+          const int n = min(RCH, nc - ch);
+          for (int l = tid; l < n; l += blockDim.x) {   // per correspondence, in parallel
+            const int i = ch + l;
+            bool ok = a.out_mask[c0 + i] != 0;
+            double r[4];
+            ok = ok && residuals(s_k1, s_k2, S, P(i, 1), P(i, 2), U(i, 1), U(i, 2), r);
+            for (int j = 0; j < 7 && ok; ++j) {
+              double dp[7] = {0, 0, 0, 0, 0, 0, 0}, dm[7] = {0, 0, 0, 0, 0, 0, 0};
+              dp[j] = h; dm[j] = -h;
+              double Sp[13], Sm[13], rp[4], rm[4];
+              retract(dp, S, Sp);
+              retract(dm, S, Sm);
+              ok = residuals(s_k1, s_k2, Sp, P(i, 1), P(i, 2), U(i, 1), U(i, 2), rp) &&
+                   residuals(s_k1, s_k2, Sm, P(i, 1), P(i, 2), U(i, 1), U(i, 2), rm);
+              for (int q = 0; q < 4; ++q) s_J[l][q][j] = (rp[q] - rm[q]) / (2.0 * h);
+            }
+            s_ok[l] = ok ? 1 : 0;
+            if (ok) {
+              const double s1 = (double)a.sig1[c0 + i], s2 = (double)a.sig2[c0 + i];
+              const double e1 = (r[0] * r[0] + r[1] * r[1]) / s1, e2 = (r[2] * r[2] + r[3] * r[3]) / s2;
+              for (int q = 0; q < 4; ++q) s_r[l][q] = r[q];
+              s_w[l][0] = huber_w(e1, delta) / s1;
+              s_w[l][1] = huber_w(e2, delta) / s2;
+            }
+          }
+          __syncthreads();
+          if (tid < 35) {   // one entry per thread, accumulated in (correspondence, residual) order
+            int x, y;
+            if (tid < 28) { x = 0; while ((x + 1) * (x + 2) / 2 <= tid) ++x; y = tid - x * (x + 1) / 2; }
+            else { x = tid - 28; y = -1; }
+            double acc = y >= 0 ? s_H[7 * x + y] : s_g[x];
+            for (int l = 0; l < n; ++l) {
+              if (!s_ok[l]) continue;
+              for (int q = 0; q < 4; ++q) {
+                const double wq = q < 2 ? s_w[l][0] : s_w[l][1];
+                if (y >= 0) acc = acc + wq * s_J[l][q][x] * s_J[l][q][y];
+                else acc = acc + wq * s_J[l][q][x] * s_r[l][q];
+              }
+            }
+            if (y >= 0) s_H[7 * x + y] = acc; else s_g[x] = acc;
+          }
+          __syncthreads();
+        }
+        if (tid == 0) {   // H + lambda diag(H) = L L^T, H d = -g, S <- retract(d) S
+          double L[49];
+          for (int x = 0; x < 7; ++x)
+            for (int y = 0; y <= x; ++y) L[7 * x + y] = s_H[7 * x + y] + (x == y ? a.lambda * s_H[7 * x + x] : 0.0);
+          int spd = 1;
+          for (int x = 0; x < 7 && spd; ++x)
+            for (int y = 0; y <= x; ++y) {
+              double acc = L[7 * x + y];
+              for (int k = 0; k < y; ++k) acc = acc - L[7 * x + k] * L[7 * y + k];
+              if (x == y) {
+                if (!(acc > 0.0)) { spd = 0; break; }
+                L[7 * x + x] = sqrt(acc);
+              } else {
+                L[7 * x + y] = acc / L[7 * y + y];
+              }
+            }
+          s_spd = spd;
+          if (spd) {
+            double z[7], d[7];
+            for (int x = 0; x < 7; ++x) {
+              double acc = -s_g[x];
+              for (int k = 0; k < x; ++k) acc = acc - L[7 * x + k] * z[k];
+              z[x] = acc / L[7 * x + x];
+            }
+            for (int x = 6; x >= 0; --x) {
+              double acc = z[x];
+              for (int k = x + 1; k < 7; ++k) acc = acc - L[7 * k + x] * d[k];
+              d[x] = acc / L[7 * x + x];
+            }
+            double S2[13];
+            retract(d, S, S2);
+            for (int i = 0; i < 13; ++i) s_S[i] = S2[i];
+            double dn = 0.0;
+            for (int x = 0; x < 7; ++x) dn = dn + d[x] * d[x];
+            s_dn = dn;
+            ++c_it;
+          }
+        }
+        __syncthreads();
+        if (!s_spd || s_dn < 1e-20) break;
+      }
+      if (phase == 0) {   // drop correspondences with a chi2 >= th2 (EXT OptimizeSim3)
+        double S[13];
+        for (int i = 0; i < 13; ++i) S[i] = s_S[i];
+        for (int i = tid; i < nc; i += blockDim.x) {
+          double e1, e2;
+          const bool in = chi2(S, i, e1, e2) && e1 < a.th2 && e2 < a.th2;
+          a.out_mask[c0 + i] = in ? 1 : 0;
+        }
+        __syncthreads();
+      }
+    }
+    double S[13];
+    for (int i = 0; i < 13; ++i) S[i] = s_S[i];
+    for (int i = tid; i < nc; i += blockDim.x) {
+      double e1, e2;
+      const bool in = chi2(S, i, e1, e2) && e1 < a.th2 && e2 < a.th2;
+      a.out_mask[c0 + i] = in ? 1 : 0;
+      if (in) atomicAdd(&s_ninl, 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      a.out_inl[b] = s_ninl;
+      c_inl += (uint32_t)s_ninl;
+      for (int i = 0; i < 13; ++i) a.out_S[13 * (size_t)b + i] = s_S[i];
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && (c_it || c_inl)) {
+    atomicAdd(&a.counts[LC_COUNT_REFINE_ITERS], (unsigned long long)c_it);
+    atomicAdd(&a.counts[LC_COUNT_REFINE_INLIERS], (unsigned long long)c_inl);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_refine(lc_ctx* c, int n_prob, const int32_t* d_pbeg, const double* P1, const double* P2,
+                          const float* uv1, const float* uv2, const float* sig1, const float* sig2,
+                          const int32_t* d_cam1, const int32_t* d_cam2, const double* S_in, int max_iter,
+                          double th2, double lambda, double* out_S, int32_t* out_inl, uint8_t* out_mask,
+                          unsigned long long* counts, cudaStream_t s) {
+  if (n_prob <= 0) return cudaSuccess;
+  RefineArgs a;
+  a.n_prob = n_prob; a.max_iter = max_iter; a.th2 = th2; a.lambda = lambda;
+  a.pbeg = d_pbeg; a.P1 = P1; a.P2 = P2; a.uv1 = uv1; a.uv2 = uv2; a.sig1 = sig1; a.sig2 = sig2;
+  a.cam1 = d_cam1; a.cam2 = d_cam2; a.S_in = S_in; a.cams = c->st.cams;
+  a.out_S = out_S; a.out_inl = out_inl; a.out_mask = out_mask; a.counts = counts;
+  k_refine<<<std::min(n_prob, 148 * 8), LC_NTHREADS, 0, s>>>(a);
+  c->launches++;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_ransac(lc_ctx* c, int n_prob, const int32_t* d_pbeg, const double* P1, const double* P2,
                           const float* uv1, const float* uv2, const float* sig1, const float* sig2,

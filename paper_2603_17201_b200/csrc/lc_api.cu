@@ -834,6 +834,59 @@ lc_status lc_sim3_ransac(lc_ctx* c, int32_t n_prob, const int32_t* prob_begin, c
   });
 }
 
+lc_status lc_sim3_refine(lc_ctx* c, int32_t n_prob, const int32_t* prob_begin, const double* P1,
+                         const double* P2, const float* uv1, const float* uv2, const float* sigma2_1,
+                         const float* sigma2_2, const int32_t* cam1, const int32_t* cam2,
+                         const lc_sim3* S_init, int32_t max_iter, double th2, double lambda,
+                         lc_sim3* out_S, int32_t* out_inliers, uint8_t* out_mask, int64_t* out_counts,
+                         void* stream) {
+  return guarded(c, [&] {
+    capture_gate(c, stream, true);
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded (cameras)");
+    REQUIRE(n_prob >= 0 && max_iter >= 0 && th2 > 0.0 && lambda >= 0.0, LC_EINVAL, "bad sizes / parameters");
+    REQUIRE(n_prob == 0 || (prob_begin && cam1 && cam2 && S_init && out_S && out_inliers), LC_EINVAL,
+            "null argument");
+    Call call(c, stream);
+    int64_t n_corr = 0;
+    if (n_prob > 0) {
+      REQUIRE(prob_begin[0] == 0, LC_EINVAL, "prob_begin[0] must be 0");
+      for (int b = 0; b < n_prob; ++b) {
+        REQUIRE(prob_begin[b + 1] >= prob_begin[b], LC_EINVAL, "prob_begin not monotone");
+        REQUIRE(cam1[b] >= 0 && cam1[b] < c->st.n_cams && cam2[b] >= 0 && cam2[b] < c->st.n_cams, LC_EINVAL,
+                "camera index out of range");
+      }
+      n_corr = prob_begin[n_prob];
+      REQUIRE(n_corr == 0 || (P1 && P2 && uv1 && uv2 && sigma2_1 && sigma2_2 && out_mask), LC_EINVAL,
+              "null correspondence array");
+    }
+    const int32_t *d_pb = nullptr, *d_c1 = nullptr, *d_c2 = nullptr;
+    if (n_prob > 0) {
+      call.arg(prob_begin, (size_t)n_prob + 1, &d_pb);
+      call.arg(cam1, (size_t)n_prob, &d_c1);
+      call.arg(cam2, (size_t)n_prob, &d_c2);
+      call.commit();
+    }
+    const double* dP1 = call.in(P1, 3 * (size_t)n_corr);
+    const double* dP2 = call.in(P2, 3 * (size_t)n_corr);
+    const float* du1 = call.in(uv1, 2 * (size_t)n_corr);
+    const float* du2 = call.in(uv2, 2 * (size_t)n_corr);
+    const float* ds1 = call.in(sigma2_1, (size_t)n_corr);
+    const float* ds2 = call.in(sigma2_2, (size_t)n_corr);
+    const double* dS0 = call.in((const double*)S_init, 13 * (size_t)n_prob);
+    double* dS = (double*)call.out((double*)out_S, 13 * (size_t)n_prob);
+    int32_t* dI = call.out(out_inliers, (size_t)n_prob);
+    uint8_t* dM = call.out(out_mask, (size_t)n_corr);
+    unsigned long long* cnt = call.counts(out_counts, LC_NCOUNT);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
+    {
+      Prof pr(c, LC_PROF_REFINE, call.s);
+      CK(launch_refine(c, n_prob, d_pb, dP1, dP2, du1, du2, ds1, ds2, d_c1, d_c2, dS0, max_iter, th2, lambda,
+                       dS, dI, dM, cnt, call.s));
+    }
+    call.finish();
+  });
+}
+
 lc_status lc_state_save(lc_ctx* c, void* stream) {
   return guarded(c, [&] {
     capture_gate(c, stream, false);

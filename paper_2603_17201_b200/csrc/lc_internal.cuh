@@ -348,6 +348,11 @@ cudaError_t launch_obs_lists(lc_ctx* c, int32_t* d_obeg, int32_t* d_cursor, int3
                              int32_t* d_obs, int32_t* d_obs_kf, cudaStream_t s);   // per-point observation lists
 int obs_scan_blocks(int n_mp);
 int connections_max_kf();
+cudaError_t launch_refine(lc_ctx* c, int n_prob, const int32_t* d_pbeg, const double* P1, const double* P2,
+                          const float* uv1, const float* uv2, const float* sig1, const float* sig2,
+                          const int32_t* d_cam1, const int32_t* d_cam2, const double* S_in, int max_iter,
+                          double th2, double lambda, double* out_S, int32_t* out_inl, uint8_t* out_mask,
+                          unsigned long long* counts, cudaStream_t s);
 cudaError_t launch_ransac(lc_ctx* c, int n_prob, const int32_t* d_pbeg, const double* P1, const double* P2,
                           const float* uv1, const float* uv2, const float* sig1, const float* sig2,
                           const int32_t* d_cam1, const int32_t* d_cam2, const int32_t* samples, int n_iter,

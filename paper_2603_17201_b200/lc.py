@@ -329,6 +329,34 @@ class Context:
             return S, inl, mask, counts_dict(cnt)
         return S.view(n_prob, 13), inl, mask, cnt
 
+    def sim3_refine(self, prob_begin, P1, P2, uv1, uv2, sig1, sig2, cam1, cam2, S_init, max_iter=10,
+                    th2=10.0, lam=1e-6, host=True):
+        """Gauss-Newton Sim3 refinement: (S [n_prob, 13], inliers [n_prob], mask [n_corr], counts)."""
+        k = self._keep(host)
+        pb = np.ascontiguousarray(prob_begin, np.int32)
+        n_prob = len(pb) - 1
+        n_corr = int(pb[-1]) if n_prob > 0 else 0
+        if host:
+            S = np.zeros((n_prob, 13), np.float64)
+            inl = np.zeros(n_prob, np.int32)
+            mask = np.zeros(n_corr, np.uint8)
+            cnt = np.zeros(LC_NCOUNT, np.int64)
+        else:
+            S = self._dev(n_prob * 13, torch.float64)
+            inl = self._dev(n_prob, torch.int32)
+            mask = self._dev(n_corr, torch.uint8)
+            cnt = self._dev(LC_NCOUNT, torch.int64)
+        st = self.lib.lc_sim3_refine(self.h, n_prob, k.ptr(pb), k.ptr(P1, np.float64), k.ptr(P2, np.float64),
+                                     k.ptr(uv1, np.float32), k.ptr(uv2, np.float32), k.ptr(sig1, np.float32),
+                                     k.ptr(sig2, np.float32), k.ptr(cam1, np.int32), k.ptr(cam2, np.int32),
+                                     k.ptr(S_init, np.float64), int(max_iter), float(th2), float(lam),
+                                     k.ptr(S), k.ptr(inl), k.ptr(mask), k.ptr(cnt), self._stream())
+        self._check("lc_sim3_refine", st)
+        if host:
+            self.synchronize()
+            return S, inl, mask, counts_dict(cnt)
+        return S.view(n_prob, 13), inl, mask, cnt
+
     # -- lc_correct_sim3 ----------------------------------------------------------
     def correct_window(self, cur_kf, S_cw_corr, window, host=True):
         k = self._keep(host)

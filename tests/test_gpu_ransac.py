@@ -72,3 +72,33 @@ def test_ransac_batch_matches_oracle(Ctx, world, refit):
     assert g[1][3] == 0 and not g[0][3].any()
     good = [b for b in range(n_prob) if b != 3 and g[1][b] >= 10]
     assert len(good) > n_prob // 2
+
+
+@pytest.mark.parametrize("world", ["T1", "T2"], ids=["pinhole", "kannala-brandt"])
+def test_refine_batch_matches_oracle(Ctx, world):
+    """Gauss-Newton Sim3 refinement (lc_sim3_refine, readings A45-A48) against oracle O14
+    from the RANSAC models: pinhole is rational arithmetic -> bit-identical; the
+    Kannala-Brandt projection uses atan2 (libm vs CUDA may differ by <= 2 ulp) -> models
+    within 1e-9, same masks and counters."""
+    w = make_world(world, 0)
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    om = oracle.OracleMap(w)
+    rng = np.random.default_rng(32)
+    pb, P1, P2, U1, U2, S1, S2, smp, truth = _batch(rng, w.cam, n_prob=16, big=(600,))
+    cams = np.zeros(len(pb) - 1, np.int32)
+    S0 = om.sim3_ransac(pb, P1, P2, U1, U2, S1, S2, cams, cams, smp)[0]
+    ok = np.abs(S0).sum(1) > 0
+    g = ctx.sim3_refine(pb, P1, P2, U1, U2, S1, S2, cams, cams, S0, max_iter=10)
+    o = om.sim3_refine(pb, P1, P2, U1, U2, S1, S2, cams, cams, S0, max_iter=10)
+    assert np.array_equal(g[1], o[1]) and np.array_equal(g[2], o[2])
+    assert g[3]["refine_inliers"] == o[3]["refine_inliers"]
+    if world == "T1":
+        assert g[3]["refine_iters"] == o[3]["refine_iters"]
+        assert np.array_equal(g[0][ok], o[0][ok])
+    else:   # the |d|^2 < 1e-20 stop sits at the ulp level: at most one step apart per problem
+        assert abs(g[3]["refine_iters"] - o[3]["refine_iters"]) <= len(pb) - 1
+        assert np.allclose(g[0][ok], o[0][ok], rtol=1e-8, atol=1e-9)   # one last step (|d| < 1e-10) apart
+    # the refinement does not lose inliers against the RANSAC models
+    r = om.sim3_ransac(pb, P1, P2, U1, U2, S1, S2, cams, cams, smp)[1]
+    assert np.all(g[1][ok] >= r[ok] - 2)
