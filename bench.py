@@ -481,9 +481,21 @@ def main():
             if i >= args.warmup:
                 rms.append(a.elapsed_time(b))
         rc4 = rr[3].cpu().numpy()
+        fms = []
+        for i in range(args.warmup + args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            rf = c4.sim3_refine(pbeg, *rt[:6], cz, cz, rr[0], max_iter=10, host=False)
+            b.record(stream)
+            b.synchronize()
+            if i >= args.warmup:
+                fms.append(a.elapsed_time(b))
+        rf4 = rf[3].cpu().numpy()
         ransac = {"problems": nb, "correspondences": nb * nper, "iterations": nit,
                   "hypotheses": int(rc4[counts.index("ransac_hyp")]),
-                  "ms_per_call": round(float(np.mean(rms)), 5)}
+                  "ms_per_call": round(float(np.mean(rms)), 5),
+                  "refine_ms_per_call": round(float(np.mean(fms)), 5),
+                  "refine_steps": int(rf4[counts.index("refine_iters")])}
         sbp = {"config": f"C4: {len(w4.pair_kf)} (hypothesis, keyframe) pairs, "
                          f"{len(w4.pair_mp_list)} queries, 3 parameter sets",
                "ms_per_call": round(s_ms, 5), "candidates": cand4,
