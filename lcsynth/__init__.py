@@ -6,3 +6,4 @@ or the CUDA library, and neither of those imports it. Random numbers the method
 would draw do not exist (the method is deterministic).
 """
 from .world import CAMERAS, CONFIGS, World, make_world  # noqa: F401
+from .posegraph import GRAPHS, PoseGraph, make_pose_graph  # noqa: F401

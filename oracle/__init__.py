@@ -23,7 +23,7 @@ COUNTER_NAMES = [
     "winners", "orient_rej", "add", "victim_prop", "loop_skip", "bad_slot",
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
     "refresh_mp", "refresh_obs", "conn_kf", "conn_edges", "ransac_hyp", "ransac_inliers",
-    "refine_iters", "refine_inliers",
+    "refine_iters", "refine_inliers", "pgo_iters", "pgo_accepted", "pgo_solver_iters", "pgo_stop",
 ]
 NONE64 = np.iinfo(np.int64).max
 
@@ -82,7 +82,7 @@ def lib():
         _lib.orc_predict_level.restype = C.c_int
         _lib.orc_predict_level.argtypes = [C.c_double, C.c_double, C.c_void_p, C.c_int32]
         for fn in ("orc_correct_window", "orc_correct_all", "orc_fuse", "orc_search_by_projection",
-                   "orc_refresh", "orc_update_connections", "orc_sim3_ransac", "orc_sim3_refine"):
+                   "orc_refresh", "orc_update_connections", "orc_sim3_ransac", "orc_sim3_refine", "orc_pgo"):
             getattr(_lib, fn).restype = C.c_int
     return _lib
 
@@ -404,3 +404,57 @@ class OracleMap:
                               _p(sig1), _p(sig2), _p(cam1), _p(cam2), _p(S0), C.c_int32(max_iter),
                               C.c_double(th2), C.c_double(lam), _p(S), _p(inl), _p(mask), _p(cnt))
         return S, inl, mask, dict(zip(COUNTER_NAMES, cnt.tolist()))
+
+
+# ----------------------------------------------------------------------------
+# O15: essential-graph Sim3 pose-graph optimisation (readings A49-A53)
+# ----------------------------------------------------------------------------
+class _PgoParams(C.Structure):
+    _fields_ = [("max_iter", C.c_int32), ("cg_max_iter", C.c_int32), ("lambda0", C.c_double),
+                ("eps_dx", C.c_double), ("eps_chi2", C.c_double), ("cg_tol", C.c_double)]
+
+
+PGO_STOP = {1: "dx", 2: "chi2", 3: "max_iter", 4: "lambda", 5: "zero"}
+
+
+def pgo_exp(x):
+    """Sim3 exponential of x = (omega, upsilon, sigma) (A49)."""
+    out = np.zeros(13, np.float64)
+    lib().orc_pgo_exp(_p(np.ascontiguousarray(x, np.float64)), _p(out))
+    return out
+
+
+def pgo_log(S):
+    """Sim3 logarithm (A49): (omega, upsilon, sigma)."""
+    out = np.zeros(7, np.float64)
+    lib().orc_pgo_log(_p(np.ascontiguousarray(S, np.float64)), _p(out))
+    return out
+
+
+def pgo_edge(M, Si, Sj):
+    """Residual e = log(M o S_i o S_j^-1) and its dual-number Jacobians (A50):
+    (e [7], J_i [7, 7], J_j [7, 7]), J[r, k] = d e_r / d delta_k."""
+    e = np.zeros(7, np.float64)
+    Ji = np.zeros((7, 7), np.float64)
+    Jj = np.zeros((7, 7), np.float64)
+    lib().orc_pgo_edge(*[_p(np.ascontiguousarray(a, np.float64)) for a in (M, Si, Sj)], _p(e), _p(Ji), _p(Jj))
+    return e, Ji, Jj
+
+
+def pgo(S_init, fixed, edges, M, max_iter=20, lambda0=1e-4, eps_dx=1e-8, eps_chi2=1e-10):
+    """Levenberg-Marquardt essential-graph optimisation with dense LDL^T (A51-A53).
+    Returns (S [n_v, 13], trace [iters, 6], (chi2_0, chi2_final), counts)."""
+    S0 = np.ascontiguousarray(S_init, np.float64).reshape(-1, 13)
+    n_v = len(S0)
+    fx = np.ascontiguousarray(fixed, np.uint8)
+    E = np.ascontiguousarray(edges, np.int32).reshape(-1, 2)
+    Mm = np.ascontiguousarray(M, np.float64).reshape(-1, 13)
+    prm = _PgoParams(int(max_iter), 0, float(lambda0), float(eps_dx), float(eps_chi2), 0.0)
+    S = np.zeros((n_v, 13), np.float64)
+    tr = np.zeros((max(int(max_iter), 1), 6), np.float64)
+    c2 = np.zeros(2, np.float64)
+    cnt = np.zeros(len(COUNTER_NAMES), np.int64)
+    lib().orc_pgo(C.c_int32(n_v), _p(S0), _p(fx), C.c_int32(len(E)), _p(E), _p(Mm), C.byref(prm), _p(S),
+                  _p(tr), _p(c2), _p(cnt))
+    cd = dict(zip(COUNTER_NAMES, cnt.tolist()))
+    return S, tr[:cd["pgo_iters"]], (float(c2[0]), float(c2[1])), cd

@@ -33,6 +33,11 @@
  *     SURVEY.md §8(f) f3, readings A41-A44)                     -> orc_sim3_ransac (O13)
  *   - its Gauss-Newton Sim3 refinement with a Huber kernel (SPEC.md refine_sim3;
  *     readings A45-A48)                                        -> orc_sim3_refine (O14)
+ *   - Essential-graph Sim3 pose-graph optimisation: Levenberg-Marquardt with
+ *     automatic-differentiation Jacobians and an LDLT linear solve ("we use
+ *     automatic differentiation", "Eigen LDLT for the linear solver",
+ *     PAPER.md:244-248 §IV.F, readings A49-A53)
+ *                                                               -> orc_pgo (O15)
  * The paper gives no matching math (SURVEY.md §0 "Key finding"); every
  * constant and tie-break is a DESIGN.md reading (A1-A32), noted inline.
  *
@@ -58,7 +63,8 @@ enum {
   C_WINNERS, C_ORIENT_REJ, C_ADD, C_VICTIM_PROP, C_LOOP_SKIP, C_BAD_SLOT,
   C_VICTIMS, C_REWIRED, C_DUP_CLEARED, C_ADDED, C_CORR_KF, C_CORR_MP,
   C_REFRESH_MP, C_REFRESH_OBS, C_CONN_KF, C_CONN_EDGES, C_RANSAC_HYP, C_RANSAC_INLIERS,
-  C_REFINE_ITERS, C_REFINE_INLIERS, C_N
+  C_REFINE_ITERS, C_REFINE_INLIERS, C_PGO_ITERS, C_PGO_ACCEPTED, C_PGO_SOLVER_ITERS,
+  C_PGO_STOP, C_N
 };
 
 /* query status codes written to out_status (negative = culled/skipped) */
@@ -1174,6 +1180,444 @@ int orc_sim3_refine(const orc_map *m, int32_t n_prob, const int32_t *pbeg, const
     memcpy(out_S + 13 * (size_t)b, S, sizeof(S));
     free(act);
   }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O15 Essential-graph Sim3 pose-graph optimisation.     */
+/* PAPER.md:244-248 §IV.F: "an essential (pose) graph optimization to          */
+/* propagate the loop correction", Jacobians by "automatic differentiation",   */
+/* "Eigen LDLT for the linear solver"; "Levenberg-Marquardt pose optimization  */
+/* scheme" (Conclusion). The paper gives no formulas: the residual, tangent     */
+/* order, exp/log branches, damping and stopping rules are readings A49-A53.    */
+/* ------------------------------------------------------------------------- */
+/* Forward-mode dual numbers with 7 partials (SPEC.md DualNumber7): a value and
+ * its derivatives w.r.t. the 7 tangent coordinates of one vertex. */
+typedef struct { double v; double d[7]; } d7;
+
+static d7 d7c(double x) { d7 r; r.v = x; for (int k = 0; k < 7; ++k) r.d[k] = 0.0; return r; }
+static d7 d7add(d7 a, d7 b) { d7 r; r.v = a.v + b.v; for (int k = 0; k < 7; ++k) r.d[k] = a.d[k] + b.d[k]; return r; }
+static d7 d7sub(d7 a, d7 b) { d7 r; r.v = a.v - b.v; for (int k = 0; k < 7; ++k) r.d[k] = a.d[k] - b.d[k]; return r; }
+static d7 d7mul(d7 a, d7 b) {
+  d7 r; r.v = a.v * b.v;
+  for (int k = 0; k < 7; ++k) r.d[k] = a.d[k] * b.v + a.v * b.d[k];
+  return r;
+}
+static d7 d7div(d7 a, d7 b) {
+  d7 r; r.v = a.v / b.v;
+  for (int k = 0; k < 7; ++k) r.d[k] = (a.d[k] * b.v - a.v * b.d[k]) / (b.v * b.v);
+  return r;
+}
+static d7 d7scl(d7 a, double c) { d7 r; r.v = a.v * c; for (int k = 0; k < 7; ++k) r.d[k] = a.d[k] * c; return r; }
+static d7 d7addc(d7 a, double c) { a.v += c; return a; }
+/* chain rule: f(a) with f' = df at a.v */
+static d7 d7fn(d7 a, double f, double df) { d7 r; r.v = f; for (int k = 0; k < 7; ++k) r.d[k] = df * a.d[k]; return r; }
+static d7 d7sqrt(d7 a) { const double s = sqrt(a.v); return d7fn(a, s, 0.5 / s); }
+static d7 d7sin(d7 a) { return d7fn(a, sin(a.v), cos(a.v)); }
+static d7 d7cos(d7 a) { return d7fn(a, cos(a.v), -sin(a.v)); }
+static d7 d7exp(d7 a) { const double e = exp(a.v); return d7fn(a, e, e); }
+static d7 d7expm1(d7 a) { return d7fn(a, expm1(a.v), exp(a.v)); }
+static d7 d7log(d7 a) { return d7fn(a, log(a.v), 1.0 / a.v); }
+static d7 d7atan2(d7 y, d7 x) {
+  d7 r; r.v = atan2(y.v, x.v);
+  const double den = x.v * x.v + y.v * y.v;
+  for (int k = 0; k < 7; ++k) r.d[k] = (x.v * y.d[k] - y.v * x.d[k]) / den;
+  return r;
+}
+static d7 d7dot3(const d7 *a, const d7 *b) { return d7add(d7add(d7mul(a[0], b[0]), d7mul(a[1], b[1])), d7mul(a[2], b[2])); }
+static void d7cross(const d7 *a, const d7 *b, d7 *o) {
+  d7 r[3];
+  r[0] = d7sub(d7mul(a[1], b[2]), d7mul(a[2], b[1]));
+  r[1] = d7sub(d7mul(a[2], b[0]), d7mul(a[0], b[2]));
+  r[2] = d7sub(d7mul(a[0], b[1]), d7mul(a[1], b[0]));
+  o[0] = r[0]; o[1] = r[1]; o[2] = r[2];
+}
+
+/* Sim3 with dual entries: p' = s R p + t (reading A1 layout) */
+typedef struct { d7 R[9]; d7 t[3]; d7 s; } s7;
+
+static s7 s7c(const double *S) {
+  s7 r;
+  for (int i = 0; i < 9; ++i) r.R[i] = d7c(S[i]);
+  for (int i = 0; i < 3; ++i) r.t[i] = d7c(S[9 + i]);
+  r.s = d7c(S[12]);
+  return r;
+}
+/* A o B: R = R_A R_B, t = s_A R_A t_B + t_A, s = s_A s_B (same as orc_sim3_compose) */
+static s7 s7compose(const s7 *A, const s7 *B) {
+  s7 r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      r.R[3 * i + j] = d7add(d7add(d7mul(A->R[3 * i + 0], B->R[0 + j]), d7mul(A->R[3 * i + 1], B->R[3 + j])),
+                             d7mul(A->R[3 * i + 2], B->R[6 + j]));
+  for (int i = 0; i < 3; ++i)
+    r.t[i] = d7add(d7mul(A->s, d7dot3(A->R + 3 * i, B->t)), A->t[i]);
+  r.s = d7mul(A->s, B->s);
+  return r;
+}
+/* inverse: R^T, -R^T t / s, 1/s */
+static s7 s7inverse(const s7 *S) {
+  s7 r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) r.R[3 * i + j] = S->R[3 * j + i];
+  for (int i = 0; i < 3; ++i) {
+    d7 c = d7add(d7add(d7mul(S->R[0 + i], S->t[0]), d7mul(S->R[3 + i], S->t[1])), d7mul(S->R[6 + i], S->t[2]));
+    r.t[i] = d7scl(d7div(c, S->s), -1.0);
+  }
+  r.s = d7div(d7c(1.0), S->s);
+  return r;
+}
+
+/* A49: coefficients of W(omega, sigma) = A I + B Omega + C Omega^2, the integral
+ * int_0^1 e^(sigma tau) exp(tau Omega) dtau, with th2 = |omega|^2:
+ *   A = expm1(s)/s; B = (e^s s sin(th) + th (2 sin^2(th/2) - expm1(s) cos(th))) / (th (s^2 + th^2));
+ *   C = (A - ((expm1(s) cos(th) - 2 sin^2(th/2)) s + e^s sin(th) th) / (s^2 + th^2)) / th^2;
+ * for |s| < 1e-3 A is its Taylor series to s^3; for th < 1e-4 B, C are their th -> 0
+ * limits B0(s) = int tau e^(s tau), C0(s) = int tau^2/2 e^(s tau) (Taylor series to s^3
+ * when |s| < 1e-3, else closed form). */
+static void pgo_coef(d7 th2, d7 sg, d7 *A, d7 *B, d7 *C) {
+  const int ssmall = fabs(sg.v) < 1e-3;
+  if (ssmall) {  /* 1 + s/2 + s^2/6 + s^3/24 */
+    *A = d7addc(d7mul(sg, d7addc(d7mul(sg, d7addc(d7scl(sg, 1.0 / 24.0), 1.0 / 6.0)), 0.5)), 1.0);
+  } else {
+    *A = d7div(d7expm1(sg), sg);
+  }
+  if (th2.v < 1e-8) {
+    if (ssmall) {  /* B0 = 1/2 + s/3 + s^2/8 + s^3/30; C0 = 1/6 + s/8 + s^2/20 + s^3/72 */
+      *B = d7addc(d7mul(sg, d7addc(d7mul(sg, d7addc(d7scl(sg, 1.0 / 30.0), 1.0 / 8.0)), 1.0 / 3.0)), 0.5);
+      *C = d7addc(d7mul(sg, d7addc(d7mul(sg, d7addc(d7scl(sg, 1.0 / 72.0), 1.0 / 20.0)), 1.0 / 8.0)), 1.0 / 6.0);
+    } else {       /* B0 = ((s - 1) e^s + 1) / s^2; C0 = ((s^2 - 2 s + 2) e^s - 2) / (2 s^3) */
+      const d7 es = d7exp(sg), s2 = d7mul(sg, sg);
+      *B = d7div(d7addc(d7mul(d7addc(sg, -1.0), es), 1.0), s2);
+      *C = d7div(d7addc(d7mul(d7addc(d7sub(s2, d7scl(sg, 2.0)), 2.0), es), -2.0), d7scl(d7mul(s2, sg), 2.0));
+    }
+    return;
+  }
+  const d7 th = d7sqrt(th2), sn = d7sin(th), cs = d7cos(th), h = d7sin(d7scl(th, 0.5));
+  const d7 es = d7exp(sg), em = d7expm1(sg);
+  const d7 h2 = d7scl(d7mul(h, h), 2.0);              /* 2 sin^2(th/2) = 1 - cos(th) */
+  const d7 den = d7add(d7mul(sg, sg), th2);
+  const d7 nb = d7add(d7mul(d7mul(es, sg), sn), d7mul(th, d7sub(h2, d7mul(em, cs))));
+  *B = d7div(nb, d7mul(th, den));
+  const d7 nc = d7add(d7mul(d7sub(d7mul(em, cs), h2), sg), d7mul(d7mul(es, sn), th));
+  *C = d7div(d7sub(*A, d7div(nc, den)), th2);
+}
+
+/* A49: x = (omega0..2, upsilon0..2, sigma). exp(x) = (R, W upsilon, e^sigma),
+ * R = I + a Omega + b Omega^2, a = sin(th)/th, b = 2 sin^2(th/2)/th^2 (th < 1e-4:
+ * a = 1 - th^2/6, b = 1/2 - th^2/24). */
+static s7 pgo_exp(const d7 *x) {
+  const d7 *w = x, *u = x + 3;
+  const d7 th2 = d7dot3(w, w);
+  d7 a, b;
+  if (th2.v < 1e-8) {
+    a = d7addc(d7scl(th2, -1.0 / 6.0), 1.0);
+    b = d7addc(d7scl(th2, -1.0 / 24.0), 0.5);
+  } else {
+    const d7 th = d7sqrt(th2), hh = d7sin(d7scl(th, 0.5));
+    a = d7div(d7sin(th), th);
+    b = d7div(d7scl(d7mul(hh, hh), 2.0), th2);
+  }
+  /* Omega = [w]x, Omega^2 = w w^T - th2 I */
+  const d7 O[9] = {d7c(0.0), d7scl(w[2], -1.0), w[1], w[2], d7c(0.0), d7scl(w[0], -1.0),
+                   d7scl(w[1], -1.0), w[0], d7c(0.0)};
+  s7 r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      d7 o2 = d7mul(w[i], w[j]);
+      if (i == j) o2 = d7sub(o2, th2);
+      d7 e = d7add(d7mul(a, O[3 * i + j]), d7mul(b, o2));
+      if (i == j) e = d7addc(e, 1.0);
+      r.R[3 * i + j] = e;
+    }
+  d7 A, B, C, wu[3], wwu[3];
+  pgo_coef(th2, x[6], &A, &B, &C);
+  d7cross(w, u, wu);
+  d7cross(w, wu, wwu);
+  for (int i = 0; i < 3; ++i) r.t[i] = d7add(d7add(d7mul(A, u[i]), d7mul(B, wu[i])), d7mul(C, wwu[i]));
+  r.s = d7exp(x[6]);
+  return r;
+}
+
+/* A49: log(S) = (omega, W^-1 t, ln s): v = vee(R - R^T), c = (tr R - 1)/2; if
+ * |v|^2 < 4e-8 and c > 0, omega = (1/2 + |v|^2/48) v (theta/(2 sin theta) to second
+ * order with sin^2 theta = |v|^2/4); else theta = atan2(|v|/2, c), omega = theta v / |v|.
+ * upsilon solves W upsilon = t by Cramer's rule. Rotation angles near pi are outside
+ * the reading (the residuals of an essential graph are small rotations). */
+static void pgo_log(const s7 *S, d7 *x) {
+  const d7 *R = S->R;
+  const d7 v[3] = {d7sub(R[7], R[5]), d7sub(R[2], R[6]), d7sub(R[3], R[1])};
+  const d7 c = d7scl(d7addc(d7add(d7add(R[0], R[4]), R[8]), -1.0), 0.5);
+  const d7 n2 = d7dot3(v, v);
+  d7 w[3];
+  if (n2.v < 4e-8 && c.v > 0.0) {
+    const d7 f = d7addc(d7scl(n2, 1.0 / 48.0), 0.5);
+    for (int i = 0; i < 3; ++i) w[i] = d7mul(f, v[i]);
+  } else {
+    const d7 nv = d7sqrt(n2);
+    const d7 th = d7atan2(d7scl(nv, 0.5), c);
+    const d7 f = d7div(th, nv);
+    for (int i = 0; i < 3; ++i) w[i] = d7mul(f, v[i]);
+  }
+  const d7 sg = d7log(S->s);
+  const d7 th2 = d7dot3(w, w);
+  d7 A, B, C;
+  pgo_coef(th2, sg, &A, &B, &C);
+  const d7 O[9] = {d7c(0.0), d7scl(w[2], -1.0), w[1], w[2], d7c(0.0), d7scl(w[0], -1.0),
+                   d7scl(w[1], -1.0), w[0], d7c(0.0)};
+  d7 W[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      d7 o2 = d7mul(w[i], w[j]);
+      if (i == j) o2 = d7sub(o2, th2);
+      d7 e = d7add(d7mul(B, O[3 * i + j]), d7mul(C, o2));
+      if (i == j) e = d7add(e, A);
+      W[3 * i + j] = e;
+    }
+  /* Cramer: u_k = det(W with column k := t) / det(W) */
+  d7 det = d7c(0.0);
+  {
+    const d7 m0 = d7sub(d7mul(W[4], W[8]), d7mul(W[5], W[7]));
+    const d7 m1 = d7sub(d7mul(W[3], W[8]), d7mul(W[5], W[6]));
+    const d7 m2 = d7sub(d7mul(W[3], W[7]), d7mul(W[4], W[6]));
+    det = d7add(d7sub(d7mul(W[0], m0), d7mul(W[1], m1)), d7mul(W[2], m2));
+  }
+  for (int k = 0; k < 3; ++k) {
+    d7 Wk[9];
+    for (int i = 0; i < 9; ++i) Wk[i] = W[i];
+    for (int i = 0; i < 3; ++i) Wk[3 * i + k] = S->t[i];
+    const d7 m0 = d7sub(d7mul(Wk[4], Wk[8]), d7mul(Wk[5], Wk[7]));
+    const d7 m1 = d7sub(d7mul(Wk[3], Wk[8]), d7mul(Wk[5], Wk[6]));
+    const d7 m2 = d7sub(d7mul(Wk[3], Wk[7]), d7mul(Wk[4], Wk[6]));
+    const d7 dk = d7add(d7sub(d7mul(Wk[0], m0), d7mul(Wk[1], m1)), d7mul(Wk[2], m2));
+    x[3 + k] = d7div(dk, det);
+  }
+  x[0] = w[0]; x[1] = w[1]; x[2] = w[2];
+  x[6] = sg;
+}
+
+static void s7out(const s7 *S, double *o) {
+  for (int i = 0; i < 9; ++i) o[i] = S->R[i].v;
+  for (int i = 0; i < 3; ++i) o[9 + i] = S->t[i].v;
+  o[12] = S->s.v;
+}
+
+/* plain-value exp / log (pins) */
+void orc_pgo_exp(const double *x, double *S) {
+  d7 xd[7];
+  for (int k = 0; k < 7; ++k) xd[k] = d7c(x[k]);
+  const s7 r = pgo_exp(xd);
+  s7out(&r, S);
+}
+void orc_pgo_log(const double *S, double *x) {
+  const s7 Sd = s7c(S);
+  d7 xd[7];
+  pgo_log(&Sd, xd);
+  for (int k = 0; k < 7; ++k) x[k] = xd[k].v;
+}
+
+/* A50: residual of edge (i, j) with measurement M (= S_j S_i^-1 when the edge was
+ * made): e = log(M o S_i o S_j^-1), identity information; left-multiplicative
+ * updates S <- exp(delta) o S. which = 0 seeds delta_i, 1 seeds delta_j (seven unit
+ * seed directions, evaluated at delta = 0). */
+static void pgo_edge_dual(const double *M, const double *Si, const double *Sj, int which, d7 *e) {
+  d7 x[7];
+  for (int k = 0; k < 7; ++k) { x[k] = d7c(0.0); x[k].d[k] = 1.0; }
+  const s7 E = pgo_exp(x);
+  const s7 Md = s7c(M);
+  s7 SI = s7c(Si), SJ = s7c(Sj);
+  if (which == 0) SI = s7compose(&E, &SI);
+  else SJ = s7compose(&E, &SJ);
+  const s7 SJi = s7inverse(&SJ);
+  const s7 T1 = s7compose(&Md, &SI);
+  const s7 T = s7compose(&T1, &SJi);
+  pgo_log(&T, e);
+}
+
+/* e[7], Ji[7][7], Jj[7][7] row-major: J[r][k] = d e_r / d delta_k */
+void orc_pgo_edge(const double *M, const double *Si, const double *Sj, double *e, double *Ji, double *Jj) {
+  d7 ea[7], eb[7];
+  pgo_edge_dual(M, Si, Sj, 0, ea);
+  pgo_edge_dual(M, Si, Sj, 1, eb);
+  for (int r = 0; r < 7; ++r) {
+    e[r] = ea[r].v;
+    for (int k = 0; k < 7; ++k) {
+      Ji[7 * r + k] = ea[r].d[k];
+      Jj[7 * r + k] = eb[r].d[k];
+    }
+  }
+}
+
+typedef struct {
+  int32_t max_iter, cg_max_iter;
+  double lambda0, eps_dx, eps_chi2, cg_tol;
+} orc_pgo_params;
+
+/* chi2 = sum over edges (ascending) of e^T e (r ascending) */
+static double pgo_chi2(int32_t n_e, const int32_t *eij, const double *M, const double *S) {
+  double chi2 = 0.0;
+  for (int32_t k = 0; k < n_e; ++k) {
+    const int32_t i = eij[2 * k], j = eij[2 * k + 1];
+    const s7 Md = s7c(M + 13 * (size_t)k), SI = s7c(S + 13 * (size_t)i), SJ = s7c(S + 13 * (size_t)j);
+    const s7 SJi = s7inverse(&SJ);
+    const s7 T1 = s7compose(&Md, &SI);
+    const s7 T = s7compose(&T1, &SJi);
+    d7 e[7];
+    pgo_log(&T, e);
+    double c = 0.0;
+    for (int r = 0; r < 7; ++r) c += e[r].v * e[r].v;
+    chi2 += c;
+  }
+  return chi2;
+}
+
+/* A51: dense LDL^T of the N x N symmetric matrix A (lower triangle used), no pivoting;
+ * fails (returns 0) when a pivot is not > 0 (not SPD). Solves A x = r. */
+static int ldlt_solve(int64_t N, const double *A, const double *r, double *x) {
+  double *L = (double *)calloc((size_t)(N * N > 0 ? N * N : 1), sizeof(double));
+  double *D = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
+  int ok = 1;
+  for (int64_t j = 0; j < N && ok; ++j) {
+    double dj = A[j * N + j];
+    for (int64_t k = 0; k < j; ++k) dj -= L[j * N + k] * L[j * N + k] * D[k];
+    if (!(dj > 0.0)) { ok = 0; break; }
+    D[j] = dj;
+    L[j * N + j] = 1.0;
+    for (int64_t i = j + 1; i < N; ++i) {
+      double a = A[i * N + j];
+      for (int64_t k = 0; k < j; ++k) a -= L[i * N + k] * L[j * N + k] * D[k];
+      L[i * N + j] = a / dj;
+    }
+  }
+  if (ok) {
+    for (int64_t i = 0; i < N; ++i) {      /* L y = r */
+      double y = r[i];
+      for (int64_t k = 0; k < i; ++k) y -= L[i * N + k] * x[k];
+      x[i] = y;
+    }
+    for (int64_t i = 0; i < N; ++i) x[i] /= D[i];
+    for (int64_t i = N - 1; i >= 0; --i) { /* L^T x = z */
+      double y = x[i];
+      for (int64_t k = i + 1; k < N; ++k) y -= L[k * N + i] * x[k];
+      x[i] = y;
+    }
+  }
+  free(L);
+  free(D);
+  return ok;
+}
+
+/* A52/A53: Levenberg-Marquardt over the free vertices (fixed vertices are excluded
+ * from the reduced system). Each iteration: (re)linearise after an accepted step --
+ * H = sum_e J^T J, b = sum_e J^T e accumulated in ascending edge order --, solve
+ * (H + lambda diag(H)) delta = -b by LDL^T; a failed factorisation multiplies lambda
+ * by 4; |delta| < eps_dx stops; else the trial S_v' = exp(delta_v) o S_v is accepted
+ * iff chi2' < chi2 (lambda <- max(lambda/2, 1e-12); stop when (chi2 - chi2')/chi2 <
+ * eps_chi2), otherwise lambda <- 4 lambda. lambda > 1e8 stops; so does max_iter.
+ * chi2 == 0 at the start stops before any solve. trace [max_iter][6]: chi2, lambda,
+ * chi2 trial (-1: solve failed; chi2 when |delta| stopped), accepted, |delta|, solver
+ * iterations (1 = one direct solve). stop codes: 1 |delta|, 2 chi2 change, 3 max_iter,
+ * 4 lambda, 5 zero chi2. */
+int orc_pgo(int32_t n_v, const double *S_in, const uint8_t *fixed, int32_t n_e, const int32_t *eij,
+            const double *M, const orc_pgo_params *p, double *out_S, double *trace, double *chi2_out,
+            int64_t *cnt) {
+  int32_t *fidx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n_v > 0 ? n_v : 1));
+  int64_t nf = 0;
+  for (int32_t v = 0; v < n_v; ++v) fidx[v] = fixed[v] ? -1 : (int32_t)nf++;
+  const int64_t N = 7 * nf;
+  double *S = out_S;
+  memcpy(S, S_in, sizeof(double) * 13 * (size_t)n_v);
+  double *St = (double *)malloc(sizeof(double) * 13 * (size_t)(n_v > 0 ? n_v : 1));
+  double *H = (double *)calloc((size_t)(N * N > 0 ? N * N : 1), sizeof(double));
+  double *A = (double *)malloc(sizeof(double) * (size_t)(N * N > 0 ? N * N : 1));
+  double *b = (double *)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
+  double *nb = (double *)malloc(sizeof(double) * (size_t)(N > 0 ? N : 1));
+  double *dx = (double *)malloc(sizeof(double) * (size_t)(N > 0 ? N : 1));
+  double chi2 = pgo_chi2(n_e, eij, M, S);
+  if (chi2_out) chi2_out[0] = chi2;
+  double lambda = p->lambda0;
+  int stop = chi2 == 0.0 ? 5 : 0, relin = 1;
+  int32_t it = 0;
+  while (!stop) {
+    if (it >= p->max_iter) { stop = 3; break; }
+    if (relin) {
+      memset(H, 0, sizeof(double) * (size_t)(N * N));
+      memset(b, 0, sizeof(double) * (size_t)N);
+      for (int32_t k = 0; k < n_e; ++k) {
+        const int32_t i = eij[2 * k], j = eij[2 * k + 1];
+        double e[7], J[2][49];
+        orc_pgo_edge(M + 13 * (size_t)k, S + 13 * (size_t)i, S + 13 * (size_t)j, e, J[0], J[1]);
+        const int32_t vv[2] = {i, j};
+        for (int a = 0; a < 2; ++a) {
+          if (fidx[vv[a]] < 0) continue;
+          const int64_t ra = 7 * (int64_t)fidx[vv[a]];
+          for (int r = 0; r < 7; ++r) {
+            double g = 0.0;
+            for (int q = 0; q < 7; ++q) g += J[a][7 * q + r] * e[q];
+            b[ra + r] += g;
+          }
+          for (int c2 = 0; c2 < 2; ++c2) {
+            if (fidx[vv[c2]] < 0) continue;
+            const int64_t rc = 7 * (int64_t)fidx[vv[c2]];
+            for (int r = 0; r < 7; ++r)
+              for (int cc = 0; cc < 7; ++cc) {
+                double h = 0.0;
+                for (int q = 0; q < 7; ++q) h += J[a][7 * q + r] * J[c2][7 * q + cc];
+                H[(ra + r) * N + rc + cc] += h;
+              }
+          }
+        }
+      }
+      relin = 0;
+    }
+    memcpy(A, H, sizeof(double) * (size_t)(N * N));
+    for (int64_t k = 0; k < N; ++k) A[k * N + k] = H[k * N + k] + lambda * H[k * N + k];
+    for (int64_t k = 0; k < N; ++k) nb[k] = -b[k];
+    const int ok = ldlt_solve(N, A, nb, dx);
+    double *row = trace ? trace + 6 * (size_t)it : NULL;
+    ++it;
+    cnt[C_PGO_ITERS]++;
+    if (row) { row[0] = chi2; row[1] = lambda; row[2] = -1.0; row[3] = 0.0; row[4] = -1.0; row[5] = 1.0; }
+    if (!ok) {
+      lambda *= 4.0;
+      if (lambda > 1e8) stop = 4;
+      continue;
+    }
+    double dn = 0.0;
+    for (int64_t k = 0; k < N; ++k) dn += dx[k] * dx[k];
+    dn = sqrt(dn);
+    if (row) row[4] = dn;
+    if (dn < p->eps_dx) {
+      if (row) row[2] = chi2;
+      stop = 1;
+      break;
+    }
+    for (int32_t v = 0; v < n_v; ++v) {
+      if (fidx[v] < 0) { memcpy(St + 13 * (size_t)v, S + 13 * (size_t)v, sizeof(double) * 13); continue; }
+      double E[13];
+      orc_pgo_exp(dx + 7 * (int64_t)fidx[v], E);
+      orc_sim3_compose(E, S + 13 * (size_t)v, St + 13 * (size_t)v);
+    }
+    const double chi2t = pgo_chi2(n_e, eij, M, St);
+    if (row) row[2] = chi2t;
+    if (chi2t < chi2) {
+      if (row) row[3] = 1.0;
+      cnt[C_PGO_ACCEPTED]++;
+      const double rel = (chi2 - chi2t) / chi2;
+      memcpy(S, St, sizeof(double) * 13 * (size_t)n_v);
+      chi2 = chi2t;
+      lambda = lambda * 0.5 < 1e-12 ? 1e-12 : lambda * 0.5;
+      relin = 1;
+      if (rel < p->eps_chi2) stop = 2;
+    } else {
+      lambda *= 4.0;
+      if (lambda > 1e8) stop = 4;
+    }
+  }
+  cnt[C_PGO_SOLVER_ITERS] += it;
+  cnt[C_PGO_STOP] = stop;
+  if (chi2_out) chi2_out[1] = chi2;
+  free(fidx); free(St); free(H); free(A); free(b); free(nb); free(dx);
   return 0;
 }
 
