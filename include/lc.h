@@ -194,6 +194,10 @@ enum {
   LC_COUNT_RANSAC_INLIERS, /* Sim3 RANSAC: inliers of the selected models             */
   LC_COUNT_REFINE_ITERS,   /* Sim3 refinement: Gauss-Newton steps taken              */
   LC_COUNT_REFINE_INLIERS, /* Sim3 refinement: inliers under the refined models      */
+  LC_COUNT_PGO_ITERS,      /* pose graph: Levenberg-Marquardt iterations (linear solves) */
+  LC_COUNT_PGO_ACCEPTED,   /* pose graph: accepted steps                             */
+  LC_COUNT_PGO_SOLVER_ITERS, /* pose graph: conjugate-gradient iterations, all solves */
+  LC_COUNT_PGO_STOP,       /* pose graph: stop reason (LC_PGO_STOP_*)                 */
   LC_NCOUNT
 };
 
@@ -234,7 +238,7 @@ int64_t lc_kernel_launches(const lc_ctx* ctx);
 enum { LC_PROF_UPLOAD = 0, LC_PROF_CORRECT_WINDOW, LC_PROF_CORRECT_ALL, LC_PROF_FUSE_PREP,
        LC_PROF_MATCH, LC_PROF_RESOLVE, LC_PROF_APPLY, LC_PROF_SBP_MATCH, LC_PROF_SBP_RESOLVE,
        LC_PROF_STATE, LC_PROF_PROJECT, LC_PROF_REFRESH, LC_PROF_CONN, LC_PROF_RANSAC, LC_PROF_REFINE,
-       LC_NPROF };
+       LC_PROF_PGO, LC_NPROF };
 lc_status lc_profile_enable(lc_ctx* ctx, int32_t on);
 lc_status lc_profile_read(lc_ctx* ctx, double* ms, int64_t* launches);
 
@@ -499,6 +503,57 @@ lc_status lc_search_by_projection(lc_ctx* ctx, int32_t n_pairs, const int32_t* p
                                   const int32_t* pair_taken, int32_t* out_feat_mp,
                                   int32_t* out_feat_dist, const lc_query_debug* dbg,
                                   int64_t* out_counts, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * lc_pgo_sim3 -- essential-graph Sim3 pose-graph optimisation (
+ * PAPER.md:244-248 §IV.F "an essential (pose) graph optimization to propagate the
+ * loop correction to the rest of the map", Jacobians by "automatic differentiation";
+ * "Levenberg-Marquardt" (Conclusion); SPEC.md pose-graph; readings A49-A54).
+ * Its output S_opt is what lc_correct_sim3(LC_CORRECT_ALL) propagates to the map.
+ * Needs a context, not a map.
+ *
+ *   n_v vertices: S_init [host|dev] [n_v] world->camera Sim3 estimates; fixed [host]
+ *     [n_v] (non-zero = held constant, e.g. the loop keyframe).
+ *   n_e edges: edge_ij [host] [n_e][2] (i, j), i != j, both < n_v; M [host|dev] [n_e]
+ *     the measurement, S_j o S_i^-1 when the edge was made. Residual
+ *     e = log(M o S_i o S_j^-1) (7-vector (omega, upsilon, sigma), A49/A50), identity
+ *     information; chi2 = sum_e |e|^2. Updates S <- exp(delta) o S.
+ *   Levenberg-Marquardt (A52/A53): linearise (Jacobians by forward-mode dual numbers),
+ *     solve (H + lambda diag(H)) delta = -b over the free vertices by block-Jacobi
+ *     preconditioned conjugate gradients (A54: stop when |r| <= cg_tol |b| or after
+ *     cg_max_iter; a non-SPD diagonal block or p^T A p <= 0 is a failed solve ->
+ *     lambda *= 4). |delta| < eps_dx stops; a trial exp(delta_v) o S_v is accepted iff
+ *     chi2 decreases (lambda <- max(lambda / 2, 1e-12); stop when the relative
+ *     decrease < eps_chi2), else lambda *= 4; lambda > 1e8 stops; max_iter solves.
+ *   out_S [host|dev] [n_v] the optimised estimates (fixed vertices unchanged).
+ *   out_trace [host|dev] nullable [max_iter][6] per iteration: chi2, lambda, trial
+ *     chi2 (-1: solve failed; chi2 when the |delta| test stopped), accepted (0/1),
+ *     |delta| (-1 if failed), CG iterations.
+ *   out_chi2 [host|dev] nullable [2]: initial and final chi2.
+ *   out_counts [host|dev] nullable [LC_NCOUNT] (PGO_ITERS, PGO_ACCEPTED,
+ *     PGO_SOLVER_ITERS, PGO_STOP).
+ * The whole loop runs in one cooperative kernel (no host round trip per iteration);
+ * results are deterministic for a given problem. Not capturable (LC_ESTATE while a
+ * graph capture is open).
+ * Errors: LC_EINVAL (null pointers, sizes, params, i == j), LC_ERANGE (vertex index),
+ * LC_ECUDA (cooperative launch failed).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t max_iter;      /* Levenberg-Marquardt iterations (linear solves), >= 0 (ORB-SLAM3: 20) */
+  int32_t cg_max_iter;   /* CG iterations per solve, >= 1                                */
+  double lambda0;        /* initial damping, > 0 (SPEC: 1e-4)                            */
+  double eps_dx;         /* stop when |delta| < eps_dx (1e-8)                            */
+  double eps_chi2;       /* stop when an accepted step lowers chi2 by < eps_chi2 relative */
+  double cg_tol;         /* CG relative residual target (1e-10)                          */
+} lc_pgo_params;
+
+enum { LC_PGO_STOP_DX = 1, LC_PGO_STOP_CHI2 = 2, LC_PGO_STOP_MAX_ITER = 3, LC_PGO_STOP_LAMBDA = 4,
+       LC_PGO_STOP_ZERO = 5 };
+
+lc_status lc_pgo_sim3(lc_ctx* ctx, int32_t n_v, const lc_sim3* S_init, const uint8_t* fixed, int32_t n_e,
+                      const int32_t* edge_ij, const lc_sim3* M, const lc_pgo_params* params,
+                      lc_sim3* out_S, double* out_trace, double* out_chi2, int64_t* out_counts,
+                      void* cuda_stream);
 
 #ifdef __cplusplus
 }

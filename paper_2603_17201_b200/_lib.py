@@ -24,11 +24,11 @@ COUNTER_NAMES = [
     "winners", "orient_rej", "add", "victim_prop", "loop_skip", "bad_slot",
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
     "refresh_mp", "refresh_obs", "conn_kf", "conn_edges", "ransac_hyp", "ransac_inliers",
-    "refine_iters", "refine_inliers",
+    "refine_iters", "refine_inliers", "pgo_iters", "pgo_accepted", "pgo_solver_iters", "pgo_stop",
 ]
 LC_NCOUNT = len(COUNTER_NAMES)
 PROF_NAMES = ["upload", "correct_window", "correct_all", "fuse_prep", "match", "resolve", "apply",
-              "sbp_match", "sbp_resolve", "state", "project", "refresh", "conn", "ransac", "refine"]
+              "sbp_match", "sbp_resolve", "state", "project", "refresh", "conn", "ransac", "refine", "pgo"]
 
 
 class lc_sim3(C.Structure):
@@ -68,6 +68,11 @@ class lc_match_params(C.Structure):
 
 class lc_query_debug(C.Structure):
     _fields_ = [("best", C.c_void_p), ("uv", C.c_void_p), ("ncand", C.c_void_p)]
+
+
+class lc_pgo_params(C.Structure):
+    _fields_ = [("max_iter", C.c_int32), ("cg_max_iter", C.c_int32), ("lambda0", C.c_double),
+                ("eps_dx", C.c_double), ("eps_chi2", C.c_double), ("cg_tol", C.c_double)]
 
 
 class LcError(RuntimeError):
@@ -112,6 +117,7 @@ def load():
                                  i32, vp, vp, vp, vp, vp]),
         "lc_sim3_refine": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, C.c_double,
                                  C.c_double, vp, vp, vp, vp, vp]),
+        "lc_pgo_sim3": (i32, [vp, i32, vp, vp, i32, vp, vp, P(lc_pgo_params), vp, vp, vp, vp, vp]),
         "lc_graph_begin": (i32, [vp, vp]),
         "lc_graph_end": (i32, [vp, vp, P(vp)]),
         "lc_graph_launch": (i32, [vp, vp, vp]),
@@ -129,5 +135,5 @@ def exported_symbols():
     return ["lc_create", "lc_destroy", "lc_last_error", "lc_kernel_launches", "lc_profile_enable",
             "lc_profile_read", "lc_upload_map",
             "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse",
-            "lc_search_by_projection", "lc_refresh_mappoints", "lc_update_connections", "lc_sim3_ransac", "lc_sim3_refine", "lc_graph_begin", "lc_graph_end", "lc_graph_launch",
+            "lc_search_by_projection", "lc_refresh_mappoints", "lc_update_connections", "lc_sim3_ransac", "lc_sim3_refine", "lc_pgo_sim3", "lc_graph_begin", "lc_graph_end", "lc_graph_launch",
             "lc_graph_destroy"]

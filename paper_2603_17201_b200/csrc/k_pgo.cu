@@ -1,0 +1,727 @@
+// k_pgo.cu -- essential-graph Sim3 pose-graph optimisation on the device (SURVEY.md
+// §8(f) f1; §IV.F: "essential (pose) graph optimization to propagate
+// the loop correction", Jacobians by "automatic differentiation"; Conclusion:
+// "Levenberg-Marquardt"). Readings A49-A54.
+//
+// One persistent cooperative kernel runs the whole Levenberg-Marquardt loop: no host
+// round trip per iteration or per linear-solver step. Phases are separated by a
+// grid-wide barrier; every CTA reduces the same per-CTA partials in the same order,
+// so all CTAs take identical control decisions (accept / reject / stop) and the
+// result is deterministic for a given grid size.
+//
+//   linearise   16-lane group per edge: lane k < 14 evaluates the residual
+//               e = log(M o S_i o S_j^-1) on a forward-mode dual number seeded with
+//               tangent direction k of vertex i (k < 7) or j (k >= 7) (A50), i.e. one
+//               Jacobian column per lane; the group forms J^T J and J^T e blocks in
+//               shared memory and writes one 1.7-KB record per edge.
+//   assemble    warp per vertex: diagonal block and gradient summed over the vertex's
+//               incident edges in ascending edge order (the oracle's order).
+//   solve       (H + lambda diag(H)) delta = -b by block-Jacobi preconditioned CG
+//               (A54: the paper's LDLT is a CPU library solve; CG on the block-sparse
+//               matrix is the data-parallel equivalent); 8-lane group per vertex.
+//   trial       S_v' = exp(delta_v) o S_v, chi2' by thread per edge; accept iff it
+//               decreases (A52/A53).
+#include <cooperative_groups.h>
+
+#include "lc_internal.cuh"
+
+namespace {
+
+constexpr int kT = 256;        // threads per CTA
+constexpr int kRec = 212;      // doubles per edge record
+// record layout: Hii [0,49) Hjj [49,98) Hij [98,147) Hji [147,196) bi [196,203) bj [203,210) chi2 [210]
+constexpr int kOffHii = 0, kOffHjj = 49, kOffHij = 98, kOffHji = 147, kOffBi = 196, kOffBj = 203;
+constexpr int kVD = 56;        // per-vertex diagonal block (49) + gradient (7)
+constexpr int kVL = 28;        // per-vertex Cholesky factor of the damped diagonal block
+constexpr int kVec = 8;        // padded 7-vectors
+
+// ---------------------------------------------------------------------------
+// forward-mode dual number with one partial (A50): value and derivative along one seed
+// ---------------------------------------------------------------------------
+struct dd {
+  double v, d;
+};
+__device__ __forceinline__ dd operator+(dd a, dd b) { return {a.v + b.v, a.d + b.d}; }
+__device__ __forceinline__ dd operator-(dd a, dd b) { return {a.v - b.v, a.d - b.d}; }
+__device__ __forceinline__ dd operator*(dd a, dd b) { return {a.v * b.v, a.d * b.v + a.v * b.d}; }
+__device__ __forceinline__ dd operator/(dd a, dd b) { return {a.v / b.v, (a.d * b.v - a.v * b.d) / (b.v * b.v)}; }
+__device__ __forceinline__ dd scl(dd a, double c) { return {a.v * c, a.d * c}; }
+__device__ __forceinline__ dd addc(dd a, double c) { return {a.v + c, a.d}; }
+__device__ __forceinline__ dd neg(dd a) { return {-a.v, -a.d}; }
+__device__ __forceinline__ double val(dd a) { return a.v; }
+__device__ __forceinline__ dd vsqrt(dd a) { const double s = sqrt(a.v); return {s, (0.5 / s) * a.d}; }
+__device__ __forceinline__ dd vsin(dd a) { return {sin(a.v), cos(a.v) * a.d}; }
+__device__ __forceinline__ dd vcos(dd a) { return {cos(a.v), -sin(a.v) * a.d}; }
+__device__ __forceinline__ dd vexp(dd a) { const double e = exp(a.v); return {e, e * a.d}; }
+__device__ __forceinline__ dd vexpm1(dd a) { return {expm1(a.v), exp(a.v) * a.d}; }
+__device__ __forceinline__ dd vlog(dd a) { return {log(a.v), (1.0 / a.v) * a.d}; }
+__device__ __forceinline__ dd vatan2(dd y, dd x) {
+  const double den = x.v * x.v + y.v * y.v;
+  return {atan2(y.v, x.v), (x.v * y.d - y.v * x.d) / den};
+}
+// plain doubles
+__device__ __forceinline__ double scl(double a, double c) { return a * c; }
+__device__ __forceinline__ double addc(double a, double c) { return a + c; }
+__device__ __forceinline__ double neg(double a) { return -a; }
+__device__ __forceinline__ double val(double a) { return a; }
+__device__ __forceinline__ double vsqrt(double a) { return sqrt(a); }
+__device__ __forceinline__ double vsin(double a) { return sin(a); }
+__device__ __forceinline__ double vcos(double a) { return cos(a); }
+__device__ __forceinline__ double vexp(double a) { return exp(a); }
+__device__ __forceinline__ double vexpm1(double a) { return expm1(a); }
+__device__ __forceinline__ double vlog(double a) { return log(a); }
+__device__ __forceinline__ double vatan2(double y, double x) { return atan2(y, x); }
+template <class T> __device__ __forceinline__ T zero();
+template <> __device__ __forceinline__ double zero<double>() { return 0.0; }
+template <> __device__ __forceinline__ dd zero<dd>() { return {0.0, 0.0}; }
+
+template <class T>
+__device__ __forceinline__ T dot3(const T* a, const T* b) {
+  return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];
+}
+template <class T>
+__device__ __forceinline__ void cross3(const T* a, const T* b, T* o) {
+  const T r0 = a[1] * b[2] - a[2] * b[1];
+  const T r1 = a[2] * b[0] - a[0] * b[2];
+  const T r2 = a[0] * b[1] - a[1] * b[0];
+  o[0] = r0; o[1] = r1; o[2] = r2;
+}
+
+// A49: W(omega, sigma) = A I + B Omega + C Omega^2 coefficients (th2 = |omega|^2)
+template <class T>
+__device__ __forceinline__ void w_coef(T th2, T sg, T& A, T& B, T& C) {
+  const bool ssmall = fabs(val(sg)) < 1e-3;
+  if (ssmall) A = addc(sg * addc(sg * addc(scl(sg, 1.0 / 24.0), 1.0 / 6.0), 0.5), 1.0);
+  else A = vexpm1(sg) / sg;
+  if (val(th2) < 1e-8) {
+    if (ssmall) {
+      B = addc(sg * addc(sg * addc(scl(sg, 1.0 / 30.0), 1.0 / 8.0), 1.0 / 3.0), 0.5);
+      C = addc(sg * addc(sg * addc(scl(sg, 1.0 / 72.0), 1.0 / 20.0), 1.0 / 8.0), 1.0 / 6.0);
+    } else {
+      const T es = vexp(sg), s2 = sg * sg;
+      B = addc(addc(sg, -1.0) * es, 1.0) / s2;
+      C = addc(addc(s2 - scl(sg, 2.0), 2.0) * es, -2.0) / scl(s2 * sg, 2.0);
+    }
+    return;
+  }
+  const T th = vsqrt(th2), sn = vsin(th), cs = vcos(th), h = vsin(scl(th, 0.5));
+  const T es = vexp(sg), em = vexpm1(sg);
+  const T h2 = scl(h * h, 2.0);
+  const T den = sg * sg + th2;
+  const T nb = (es * sg) * sn + th * (h2 - em * cs);
+  B = nb / (th * den);
+  const T nc = (em * cs - h2) * sg + (es * sn) * th;
+  C = (A - nc / den) / th2;
+}
+
+// A49: Sim3 log -> x = (omega, upsilon, sigma); R row-major, p' = s R p + t
+template <class T>
+__device__ __forceinline__ void sim3_log(const T* R, const T* t, T s, T* x) {
+  const T v[3] = {R[7] - R[5], R[2] - R[6], R[3] - R[1]};
+  const T c = scl(addc((R[0] + R[4]) + R[8], -1.0), 0.5);
+  const T n2 = dot3(v, v);
+  T w[3];
+  if (val(n2) < 4e-8 && val(c) > 0.0) {
+    const T f = addc(scl(n2, 1.0 / 48.0), 0.5);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) w[i] = f * v[i];
+  } else {
+    const T nv = vsqrt(n2);
+    const T th = vatan2(scl(nv, 0.5), c);
+    const T f = th / nv;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) w[i] = f * v[i];
+  }
+  const T sg = vlog(s);
+  const T th2 = dot3(w, w);
+  T A, B, C;
+  w_coef(th2, sg, A, B, C);
+  const T z = zero<T>();
+  const T O[9] = {z, neg(w[2]), w[1], w[2], z, neg(w[0]), neg(w[1]), w[0], z};
+  T W[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      T o2 = w[i] * w[j];
+      if (i == j) o2 = o2 - th2;
+      T e = B * O[3 * i + j] + C * o2;
+      if (i == j) e = e + A;
+      W[3 * i + j] = e;
+    }
+  const T det = (W[0] * (W[4] * W[8] - W[5] * W[7]) - W[1] * (W[3] * W[8] - W[5] * W[6])) +
+                W[2] * (W[3] * W[7] - W[4] * W[6]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    T Wk[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Wk[i] = W[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) Wk[3 * i + k] = t[i];
+    const T dk = (Wk[0] * (Wk[4] * Wk[8] - Wk[5] * Wk[7]) - Wk[1] * (Wk[3] * Wk[8] - Wk[5] * Wk[6])) +
+                 Wk[2] * (Wk[3] * Wk[7] - Wk[4] * Wk[6]);
+    x[3 + k] = dk / det;
+  }
+  x[0] = w[0]; x[1] = w[1]; x[2] = w[2];
+  x[6] = sg;
+}
+
+// A49: Sim3 exp of x (plain doubles; the trial update S' = exp(delta) o S)
+__device__ __forceinline__ void sim3_exp(const double* x, double* S) {
+  const double* w = x;
+  const double* u = x + 3;
+  const double th2 = dot3(w, w);
+  double a, b;
+  if (th2 < 1e-8) {
+    a = th2 * (-1.0 / 6.0) + 1.0;
+    b = th2 * (-1.0 / 24.0) + 0.5;
+  } else {
+    const double th = sqrt(th2), hh = sin(th * 0.5);
+    a = sin(th) / th;
+    b = ((hh * hh) * 2.0) / th2;
+  }
+  const double O[9] = {0.0, -w[2], w[1], w[2], 0.0, -w[0], -w[1], w[0], 0.0};
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double o2 = w[i] * w[j];
+      if (i == j) o2 = o2 - th2;
+      double e = a * O[3 * i + j] + b * o2;
+      if (i == j) e = e + 1.0;
+      S[3 * i + j] = e;
+    }
+  double A, B, C, wu[3], wwu[3];
+  w_coef(th2, x[6], A, B, C);
+  cross3(w, u, wu);
+  cross3(w, wu, wwu);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) S[9 + i] = (A * u[i] + B * wu[i]) + C * wwu[i];
+  S[12] = exp(x[6]);
+}
+
+// residual value of edge (M, S_i, S_j): e = log((M o S_i) o S_j^-1)
+__device__ __forceinline__ void edge_value(const double* M, const double* Si, const double* Sj, double* Q,
+                                           double* e) {
+  double T1[13], Sji[13];
+  lc_sim3_compose(M, Si, T1);
+  lc_sim3_inverse(Sj, Sji);
+  lc_sim3_compose(T1, Sji, Q);
+  sim3_log<double>(Q, Q + 9, Q[12], e);
+}
+
+struct PgoArgs {
+  int n_v, n_e, max_iter, cg_max;
+  double lambda0, eps_dx, eps_chi2, cg_tol;
+  const int32_t* eij;      // [n_e][2]
+  const double* M;         // [n_e][13]
+  const double* S_in;      // [n_v][13]
+  const uint8_t* fixed;    // [n_v]
+  const int32_t* vbeg;     // [n_v+1] incidence CSR
+  const int32_t* vinc;     // [2 n_e] (edge << 1) | role (0: vertex is i, 1: vertex is j), ascending edge
+  double* S_out;           // [n_v][13] estimate (buffer 0)
+  double* S_tmp;           // [n_v][13] (buffer 1)
+  double* rec;             // [n_e][kRec]
+  double* vd;              // [n_v][kVD]
+  double* vl;              // [n_v][kVL]
+  double* vx;              // 5 vectors [n_v][kVec]: x, r, z, p, q
+  double* part;            // [gridDim][4] per-CTA partial sums
+  unsigned int* bar;       // grid barrier counter (zeroed before launch)
+  double* trace;           // [max_iter][6] or null
+  double* chi2_out;        // [2] or null
+  unsigned long long* counts;
+};
+
+// grid-wide barrier (all CTAs co-resident: cooperative launch); monotone counter
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while ((int)(v - target) < 0);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// deterministic CTA reduction of 4 partials -> part[blockIdx]; then every CTA sums the
+// gridDim partials in the same fixed order (after the barrier)
+__device__ __forceinline__ void cta_partial(double a0, double a1, double a2, double a3, double* part,
+                                            double (*sh)[4]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double a[4] = {a0, a1, a2, a3};
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sh[wid][k] = a[k];
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double s = 0.0;
+    for (int w = 0; w < kT / 32; ++w) s += sh[w][threadIdx.x];
+    part[4 * blockIdx.x + threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void grid_total(const double* part, double* out4, double (*sh)[4]) {
+  if (threadIdx.x < 32) {
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a[k] += __ldcg(part + 4 * b + k);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) sh[0][k] = a[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) out4[k] = sh[0][k];
+  __syncthreads();
+}
+
+// chi2 partial of this thread: thread per edge, value-only residuals at estimate S
+__device__ __forceinline__ double chi2_part(const PgoArgs& a, const double* S) {
+  double acc = 0.0;
+  for (int e = blockIdx.x * kT + threadIdx.x; e < a.n_e; e += gridDim.x * kT) {
+    const int i = a.eij[2 * e], j = a.eij[2 * e + 1];
+    double M[13], Si[13], Sj[13], Q[13], r[7];
+#pragma unroll
+    for (int k = 0; k < 13; ++k) {
+      M[k] = a.M[13 * (size_t)e + k];
+      Si[k] = __ldcg(S + 13 * (size_t)i + k);
+      Sj[k] = __ldcg(S + 13 * (size_t)j + k);
+    }
+    edge_value(M, Si, Sj, Q, r);
+    double c = 0.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) c += r[k] * r[k];
+    acc += c;
+  }
+  return acc;
+}
+
+// hat(g) for the 3-vector g
+__device__ __forceinline__ void hat3(const double* g, double* H) {
+  H[0] = 0.0; H[1] = -g[2]; H[2] = g[1];
+  H[3] = g[2]; H[4] = 0.0; H[5] = -g[0];
+  H[6] = -g[1]; H[7] = g[0]; H[8] = 0.0;
+}
+__device__ __forceinline__ void mat3(const double* A, const double* B, double* o) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) o[3 * i + j] = (A[3 * i] * B[j] + A[3 * i + 1] * B[3 + j]) + A[3 * i + 2] * B[6 + j];
+}
+
+// linearise: 16-lane group per edge -> record
+__device__ void linearise(const PgoArgs& a, const double* S, double* shJ) {
+  const int lane16 = threadIdx.x & 15;
+  const int grp = (blockIdx.x * kT + threadIdx.x) >> 4, ngrp = (gridDim.x * kT) >> 4;
+  double* J = shJ + (threadIdx.x >> 4) * 112;   // [14][7] columns + e[7]
+  const unsigned mask = 0xffffu << (threadIdx.x & 16);
+  for (int e = grp; e < a.n_e; e += ngrp) {
+    const int i = a.eij[2 * e], j = a.eij[2 * e + 1];
+    double M[13], Si[13], Sj[13], Q[13], P[13], Sji[13], T1[13];
+#pragma unroll
+    for (int k = 0; k < 13; ++k) {
+      M[k] = a.M[13 * (size_t)e + k];
+      Si[k] = __ldcg(S + 13 * (size_t)i + k);
+      Sj[k] = __ldcg(S + 13 * (size_t)j + k);
+    }
+    lc_sim3_compose(M, Si, T1);
+    lc_sim3_inverse(Sj, Sji);
+    lc_sim3_compose(T1, Sji, Q);
+    if (lane16 < 14) {
+      const int k = lane16 < 7 ? lane16 : lane16 - 7;
+      const bool fixed_v = a.fixed[lane16 < 7 ? i : j] != 0;
+      double g[7] = {0, 0, 0, 0, 0, 0, 0};
+      g[k] = 1.0;
+      double Hg[9], dR[9], dt[3], ds;
+      hat3(g, Hg);
+      if (lane16 < 7) {
+        // d/d delta_i of M o exp(delta) o P, P = S_i o S_j^-1
+        lc_sim3_compose(Si, Sji, P);
+        double tmp[9];
+        mat3(M, Hg, tmp);
+        mat3(tmp, P, dR);
+        double u[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) u[r] = ((g[6] * P[9 + r] + lc_row3(Hg + 3 * r, P + 9)) + g[3 + r]);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) dt[r] = M[12] * lc_row3(M + 3 * r, u);
+        ds = (M[12] * g[6]) * P[12];
+      } else {
+        // d/d delta_j of Q o exp(-delta)
+#pragma unroll
+        for (int r = 0; r < 9; ++r) dR[r] = 0.0;
+        double tmp[9];
+        mat3(Q, Hg, tmp);
+#pragma unroll
+        for (int r = 0; r < 9; ++r) dR[r] = -tmp[r];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) dt[r] = -(Q[12] * lc_row3(Q + 3 * r, g + 3));
+        ds = -(Q[12] * g[6]);
+      }
+      dd R[9], t[3], x[7];
+#pragma unroll
+      for (int r = 0; r < 9; ++r) R[r] = {Q[r], dR[r]};
+#pragma unroll
+      for (int r = 0; r < 3; ++r) t[r] = {Q[9 + r], dt[r]};
+      sim3_log<dd>(R, t, dd{Q[12], ds}, x);
+#pragma unroll
+      for (int r = 0; r < 7; ++r) J[7 * lane16 + r] = fixed_v ? 0.0 : x[r].d;
+      if (lane16 == 0)
+#pragma unroll
+        for (int r = 0; r < 7; ++r) J[98 + r] = x[r].v;
+    }
+    __syncwarp(mask);
+    double* R = a.rec + (size_t)e * kRec;
+    for (int o = lane16; o < 211; o += 16) {
+      double v = 0.0;
+      if (o < 196) {
+        const int blk = o / 49, ab = o - 49 * blk, r = ab / 7, c = ab - 7 * r;
+        // Hii: (i, i); Hjj: (j, j); Hij: (i row, j col); Hji: (j row, i col)
+        const int cr = (blk == 0 || blk == 2) ? r : 7 + r;
+        const int cc = (blk == 0 || blk == 3) ? c : 7 + c;
+#pragma unroll
+        for (int q = 0; q < 7; ++q) v += J[7 * cr + q] * J[7 * cc + q];
+      } else if (o < 210) {
+        const int col = o - 196;   // 0..6 vertex i, 7..13 vertex j
+#pragma unroll
+        for (int q = 0; q < 7; ++q) v += J[7 * col + q] * J[98 + q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 7; ++q) v += J[98 + q] * J[98 + q];
+      }
+      R[o] = v;
+    }
+    __syncwarp(mask);
+  }
+}
+
+__device__ __forceinline__ double vget(const double* base, int v, int r) {
+  return __ldcg(base + (size_t)v * kVec + r);
+}
+
+// z = (L L^T)^-1 r for vertex v, every lane of the group computes all 7 and keeps its own
+__device__ __forceinline__ double precond(const double* L, const double* rv, int lane) {
+  double y[7];
+#pragma unroll
+  for (int i = 0; i < 7; ++i) {
+    double s = rv[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) s -= L[i * (i + 1) / 2 + k] * y[k];
+    y[i] = s / L[i * (i + 1) / 2 + i];
+  }
+#pragma unroll
+  for (int i = 6; i >= 0; --i) {
+    double s = y[i];
+#pragma unroll
+    for (int k = i + 1; k < 7; ++k) s -= L[k * (k + 1) / 2 + i] * y[k];
+    y[i] = s / L[i * (i + 1) / 2 + i];
+  }
+  double out = 0.0;
+#pragma unroll
+  for (int i = 0; i < 7; ++i) out = (lane == i) ? y[i] : out;
+  return out;
+}
+
+__global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
+  __shared__ double shJ[(kT / 16) * 112];
+  __shared__ double shR[kT / 32][4];
+  unsigned int bt = 0;
+  const int tid = blockIdx.x * kT + threadIdx.x, nth = gridDim.x * kT;
+  const int lane8 = threadIdx.x & 7, g8 = tid >> 3, ng8 = nth >> 3;
+  const unsigned m8 = 0xffu << (threadIdx.x & 24);
+  const int warp = tid >> 5, nwarp = nth >> 5, lane = threadIdx.x & 31;
+  double* X = a.vx;
+  double* Rr = a.vx + (size_t)a.n_v * kVec;
+  double* Z = a.vx + 2 * (size_t)a.n_v * kVec;
+  double* Pp = a.vx + 3 * (size_t)a.n_v * kVec;
+  double* Qq = a.vx + 4 * (size_t)a.n_v * kVec;
+
+  for (int k = tid; k < 13 * a.n_v; k += nth) {
+    const double s = a.S_in[k];
+    a.S_out[k] = s;
+    a.S_tmp[k] = s;
+  }
+  grid_barrier(a.bar, bt);
+  double* S = a.S_out;
+  double* St = a.S_tmp;
+  double tot[4];
+  cta_partial(chi2_part(a, S), 0.0, 0.0, 0.0, a.part, shR);
+  grid_barrier(a.bar, bt);
+  grid_total(a.part, tot, shR);
+  double chi2 = tot[0];
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  if (lead && a.chi2_out) a.chi2_out[0] = chi2;
+  double lambda = a.lambda0;
+  int stop = chi2 == 0.0 ? 5 : 0, it = 0, accepted = 0;
+  long long cg_total = 0;
+  bool relin = true;
+  while (!stop) {
+    if (it >= a.max_iter) { stop = 3; break; }
+    if (relin) {
+      linearise(a, S, shJ);
+      grid_barrier(a.bar, bt);
+      // assemble: warp per vertex, lanes over the 56 outputs
+      for (int v = warp; v < a.n_v; v += nwarp) {
+        const bool fx = a.fixed[v] != 0;
+        const int b0 = a.vbeg[v], b1 = a.vbeg[v + 1];
+        for (int o = lane; o < kVD; o += 32) {
+          double s = 0.0;
+          if (fx) {
+            s = (o < 49 && (o / 7) == (o % 7)) ? 1.0 : 0.0;
+          } else {
+            for (int q = b0; q < b1; ++q) {
+              const int w = a.vinc[q], e = w >> 1, role = w & 1;
+              const int off = o < 49 ? (role ? kOffHjj : kOffHii) + o : (role ? kOffBj : kOffBi) + (o - 49);
+              s += __ldcg(a.rec + (size_t)e * kRec + off);
+            }
+          }
+          a.vd[(size_t)v * kVD + o] = s;
+        }
+      }
+      relin = false;
+      grid_barrier(a.bar, bt);
+    }
+    // damped diagonal blocks -> Cholesky factors; x = 0, r = -b, z = P r, p = z
+    double fail = 0.0, rz = 0.0, bb = 0.0;
+    for (int v = g8; v < a.n_v; v += ng8) {
+      const double* D = a.vd + (size_t)v * kVD;
+      double* L = a.vl + (size_t)v * kVL;
+      int okv = 1;
+      if (lane8 == 0) {
+        double Ld[28];
+        for (int i = 0; i < 7 && okv; ++i)
+          for (int j = 0; j <= i; ++j) {
+            double s = __ldcg(D + 7 * i + j);
+            if (i == j) s = s + lambda * s;
+            for (int k = 0; k < j; ++k) s -= Ld[i * (i + 1) / 2 + k] * Ld[j * (j + 1) / 2 + k];
+            if (i == j) {
+              if (!(s > 0.0)) { okv = 0; break; }
+              Ld[i * (i + 1) / 2 + i] = sqrt(s);
+            } else {
+              Ld[i * (i + 1) / 2 + j] = s / Ld[j * (j + 1) / 2 + j];
+            }
+          }
+        if (okv)
+          for (int k = 0; k < 28; ++k) L[k] = Ld[k];
+      }
+      okv = __shfl_sync(m8, okv, threadIdx.x & 24);
+      if (!okv) { fail = 1.0; continue; }
+      __syncwarp(m8);
+      const double bv = lane8 < 7 ? __ldcg(D + 49 + lane8) : 0.0;
+      double rv[7];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) rv[i] = -__shfl_sync(m8, bv, (threadIdx.x & 24) + i);
+      const double zl = precond(L, rv, lane8);
+      if (lane8 < 7) {
+        X[(size_t)v * kVec + lane8] = 0.0;
+        Rr[(size_t)v * kVec + lane8] = -bv;
+        Z[(size_t)v * kVec + lane8] = zl;
+        Pp[(size_t)v * kVec + lane8] = zl;
+        rz += (-bv) * zl;
+        bb += bv * bv;
+      }
+    }
+    cta_partial(fail, rz, bb, 0.0, a.part, shR);
+    grid_barrier(a.bar, bt);
+    grid_total(a.part, tot, shR);
+    ++it;
+    double* row = (lead && a.trace) ? a.trace + 6 * (size_t)(it - 1) : nullptr;
+    if (row) { row[0] = chi2; row[1] = lambda; row[2] = -1.0; row[3] = 0.0; row[4] = -1.0; row[5] = 0.0; }
+    if (tot[0] != 0.0) {
+      lambda *= 4.0;
+      if (lambda > 1e8) stop = 4;
+      continue;
+    }
+    rz = tot[1];
+    bb = tot[2];
+    double xx = 0.0;
+    int k = 0;
+    bool bad = false;
+    const double stop2 = (a.cg_tol * a.cg_tol) * bb;
+    double rr = bb;
+    while (k < a.cg_max && rr > stop2) {
+      // q = (H + lambda diag H) p
+      double pq = 0.0;
+      for (int v = g8; v < a.n_v; v += ng8) {
+        if (lane8 >= 7) continue;
+        const double* D = a.vd + (size_t)v * kVD + 7 * lane8;
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < 7; ++c) s += __ldcg(D + c) * vget(Pp, v, c);
+        s += lambda * __ldcg(D + lane8) * vget(Pp, v, lane8);
+        if (!a.fixed[v]) {
+          const int b0 = a.vbeg[v], b1 = a.vbeg[v + 1];
+          for (int q = b0; q < b1; ++q) {
+            const int w = a.vinc[q], e = w >> 1, role = w & 1;
+            const int o = role ? a.eij[2 * e] : a.eij[2 * e + 1];
+            const double* B = a.rec + (size_t)e * kRec + (role ? kOffHji : kOffHij) + 7 * lane8;
+            double t = 0.0;
+#pragma unroll
+            for (int c = 0; c < 7; ++c) t += __ldcg(B + c) * vget(Pp, o, c);
+            s += t;
+          }
+        }
+        Qq[(size_t)v * kVec + lane8] = s;
+        pq += vget(Pp, v, lane8) * s;
+      }
+      cta_partial(pq, 0.0, 0.0, 0.0, a.part, shR);
+      grid_barrier(a.bar, bt);
+      grid_total(a.part, tot, shR);
+      pq = tot[0];
+      if (!(pq > 0.0)) { bad = true; break; }
+      const double alpha = rz / pq;
+      double rzn = 0.0, rrn = 0.0, xxn = 0.0;
+      for (int v = g8; v < a.n_v; v += ng8) {
+        const size_t o = (size_t)v * kVec + lane8;
+        double rl = 0.0;
+        if (lane8 < 7) {
+          const double xl = X[o] + alpha * Pp[o];
+          X[o] = xl;
+          rl = Rr[o] - alpha * Qq[o];
+          Rr[o] = rl;
+          xxn += xl * xl;
+          rrn += rl * rl;
+        }
+        double rv[7];
+#pragma unroll
+        for (int i = 0; i < 7; ++i) rv[i] = __shfl_sync(m8, rl, (threadIdx.x & 24) + i);
+        const double zl = precond(a.vl + (size_t)v * kVL, rv, lane8);
+        if (lane8 < 7) {
+          Z[o] = zl;
+          rzn += rl * zl;
+        }
+      }
+      cta_partial(rzn, rrn, xxn, 0.0, a.part, shR);
+      grid_barrier(a.bar, bt);
+      grid_total(a.part, tot, shR);
+      ++k;
+      const double beta = tot[0] / rz;
+      rz = tot[0];
+      rr = tot[1];
+      xx = tot[2];
+      if (k >= a.cg_max || rr <= stop2) break;
+      for (int v = g8; v < a.n_v; v += ng8) {
+        if (lane8 >= 7) continue;
+        const size_t o = (size_t)v * kVec + lane8;
+        Pp[o] = Z[o] + beta * Pp[o];
+      }
+      grid_barrier(a.bar, bt);
+    }
+    cg_total += k;
+    if (row) row[5] = (double)k;
+    if (bad) {
+      lambda *= 4.0;
+      if (lambda > 1e8) stop = 4;
+      continue;
+    }
+    const double dn = sqrt(xx);
+    if (row) row[4] = dn;
+    if (dn < a.eps_dx) {
+      if (row) row[2] = chi2;
+      stop = 1;
+      break;
+    }
+    // trial estimate
+    for (int v = tid; v < a.n_v; v += nth) {
+      if (a.fixed[v]) continue;
+      double d[7], E[13], Sv[13], o[13];
+#pragma unroll
+      for (int r = 0; r < 7; ++r) d[r] = __ldcg(X + (size_t)v * kVec + r);
+#pragma unroll
+      for (int r = 0; r < 13; ++r) Sv[r] = __ldcg(S + 13 * (size_t)v + r);
+      sim3_exp(d, E);
+      lc_sim3_compose(E, Sv, o);
+#pragma unroll
+      for (int r = 0; r < 13; ++r) St[13 * (size_t)v + r] = o[r];
+    }
+    grid_barrier(a.bar, bt);
+    cta_partial(chi2_part(a, St), 0.0, 0.0, 0.0, a.part, shR);
+    grid_barrier(a.bar, bt);
+    grid_total(a.part, tot, shR);
+    const double chi2t = tot[0];
+    if (row) row[2] = chi2t;
+    if (chi2t < chi2) {
+      if (row) row[3] = 1.0;
+      ++accepted;
+      const double rel = (chi2 - chi2t) / chi2;
+      double* sw = S; S = St; St = sw;
+      chi2 = chi2t;
+      lambda = lambda * 0.5 < 1e-12 ? 1e-12 : lambda * 0.5;
+      relin = true;
+      if (rel < a.eps_chi2) stop = 2;
+      // the rejected buffer must equal the new estimate on free vertices before the next
+      // trial overwrites them: trial writes every free vertex, fixed ones are equal in both
+    } else {
+      lambda *= 4.0;
+      if (lambda > 1e8) stop = 4;
+    }
+  }
+  if (S != a.S_out)
+    for (int k = tid; k < 13 * a.n_v; k += nth) a.S_out[k] = __ldcg(S + k);
+  if (lead) {
+    if (a.chi2_out) a.chi2_out[1] = chi2;
+    a.counts[LC_COUNT_PGO_ITERS] = (unsigned long long)it;
+    a.counts[LC_COUNT_PGO_ACCEPTED] = (unsigned long long)accepted;
+    a.counts[LC_COUNT_PGO_SOLVER_ITERS] = (unsigned long long)cg_total;
+    a.counts[LC_COUNT_PGO_STOP] = (unsigned long long)stop;
+  }
+}
+
+}  // namespace
+
+size_t pgo_scratch_bytes(int n_v, int n_e, int grid) {
+  const size_t d = (size_t)n_e * kRec + (size_t)n_v * (kVD + kVL + 5 * kVec + 13) + 4 * (size_t)grid;
+  return sizeof(double) * d + 256;
+}
+
+int pgo_grid(lc_ctx* c, int n_v, int n_e) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pgo, kT, 0);
+  (void)c;
+  const int64_t work = std::max<int64_t>((int64_t)n_e * 16, (int64_t)n_v * 8);
+  const int need = (int)std::max<int64_t>(1, (work + kT - 1) / kT);
+  return std::max(1, std::min(need, sms * std::max(per, 1)));
+}
+
+cudaError_t launch_pgo(lc_ctx* c, int n_v, int n_e, const int32_t* d_eij, const double* d_M, const double* d_S_in,
+                       const uint8_t* d_fixed, const int32_t* d_vbeg, const int32_t* d_vinc,
+                       const lc_pgo_params& p, double* d_S_out, void* scratch, int grid, double* d_trace,
+                       double* d_chi2, unsigned long long* counts, cudaStream_t s) {
+  PgoArgs a;
+  a.n_v = n_v; a.n_e = n_e; a.max_iter = p.max_iter; a.cg_max = p.cg_max_iter;
+  a.lambda0 = p.lambda0; a.eps_dx = p.eps_dx; a.eps_chi2 = p.eps_chi2; a.cg_tol = p.cg_tol;
+  a.eij = d_eij; a.M = d_M; a.S_in = d_S_in; a.fixed = d_fixed; a.vbeg = d_vbeg; a.vinc = d_vinc;
+  a.S_out = d_S_out;
+  double* base = (double*)scratch;
+  a.rec = base; base += (size_t)n_e * kRec;
+  a.vd = base; base += (size_t)n_v * kVD;
+  a.vl = base; base += (size_t)n_v * kVL;
+  a.vx = base; base += (size_t)n_v * 5 * kVec;
+  a.S_tmp = base; base += (size_t)n_v * 13;
+  a.part = base; base += 4 * (size_t)grid;
+  a.bar = (unsigned int*)base;
+  a.trace = d_trace; a.chi2_out = d_chi2; a.counts = counts;
+  cudaError_t e = cudaMemsetAsync(a.bar, 0, 256, s);
+  if (e != cudaSuccess) return e;
+  void* args[] = {&a};
+  e = cudaLaunchCooperativeKernel((const void*)k_pgo, dim3(grid), dim3(kT), args, 0, s);
+  c->launches++;
+  return e;
+}

@@ -887,6 +887,73 @@ lc_status lc_sim3_refine(lc_ctx* c, int32_t n_prob, const int32_t* prob_begin, c
   });
 }
 
+lc_status lc_pgo_sim3(lc_ctx* c, int32_t n_v, const lc_sim3* S_init, const uint8_t* fixed, int32_t n_e,
+                      const int32_t* edge_ij, const lc_sim3* M, const lc_pgo_params* params, lc_sim3* out_S,
+                      double* out_trace, double* out_chi2, int64_t* out_counts, void* stream) {
+  return guarded(c, [&] {
+    capture_gate(c, stream, false);
+    REQUIRE(params, LC_EINVAL, "null params");
+    const lc_pgo_params p = *params;
+    REQUIRE(n_v >= 0 && n_e >= 0 && p.max_iter >= 0 && p.cg_max_iter >= 1 && p.lambda0 > 0.0 &&
+                p.eps_dx >= 0.0 && p.eps_chi2 >= 0.0 && p.cg_tol >= 0.0,
+            LC_EINVAL, "bad sizes / parameters");
+    REQUIRE(n_v == 0 || (S_init && fixed && out_S), LC_EINVAL, "null vertex array");
+    REQUIRE(n_e == 0 || (edge_ij && M), LC_EINVAL, "null edge array");
+    // incidence lists (symbolic structure of the block-sparse system): per vertex, its
+    // edges in ascending edge order, tagged with the vertex's role (0: i, 1: j)
+    std::vector<int32_t> vbeg((size_t)n_v + 1, 0), vinc((size_t)2 * n_e);
+    for (int32_t e = 0; e < n_e; ++e) {
+      const int32_t i = edge_ij[2 * e], j = edge_ij[2 * e + 1];
+      REQUIRE(i >= 0 && i < n_v && j >= 0 && j < n_v, LC_ERANGE, "edge vertex out of range");
+      REQUIRE(i != j, LC_EINVAL, "edge with i == j");
+      vbeg[i + 1]++;
+      vbeg[j + 1]++;
+    }
+    for (int32_t v = 0; v < n_v; ++v) vbeg[v + 1] += vbeg[v];
+    {
+      std::vector<int32_t> cur(vbeg.begin(), vbeg.end() - 1);
+      for (int32_t e = 0; e < n_e; ++e) {
+        vinc[cur[edge_ij[2 * e]]++] = (e << 1);
+        vinc[cur[edge_ij[2 * e + 1]]++] = (e << 1) | 1;
+      }
+    }
+    Call call(c, stream);
+    unsigned long long* cnt = call.counts(out_counts, LC_NCOUNT);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(uint64_t) * LC_NCOUNT, call.s));
+    if (n_v == 0) {
+      if (out_chi2) {
+        double* dc = call.out(out_chi2, 2);
+        CK(cudaMemsetAsync(dc, 0, 2 * sizeof(double), call.s));
+      }
+      call.finish();
+      return;
+    }
+    const int32_t *d_eij = nullptr, *d_vbeg = nullptr, *d_vinc = nullptr;
+    const uint8_t* d_fixed = nullptr;
+    call.arg(fixed, (size_t)n_v, &d_fixed);
+    call.arg(vbeg.data(), vbeg.size(), &d_vbeg);
+    if (n_e > 0) {
+      call.arg(edge_ij, (size_t)2 * n_e, &d_eij);
+      call.arg(vinc.data(), vinc.size(), &d_vinc);
+    }
+    call.commit();
+    const double* dM = call.in((const double*)M, 13 * (size_t)n_e);
+    const double* dS0 = call.in((const double*)S_init, 13 * (size_t)n_v);
+    double* dS = (double*)call.out((double*)out_S, 13 * (size_t)n_v);
+    double* dT = out_trace ? call.out(out_trace, 6 * (size_t)std::max(p.max_iter, 1)) : nullptr;
+    double* dC = out_chi2 ? call.out(out_chi2, 2) : nullptr;
+    if (dT) CK(cudaMemsetAsync(dT, 0, 6 * sizeof(double) * std::max(p.max_iter, 1), call.s));
+    const int grid = pgo_grid(c, n_v, n_e);
+    void* scr = call.scratch(pgo_scratch_bytes(n_v, n_e, grid));
+    {
+      Prof pr(c, LC_PROF_PGO, call.s);
+      CK(launch_pgo(c, n_v, n_e, d_eij, dM, dS0, d_fixed, d_vbeg, d_vinc, p, dS, scr, grid, dT, dC, cnt,
+                    call.s));
+    }
+    call.finish();
+  });
+}
+
 lc_status lc_state_save(lc_ctx* c, void* stream) {
   return guarded(c, [&] {
     capture_gate(c, stream, false);

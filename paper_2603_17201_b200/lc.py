@@ -357,6 +357,40 @@ class Context:
             return S, inl, mask, counts_dict(cnt)
         return S.view(n_prob, 13), inl, mask, cnt
 
+    # -- lc_pgo_sim3 ----------------------------------------------------------------
+    def pgo_sim3(self, S_init, fixed, edges, M, max_iter=20, cg_max_iter=500, lambda0=1e-4, eps_dx=1e-8,
+                 eps_chi2=1e-10, cg_tol=1e-10, host=True):
+        """Essential-graph Sim3 Levenberg-Marquardt: (S [n_v, 13], trace [iters, 6],
+        (chi2_0, chi2_final), counts). With host=False S/trace/chi2/counts are device
+        tensors (trace [max_iter, 6], counts raw)."""
+        k = self._keep(host)
+        n_v = int(len(S_init)) if not isinstance(S_init, torch.Tensor) else int(S_init.numel() // 13)
+        E = np.ascontiguousarray(edges, np.int32).reshape(-1, 2)
+        n_e = len(E)
+        fx = np.ascontiguousarray(fixed, np.uint8)
+        prm = _lib.lc_pgo_params(int(max_iter), int(cg_max_iter), float(lambda0), float(eps_dx),
+                                 float(eps_chi2), float(cg_tol))
+        rows = max(int(max_iter), 1)
+        if host:
+            S = np.zeros((n_v, 13), np.float64)
+            tr = np.zeros((rows, 6), np.float64)
+            c2 = np.zeros(2, np.float64)
+            cnt = np.zeros(LC_NCOUNT, np.int64)
+        else:
+            S = self._dev(n_v * 13, torch.float64)
+            tr = self._dev(rows * 6, torch.float64)
+            c2 = self._dev(2, torch.float64)
+            cnt = self._dev(LC_NCOUNT, torch.int64)
+        st = self.lib.lc_pgo_sim3(self.h, n_v, k.ptr(S_init, np.float64), k.ptr(fx), n_e, k.ptr(E),
+                                  k.ptr(M, np.float64), C.byref(prm), k.ptr(S), k.ptr(tr), k.ptr(c2),
+                                  k.ptr(cnt), self._stream())
+        self._check("lc_pgo_sim3", st)
+        if host:
+            self.synchronize()
+            cd = counts_dict(cnt)
+            return S, tr[:cd["pgo_iters"]], (float(c2[0]), float(c2[1])), cd
+        return S.view(n_v, 13), tr.view(rows, 6), c2, cnt
+
     # -- lc_correct_sim3 ----------------------------------------------------------
     def correct_window(self, cur_kf, S_cw_corr, window, host=True):
         k = self._keep(host)
