@@ -201,7 +201,7 @@ def cpu_baseline(w, seconds):
 def main():
     args = parse()
     ws, rank, local = dist_env()
-    from lcsynth import make_world
+    from lcsynth import make_pose_graph, make_world
     if args.impl == "reference":
         if rank != 0:
             return
@@ -429,7 +429,7 @@ def main():
 
     # secondary: SURVEY §8 a9, batched read-only guided search on C4 (32 hypotheses x
     # (current KF + 3 covisible) pairs, PS2a / PS2b / PS1-3 parameter sets)
-    sbp = ransac = None
+    sbp = ransac = pgo = None
     if ws == 1 and not args.profile_only and not args.no_sbp:
         from lcsynth.world import SBP_PARAMS
         w4 = make_world("C4", args.seed)
@@ -496,6 +496,30 @@ def main():
                   "ms_per_call": round(float(np.mean(rms)), 5),
                   "refine_ms_per_call": round(float(np.mean(fms)), 5),
                   "refine_steps": int(rf4[counts.index("refine_iters")])}
+        # essential-graph Sim3 pose-graph optimisation (the producer of the
+        # S_opt that lc_correct_sim3 ALL propagates) on the C3- and C5-sized graphs
+        pgo = {}
+        for gname, nrun in (("C3", max(2, min(args.steps, 3))), ("C5", 2)):
+            g = make_pose_graph(gname, args.seed)
+            gS, gM = torch.from_numpy(g.S_init).to(dev), torch.from_numpy(g.M).to(dev)
+            pms = []
+            for i in range(1 + nrun):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                pr = c4.pgo_sim3(gS, g.fixed, g.edges, gM, max_iter=20, host=False)
+                b.record(stream)
+                b.synchronize()
+                if i >= 1:
+                    pms.append(a.elapsed_time(b))
+            pc = pr[3].cpu().numpy()
+            p2 = pr[2].cpu().numpy()
+            pgo[gname] = {"keyframes": g.n_v, "edges": g.n_e, "ms_per_call": round(float(np.mean(pms)), 3),
+                          "lm_iterations": int(pc[counts.index("pgo_iters")]),
+                          "accepted": int(pc[counts.index("pgo_accepted")]),
+                          "solver_iterations": int(pc[counts.index("pgo_solver_iters")]),
+                          "chi2": [float(p2[0]), float(p2[1])],
+                          "solver": "banded Cholesky (RCM order)" if pc[counts.index("pgo_solver_iters")]
+                          == pc[counts.index("pgo_iters")] else "block-Jacobi CG"}
         sbp = {"config": f"C4: {len(w4.pair_kf)} (hypothesis, keyframe) pairs, "
                          f"{len(w4.pair_mp_list)} queries, 3 parameter sets",
                "ms_per_call": round(s_ms, 5), "candidates": cand4,
@@ -533,6 +557,7 @@ def main():
             "refresh": refresh,
             "connections": connections,
             "ransac": ransac,
+            "pgo": pgo,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -519,16 +519,17 @@ lc_status lc_search_by_projection(lc_ctx* ctx, int32_t n_pairs, const int32_t* p
  *     e = log(M o S_i o S_j^-1) (7-vector (omega, upsilon, sigma), A49/A50), identity
  *     information; chi2 = sum_e |e|^2. Updates S <- exp(delta) o S.
  *   Levenberg-Marquardt (A52/A53): linearise (Jacobians by forward-mode dual numbers),
- *     solve (H + lambda diag(H)) delta = -b over the free vertices by block-Jacobi
- *     preconditioned conjugate gradients (A54: stop when |r| <= cg_tol |b| or after
- *     cg_max_iter; a non-SPD diagonal block or p^T A p <= 0 is a failed solve ->
- *     lambda *= 4). |delta| < eps_dx stops; a trial exp(delta_v) o S_v is accepted iff
+ *     solve (H + lambda diag(H)) delta = -b over the free vertices (A54) by a banded
+ *     Cholesky factorisation in a reverse Cuthill-McKee order (a non-positive pivot is
+ *     a failed solve -> lambda *= 4), or by block-Jacobi preconditioned conjugate
+ *     gradients (stop when |r| <= cg_tol |b| or after cg_max_iter; a non-SPD diagonal
+ *     block or p^T A p <= 0 is a failed solve); params->solver selects. |delta| < eps_dx stops; a trial exp(delta_v) o S_v is accepted iff
  *     chi2 decreases (lambda <- max(lambda / 2, 1e-12); stop when the relative
  *     decrease < eps_chi2), else lambda *= 4; lambda > 1e8 stops; max_iter solves.
  *   out_S [host|dev] [n_v] the optimised estimates (fixed vertices unchanged).
  *   out_trace [host|dev] nullable [max_iter][6] per iteration: chi2, lambda, trial
  *     chi2 (-1: solve failed; chi2 when the |delta| test stopped), accepted (0/1),
- *     |delta| (-1 if failed), CG iterations.
+ *     |delta| (-1 if failed), solver iterations (CG iterations; 1 for the banded solve).
  *   out_chi2 [host|dev] nullable [2]: initial and final chi2.
  *   out_counts [host|dev] nullable [LC_NCOUNT] (PGO_ITERS, PGO_ACCEPTED,
  *     PGO_SOLVER_ITERS, PGO_STOP).
@@ -545,7 +546,15 @@ typedef struct {
   double eps_dx;         /* stop when |delta| < eps_dx (1e-8)                            */
   double eps_chi2;       /* stop when an accepted step lowers chi2 by < eps_chi2 relative */
   double cg_tol;         /* CG relative residual target (1e-10)                          */
+  int32_t solver;        /* LC_PGO_SOLVER_AUTO / _BAND / _CG                              */
+  int32_t reserved;
 } lc_pgo_params;
+
+/* Linear solver of lc_pgo_sim3 (A54). AUTO: the banded Cholesky when the reverse
+ * Cuthill-McKee ordering of the free vertices has a block bandwidth <= 28 (the
+ * shared-memory window of one CTA), else CG. BAND: banded Cholesky (LC_EINVAL if the
+ * bandwidth exceeds 28). CG: block-Jacobi preconditioned conjugate gradients. */
+enum { LC_PGO_SOLVER_AUTO = 0, LC_PGO_SOLVER_BAND = 1, LC_PGO_SOLVER_CG = 2 };
 
 enum { LC_PGO_STOP_DX = 1, LC_PGO_STOP_CHI2 = 2, LC_PGO_STOP_MAX_ITER = 3, LC_PGO_STOP_LAMBDA = 4,
        LC_PGO_STOP_ZERO = 5 };

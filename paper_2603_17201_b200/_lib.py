@@ -72,7 +72,8 @@ class lc_query_debug(C.Structure):
 
 class lc_pgo_params(C.Structure):
     _fields_ = [("max_iter", C.c_int32), ("cg_max_iter", C.c_int32), ("lambda0", C.c_double),
-                ("eps_dx", C.c_double), ("eps_chi2", C.c_double), ("cg_tol", C.c_double)]
+                ("eps_dx", C.c_double), ("eps_chi2", C.c_double), ("cg_tol", C.c_double),
+                ("solver", C.c_int32), ("reserved", C.c_int32)]
 
 
 class LcError(RuntimeError):

@@ -34,6 +34,7 @@ constexpr int kOffHii = 0, kOffHjj = 49, kOffHij = 98, kOffHji = 147, kOffBi = 1
 constexpr int kVD = 56;        // per-vertex diagonal block (49) + gradient (7)
 constexpr int kVL = 28;        // per-vertex Cholesky factor of the damped diagonal block
 constexpr int kVec = 8;        // padded 7-vectors
+constexpr int kBWMax = 28;     // largest block bandwidth of the banded direct solve (435-block window)
 
 // ---------------------------------------------------------------------------
 // forward-mode dual number with one partial (A50): value and derivative along one seed
@@ -218,14 +219,23 @@ struct PgoArgs {
   const double* S_in;      // [n_v][13]
   const uint8_t* fixed;    // [n_v]
   const int32_t* vbeg;     // [n_v+1] incidence CSR
-  const int32_t* vinc;     // [2 n_e] (edge << 1) | role (0: vertex is i, 1: vertex is j), ascending edge
+  const int2* vinc2;       // [2 n_e] ((edge << 1) | role (0: vertex is i, 1: j), other vertex), ascending edge
   double* S_out;           // [n_v][13] estimate (buffer 0)
   double* S_tmp;           // [n_v][13] (buffer 1)
   double* rec;             // [n_e][kRec]
   double* vd;              // [n_v][kVD]
   double* vl;              // [n_v][kVL]
-  double* vx;              // 5 vectors [n_v][kVec]: x, r, z, p, q
+  double* vx;              // 6 vectors [n_v][kVec]: x, r, u, w, p, s
   double* part;            // [gridDim][4] per-CTA partial sums
+  // banded direct solve (A54): bw >= 0 selects it; pos/ord the host's reverse Cuthill-McKee
+  // ordering (free vertices first), bw its block bandwidth
+  int bw;
+  const int32_t* pos;      // [n_v] vertex -> position
+  const int32_t* ord;      // [n_v] position -> vertex
+  double* band;            // [n_v][bw+1][49] assembled H in band storage: (p + d, p) blocks
+  double* lband;           // [n_v][bw+1][49] Cholesky factor, same layout
+  double* yb;              // [n_v][8] forward-substitution result
+  double* bres;            // [2] fail flag, |delta|^2
   unsigned int* bar;       // grid barrier counter (zeroed before launch)
   double* trace;           // [max_iter][6] or null
   double* chi2_out;        // [2] or null
@@ -240,9 +250,11 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int& ta
     __threadfence();
     atomicAdd(bar, 1u);
     unsigned int v;
-    do {
+    for (;;) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while ((int)(v - target) < 0);
+      if ((int)(v - target) >= 0) break;
+      __nanosleep(32);
+    }
     __threadfence();
   }
   __syncthreads();
@@ -437,9 +449,312 @@ __device__ __forceinline__ double precond(const double* L, const double* rv, int
   return out;
 }
 
+// row lane8 of (H + lambda diag H) y at vertex v: diagonal block, then the off-diagonal
+// blocks of the incident edges in ascending edge order (incidences loaded 4 at a time so
+// their block-row and neighbour loads are in flight together)
+__device__ __forceinline__ double spmv_row(const PgoArgs& a, int v, int lane8, const double* y, double lambda) {
+  const double* D = a.vd + (size_t)v * kVD + 7 * lane8;
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 7; ++c) s += __ldcg(D + c) * vget(y, v, c);
+  s += lambda * __ldcg(D + lane8) * vget(y, v, lane8);
+  if (a.fixed[v]) return s;
+  const int b0 = a.vbeg[v], b1 = a.vbeg[v + 1];
+  for (int q0 = b0; q0 < b1; q0 += 4) {
+    int2 w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = q0 + u < b1 ? __ldcg(a.vinc2 + q0 + u) : make_int2(-1, 0);
+    double t[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      t[u] = 0.0;
+      if (w[u].x >= 0) {
+        const double* B = a.rec + (size_t)(w[u].x >> 1) * kRec + ((w[u].x & 1) ? kOffHji : kOffHij) + 7 * lane8;
+#pragma unroll
+        for (int c = 0; c < 7; ++c) t[u] += __ldcg(B + c) * vget(y, w[u].y, c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (w[u].x >= 0) s += t[u];
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// banded direct solve (A54). Positions p = pos[v] come from a reverse Cuthill-McKee
+// ordering with block bandwidth bw, so the damped matrix is block-banded: block (p+d, p)
+// nonzero only for d <= bw. band[p][d] holds it (d = 0: the vertex's diagonal block).
+// ---------------------------------------------------------------------------
+__device__ void band_assemble(const PgoArgs& a) {
+  const int NB = a.bw + 1;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * kT + threadIdx.x) >> 5, nwarp = (gridDim.x * kT) >> 5;
+  for (int p = warp; p < a.n_v; p += nwarp) {
+    const int v = a.ord[p];
+    double* Ab = a.band + (size_t)p * NB * 49;
+    for (int o = lane; o < NB * 49; o += 32) Ab[o] = o < 49 ? __ldcg(a.vd + (size_t)v * kVD + o) : 0.0;
+    __syncwarp();
+    if (a.fixed[v]) continue;
+    const int b0 = a.vbeg[v], b1 = a.vbeg[v + 1];
+    for (int q = b0; q < b1; ++q) {
+      const int2 w = __ldg(a.vinc2 + q);
+      if (a.fixed[w.y]) continue;
+      const int d = a.pos[w.y] - p;
+      if (d < 1) continue;
+      // block (rows other, cols v): Hji when v is i (role 0), Hij when v is j
+      const double* B = a.rec + (size_t)(w.x >> 1) * kRec + ((w.x & 1) ? kOffHij : kOffHji);
+      for (int o = lane; o < 49; o += 32) Ab[d * 49 + o] += __ldcg(B + o);
+      __syncwarp();
+    }
+  }
+}
+
+// CTA-wide: Cholesky of the damped band matrix, forward substitution fused; then back
+// substitution. The active window -- positions j..j+bw, lower-triangular blocks -- lives
+// in shared memory; a block (r, c), r >= c, sits at the unordered slot pair
+// (r mod NB, c mod NB), so the window needs NB (NB + 1) / 2 blocks and the position
+// that retires at step j frees exactly the slots the entering position j + NB takes.
+// x -> X (vertex order); writes bres = (fail, |x|^2).
+__device__ __forceinline__ int tri_slot(int a, int b) {
+  const int hi = a > b ? a : b, lo = a > b ? b : a;
+  return hi * (hi + 1) / 2 + lo;
+}
+__device__ __forceinline__ int wslot(int r, int c, int NB) { return tri_slot(r % NB, c % NB); }
+
+__device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* X) {
+  const int n = a.n_v, BW = a.bw, NB = BW + 1, t = threadIdx.x;
+  const int nw = NB * (NB + 1) / 2;
+  double* Wn = sm;                        // [nw][49] window blocks
+  double* Yw = Wn + (size_t)nw * 49;      // [NB][8]
+  double* Xs = Yw + NB * 8;               // [NB][8] back-substitution window
+  double* Lc = Xs + NB * 8;               // [NB][49] one factor column (back substitution)
+  double* part = Lc + NB * 49;            // [NB][8]
+  unsigned short* pairs = (unsigned short*)(part + NB * 8);   // [BW (BW + 1) / 2] (d1, d2)
+  __shared__ int s_fail;
+  if (t == 0) {
+    s_fail = 0;
+    int k = 0;
+    for (int d1 = 1; d1 <= BW; ++d1)
+      for (int d2 = d1; d2 <= BW; ++d2) pairs[k++] = (unsigned short)(d1 | (d2 << 8));
+  }
+  // block (r, c) of the damped matrix, entry e (0 if outside the matrix)
+  auto blk_val = [&](int r, int c, int e) -> double {
+    if (r >= n) return 0.0;
+    double v = __ldcg(a.band + ((size_t)c * NB + (r - c)) * 49 + e);
+    if (r == c && (e / 7) == (e % 7)) v = v + lambda * v;
+    return v;
+  };
+  auto rhs_val = [&](int q, int r) -> double {
+    return q < n ? -__ldcg(a.vd + (size_t)a.ord[q] * kVD + 49 + r) : 0.0;
+  };
+  for (int idx = t; idx < nw * 49; idx += kT) {
+    const int blk = idx / 49, e = idx - 49 * blk;
+    int r = 0;
+    while ((r + 1) * (r + 2) / 2 <= blk) ++r;
+    const int c = blk - r * (r + 1) / 2;    // initial window: positions 0..BW, slot = position
+    Wn[(size_t)blk * 49 + e] = r < NB ? blk_val(r, c, e) : 0.0;
+  }
+  if (t < NB * 8) Yw[t] = (t % 8) < 7 ? rhs_val(t / 8, t % 8) : 0.0;
+  __syncthreads();
+  const int per = (NB * 49 + kT - 1) / kT;
+  double pf[8];   // prefetched blocks of the entering position
+  for (int j = 0; j < n; ++j) {
+    const int q = j + NB;
+    const double pfr = t < 7 ? rhs_val(q, t) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = t + u * kT;
+      pf[u] = 0.0;
+      if (u < per && idx < NB * 49) {
+        const int c = q - BW + idx / 49;   // blocks (q, c), c = j+1 .. q (damping added at store)
+        if (q < n) pf[u] = __ldcg(a.band + ((size_t)c * NB + (q - c)) * 49 + idx % 49);
+      }
+    }
+    double* A0 = Wn + (size_t)wslot(j, j, NB) * 49;
+    // (1) diagonal block: right-looking Cholesky by warp 0 in registers (lane l < 28 owns
+    //     entry l of the lower triangle, row-major), then y_j = L_jj^-1 y_j. The pivots'
+    //     reciprocals go to the unused upper triangle: invd[0] -> (1, 2), invd[k] -> (0, k).
+    if (t < 32) {
+      int i = 0, jj = 0;
+      if (t < 28) { while ((i + 1) * (i + 2) / 2 <= t) ++i; jj = t - i * (i + 1) / 2; }
+      double v = t < 28 ? A0[7 * i + jj] : 0.0;
+      double myinv = 0.0;
+      bool okc = true;
+      for (int k = 0; k < 7; ++k) {
+        const double akk = __shfl_sync(0xffffffffu, v, k * (k + 1) / 2 + k);
+        if (!(akk > 0.0)) { okc = false; break; }
+        const double inv = 1.0 / sqrt(akk);
+        if (t == k) myinv = inv;
+        if (t < 28 && jj == k) v = i == k ? akk * inv : v * inv;
+        const double lik = __shfl_sync(0xffffffffu, v, i * (i + 1) / 2 + k);
+        const double ljk = __shfl_sync(0xffffffffu, v, jj * (jj + 1) / 2 + k);
+        if (t < 28 && jj > k) v -= lik * ljk;
+      }
+      if (!okc) {
+        if (t == 0) s_fail = 1;
+      } else {
+        if (t < 28) A0[7 * i + jj] = v;
+        if (t < 7) A0[t == 0 ? 9 : t] = myinv;
+        // forward substitution of y_j with the factor in registers
+        double y = t < 7 ? Yw[(j % NB) * 8 + t] : 0.0;
+        for (int k = 0; k < 7; ++k) {
+          if (t == k) y *= myinv;
+          const double yk = __shfl_sync(0xffffffffu, y, k);
+          const double lrk = __shfl_sync(0xffffffffu, v, t < 7 ? t * (t + 1) / 2 + k : 0);
+          if (t > k && t < 7) y -= lrk * yk;
+        }
+        if (t < 7) Yw[(j % NB) * 8 + t] = y;
+      }
+    }
+    __syncthreads();
+    if (s_fail) break;
+    // (2) panel: L_{j+d, j} = A_{j+d, j} L_jj^-T (thread per scalar row); y_{j+d} -= L y_j
+    if (t < 7 * BW) {
+      const int d = 1 + t / 7, r = t % 7;
+      if (j + d < n) {
+        double* Ar = Wn + (size_t)wslot(j + d, j, NB) * 49 + 7 * r;
+        double x[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+          double s = Ar[k];
+#pragma unroll
+          for (int m = 0; m < k; ++m) s -= x[m] * A0[7 * k + m];
+          x[k] = s * A0[k == 0 ? 9 : k];
+        }
+        const double* yj = Yw + (j % NB) * 8;
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) { Ar[k] = x[k]; acc += x[k] * yj[k]; }
+        Yw[((j + d) % NB) * 8 + r] -= acc;
+      }
+    }
+    __syncthreads();
+    // (3) trailing update of the window: block (j+d2, j+d1) -= L_{j+d2, j} L_{j+d1, j}^T,
+    //     thread per block pair (L_{j+d1, j} held in registers)
+    {
+      const int nblk = BW * (BW + 1) / 2, jm = j % NB;
+      for (int b = t; b < nblk; b += kT) {
+        const int pr = pairs[b], d1 = pr & 0xff, d2 = pr >> 8;
+        if (j + d2 >= n) continue;
+        int s2 = jm + d2, s1 = jm + d1;
+        if (s2 >= NB) s2 -= NB;
+        if (s1 >= NB) s1 -= NB;
+        const double* L2 = Wn + (size_t)tri_slot(s2, jm) * 49;
+        const double* L1 = Wn + (size_t)tri_slot(s1, jm) * 49;
+        double* T = Wn + (size_t)tri_slot(s2, s1) * 49;
+        double l1[49];
+#pragma unroll
+        for (int k = 0; k < 49; ++k) l1[k] = L1[k];
+#pragma unroll
+        for (int r = 0; r < 7; ++r) {
+          double l2[7];
+#pragma unroll
+          for (int m = 0; m < 7; ++m) l2[m] = L2[7 * r + m];
+#pragma unroll
+          for (int c = 0; c < 7; ++c) {
+            double acc = 0.0;
+#pragma unroll
+            for (int m = 0; m < 7; ++m) acc += l2[m] * l1[7 * c + m];
+            T[7 * r + c] -= acc;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // (4) retire position j (factor column + y_j to global); position j + NB enters
+    for (int idx = t; idx < NB * 49; idx += kT) {
+      const int d = idx / 49, e = idx - 49 * d;
+      a.lband[(size_t)j * NB * 49 + idx] = (j + d < n) ? Wn[(size_t)wslot(j + d, j, NB) * 49 + e] : 0.0;
+    }
+    if (t < 8) a.yb[(size_t)j * 8 + t] = Yw[(j % NB) * 8 + t];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = t + u * kT;
+      if (u < per && idx < NB * 49) {
+        const int c = q - BW + idx / 49, e = idx % 49;
+        double v = pf[u];
+        if (c == q && (e / 7) == (e % 7)) v = v + lambda * v;
+        Wn[(size_t)wslot(q, c, NB) * 49 + e] = v;
+      }
+    }
+    if (t < 8) Yw[(j % NB) * 8 + t] = pfr;
+    __syncthreads();
+  }
+  double xx = 0.0;
+  if (!s_fail) {
+    // back substitution: x_j = L_jj^-T (y_j - sum_d L_{j+d,j}^T x_{j+d}); the factor
+    // column of the next step is prefetched into registers while this one is used
+    const int per = (NB * 49 + kT - 1) / kT;
+    double pf[8], pfy = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = t + u * kT;
+      pf[u] = (u < per && idx < NB * 49) ? __ldcg(a.lband + (size_t)(n - 1) * NB * 49 + idx) : 0.0;
+    }
+    if (t < 7) pfy = __ldcg(a.yb + (size_t)(n - 1) * 8 + t);
+    for (int j = n - 1; j >= 0; --j) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = t + u * kT;
+        if (u < per && idx < NB * 49) Lc[idx] = pf[u];
+      }
+      if (t < 7) part[NB * 8 - 8 + t] = pfy;   // y_j (last row of part is free: d <= BW)
+      __syncthreads();
+      if (j > 0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = t + u * kT;
+          if (u < per && idx < NB * 49) pf[u] = __ldcg(a.lband + (size_t)(j - 1) * NB * 49 + idx);
+        }
+        if (t < 7) pfy = __ldcg(a.yb + (size_t)(j - 1) * 8 + t);
+      }
+      if (t < 7 * BW) {
+        const int d = 1 + t / 7, r = t % 7;
+        double s = 0.0;
+        if (j + d < n) {
+          const double* xd = Xs + ((j + d) % NB) * 8;
+#pragma unroll
+          for (int m = 0; m < 7; ++m) s += Lc[d * 49 + 7 * m + r] * xd[m];
+        }
+        part[(d - 1) * 8 + r] = s;
+      }
+      __syncthreads();
+      if (t < 7) {
+        double s = part[NB * 8 - 8 + t];
+        for (int d = 0; d < BW; ++d) s -= part[d * 8 + t];
+        part[NB * 8 - 8 + t] = s;
+      }
+      __syncthreads();
+      if (t == 0) {
+        double x[7];
+        for (int r = 0; r < 7; ++r) x[r] = part[NB * 8 - 8 + r];
+        for (int r = 6; r >= 0; --r) {
+          double s = x[r];
+          for (int m = r + 1; m < 7; ++m) s -= Lc[7 * m + r] * x[m];
+          x[r] = s * Lc[r == 0 ? 9 : r];
+        }
+        const int v = a.ord[j];
+        for (int r = 0; r < 7; ++r) {
+          Xs[(j % NB) * 8 + r] = x[r];
+          X[(size_t)v * kVec + r] = x[r];
+          xx += x[r] * x[r];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (t == 0) {
+    a.bres[0] = s_fail ? 1.0 : 0.0;
+    a.bres[1] = xx;
+  }
+}
+
 __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
   __shared__ double shJ[(kT / 16) * 112];
   __shared__ double shR[kT / 32][4];
+  extern __shared__ double dsm[];
   unsigned int bt = 0;
   const int tid = blockIdx.x * kT + threadIdx.x, nth = gridDim.x * kT;
   const int lane8 = threadIdx.x & 7, g8 = tid >> 3, ng8 = nth >> 3;
@@ -447,9 +762,10 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
   const int warp = tid >> 5, nwarp = nth >> 5, lane = threadIdx.x & 31;
   double* X = a.vx;
   double* Rr = a.vx + (size_t)a.n_v * kVec;
-  double* Z = a.vx + 2 * (size_t)a.n_v * kVec;
-  double* Pp = a.vx + 3 * (size_t)a.n_v * kVec;
-  double* Qq = a.vx + 4 * (size_t)a.n_v * kVec;
+  double* U = a.vx + 2 * (size_t)a.n_v * kVec;
+  double* W = a.vx + 3 * (size_t)a.n_v * kVec;
+  double* Pp = a.vx + 4 * (size_t)a.n_v * kVec;
+  double* Sv = a.vx + 5 * (size_t)a.n_v * kVec;
 
   for (int k = tid; k < 13 * a.n_v; k += nth) {
     const double s = a.S_in[k];
@@ -469,7 +785,7 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
   double lambda = a.lambda0;
   int stop = chi2 == 0.0 ? 5 : 0, it = 0, accepted = 0;
   long long cg_total = 0;
-  bool relin = true;
+  bool relin = true, band_dirty = true;
   while (!stop) {
     if (it >= a.max_iter) { stop = 3; break; }
     if (relin) {
@@ -485,7 +801,7 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
             s = (o < 49 && (o / 7) == (o % 7)) ? 1.0 : 0.0;
           } else {
             for (int q = b0; q < b1; ++q) {
-              const int w = a.vinc[q], e = w >> 1, role = w & 1;
+              const int w = __ldg(&a.vinc2[q].x), e = w >> 1, role = w & 1;
               const int off = o < 49 ? (role ? kOffHjj : kOffHii) + o : (role ? kOffBj : kOffBi) + (o - 49);
               s += __ldcg(a.rec + (size_t)e * kRec + off);
             }
@@ -494,10 +810,35 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
         }
       }
       relin = false;
+      band_dirty = true;
       grid_barrier(a.bar, bt);
     }
-    // damped diagonal blocks -> Cholesky factors; x = 0, r = -b, z = P r, p = z
-    double fail = 0.0, rz = 0.0, bb = 0.0;
+    double xx = 0.0;
+    int k = 0;
+    bool bad = false;
+    double* row = nullptr;
+    if (a.bw >= 0) {
+      if (band_dirty) {
+        band_assemble(a);
+        band_dirty = false;
+        grid_barrier(a.bar, bt);
+      }
+      if (blockIdx.x == 0) band_solve(a, lambda, dsm, X);
+      grid_barrier(a.bar, bt);
+      const double bfail = __ldcg(a.bres), bxx = __ldcg(a.bres + 1);
+      ++it;
+      row = (lead && a.trace) ? a.trace + 6 * (size_t)(it - 1) : nullptr;
+      if (row) { row[0] = chi2; row[1] = lambda; row[2] = -1.0; row[3] = 0.0; row[4] = -1.0; row[5] = 1.0; }
+      if (bfail != 0.0) {
+        lambda *= 4.0;
+        if (lambda > 1e8) stop = 4;
+        continue;
+      }
+      xx = bxx;
+      k = 1;
+    } else {
+    // damped diagonal blocks -> Cholesky factors; x = 0, r = -b, u = P r
+    double fail = 0.0, gam = 0.0, dlt = 0.0, rr = 0.0;
     for (int v = g8; v < a.n_v; v += ng8) {
       const double* D = a.vd + (size_t)v * kVD;
       double* L = a.vl + (size_t)v * kVL;
@@ -526,101 +867,99 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
       double rv[7];
 #pragma unroll
       for (int i = 0; i < 7; ++i) rv[i] = -__shfl_sync(m8, bv, (threadIdx.x & 24) + i);
-      const double zl = precond(L, rv, lane8);
+      const double ul = precond(L, rv, lane8);
       if (lane8 < 7) {
-        X[(size_t)v * kVec + lane8] = 0.0;
-        Rr[(size_t)v * kVec + lane8] = -bv;
-        Z[(size_t)v * kVec + lane8] = zl;
-        Pp[(size_t)v * kVec + lane8] = zl;
-        rz += (-bv) * zl;
-        bb += bv * bv;
+        const size_t o = (size_t)v * kVec + lane8;
+        X[o] = 0.0;
+        Rr[o] = -bv;
+        U[o] = ul;
+        gam += (-bv) * ul;
+        rr += bv * bv;
       }
     }
-    cta_partial(fail, rz, bb, 0.0, a.part, shR);
+    grid_barrier(a.bar, bt);
+    for (int v = g8; v < a.n_v; v += ng8) {
+      if (lane8 >= 7) continue;
+      const double wl = spmv_row(a, v, lane8, U, lambda);
+      const size_t o = (size_t)v * kVec + lane8;
+      W[o] = wl;
+      dlt += wl * U[o];
+    }
+    cta_partial(gam, dlt, rr, fail, a.part, shR);
     grid_barrier(a.bar, bt);
     grid_total(a.part, tot, shR);
     ++it;
-    double* row = (lead && a.trace) ? a.trace + 6 * (size_t)(it - 1) : nullptr;
+    row = (lead && a.trace) ? a.trace + 6 * (size_t)(it - 1) : nullptr;
     if (row) { row[0] = chi2; row[1] = lambda; row[2] = -1.0; row[3] = 0.0; row[4] = -1.0; row[5] = 0.0; }
-    if (tot[0] != 0.0) {
+    if (tot[3] != 0.0) {
       lambda *= 4.0;
       if (lambda > 1e8) stop = 4;
       continue;
     }
-    rz = tot[1];
-    bb = tot[2];
-    double xx = 0.0;
-    int k = 0;
-    bool bad = false;
-    const double stop2 = (a.cg_tol * a.cg_tol) * bb;
-    double rr = bb;
-    while (k < a.cg_max && rr > stop2) {
-      // q = (H + lambda diag H) p
-      double pq = 0.0;
-      for (int v = g8; v < a.n_v; v += ng8) {
-        if (lane8 >= 7) continue;
-        const double* D = a.vd + (size_t)v * kVD + 7 * lane8;
-        double s = 0.0;
-#pragma unroll
-        for (int c = 0; c < 7; ++c) s += __ldcg(D + c) * vget(Pp, v, c);
-        s += lambda * __ldcg(D + lane8) * vget(Pp, v, lane8);
-        if (!a.fixed[v]) {
-          const int b0 = a.vbeg[v], b1 = a.vbeg[v + 1];
-          for (int q = b0; q < b1; ++q) {
-            const int w = a.vinc[q], e = w >> 1, role = w & 1;
-            const int o = role ? a.eij[2 * e] : a.eij[2 * e + 1];
-            const double* B = a.rec + (size_t)e * kRec + (role ? kOffHji : kOffHij) + 7 * lane8;
-            double t = 0.0;
-#pragma unroll
-            for (int c = 0; c < 7; ++c) t += __ldcg(B + c) * vget(Pp, o, c);
-            s += t;
-          }
-        }
-        Qq[(size_t)v * kVec + lane8] = s;
-        pq += vget(Pp, v, lane8) * s;
+    // preconditioned CG, Chronopoulos-Gear form (one reduction per iteration: two grid
+    // barriers -- after the vector update (u visible to the neighbours' SpMV) and after
+    // the SpMV + dot products)
+    gam = tot[0];
+    dlt = tot[1];
+    rr = tot[2];
+    const double stop2 = (a.cg_tol * a.cg_tol) * rr;
+    double alpha = 0.0, gam_old = 0.0, alpha_old = 0.0;
+    while (rr > stop2 && k < a.cg_max) {
+      double beta = 0.0;
+      if (k == 0) {
+        if (!(dlt > 0.0)) { bad = true; break; }
+        alpha = gam / dlt;
+      } else {
+        beta = gam / gam_old;
+        const double den = dlt - beta * gam / alpha_old;
+        if (!(den > 0.0)) { bad = true; break; }
+        alpha = gam / den;
       }
-      cta_partial(pq, 0.0, 0.0, 0.0, a.part, shR);
-      grid_barrier(a.bar, bt);
-      grid_total(a.part, tot, shR);
-      pq = tot[0];
-      if (!(pq > 0.0)) { bad = true; break; }
-      const double alpha = rz / pq;
-      double rzn = 0.0, rrn = 0.0, xxn = 0.0;
+      double gn = 0.0, rn = 0.0, xn = 0.0;
       for (int v = g8; v < a.n_v; v += ng8) {
         const size_t o = (size_t)v * kVec + lane8;
         double rl = 0.0;
         if (lane8 < 7) {
-          const double xl = X[o] + alpha * Pp[o];
+          const double pl = k == 0 ? U[o] : U[o] + beta * Pp[o];
+          const double sl = k == 0 ? W[o] : W[o] + beta * Sv[o];
+          Pp[o] = pl;
+          Sv[o] = sl;
+          const double xl = X[o] + alpha * pl;
           X[o] = xl;
-          rl = Rr[o] - alpha * Qq[o];
+          rl = Rr[o] - alpha * sl;
           Rr[o] = rl;
-          xxn += xl * xl;
-          rrn += rl * rl;
+          xn += xl * xl;
+          rn += rl * rl;
         }
         double rv[7];
 #pragma unroll
         for (int i = 0; i < 7; ++i) rv[i] = __shfl_sync(m8, rl, (threadIdx.x & 24) + i);
-        const double zl = precond(a.vl + (size_t)v * kVL, rv, lane8);
+        const double ul = precond(a.vl + (size_t)v * kVL, rv, lane8);
         if (lane8 < 7) {
-          Z[o] = zl;
-          rzn += rl * zl;
+          U[o] = ul;
+          gn += rl * ul;
         }
       }
-      cta_partial(rzn, rrn, xxn, 0.0, a.part, shR);
       grid_barrier(a.bar, bt);
-      grid_total(a.part, tot, shR);
-      ++k;
-      const double beta = tot[0] / rz;
-      rz = tot[0];
-      rr = tot[1];
-      xx = tot[2];
-      if (k >= a.cg_max || rr <= stop2) break;
+      double dn2 = 0.0;
       for (int v = g8; v < a.n_v; v += ng8) {
         if (lane8 >= 7) continue;
+        const double wl = spmv_row(a, v, lane8, U, lambda);
         const size_t o = (size_t)v * kVec + lane8;
-        Pp[o] = Z[o] + beta * Pp[o];
+        W[o] = wl;
+        dn2 += wl * U[o];
       }
+      cta_partial(gn, dn2, rn, xn, a.part, shR);
       grid_barrier(a.bar, bt);
+      grid_total(a.part, tot, shR);
+      gam_old = gam;
+      alpha_old = alpha;
+      gam = tot[0];
+      dlt = tot[1];
+      rr = tot[2];
+      xx = tot[3];
+      ++k;
+    }
     }
     cg_total += k;
     if (row) row[5] = (double)k;
@@ -684,16 +1023,27 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
 
 }  // namespace
 
-size_t pgo_scratch_bytes(int n_v, int n_e, int grid) {
-  const size_t d = (size_t)n_e * kRec + (size_t)n_v * (kVD + kVL + 5 * kVec + 13) + 4 * (size_t)grid;
+static size_t band_smem_bytes(int bw) {
+  if (bw < 0) return 0;
+  const size_t NB = (size_t)bw + 1;
+  return sizeof(double) * (NB * (NB + 1) / 2 * 49 + NB * 8 * 3 + NB * 49) + 2 * NB * NB;
+}
+
+int pgo_max_bw() { return kBWMax; }
+
+size_t pgo_scratch_bytes(int n_v, int n_e, int grid, int bw) {
+  size_t d = (size_t)n_e * kRec + (size_t)n_v * (kVD + kVL + 6 * kVec + 13) + 4 * (size_t)grid + 8;
+  if (bw >= 0) d += 2 * (size_t)n_v * (bw + 1) * 49 + (size_t)n_v * 8;
   return sizeof(double) * d + 256;
 }
 
-int pgo_grid(lc_ctx* c, int n_v, int n_e) {
+int pgo_grid(lc_ctx* c, int n_v, int n_e, int bw) {
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pgo, kT, 0);
+  const size_t smem = band_smem_bytes(bw);
+  cudaFuncSetAttribute(k_pgo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pgo, kT, smem);
   (void)c;
   const int64_t work = std::max<int64_t>((int64_t)n_e * 16, (int64_t)n_v * 8);
   const int need = (int)std::max<int64_t>(1, (work + kT - 1) / kT);
@@ -701,27 +1051,37 @@ int pgo_grid(lc_ctx* c, int n_v, int n_e) {
 }
 
 cudaError_t launch_pgo(lc_ctx* c, int n_v, int n_e, const int32_t* d_eij, const double* d_M, const double* d_S_in,
-                       const uint8_t* d_fixed, const int32_t* d_vbeg, const int32_t* d_vinc,
-                       const lc_pgo_params& p, double* d_S_out, void* scratch, int grid, double* d_trace,
-                       double* d_chi2, unsigned long long* counts, cudaStream_t s) {
+                       const uint8_t* d_fixed, const int32_t* d_vbeg, const int32_t* d_vinc, int bw,
+                       const int32_t* d_pos, const int32_t* d_ord, const lc_pgo_params& p, double* d_S_out,
+                       void* scratch, int grid, double* d_trace, double* d_chi2, unsigned long long* counts,
+                       cudaStream_t s) {
   PgoArgs a;
+  a.vinc2 = (const int2*)d_vinc;
   a.n_v = n_v; a.n_e = n_e; a.max_iter = p.max_iter; a.cg_max = p.cg_max_iter;
   a.lambda0 = p.lambda0; a.eps_dx = p.eps_dx; a.eps_chi2 = p.eps_chi2; a.cg_tol = p.cg_tol;
-  a.eij = d_eij; a.M = d_M; a.S_in = d_S_in; a.fixed = d_fixed; a.vbeg = d_vbeg; a.vinc = d_vinc;
+  a.eij = d_eij; a.M = d_M; a.S_in = d_S_in; a.fixed = d_fixed; a.vbeg = d_vbeg;
   a.S_out = d_S_out;
+  a.bw = bw; a.pos = d_pos; a.ord = d_ord;
   double* base = (double*)scratch;
   a.rec = base; base += (size_t)n_e * kRec;
   a.vd = base; base += (size_t)n_v * kVD;
   a.vl = base; base += (size_t)n_v * kVL;
-  a.vx = base; base += (size_t)n_v * 5 * kVec;
+  a.vx = base; base += (size_t)n_v * 6 * kVec;
   a.S_tmp = base; base += (size_t)n_v * 13;
   a.part = base; base += 4 * (size_t)grid;
+  a.bres = base; base += 8;
+  a.band = a.lband = a.yb = nullptr;
+  if (bw >= 0) {
+    a.band = base; base += (size_t)n_v * (bw + 1) * 49;
+    a.lband = base; base += (size_t)n_v * (bw + 1) * 49;
+    a.yb = base; base += (size_t)n_v * 8;
+  }
   a.bar = (unsigned int*)base;
   a.trace = d_trace; a.chi2_out = d_chi2; a.counts = counts;
   cudaError_t e = cudaMemsetAsync(a.bar, 0, 256, s);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
-  e = cudaLaunchCooperativeKernel((const void*)k_pgo, dim3(grid), dim3(kT), args, 0, s);
+  e = cudaLaunchCooperativeKernel((const void*)k_pgo, dim3(grid), dim3(kT), args, band_smem_bytes(bw), s);
   c->launches++;
   return e;
 }

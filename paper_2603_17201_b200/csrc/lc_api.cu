@@ -887,6 +887,89 @@ lc_status lc_sim3_refine(lc_ctx* c, int32_t n_prob, const int32_t* prob_begin, c
   });
 }
 
+// Reverse Cuthill-McKee ordering of the free vertices (the symbolic phase of the banded
+// direct solve, A54): BFS from a pseudo-peripheral vertex of each component, neighbours
+// in ascending (degree, index); fixed vertices (no couplings) are placed last. Returns
+// the block bandwidth max |pos(i) - pos(j)| over free-free edges.
+static int pgo_rcm(int32_t n_v, const uint8_t* fixed, int32_t n_e, const int32_t* eij, std::vector<int32_t>& pos,
+                   std::vector<int32_t>& ord) {
+  std::vector<int32_t> deg(n_v, 0), beg((size_t)n_v + 1, 0), adj;
+  for (int32_t e = 0; e < n_e; ++e) {
+    const int32_t i = eij[2 * e], j = eij[2 * e + 1];
+    if (fixed[i] || fixed[j]) continue;
+    deg[i]++;
+    deg[j]++;
+  }
+  for (int32_t v = 0; v < n_v; ++v) beg[v + 1] = beg[v] + deg[v];
+  adj.resize(beg[n_v]);
+  {
+    std::vector<int32_t> cur(beg.begin(), beg.end() - 1);
+    for (int32_t e = 0; e < n_e; ++e) {
+      const int32_t i = eij[2 * e], j = eij[2 * e + 1];
+      if (fixed[i] || fixed[j]) continue;
+      adj[cur[i]++] = j;
+      adj[cur[j]++] = i;
+    }
+  }
+  for (int32_t v = 0; v < n_v; ++v)
+    std::sort(adj.begin() + beg[v], adj.begin() + beg[v + 1], [&](int32_t x, int32_t y) {
+      return deg[x] != deg[y] ? deg[x] < deg[y] : x < y;
+    });
+  std::vector<int32_t> seen(n_v, 0), level(n_v, -1), order, comp, clev;
+  order.reserve(n_v);
+  auto bfs = [&](int32_t s) {   // level structure of s's component (unseen vertices)
+    comp.clear();
+    clev.clear();
+    comp.push_back(s);
+    clev.push_back(0);
+    level[s] = 0;
+    for (size_t h = 0; h < comp.size(); ++h) {
+      const int32_t u = comp[h];
+      for (int32_t q = beg[u]; q < beg[u + 1]; ++q) {
+        const int32_t w = adj[q];
+        if (!seen[w] && level[w] < 0) {
+          level[w] = level[u] + 1;
+          comp.push_back(w);
+          clev.push_back(level[w]);
+        }
+      }
+    }
+    for (int32_t u : comp) level[u] = -1;
+  };
+  for (int32_t s0 = 0; s0 < n_v; ++s0) {
+    if (fixed[s0] || seen[s0]) continue;
+    int32_t s = s0;
+    for (int sweep = 0; sweep < 2; ++sweep) {   // pseudo-peripheral start: min degree in the last level
+      bfs(s);
+      const int32_t lmax = clev.back();
+      int32_t best = -1;
+      for (size_t h = 0; h < comp.size(); ++h)
+        if (clev[h] == lmax && (best < 0 || deg[comp[h]] < deg[best] ||
+                                (deg[comp[h]] == deg[best] && comp[h] < best)))
+          best = comp[h];
+      s = best;
+    }
+    bfs(s);
+    for (int32_t u : comp) {
+      seen[u] = 1;
+      order.push_back(u);
+    }
+  }
+  std::reverse(order.begin(), order.end());
+  for (int32_t v = 0; v < n_v; ++v)
+    if (fixed[v]) order.push_back(v);
+  pos.assign(n_v, 0);
+  ord = order;
+  for (int32_t p = 0; p < n_v; ++p) pos[order[p]] = p;
+  int bw = 0;
+  for (int32_t e = 0; e < n_e; ++e) {
+    const int32_t i = eij[2 * e], j = eij[2 * e + 1];
+    if (fixed[i] || fixed[j]) continue;
+    bw = std::max(bw, std::abs(pos[i] - pos[j]));
+  }
+  return bw;
+}
+
 lc_status lc_pgo_sim3(lc_ctx* c, int32_t n_v, const lc_sim3* S_init, const uint8_t* fixed, int32_t n_e,
                       const int32_t* edge_ij, const lc_sim3* M, const lc_pgo_params* params, lc_sim3* out_S,
                       double* out_trace, double* out_chi2, int64_t* out_counts, void* stream) {
@@ -894,14 +977,14 @@ lc_status lc_pgo_sim3(lc_ctx* c, int32_t n_v, const lc_sim3* S_init, const uint8
     capture_gate(c, stream, false);
     REQUIRE(params, LC_EINVAL, "null params");
     const lc_pgo_params p = *params;
-    REQUIRE(n_v >= 0 && n_e >= 0 && p.max_iter >= 0 && p.cg_max_iter >= 1 && p.lambda0 > 0.0 &&
-                p.eps_dx >= 0.0 && p.eps_chi2 >= 0.0 && p.cg_tol >= 0.0,
+    REQUIRE(n_v >= 0 && n_e >= 0 && n_e < (1 << 30) && p.max_iter >= 0 && p.cg_max_iter >= 1 && p.lambda0 > 0.0 &&
+                p.eps_dx >= 0.0 && p.eps_chi2 >= 0.0 && p.cg_tol >= 0.0 && p.solver >= 0 && p.solver <= 2,
             LC_EINVAL, "bad sizes / parameters");
     REQUIRE(n_v == 0 || (S_init && fixed && out_S), LC_EINVAL, "null vertex array");
     REQUIRE(n_e == 0 || (edge_ij && M), LC_EINVAL, "null edge array");
     // incidence lists (symbolic structure of the block-sparse system): per vertex, its
-    // edges in ascending edge order, tagged with the vertex's role (0: i, 1: j)
-    std::vector<int32_t> vbeg((size_t)n_v + 1, 0), vinc((size_t)2 * n_e);
+    // edges in ascending edge order as ((edge << 1) | role (0: i, 1: j), other vertex)
+    std::vector<int32_t> vbeg((size_t)n_v + 1, 0), vinc((size_t)4 * n_e);
     for (int32_t e = 0; e < n_e; ++e) {
       const int32_t i = edge_ij[2 * e], j = edge_ij[2 * e + 1];
       REQUIRE(i >= 0 && i < n_v && j >= 0 && j < n_v, LC_ERANGE, "edge vertex out of range");
@@ -913,8 +996,12 @@ lc_status lc_pgo_sim3(lc_ctx* c, int32_t n_v, const lc_sim3* S_init, const uint8
     {
       std::vector<int32_t> cur(vbeg.begin(), vbeg.end() - 1);
       for (int32_t e = 0; e < n_e; ++e) {
-        vinc[cur[edge_ij[2 * e]]++] = (e << 1);
-        vinc[cur[edge_ij[2 * e + 1]]++] = (e << 1) | 1;
+        const int32_t i = edge_ij[2 * e], j = edge_ij[2 * e + 1];
+        const int32_t qi = cur[i]++, qj = cur[j]++;
+        vinc[2 * qi] = (e << 1);
+        vinc[2 * qi + 1] = j;
+        vinc[2 * qj] = (e << 1) | 1;
+        vinc[2 * qj + 1] = i;
       }
     }
     Call call(c, stream);
@@ -936,19 +1023,31 @@ lc_status lc_pgo_sim3(lc_ctx* c, int32_t n_v, const lc_sim3* S_init, const uint8
       call.arg(edge_ij, (size_t)2 * n_e, &d_eij);
       call.arg(vinc.data(), vinc.size(), &d_vinc);
     }
-    call.commit();
     const double* dM = call.in((const double*)M, 13 * (size_t)n_e);
     const double* dS0 = call.in((const double*)S_init, 13 * (size_t)n_v);
     double* dS = (double*)call.out((double*)out_S, 13 * (size_t)n_v);
     double* dT = out_trace ? call.out(out_trace, 6 * (size_t)std::max(p.max_iter, 1)) : nullptr;
     double* dC = out_chi2 ? call.out(out_chi2, 2) : nullptr;
     if (dT) CK(cudaMemsetAsync(dT, 0, 6 * sizeof(double) * std::max(p.max_iter, 1), call.s));
-    const int grid = pgo_grid(c, n_v, n_e);
-    void* scr = call.scratch(pgo_scratch_bytes(n_v, n_e, grid));
+    // solver (A54): banded Cholesky in a reverse Cuthill-McKee order when the block
+    // bandwidth fits the shared-memory window, else block-Jacobi CG
+    std::vector<int32_t> pos, ord;
+    int bw = pgo_rcm(n_v, fixed, n_e, edge_ij, pos, ord);
+    REQUIRE(!(p.solver == LC_PGO_SOLVER_BAND && bw > pgo_max_bw()), LC_EINVAL,
+            "LC_PGO_SOLVER_BAND: block bandwidth exceeds the banded solver's window");
+    if (p.solver == LC_PGO_SOLVER_CG || bw > pgo_max_bw()) bw = -1;
+    const int32_t *d_pos = nullptr, *d_ord = nullptr;
+    if (bw >= 0) {
+      call.arg(pos.data(), pos.size(), &d_pos);
+      call.arg(ord.data(), ord.size(), &d_ord);
+    }
+    call.commit();
+    const int grid = pgo_grid(c, n_v, n_e, bw);
+    void* scr = call.scratch(pgo_scratch_bytes(n_v, n_e, grid, bw));
     {
       Prof pr(c, LC_PROF_PGO, call.s);
-      CK(launch_pgo(c, n_v, n_e, d_eij, dM, dS0, d_fixed, d_vbeg, d_vinc, p, dS, scr, grid, dT, dC, cnt,
-                    call.s));
+      CK(launch_pgo(c, n_v, n_e, d_eij, dM, dS0, d_fixed, d_vbeg, d_vinc, bw, d_pos, d_ord, p, dS, scr, grid,
+                    dT, dC, cnt, call.s));
     }
     call.finish();
   });

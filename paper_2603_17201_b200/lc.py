@@ -359,7 +359,7 @@ class Context:
 
     # -- lc_pgo_sim3 ----------------------------------------------------------------
     def pgo_sim3(self, S_init, fixed, edges, M, max_iter=20, cg_max_iter=500, lambda0=1e-4, eps_dx=1e-8,
-                 eps_chi2=1e-10, cg_tol=1e-10, host=True):
+                 eps_chi2=1e-10, cg_tol=1e-10, solver="auto", host=True):
         """Essential-graph Sim3 Levenberg-Marquardt: (S [n_v, 13], trace [iters, 6],
         (chi2_0, chi2_final), counts). With host=False S/trace/chi2/counts are device
         tensors (trace [max_iter, 6], counts raw)."""
@@ -369,7 +369,7 @@ class Context:
         n_e = len(E)
         fx = np.ascontiguousarray(fixed, np.uint8)
         prm = _lib.lc_pgo_params(int(max_iter), int(cg_max_iter), float(lambda0), float(eps_dx),
-                                 float(eps_chi2), float(cg_tol))
+                                 float(eps_chi2), float(cg_tol), {"auto": 0, "band": 1, "cg": 2}[solver], 0)
         rows = max(int(max_iter), 1)
         if host:
             S = np.zeros((n_v, 13), np.float64)

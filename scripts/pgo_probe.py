@@ -14,21 +14,21 @@ for name in sys.argv[1:] or ["C2", "C3", "C5"]:
     g = make_pose_graph(name, 0)
     S0 = torch.from_numpy(g.S_init).cuda()
     M = torch.from_numpy(g.M).cuda()
-    for cg_tol in (1e-10, 1e-6):
-        ctx.pgo_sim3(S0, g.fixed, g.edges, M, host=False, cg_tol=cg_tol)
+    for solver, cg_tol in (("auto", 1e-10), ("cg", 1e-10)):
+        ctx.pgo_sim3(S0, g.fixed, g.edges, M, host=False, cg_tol=cg_tol, solver=solver)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ms = []
         for _ in range(3):
             a.record()
-            S, tr, c2, cnt = ctx.pgo_sim3(S0, g.fixed, g.edges, M, host=False, cg_tol=cg_tol)
+            S, tr, c2, cnt = ctx.pgo_sim3(S0, g.fixed, g.edges, M, host=False, cg_tol=cg_tol, solver=solver)
             b.record()
             torch.cuda.synchronize()
             ms.append(a.elapsed_time(b))
         cnt = cnt.cpu().numpy()
         c2 = c2.cpu().numpy()
         tr = tr.cpu().numpy()[:cnt[-4]]
-        print(f"{name} n_v={g.n_v} n_e={g.n_e} cg_tol={cg_tol:g} ms={np.median(ms):.3f} iters={cnt[-4]} "
+        print(f"{name} n_v={g.n_v} n_e={g.n_e} {solver} cg_tol={cg_tol:g} ms={np.median(ms):.3f} iters={cnt[-4]} "
               f"acc={cnt[-3]} cg={cnt[-2]} stop={cnt[-1]} chi2 {c2[0]:.6g}->{c2[1]:.6g}", flush=True)
         print("   cg per iter", tr[:, 5].astype(int).tolist())
 ctx.close()

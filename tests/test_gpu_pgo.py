@@ -45,32 +45,35 @@ def compare(g_res, o_res, s_atol=1e-8):
     np.testing.assert_allclose(S, So, rtol=0, atol=s_atol)
 
 
+@pytest.mark.parametrize("solver", ["band", "cg"])
 @pytest.mark.parametrize("name,seed,mode", [("G0", 0, "drift"), ("G0", 3, "exact"), ("G1", 0, "drift"),
                                             ("G1", 1, "exact"), ("G1", 5, "drift")])
-def test_pgo_matches_oracle(ctx, name, seed, mode):
+def test_pgo_matches_oracle(ctx, name, seed, mode, solver):
     g = make_pose_graph(name, seed, mode=mode)
-    gr = ctx.pgo_sim3(g.S_init, g.fixed, g.edges, g.M, max_iter=30, **TIGHT)
+    gr = ctx.pgo_sim3(g.S_init, g.fixed, g.edges, g.M, max_iter=30, solver=solver, **TIGHT)
     orr = oracle.pgo(g.S_init, g.fixed, g.edges, g.M, max_iter=30)
     compare(gr, orr)
     assert gr[3]["pgo_solver_iters"] > 0
 
 
-def test_one_iteration_is_the_same_step(ctx):
+@pytest.mark.parametrize("solver", ["band", "cg"])
+def test_one_iteration_is_the_same_step(ctx, solver):
     """max_iter = 1: the first linearisation, solve and exp update agree to 1e-11."""
     g = make_pose_graph("G1", 2)
-    gr = ctx.pgo_sim3(g.S_init, g.fixed, g.edges, g.M, max_iter=1, **TIGHT)
+    gr = ctx.pgo_sim3(g.S_init, g.fixed, g.edges, g.M, max_iter=1, solver=solver, **TIGHT)
     orr = oracle.pgo(g.S_init, g.fixed, g.edges, g.M, max_iter=1)
     np.testing.assert_allclose(gr[0], orr[0], rtol=0, atol=1e-11)
     np.testing.assert_allclose(gr[1][0, :5], orr[1][0, :5], rtol=1e-9)
 
 
-def test_multiple_fixed_and_duplicate_edges(ctx):
+@pytest.mark.parametrize("solver", ["band", "cg"])
+def test_multiple_fixed_and_duplicate_edges(ctx, solver):
     g = make_pose_graph("G1", 4)
     fixed = g.fixed.copy()
     fixed[[10, 37]] = 1
     E = np.concatenate([g.edges, g.edges[:5]])
     M = np.concatenate([g.M, g.M[:5]])
-    gr = ctx.pgo_sim3(g.S_init, fixed, E, M, max_iter=25, **TIGHT)
+    gr = ctx.pgo_sim3(g.S_init, fixed, E, M, max_iter=25, solver=solver, **TIGHT)
     orr = oracle.pgo(g.S_init, fixed, E, M, max_iter=25)
     compare(gr, orr)
     np.testing.assert_array_equal(gr[0][fixed == 1], g.S_init[fixed == 1])
@@ -86,27 +89,54 @@ def test_single_edge_closed_form(ctx):
     np.testing.assert_allclose(S[1], oracle.sim3_compose(M, S0[0]), rtol=0, atol=1e-9)
 
 
-def test_degenerate_cases(ctx):
+def test_wide_graph_falls_back_to_cg(ctx):
+    """Random long-range edges push the RCM bandwidth past the banded window: BAND is
+    refused, AUTO solves by CG, and both CG and the oracle agree."""
+    g = make_pose_graph("G1", 6)
+    rng = np.random.default_rng(1)
+    extra = []
+    while len(extra) < 40:
+        i, j = rng.integers(0, g.n_v, 2)
+        if abs(int(i) - int(j)) > 10:
+            extra.append((int(i), int(j)))
+    extra = np.asarray(extra, np.int32)
+    Mx = np.stack([oracle.sim3_compose(g.S_init[j], oracle.sim3_inverse(g.S_init[i])) for i, j in extra])
+    E = np.concatenate([g.edges, extra])
+    M = np.concatenate([g.M, Mx])
+    from paper_2603_17201_b200._lib import LcError
+    with pytest.raises(LcError, match="LC_EINVAL"):
+        ctx.pgo_sim3(g.S_init, g.fixed, E, M, solver="band")
+    gr = ctx.pgo_sim3(g.S_init, g.fixed, E, M, max_iter=30, **TIGHT)
+    assert gr[1][0, 5] > 1   # CG iterations, not the one-shot banded solve
+    compare(gr, oracle.pgo(g.S_init, g.fixed, E, M, max_iter=30))
+
+
+@pytest.mark.parametrize("solver", ["band", "cg"])
+def test_degenerate_cases(ctx, solver):
     g = make_pose_graph("G0", 0)
+    ctx_pgo = ctx.pgo_sim3
+
+    def pgo(*args, **kw):
+        return ctx_pgo(*args, solver=solver, **kw)
     # no edges: chi2 = 0, nothing to do
-    S, tr, (c0, c1), cnt = ctx.pgo_sim3(g.S_init, g.fixed, np.zeros((0, 2), np.int32), np.zeros((0, 13)))
+    S, tr, (c0, c1), cnt = pgo(g.S_init, g.fixed, np.zeros((0, 2), np.int32), np.zeros((0, 13)))
     assert cnt["pgo_iters"] == 0 and cnt["pgo_stop"] == 5 and c0 == 0.0
     np.testing.assert_array_equal(S, g.S_init)
     # every vertex fixed: the reduced system is empty, delta = 0
-    S, tr, _, cnt = ctx.pgo_sim3(g.S_init, np.ones(g.n_v, np.uint8), g.edges, g.M)
+    S, tr, _, cnt = pgo(g.S_init, np.ones(g.n_v, np.uint8), g.edges, g.M)
     o = oracle.pgo(g.S_init, np.ones(g.n_v, np.uint8), g.edges, g.M)
     assert cnt["pgo_stop"] == o[3]["pgo_stop"] == 1
     np.testing.assert_array_equal(S, g.S_init)
     # a free vertex without edges: singular system, lambda overflows, nothing moves
     S0 = np.concatenate([g.S_init, g.S_init[:1]])
     fx = np.concatenate([g.fixed, [0]]).astype(np.uint8)
-    S, tr, _, cnt = ctx.pgo_sim3(S0, fx, g.edges, g.M, max_iter=100)
+    S, tr, _, cnt = pgo(S0, fx, g.edges, g.M, max_iter=100)
     o = oracle.pgo(S0, fx, g.edges, g.M, max_iter=100)
     assert cnt["pgo_stop"] == o[3]["pgo_stop"] == 4
     assert cnt["pgo_iters"] == o[3]["pgo_iters"]
     np.testing.assert_array_equal(S, S0)
     # no vertices
-    S, tr, (c0, c1), cnt = ctx.pgo_sim3(np.zeros((0, 13)), np.zeros(0, np.uint8), np.zeros((0, 2), np.int32),
+    S, tr, (c0, c1), cnt = pgo(np.zeros((0, 13)), np.zeros(0, np.uint8), np.zeros((0, 2), np.int32),
                                         np.zeros((0, 13)))
     assert S.shape == (0, 13) and cnt["pgo_iters"] == 0
 
