@@ -522,6 +522,12 @@ __device__ __forceinline__ int tri_slot(int a, int b) {
 }
 __device__ __forceinline__ int wslot(int r, int c, int NB) { return tri_slot(r % NB, c % NB); }
 
+#ifdef LC_PGO_TIMING
+#define PGO_TIC(k) do { if (t == 0) { const long long c_ = clock64(); tim[k] += c_ - tlast; tlast = c_; } } while (0)
+#else
+#define PGO_TIC(k) do { } while (0)
+#endif
+
 __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* X) {
   const int n = a.n_v, BW = a.bw, NB = BW + 1, t = threadIdx.x;
   const int nw = NB * (NB + 1) / 2;
@@ -532,6 +538,9 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
   double* part = Lc + NB * 49;            // [NB][8]
   unsigned short* pairs = (unsigned short*)(part + NB * 8);   // [BW (BW + 1) / 2] (d1, d2)
   __shared__ int s_fail;
+#ifdef LC_PGO_TIMING
+  long long tim[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = clock64();
+#endif
   if (t == 0) {
     s_fail = 0;
     int k = 0;
@@ -545,8 +554,8 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
     if (r == c && (e / 7) == (e % 7)) v = v + lambda * v;
     return v;
   };
-  auto rhs_val = [&](int q, int r) -> double {
-    return q < n ? -__ldcg(a.vd + (size_t)a.ord[q] * kVD + 49 + r) : 0.0;
+  auto grad_val = [&](int q, int r) -> double {   // b (the right-hand side is -b)
+    return q < n ? __ldcg(a.vd + (size_t)a.ord[q] * kVD + 49 + r) : 0.0;
   };
   for (int idx = t; idx < nw * 49; idx += kT) {
     const int blk = idx / 49, e = idx - 49 * blk;
@@ -555,13 +564,13 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
     const int c = blk - r * (r + 1) / 2;    // initial window: positions 0..BW, slot = position
     Wn[(size_t)blk * 49 + e] = r < NB ? blk_val(r, c, e) : 0.0;
   }
-  if (t < NB * 8) Yw[t] = (t % 8) < 7 ? rhs_val(t / 8, t % 8) : 0.0;
+  if (t < NB * 8) Yw[t] = (t % 8) < 7 ? -grad_val(t / 8, t % 8) : 0.0;
   __syncthreads();
   const int per = (NB * 49 + kT - 1) / kT;
   double pf[8];   // prefetched blocks of the entering position
   for (int j = 0; j < n; ++j) {
     const int q = j + NB;
-    const double pfr = t < 7 ? rhs_val(q, t) : 0.0;
+    const double pfr = t < 7 ? grad_val(q, t) : 0.0;   // negated at the store
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int idx = t + u * kT;
@@ -584,7 +593,7 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
       for (int k = 0; k < 7; ++k) {
         const double akk = __shfl_sync(0xffffffffu, v, k * (k + 1) / 2 + k);
         if (!(akk > 0.0)) { okc = false; break; }
-        const double inv = 1.0 / sqrt(akk);
+        const double inv = rsqrt(akk);
         if (t == k) myinv = inv;
         if (t < 28 && jj == k) v = i == k ? akk * inv : v * inv;
         const double lik = __shfl_sync(0xffffffffu, v, i * (i + 1) / 2 + k);
@@ -608,6 +617,7 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
       }
     }
     __syncthreads();
+    PGO_TIC(0);
     if (s_fail) break;
     // (2) panel: L_{j+d, j} = A_{j+d, j} L_jj^-T (thread per scalar row); y_{j+d} -= L y_j
     if (t < 7 * BW) {
@@ -630,8 +640,10 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
       }
     }
     __syncthreads();
+    PGO_TIC(1);
     // (3) trailing update of the window: block (j+d2, j+d1) -= L_{j+d2, j} L_{j+d1, j}^T,
-    //     thread per block pair (L_{j+d1, j} held in registers)
+    //     thread per block pair (L_{j+d1, j} held in registers: 98 shared loads per 343
+    //     FMAs; a thread per (pair, row) re-reads L_{j+d1, j} 7 times and measured slower)
     {
       const int nblk = BW * (BW + 1) / 2, jm = j % NB;
       for (int b = t; b < nblk; b += kT) {
@@ -662,25 +674,34 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
       }
     }
     __syncthreads();
-    // (4) retire position j (factor column + y_j to global); position j + NB enters
-    for (int idx = t; idx < NB * 49; idx += kT) {
-      const int d = idx / 49, e = idx - 49 * d;
-      a.lband[(size_t)j * NB * 49 + idx] = (j + d < n) ? Wn[(size_t)wslot(j + d, j, NB) * 49 + e] : 0.0;
-    }
-    if (t < 8) a.yb[(size_t)j * 8 + t] = Yw[(j % NB) * 8 + t];
-    __syncthreads();
+    PGO_TIC(2);
+    // (4) retire position j (factor column + y_j to global) and let position j + NB enter:
+    //     the entering block (q, j+1+d') takes the slot of the retiring block (j+d'+1, j)
+    //     (d' = bw: the diagonal (q, q) takes (j, j)), so each thread moves its own entries
+    {
+      const int jm = j % NB;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int idx = t + u * kT;
-      if (u < per && idx < NB * 49) {
-        const int c = q - BW + idx / 49, e = idx % 49;
-        double v = pf[u];
-        if (c == q && (e / 7) == (e % 7)) v = v + lambda * v;
-        Wn[(size_t)wslot(q, c, NB) * 49 + e] = v;
+      for (int u = 0; u < 8; ++u) {
+        const int idx = t + u * kT;
+        if (u < per && idx < NB * 49) {
+          const int dp = idx / 49, e = idx - 49 * dp;
+          const int d = dp == BW ? 0 : dp + 1;       // retiring block (j + d, j)
+          int sc = jm + 1 + dp;
+          if (sc >= NB) sc -= NB;
+          double* slot = Wn + (size_t)tri_slot(jm, sc) * 49 + e;
+          a.lband[(size_t)j * NB * 49 + d * 49 + e] = (j + d < n) ? *slot : 0.0;
+          double v = pf[u];
+          if (dp == BW && (e / 7) == (e % 7)) v = v + lambda * v;
+          *slot = v;
+        }
+      }
+      if (t < 8) {
+        a.yb[(size_t)j * 8 + t] = Yw[jm * 8 + t];
+        Yw[jm * 8 + t] = t < 7 ? -pfr : 0.0;
       }
     }
-    if (t < 8) Yw[(j % NB) * 8 + t] = pfr;
     __syncthreads();
+    PGO_TIC(4);
   }
   double xx = 0.0;
   if (!s_fail) {
@@ -745,9 +766,14 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
       __syncthreads();
     }
   }
+  PGO_TIC(5);
   if (t == 0) {
     a.bres[0] = s_fail ? 1.0 : 0.0;
     a.bres[1] = xx;
+#ifdef LC_PGO_TIMING
+    for (int k = 0; k < 6; ++k) a.counts[k] += (unsigned long long)tim[k];
+    a.counts[6] += n;
+#endif
   }
 }
 
