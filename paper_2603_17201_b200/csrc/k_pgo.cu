@@ -570,7 +570,10 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
   double pf[8];   // prefetched blocks of the entering position
   for (int j = 0; j < n; ++j) {
     const int q = j + NB;
-    const double pfr = t < 7 ? grad_val(q, t) : 0.0;   // negated at the store
+    // the entering gradient: a dependent load pair (ord, then vd), issued by the last warp,
+    // which has no work in steps (1)-(2) and little in (3), so the Cholesky warp never waits on it
+    const int tr = t - (kT - 32);
+    const double pfr = (tr >= 0 && tr < 7) ? grad_val(q, tr) : 0.0;   // negated at the store
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int idx = t + u * kT;
@@ -581,39 +584,51 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
       }
     }
     double* A0 = Wn + (size_t)wslot(j, j, NB) * 49;
-    // (1) diagonal block: right-looking Cholesky by warp 0 in registers (lane l < 28 owns
-    //     entry l of the lower triangle, row-major), then y_j = L_jj^-1 y_j. The pivots'
-    //     reciprocals go to the unused upper triangle: invd[0] -> (1, 2), invd[k] -> (0, k).
-    if (t < 32) {
-      int i = 0, jj = 0;
-      if (t < 28) { while ((i + 1) * (i + 2) / 2 <= t) ++i; jj = t - i * (i + 1) / 2; }
-      double v = t < 28 ? A0[7 * i + jj] : 0.0;
-      double myinv = 0.0;
+    // (1) diagonal block: Cholesky by one thread with the block in registers (shuffle
+    //     latency made the warp-parallel version slower), then y_j = L_jj^-1 y_j. The
+    //     pivots' reciprocals go to the unused upper triangle: invd[0] -> (1, 2),
+    //     invd[k] -> (0, k).
+    if (t == 0) {
+      double L[28], inv[7];
+#pragma unroll
+      for (int i = 0; i < 7; ++i)
+#pragma unroll
+        for (int k = 0; k <= i; ++k) L[i * (i + 1) / 2 + k] = A0[7 * i + k];
       bool okc = true;
+#pragma unroll
       for (int k = 0; k < 7; ++k) {
-        const double akk = __shfl_sync(0xffffffffu, v, k * (k + 1) / 2 + k);
+        const double akk = L[k * (k + 1) / 2 + k];
         if (!(akk > 0.0)) { okc = false; break; }
-        const double inv = rsqrt(akk);
-        if (t == k) myinv = inv;
-        if (t < 28 && jj == k) v = i == k ? akk * inv : v * inv;
-        const double lik = __shfl_sync(0xffffffffu, v, i * (i + 1) / 2 + k);
-        const double ljk = __shfl_sync(0xffffffffu, v, jj * (jj + 1) / 2 + k);
-        if (t < 28 && jj > k) v -= lik * ljk;
+        inv[k] = rsqrt(akk);
+        L[k * (k + 1) / 2 + k] = akk * inv[k];
+#pragma unroll
+        for (int i = k + 1; i < 7; ++i) L[i * (i + 1) / 2 + k] *= inv[k];
+#pragma unroll
+        for (int i = k + 1; i < 7; ++i)
+#pragma unroll
+          for (int jj = k + 1; jj <= i; ++jj) L[i * (i + 1) / 2 + jj] -= L[i * (i + 1) / 2 + k] * L[jj * (jj + 1) / 2 + k];
       }
       if (!okc) {
-        if (t == 0) s_fail = 1;
+        s_fail = 1;
       } else {
-        if (t < 28) A0[7 * i + jj] = v;
-        if (t < 7) A0[t == 0 ? 9 : t] = myinv;
-        // forward substitution of y_j with the factor in registers
-        double y = t < 7 ? Yw[(j % NB) * 8 + t] : 0.0;
-        for (int k = 0; k < 7; ++k) {
-          if (t == k) y *= myinv;
-          const double yk = __shfl_sync(0xffffffffu, y, k);
-          const double lrk = __shfl_sync(0xffffffffu, v, t < 7 ? t * (t + 1) / 2 + k : 0);
-          if (t > k && t < 7) y -= lrk * yk;
+#pragma unroll
+        for (int i = 0; i < 7; ++i)
+#pragma unroll
+          for (int k = 0; k <= i; ++k) A0[7 * i + k] = L[i * (i + 1) / 2 + k];
+        A0[9] = inv[0];
+#pragma unroll
+        for (int k = 1; k < 7; ++k) A0[k] = inv[k];
+        double* yv = Yw + (j % NB) * 8;
+        double y[7];
+#pragma unroll
+        for (int r = 0; r < 7; ++r) {
+          double sacc = yv[r];
+#pragma unroll
+          for (int m = 0; m < r; ++m) sacc -= L[r * (r + 1) / 2 + m] * y[m];
+          y[r] = sacc * inv[r];
         }
-        if (t < 7) Yw[(j % NB) * 8 + t] = y;
+#pragma unroll
+        for (int r = 0; r < 7; ++r) yv[r] = y[r];
       }
     }
     __syncthreads();
@@ -695,9 +710,9 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
           *slot = v;
         }
       }
-      if (t < 8) {
-        a.yb[(size_t)j * 8 + t] = Yw[jm * 8 + t];
-        Yw[jm * 8 + t] = t < 7 ? -pfr : 0.0;
+      if (tr >= 0 && tr < 8) {
+        a.yb[(size_t)j * 8 + tr] = Yw[jm * 8 + tr];
+        Yw[jm * 8 + tr] = tr < 7 ? -pfr : 0.0;
       }
     }
     __syncthreads();
@@ -709,6 +724,7 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
     // column of the next step is prefetched into registers while this one is used
     const int per = (NB * 49 + kT - 1) / kT;
     double pf[8], pfy = 0.0;
+    int vnext = t == 0 ? a.ord[n - 1] : 0;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int idx = t + u * kT;
@@ -731,6 +747,8 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
         }
         if (t < 7) pfy = __ldcg(a.yb + (size_t)(j - 1) * 8 + t);
       }
+      const int vcur = vnext;
+      if (t == 0 && j > 0) vnext = a.ord[j - 1];
       if (t < 7 * BW) {
         const int d = 1 + t / 7, r = t % 7;
         double s = 0.0;
@@ -756,7 +774,7 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
           for (int m = r + 1; m < 7; ++m) s -= Lc[7 * m + r] * x[m];
           x[r] = s * Lc[r == 0 ? 9 : r];
         }
-        const int v = a.ord[j];
+        const int v = vcur;
         for (int r = 0; r < 7; ++r) {
           Xs[(j % NB) * 8 + r] = x[r];
           X[(size_t)v * kVec + r] = x[r];
