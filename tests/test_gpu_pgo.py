@@ -193,3 +193,52 @@ def test_full_size_drift_graph_properties(ctx, name):
         r = oracle.pgo_edge(g.M[e], S[i], S[j])[0]
         ch += float(r @ r)
     assert ch <= c1 * 1.000001
+
+
+def test_loop_event_chain_window_fuse_pgo_all(ctx):
+    """The whole loop-closing path on device data: WINDOW correction -> fuse -> essential-
+    graph PGO -> ALL propagation of the optimised Sim3s, each
+    stage checked against the oracle chain run on the same inputs."""
+    from lcsynth import make_world
+    from lcsynth.world import FUSE_PARAMS_CHECKS
+    from paper_2603_17201_b200 import Context
+    w = make_world("T1", 0)
+    c = Context(0)
+    c.upload_map(w.map_arrays(), [w.cam])
+    om = oracle.OracleMap(w)
+    S_g, _ = c.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    S_o, _ = om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    np.testing.assert_allclose(S_g, S_o, rtol=1e-12, atol=1e-12)
+    g = c.fuse(w.window, w.mp_list, FUSE_PARAMS_CHECKS)
+    o = om.fuse(w.window, w.mp_list, FUSE_PARAMS_CHECKS)
+    assert np.array_equal(g["winner"], o["winner"]) and np.array_equal(g["victim"], o["victim"])
+    # essential graph (SPEC build_essential_problem): every keyframe a vertex, corrected
+    # Sim3 for the window, pre-correction pose otherwise; temporal tree edges measured
+    # from the pre-correction poses; loop edges window KF -> its pass-A twin (KF i - n/2)
+    # measured from the corrected pose; the matched keyframe is fixed
+    n = w.n_kf
+    half = n // 2
+    S0 = w.kf_pose.copy()
+    S0[w.window] = S_o
+    edges, M = [], []
+    for k in range(1, n):
+        edges.append((k - 1, k))
+        M.append(oracle.sim3_compose(w.kf_pose[k], oracle.sim3_inverse(w.kf_pose[k - 1])))
+    for k in w.window:
+        edges.append((k - half, k))
+        M.append(oracle.sim3_compose(S0[k], oracle.sim3_inverse(S0[k - half])))
+    edges = np.asarray(edges, np.int32)
+    M = np.stack(M)
+    fixed = np.zeros(n, np.uint8)
+    fixed[w.cur_kf - half] = 1
+    Sg, trg, cg, cntg = c.pgo_sim3(S0, fixed, edges, M, max_iter=20, solver="band")
+    So, tro, co, cnto = oracle.pgo(S0, fixed, edges, M, max_iter=20)
+    assert co[0] > 0.0 and cg[1] < co[0]
+    compare((Sg, trg, cg, cntg), (So, tro, co, cnto))
+    c.correct_all(Sg)
+    om.correct_all(So)
+    st = c.download_map()
+    np.testing.assert_allclose(st["kf_pose"], om.kf_pose, rtol=0, atol=1e-8)
+    np.testing.assert_allclose(st["mp_pos"], om.mp_pos, rtol=1e-6, atol=1e-5)
+    assert np.array_equal(st["feat_mp"], om.feat_mp)
+    c.close()
