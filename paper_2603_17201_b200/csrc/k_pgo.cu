@@ -568,27 +568,15 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
   __syncthreads();
   const int per = (NB * 49 + kT - 1) / kT;
   double pf[8];   // prefetched blocks of the entering position
-  for (int j = 0; j < n; ++j) {
-    const int q = j + NB;
-    // the entering gradient: a dependent load pair (ord, then vd), issued by the last warp,
-    // which has no work in steps (1)-(2) and little in (3), so the Cholesky warp never waits on it
-    const int tr = t - (kT - 32);
-    const double pfr = (tr >= 0 && tr < 7) ? grad_val(q, tr) : 0.0;   // negated at the store
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int idx = t + u * kT;
-      pf[u] = 0.0;
-      if (u < per && idx < NB * 49) {
-        const int c = q - BW + idx / 49;   // blocks (q, c), c = j+1 .. q (damping added at store)
-        if (q < n) pf[u] = __ldcg(a.band + ((size_t)c * NB + (q - c)) * 49 + idx % 49);
-      }
-    }
-    double* A0 = Wn + (size_t)wslot(j, j, NB) * 49;
-    // (1) diagonal block: Cholesky by one thread with the block in registers (shuffle
-    //     latency made the warp-parallel version slower), then y_j = L_jj^-1 y_j. The
-    //     pivots' reciprocals go to the unused upper triangle: invd[0] -> (1, 2),
-    //     invd[k] -> (0, k).
-    if (t == 0) {
+  // Diagonal-block Cholesky by one thread with the block in registers (shuffle latency
+  // made a warp-parallel version slower), then y_jd = L^-1 y_jd. The pivots'
+  // reciprocals go to the unused upper triangle: invd[0] -> (1, 2), invd[k] -> (0, k).
+  // Look-ahead: block (j+1, j+1) only needs pair (1, 1) of the update of step j, so the
+  // last warp applies that pair with all its lanes and factors the block while the other
+  // warps apply the remaining pairs (the Cholesky leaves the critical path).
+  auto chol_diag = [&](int jd) {   // one thread
+    double* A0 = Wn + (size_t)wslot(jd, jd, NB) * 49;
+    {
       double L[28], inv[7];
 #pragma unroll
       for (int i = 0; i < 7; ++i)
@@ -618,7 +606,7 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
         A0[9] = inv[0];
 #pragma unroll
         for (int k = 1; k < 7; ++k) A0[k] = inv[k];
-        double* yv = Yw + (j % NB) * 8;
+        double* yv = Yw + (jd % NB) * 8;
         double y[7];
 #pragma unroll
         for (int r = 0; r < 7; ++r) {
@@ -631,6 +619,31 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
         for (int r = 0; r < 7; ++r) yv[r] = y[r];
       }
     }
+  };
+  if (t == 0 && n > 0) chol_diag(0);
+  __syncthreads();
+  int ordq = (t >= kT - 32 && t < kT - 25 && NB < n) ? __ldg(a.ord + NB) : 0;
+  for (int j = 0; j < n; ++j) {
+    const int q = j + NB;
+    // the entering gradient: a dependent load pair (ord, then vd), issued by the last warp,
+    // which has no work in steps (1)-(2) and little in (3), so the Cholesky warp never waits on it
+    const int tr = t - (kT - 32);
+    // (ord[q] was loaded one step earlier, so the gradient load does not wait on it)
+    const double pfr = (tr >= 0 && tr < 7 && q < n) ? __ldcg(a.vd + (size_t)ordq * kVD + 49 + tr) : 0.0;
+    ordq = (tr >= 0 && tr < 7 && q + 1 < n) ? __ldg(a.ord + q + 1) : 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = t + u * kT;
+      pf[u] = 0.0;
+      if (u < per && idx < NB * 49) {
+        const int c = q - BW + idx / 49;   // blocks (q, c), c = j+1 .. q (damping added at store)
+        if (q < n) pf[u] = __ldcg(a.band + ((size_t)c * NB + (q - c)) * 49 + idx % 49);
+      }
+    }
+    double* A0 = Wn + (size_t)wslot(j, j, NB) * 49;
+    // (1) the diagonal block was factored by the look-ahead of the previous step (with
+    //     bw = 0 position j enters the window only at the end of step j - 1: factor here)
+    if (BW == 0 && t == 0 && j > 0) chol_diag(j);
     __syncthreads();
     PGO_TIC(0);
     if (s_fail) break;
@@ -658,32 +671,52 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
     PGO_TIC(1);
     // (3) trailing update of the window: block (j+d2, j+d1) -= L_{j+d2, j} L_{j+d1, j}^T,
     //     thread per block pair (L_{j+d1, j} held in registers: 98 shared loads per 343
-    //     FMAs; a thread per (pair, row) re-reads L_{j+d1, j} 7 times and measured slower)
+    //     FMAs; a thread per (pair, row) re-reads L_{j+d1, j} 7 times and measured slower).
+    //     Pair (1, 1) belongs to the look-ahead warp.
     {
       const int nblk = BW * (BW + 1) / 2, jm = j % NB;
-      for (int b = t; b < nblk; b += kT) {
-        const int pr = pairs[b], d1 = pr & 0xff, d2 = pr >> 8;
-        if (j + d2 >= n) continue;
-        int s2 = jm + d2, s1 = jm + d1;
-        if (s2 >= NB) s2 -= NB;
-        if (s1 >= NB) s1 -= NB;
-        const double* L2 = Wn + (size_t)tri_slot(s2, jm) * 49;
-        const double* L1 = Wn + (size_t)tri_slot(s1, jm) * 49;
-        double* T = Wn + (size_t)tri_slot(s2, s1) * 49;
-        double l1[49];
-#pragma unroll
-        for (int k = 0; k < 49; ++k) l1[k] = L1[k];
-#pragma unroll
-        for (int r = 0; r < 7; ++r) {
-          double l2[7];
-#pragma unroll
-          for (int m = 0; m < 7; ++m) l2[m] = L2[7 * r + m];
-#pragma unroll
-          for (int c = 0; c < 7; ++c) {
+      if (t >= kT - 32) {
+        const int lane = t - (kT - 32);
+        if (BW > 0 && j + 1 < n) {
+          int s1 = jm + 1;
+          if (s1 >= NB) s1 -= NB;
+          const double* L1 = Wn + (size_t)tri_slot(s1, jm) * 49;
+          double* T = Wn + (size_t)tri_slot(s1, s1) * 49;
+          for (int e = lane; e < 49; e += 32) {
+            const int r = e / 7, c = e - 7 * r;
             double acc = 0.0;
 #pragma unroll
-            for (int m = 0; m < 7; ++m) acc += l2[m] * l1[7 * c + m];
-            T[7 * r + c] -= acc;
+            for (int m = 0; m < 7; ++m) acc += L1[7 * r + m] * L1[7 * c + m];
+            T[e] -= acc;
+          }
+          __syncwarp();
+          if (lane == 0) chol_diag(j + 1);
+        }
+      } else {
+        for (int b = 1 + t; b < nblk; b += kT - 32) {
+          const int pr = pairs[b], d1 = pr & 0xff, d2 = pr >> 8;
+          if (j + d2 >= n) continue;
+          int s2 = jm + d2, s1 = jm + d1;
+          if (s2 >= NB) s2 -= NB;
+          if (s1 >= NB) s1 -= NB;
+          const double* L2 = Wn + (size_t)tri_slot(s2, jm) * 49;
+          const double* L1 = Wn + (size_t)tri_slot(s1, jm) * 49;
+          double* T = Wn + (size_t)tri_slot(s2, s1) * 49;
+          double l1[49];
+#pragma unroll
+          for (int k = 0; k < 49; ++k) l1[k] = L1[k];
+#pragma unroll
+          for (int r = 0; r < 7; ++r) {
+            double l2[7];
+#pragma unroll
+            for (int m = 0; m < 7; ++m) l2[m] = L2[7 * r + m];
+#pragma unroll
+            for (int c = 0; c < 7; ++c) {
+              double acc = 0.0;
+#pragma unroll
+              for (int m = 0; m < 7; ++m) acc += l2[m] * l1[7 * c + m];
+              T[7 * r + c] -= acc;
+            }
           }
         }
       }
