@@ -535,8 +535,8 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
   double* Yw = Wn + (size_t)nw * 49;      // [NB][8]
   double* Xs = Yw + NB * 8;               // [NB][8] back-substitution window
   double* Lc = Xs + NB * 8;               // [NB][49] one factor column (back substitution)
-  double* part = Lc + NB * 49;            // [NB][8]
-  unsigned short* pairs = (unsigned short*)(part + NB * 8);   // [BW (BW + 1) / 2] (d1, d2)
+  double* part = Lc + NB * 49;            // [NB + 2][8]
+  unsigned short* pairs = (unsigned short*)(part + NB * 8 + 16);   // [BW (BW + 1) / 2] (d1, d2)
   __shared__ int s_fail;
 #ifdef LC_PGO_TIMING
   long long tim[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = clock64();
@@ -753,79 +753,88 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
   }
   double xx = 0.0;
   if (!s_fail) {
-    // back substitution: x_j = L_jj^-T (y_j - sum_d L_{j+d,j}^T x_{j+d}); the factor
-    // column of the next step is prefetched into registers while this one is used
-    const int per = (NB * 49 + kT - 1) / kT;
-    double pf[8], pfy = 0.0;
-    int vnext = t == 0 ? a.ord[n - 1] : 0;
+    // back substitution: x_j = L_jj^-T (y_j - sum_d L_{j+d,j}^T x_{j+d}), two barriers per
+    // position. Warps 0-6 = rows r of the 7-vector, lane d-1 = block d: each thread holds
+    // the 7 factor entries L_{j+d,j}[m][r] it needs (prefetched one position ahead), the
+    // warp's butterfly sums over d; the last warp holds the diagonal block (2 entries per
+    // lane), y_j and the vertex index, and its lane 0 solves the 7x7 triangle.
+    const int r = t >> 5, dl = t & 31, d = dl + 1;
+    const bool part_thr = t < kT - 32 && d <= BW;
+    const int lw = t - (kT - 32);   // lane in the last warp, < 0 elsewhere
+    const size_t col = (size_t)NB * 49;
+    double pf[7], pd0 = 0.0, pd1 = 0.0, pfy = 0.0;
+    int vnext = 0;
+    auto prefetch = [&](int jj) {
+      if (part_thr) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int idx = t + u * kT;
-      pf[u] = (u < per && idx < NB * 49) ? __ldcg(a.lband + (size_t)(n - 1) * NB * 49 + idx) : 0.0;
-    }
-    if (t < 7) pfy = __ldcg(a.yb + (size_t)(n - 1) * 8 + t);
+        for (int m = 0; m < 7; ++m) pf[m] = __ldcg(a.lband + jj * col + d * 49 + 7 * m + r);
+      }
+      if (lw >= 0) {
+        pd0 = __ldcg(a.lband + jj * col + lw);
+        pd1 = lw + 32 < 49 ? __ldcg(a.lband + jj * col + lw + 32) : 0.0;
+        pfy = lw < 7 ? __ldcg(a.yb + (size_t)jj * 8 + lw) : 0.0;
+        if (lw == 0) vnext = a.ord[jj];
+      }
+    };
+    prefetch(n - 1);
+    double* Dg = Lc;          // diagonal block of the current position
+    double* ssum = part;      // [8] sum over d
+    double* sy = part + 8;    // [8] y_j
     for (int j = n - 1; j >= 0; --j) {
+      double cur[7];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = t + u * kT;
-        if (u < per && idx < NB * 49) Lc[idx] = pf[u];
-      }
-      if (t < 7) part[NB * 8 - 8 + t] = pfy;   // y_j (last row of part is free: d <= BW)
-      __syncthreads();
-      if (j > 0) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int idx = t + u * kT;
-          if (u < per && idx < NB * 49) pf[u] = __ldcg(a.lband + (size_t)(j - 1) * NB * 49 + idx);
-        }
-        if (t < 7) pfy = __ldcg(a.yb + (size_t)(j - 1) * 8 + t);
-      }
+      for (int m = 0; m < 7; ++m) cur[m] = pf[m];
+      const double c0 = pd0, c1 = pd1, cy = pfy;
       const int vcur = vnext;
-      if (t == 0 && j > 0) vnext = a.ord[j - 1];
-      if (t < 7 * BW) {
-        const int d = 1 + t / 7, r = t % 7;
-        double s = 0.0;
-        if (j + d < n) {
+      if (j > 0) prefetch(j - 1);
+      if (t < kT - 32) {
+        double sacc = 0.0;
+        if (part_thr && j + d < n) {
           const double* xd = Xs + ((j + d) % NB) * 8;
 #pragma unroll
-          for (int m = 0; m < 7; ++m) s += Lc[d * 49 + 7 * m + r] * xd[m];
+          for (int m = 0; m < 7; ++m) sacc += cur[m] * xd[m];
         }
-        part[(d - 1) * 8 + r] = s;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        if (dl == 0) ssum[r] = sacc;
+      } else {
+        Dg[lw] = c0;
+        if (lw + 32 < 49) Dg[lw + 32] = c1;
+        if (lw < 7) sy[lw] = cy;
       }
       __syncthreads();
-      if (t < 7) {
-        double s = part[NB * 8 - 8 + t];
-        for (int d = 0; d < BW; ++d) s -= part[d * 8 + t];
-        part[NB * 8 - 8 + t] = s;
-      }
-      __syncthreads();
-      if (t == 0) {
+      if (lw == 0) {
         double x[7];
-        for (int r = 0; r < 7; ++r) x[r] = part[NB * 8 - 8 + r];
-        for (int r = 6; r >= 0; --r) {
-          double s = x[r];
-          for (int m = r + 1; m < 7; ++m) s -= Lc[7 * m + r] * x[m];
-          x[r] = s * Lc[r == 0 ? 9 : r];
+#pragma unroll
+        for (int q = 0; q < 7; ++q) x[q] = sy[q] - ssum[q];
+#pragma unroll
+        for (int q = 6; q >= 0; --q) {
+          double sacc = x[q];
+#pragma unroll
+          for (int m = q + 1; m < 7; ++m) sacc -= Dg[7 * m + q] * x[m];
+          x[q] = sacc * Dg[q == 0 ? 9 : q];
         }
-        const int v = vcur;
-        for (int r = 0; r < 7; ++r) {
-          Xs[(j % NB) * 8 + r] = x[r];
-          X[(size_t)v * kVec + r] = x[r];
-          xx += x[r] * x[r];
+#pragma unroll
+        for (int q = 0; q < 7; ++q) {
+          Xs[(j % NB) * 8 + q] = x[q];
+          X[(size_t)vcur * kVec + q] = x[q];
+          xx += x[q] * x[q];
         }
       }
       __syncthreads();
     }
   }
   PGO_TIC(5);
-  if (t == 0) {
+  if (t == kT - 32) {   // the back substitution's solving thread holds |x|^2
     a.bres[0] = s_fail ? 1.0 : 0.0;
     a.bres[1] = xx;
+  }
 #ifdef LC_PGO_TIMING
+  if (t == 0) {
     for (int k = 0; k < 6; ++k) a.counts[k] += (unsigned long long)tim[k];
     a.counts[6] += n;
-#endif
   }
+#endif
 }
 
 __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
@@ -1103,7 +1112,7 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
 static size_t band_smem_bytes(int bw) {
   if (bw < 0) return 0;
   const size_t NB = (size_t)bw + 1;
-  return sizeof(double) * (NB * (NB + 1) / 2 * 49 + NB * 8 * 3 + NB * 49) + 2 * NB * NB;
+  return sizeof(double) * (NB * (NB + 1) / 2 * 49 + NB * 8 * 3 + 16 + NB * 49) + 2 * NB * NB;
 }
 
 int pgo_max_bw() { return kBWMax; }
