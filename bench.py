@@ -518,8 +518,20 @@ def main():
                           "accepted": int(pc[counts.index("pgo_accepted")]),
                           "solver_iterations": int(pc[counts.index("pgo_solver_iters")]),
                           "chi2": [float(p2[0]), float(p2[1])],
-                          "solver": "banded Cholesky (RCM order)" if pc[counts.index("pgo_solver_iters")]
-                          == pc[counts.index("pgo_iters")] else "block-Jacobi CG"}
+                          "solver": "banded Cholesky (RCM order)" if pc[counts.index("pgo_band")] > 0
+                          else "block-Jacobi CG"}
+            bw = int(pc[counts.index("pgo_band")]) - 1
+            if bw >= 0:
+                # window-update FLOPs of the banded factorisations (BW(BW+1)/2 block pairs x
+                # 7x7x7 FMAs per position; the panel, Cholesky and solves are < 10% more)
+                # against ONE SM's fp64 peak (64 FMA/clk x 2 x 1.965 GHz = 251 GFLOP/s,
+                # derived from the unit count: the factorisation runs in one CTA)
+                flops = float(pgo[gname]["lm_iterations"]) * g.n_v * bw * (bw + 1) / 2 * 343 * 2
+                ach = flops / (pgo[gname]["ms_per_call"] * 1e-3) / 1e9
+                pgo[gname]["bandwidth_blocks"] = bw
+                pgo[gname]["roofline"] = {"bound": "latency (one-CTA banded factorisation)", "achieved": round(ach, 2),
+                                          "peak": 251.5, "unit": "GFLOP/s fp64 (one SM)",
+                                          "frac": round(ach / 251.5, 4)}
         sbp = {"config": f"C4: {len(w4.pair_kf)} (hypothesis, keyframe) pairs, "
                          f"{len(w4.pair_mp_list)} queries, 3 parameter sets",
                "ms_per_call": round(s_ms, 5), "candidates": cand4,

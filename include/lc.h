@@ -198,6 +198,7 @@ enum {
   LC_COUNT_PGO_ACCEPTED,   /* pose graph: accepted steps                             */
   LC_COUNT_PGO_SOLVER_ITERS, /* pose graph: conjugate-gradient iterations, all solves */
   LC_COUNT_PGO_STOP,       /* pose graph: stop reason (LC_PGO_STOP_*)                 */
+  LC_COUNT_PGO_BAND,       /* pose graph: 1 + block bandwidth of the banded solve, 0 = CG */
   LC_NCOUNT
 };
 
@@ -532,7 +533,7 @@ lc_status lc_search_by_projection(lc_ctx* ctx, int32_t n_pairs, const int32_t* p
  *     |delta| (-1 if failed), solver iterations (CG iterations; 1 for the banded solve).
  *   out_chi2 [host|dev] nullable [2]: initial and final chi2.
  *   out_counts [host|dev] nullable [LC_NCOUNT] (PGO_ITERS, PGO_ACCEPTED,
- *     PGO_SOLVER_ITERS, PGO_STOP).
+ *     PGO_SOLVER_ITERS, PGO_STOP, PGO_BAND).
  * The whole loop runs in one cooperative kernel (no host round trip per iteration);
  * results are deterministic for a given problem. Not capturable (LC_ESTATE while a
  * graph capture is open).

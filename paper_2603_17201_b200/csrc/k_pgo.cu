@@ -1104,6 +1104,7 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
     a.counts[LC_COUNT_PGO_ACCEPTED] = (unsigned long long)accepted;
     a.counts[LC_COUNT_PGO_SOLVER_ITERS] = (unsigned long long)cg_total;
     a.counts[LC_COUNT_PGO_STOP] = (unsigned long long)stop;
+    a.counts[LC_COUNT_PGO_BAND] = (unsigned long long)(a.bw + 1);
   }
 }
 

@@ -54,6 +54,7 @@ def test_pgo_matches_oracle(ctx, name, seed, mode, solver):
     orr = oracle.pgo(g.S_init, g.fixed, g.edges, g.M, max_iter=30)
     compare(gr, orr)
     assert gr[3]["pgo_solver_iters"] > 0
+    assert (gr[3]["pgo_band"] > 0) == (solver == "band")
 
 
 @pytest.mark.parametrize("solver", ["band", "cg"])
