@@ -25,10 +25,11 @@ for name in sys.argv[1:] or ["C2", "C3", "C5"]:
             b.record()
             torch.cuda.synchronize()
             ms.append(a.elapsed_time(b))
-        cnt = cnt.cpu().numpy()
+        from paper_2603_17201_b200 import COUNTER_NAMES
+        cd = dict(zip(COUNTER_NAMES, cnt.cpu().numpy().tolist()))
         c2 = c2.cpu().numpy()
-        tr = tr.cpu().numpy()[:cnt[-4]]
-        print(f"{name} n_v={g.n_v} n_e={g.n_e} {solver} cg_tol={cg_tol:g} ms={np.median(ms):.3f} iters={cnt[-4]} "
-              f"acc={cnt[-3]} cg={cnt[-2]} stop={cnt[-1]} chi2 {c2[0]:.6g}->{c2[1]:.6g}", flush=True)
+        tr = tr.cpu().numpy()[:cd["pgo_iters"]]
+        print(f"{name} n_v={g.n_v} n_e={g.n_e} {solver} cg_tol={cg_tol:g} ms={np.median(ms):.3f} iters={cd['pgo_iters']} "
+              f"acc={cd['pgo_accepted']} solver_it={cd['pgo_solver_iters']} stop={cd['pgo_stop']} bw={cd['pgo_band'] - 1} chi2 {c2[0]:.6g}->{c2[1]:.6g}", flush=True)
         print("   cg per iter", tr[:, 5].astype(int).tolist())
 ctx.close()
