@@ -243,3 +243,16 @@ def test_loop_event_chain_window_fuse_pgo_all(ctx):
     np.testing.assert_allclose(st["mp_pos"], om.mp_pos, rtol=1e-6, atol=1e-5)
     assert np.array_equal(st["feat_mp"], om.feat_mp)
     c.close()
+
+
+@pytest.mark.parametrize("solver", ["band", "cg"])
+def test_two_components_each_with_a_fixed_vertex(ctx, solver):
+    """Two disjoint graphs in one call (the RCM ordering handles components one after the
+    other; CG's block-Jacobi preconditioner sees one block-diagonal system)."""
+    g1, g2 = make_pose_graph("G1", 8), make_pose_graph("G0", 9)
+    S0 = np.concatenate([g1.S_init, g2.S_init])
+    fixed = np.concatenate([g1.fixed, g2.fixed]).astype(np.uint8)
+    E = np.concatenate([g1.edges, g2.edges + g1.n_v])
+    M = np.concatenate([g1.M, g2.M])
+    gr = ctx.pgo_sim3(S0, fixed, E, M, max_iter=30, solver=solver, **TIGHT)
+    compare(gr, oracle.pgo(S0, fixed, E, M, max_iter=30))
