@@ -429,7 +429,7 @@ def main():
 
     # secondary: SURVEY §8 a9, batched read-only guided search on C4 (32 hypotheses x
     # (current KF + 3 covisible) pairs, PS2a / PS2b / PS1-3 parameter sets)
-    sbp = ransac = pgo = None
+    sbp = ransac = pgo = loops = None
     if ws == 1 and not args.profile_only and not args.no_sbp:
         from lcsynth.world import SBP_PARAMS
         w4 = make_world("C4", args.seed)
@@ -496,6 +496,38 @@ def main():
                   "ms_per_call": round(float(np.mean(rms)), 5),
                   "refine_ms_per_call": round(float(np.mean(fms)), 5),
                   "refine_steps": int(rf4[counts.index("refine_iters")])}
+        # the same loop event on the EuRoC- and TUM-VI-shaped maps:
+        # device-timed like the headline (L2 flushed, state restored between steps)
+        loops = {}
+        for cname in ("C2", "C3"):
+            wc = make_world(cname, args.seed)
+            cc = Context(local)
+            cc.upload_map(wc.map_arrays(), [wc.cam], grid=grid)
+            cc.state_save()
+            lst = torch.from_numpy(wc.mp_list).to(dev)
+            Sop = torch.from_numpy(wc.S_opt).to(dev)
+            lms, lcnt = [], None
+            for i in range(args.warmup + args.steps):
+                cc.state_restore()
+                flush.fill_(1.0)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                cc.correct_window(wc.cur_kf, wc.S_cw_corr, wc.window, host=False)
+                rl = cc.fuse(wc.window, lst, FUSE_PARAMS, window_S=wc.win_S, win_list_begin=wc.win_list_begin,
+                             action=False, host=False)
+                cc.correct_all(Sop, host=False)
+                b.record(stream)
+                b.synchronize()
+                if i >= args.warmup:
+                    lms.append(a.elapsed_time(b))
+                lcnt = rl["counts"]
+            lc = lcnt.cpu().numpy()
+            cand = int(lc[counts.index("candidates")])
+            lm = float(np.mean(lms))
+            loops[cname] = {"keyframes": wc.n_kf, "map_points": wc.n_mp, "window": len(wc.window),
+                            "queries": int(lc[counts.index("queries")]), "candidates": cand,
+                            "ms_per_loop": round(lm, 5), "value": round(cand / (lm / 1000.0), 1), "unit": UNIT}
+            cc.close()
         # essential-graph Sim3 pose-graph optimisation (the producer of the
         # S_opt that lc_correct_sim3 ALL propagates) on the C3- and C5-sized graphs
         pgo = {}
@@ -570,6 +602,7 @@ def main():
             "connections": connections,
             "ransac": ransac,
             "pgo": pgo,
+            "loop_configs": loops,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -25,7 +25,9 @@ constexpr int WSTR = 56;
 constexpr int ASTR = 28;
 constexpr int32_t OWNER_NONE = 0x7F7F7F7F;  // memset byte pattern 0x7F
 #ifndef LC_PT_MINB
+#ifndef LC_PT_MINB
 #define LC_PT_MINB 2   // point kernels: CTAs per SM the register budget is cut for
+#endif
 #endif
 #ifndef LC_OWN_PRECHECK
 #define LC_OWN_PRECHECK 0
