@@ -218,10 +218,17 @@ def main():
 
     if args.warmup < 3:
         args.warmup = 3
+    # one rank per GPU; the modulo only matters for a test launch of several ranks on one
+    # device (LC_DIST_BACKEND=gloo), never on a real node
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if ws > 1:
-        tdist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("LC_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=dev)
+        else:
+            tdist.init_process_group(backend)
     w = make_world(args.config, args.seed)
     ctx = Context(local)
     grid = tuple(int(x) for x in args.grid.lower().split("x"))
@@ -246,6 +253,8 @@ def main():
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     cnt_fuse = None
 
+    comm_ev = []   # (start, end) around the all-reduce of the current step (N > 1)
+
     def step():
         ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
         if ws == 1:
@@ -255,7 +264,8 @@ def main():
             c = r["counts"]
         else:
             c, _, _ = lcdist.fuse_sharded(ctx, w.window, mp_list_d, FUSE_PARAMS, window_S=w.win_S,
-                                          win_list_begin=w.win_list_begin, device=dev, tables=tables)
+                                          win_list_begin=w.win_list_begin, device=dev, tables=tables,
+                                          events=comm_ev[0] if comm_ev else None)
         ctx.correct_all(S_opt_d, host=False)
         return c
 
@@ -284,12 +294,17 @@ def main():
     clocks = Clocks(local)
     l0 = ctx.kernel_launches()
     ctx.profile_enable(True)
+    comm_pairs = []
     for i in range(args.steps):
         reset()
+        if ws > 1:
+            comm_ev[:] = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))]
+            comm_pairs.append(comm_ev[0])
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)
     torch.cuda.synchronize()
+    comm_ev.clear()
     if ws > 1:
         tdist.barrier()
     prof = ctx.profile_read()
@@ -305,6 +320,14 @@ def main():
         tdist.all_reduce(cand_t, op=tdist.ReduceOp.SUM)
     ms_step = float(ms_t.item())
     cand_total = int(cand_t.item())
+    multi = None
+    if ws > 1:   # the exchange's share of the step (max over ranks)
+        cm = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in comm_pairs]))], dtype=torch.float64,
+                          device=dev)
+        tdist.all_reduce(cm, op=tdist.ReduceOp.MAX)
+        multi = {"allreduce_ms_per_step": round(float(cm.item()), 5), "allreduce_bytes": int(tables.numel() * 8),
+                 "collective": "all_reduce(MIN) int64 [winner | victim] (" + tdist.get_backend() + ")",
+                 "compute_ms_per_step": round(ms_step - float(cm.item()), 5)}
     value = cand_total / (ms_step / 1000.0)
 
     # roofline of the dominant stage: fuse matching = k_project -> k_match (one launch each
@@ -603,6 +626,7 @@ def main():
             "ransac": ransac,
             "pgo": pgo,
             "loop_configs": loops,
+            "multi_gpu": multi,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -38,11 +38,13 @@ def shard_bounds(n_window: int, world: int, win_list_begin=None, n_list: int = 0
 
 
 def fuse_sharded(fuser, window, mp_list, params, *, window_S=None, win_list_begin=None,
-                 group=None, device=None, tables=None):
+                 group=None, device=None, tables=None, events=None):
     """PLAN on this rank's shard -> all_reduce(MIN) of [winner | victim] -> APPLY.
 
     tables: optional preallocated int64 tensor of n_wfeat + n_mp entries on `device`
-    (the NCCL buffer); returns (plan_counts, apply_counts, merged tables)."""
+    (the NCCL buffer); events: optional (start, end) CUDA events recorded on the current
+    stream around the all-reduce (the exchange's share of the step);
+    returns (plan_counts, apply_counts, merged tables)."""
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     n_w = len(window)
@@ -60,7 +62,11 @@ def fuse_sharded(fuser, window, mp_list, params, *, window_S=None, win_list_begi
     plan = fuser.fuse(window, mp_list, params, window_S=window_S, win_list_begin=win_list_begin,
                       phase=LC_FUSE_PLAN, w_lo=lo, w_hi=hi, winner=w_arg, victim=v_arg,
                       action=False, host=host)
+    if events is not None:
+        events[0].record()
     dist.all_reduce(tables, op=dist.ReduceOp.MIN, group=group)
+    if events is not None:
+        events[1].record()
     app = fuser.fuse(window, mp_list, params, window_S=window_S, win_list_begin=win_list_begin,
                      phase=LC_FUSE_APPLY, winner=w_arg, victim=v_arg, action=False, host=host)
     return plan["counts"], app["counts"], tables
