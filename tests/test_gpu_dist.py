@@ -71,3 +71,23 @@ def test_sharded_fuse_two_ranks_equals_single_gpu(tmp_path, name, on_device):
         assert np.array_equal(d["tables"], ref_tables), f"rank {r}: merged tables"
         for key in ("feat_mp", "mp_flags", "mp_replaced_by", "mp_nobs"):
             assert np.array_equal(d[key], st[key]), f"rank {r}: {key}"
+
+
+def test_bench_two_ranks_gloo_one_device():
+    """bench.py's N > 1 path (keyframe-sharded fuse, all-reduce, max-over-ranks timing,
+    multi_gpu entry) end to end: two ranks on the one device over gloo (LC_DIST_BACKEND)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LC_DIST_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29541", "bench.py", "--gpus", "2",
+                          "--steps", "3", "--warmup", "3", "--config", "C2"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert line["multi_gpu"]["allreduce_bytes"] > 0
+    assert line["config"]["parallelism"] == "keyframe-sharded x2"
