@@ -535,8 +535,8 @@ lc_status lc_search_by_projection(lc_ctx* ctx, int32_t n_pairs, const int32_t* p
  *   out_counts [host|dev] nullable [LC_NCOUNT] (PGO_ITERS, PGO_ACCEPTED,
  *     PGO_SOLVER_ITERS, PGO_STOP, PGO_BAND).
  * The whole loop runs in one cooperative kernel (no host round trip per iteration);
- * results are deterministic for a given problem. Not capturable (LC_ESTATE while a
- * graph capture is open).
+ * results are deterministic for a given problem. Capturable (lc_graph_*): the edge
+ * list, fixed flags and the host-built incidence / RCM order are constants of the graph.
  * Errors: LC_EINVAL (null pointers, sizes, params, i == j), LC_ERANGE (vertex index),
  * LC_ECUDA (cooperative launch failed).
  * ------------------------------------------------------------------------- */

@@ -974,7 +974,7 @@ lc_status lc_pgo_sim3(lc_ctx* c, int32_t n_v, const lc_sim3* S_init, const uint8
                       const int32_t* edge_ij, const lc_sim3* M, const lc_pgo_params* params, lc_sim3* out_S,
                       double* out_trace, double* out_chi2, int64_t* out_counts, void* stream) {
   return guarded(c, [&] {
-    capture_gate(c, stream, false);
+    capture_gate(c, stream, true);
     REQUIRE(params, LC_EINVAL, "null params");
     const lc_pgo_params p = *params;
     REQUIRE(n_v >= 0 && n_e >= 0 && n_e < (1 << 30) && p.max_iter >= 0 && p.cg_max_iter >= 1 && p.lambda0 > 0.0 &&

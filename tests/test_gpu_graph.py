@@ -115,3 +115,43 @@ def test_capture_misuse_fails_loudly(Ctx):
     So, _ = om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
     assert np.array_equal(Sg, So)
     ctx.close()
+
+
+def test_graph_pgo_then_all_correction(Ctx):
+    """lc_pgo_sim3 inside a captured graph (its cooperative kernel and argument block are
+    graph-owned), feeding lc_correct_sim3(ALL) on the device: a replay equals the eager
+    calls bit for bit."""
+    from lcsynth import make_pose_graph
+    w = make_world("T1", 0)
+    g = make_pose_graph("G0", 0)   # any graph with n_v = n_kf vertices works for the plumbing
+    n = w.n_kf
+    rng = np.random.default_rng(0)
+    S0 = np.concatenate([g.S_init] * (n // g.n_v + 1))[:n].copy()
+    E = np.stack([np.arange(n - 1), np.arange(1, n)], 1).astype(np.int32)
+    M = np.stack([oracle.sim3_compose(oracle.pgo_exp(0.01 * rng.standard_normal(7)),
+                                      oracle.sim3_compose(S0[j], oracle.sim3_inverse(S0[i]))) for i, j in E])
+    fixed = np.zeros(n, np.uint8)
+    fixed[0] = 1
+    dev = torch.device("cuda:0")
+    S0_d, M_d = torch.from_numpy(S0).to(dev), torch.from_numpy(M).to(dev)
+    outs = []
+    for mode in ("eager", "graph"):
+        ctx = Ctx(0)
+        ctx.upload_map(w.map_arrays(), [w.cam])
+        ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+        if mode == "eager":
+            S, tr, c2, cnt = ctx.pgo_sim3(S0_d, fixed, E, M_d, host=False)
+            ctx.correct_all(S, host=False)
+        else:
+            with ctx.capture() as cap:
+                S, tr, c2, cnt = ctx.pgo_sim3(S0_d, fixed, E, M_d, host=False)
+                ctx.correct_all(S, host=False)
+            cap.graph.launch()
+        torch.cuda.synchronize()
+        outs.append((S.cpu().numpy().copy(), cnt.cpu().numpy().copy(), ctx.download_map()))
+        ctx.close()
+    (Se, ce, me), (Sg, cg, mg) = outs
+    np.testing.assert_array_equal(Se, Sg)
+    np.testing.assert_array_equal(ce, cg)
+    np.testing.assert_array_equal(me["kf_pose"], mg["kf_pose"])
+    np.testing.assert_array_equal(me["mp_pos"], mg["mp_pos"])
