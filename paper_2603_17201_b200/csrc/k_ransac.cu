@@ -321,7 +321,7 @@ struct RefineArgs {
 
 __global__ void __launch_bounds__(LC_NTHREADS) k_refine(const RefineArgs a) {
   __shared__ double s_J[RCH][4][7], s_r[RCH][4], s_w[RCH][2];
-  __shared__ uint8_t s_ok[RCH];
+  __shared__ uint8_t s_ok[RCH], s_okj[RCH][7];
   __shared__ double s_H[49], s_g[7], s_S[13], s_dn;
   __shared__ int s_spd, s_ninl;
   __shared__ DevCam s_k1, s_k2;
@@ -357,12 +357,25 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_refine(const RefineArgs a) {
         __syncthreads();
         for (int ch = 0; ch < nc; ch += RCH) {
           const int n = min(RCH, nc - ch);
-          for (int l = tid; l < n; l += blockDim.x) {   // per correspondence, in parallel
-            const int i = ch + l;
+          // one work item per (correspondence, Jacobian column): the 14 perturbed residual
+          // evaluations of a correspondence run on 7 threads (the values are the same as
+          // a thread per correspondence would compute; only the assignment changes)
+          for (int wk = tid; wk < n * 7; wk += blockDim.x) {
+            const int l = wk / 7, j = wk - 7 * l, i = ch + l;
             bool ok = a.out_mask[c0 + i] != 0;
-            double r[4];
-            ok = ok && residuals(s_k1, s_k2, S, P(i, 1), P(i, 2), U(i, 1), U(i, 2), r);
-            for (int j = 0; j < 7 && ok; ++j) {
+            if (j == 0) {
+              double r[4];
+              const bool ok0 = ok && residuals(s_k1, s_k2, S, P(i, 1), P(i, 2), U(i, 1), U(i, 2), r);
+              s_ok[l] = ok0 ? 1 : 0;
+              if (ok0) {
+                const double s1 = (double)a.sig1[c0 + i], s2 = (double)a.sig2[c0 + i];
+                const double e1 = (r[0] * r[0] + r[1] * r[1]) / s1, e2 = (r[2] * r[2] + r[3] * r[3]) / s2;
+                for (int q = 0; q < 4; ++q) s_r[l][q] = r[q];
+                s_w[l][0] = huber_w(e1, delta) / s1;
+                s_w[l][1] = huber_w(e2, delta) / s2;
+              }
+            }
+            if (ok) {
               double dp[7] = {0, 0, 0, 0, 0, 0, 0}, dm[7] = {0, 0, 0, 0, 0, 0, 0};
               dp[j] = h; dm[j] = -h;
               double Sp[13], Sm[13], rp[4], rm[4];
@@ -372,14 +385,13 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_refine(const RefineArgs a) {
                    residuals(s_k1, s_k2, Sm, P(i, 1), P(i, 2), U(i, 1), U(i, 2), rm);
               for (int q = 0; q < 4; ++q) s_J[l][q][j] = (rp[q] - rm[q]) / (2.0 * h);
             }
-            s_ok[l] = ok ? 1 : 0;
-            if (ok) {
-              const double s1 = (double)a.sig1[c0 + i], s2 = (double)a.sig2[c0 + i];
-              const double e1 = (r[0] * r[0] + r[1] * r[1]) / s1, e2 = (r[2] * r[2] + r[3] * r[3]) / s2;
-              for (int q = 0; q < 4; ++q) s_r[l][q] = r[q];
-              s_w[l][0] = huber_w(e1, delta) / s1;
-              s_w[l][1] = huber_w(e2, delta) / s2;
-            }
+            s_okj[l][j] = ok ? 1 : 0;
+          }
+          __syncthreads();
+          for (int l = tid; l < n; l += blockDim.x) {   // usable iff every evaluation succeeded
+            uint8_t all = s_ok[l];
+            for (int j = 0; j < 7; ++j) all &= s_okj[l][j];
+            s_ok[l] = all;
           }
           __syncthreads();
           if (tid < 35) {   // one entry per thread, accumulated in (correspondence, residual) order
