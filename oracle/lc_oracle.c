@@ -45,9 +45,11 @@
  * written (compile with -O2 -ffp-contract=off, no -ffast-math), fp32 only for
  * stored values. No grid, no atomics, no reordering.
  *
- * Parity status: every function is pinned by tests/test_oracle_pins.py except
- * the orientation-histogram rule beyond its hand-built cases (A15), which is
- * "parity unpinned" against the paper (the paper prints nothing about it).
+ * Parity status: every function is pinned by tests/test_oracle_pins.py (O1-O14) and
+ * tests/test_oracle_pgo.py (O15: scipy expm/logm, central differences, the hand-derived
+ * adjoint, closed forms, exact-truth recovery) except the orientation-histogram rule
+ * beyond its hand-built cases (A15), which is "parity unpinned" against the paper (the
+ * paper prints nothing about it).
  */
 #include <math.h>
 #include <stdint.h>
