@@ -399,12 +399,18 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_refine(const RefineArgs a) {
             if (tid < 28) { x = 0; while ((x + 1) * (x + 2) / 2 <= tid) ++x; y = tid - x * (x + 1) / 2; }
             else { x = tid - 28; y = -1; }
             double acc = y >= 0 ? s_H[7 * x + y] : s_g[x];
+            // branch-free so the products of later correspondences are formed while the
+            // ordered additions run: a skipped correspondence adds +0.0, which leaves the
+            // accumulator's bits unchanged (it starts at +0.0 and never becomes -0.0)
+#pragma unroll 4
             for (int l = 0; l < n; ++l) {
-              if (!s_ok[l]) continue;
+              const bool okl = s_ok[l] != 0;
+#pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const double wq = q < 2 ? s_w[l][0] : s_w[l][1];
-                if (y >= 0) acc = acc + wq * s_J[l][q][x] * s_J[l][q][y];
-                else acc = acc + wq * s_J[l][q][x] * s_r[l][q];
+                const double other = y >= 0 ? s_J[l][q][y] : s_r[l][q];
+                const double prod = wq * s_J[l][q][x] * other;
+                acc = acc + (okl ? prod : 0.0);
               }
             }
             if (y >= 0) s_H[7 * x + y] = acc; else s_g[x] = acc;
