@@ -243,12 +243,32 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_refresh(const RefreshArgs a) {
       __syncwarp();
       if (a.what & LC_REFRESH_DESC) {   // A35
         uint32_t best = 0xFFFFFFFFu;   // (median << 16) | rank
-        for (int i = lane; i < N; i += 32) {
-          const uint4 x0 = s_d[warp][i][0], x1 = s_d[warp][i][1];
-          uint16_t row[OBS_CAP];   // the row once; the median search then only compares
-          for (int j = 0; j < N; ++j) row[j] = (uint16_t)hamming32(x0, x1, s_d[warp][j][0], s_d[warp][j][1]);
-          const int med = row_median(N, [&](int j) { return (int)row[j]; });
-          best = min(best, ((uint32_t)med << 16) | (uint32_t)i);
+        if (N <= 16) {   // the common case: the row in registers (fully unrolled, no local memory)
+          for (int i = lane; i < N; i += 32) {
+            const uint4 x0 = s_d[warp][i][0], x1 = s_d[warp][i][1];
+            int row[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              row[j] = j < N ? hamming32(x0, x1, s_d[warp][j][0], s_d[warp][j][1]) : 1 << 20;
+            const int k = (N - 1) / 2;
+            int lo = 0, hi = 256;   // smallest v with #{d <= v} >= k + 1 (as row_median)
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              int c = 0;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) c += row[j] <= mid;
+              if (c >= k + 1) hi = mid; else lo = mid + 1;
+            }
+            best = min(best, ((uint32_t)lo << 16) | (uint32_t)i);
+          }
+        } else {
+          for (int i = lane; i < N; i += 32) {
+            const uint4 x0 = s_d[warp][i][0], x1 = s_d[warp][i][1];
+            uint16_t row[OBS_CAP];   // the row once; the median search then only compares
+            for (int j = 0; j < N; ++j) row[j] = (uint16_t)hamming32(x0, x1, s_d[warp][j][0], s_d[warp][j][1]);
+            const int med = row_median(N, [&](int j) { return (int)row[j]; });
+            best = min(best, ((uint32_t)med << 16) | (uint32_t)i);
+          }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
