@@ -207,7 +207,10 @@ __device__ __forceinline__ int row_median(int N, DistAt dist_at) {
   return lo;
 }
 
-__global__ void __launch_bounds__(LC_NTHREADS) k_refresh(const RefreshArgs a) {
+#ifndef LC_RF_MINB
+#define LC_RF_MINB 5   // k_refresh CTAs per SM the register budget is cut for (shared memory allows 5)
+#endif
+__global__ void __launch_bounds__(LC_NTHREADS, LC_RF_MINB) k_refresh(const RefreshArgs a) {
   __shared__ int32_t s_tmp[RWARPS][OBS_CAP];
   __shared__ int32_t s_ord[RWARPS][OBS_CAP];
   __shared__ uint4 s_d[RWARPS][OBS_CAP][2];
