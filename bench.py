@@ -176,6 +176,17 @@ def run_reference(args, w, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def pgo_cpu_baseline(seed):
+    """Oracle O15 (never tuned: dense LDL^T of the reduced system) for ONE Levenberg-Marquardt
+    iteration on the C2 essential graph (300 keyframes, 2,093 unknowns)."""
+    import oracle
+    from lcsynth import make_pose_graph
+    g = make_pose_graph("C2", seed)
+    t0 = time.perf_counter()
+    oracle.pgo(g.S_init, g.fixed, g.edges, g.M, max_iter=1)
+    return (time.perf_counter() - t0) * 1000.0
+
+
 def cpu_baseline(w, seconds):
     """Oracle (never tuned) on a bounded sample of the benchmark workload."""
     import oracle
@@ -587,6 +598,23 @@ def main():
                 pgo[gname]["roofline"] = {"bound": "latency (one-CTA banded factorisation)", "achieved": round(ach, 2),
                                           "peak": 251.5, "unit": "GFLOP/s fp64 (one SM)",
                                           "frac": round(ach / 251.5, 4)}
+        if rank == 0 and not args.no_cpu_baseline:
+            # one LM iteration on C2, device vs the oracle on one host core (context)
+            g2 = make_pose_graph("C2", args.seed)
+            gS2, gM2 = torch.from_numpy(g2.S_init).to(dev), torch.from_numpy(g2.M).to(dev)
+            ones = []
+            for i in range(3):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                c4.pgo_sim3(gS2, g2.fixed, g2.edges, gM2, max_iter=1, host=False)
+                b.record(stream)
+                b.synchronize()
+                if i:
+                    ones.append(a.elapsed_time(b))
+            pgo["C2_one_iteration"] = {"gpu_ms": round(float(np.mean(ones)), 3),
+                                       "cpu_baseline": {"ms": round(pgo_cpu_baseline(args.seed), 1), "cores": 1,
+                                                        "kind": "oracle (dense LDL^T, dual-number Jacobians)",
+                                                        "sample": "one LM iteration, C2 graph (300 KFs)"}}
         sbp = {"config": f"C4: {len(w4.pair_kf)} (hypothesis, keyframe) pairs, "
                          f"{len(w4.pair_mp_list)} queries, 3 parameter sets",
                "ms_per_call": round(s_ms, 5), "candidates": cand4,
