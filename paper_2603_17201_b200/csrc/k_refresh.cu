@@ -207,6 +207,91 @@ __device__ __forceinline__ int row_median(int N, DistAt dist_at) {
   return lo;
 }
 
+// One point with <= 16 observations on a 16-lane group (lane gl, group mask): the full-warp
+// path's expressions and orders (A34-A37), so the results are the same bits.
+__device__ __forceinline__ void point_small(const RefreshArgs& a, const int q, const int b, const int N,
+                                            const int gl, const unsigned mask, int32_t* tmp, int32_t* ord,
+                                            int32_t* kfa, uint4 (*d)[2], double (*u)[3], double* len) {
+  const int32_t* gobs = a.obs + b;
+  if (gl < N) tmp[gl] = gobs[gl];
+  __syncwarp(mask);
+  if (gl < N) {   // A34: rank by feature index (distinct)
+    const int32_t f = tmp[gl];
+    int r = 0;
+    for (int j = 0; j < N; ++j) r += tmp[j] < f;
+    ord[r] = f;
+    kfa[r] = a.obs_kf[b + gl];
+  }
+  __syncwarp(mask);
+  if (gl < N) {
+    const int cp = a.feat_cpos[ord[gl]];
+    d[gl][0] = a.fc_desc[2 * (size_t)cp];
+    d[gl][1] = a.fc_desc[2 * (size_t)cp + 1];
+  }
+  __syncwarp(mask);
+  if (a.what & LC_REFRESH_DESC) {   // A35
+    uint32_t best = 0xFFFFFFFFu;
+    if (gl < N) {
+      const uint4 x0 = d[gl][0], x1 = d[gl][1];
+      int row[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) row[j] = j < N ? hamming32(x0, x1, d[j][0], d[j][1]) : 1 << 20;
+      const int k = (N - 1) / 2;
+      int lo = 0, hi = 256;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) c += row[j] <= mid;
+        if (c >= k + 1) hi = mid; else lo = mid + 1;
+      }
+      best = ((uint32_t)lo << 16) | (uint32_t)gl;
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(mask, best, o));
+    if (gl == 0) {
+      const int i = (int)(best & 0xFFFFu);
+      uint4* dst = reinterpret_cast<uint4*>(&a.rec[q].desc[0]);
+      dst[0] = d[i][0];
+      dst[1] = d[i][1];
+    }
+  }
+  if (a.what & LC_REFRESH_NORMAL) {   // A36 / A37
+    MpRec& r = a.rec[q];
+    const double p[3] = {(double)r.pos[0], (double)r.pos[1], (double)r.pos[2]};
+    if (gl < N) {
+      const int k = kfa[gl];
+      double O[3], v[3];
+      kf_centre(a.kf_pose, k, O);
+      for (int j = 0; j < 3; ++j) v[j] = p[j] - O[j];
+      const double l = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+      for (int j = 0; j < 3; ++j) u[gl][j] = l == 0.0 ? 0.0 : v[j] / l;
+      len[gl] = l;
+    }
+    __syncwarp(mask);
+    if (gl == 0) {
+      double acc[3] = {0.0, 0.0, 0.0};
+      int nn = 0;
+      for (int i = 0; i < N; ++i) {
+        if (len[i] == 0.0) continue;
+        for (int j = 0; j < 3; ++j) acc[j] = acc[j] + u[i][j];
+        ++nn;
+      }
+      if (nn > 0)
+        for (int j = 0; j < 3; ++j) r.normal[j] = (float)(acc[j] / (double)nn);
+      const int ref = a.ref_kf[q];
+      for (int i = 0; i < N; ++i) {
+        if (kfa[i] != ref) continue;
+        int lvl = (int)((a.fc_meta[a.feat_cpos[ord[i]]] >> 16) & 0xFFu);
+        if (lvl >= a.n_levels) lvl = a.n_levels - 1;
+        r.dmax = (float)(len[i] * a.scale[lvl]);
+        break;
+      }
+    }
+  }
+  __syncwarp(mask);
+}
+
 #ifndef LC_RF_MINB
 #define LC_RF_MINB 5   // k_refresh CTAs per SM the register budget is cut for (shared memory allows 5)
 #endif
@@ -219,11 +304,16 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_RF_MINB) k_refresh(const Refre
   __shared__ int32_t s_kf[RWARPS][OBS_CAP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t c_mp = 0, c_obs = 0;
-  for (int t = blockIdx.x * RWARPS + warp; t < a.n_sel; t += gridDim.x * RWARPS) {
-    const int q = a.idx ? a.idx[t] : t;
-    if ((unsigned)q >= (unsigned)a.n_mp || (a.flags[q] & 1u)) continue;   // A33
-    const int b = a.obeg[q], N = a.obeg[q + 1] - b;
-    if (N <= 0) continue;
+  // A33: the point of selection entry t, or -1 (out of range, bad, unobserved)
+  auto point_of = [&](int t, int& q, int& b, int& N) {
+    q = a.idx ? a.idx[t] : t;
+    N = 0;
+    if ((unsigned)q >= (unsigned)a.n_mp || (a.flags[q] & 1u)) return;
+    b = a.obeg[q];
+    N = a.obeg[q + 1] - b;
+  };
+  // one point with the whole warp (any N)
+  auto full_point = [&](const int q, const int b, const int N) {
     if (lane == 0) { ++c_mp; c_obs += (uint32_t)N; }
     const int32_t* gobs = a.obs + b;
     if (N <= OBS_CAP) {
@@ -350,6 +440,28 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_RF_MINB) k_refresh(const Refre
         }
       }
       if ((a.what & LC_REFRESH_NORMAL) && lane == 0) refresh_geometry(a, q, N, nullptr, gobs);
+    }
+  };
+  // points are taken two at a time: when both have <= 16 observations (the common case)
+  // each half-warp refreshes one (point_small, the same expressions and orders), else the
+  // whole warp does them one after the other
+  for (int t0 = 2 * (blockIdx.x * RWARPS + warp); t0 < a.n_sel; t0 += 2 * gridDim.x * RWARPS) {
+    int qq[2] = {0, 0}, bb[2] = {0, 0}, NN[2] = {0, 0};
+    point_of(t0, qq[0], bb[0], NN[0]);
+    if (t0 + 1 < a.n_sel) point_of(t0 + 1, qq[1], bb[1], NN[1]);
+    if (NN[0] <= 16 && NN[1] <= 16) {
+      const int h = lane >> 4, gl = lane & 15;
+      if (NN[h] > 0) {
+        if (gl == 0) { ++c_mp; c_obs += (uint32_t)NN[h]; }
+        point_small(a, qq[h], bb[h], NN[h], gl, 0xFFFFu << (16 * h), &s_tmp[warp][32 * h], &s_ord[warp][32 * h],
+                    &s_kf[warp][32 * h], &s_d[warp][32 * h], &s_u[warp][32 * h], &s_len[warp][32 * h]);
+      }
+    } else {
+      for (int h = 0; h < 2; ++h)
+        if (NN[h] > 0) {
+          full_point(qq[h], bb[h], NN[h]);
+          __syncwarp();
+        }
     }
     __syncwarp();
   }
