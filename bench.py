@@ -561,6 +561,27 @@ def main():
             loops[cname] = {"keyframes": wc.n_kf, "map_points": wc.n_mp, "window": len(wc.window),
                             "queries": int(lc[counts.index("queries")]), "candidates": cand,
                             "ms_per_loop": round(lm, 5), "value": round(cand / (lm / 1000.0), 1), "unit": UNIT}
+            if not args.no_graph:   # the same event replayed as one CUDA graph (launch gaps gone)
+                cc.state_restore()
+                torch.cuda.synchronize()
+                with cc.capture() as cap:
+                    cc.correct_window(wc.cur_kf, wc.S_cw_corr, wc.window, host=False)
+                    cc.fuse(wc.window, lst, FUSE_PARAMS, window_S=wc.win_S, win_list_begin=wc.win_list_begin,
+                            action=False, host=False)
+                    cc.correct_all(Sop, host=False)
+                gl = []
+                for i in range(args.warmup + args.steps):
+                    cc.state_restore()
+                    flush.fill_(1.0)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    cap.graph.launch()
+                    b.record(stream)
+                    b.synchronize()
+                    if i >= args.warmup:
+                        gl.append(a.elapsed_time(b))
+                loops[cname]["graph_ms_per_loop"] = round(float(np.mean(gl)), 5)
+                cap.graph.close()
             cc.close()
         # essential-graph Sim3 pose-graph optimisation (the producer of the
         # S_opt that lc_correct_sim3 ALL propagates) on the C3- and C5-sized graphs
