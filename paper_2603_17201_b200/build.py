@@ -2,6 +2,7 @@
 import glob
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -30,10 +31,25 @@ def build(force=False, verbose=False):
     if not force and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), "-o", LIB, *sources()]
+    inc = "-I" + os.path.join(ROOT, "include")
+    odir = os.path.join(PKG, "build")
+    os.makedirs(odir, exist_ok=True)
+    comp = [f for f in NVCC_FLAGS if f != "-shared"]
+    objs = []
+    cmds = []
+    for src in sources():   # one translation unit per kernel file, compiled in parallel
+        obj = os.path.join(odir, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        cmds.append([nvcc, *comp, inc, "-c", "-o", obj, src])
     if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+        for cmd in cmds:
+            print(" ".join(cmd))
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+        list(ex.map(subprocess.check_call, cmds))
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs]
+    if verbose:
+        print(" ".join(link))
+    subprocess.check_call(link)
     return LIB
 
 

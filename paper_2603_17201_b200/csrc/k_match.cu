@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_resolve(const MatchArgs a) {
 // Per-call setup: LoopSet stamps, winner/victim init, window membership. The call's
 // epoch is ep[0] + 1 (device counter, so that a replayed CUDA graph gets a fresh one);
 // the last block to finish publishes it in ep[0] for the kernels that follow.
-__global__ void k_fuse_prep(int phase, int init_winner, uint32_t* __restrict__ ep, int n_w,
+__global__ void k_fuse_prep(int phase, int64_t skip_lo, int64_t skip_hi, uint32_t* __restrict__ ep, int n_w,
                             const int32_t* __restrict__ window, int64_t n_wfeat,
                             const int32_t* __restrict__ mp_list, int64_t n_list, int n_mp,
                             unsigned long long* __restrict__ winner,
@@ -804,8 +804,10 @@ __global__ void k_fuse_prep(int phase, int init_winner, uint32_t* __restrict__ e
       const int32_t q = mp_list[i];
       if ((unsigned)q < (unsigned)n_mp) loop_ep[q] = epoch;
     }
-    if (init_winner)
-      for (int64_t i = t0; i < n_wfeat; i += stride) winner[i] = NONE;
+    // every winner word is NONE after PLAN except those a sole-mode match CTA owns
+    // ([skip_lo, skip_hi): the shard's own units, initialised by their CTAs)
+    for (int64_t i = t0; i < n_wfeat; i += stride)
+      if (i < skip_lo || i >= skip_hi) winner[i] = NONE;
     for (int64_t i = t0; i < n_mp; i += stride) victim[i] = NONE;
   }
   __syncthreads();
@@ -1077,8 +1079,9 @@ cudaError_t launch_resolve(lc_ctx* c, int mode, const MatchArgs& a, int n_units,
   return cudaGetLastError();
 }
 
-cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, const int32_t* d_window,
-                             int64_t n_wfeat, const int32_t* mp_list, int64_t n_list_total,
+cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int64_t skip_lo, int64_t skip_hi, int n_w,
+                             const int32_t* d_window, int64_t n_wfeat, const int32_t* mp_list,
+                             int64_t n_list_total,
                              unsigned long long* winner, unsigned long long* victim,
                              unsigned long long* counts, cudaStream_t s) {
   Store& st = c->st;
@@ -1086,10 +1089,10 @@ cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, con
   int64_t n = std::max<int64_t>(n_w, n_vbits);
   if (phase & LC_FUSE_PLAN) {
     n = std::max<int64_t>(n, n_list_total);
-    if (init_winner) n = std::max<int64_t>(n, n_wfeat);
+    if (skip_hi - skip_lo < n_wfeat) n = std::max<int64_t>(n, n_wfeat);
     n = std::max<int64_t>(n, st.n_mp);
   }
-  k_fuse_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(phase, init_winner, st.ep, n_w, d_window, n_wfeat,
+  k_fuse_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(phase, skip_lo, skip_hi, st.ep, n_w, d_window, n_wfeat,
                                                  mp_list, n_list_total, st.n_mp, winner, victim,
                                                  st.mp_loop_ep, st.kf_win_ep, st.kf_win_pos,
                                                  st.mp_vbits, n_vbits, st.kf_dirty, counts);

@@ -1273,7 +1273,10 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     else epoch_reserve(c, 1, call.s);
     {
       Prof pr(c, LC_PROF_FUSE_PREP, call.s);
-      CK(launch_fuse_prep(c, phase, sole ? 0 : 1, n_window, d_win, n_wfeat, d_list, pipe ? 0 : n_list,
+      // sole-mode CTAs initialise their own units' words; every other word of the
+      // table (the other shards' units included) is set to NONE here (lc.h contract)
+      const int64_t skip_lo = sole ? woff[w_lo] : 0, skip_hi = sole ? woff[w_hi] : 0;
+      CK(launch_fuse_prep(c, phase, skip_lo, skip_hi, n_window, d_win, n_wfeat, d_list, pipe ? 0 : n_list,
                           win, vic, cnt, call.s));
     }
     if (phase & LC_FUSE_PLAN) {

@@ -324,8 +324,10 @@ cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, co
                                cudaStream_t s);
 cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max, int part,
                          cudaStream_t s, bool pdl = true);  // part 0: k_project, 1: k_match; blocks [a.blk_base, +n_blocks)
-cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int init_winner, int n_w, const int32_t* d_window,
-                             int64_t n_wfeat, const int32_t* mp_list, int64_t n_list_total,
+// winner words [0, n_wfeat) are set to NONE except [skip_lo, skip_hi) (sole-mode units)
+cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int64_t skip_lo, int64_t skip_hi, int n_w,
+                             const int32_t* d_window, int64_t n_wfeat, const int32_t* mp_list,
+                             int64_t n_list_total,
                              unsigned long long* winner, unsigned long long* victim,
                              unsigned long long* counts, cudaStream_t s);   // zeroes counts
 cudaError_t launch_resolve(lc_ctx* c, int mode, const MatchArgs& a, int n_units, cudaStream_t s);

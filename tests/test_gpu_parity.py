@@ -322,3 +322,52 @@ def test_C5_pipelined_host_list_equals_device_list(Ctx, pinned):
     assert gd["counts"] == gh["counts"]
     for key in md:
         assert np.array_equal(md[key], mh[key]), key
+
+
+@pytest.mark.slow
+def test_C5_sharded_sole_mode_plan_merge_apply_equals_fuse_all(Ctx):
+    """The C5 window split into 2 / 4 / 8 keyframe shards (1250 / 625 / 312 keyframes:
+    every shard takes the sole-mode launch, one CTA per keyframe). Each PLAN writes into
+    tables prefilled with a non-NONE pattern: lc.h promises every winner word outside the
+    shard and every victim word is NONE afterwards, so the elementwise MIN (what NCCL
+    all_reduce(MIN) computes) followed by APPLY must equal FUSE_ALL byte for byte
+    (§IV.D.3: keyframes are independent)."""
+    from paper_2603_17201_b200 import LC_FUSE_APPLY, LC_FUSE_PLAN
+    from paper_2603_17201_b200.dist import shard_bounds
+    w = world("C5")
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    ctx.state_save()
+    dev = torch.device("cuda:0")
+    lst = torch.from_numpy(w.mp_list).to(dev)
+    ref = ctx.fuse(w.window, lst, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+    ref_map = ctx.download_map()
+    woff = np.r_[0, np.cumsum(np.diff(w.kf_feat_begin)[w.window])]
+    n_w = len(w.window)
+    garbage = 0x0000000500001234   # (H = 5, q = 0x1234): would win every MIN it meets
+    for W in (2, 4, 8):
+        ctx.state_restore()
+        bounds = shard_bounds(n_w, W, w.win_list_begin)
+        assert min(hi - lo for lo, hi in bounds) >= 296   # sole mode on every shard
+        win = vic = None
+        for lo, hi in bounds:
+            tw = torch.full((int(woff[-1]),), garbage, dtype=torch.int64, device=dev)
+            tv = torch.full((w.n_mp,), garbage, dtype=torch.int64, device=dev)
+            ctx.fuse(w.window, lst, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin,
+                     phase=LC_FUSE_PLAN, w_lo=lo, w_hi=hi, winner=tw, victim=tv, action=False, host=False)
+            torch.cuda.synchronize()
+            out = torch.ones(int(woff[-1]), dtype=torch.bool, device=dev)
+            out[int(woff[lo]):int(woff[hi])] = False
+            assert bool((tw[out] == NONE).all()), (W, lo, hi, "winner words outside the shard")
+            assert not bool((tv == garbage).any()), (W, lo, hi, "victim words")
+            win = tw if win is None else torch.minimum(win, tw)
+            vic = tv if vic is None else torch.minimum(vic, tv)
+        assert np.array_equal(win.cpu().numpy(), ref["winner"]), W
+        assert np.array_equal(vic.cpu().numpy(), ref["victim"]), W
+        ctx.fuse(w.window, lst, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin,
+                 phase=LC_FUSE_APPLY, winner=win, victim=vic, action=False, host=False)
+        m = ctx.download_map()
+        for key in ref_map:
+            assert np.array_equal(m[key], ref_map[key]), (W, key)
+    ctx.close()
