@@ -24,7 +24,7 @@ COUNTER_NAMES = [
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
     "refresh_mp", "refresh_obs", "conn_kf", "conn_edges", "ransac_hyp", "ransac_inliers",
     "refine_iters", "refine_inliers", "pgo_iters", "pgo_accepted", "pgo_solver_iters", "pgo_stop",
-    "pgo_band",
+    "pgo_band", "forced", "edge_amb",
 ]
 NONE64 = np.iinfo(np.int64).max
 
@@ -36,7 +36,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle (plain C, -ffp-contract=off so fp64 runs in written order)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-                               "-shared", "-o", _LIB, _SRC, "-lm"])
+                               "-shared", "-o", _LIB, _SRC, "-lm", "-lpthread"])
     return _LIB
 
 
@@ -83,8 +83,11 @@ def lib():
         _lib.orc_predict_level.restype = C.c_int
         _lib.orc_predict_level.argtypes = [C.c_double, C.c_double, C.c_void_p, C.c_int32]
         for fn in ("orc_correct_window", "orc_correct_all", "orc_fuse", "orc_search_by_projection",
-                   "orc_refresh", "orc_update_connections", "orc_sim3_ransac", "orc_sim3_refine", "orc_pgo"):
+                   "orc_refresh", "orc_update_connections", "orc_sim3_ransac", "orc_sim3_refine", "orc_pgo",
+                   "orc_correct_window_batch", "orc_fuse_plan_grid"):
             getattr(_lib, fn).restype = C.c_int
+        _lib.orc_grid_build.restype = C.c_void_p
+        _lib.orc_grid_free.argtypes = [C.c_void_p]
     return _lib
 
 
@@ -189,6 +192,15 @@ def predict_level(d, dmax, L=8, f=1.2):
 # ----------------------------------------------------------------------------
 # map state
 # ----------------------------------------------------------------------------
+class _Grid:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if self.h:
+            lib().orc_grid_free(self.h)
+            self.h = None
+
 class OracleMap:
     """Mutable copy of a world's map plus the loop state, driven by the C oracle."""
 
@@ -262,6 +274,30 @@ class OracleMap:
             raise ValueError("orc_correct_window: invalid arguments")
         return out_S, dict(zip(COUNTER_NAMES, cnt.tolist()))
 
+    # -- O3' -----------------------------------------------------------------
+    def correct_window_batch(self, cur_kf, S_cw_corr, window_begin, window, capacity=None):
+        """Dry-run window corrections of several hypotheses (no write-back): returns
+        (S_corr [sum window, 13], mp_begin [n_batch + 1], mp_idx, mp_pos [n, 3], counts)."""
+        cur = np.ascontiguousarray(cur_kf, np.int32)
+        nb = len(cur)
+        S = np.ascontiguousarray(S_cw_corr, np.float64).reshape(nb, 13)
+        wb = np.ascontiguousarray(window_begin, np.int32)
+        win = np.ascontiguousarray(window, np.int32)
+        out_S = np.zeros((len(win), 13), np.float64)
+        mb = np.zeros(nb + 1, np.int32)
+        cap = nb * self.n_mp if capacity is None else int(capacity)
+        idx = np.zeros(max(cap, 1), np.int32)
+        pos = np.zeros((max(cap, 1), 3), np.float32)
+        cnt = np.zeros(len(COUNTER_NAMES), np.int64)
+        rc = lib().orc_correct_window_batch(C.byref(self._m), C.c_int32(nb), _p(cur), _p(S), _p(wb), _p(win),
+                                            _p(out_S), _p(mb), _p(idx), _p(pos), C.c_int64(cap), _p(cnt))
+        if rc == -1:
+            raise ValueError("orc_correct_window_batch: invalid arguments")
+        if rc == -2:
+            raise OverflowError(f"capacity {cap} < {int(mb[-1])} corrected points")
+        n = int(mb[-1])
+        return out_S, mb, idx[:n], pos[:n], dict(zip(COUNTER_NAMES, cnt.tolist()))
+
     # -- O10 -----------------------------------------------------------------
     def correct_all(self, S_opt):
         S = np.ascontiguousarray(S_opt, np.float64).reshape(-1, 13)
@@ -274,7 +310,7 @@ class OracleMap:
         return int(sum(self.n_feat_of(int(k)) for k in window))
 
     def fuse(self, window, mp_list, params, *, window_S=None, win_list_begin=None, phase=3,
-             w_lo=0, w_hi=None, winner=None, victim=None, debug=False):
+             w_lo=0, w_hi=None, winner=None, victim=None, debug=False, cur_kf=-1, forced_mp=None):
         window = np.ascontiguousarray(window, np.int32)
         n_w = len(window)
         w_hi = n_w if w_hi is None else w_hi
@@ -295,13 +331,41 @@ class OracleMap:
         prm = make_params(params)
         if not (0 <= w_lo <= w_hi <= n_w):
             raise ValueError("bad shard range")
-        lib().orc_fuse(C.byref(self._m), C.c_int32(phase), C.c_int32(w_lo), C.c_int32(w_hi),
+        fm = None if forced_mp is None else np.ascontiguousarray(forced_mp, np.int32)
+        if fm is not None and len(fm) != self.n_feat_of(int(cur_kf)):
+            raise ValueError("forced_mp must have F(cur_kf) entries")
+        rc = lib().orc_fuse(C.byref(self._m), C.c_int32(phase), C.c_int32(w_lo), C.c_int32(w_hi),
                        C.c_int32(n_w), _p(window), _p(wS), _p(wb), _p(mp_list),
-                       C.c_int32(len(mp_list)), C.byref(prm), _p(winner), _p(victim), _p(action),
+                       C.c_int32(len(mp_list)), C.byref(prm), C.c_int32(int(cur_kf)), _p(fm),
+                       _p(winner), _p(victim), _p(action),
                        _p(dbg.get("status")), _p(dbg.get("best")), _p(dbg.get("uv")),
                        _p(dbg.get("ncand")), _p(dbg.get("edge")), _p(cnt))
+        if rc != 0:
+            raise ValueError("orc_fuse: invalid arguments")
         return dict(winner=winner, victim=victim, action=action,
                     counts=dict(zip(COUNTER_NAMES, cnt.tolist())), **dbg)
+
+    # -- timing-only grid / threaded PLAN (bench.py cpu_baseline) --------------
+    def grid(self, cols=64, rows=48):
+        """Per-keyframe cell grid for fuse_plan_grid (built once per map, untimed)."""
+        h = lib().orc_grid_build(C.byref(self._m), C.c_int32(cols), C.c_int32(rows))
+        return _Grid(h)
+
+    def fuse_plan_grid(self, grid, n_threads, window, mp_list, params, *, window_S=None, win_list_begin=None):
+        window = np.ascontiguousarray(window, np.int32)
+        mp_list = np.ascontiguousarray(mp_list, np.int32)
+        wb = None if win_list_begin is None else np.ascontiguousarray(win_list_begin, np.int32)
+        wS = None if window_S is None else np.ascontiguousarray(window_S, np.float64).reshape(-1, 13)
+        winner = np.full(self.window_feat_total(window), NONE64, np.int64)
+        victim = np.full(self.n_mp, NONE64, np.int64)
+        cnt = np.zeros(len(COUNTER_NAMES), np.int64)
+        prm = make_params(params)
+        rc = lib().orc_fuse_plan_grid(C.byref(self._m), C.c_void_p(grid.h), C.c_int32(n_threads),
+                                      C.c_int32(len(window)), _p(window), _p(wS), _p(wb), _p(mp_list),
+                                      C.c_int32(len(mp_list)), C.byref(prm), _p(winner), _p(victim), _p(cnt))
+        if rc != 0:
+            raise ValueError("orc_fuse_plan_grid: invalid arguments")
+        return dict(winner=winner, victim=victim, counts=dict(zip(COUNTER_NAMES, cnt.tolist())))
 
     # -- batched projection search -------------------------------------------
     def search_by_projection(self, pair_kf, pair_S, pair_param, params, pair_list_begin, mp_list,

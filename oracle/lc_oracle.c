@@ -14,6 +14,14 @@
  *   - Loop fusion: project the loop map points into every window keyframe,
  *     match by descriptor "within close spatial proximity", and merge
  *     duplicates (§III.B; §IV.D.3)  -> orc_fuse        (O4-O9)
+ *     including the forced loop matches of the current keyframe, fused first
+ *     (O9.4, reading A23)
+ *   - the same window correction as a batch of dry runs (no write-back), one per
+ *     loop-candidate hypothesis (§IV.C: candidates in batches)
+ *                                                               -> orc_correct_window_batch (O3')
+ *   - a thread-parallel, cell-grid version of the fuse PLAN for TIMING ONLY (the
+ *     CPU baseline); it is tested equal to the brute-force definition
+ *                                                               -> orc_fuse_plan_grid
  *   - Projection search PS1 / PS2a||PS2b / PS3a-c, one result batch per
  *     (keyframe, transform) pair (§IV.C; §IV.D.1-2)
  *                                                               -> orc_search_by_projection
@@ -45,13 +53,17 @@
  * written (compile with -O2 -ffp-contract=off, no -ffast-math), fp32 only for
  * stored values. No grid, no atomics, no reordering.
  *
- * Parity status: every function is pinned by tests/test_oracle_pins.py (O1-O14) and
+ * Parity status: every function is pinned by tests/test_oracle_pins.py (O1-O14),
  * tests/test_oracle_pgo.py (O15: scipy expm/logm, central differences, the hand-derived
- * adjoint, closed forms, exact-truth recovery) except the orientation-histogram rule
- * beyond its hand-built cases (A15), which is "parity unpinned" against the paper (the
- * paper prints nothing about it).
+ * adjoint, closed forms, exact-truth recovery) and tests/test_oracle_pins_r2.py (O9.4
+ * forced matches against an independent restatement of EXT Replace; O3' dry runs against
+ * the O3 invariant and 4x4 products; the A15 bin mapping by a histogram that floor(),
+ * 30-degree bins or a missing 30 -> 0 wrap each change; the edge flag at constructed
+ * distances; grid PLAN == brute-force PLAN). The orientation rule itself (three maxima,
+ * 0.1 ratio) remains "parity unpinned" against the paper, which prints nothing about it.
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -66,7 +78,7 @@ enum {
   C_VICTIMS, C_REWIRED, C_DUP_CLEARED, C_ADDED, C_CORR_KF, C_CORR_MP,
   C_REFRESH_MP, C_REFRESH_OBS, C_CONN_KF, C_CONN_EDGES, C_RANSAC_HYP, C_RANSAC_INLIERS,
   C_REFINE_ITERS, C_REFINE_INLIERS, C_PGO_ITERS, C_PGO_ACCEPTED, C_PGO_SOLVER_ITERS,
-  C_PGO_STOP, C_PGO_BAND, C_N
+  C_PGO_STOP, C_PGO_BAND, C_FORCED, C_EDGE_AMB, C_N
 };
 
 /* query status codes written to out_status (negative = culled/skipped) */
@@ -357,15 +369,12 @@ static void orientation_filter(const orc_map *m, int32_t k, int64_t *win, int32_
 /* ------------------------------------------------------------------------- */
 /* O3 window correction (SPEC.md:391-399 gives the shape).       */
 /* ------------------------------------------------------------------------- */
-int orc_correct_window(orc_map *m, int32_t cur_kf, const double *S_cw_corr, int32_t n_w,
-                       const int32_t *window, double *out_S_corr, int64_t *cnt) {
-  if (n_w <= 0 || window[0] != cur_kf) return -1;
-  for (int32_t i = 0; i < m->n_mp; ++i) m->mp_corr_ref[i] = -1;
-  for (int32_t k = 0; k < m->n_kf; ++k) m->kf_in_window[k] = 0;
-  /* 1. S_iw^corr from the OLD poses */
+/* O3 steps 1-2: S_iw^corr of every window keyframe from the OLD poses, and the
+ * owner (first window keyframe in list order observing it) of every non-bad map point. */
+static void window_sim3_owner(const orc_map *m, int32_t cur_kf, const double *S_cw_corr, int32_t n_w,
+                              const int32_t *window, double *Sc, int32_t *owner) {
   double Tc_inv[13];
   orc_sim3_inverse(m->kf_pose + 13 * (size_t)cur_kf, Tc_inv);
-  double *Sc = (double *)malloc(sizeof(double) * 13 * (size_t)n_w);
   for (int32_t i = 0; i < n_w; ++i) {
     int32_t k = window[i];
     if (k == cur_kf) { memcpy(Sc + 13 * i, S_cw_corr, 13 * sizeof(double)); continue; }
@@ -373,8 +382,6 @@ int orc_correct_window(orc_map *m, int32_t cur_kf, const double *S_cw_corr, int3
     orc_sim3_compose(m->kf_pose + 13 * (size_t)k, Tc_inv, S_ic);
     orc_sim3_compose(S_ic, S_cw_corr, Sc + 13 * i);
   }
-  /* 2-4. owner = first window KF (list order) observing the non-bad MP */
-  int32_t *owner = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_mp > 0 ? m->n_mp : 1));
   for (int32_t q = 0; q < m->n_mp; ++q) owner[q] = -1;
   for (int32_t i = 0; i < n_w; ++i) {
     int32_t k = window[i];
@@ -384,16 +391,31 @@ int orc_correct_window(orc_map *m, int32_t cur_kf, const double *S_cw_corr, int3
       if (owner[q] < 0) owner[q] = i;
     }
   }
-  for (int32_t q = 0; q < m->n_mp; ++q) {
+}
+
+/* O3 step 3: p <- fl32( inverse(S_owner^corr)( T_owner,w^old (p) ) ) */
+static void window_point(const orc_map *m, const double *T_old, const double *S_corr, int32_t q, float *out) {
+  double p[3], pc[3], pw[3], Sinv[13];
+  for (int j = 0; j < 3; ++j) p[j] = (double)m->mp_pos[3 * q + j];
+  orc_sim3_apply(T_old, p, pc);                                /* T_owner,w^old (p) */
+  orc_sim3_inverse(S_corr, Sinv);
+  orc_sim3_apply(Sinv, pc, pw);                                /* inverse(S^corr)(.) */
+  for (int j = 0; j < 3; ++j) out[j] = (float)pw[j];
+}
+
+int orc_correct_window(orc_map *m, int32_t cur_kf, const double *S_cw_corr, int32_t n_w,
+                       const int32_t *window, double *out_S_corr, int64_t *cnt) {
+  if (n_w <= 0 || window[0] != cur_kf) return -1;
+  for (int32_t i = 0; i < m->n_mp; ++i) m->mp_corr_ref[i] = -1;
+  for (int32_t k = 0; k < m->n_kf; ++k) m->kf_in_window[k] = 0;
+  double *Sc = (double *)malloc(sizeof(double) * 13 * (size_t)n_w);
+  int32_t *owner = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_mp > 0 ? m->n_mp : 1));
+  window_sim3_owner(m, cur_kf, S_cw_corr, n_w, window, Sc, owner);   /* 1, 2 */
+  for (int32_t q = 0; q < m->n_mp; ++q) {                              /* 3, 4 */
     if (owner[q] < 0) continue;
     int32_t i = owner[q];
     int32_t k = window[i];
-    double p[3], pc[3], pw[3], Sinv[13];
-    for (int j = 0; j < 3; ++j) p[j] = (double)m->mp_pos[3 * q + j];
-    orc_sim3_apply(m->kf_pose + 13 * (size_t)k, p, pc);       /* T_owner,w^old (p) */
-    orc_sim3_inverse(Sc + 13 * i, Sinv);
-    orc_sim3_apply(Sinv, pc, pw);                              /* inverse(S^corr)(.) */
-    for (int j = 0; j < 3; ++j) m->mp_pos[3 * q + j] = (float)pw[j];
+    window_point(m, m->kf_pose + 13 * (size_t)k, Sc + 13 * i, q, m->mp_pos + 3 * (size_t)q);
     m->mp_corr_ref[q] = k;
     cnt[C_CORR_MP]++;
   }
@@ -408,6 +430,54 @@ int orc_correct_window(orc_map *m, int32_t cur_kf, const double *S_cw_corr, int3
   }
   free(owner);
   free(Sc);
+  return 0;
+}
+
+/* O3' the window correction of several loop-candidate hypotheses as dry runs (SURVEY.md
+ * §8(d) C4: "32 lc_correct_sim3 dry runs"; §IV.C processes loop candidates
+ * in batches). Batch b = (cur_kf[b], S_cw_corr[b], window wbeg[b]..wbeg[b+1]) gets O3
+ * steps 1-3 against the map as it is (nothing is written back, batches are independent):
+ * out_S [sum window][13] = S_iw^corr; out_mp_begin [n_batch+1] = CSR of the corrected
+ * points, out_mp_idx / out_mp_pos = the owned map points of the batch in ascending index
+ * with their corrected positions. Returns -1 on bad arguments, -2 if the points do not
+ * fit in `capacity` (out_mp_begin is still complete). */
+int orc_correct_window_batch(const orc_map *m, int32_t n_batch, const int32_t *cur_kf,
+                             const double *S_cw_corr, const int32_t *wbeg, const int32_t *window,
+                             double *out_S, int32_t *out_mp_begin, int32_t *out_mp_idx,
+                             float *out_mp_pos, int64_t capacity, int64_t *cnt) {
+  if (n_batch < 0 || wbeg[0] != 0) return -1;
+  for (int32_t b = 0; b < n_batch; ++b)
+    if (wbeg[b + 1] <= wbeg[b] || window[wbeg[b]] != cur_kf[b]) return -1;
+  int32_t *owner = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_mp > 0 ? m->n_mp : 1));
+  /* pass 1: point counts */
+  out_mp_begin[0] = 0;
+  for (int32_t b = 0; b < n_batch; ++b) {
+    const int32_t n_w = wbeg[b + 1] - wbeg[b];
+    double *Sc = out_S + 13 * (size_t)wbeg[b];
+    window_sim3_owner(m, cur_kf[b], S_cw_corr + 13 * (size_t)b, n_w, window + wbeg[b], Sc, owner);
+    int32_t n = 0;
+    for (int32_t q = 0; q < m->n_mp; ++q) n += owner[q] >= 0;
+    out_mp_begin[b + 1] = out_mp_begin[b] + n;
+  }
+  if ((int64_t)out_mp_begin[n_batch] > capacity) { free(owner); return -2; }
+  /* pass 2: the corrected points */
+  for (int32_t b = 0; b < n_batch; ++b) {
+    const int32_t n_w = wbeg[b + 1] - wbeg[b];
+    const int32_t *win = window + wbeg[b];
+    const double *Sc = out_S + 13 * (size_t)wbeg[b];
+    window_sim3_owner(m, cur_kf[b], S_cw_corr + 13 * (size_t)b, n_w, win, out_S + 13 * (size_t)wbeg[b], owner);
+    int32_t o = out_mp_begin[b];
+    for (int32_t q = 0; q < m->n_mp; ++q) {
+      if (owner[q] < 0) continue;
+      const int32_t i = owner[q];
+      out_mp_idx[o] = q;
+      window_point(m, m->kf_pose + 13 * (size_t)win[i], Sc + 13 * i, q, out_mp_pos + 3 * (size_t)o);
+      ++o;
+      cnt[C_CORR_MP]++;
+    }
+    cnt[C_CORR_KF] += n_w;
+  }
+  free(owner);
   return 0;
 }
 
@@ -452,13 +522,101 @@ static void list_of(int32_t i, const int32_t *wb, const int32_t *mp_list, int32_
   else { *lst = mp_list; *n = n_list; }
 }
 
+/* O9.3 apply of a winner table (window-major, woff) and a victim table to the map:
+ * (i) every association of a victim -> its survivor (priority 2); (ii) ADDs on empty
+ * window slots (priority 1); (iii) per keyframe, a map point in > 1 slot keeps the
+ * least (priority, f); (iv) victims flagged bad with replaced_by; (v) n_obs recount. */
+static void apply_tables(orc_map *m, int32_t n_w, const int32_t *window, const int64_t *woff,
+                         const int64_t *io_winner, const int64_t *io_victim, int64_t *cnt) {
+  int32_t *win_pos = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_kf > 0 ? m->n_kf : 1));
+  for (int32_t k = 0; k < m->n_kf; ++k) win_pos[k] = -1;
+  for (int32_t i = 0; i < n_w; ++i) win_pos[window[i]] = i;
+  for (int32_t q = 0; q < m->n_mp; ++q) if (io_victim[q] != ORC_NONE) cnt[C_VICTIMS]++;
+  for (int32_t k = 0; k < m->n_kf; ++k) {
+    int32_t f0 = m->kf_feat_begin[k], nf = m->kf_feat_begin[k + 1] - f0;
+    int32_t *nv = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nf > 0 ? nf : 1));
+    int *prio = (int *)malloc(sizeof(int) * (size_t)(nf > 0 ? nf : 1));
+    for (int32_t f = 0; f < nf; ++f) {
+      int32_t s = m->feat_mp[f0 + f];
+      nv[f] = s; prio[f] = 0;
+      if (s >= 0 && io_victim[s] != ORC_NONE) {
+        nv[f] = (int32_t)(io_victim[s] & 0xffffffff); prio[f] = 2; cnt[C_REWIRED]++;
+      } else if (s < 0 && win_pos[k] >= 0 && io_winner[woff[win_pos[k]] + f] != ORC_NONE) {
+        nv[f] = (int32_t)(io_winner[woff[win_pos[k]] + f] & 0xffffffff); prio[f] = 1;
+      }
+    }
+    /* (iii) keep the least (priority, f) slot of every MP occupying > 1 slot (A22) */
+    uint8_t *clear = (uint8_t *)calloc((size_t)(nf > 0 ? nf : 1), 1);
+    for (int32_t f = 0; f < nf; ++f) {
+      if (nv[f] < 0) continue;
+      for (int32_t g = 0; g < nf; ++g)
+        if (g != f && nv[g] == nv[f] && (prio[g] < prio[f] || (prio[g] == prio[f] && g < f)))
+          clear[f] = 1;
+    }
+    for (int32_t f = 0; f < nf; ++f) {
+      if (clear[f]) { nv[f] = -1; cnt[C_DUP_CLEARED]++; }
+      else if (prio[f] == 1) cnt[C_ADDED]++;
+      m->feat_mp[f0 + f] = nv[f];
+    }
+    free(clear);
+    free(nv); free(prio);
+  }
+  for (int32_t q = 0; q < m->n_mp; ++q) {                             /* (iv) */
+    if (io_victim[q] == ORC_NONE) continue;
+    m->mp_flags[q] |= 1u;
+    m->mp_replaced_by[q] = (int32_t)(io_victim[q] & 0xffffffff);
+  }
+  for (int32_t q = 0; q < m->n_mp; ++q) m->mp_nobs[q] = 0;             /* (v) recount */
+  for (int32_t f = 0; f < m->n_feat; ++f)
+    if (m->feat_mp[f] >= 0) m->mp_nobs[m->feat_mp[f]]++;
+  free(win_pos);
+}
+
+/* O9.4 forced loop matches of the current keyframe (reading A23; EXT CorrectLoop fuses
+ * mvpLoopMatchedMPs -- the loop map points matched to the current keyframe's features
+ * during detection -- before SearchAndFuse). forced_mp [F(cur_kf)]: -1 or a map point
+ * for feature f. With the same rules as O9.1, against the slot's occupant m:
+ *   q bad or m == q -> nothing; m == -1 -> ADD(cur_kf, f, q); m bad -> nothing;
+ *   m in LoopSet -> nothing (loop-victim-skipped, keeps the result chain-free);
+ *   else m is a victim with survivor q (key (0, q): m sits in one slot of cur_kf).
+ * The tables are applied (O9.3) before the search, which sees the updated map. */
+static void forced_step(orc_map *m, int32_t cur_kf, const int32_t *forced_mp, int32_t n_w,
+                        const int32_t *window, const int64_t *woff, const uint8_t *loopset, int64_t *cnt) {
+  int32_t pos = -1;
+  for (int32_t i = 0; i < n_w; ++i) if (window[i] == cur_kf) pos = i;
+  int64_t *win = (int64_t *)malloc(sizeof(int64_t) * (size_t)(woff[n_w] > 0 ? woff[n_w] : 1));
+  int64_t *vic = (int64_t *)malloc(sizeof(int64_t) * (size_t)(m->n_mp > 0 ? m->n_mp : 1));
+  for (int64_t j = 0; j < woff[n_w]; ++j) win[j] = ORC_NONE;
+  for (int32_t q = 0; q < m->n_mp; ++q) vic[q] = ORC_NONE;
+  int32_t f0 = m->kf_feat_begin[cur_kf], nf = m->kf_feat_begin[cur_kf + 1] - f0;
+  for (int32_t f = 0; f < nf; ++f) {
+    int32_t q = forced_mp[f];
+    if (q < 0 || (m->mp_flags[q] & 1u)) continue;
+    int32_t slot = m->feat_mp[f0 + f];
+    if (slot == q) continue;
+    if (slot < 0) { win[woff[pos] + f] = (int64_t)q; cnt[C_FORCED]++; }
+    else if (m->mp_flags[slot] & 1u) continue;
+    else if (loopset[slot]) continue;
+    else { vic[slot] = (int64_t)q; cnt[C_FORCED]++; }
+  }
+  apply_tables(m, n_w, window, woff, win, vic, cnt);
+  free(win);
+  free(vic);
+}
+
 int orc_fuse(orc_map *m, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_w,
              const int32_t *window, const double *window_S, const int32_t *win_list_begin,
              const int32_t *mp_list, int32_t n_list, const orc_params *prm,
+             int32_t cur_kf, const int32_t *forced_mp,
              int64_t *io_winner, int64_t *io_victim, int8_t *out_action,
              int32_t *out_status, int64_t *out_best, double *out_uv, int32_t *out_ncand,
              uint8_t *out_edge, int64_t *cnt) {
   if (n_w <= 0 || w_lo < 0 || w_hi > n_w || w_lo > w_hi) return -1;
+  if (forced_mp) {
+    int in = 0;
+    for (int32_t i = 0; i < n_w; ++i) in |= window[i] == cur_kf;
+    if (!in) return -1;
+  }
   double scale[64];
   orc_scale_table(m->n_levels, m->scale_factor, scale);
   int64_t *woff = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_w + 1));
@@ -474,8 +632,6 @@ int orc_fuse(orc_map *m, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_w,
   }
 
   if (phase & 1) {
-    for (int64_t j = 0; j < woff[n_w]; ++j) io_winner[j] = ORC_NONE;
-    for (int32_t q = 0; q < m->n_mp; ++q) io_victim[q] = ORC_NONE;
     /* LoopSet = union of all window KFs' loop lists (A21) */
     uint8_t *loopset = (uint8_t *)calloc((size_t)(m->n_mp > 0 ? m->n_mp : 1), 1);
     for (int32_t i = 0; i < n_w; ++i) {
@@ -483,6 +639,9 @@ int orc_fuse(orc_map *m, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_w,
       list_of(i, win_list_begin, mp_list, n_list, &l, &n);
       for (int32_t j = 0; j < n; ++j) loopset[l[j]] = 1;
     }
+    if (forced_mp) forced_step(m, cur_kf, forced_mp, n_w, window, woff, loopset, cnt);   /* O9.4 */
+    for (int64_t j = 0; j < woff[n_w]; ++j) io_winner[j] = ORC_NONE;
+    for (int32_t q = 0; q < m->n_mp; ++q) io_victim[q] = ORC_NONE;
     for (int32_t i = w_lo; i < w_hi; ++i) {
       int32_t k = window[i];
       const double *S = window_S ? window_S + 13 * (size_t)i : m->kf_S_corr + 13 * (size_t)k;
@@ -497,6 +656,7 @@ int orc_fuse(orc_map *m, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_w,
         cnt[C_QUERIES]++;
         query_one(m, k, S, q, prm, NULL, 0, scale, &r);
         int64_t qi = qoff[i] + j;
+        if (r.edge) cnt[C_EDGE_AMB]++;
         if (out_status) out_status[qi] = r.status;
         if (out_uv) { out_uv[2 * qi] = r.u; out_uv[2 * qi + 1] = r.v; }
         if (out_ncand) out_ncand[qi] = r.ncand;
@@ -545,52 +705,265 @@ int orc_fuse(orc_map *m, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_w,
     free(loopset);
   }
 
-  if (phase & 2) {                                                      /* O9.3 apply */
-    int32_t *win_pos = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_kf > 0 ? m->n_kf : 1));
-    for (int32_t k = 0; k < m->n_kf; ++k) win_pos[k] = -1;
-    for (int32_t i = 0; i < n_w; ++i) win_pos[window[i]] = i;
-    for (int32_t q = 0; q < m->n_mp; ++q) if (io_victim[q] != ORC_NONE) cnt[C_VICTIMS]++;
-    for (int32_t k = 0; k < m->n_kf; ++k) {
-      int32_t f0 = m->kf_feat_begin[k], nf = m->kf_feat_begin[k + 1] - f0;
-      int32_t *nv = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nf > 0 ? nf : 1));
-      int *prio = (int *)malloc(sizeof(int) * (size_t)(nf > 0 ? nf : 1));
-      for (int32_t f = 0; f < nf; ++f) {
-        int32_t s = m->feat_mp[f0 + f];
-        nv[f] = s; prio[f] = 0;
-        if (s >= 0 && io_victim[s] != ORC_NONE) {
-          nv[f] = (int32_t)(io_victim[s] & 0xffffffff); prio[f] = 2; cnt[C_REWIRED]++;
-        } else if (s < 0 && win_pos[k] >= 0 && io_winner[woff[win_pos[k]] + f] != ORC_NONE) {
-          nv[f] = (int32_t)(io_winner[woff[win_pos[k]] + f] & 0xffffffff); prio[f] = 1;
-        }
-      }
-      /* (iii) keep the least (priority, f) slot of every MP occupying > 1 slot (A22) */
-      uint8_t *clear = (uint8_t *)calloc((size_t)(nf > 0 ? nf : 1), 1);
-      for (int32_t f = 0; f < nf; ++f) {
-        if (nv[f] < 0) continue;
-        for (int32_t g = 0; g < nf; ++g)
-          if (g != f && nv[g] == nv[f] && (prio[g] < prio[f] || (prio[g] == prio[f] && g < f)))
-            clear[f] = 1;
-      }
-      for (int32_t f = 0; f < nf; ++f) {
-        if (clear[f]) { nv[f] = -1; cnt[C_DUP_CLEARED]++; }
-        else if (prio[f] == 1) cnt[C_ADDED]++;
-        m->feat_mp[f0 + f] = nv[f];
-      }
-      free(clear);
-      free(nv); free(prio);
-    }
-    for (int32_t q = 0; q < m->n_mp; ++q) {                             /* (iv) */
-      if (io_victim[q] == ORC_NONE) continue;
-      m->mp_flags[q] |= 1u;
-      m->mp_replaced_by[q] = (int32_t)(io_victim[q] & 0xffffffff);
-    }
-    for (int32_t q = 0; q < m->n_mp; ++q) m->mp_nobs[q] = 0;             /* (v) recount */
-    for (int32_t f = 0; f < m->n_feat; ++f)
-      if (m->feat_mp[f] >= 0) m->mp_nobs[m->feat_mp[f]]++;
-    free(win_pos);
-  }
+  if (phase & 2) apply_tables(m, n_w, window, woff, io_winner, io_victim, cnt);   /* O9.3 */
   free(woff);
   free(qoff);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* TIMING ONLY: orc_fuse_plan_grid, the fuse PLAN (O4-O8 + the O9.1 victim        */
+/* proposals) with an ORB-SLAM-style cell grid (EXT GetFeaturesInArea) and the     */
+/* window keyframes spread over POSIX threads. It is the CPU baseline bench.py     */
+/* reports ("Grid mode is the timed baseline ... at T = all host  */
+/* cores"); it is NOT the parity definition (orc_fuse is) and tests check that its */
+/* tables and counters equal orc_fuse's. Cell ranges are supersets of the window   */
+/* (floor of monotone fp64 cell coordinates), the per-candidate test is O5's.      */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t cols, rows;
+  int32_t *cell_beg;   /* [n_kf][cols*rows + 1] offsets into cell_f (per keyframe, local) */
+  int32_t *cell_f;     /* [n_feat] keyframe-local feature indices, by (cell, f) */
+} orc_grid;
+
+static int grid_cell(double x, double lo, double hi, int32_t n) {
+  int c = (int)floor((x - lo) * ((double)n / (hi - lo)));
+  return c < 0 ? 0 : (c >= n ? n - 1 : c);
+}
+
+orc_grid *orc_grid_build(const orc_map *m, int32_t cols, int32_t rows) {
+  orc_grid *g = (orc_grid *)calloc(1, sizeof(orc_grid));
+  const int32_t G = cols * rows;
+  g->cols = cols; g->rows = rows;
+  g->cell_beg = (int32_t *)malloc(sizeof(int32_t) * ((size_t)m->n_kf * (G + 1) + 1));
+  g->cell_f = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_feat > 0 ? m->n_feat : 1));
+  int32_t *cell = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m->n_feat > 0 ? m->n_feat : 1));
+  for (int32_t k = 0; k < m->n_kf; ++k) {
+    const orc_camera *cam = &m->cams[m->kf_cam[k]];
+    int32_t f0 = m->kf_feat_begin[k], nf = m->kf_feat_begin[k + 1] - f0;
+    int32_t *beg = g->cell_beg + (size_t)k * (G + 1);
+    for (int c = 0; c <= G; ++c) beg[c] = 0;
+    for (int32_t f = 0; f < nf; ++f) {
+      int cx = grid_cell((double)m->feat_uv[2 * (f0 + f)], cam->min_x, cam->max_x, cols);
+      int cy = grid_cell((double)m->feat_uv[2 * (f0 + f) + 1], cam->min_y, cam->max_y, rows);
+      cell[f0 + f] = cy * cols + cx;
+      beg[cell[f0 + f] + 1]++;
+    }
+    for (int c = 0; c < G; ++c) beg[c + 1] += beg[c];
+    int32_t *cur = (int32_t *)malloc(sizeof(int32_t) * (size_t)(G + 1));
+    memcpy(cur, beg, sizeof(int32_t) * (size_t)(G + 1));
+    for (int32_t f = 0; f < nf; ++f) g->cell_f[f0 + cur[cell[f0 + f]]++] = f;
+    free(cur);
+  }
+  free(cell);
+  return g;
+}
+
+void orc_grid_free(orc_grid *g) {
+  if (!g) return;
+  free(g->cell_beg);
+  free(g->cell_f);
+  free(g);
+}
+
+typedef struct { int32_t m; int64_t key; } orc_vprop;
+
+typedef struct {
+  orc_map *m;
+  const orc_grid *g;
+  int32_t n_w;
+  const int32_t *window;
+  const double *window_S;
+  const int32_t *win_list_begin, *mp_list;
+  int32_t n_list;
+  const orc_params *prm;
+  const int64_t *woff;
+  const uint8_t *loopset;
+  int64_t *io_winner;
+  const double *scale;
+  int32_t next;                 /* next window position (shared work counter) */
+  pthread_mutex_t mu;
+} grid_job;
+
+typedef struct {
+  grid_job *job;
+  int64_t cnt[C_N];
+  orc_vprop *vp;
+  int64_t nvp, cap;
+} grid_worker;
+
+static int cmp_i32(const void *a, const void *b) {
+  int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+  return (x > y) - (x < y);
+}
+
+static void grid_query(const orc_map *m, const orc_grid *g, int32_t k, const double *T, const double *Ow,
+                       const int32_t *held, int32_t n_held, int32_t q, const orc_params *prm,
+                       const double *scale, orc_qres *r) {
+  memset(r, 0, sizeof(*r));
+  r->best_f = -1; r->best_h = 256; r->second_h = 256; r->level = -1;
+  if (m->mp_flags[q] & 1u) { r->status = Q_BAD; return; }
+  if (n_held && bsearch(&q, held, (size_t)n_held, sizeof(int32_t), cmp_i32)) { r->status = Q_FOUND; return; }
+  double p[3], pc[3];
+  for (int i = 0; i < 3; ++i) p[i] = (double)m->mp_pos[3 * q + i];
+  for (int i = 0; i < 3; ++i) pc[i] = row3(T + 3 * i, p) + T[9 + i];
+  if (pc[2] <= 0.0) { r->status = Q_DEPTH; return; }
+  const orc_camera *cam = &m->cams[m->kf_cam[k]];
+  double uv[2];
+  orc_project(cam, pc, uv);
+  if (!(uv[0] >= cam->min_x && uv[0] < cam->max_x && uv[1] >= cam->min_y && uv[1] < cam->max_y)) {
+    r->status = Q_BOUNDS; return;
+  }
+  double PO[3];
+  for (int i = 0; i < 3; ++i) PO[i] = p[i] - Ow[i];
+  double d = sqrt((PO[0] * PO[0] + PO[1] * PO[1]) + PO[2] * PO[2]);
+  double dmax = (double)m->mp_max_dist[q];
+  if (d < 0.8 * (dmax / scale[m->n_levels - 1]) || d > 1.2 * dmax) { r->status = Q_DIST; return; }
+  double n[3];
+  for (int i = 0; i < 3; ++i) n[i] = (double)m->mp_normal[3 * q + i];
+  if (row3(PO, n) < 0.5 * d) { r->status = Q_ANGLE; return; }
+  int lvl = orc_predict_level(d, dmax, scale, m->n_levels);
+  double rad = (double)prm->th * scale[lvl];
+  int32_t f0 = m->kf_feat_begin[k];
+  const uint8_t *dq = m->mp_desc + 32 * (size_t)q;
+  const int32_t G = g->cols * g->rows;
+  const int32_t *beg = g->cell_beg + (size_t)k * (G + 1);
+  int cx0 = grid_cell(uv[0] - rad, cam->min_x, cam->max_x, g->cols);
+  int cx1 = grid_cell(uv[0] + rad, cam->min_x, cam->max_x, g->cols);
+  int cy0 = grid_cell(uv[1] - rad, cam->min_y, cam->max_y, g->rows);
+  int cy1 = grid_cell(uv[1] + rad, cam->min_y, cam->max_y, g->rows);
+  for (int cy = cy0; cy <= cy1; ++cy)
+    for (int cx = cx0; cx <= cx1; ++cx)
+      for (int32_t j = beg[cy * g->cols + cx]; j < beg[cy * g->cols + cx + 1]; ++j) {
+        int32_t f = g->cell_f[f0 + j];
+        int oct = m->feat_octave[f0 + f];
+        if (oct < lvl - 1 || oct > lvl) continue;
+        double du = fabs((double)m->feat_uv[2 * (f0 + f)] - uv[0]);
+        double dv = fabs((double)m->feat_uv[2 * (f0 + f) + 1] - uv[1]);
+        if (!(du < rad && dv < rad)) continue;
+        r->ncand++;
+        int h = orc_hamming(dq, m->feat_desc + 32 * (size_t)(f0 + f));
+        if (h < r->best_h || (h == r->best_h && f < r->best_f)) {
+          if (r->best_f >= 0 && r->best_h < r->second_h) r->second_h = r->best_h;
+          r->best_h = h; r->best_f = f;
+        } else if (h < r->second_h) {
+          r->second_h = h;
+        }
+      }
+  r->status = Q_MATCHED_STAGE;
+}
+
+static void *grid_worker_main(void *arg) {
+  grid_worker *wk = (grid_worker *)arg;
+  grid_job *jb = wk->job;
+  orc_map *m = jb->m;
+  int32_t *held = NULL;
+  int32_t held_cap = 0;
+  for (;;) {
+    pthread_mutex_lock(&jb->mu);
+    int32_t i = jb->next++;
+    pthread_mutex_unlock(&jb->mu);
+    if (i >= jb->n_w) break;
+    int32_t k = jb->window[i];
+    const double *S = jb->window_S ? jb->window_S + 13 * (size_t)i : m->kf_S_corr + 13 * (size_t)k;
+    double T[13], Ow[3];
+    orc_sim3_se3(S, T);
+    for (int j = 0; j < 3; ++j) Ow[j] = -col3(T, j, T + 9);
+    int32_t f0 = m->kf_feat_begin[k], nf = m->kf_feat_begin[k + 1] - f0;
+    if (nf > held_cap) { held_cap = nf; held = (int32_t *)realloc(held, sizeof(int32_t) * (size_t)held_cap); }
+    int32_t n_held = 0;
+    for (int32_t f = 0; f < nf; ++f) if (m->feat_mp[f0 + f] >= 0) held[n_held++] = m->feat_mp[f0 + f];
+    qsort(held, (size_t)n_held, sizeof(int32_t), cmp_i32);
+    int64_t *win = jb->io_winner + jb->woff[i];
+    const int32_t *l; int32_t n;
+    list_of(i, jb->win_list_begin, jb->mp_list, jb->n_list, &l, &n);
+    int64_t *cnt = wk->cnt;
+    for (int32_t j = 0; j < n; ++j) {
+      int32_t q = l[j];
+      orc_qres r;
+      cnt[C_QUERIES]++;
+      grid_query(m, jb->g, k, T, Ow, held, n_held, q, jb->prm, jb->scale, &r);
+      switch (r.status) {
+        case Q_BAD: cnt[C_SKIP_BAD]++; continue;
+        case Q_FOUND: cnt[C_SKIP_FOUND]++; continue;
+        case Q_DEPTH: cnt[C_CULL_DEPTH]++; continue;
+        case Q_BOUNDS: cnt[C_CULL_BOUNDS]++; continue;
+        case Q_DIST: cnt[C_CULL_DIST]++; continue;
+        case Q_ANGLE: cnt[C_CULL_ANGLE]++; continue;
+        default: break;
+      }
+      cnt[C_CANDIDATES] += r.ncand;
+      if (!proposal_ok(&r, jb->prm, cnt)) continue;
+      int64_t key = ((int64_t)r.best_h << 32) | (int64_t)q;
+      if (key < win[r.best_f]) win[r.best_f] = key;
+    }
+    for (int32_t f = 0; f < nf; ++f) if (win[f] != ORC_NONE) cnt[C_WINNERS]++;
+    if (jb->prm->check_orientation) orientation_filter(m, k, win, nf, cnt);
+    for (int32_t f = 0; f < nf; ++f) {
+      if (win[f] == ORC_NONE) continue;
+      int32_t slot = m->feat_mp[f0 + f];
+      if (slot < 0) cnt[C_ADD]++;
+      else if (m->mp_flags[slot] & 1u) cnt[C_BAD_SLOT]++;
+      else if (jb->loopset[slot]) cnt[C_LOOP_SKIP]++;
+      else {
+        cnt[C_VICTIM_PROP]++;
+        if (wk->nvp == wk->cap) {
+          wk->cap = wk->cap ? 2 * wk->cap : 1024;
+          wk->vp = (orc_vprop *)realloc(wk->vp, sizeof(orc_vprop) * (size_t)wk->cap);
+        }
+        wk->vp[wk->nvp].m = slot;
+        wk->vp[wk->nvp].key = win[f];
+        wk->nvp++;
+      }
+    }
+  }
+  free(held);
+  return NULL;
+}
+
+/* PLAN over the whole window with n_threads threads; io_winner / io_victim / cnt as
+ * orc_fuse(phase = PLAN) (no forced matches, no debug outputs). */
+int orc_fuse_plan_grid(orc_map *m, const orc_grid *g, int32_t n_threads, int32_t n_w,
+                       const int32_t *window, const double *window_S, const int32_t *win_list_begin,
+                       const int32_t *mp_list, int32_t n_list, const orc_params *prm,
+                       int64_t *io_winner, int64_t *io_victim, int64_t *cnt) {
+  if (n_w <= 0 || n_threads < 1 || !g) return -1;
+  double scale[64];
+  orc_scale_table(m->n_levels, m->scale_factor, scale);
+  int64_t *woff = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n_w + 1));
+  woff[0] = 0;
+  for (int32_t i = 0; i < n_w; ++i)
+    woff[i + 1] = woff[i] + (m->kf_feat_begin[window[i] + 1] - m->kf_feat_begin[window[i]]);
+  uint8_t *loopset = (uint8_t *)calloc((size_t)(m->n_mp > 0 ? m->n_mp : 1), 1);
+  for (int32_t i = 0; i < n_w; ++i) {
+    const int32_t *l; int32_t n;
+    list_of(i, win_list_begin, mp_list, n_list, &l, &n);
+    for (int32_t j = 0; j < n; ++j) loopset[l[j]] = 1;
+  }
+  for (int64_t j = 0; j < woff[n_w]; ++j) io_winner[j] = ORC_NONE;
+  for (int32_t q = 0; q < m->n_mp; ++q) io_victim[q] = ORC_NONE;
+  grid_job jb;
+  memset(&jb, 0, sizeof(jb));
+  jb.m = m; jb.g = g; jb.n_w = n_w; jb.window = window; jb.window_S = window_S;
+  jb.win_list_begin = win_list_begin; jb.mp_list = mp_list; jb.n_list = n_list; jb.prm = prm;
+  jb.woff = woff; jb.loopset = loopset; jb.io_winner = io_winner; jb.scale = scale; jb.next = 0;
+  pthread_mutex_init(&jb.mu, NULL);
+  grid_worker *wk = (grid_worker *)calloc((size_t)n_threads, sizeof(grid_worker));
+  pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)n_threads);
+  for (int32_t t = 0; t < n_threads; ++t) {
+    wk[t].job = &jb;
+    if (t > 0) pthread_create(&th[t], NULL, grid_worker_main, &wk[t]);
+  }
+  grid_worker_main(&wk[0]);
+  for (int32_t t = 1; t < n_threads; ++t) pthread_join(th[t], NULL);
+  for (int32_t t = 0; t < n_threads; ++t) {
+    for (int c = 0; c < C_N; ++c) cnt[c] += wk[t].cnt[c];
+    for (int64_t j = 0; j < wk[t].nvp; ++j)
+      if (wk[t].vp[j].key < io_victim[wk[t].vp[j].m]) io_victim[wk[t].vp[j].m] = wk[t].vp[j].key;
+    free(wk[t].vp);
+  }
+  pthread_mutex_destroy(&jb.mu);
+  free(wk); free(th); free(loopset); free(woff);
   return 0;
 }
 
@@ -624,6 +997,7 @@ int orc_search_by_projection(const orc_map *m, int32_t n_pairs, const int32_t *p
       if (out_uv) { out_uv[2 * j] = r.u; out_uv[2 * j + 1] = r.v; }
       if (out_ncand) out_ncand[j] = r.ncand;
       if (out_edge) out_edge[j] = (uint8_t)r.edge;
+      if (r.edge) c[C_EDGE_AMB]++;
       if (out_best) out_best[j] = r.status < 0 ? (int64_t)r.status
           : (((int64_t)r.best_h << 48) | ((int64_t)r.second_h << 32) | (uint32_t)r.best_f);
       switch (r.status) {
