@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define LC_ABI_VERSION 1
+#define LC_ABI_VERSION 2
 #define LC_NONE INT64_MAX
 #define LC_MAX_FEAT_PER_KF 8192
 #define LC_MAX_LEVELS 16
@@ -199,12 +199,17 @@ enum {
   LC_COUNT_PGO_SOLVER_ITERS, /* pose graph: conjugate-gradient iterations, all solves */
   LC_COUNT_PGO_STOP,       /* pose graph: stop reason (LC_PGO_STOP_*)                 */
   LC_COUNT_PGO_BAND,       /* pose graph: 1 + block bandwidth of the banded solve, 0 = CG */
+  LC_COUNT_FORCED,         /* fuse: forced loop matches turned into an ADD or a victim (O9.4) */
+  LC_COUNT_EDGE_AMB,       /* queries whose bounds or window decision lies within 1e-4 px of
+                              the edge (SURVEY.md §8(c) "Edge-ambiguous"): the only queries
+                              where a differently-rounded projection may decide otherwise */
   LC_NCOUNT
 };
 
 /* lc_correct_sim3 modes */
 #define LC_CORRECT_WINDOW 1
 #define LC_CORRECT_ALL 2
+#define LC_DRY_RUN 4          /* with LC_CORRECT_WINDOW: a batch of corrections, nothing written back */
 /* lc_fuse phases */
 #define LC_FUSE_PLAN 1
 #define LC_FUSE_APPLY 2
@@ -402,30 +407,47 @@ lc_status lc_state_restore(lc_ctx* ctx, void* cuda_stream);
 /* ---------------------------------------------------------------------------
  * lc_correct_sim3 -- Sim3 pose correction (§III.B).
  *
- * mode LC_CORRECT_WINDOW (reading O3; old poses read before any write-back):
- *   for window position i (window_kf[0] must be cur_kf):
+ * mode LC_CORRECT_WINDOW (reading O3; old poses read before any write-back),
+ *   n_batch = 1, window = window_kf[window_begin[0] .. window_begin[1]):
+ *   for window position i (window[0] must be cur_kf[0]):
  *     S_i^corr = (T_iw * inverse(T_cw)) * S_cw_corr   (S_c^corr = S_cw_corr);
  *   every non-bad map point observed by the window is re-anchored through its
  *   owner o = the first window keyframe (list order) observing it:
  *     p <- fl32( inverse(S_o^corr)( T_ow(p) ) );
  *   then T_iw <- SE3(S_i^corr) = (R, t/s). S_i^corr is kept (loop state) as the
  *   default projection transform of lc_fuse and as S^pre of LC_CORRECT_ALL.
- *   cur_kf, S_cw_corr [host]; n_window >= 1 distinct keyframes window_kf [host].
- *   out_S_corr [host|dev] nullable, [n_window].
+ *   out_S_corr [host|dev] nullable, [n_window]. out_mp_* ignored.
+ * mode LC_CORRECT_WINDOW | LC_DRY_RUN (reading O3', PAPER.md:200
+ *   §IV.C: loop candidates are evaluated in batches): n_batch >= 1 hypotheses
+ *   b = (cur_kf[b], S_cw_corr[b], window_kf[window_begin[b] .. window_begin[b+1]),
+ *   window_kf[window_begin[b]] == cur_kf[b]); each gets the WINDOW arithmetic above
+ *   against the map as it is, and NOTHING is written back (no pose, point or loop
+ *   state changes; hypotheses are independent):
+ *     out_S_corr [host|dev] required, [window_begin[n_batch]]: S_i^corr per slot;
+ *     out_mp_begin [host|dev] required, [n_batch + 1]: CSR of the corrected points;
+ *     out_mp_idx [out_capacity] / out_mp_pos [out_capacity][3] [host|dev]: the owned
+ *       non-bad map points of hypothesis b in ascending index, fl32 positions.
+ *   The call reads the point total back (one stream synchronisation) and returns
+ *   LC_ECAPACITY when it exceeds out_capacity (out_mp_begin is complete, points
+ *   beyond the capacity are not written). Not capturable into a graph.
  * mode LC_CORRECT_ALL (reading O10; propagation after pose-graph optimisation):
  *   S_k^pre = S_k^corr if k was in the last window, else T_kw;
  *   every non-bad map point p <- fl32( inverse(S_r^opt)( S_r^pre(p) ) ) with
  *   r = its window owner if corrected by the last WINDOW call, else mp_ref_kf;
  *   then T_kw <- SE3(S_k^opt) for every k. Consumes the loop state.
- *   S_opt [host|dev] [n_kf]. cur_kf / S_cw_corr / window ignored.
+ *   S_opt [host|dev] [n_kf]. Every other argument ignored (may be NULL).
+ * cur_kf, S_cw_corr, window_begin, window_kf [host] (WINDOW modes).
  * All transforms are evaluated in fp64 in the order of DESIGN.md "Sim3
  * arithmetic"; positions are stored fp32 (round to nearest).
  * out_counts [host|dev] nullable, [LC_NCOUNT] (CORR_KF, CORR_MP).
- * Errors: LC_ESTATE (no map), LC_EINVAL (bad mode, n_window < 1, window_kf[0]
- * != cur_kf, duplicate window keyframes, null S), LC_ERANGE (keyframe index). */
-lc_status lc_correct_sim3(lc_ctx* ctx, int32_t mode, int32_t cur_kf, const lc_sim3* S_cw_corr,
-                          int32_t n_window, const int32_t* window_kf, const lc_sim3* S_opt,
-                          lc_sim3* out_S_corr, int64_t* out_counts, void* cuda_stream);
+ * Errors: LC_ESTATE (no map), LC_EINVAL (bad mode, n_batch != 1 without DRY_RUN,
+ * an empty window, window[0] != cur_kf, duplicate keyframes in a window, null
+ * required pointer), LC_ERANGE (keyframe index), LC_ECAPACITY (DRY_RUN). */
+lc_status lc_correct_sim3(lc_ctx* ctx, int32_t mode, int32_t n_batch, const int32_t* cur_kf,
+                          const lc_sim3* S_cw_corr, const int32_t* window_begin,
+                          const int32_t* window_kf, const lc_sim3* S_opt, lc_sim3* out_S_corr,
+                          int32_t* out_mp_begin, int32_t* out_mp_idx, float* out_mp_pos,
+                          int64_t out_capacity, int64_t* out_counts, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * lc_fuse -- loop fusion (§IV.D.3), readings O4-O9.
@@ -450,9 +472,20 @@ lc_status lc_correct_sim3(lc_ctx* ctx, int32_t mode, int32_t cur_kf, const lc_si
  * least (priority, f) slot, priority 0 unchanged / 1 ADD / 2 redirected; victims
  * get flags |= bad and replaced_by = survivor; n_obs is updated.
  *
- * phase LC_FUSE_PLAN  : steps up to the victim words, for window positions
- *                       [w_lo, w_hi) only (a keyframe shard); initialises all of
- *                       io_winner and io_victim to LC_NONE first. Map unchanged.
+ * Forced loop matches (reading O9.4 / A23; EXT CorrectLoop fuses the loop map
+ * points matched to the current keyframe during detection before the search):
+ * forced_mp [host|dev] nullable, [F(cur_kf)], cur_kf a window keyframe. For each
+ * feature f with q = forced_mp[f] >= 0, q not bad, against the slot's occupant m:
+ * m == q or m bad or m in LoopSet -> nothing; m == -1 -> ADD; else m is a victim
+ * with survivor q. These tables are applied (as APPLY below) at the start of PLAN,
+ * so the search sees the updated map. Re-running them on an already forced map
+ * changes nothing (every shard's PLAN may carry them).
+ *
+ * phase LC_FUSE_PLAN  : [forced matches, then] steps up to the victim words, for
+ *                       window positions [w_lo, w_hi) only (a keyframe shard);
+ *                       every word of io_winner outside the shard and every word
+ *                       of io_victim is LC_NONE or a proposal of this call
+ *                       afterwards. Map unchanged (except the forced matches).
  * phase LC_FUSE_APPLY : apply from io_winner / io_victim (e.g. after an NCCL MIN
  *                       all-reduce of the shards' tables). w_lo / w_hi ignored.
  * phase LC_FUSE_ALL   : PLAN over the whole window, then APPLY.
@@ -476,7 +509,8 @@ lc_status lc_correct_sim3(lc_ctx* ctx, int32_t mode, int32_t cur_kf, const lc_si
 lc_status lc_fuse(lc_ctx* ctx, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_window,
                   const int32_t* window_kf, const lc_sim3* window_S,
                   const int32_t* win_list_begin, const int32_t* mp_list, int64_t n_list,
-                  const lc_match_params* params, int64_t* io_winner, int64_t* io_victim,
+                  const lc_match_params* params, int32_t cur_kf, const int32_t* forced_mp,
+                  int64_t* io_winner, int64_t* io_victim,
                   int8_t* out_action, const lc_query_debug* dbg, int64_t* out_counts,
                   void* cuda_stream);
 

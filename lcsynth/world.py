@@ -218,6 +218,10 @@ class World:
     pair_list_begin: Optional[np.ndarray] = None
     pair_mp_list: Optional[np.ndarray] = None
     pair_taken: Optional[np.ndarray] = None      # (sum F(pair_kf),) i32, -1 free
+    hyp_cur: Optional[np.ndarray] = None         # C4: per hypothesis, its current keyframe
+    hyp_S_cw: Optional[np.ndarray] = None        # (H, 13) its loop Sim3
+    hyp_win_begin: Optional[np.ndarray] = None   # (H+1,) CSR into hyp_window
+    hyp_window: Optional[np.ndarray] = None      # its window (current first) = its pairs' keyframes
 
     @property
     def n_kf(self):
@@ -582,21 +586,31 @@ def _kf_mps(w: World, kfs):
 def _make_hypotheses(w: World, rng, covis, kf_est, ideal, K):
     H = w.cfg.n_hyp
     pair_kf, pair_S, pair_param, lists, begin = [], [], [], [], [0]
+    hyp_cur, hyp_S, pair_hyp = [], [], []
     for h in range(H):
         j = int(round((h + 0.5) * K / H)) % K
         cur = K + j
         S_cw = _compose(_noise(rng, 1e-3), ideal[cur])
+        hyp_cur.append(cur)
+        hyp_S.append(_to13(S_cw))
         loop_kfs = [j] + _top_covisible(covis, j, w.cfg.loop_covis, lambda x: x < K)
         lst = _kf_mps(w, loop_kfs)
         for kk in [cur] + _top_covisible(covis, cur, 3, lambda x: x >= K):
             S_ic = _compose(kf_est[kk], _inverse(kf_est[cur]))
             pair_kf.append(kk)
+            pair_hyp.append(h)
             pair_S.append(_to13(_compose(S_ic, S_cw)))
             pair_param.append(h % 3)
             lists.append(lst)
             begin.append(begin[-1] + len(lst))
     w.pair_kf = np.asarray(pair_kf, np.int32)
     w.pair_S = np.stack(pair_S)
+    # the hypotheses' own window corrections (SURVEY §8(d) C4 "32 lc_correct_sim3 dry runs"):
+    # hypothesis h = (current KF, S_cw, window = its 4 pairs' keyframes, current first)
+    w.hyp_cur = np.asarray(hyp_cur, np.int32)
+    w.hyp_S_cw = np.stack(hyp_S)
+    w.hyp_window = w.pair_kf.copy()
+    w.hyp_win_begin = np.searchsorted(np.asarray(pair_hyp), np.arange(H + 1)).astype(np.int32)
     w.pair_param = np.asarray(pair_param, np.int32)
     w.pair_list_begin = np.asarray(begin, np.int32)
     w.pair_mp_list = np.concatenate(lists).astype(np.int32)

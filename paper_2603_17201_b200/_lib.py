@@ -15,7 +15,7 @@ LC_OK, LC_EINVAL, LC_ESTATE, LC_ECUDA, LC_ENOMEM, LC_ERANGE, LC_ECAPACITY = 0, -
 STATUS_NAMES = {0: "LC_OK", -1: "LC_EINVAL", -2: "LC_ESTATE", -3: "LC_ECUDA", -4: "LC_ENOMEM",
                 -5: "LC_ERANGE", -6: "LC_ECAPACITY"}
 LC_NONE = (1 << 63) - 1
-LC_CORRECT_WINDOW, LC_CORRECT_ALL = 1, 2
+LC_CORRECT_WINDOW, LC_CORRECT_ALL, LC_DRY_RUN = 1, 2, 4
 LC_FUSE_PLAN, LC_FUSE_APPLY, LC_FUSE_ALL = 1, 2, 3
 LC_REFRESH_DESC, LC_REFRESH_NORMAL = 1, 2
 COUNTER_NAMES = [
@@ -25,7 +25,7 @@ COUNTER_NAMES = [
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
     "refresh_mp", "refresh_obs", "conn_kf", "conn_edges", "ransac_hyp", "ransac_inliers",
     "refine_iters", "refine_inliers", "pgo_iters", "pgo_accepted", "pgo_solver_iters", "pgo_stop",
-    "pgo_band",
+    "pgo_band", "forced", "edge_amb",
 ]
 LC_NCOUNT = len(COUNTER_NAMES)
 PROF_NAMES = ["upload", "correct_window", "correct_all", "fuse_prep", "match", "resolve", "apply",
@@ -108,8 +108,8 @@ def load():
         "lc_download_map": (i32, [vp, P(lc_map_state), vp]),
         "lc_state_save": (i32, [vp, vp]),
         "lc_state_restore": (i32, [vp, vp]),
-        "lc_correct_sim3": (i32, [vp, i32, i32, vp, i32, vp, vp, vp, vp, vp]),
-        "lc_fuse": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, vp, i64, P(lc_match_params), vp,
+        "lc_correct_sim3": (i32, [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp]),
+        "lc_fuse": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, vp, i64, P(lc_match_params), i32, vp, vp,
                           vp, vp, vp, vp, vp]),
         "lc_search_by_projection": (i32, [vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp,
                                           vp, vp]),

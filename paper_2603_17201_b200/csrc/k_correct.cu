@@ -262,6 +262,157 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_all_points(
   warp_count(n, &counts[LC_COUNT_CORR_MP]);
 }
 
+// ---------------------------------------------------------------------------
+// WINDOW | DRY_RUN over a batch of hypotheses (oracle O3'): the
+// same S^corr / owner / re-anchoring arithmetic as the WINDOW kernels above, per batch
+// b (its window = slots [wbeg[b], wbeg[b+1]) of the concatenated window list), with
+// nothing written back: S^corr rows and the corrected positions of the owned points
+// (ascending map-point index, CSR by batch) go to the caller's buffers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int batch_of(const int32_t* __restrict__ wbeg, int n_batch, int j) {
+  int lo = 0, hi = n_batch - 1;   // last b with wbeg[b] <= j
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (wbeg[mid] <= j) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// thread per window slot j: S_j^corr = (T_jw * inverse(T_cw)) * S_cw^corr[b] (cur first)
+__global__ void k_dry_sim3(int n_slots, int n_batch, const int32_t* __restrict__ wbeg,
+                           const int32_t* __restrict__ window, const double* __restrict__ kf_pose,
+                           const double* __restrict__ Scw, double* __restrict__ scr, double* __restrict__ out_S,
+                           unsigned long long* __restrict__ counts) {
+  if (blockIdx.x == 0 && threadIdx.x < LC_NCOUNT)   // the call's counters
+    counts[threadIdx.x] = threadIdx.x == LC_COUNT_CORR_KF ? (unsigned long long)n_slots : 0ull;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_slots) return;
+  const int b = batch_of(wbeg, n_batch, j);
+  const int k = window[j];
+  double T[13], S[13], Si[13];
+  for (int i = 0; i < 13; ++i) T[i] = kf_pose[13 * (size_t)k + i];
+  if (j == wbeg[b]) {
+    for (int i = 0; i < 13; ++i) S[i] = Scw[13 * (size_t)b + i];
+  } else {
+    double Tc[13], Tci[13], Sic[13];
+    const int c = window[wbeg[b]];
+    for (int i = 0; i < 13; ++i) Tc[i] = kf_pose[13 * (size_t)c + i];
+    lc_sim3_inverse(Tc, Tci);
+    lc_sim3_compose(T, Tci, Sic);
+    lc_sim3_compose(Sic, Scw + 13 * (size_t)b, S);
+  }
+  lc_sim3_inverse(S, Si);
+  double* o = scr + (size_t)WSTR * j;
+  for (int i = 0; i < 13; ++i) { o[i] = T[i]; o[14 + i] = Si[i]; o[28 + i] = S[i]; }
+  o[13] = o[27] = o[41] = 0.0;
+  if (out_S)
+    for (int i = 0; i < 13; ++i) out_S[13 * (size_t)j + i] = S[i];
+}
+
+// warp per window slot j: owner[b][m] = min local position observing m
+__global__ void __launch_bounds__(LC_NTHREADS) k_dry_mark(
+    int n_slots, int n_batch, int n_mp, const int32_t* __restrict__ wbeg, const int32_t* __restrict__ window,
+    const int32_t* __restrict__ kf_fbeg, const int32_t* __restrict__ feat_mp, int32_t* owner) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int j = gw; j < n_slots; j += nw) {
+    const int b = batch_of(wbeg, n_batch, j);
+    const int i = j - wbeg[b];
+    int32_t* ob = owner + (size_t)b * n_mp;
+    const int k = window[j];
+    for (int f = kf_fbeg[k] + lane; f < kf_fbeg[k + 1]; f += 32) {
+      const int m = feat_mp[f];
+      if (m >= 0) atomicMin(&ob[m], i);
+    }
+  }
+}
+
+// (b, q) grid, one point per thread: per-block count of owned non-bad points
+__global__ void __launch_bounds__(LC_NTHREADS) k_dry_count(int n_mp, int nblk, const int32_t* __restrict__ owner,
+                                                           const uint8_t* __restrict__ flags, int32_t* __restrict__ bcnt) {
+  const int b = blockIdx.y;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool own = q < n_mp && owner[(size_t)b * n_mp + q] != OWNER_NONE && !(flags[q] & 1u);
+  const int n = __syncthreads_count(own);
+  if (threadIdx.x == 0) bcnt[(size_t)b * nblk + blockIdx.x] = n;
+}
+
+// one CTA: exclusive scan of the block counts (batch-major) -> block offsets, CSR begin
+__global__ void __launch_bounds__(1024) k_dry_scan(int n_batch, int nblk, int32_t* __restrict__ bcnt,
+                                                   int32_t* __restrict__ mp_begin) {
+  __shared__ int32_t s_w[32];
+  __shared__ int32_t s_carry;
+  const int n = n_batch * nblk;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int v = i < n ? bcnt[i] : 0;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) s_w[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int w = threadIdx.x < (int)(blockDim.x >> 5) ? s_w[threadIdx.x] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (threadIdx.x >= o) w += y;
+      }
+      s_w[threadIdx.x] = w;
+    }
+    __syncthreads();
+    const int excl = s_carry + (threadIdx.x >= 32 ? s_w[(threadIdx.x >> 5) - 1] : 0) + x - v;
+    if (i < n) {
+      bcnt[i] = excl;
+      if (i % nblk == 0) mp_begin[i / nblk] = excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) mp_begin[n_batch] = s_carry;
+}
+
+// (b, q) grid: owned point -> (idx, fl32(inverse(S_o^corr)(T_ow^old(p)))) at its CSR slot
+__global__ void __launch_bounds__(LC_NTHREADS) k_dry_points(
+    int n_mp, int nblk, long long capacity, const int32_t* __restrict__ wbeg, const int32_t* __restrict__ owner,
+    const uint8_t* __restrict__ flags, const int32_t* __restrict__ boff, const double* __restrict__ scr,
+    const MpRec* __restrict__ rec, int32_t* __restrict__ out_idx, float* __restrict__ out_pos,
+    unsigned long long* __restrict__ counts) {
+  __shared__ int32_t s_w[LC_NTHREADS / 32];
+  const int b = blockIdx.y;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int o = q < n_mp ? owner[(size_t)b * n_mp + q] : OWNER_NONE;
+  const bool own = o != OWNER_NONE && !(flags[q] & 1u);
+  const unsigned m = __ballot_sync(0xffffffffu, own);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) s_w[warp] = __popc(m);
+  __syncthreads();
+  int before = 0;
+  for (int w = 0; w < warp; ++w) before += s_w[w];
+  if (own) {
+    const long long slot = (long long)boff[(size_t)b * nblk + blockIdx.x] + before + __popc(m & ((1u << lane) - 1u));
+    if (slot < capacity) {
+      const double* S = scr + (size_t)WSTR * (wbeg[b] + o);
+      double T[13], Si[13];
+      load13(S, T);
+      load13(S + 14, Si);
+      double p[3] = {rec[q].pos[0], rec[q].pos[1], rec[q].pos[2]}, pc[3], pw[3];
+      lc_sim3_apply(T, p, pc);
+      lc_sim3_apply(Si, pc, pw);
+      out_idx[slot] = q;
+      out_pos[3 * slot + 0] = __double2float_rn(pw[0]);
+      out_pos[3 * slot + 1] = __double2float_rn(pw[1]);
+      out_pos[3 * slot + 2] = __double2float_rn(pw[2]);
+    }
+  }
+  warp_count(own ? 1u : 0u, &counts[LC_COUNT_CORR_MP]);
+}
+
 }  // namespace
 
 int correct_window_scratch_stride() { return WSTR; }
@@ -304,5 +455,37 @@ cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
     if (e != cudaSuccess) return e;
     c->launches++;
   }
+  return cudaGetLastError();
+}
+
+size_t correct_dry_scratch_bytes(int n_batch, int n_slots, int n_mp) {
+  const int nblk = std::max(1, (n_mp + LC_NTHREADS - 1) / LC_NTHREADS);
+  return sizeof(double) * WSTR * (size_t)std::max(n_slots, 1) + sizeof(int32_t) * (size_t)n_batch * std::max(n_mp, 1) +
+         sizeof(int32_t) * ((size_t)n_batch * nblk + 64);
+}
+
+cudaError_t launch_correct_dry(lc_ctx* c, int n_batch, int n_slots, const int32_t* d_wbeg, const int32_t* d_window,
+                               const double* d_Scw, void* scratch, double* d_outS, int32_t* d_mp_begin,
+                               int64_t capacity, int32_t* d_idx, float* d_pos, unsigned long long* counts,
+                               cudaStream_t s) {
+  Store& st = c->st;
+  const int n_mp = st.n_mp;
+  const int nblk = std::max(1, (n_mp + LC_NTHREADS - 1) / LC_NTHREADS);
+  double* scr = (double*)scratch;
+  int32_t* owner = (int32_t*)(scr + (size_t)WSTR * std::max(n_slots, 1));
+  int32_t* bcnt = owner + (size_t)n_batch * std::max(n_mp, 1);
+  cudaError_t e;
+  if (n_mp > 0 && (e = cudaMemsetAsync(owner, 0x7F, sizeof(int32_t) * (size_t)n_batch * n_mp, s)) != cudaSuccess)
+    return e;
+  k_dry_sim3<<<(n_slots + 63) / 64, 64, 0, s>>>(n_slots, n_batch, d_wbeg, d_window, st.kf_pose, d_Scw, scr, d_outS,
+                                              counts);
+  k_dry_mark<<<std::min((n_slots + 7) / 8, 148 * 8), LC_NTHREADS, 0, s>>>(n_slots, n_batch, n_mp, d_wbeg, d_window,
+                                                                       st.kf_fbeg, st.feat_mp, owner);
+  const dim3 g2(nblk, n_batch);
+  k_dry_count<<<g2, LC_NTHREADS, 0, s>>>(n_mp, nblk, owner, st.mp_flags, bcnt);
+  k_dry_scan<<<1, 1024, 0, s>>>(n_batch, nblk, bcnt, d_mp_begin);
+  k_dry_points<<<g2, LC_NTHREADS, 0, s>>>(n_mp, nblk, (long long)capacity, d_wbeg, owner, st.mp_flags, bcnt, scr,
+                                         st.mp_rec, d_idx, d_pos, counts);
+  c->launches += 5;
   return cudaGetLastError();
 }

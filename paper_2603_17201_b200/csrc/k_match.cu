@@ -24,12 +24,24 @@ constexpr unsigned long long NONE = 0x7FFFFFFFFFFFFFFFull;
 // local per-thread counters of the matching kernel (subset of LC_COUNT_*)
 enum { M_QUERIES, M_BAD, M_FOUND, M_DEPTH, M_BOUNDS, M_DIST, M_ANGLE, M_CAND, M_NOCAND,
        M_OVERTH, M_RATIO, M_PROP, M_N };
-__device__ __constant__ int kProjSlot[7] = {
+__device__ __constant__ int kProjSlot[8] = {
     LC_COUNT_QUERIES, LC_COUNT_SKIP_BAD, LC_COUNT_SKIP_FOUND, LC_COUNT_CULL_DEPTH,
-    LC_COUNT_CULL_BOUNDS, LC_COUNT_CULL_DIST, LC_COUNT_CULL_ANGLE};
-__device__ __constant__ int kMatchSlot2[5] = {LC_COUNT_CANDIDATES, LC_COUNT_NO_CAND,
+    LC_COUNT_CULL_BOUNDS, LC_COUNT_CULL_DIST, LC_COUNT_CULL_ANGLE, LC_COUNT_EDGE_AMB};
+__device__ __constant__ int kMatchSlot2[6] = {LC_COUNT_CANDIDATES, LC_COUNT_NO_CAND,
                                               LC_COUNT_OVER_TH, LC_COUNT_RATIO_REJ,
-                                              LC_COUNT_PROPOSALS};
+                                              LC_COUNT_PROPOSALS, LC_COUNT_EDGE_AMB};
+
+// edge-ambiguity (the oracle's flag, same fp64 expressions): a bounds
+// or window decision within 1e-4 px of the edge
+constexpr double kEdgeEps = 1e-4;
+constexpr uint32_t kSurvEdge = 1u << 30;   // Surv.jl bit: the query's bounds decision was
+__device__ __forceinline__ bool bounds_edge(const DevCam& c, double u, double v) {
+  return fabs(u - c.min_x) < kEdgeEps || fabs(u - c.max_x) < kEdgeEps || fabs(v - c.min_y) < kEdgeEps ||
+         fabs(v - c.max_y) < kEdgeEps;
+}
+__device__ __forceinline__ bool window_edge(double du, double dv, double r) {
+  return du < r + kEdgeEps && dv < r + kEdgeEps && (du > r - kEdgeEps || dv > r - kEdgeEps);
+}
 
 
 // Reduce per-thread counters over the block and add them to global memory.
@@ -236,6 +248,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
   const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
   Surv* out = a.surv + a.surv_off[blk];
   uint32_t cA = 0, cB = 0, cQ = 0;   // packed 10-bit counters (<= 64 queries per thread per block)
+  uint32_t cE = 0;                   // edge-ambiguous culled queries (survivors: flag to k_match)
   // software pipeline: the 32-B record (geometry sector) of the query two steps ahead
   // is copied by cp.async into a per-thread 3-slot ring behind the hash (no registers
   // held), its flag and the list entry three steps ahead are in flight in registers
@@ -276,6 +289,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
     int status = 0;
     double u = 0.0, v = 0.0;
     int lvl = 0;
+    bool edge = false;
     if (valid) {
       cQ += 1u;
       do {
@@ -297,10 +311,19 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
           const double va = B * rz * (2.0 - z * rz) + s_cam.cy;
           if (ua < s_cam.min_x - e || ua >= s_cam.max_x + e || va < s_cam.min_y - e ||
               va >= s_cam.max_y + e) {
+            // certainly culled; edge-ambiguous only if u or v is within 1e-4 px of a
+            // bound, which needs ua or va within e + 1e-4 of one: decide exactly then
+            const double e2 = e + kEdgeEps;
+            if (fabs(ua - s_cam.min_x) < e2 || fabs(ua - s_cam.max_x) < e2 || fabs(va - s_cam.min_y) < e2 ||
+                fabs(va - s_cam.max_y) < e2) {
+              lc_project(s_cam, x, y, z, u, v);
+              if (bounds_edge(s_cam, u, v)) cE += 1u;
+            }
             status = LC_Q_BOUNDS; cB += 1u; break;
           }
         }
         lc_project(s_cam, x, y, z, u, v);
+        edge = bounds_edge(s_cam, u, v);   // SURVEY §8(c) edge-ambiguous (oracle: before the cull)
         if (!(u >= s_cam.min_x && u < s_cam.max_x && v >= s_cam.min_y && v < s_cam.max_y)) {
           status = LC_Q_BOUNDS; cB += 1u; break;
         }
@@ -331,9 +354,11 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
     wbase = __shfl_sync(0xffffffffu, wbase, 0);
     if (surv) {
       Surv e;
-      e.q = q; e.jl = (uint32_t)(j - q0) | ((uint32_t)lvl << 27); e.fu = (float)u; e.fv = (float)v;
+      e.q = q; e.jl = (uint32_t)(j - q0) | ((uint32_t)lvl << 27) | (edge ? kSurvEdge : 0u);
+      e.fu = (float)u; e.fv = (float)v;
       out[wbase + __popc(m & ltmask)] = e;
     } else if (valid) {
+      if (edge) cE += 1u;
       const int64_t qi = qbase + (j - q0);
       if (a.dbg_best) a.dbg_best[qi] = status;
       if (a.dbg_uv) {
@@ -346,12 +371,12 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
   __syncthreads();
   if (tid == 0) a.surv_cnt[blk] = s_cnt;
   pdl_trigger();
-  uint32_t cnt[7];
+  uint32_t cnt[8];
   cnt[0] = cQ; cnt[1] = cA & 1023u; cnt[2] = (cA >> 10) & 1023u; cnt[3] = (cA >> 20) & 1023u;
-  cnt[4] = cB & 1023u; cnt[5] = (cB >> 10) & 1023u; cnt[6] = (cB >> 20) & 1023u;
+  cnt[4] = cB & 1023u; cnt[5] = (cB >> 10) & 1023u; cnt[6] = (cB >> 20) & 1023u; cnt[7] = cE;
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
   pdl_wait();   // (PDL) k_fuse_prep zeroes the counters: add after it completed
-  block_add<7>(cnt, kProjSlot, cdst);
+  block_add<8>(cnt, kProjSlot, cdst);
 }
 
 // ---- k_match ------------------------------------------------------------------
@@ -448,6 +473,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   const Surv* sv = a.surv + a.surv_off[blk];
   const int ns_tot = a.surv_cnt[blk];
   uint32_t cC = 0, cP = 0, cE = 0;   // NOCAND | OVERTH << 10 | RATIO << 20; PROP; CAND
+  uint32_t cW = 0;                   // edge-ambiguous survivors
 
   // strict square window |fuv - uv| < r (reading A8). fp32 filter: |(float)a - fu| is
   // within 2.5e-4 px of the exact |a - u| for |u| < 4096 px, so a decision farther
@@ -468,8 +494,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
     const bool act = i0 + lane < ns_tot;
     const Surv e = e_nx;
     if (i0 + NWARP * 32 + lane < ns_tot) e_nx = sv[i0 + NWARP * 32 + lane];
-    const int lvl = (int)(e.jl >> 27);
+    const int lvl = (int)((e.jl >> 27) & 7u);
     int cx0 = 0, cx1 = -1, cy0 = 0, cy1 = -1, nc = 0;
+    bool wedge = false;   // edge-ambiguous query (bounds flag from k_project, or a window decision)
     const float fr = (float)((double)prm.th * a.scale[lvl]);
     if (act) {
       // query descriptor -> shared memory, asynchronously, during the scan
@@ -482,6 +509,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
       cy0 = max(0, (int)floorf((e.fv - fr - 0.01f - fminy) * fsy));
       cy1 = min(rows - 1, (int)floorf((e.fv + fr + 0.01f - fminy) * fsy));
       const int lo = lvl - 1;
+      wedge = (e.jl & kSurvEdge) != 0u;
       // (1) window scan over the staged cells, octave filter (A9) first; slots whose
       // fp32 window test is ambiguous are marked and settled in fp64 after the scan
       uint32_t amb = 0u;
@@ -533,7 +561,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
           const int p = s_cand[lane * CPL + i];
           const float2 fuv = s_uv[p];
           if ((amb >> i) & 1u) {
-            if (!(fabs((double)fuv.x - u) < r && fabs((double)fuv.y - v) < r)) continue;
+            const double du = fabs((double)fuv.x - u), dv = fabs((double)fuv.y - v);
+            wedge |= window_edge(du, dv, r);
+            if (!(du < r && dv < r)) continue;
           }
           s_cand[lane * CPL + m++] = (uint16_t)p;
         }
@@ -599,7 +629,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
             if (oct < lvl - 1 || oct > lvl) continue;
             if (MODE == 1 && (meta & 0x80000000u)) continue;
             const float2 fuv = s_uv[p];
-            if (!(fabs((double)fuv.x - u) < r && fabs((double)fuv.y - v) < r)) continue;
+            const double du = fabs((double)fuv.x - u), dv = fabs((double)fuv.y - v);
+            wedge |= window_edge(du, dv, r);
+            if (!(du < r && dv < r)) continue;
             const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
             take(((uint32_t)popc_desc(d0, d1, __ldg(dp), __ldg(dp + 1)) << 16) | (meta & 0xFFFFu));
             ++nc;
@@ -609,6 +641,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         for (int i = 0; i < ns; ++i) take(s_key[lane * CPL + i]);
       }
       cE += nc;
+      if (wedge) cW += 1u;
       do {
         if (nc == 0) { cC += 1u; break; }
         const int hb = (int)(best >> 16);
@@ -619,7 +652,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         cP += 1u;
         atomicMin(&win[best & 0xFFFFu], ((unsigned long long)hb << 32) | (unsigned int)e.q);
       } while (0);
-      const int64_t qi = qbase + (int64_t)(e.jl & 0x07FFFFFFu);
+      const int64_t qi = qbase + (int64_t)(e.jl & 0x07FFFFFFu);   // bits 27-29 level, 30 edge
       if (a.dbg_best) {
         long long val;
         if (nc == 0) val = (256LL << 48) | (256LL << 32) | 0xFFFFFFFFLL;
@@ -636,10 +669,11 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
     __syncwarp();
   }
   pdl_trigger();
-  uint32_t cnt[5];
+  uint32_t cnt[6];
   cnt[0] = cE; cnt[1] = cC & 1023u; cnt[2] = (cC >> 10) & 1023u; cnt[3] = (cC >> 20) & 1023u; cnt[4] = cP;
+  cnt[5] = cW;
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
-  block_add<5>(cnt, kMatchSlot2, cdst);
+  block_add<6>(cnt, kMatchSlot2, cdst);
   if (a.sole) {  // all proposals of this unit are in: resolve it here (no extra launch)
     __syncthreads();
     resolve_unit<MODE>(a, unit);
@@ -779,7 +813,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_resolve(const MatchArgs a) {
 // Per-call setup: LoopSet stamps, winner/victim init, window membership. The call's
 // epoch is ep[0] + 1 (device counter, so that a replayed CUDA graph gets a fresh one);
 // the last block to finish publishes it in ep[0] for the kernels that follow.
-__global__ void k_fuse_prep(int phase, int64_t skip_lo, int64_t skip_hi, uint32_t* __restrict__ ep, int n_w,
+__global__ void k_fuse_prep(int phase, int zero_counts, int64_t skip_lo, int64_t skip_hi, uint32_t* __restrict__ ep, int n_w,
                             const int32_t* __restrict__ window, int64_t n_wfeat,
                             const int32_t* __restrict__ mp_list, int64_t n_list, int n_mp,
                             unsigned long long* __restrict__ winner,
@@ -788,7 +822,7 @@ __global__ void k_fuse_prep(int phase, int64_t skip_lo, int64_t skip_hi, uint32_
                             uint32_t* __restrict__ vbits, int n_vbits, int32_t* __restrict__ dirty_n,
                             unsigned long long* __restrict__ counts) {
   pdl_trigger();   // k_project reads none of this kernel's outputs
-  if (blockIdx.x == 0 && threadIdx.x < LC_NCOUNT) counts[threadIdx.x] = 0;   // the call's counters
+  if (zero_counts && blockIdx.x == 0 && threadIdx.x < LC_NCOUNT) counts[threadIdx.x] = 0;   // the call's counters
   uint32_t epoch = ep[0] + 1u;
   if (epoch == 0u) epoch = 1u;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -819,6 +853,32 @@ __global__ void k_fuse_prep(int phase, int64_t skip_lo, int64_t skip_hi, uint32_
       __threadfence();
     }
   }
+}
+
+// Forced loop matches of the current keyframe (reading O9.4 / A23), thread per feature f
+// of cur_kf: the tables of a separate apply that runs before the search. Map points are
+// held once per keyframe, so every victim word gets at most one proposal.
+__global__ void k_forced(int n_mp, const uint32_t* __restrict__ ep, int fb, int F,
+                         const int32_t* __restrict__ forced, const int32_t* __restrict__ feat_mp,
+                         const uint8_t* __restrict__ flags, const uint32_t* __restrict__ loop_ep,
+                         unsigned long long* __restrict__ win_cur, unsigned long long* __restrict__ victim,
+                         unsigned long long* __restrict__ counts) {
+  pdl_wait();   // k_fuse_prep: tables initialised, LoopSet stamped, epoch published
+  const uint32_t epoch = *ep;
+  uint32_t n = 0;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+    const int32_t q = forced[f];
+    if (q < 0 || q >= n_mp || (flags[q] & 1u)) continue;
+    const int32_t m = feat_mp[fb + f];
+    if (m == q) continue;
+    if (m < 0) { win_cur[f] = (unsigned long long)(uint32_t)q; ++n; }
+    else if ((flags[m] & 1u) || loop_ep[m] == epoch) continue;
+    else { atomicMin(&victim[m], (unsigned long long)(uint32_t)q); ++n; }
+  }
+  pdl_trigger();
+  const int slot[1] = {LC_COUNT_FORCED};
+  uint32_t loc[1] = {n};
+  block_add<1>(loc, slot, counts);
 }
 
 // Victim marking: flags |= bad, replaced_by = survivor (reading O9 (iv)), victim bitmap.
@@ -1079,7 +1139,7 @@ cudaError_t launch_resolve(lc_ctx* c, int mode, const MatchArgs& a, int n_units,
   return cudaGetLastError();
 }
 
-cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int64_t skip_lo, int64_t skip_hi, int n_w,
+cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int zero_counts, int64_t skip_lo, int64_t skip_hi, int n_w,
                              const int32_t* d_window, int64_t n_wfeat, const int32_t* mp_list,
                              int64_t n_list_total,
                              unsigned long long* winner, unsigned long long* victim,
@@ -1092,12 +1152,23 @@ cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int64_t skip_lo, int64_t skip
     if (skip_hi - skip_lo < n_wfeat) n = std::max<int64_t>(n, n_wfeat);
     n = std::max<int64_t>(n, st.n_mp);
   }
-  k_fuse_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(phase, skip_lo, skip_hi, st.ep, n_w, d_window, n_wfeat,
+  k_fuse_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(phase, zero_counts, skip_lo, skip_hi, st.ep, n_w, d_window, n_wfeat,
                                                  mp_list, n_list_total, st.n_mp, winner, victim,
                                                  st.mp_loop_ep, st.kf_win_ep, st.kf_win_pos,
                                                  st.mp_vbits, n_vbits, st.kf_dirty, counts);
   c->launches++;
   return cudaGetLastError();
+}
+
+cudaError_t launch_forced(lc_ctx* c, int cur_kf, const int32_t* d_forced, unsigned long long* win_cur,
+                          unsigned long long* victim, unsigned long long* counts, cudaStream_t s) {
+  Store& st = c->st;
+  const int fb = st.h_fbeg[cur_kf], F = st.h_fbeg[cur_kf + 1] - fb;
+  cudaError_t e = launch_pdl(k_forced, dim3(std::max(1, (F + LC_NTHREADS - 1) / LC_NTHREADS)), dim3(LC_NTHREADS), 0, s,
+                             st.n_mp, (const uint32_t*)st.ep, fb, F, d_forced, (const int32_t*)st.feat_mp,
+                             (const uint8_t*)st.mp_flags, (const uint32_t*)st.mp_loop_ep, win_cur, victim, counts);
+  c->launches++;
+  return e;
 }
 
 cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned long long* winner,

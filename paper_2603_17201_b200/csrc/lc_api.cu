@@ -1075,26 +1075,59 @@ lc_status lc_state_restore(lc_ctx* c, void* stream) {
 }
 
 // ----------------------------------------------------------------------------
-lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3* S_cw_corr,
-                          int32_t n_window, const int32_t* window_kf, const lc_sim3* S_opt,
-                          lc_sim3* out_S_corr, int64_t* out_counts, void* stream) {
+lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t n_batch, const int32_t* cur_kf,
+                          const lc_sim3* S_cw_corr, const int32_t* window_begin, const int32_t* window_kf,
+                          const lc_sim3* S_opt, lc_sim3* out_S_corr, int32_t* out_mp_begin,
+                          int32_t* out_mp_idx, float* out_mp_pos, int64_t out_capacity, int64_t* out_counts,
+                          void* stream) {
   return guarded(c, [&] {
-    capture_gate(c, stream, true);
+    const bool dry = mode == (LC_CORRECT_WINDOW | LC_DRY_RUN);
+    capture_gate(c, stream, !dry);
     REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
-    REQUIRE(mode == LC_CORRECT_WINDOW || mode == LC_CORRECT_ALL, LC_EINVAL, "bad mode");
+    REQUIRE(mode == LC_CORRECT_WINDOW || mode == LC_CORRECT_ALL || dry, LC_EINVAL, "bad mode");
     Store& st = c->st;
     Call call(c, stream);
     unsigned long long* cnt = call.counts(out_counts, LC_NCOUNT);   // zeroed by the first kernel
-    if (mode == LC_CORRECT_WINDOW) {
-      REQUIRE(S_cw_corr, LC_EINVAL, "null S_cw_corr");
-      REQUIRE(cur_kf >= 0 && cur_kf < st.n_kf, LC_ERANGE, "cur_kf out of range");
-      mark_window(c, n_window, window_kf);
-      REQUIRE(window_kf[0] == cur_kf, LC_EINVAL, "window_kf[0] must be cur_kf");
+    if (mode & LC_CORRECT_WINDOW) {
+      REQUIRE(cur_kf && S_cw_corr && window_begin && window_kf, LC_EINVAL, "null WINDOW argument");
+      REQUIRE(dry ? n_batch >= 1 : n_batch == 1, LC_EINVAL, "n_batch must be 1 (>= 1 with LC_DRY_RUN)");
+      REQUIRE(window_begin[0] == 0, LC_EINVAL, "window_begin[0] must be 0");
+      for (int b = 0; b < n_batch; ++b) {
+        REQUIRE(cur_kf[b] >= 0 && cur_kf[b] < st.n_kf, LC_ERANGE, "cur_kf out of range");
+        REQUIRE(window_begin[b + 1] > window_begin[b], LC_EINVAL, "empty window");
+        mark_window(c, window_begin[b + 1] - window_begin[b], window_kf + window_begin[b]);
+        REQUIRE(window_kf[window_begin[b]] == cur_kf[b], LC_EINVAL, "a window must start with its cur_kf");
+      }
+      const int n_slots = window_begin[n_batch];
       const int32_t* d_win = nullptr;
       const double* d_S = nullptr;
-      call.arg(window_kf, n_window, &d_win);
-      call.arg((const double*)S_cw_corr, 13, &d_S);
+      const int32_t* d_wb = nullptr;
+      call.arg(window_kf, n_slots, &d_win);
+      call.arg((const double*)S_cw_corr, 13 * (size_t)n_batch, &d_S);
+      call.arg(window_begin, (size_t)n_batch + 1, &d_wb);
       call.commit();
+      if (dry) {
+        REQUIRE(out_S_corr && out_mp_begin && out_capacity >= 0 && (out_capacity == 0 || (out_mp_idx && out_mp_pos)),
+                LC_EINVAL, "null DRY_RUN output");
+        void* scr = call.scratch(correct_dry_scratch_bytes(n_batch, n_slots, st.n_mp));
+        double* dS = (double*)call.out((double*)out_S_corr, 13 * (size_t)n_slots);
+        int32_t* dB = call.out(out_mp_begin, (size_t)n_batch + 1);
+        int32_t* dI = out_capacity ? call.out(out_mp_idx, (size_t)out_capacity) : nullptr;
+        float* dP = out_capacity ? call.out(out_mp_pos, 3 * (size_t)out_capacity) : nullptr;
+        {
+          Prof pr(c, LC_PROF_CORRECT_WINDOW, call.s);
+          CK(launch_correct_dry(c, n_batch, n_slots, d_wb, d_win, d_S, scr, dS, dB, out_capacity, dI, dP, cnt,
+                                call.s));
+        }
+        int32_t total = 0;
+        CK(cudaMemcpyAsync(&total, dB + n_batch, sizeof(int32_t), cudaMemcpyDeviceToHost, call.s));
+        call.finish();
+        CK(cudaStreamSynchronize(call.s));
+        REQUIRE((int64_t)total <= out_capacity, LC_ECAPACITY,
+                "DRY_RUN: " + std::to_string(total) + " corrected points exceed out_capacity");
+        return;
+      }
+      const int n_window = n_slots;
       double* scr = (double*)call.scratch(sizeof(double) * correct_window_scratch_stride() * (size_t)n_window);
       double* d_outS = (out_S_corr && is_device_ptr(c, out_S_corr)) ? (double*)out_S_corr : nullptr;
       {
@@ -1102,10 +1135,8 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
         CK(launch_correct_window(c, 0, n_window, d_win, d_S, scr, d_outS, cnt, call.s));
       }
       if (out_S_corr && !d_outS) {
-        {
-          CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr + 28, sizeof(double) * correct_window_scratch_stride(),
-                               sizeof(lc_sim3), n_window, cudaMemcpyDefault, call.s));
-        }
+        CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr + 28, sizeof(double) * correct_window_scratch_stride(),
+                             sizeof(lc_sim3), n_window, cudaMemcpyDefault, call.s));
       }
       std::fill(st.h_in_win.begin(), st.h_in_win.end(), 0);
       for (int i = 0; i < n_window; ++i) st.h_in_win[window_kf[i]] = 1;
@@ -1127,6 +1158,7 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t cur_kf, const lc_sim3
 lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_window,
                   const int32_t* window_kf, const lc_sim3* window_S, const int32_t* win_list_begin,
                   const int32_t* mp_list, int64_t n_list, const lc_match_params* params,
+                  int32_t cur_kf, const int32_t* forced_mp,
                   int64_t* io_winner, int64_t* io_victim, int8_t* out_action,
                   const lc_query_debug* dbg, int64_t* out_counts, void* stream) {
   return guarded(c, [&] {
@@ -1145,6 +1177,12 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
               "win_list_begin must span [0, n_list]");
       for (int i = 0; i < n_window; ++i)
         REQUIRE(win_list_begin[i + 1] >= win_list_begin[i], LC_EINVAL, "win_list_begin not monotone");
+    }
+    int cur_pos = -1;   // forced loop matches (O9.4): cur_kf must be a window keyframe
+    if (forced_mp && (phase & LC_FUSE_PLAN)) {
+      for (int i = 0; i < n_window; ++i)
+        if (window_kf[i] == cur_kf) cur_pos = i;
+      REQUIRE(cur_pos >= 0, LC_EINVAL, "forced_mp given but cur_kf is not a window keyframe");
     }
     if (!window_S && (phase & LC_FUSE_PLAN))
       for (int i = 0; i < n_window; ++i)
@@ -1178,7 +1216,8 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     // on each chunk's blocks as it lands (k_project stamps the LoopSet), the resolve
     // after all of them
     const bool pipe = (phase & LC_FUSE_PLAN) && win_list_begin && n_list >= (1 << 18) && !dbg &&
-                      !c->cap && w_lo == 0 && w_hi == n_window && !is_device_ptr(c, mp_list);
+                      !c->cap && w_lo == 0 && w_hi == n_window && !is_device_ptr(c, mp_list) &&
+                      cur_pos < 0;   // the forced step needs the LoopSet stamped up front
     const bool sole = !pipe && (w_hi - w_lo) >= 2 * 148 && max_len <= 16384;
     const int64_t ch = sole ? std::max<int64_t>(max_len, 1) : pick_chunk(total_q);
     std::vector<int32_t> bunit;
@@ -1269,15 +1308,24 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       dbg_nc = call.out(dbg->ncand, (size_t)n_q_all, true);
     }
     // ---- epoch (LoopSet stamp / window membership) ----
-    if (c->cap) c->cap->n_fuse++;
-    else epoch_reserve(c, 1, call.s);
+    const int n_ep = cur_pos >= 0 ? 2 : 1;
+    if (c->cap) c->cap->n_fuse += n_ep;
+    else epoch_reserve(c, n_ep, call.s);
+    if (cur_pos >= 0) {   // O9.4: the forced matches, applied before the search
+      const int32_t* d_forced = call.in(forced_mp, (size_t)(st.h_fbeg[cur_kf + 1] - st.h_fbeg[cur_kf]));
+      Prof pr(c, LC_PROF_APPLY, call.s);
+      CK(launch_fuse_prep(c, LC_FUSE_PLAN, 1, 0, 0, n_window, d_win, n_wfeat, d_list, n_list, win, vic, cnt,
+                          call.s));
+      CK(launch_forced(c, cur_kf, d_forced, win + woff[cur_pos], vic, cnt, call.s));
+      CK(launch_fuse_apply(c, d_woff, win, vic, cnt, call.s));
+    }
     {
       Prof pr(c, LC_PROF_FUSE_PREP, call.s);
       // sole-mode CTAs initialise their own units' words; every other word of the
       // table (the other shards' units included) is set to NONE here (lc.h contract)
       const int64_t skip_lo = sole ? woff[w_lo] : 0, skip_hi = sole ? woff[w_hi] : 0;
-      CK(launch_fuse_prep(c, phase, skip_lo, skip_hi, n_window, d_win, n_wfeat, d_list, pipe ? 0 : n_list,
-                          win, vic, cnt, call.s));
+      CK(launch_fuse_prep(c, phase, cur_pos < 0 ? 1 : 0, skip_lo, skip_hi, n_window, d_win, n_wfeat, d_list,
+                          pipe ? 0 : n_list, win, vic, cnt, call.s));
     }
     if (phase & LC_FUSE_PLAN) {
       a.unit_kf = d_win;

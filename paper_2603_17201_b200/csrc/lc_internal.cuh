@@ -325,11 +325,13 @@ cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, co
 cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max, int part,
                          cudaStream_t s, bool pdl = true);  // part 0: k_project, 1: k_match; blocks [a.blk_base, +n_blocks)
 // winner words [0, n_wfeat) are set to NONE except [skip_lo, skip_hi) (sole-mode units)
-cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int64_t skip_lo, int64_t skip_hi, int n_w,
+cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int zero_counts, int64_t skip_lo, int64_t skip_hi, int n_w,
                              const int32_t* d_window, int64_t n_wfeat, const int32_t* mp_list,
                              int64_t n_list_total,
                              unsigned long long* winner, unsigned long long* victim,
                              unsigned long long* counts, cudaStream_t s);   // zeroes counts
+cudaError_t launch_forced(lc_ctx* c, int cur_kf, const int32_t* d_forced, unsigned long long* win_cur,
+                          unsigned long long* victim, unsigned long long* counts, cudaStream_t s);
 cudaError_t launch_resolve(lc_ctx* c, int mode, const MatchArgs& a, int n_units, cudaStream_t s);
 cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned long long* winner,
                               const unsigned long long* victim, unsigned long long* counts,
@@ -341,6 +343,11 @@ int correct_window_scratch_stride();
 int correct_all_scratch_stride();
 cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
                                unsigned long long* counts, cudaStream_t s);   // zeroes counts
+size_t correct_dry_scratch_bytes(int n_batch, int n_slots, int n_mp);
+cudaError_t launch_correct_dry(lc_ctx* c, int n_batch, int n_slots, const int32_t* d_wbeg, const int32_t* d_window,
+                               const double* d_Scw, void* scratch, double* d_outS, int32_t* d_mp_begin,
+                               int64_t capacity, int32_t* d_idx, float* d_pos, unsigned long long* counts,
+                               cudaStream_t s);   // WINDOW | DRY_RUN batch (zeroes counts)
 cudaError_t launch_fill_u64(lc_ctx* c, unsigned long long* p, int64_t n, unsigned long long v,
                             cudaStream_t s);
 cudaError_t launch_state_copy(lc_ctx* c, bool save, cudaStream_t s);

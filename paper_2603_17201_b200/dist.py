@@ -38,7 +38,7 @@ def shard_bounds(n_window: int, world: int, win_list_begin=None, n_list: int = 0
 
 
 def fuse_sharded(fuser, window, mp_list, params, *, window_S=None, win_list_begin=None,
-                 group=None, device=None, tables=None, events=None):
+                 group=None, device=None, tables=None, events=None, cur_kf=-1, forced_mp=None):
     """PLAN on this rank's shard -> all_reduce(MIN) of [winner | victim] -> APPLY.
 
     tables: optional preallocated int64 tensor of n_wfeat + n_mp entries on `device`
@@ -59,9 +59,10 @@ def fuse_sharded(fuser, window, mp_list, params, *, window_S=None, win_list_begi
     win, vic = tables[:n_wfeat], tables[n_wfeat:]
     w_arg = win.numpy() if host else win
     v_arg = vic.numpy() if host else vic
+    extra = {} if forced_mp is None else dict(cur_kf=cur_kf, forced_mp=forced_mp)   # every rank: O9.4
     plan = fuser.fuse(window, mp_list, params, window_S=window_S, win_list_begin=win_list_begin,
                       phase=LC_FUSE_PLAN, w_lo=lo, w_hi=hi, winner=w_arg, victim=v_arg,
-                      action=False, host=host)
+                      action=False, host=host, **extra)
     if events is not None:
         events[0].record()
     dist.all_reduce(tables, op=dist.ReduceOp.MIN, group=group)

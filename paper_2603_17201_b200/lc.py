@@ -396,25 +396,55 @@ class Context:
         k = self._keep(host)
         window = np.ascontiguousarray(window, np.int32)
         S = np.ascontiguousarray(S_cw_corr, np.float64)
+        cur = np.array([int(cur_kf)], np.int32)
+        wb = np.array([0, len(window)], np.int32)
         if host:
             outS = np.zeros((len(window), 13), np.float64)
             cnt = np.zeros(LC_NCOUNT, np.int64)
         else:
             outS = self._dev(len(window) * 13, torch.float64)
             cnt = self._dev(LC_NCOUNT, torch.int64)
-        st = self.lib.lc_correct_sim3(self.h, LC_CORRECT_WINDOW, int(cur_kf), k.ptr(S), len(window),
-                                      k.ptr(window), None, k.ptr(outS), k.ptr(cnt), self._stream())
+        st = self.lib.lc_correct_sim3(self.h, LC_CORRECT_WINDOW, 1, k.ptr(cur), k.ptr(S), k.ptr(wb),
+                                      k.ptr(window), None, k.ptr(outS), None, None, None, 0, k.ptr(cnt),
+                                      self._stream())
         self._check("lc_correct_sim3", st)
         if host:
             self.synchronize()
             return outS, counts_dict(cnt)
         return outS.view(-1, 13), cnt
 
+    def correct_window_batch(self, cur_kf, S_cw_corr, window_begin, window, capacity=None, host=True):
+        """LC_CORRECT_WINDOW | LC_DRY_RUN: corrections of several hypotheses, nothing written
+        back. Returns (S_corr [sum window, 13], mp_begin [n_batch + 1], mp_idx, mp_pos [n, 3],
+        counts)."""
+        k = self._keep(host)
+        cur = np.ascontiguousarray(cur_kf, np.int32)
+        nb = len(cur)
+        S = np.ascontiguousarray(S_cw_corr, np.float64).reshape(nb, 13)
+        wb = np.ascontiguousarray(window_begin, np.int32)
+        win = np.ascontiguousarray(window, np.int32)
+        cap = nb * self.n_mp if capacity is None else int(capacity)
+        mk = (lambda n, dt, npdt: np.zeros(n, npdt)) if host else (lambda n, dt, npdt: self._dev(n, dt))
+        outS = mk(len(win) * 13, torch.float64, np.float64)
+        mb = mk(nb + 1, torch.int32, np.int32)
+        idx = mk(max(cap, 1), torch.int32, np.int32)
+        pos = mk(3 * max(cap, 1), torch.float32, np.float32)
+        cnt = mk(LC_NCOUNT, torch.int64, np.int64)
+        st = self.lib.lc_correct_sim3(self.h, LC_CORRECT_WINDOW | _lib.LC_DRY_RUN, nb, k.ptr(cur), k.ptr(S),
+                                      k.ptr(wb), k.ptr(win), None, k.ptr(outS), k.ptr(mb), k.ptr(idx),
+                                      k.ptr(pos), cap, k.ptr(cnt), self._stream())
+        self._check("lc_correct_sim3", st)
+        if host:
+            n = int(mb[-1])
+            return outS.reshape(-1, 13), mb, idx[:n], pos.reshape(-1, 3)[:n], counts_dict(cnt)
+        return outS.view(-1, 13), mb, idx, pos.view(-1, 3), cnt
+
     def correct_all(self, S_opt, host=True):
         k = self._keep(host)
         cnt = np.zeros(LC_NCOUNT, np.int64) if host else self._dev(LC_NCOUNT, torch.int64)
-        st = self.lib.lc_correct_sim3(self.h, LC_CORRECT_ALL, 0, None, 0, None,
-                                      k.ptr(S_opt, np.float64), None, k.ptr(cnt), self._stream())
+        st = self.lib.lc_correct_sim3(self.h, LC_CORRECT_ALL, 0, None, None, None, None,
+                                      k.ptr(S_opt, np.float64), None, None, None, None, 0, k.ptr(cnt),
+                                      self._stream())
         self._check("lc_correct_sim3", st)
         if host:
             self.synchronize()
@@ -424,7 +454,7 @@ class Context:
     # -- lc_fuse -------------------------------------------------------------------
     def fuse(self, window, mp_list, params, *, window_S=None, win_list_begin=None,
              phase=LC_FUSE_ALL, w_lo=0, w_hi=None, winner=None, victim=None, action=True,
-             debug=False, host=True):
+             debug=False, host=True, cur_kf=-1, forced_mp=None):
         """Returns dict(winner, victim, action, counts[, best, uv, ncand]).
         winner / victim: pass tensors to use them in place (PLAN -> NCCL -> APPLY)."""
         k = self._keep(host)
@@ -451,6 +481,7 @@ class Context:
             dbg = _lib.lc_query_debug(k.ptr(dd["best"]), k.ptr(dd["uv"]), k.ptr(dd["ncand"]))
         st = self.lib.lc_fuse(self.h, int(phase), int(w_lo), int(w_hi), n_w, k.ptr(window), k.ptr(wS),
                               k.ptr(wb), k.ptr(mp_list, np.int32), n_list, C.byref(_params(params)),
+                              int(cur_kf), k.ptr(forced_mp, np.int32),
                               k.ptr(winner), k.ptr(victim), k.ptr(act),
                               C.byref(dbg) if dbg is not None else None, k.ptr(cnt), self._stream())
         self._check("lc_fuse", st)

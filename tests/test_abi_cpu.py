@@ -59,8 +59,10 @@ def test_null_and_no_device_errors(lib):
         assert st == 0
         lib.lc_destroy(h)
     assert lib.lc_destroy(None) == _lib.LC_EINVAL
-    assert lib.lc_fuse(None, 3, 0, 0, 0, None, None, None, None, 0, None, None, None, None, None,
-                       None, None) == _lib.LC_EINVAL
+    assert lib.lc_fuse(None, 3, 0, 0, 0, None, None, None, None, 0, None, -1, None, None, None, None,
+                       None, None, None) == _lib.LC_EINVAL
+    assert lib.lc_correct_sim3(None, 1, 1, None, None, None, None, None, None, None, None, None, 0, None,
+                               None) == _lib.LC_EINVAL
 
 
 def test_binding_fails_loudly_without_library(monkeypatch, tmp_path):

@@ -56,6 +56,49 @@ def _compare_queries(g, o, label):
     return set(bad.tolist())
 
 
+def _reach(w, g, o, bad, params):
+    """Entries reachable from the mismatching (edge-ambiguous) queries: the features they
+    proposed to on either side (whole keyframes when the orientation histogram is on), the
+    occupants of those slots (victim words), the query points (survivors), and every
+    keyframe / map point an APPLY of those words can touch."""
+    window = np.asarray(w.window)
+    F = np.diff(w.kf_feat_begin)[window]
+    woff = np.r_[0, np.cumsum(F)]
+    wb = np.asarray(w.win_list_begin) if w.win_list_begin is not None else None
+    n_list = len(w.mp_list)
+    feats, kpos, surv = set(), set(), set()
+    for qi in bad:
+        i = int(np.searchsorted(wb, qi, side="right") - 1) if wb is not None else qi // n_list
+        kpos.add(i)
+        surv.add(int(w.mp_list[qi if wb is not None else qi % n_list]))
+        for tab in (g["best"], o["best"]):
+            b = int(tab[qi])
+            if b >= 0 and (b & 0xFFFFFFFF) != 0xFFFFFFFF:
+                feats.add(int(woff[i] + (b & 0xFFFFFFFF)))
+    if params[4]:
+        for i in kpos:
+            feats.update(range(int(woff[i]), int(woff[i + 1])))
+    feats = np.array(sorted(feats), np.int64)
+    fmask = np.zeros(int(woff[-1]), bool)
+    fmask[feats] = True
+    # window-major -> global feature index of the masked slots
+    gidx = np.concatenate([np.arange(w.kf_feat_begin[k], w.kf_feat_begin[k + 1]) for k in window])
+    occ = w.feat_mp[gidx[fmask]]
+    vmask = np.zeros(w.n_mp, bool)
+    vmask[occ[occ >= 0]] = True
+    vmask[list(surv)] = True
+    kf_of = np.repeat(np.arange(w.n_kf), np.diff(w.kf_feat_begin))
+    kmask = np.zeros(w.n_kf, bool)
+    kmask[kf_of[gidx[fmask]]] = True
+    held = w.feat_mp >= 0
+    kmask[kf_of[held & vmask[np.maximum(w.feat_mp, 0)]]] = True
+    slot_mask = kmask[kf_of]
+    mmask = vmask.copy()
+    fm = w.feat_mp[slot_mask]
+    mmask[fm[fm >= 0]] = True
+    return fmask, vmask, slot_mask, mmask
+
+
 def _run_loop(Ctx, name, params, seed=0):
     w = world(name, seed)
     ctx, om = _pair(Ctx, w)
@@ -70,25 +113,36 @@ def _run_loop(Ctx, name, params, seed=0):
                  debug=True)
     o = om.fuse(w.window, w.mp_list, params, window_S=w.win_S, win_list_begin=w.win_list_begin,
                 debug=True)
-    bad = _compare_queries(g, o, name)
+    bad = sorted(_compare_queries(g, o, name))
+    # north_star: edge-ambiguous differences are counted and reported -- the library's
+    # counter equals the oracle's, and bounds the mismatches
+    assert g["counts"]["edge_amb"] == o["counts"]["edge_amb"], (g["counts"]["edge_amb"], o["counts"]["edge_amb"])
+    assert len(bad) <= o["counts"]["edge_amb"]
     if not bad:
-        assert np.array_equal(g["winner"], o["winner"]), "winner table"
-        assert np.array_equal(g["victim"], o["victim"]), "victim table"
-        assert np.array_equal(g["action"], o["action"]), "action table"
-        assert g["counts"] == o["counts"], (g["counts"], o["counts"])
-        st = ctx.download_map()
-        assert np.array_equal(st["feat_mp"], om.feat_mp), "associations after apply"
-        assert np.array_equal(st["mp_flags"], om.mp_flags)
-        assert np.array_equal(st["mp_replaced_by"], om.mp_replaced_by)
-        assert np.array_equal(st["mp_nobs"], om.mp_nobs)
+        fmask = np.zeros(len(g["winner"]), bool)
+        vmask = mmask = np.zeros(w.n_mp, bool)
+        slot_mask = np.zeros(len(w.feat_mp), bool)
     else:
-        print(f"{name}: {len(bad)} edge-ambiguous query mismatches (tables not compared exactly)")
+        fmask, vmask, slot_mask, mmask = _reach(w, g, o, bad, params)
+        print(f"{name}: {len(bad)} edge-ambiguous query mismatches; masked {fmask.sum()} winner words, "
+              f"{vmask.sum()} victim words, {slot_mask.sum()} slots")
+        assert fmask.sum() < 0.05 * len(fmask) and slot_mask.sum() < 0.05 * len(slot_mask)
+    assert np.array_equal(g["winner"][~fmask], o["winner"][~fmask]), "winner table"
+    assert np.array_equal(g["victim"][~vmask], o["victim"][~vmask]), "victim table"
+    assert np.array_equal(g["action"][~fmask], o["action"][~fmask]), "action table"
+    if not bad:
+        assert g["counts"] == o["counts"], (g["counts"], o["counts"])
+    st = ctx.download_map()
+    assert np.array_equal(st["feat_mp"][~slot_mask], om.feat_mp[~slot_mask]), "associations after apply"
+    assert np.array_equal(st["mp_flags"][~vmask], om.mp_flags[~vmask])
+    assert np.array_equal(st["mp_replaced_by"][~vmask], om.mp_replaced_by[~vmask])
+    assert np.array_equal(st["mp_nobs"][~mmask], om.mp_nobs[~mmask])
     cg = ctx.correct_all(w.S_opt)
     co = om.correct_all(w.S_opt)
     st = ctx.download_map()
     assert np.array_equal(st["kf_pose"], om.kf_pose), "propagated poses"
+    assert np.array_equal(st["mp_pos"][~vmask], om.mp_pos[~vmask]), "propagated points"
     if not bad:
-        assert np.array_equal(st["mp_pos"], om.mp_pos), "propagated points"
         assert cg == co
     return w, g, o, ctx
 

@@ -1,0 +1,193 @@
+"""GPU (liblc) vs CPU oracle for the round-2 boundary additions: forced loop matches in
+lc_fuse (O9.4 / A23), lc_correct_sim3(WINDOW | DRY_RUN) batches (O3', SURVEY.md §8(d)
+C4), the edge-ambiguous counter (§8(c) O11) at constructed distances. Bars as in
+test_gpu_parity.py: index tables, counters and maps bit-exact; fp64 Sim3 results and
+fp32 positions bit-exact (same expression order, -fmad=false / -ffp-contract=off)."""
+import functools
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from lcsynth import make_world  # noqa: E402
+from lcsynth.world import FUSE_PARAMS, FUSE_PARAMS_CHECKS  # noqa: E402
+from tests import tinymap as tm  # noqa: E402
+
+NONE = oracle.NONE64
+
+
+@functools.lru_cache(maxsize=None)
+def world(name, seed=0):
+    return make_world(name, seed)
+
+
+@pytest.fixture(scope="module")
+def Ctx():
+    from paper_2603_17201_b200 import Context, build
+    build.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return Context
+
+
+def forced_for(w, seed=3):
+    """Forced matches as detection would hand them to CorrectLoop: the loop-side twin of
+    each landmark the current keyframe observes, plus 10% empty-slot ADDs."""
+    c = int(w.cur_kf)
+    fb = w.kf_feat_begin
+    loop_mps = np.unique(np.asarray(w.mp_list, np.int64))
+    lm_loop = {int(w.mp_lm[q]): int(q) for q in loop_mps}
+    rng = np.random.default_rng(seed)
+    forced = np.full(fb[c + 1] - fb[c], -1, np.int32)
+    for f in range(len(forced)):
+        m = w.feat_mp[fb[c] + f]
+        if m >= 0 and int(w.mp_lm[m]) in lm_loop:
+            forced[f] = lm_loop[int(w.mp_lm[m])]
+        elif m < 0 and rng.random() < 0.1:
+            forced[f] = int(rng.choice(loop_mps))
+    return forced
+
+
+@pytest.mark.parametrize("name,params", [("T1", FUSE_PARAMS), ("C1", FUSE_PARAMS_CHECKS),
+                                         ("T5", FUSE_PARAMS_CHECKS), ("C2", FUSE_PARAMS)])
+def test_forced_matches_parity(Ctx, name, params):
+    w = world(name)
+    forced = forced_for(w)
+    assert (forced >= 0).sum() > 5
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    om = oracle.OracleMap(w)
+    ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    g = ctx.fuse(w.window, w.mp_list, params, window_S=w.win_S, win_list_begin=w.win_list_begin,
+                 cur_kf=w.cur_kf, forced_mp=forced)
+    o = om.fuse(w.window, w.mp_list, params, window_S=w.win_S, win_list_begin=w.win_list_begin,
+                cur_kf=w.cur_kf, forced_mp=forced)
+    assert g["counts"]["forced"] == o["counts"]["forced"] > 0
+    assert np.array_equal(g["winner"], o["winner"]) and np.array_equal(g["victim"], o["victim"])
+    assert np.array_equal(g["action"], o["action"])
+    assert g["counts"] == o["counts"], {k: (g["counts"][k], o["counts"][k]) for k in g["counts"]
+                                        if g["counts"][k] != o["counts"][k]}
+    st = ctx.download_map()
+    for key, ref in (("feat_mp", om.feat_mp), ("mp_flags", om.mp_flags), ("mp_replaced_by", om.mp_replaced_by),
+                     ("mp_nobs", om.mp_nobs)):
+        assert np.array_equal(st[key], ref), key
+    ctx.close()
+
+
+def test_forced_matches_sharded_plan_equals_fuse_all(Ctx):
+    """Every shard's PLAN carries the forced matches (idempotent on an already forced map):
+    PLAN per shard on one device, MIN merge, APPLY == FUSE_ALL."""
+    from paper_2603_17201_b200 import LC_FUSE_APPLY, LC_FUSE_PLAN
+    w = world("T5")
+    forced = forced_for(w)
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    ctx.state_save()
+    ref = ctx.fuse(w.window, w.mp_list, FUSE_PARAMS_CHECKS, window_S=w.win_S, win_list_begin=w.win_list_begin,
+                   cur_kf=w.cur_kf, forced_mp=forced)
+    ref_map = ctx.download_map()
+    ctx.state_restore()
+    cuts = np.linspace(0, len(w.window), 4).astype(int)
+    tabs = [ctx.fuse(w.window, w.mp_list, FUSE_PARAMS_CHECKS, window_S=w.win_S, win_list_begin=w.win_list_begin,
+                     phase=LC_FUSE_PLAN, w_lo=cuts[r], w_hi=cuts[r + 1], cur_kf=w.cur_kf, forced_mp=forced)
+            for r in range(3)]
+    win = np.minimum.reduce([t["winner"] for t in tabs])
+    vic = np.minimum.reduce([t["victim"] for t in tabs])
+    assert np.array_equal(win, ref["winner"]) and np.array_equal(vic, ref["victim"])
+    ctx.fuse(w.window, w.mp_list, FUSE_PARAMS_CHECKS, window_S=w.win_S, win_list_begin=w.win_list_begin,
+             phase=LC_FUSE_APPLY, winner=win, victim=vic)
+    m = ctx.download_map()
+    for k in ref_map:
+        assert np.array_equal(m[k], ref_map[k]), k
+    ctx.close()
+
+
+def test_forced_requires_window_keyframe(Ctx):
+    from paper_2603_17201_b200 import _lib
+    from paper_2603_17201_b200._lib import LcError
+    w = world("T1")
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    outside = int(np.setdiff1d(np.arange(w.n_kf), w.window)[0])
+    with pytest.raises(LcError) as e:
+        ctx.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=np.tile(tm.IDENT, (len(w.window), 1)),
+                 cur_kf=outside, forced_mp=np.full(int(np.diff(w.kf_feat_begin)[outside]), -1, np.int32))
+    assert e.value.status == _lib.LC_EINVAL
+    ctx.close()
+
+
+@pytest.mark.parametrize("host", [True, False], ids=["host-out", "device-out"])
+def test_dry_run_batch_parity_C4(Ctx, host):
+    """The 32 C4 hypotheses' window corrections as one LC_DRY_RUN batch: S_corr, the CSR of
+    corrected points, their indices and fp32 positions bit-exact against oracle O3'; the
+    device map is untouched (nothing written back)."""
+    w = world("C4")
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    before = ctx.download_map()
+    om = oracle.OracleMap(w)
+    oS, omb, oidx, opos, oc = om.correct_window_batch(w.hyp_cur, w.hyp_S_cw, w.hyp_win_begin, w.hyp_window)
+    gS, gmb, gidx, gpos, gc = ctx.correct_window_batch(w.hyp_cur, w.hyp_S_cw, w.hyp_win_begin, w.hyp_window,
+                                                       capacity=int(omb[-1]) + 7, host=host)
+    if not host:
+        torch.cuda.synchronize()
+        n = int(gmb[-1].item())
+        gS, gmb, gidx, gpos = gS.cpu().numpy(), gmb.cpu().numpy(), gidx[:n].cpu().numpy(), gpos[:n].cpu().numpy()
+        gc = dict(zip(oracle.COUNTER_NAMES, gc.cpu().numpy().tolist()))
+    assert np.array_equal(gS, oS)
+    assert np.array_equal(gmb, omb) and np.array_equal(gidx, oidx)
+    assert np.array_equal(gpos, opos)
+    assert gc["corr_mp"] == oc["corr_mp"] and gc["corr_kf"] == oc["corr_kf"]
+    after = ctx.download_map()
+    for k in before:
+        assert np.array_equal(before[k], after[k]), k
+    ctx.close()
+
+
+def test_dry_run_capacity_and_errors(Ctx):
+    from paper_2603_17201_b200 import _lib
+    from paper_2603_17201_b200._lib import LcError
+    w = world("C4")
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    om = oracle.OracleMap(w)
+    _, omb, _, _, _ = om.correct_window_batch(w.hyp_cur[:3], w.hyp_S_cw[:3], w.hyp_win_begin[:4], w.hyp_window)
+    with pytest.raises(LcError) as e:
+        ctx.correct_window_batch(w.hyp_cur[:3], w.hyp_S_cw[:3], w.hyp_win_begin[:4], w.hyp_window,
+                                 capacity=int(omb[-1]) - 1)
+    assert e.value.status == _lib.LC_ECAPACITY
+    bad = w.hyp_window.copy()
+    bad[w.hyp_win_begin[1]] = bad[w.hyp_win_begin[1] + 1]      # window 1 does not start with its cur_kf
+    with pytest.raises(LcError) as e:
+        ctx.correct_window_batch(w.hyp_cur[:3], w.hyp_S_cw[:3], w.hyp_win_begin[:4], bad)
+    assert e.value.status == _lib.LC_EINVAL
+    ctx.close()
+
+
+BASE = np.random.default_rng(7).integers(0, 256, 32, dtype=np.uint8)
+
+
+@pytest.mark.parametrize("fu,fv,x", [
+    (254.0 - 5e-5, 250.0, 0.5), (254.0 + 5e-5, 250.0, 0.5), (254.0 - 3e-4, 250.0, 0.5),
+    (251.0, 246.0 + 5e-5, 0.5), (254.0 - 5e-5, 240.0, 0.5), (250.0, 250.0, 0.5),
+    (1.0, 1.0, 2.0 - 4e-7), (1.0, 1.0, 2.0 - 5e-6), (1.0, 1.0, 2.0 + 4e-7), (1.0, 1.0, -2.0 + 4e-7),
+])
+def test_edge_counter_constructed(Ctx, fu, fv, x):
+    """The library's edge-ambiguous counter equals the oracle's flag at constructed
+    distances from a window edge and from the image bounds (u = 100 x + 200)."""
+    p = (x, 0.5, 1.0) if x != 0.5 else (0.5, 0.5, 1.0)
+    n = np.asarray(p) / np.linalg.norm(p)
+    arrays = tm.build([dict(feats=[dict(u=fu, v=fv, desc=BASE)])],
+                      [dict(pos=p, dmax=2.0 if x != 0.5 else 1.2, normal=tuple(n), desc=BASE)])
+    om = oracle.OracleMap(arrays=arrays, cams=[tm.PIN])
+    o = om.fuse([0], [0], (4, 50, 0, 0, 0), window_S=tm.IDENT[None])
+    ctx = Ctx(0)
+    ctx.upload_map(arrays, [tm.PIN])
+    g = ctx.fuse([0], np.array([0], np.int32), (4, 50, 0, 0, 0), window_S=tm.IDENT[None])
+    assert g["counts"] == o["counts"]
+    ctx.close()
