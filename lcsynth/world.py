@@ -95,6 +95,10 @@ CONFIGS = {
     "T1": WorldConfig("T1", 12, 1500, 300, "euroc", 4.0, 8, False, overlap=3.0),
     "T2": WorldConfig("T2", 16, 2500, 400, "tumvi", 2.5, 10, False, overlap=3.0),
     "T5": WorldConfig("T5", 24, 6000, 500, "euroc", 4.0, 0, True, overlap=2.0),
+    # >= 296-keyframe windows (the sole-mode launch, one CTA per window keyframe) at sizes
+    # the oracle finishes in seconds: pinhole and Kannala-Brandt, per-keyframe lists
+    "S3": WorldConfig("S3", 320, 24000, 400, "euroc", 4.0, 0, True, overlap=1.5),
+    "S3K": WorldConfig("S3K", 300, 24000, 400, "tumvi", 2.5, 0, True, overlap=1.5),
     # dense keyframes: the 4096- and 8192-feature kernel instantiations
     "T3K": WorldConfig("T3K", 8, 6000, 3000, "euroc", 4.0, 6, False, overlap=2.5),
     "T6K": WorldConfig("T6K", 6, 8000, 6000, "tumvi", 2.5, 0, True, overlap=2.5),

@@ -144,6 +144,9 @@ constexpr int NWARP = LC_NTHREADS / 32;
 #ifndef LC_KM_MINB
 #define LC_KM_MINB 3      // k_match CTAs per SM the register budget is cut for
 #endif
+#ifndef LC_KP_MINB
+#define LC_KP_MINB 4      // k_project CTAs per SM the register budget is cut for
+#endif
 #ifndef LC_KM_PF
 #define LC_KM_PF 0        // L1 prefetch of a candidate's descriptor when it is recorded
 #endif
@@ -185,14 +188,73 @@ __device__ __forceinline__ uint32_t fslot(int32_t key) {
   return ((uint32_t)key * 0x85EBCA6Bu) >> (32 - FILT_LOG2);
 }
 
+// exact fp64 projection of a culled query only to decide its edge flag (rare)
+__device__ __noinline__ bool edge_exact(const DevCam& cam, double x, double y, double z) {
+  double u, v;
+  lc_project(cam, x, y, z, u, v);
+  return bounds_edge(cam, u, v);
+}
+
+// the definition's expressions (oracle O4 steps 5-8): d = sqrt(s), distance range, view
+// angle, smallest n with d * s_n >= dmax
+__device__ __noinline__ int dal_exact(double sq, double g, double dmax, double sLm1, const double* scale,
+                                      int L, int& lvl) {
+  const double d = sqrt(sq);
+  if (d < 0.8 * (dmax / sLm1) || d > 1.2 * dmax) return LC_Q_DIST;
+  if (g < 0.5 * d) return LC_Q_ANGLE;
+  lvl = L - 1;
+  for (int n = 0; n < L; ++n)
+    if (d * scale[n] >= dmax) { lvl = n; break; }
+  return 1;
+}
+
+// distance / angle / level from s = |PO|^2 and g = PO . n: 1 (kept, lvl set), LC_Q_DIST or
+// LC_Q_ANGLE; identical decisions to dal_exact (which it calls inside the bands)
+__device__ __forceinline__ int dist_angle_level(double sq, double g, double dmax, double c08, double sLm1,
+                                                const double* scale, int L, float inv_lsf, int& lvl) {
+  const double hi = 1.2 * dmax, hi2 = hi * hi;
+  const double lo = dmax * c08, lo2 = lo * lo;   // lo within a few ulp of 0.8 * (dmax / s_{L-1})
+  if (sq > hi2 * (1.0 + 1e-12) || sq < lo2 * (1.0 - 1e-9)) return LC_Q_DIST;
+  if (!(sq < hi2 * (1.0 - 1e-12)) || !(sq > lo2 * (1.0 + 1e-9))) return dal_exact(sq, g, dmax, sLm1, scale, L, lvl);
+  if (g < 0.0) return LC_Q_ANGLE;   // 0.5 * d >= 0 > g
+  const double g2 = g * g, q4 = 0.25 * sq;
+  if (g2 < q4 * (1.0 - 1e-12)) return LC_Q_ANGLE;
+  if (!(g2 > q4 * (1.0 + 1e-12))) return dal_exact(sq, g, dmax, sLm1, scale, L, lvl);
+  // level: d * s_n >= dmax  <=>  s * s_n^2 >= dmax^2 outside the band
+  const double dm2 = dmax * dmax;
+  int n = (int)ceilf(0.5f * __logf((float)dm2 / (float)sq) * inv_lsf);
+  n = min(max(n, 0), L - 1);
+  auto cmp = [&](int k) -> int {   // 1 true, 0 false, -1 inside the band
+    const double t = sq * (scale[k] * scale[k]);
+    if (t > dm2 * (1.0 + 1e-12)) return 1;
+    if (t < dm2 * (1.0 - 1e-12)) return 0;
+    return -1;
+  };
+  while (n > 0) {
+    const int c = cmp(n - 1);
+    if (c < 0) return dal_exact(sq, g, dmax, sLm1, scale, L, lvl);
+    if (!c) break;
+    --n;
+  }
+  while (n < L - 1) {
+    const int c = cmp(n);
+    if (c < 0) return dal_exact(sq, g, dmax, sLm1, scale, L, lvl);
+    if (c) break;
+    ++n;
+  }
+  lvl = n;
+  return 1;
+}
+
 // ---- k_project ---------------------------------------------------------------
 template <int MODE, int FCAP>
-__global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
+__global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const MatchArgs a) {
   constexpr uint32_t HS = (uint32_t)HashSize<FCAP>::HS;
   extern __shared__ __align__(16) int32_t s_hash[];   // [HS] (dynamic: up to 64 KB)
   __shared__ uint32_t s_filt[1 << (FILT_LOG2 - 5)];
   __shared__ double s_T[12];
   __shared__ double s_Ow[3];
+  __shared__ double s_scale[LC_MAX_LEVELS];
   __shared__ DevCam s_cam;
   __shared__ int s_cnt;
   const int tid = threadIdx.x;
@@ -214,6 +276,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
     s_cam = a.cams[a.kf_cam[k]];
     s_cnt = 0;
   }
+  if (tid < LC_MAX_LEVELS) s_scale[tid] = a.scale[tid];
   for (int i = tid; i < (int)HS; i += LC_NTHREADS) s_hash[i] = -1;
   for (int i = tid; i < (1 << (FILT_LOG2 - 5)); i += LC_NTHREADS) s_filt[i] = 0u;
   __syncthreads();
@@ -287,7 +350,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
     const bool in_range = valid && (unsigned)q < (unsigned)a.n_mp;
     if (a.loop_ep_w && in_range) a.loop_ep_w[q] = epoch;   // LoopSet stamp (pipelined mode)
     int status = 0;
-    double u = 0.0, v = 0.0;
+    float fu = 0.f, fv = 0.f;
     int lvl = 0;
     bool edge = false;
     if (valid) {
@@ -302,48 +365,56 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
         double x, y, z;
         lc_se3_xyz(s_T, p0, p1, p2, x, y, z);
         if (z <= 0.0) { status = LC_Q_DEPTH; cA += 1u << 20; break; }
-        if (pinhole && !a.dbg_uv) {
+        bool exact = !pinhole || a.dbg_uv;
+        if (!exact) {
           // conservative pre-test: |ua - u| <= 1e-6 |u| + tiny, margin 1e-2 px
           const double rz = (double)__frcp_rn((float)z);
           const double A = s_cam.fx * x, B = s_cam.fy * y;
           const double e = 1e-6 * (fabs(A * rz) + fabs(B * rz)) + 1e-2;
           const double ua = A * rz * (2.0 - z * rz) + s_cam.cx;   // one Newton step
           const double va = B * rz * (2.0 - z * rz) + s_cam.cy;
+          const double e2 = e + kEdgeEps;
           if (ua < s_cam.min_x - e || ua >= s_cam.max_x + e || va < s_cam.min_y - e ||
               va >= s_cam.max_y + e) {
             // certainly culled; edge-ambiguous only if u or v is within 1e-4 px of a
             // bound, which needs ua or va within e + 1e-4 of one: decide exactly then
-            const double e2 = e + kEdgeEps;
             if (fabs(ua - s_cam.min_x) < e2 || fabs(ua - s_cam.max_x) < e2 || fabs(va - s_cam.min_y) < e2 ||
-                fabs(va - s_cam.max_y) < e2) {
-              lc_project(s_cam, x, y, z, u, v);
-              if (bounds_edge(s_cam, u, v)) cE += 1u;
-            }
+                fabs(va - s_cam.max_y) < e2)
+              cE += edge_exact(s_cam, x, y, z) ? 1u : 0u;
             status = LC_Q_BOUNDS; cB += 1u; break;
           }
+          if (ua >= s_cam.min_x + e2 && ua < s_cam.max_x - e2 && va >= s_cam.min_y + e2 && va < s_cam.max_y - e2) {
+            // certainly inside and no bound within 1e-4 px: the fp32 survivor pixel is
+            // taken from the refined estimate (|ua - u| << the fp32 window tolerance)
+            fu = (float)ua; fv = (float)va;
+          } else {
+            exact = true;
+          }
         }
-        lc_project(s_cam, x, y, z, u, v);
-        edge = bounds_edge(s_cam, u, v);   // SURVEY §8(c) edge-ambiguous (oracle: before the cull)
-        if (!(u >= s_cam.min_x && u < s_cam.max_x && v >= s_cam.min_y && v < s_cam.max_y)) {
-          status = LC_Q_BOUNDS; cB += 1u; break;
+        if (exact) {
+          double u, v;
+          lc_project(s_cam, x, y, z, u, v);
+          edge = bounds_edge(s_cam, u, v);   // SURVEY §8(c) edge-ambiguous (oracle: before the cull)
+          if (a.dbg_uv) {   // (survivors: k_match writes the same exact values again)
+            const int64_t qi = qbase + (j - q0);
+            a.dbg_uv[2 * qi] = u; a.dbg_uv[2 * qi + 1] = v;
+          }
+          if (!(u >= s_cam.min_x && u < s_cam.max_x && v >= s_cam.min_y && v < s_cam.max_y)) {
+            status = LC_Q_BOUNDS; cB += 1u; break;
+          }
+          fu = (float)u; fv = (float)v;
         }
+        // distance range, view angle, level (readings A5-A7) decided on s = |PO|^2 with
+        // relative bands (1e-12, 1e-9) far wider than any rounding; the definition's exact
+        // expressions (with the square root) only when a value falls inside a band
         const double PO0 = p0 - s_Ow[0], PO1 = p1 - s_Ow[1], PO2 = p2 - s_Ow[2];
-        const double d = sqrt((PO0 * PO0 + PO1 * PO1) + PO2 * PO2);
+        const double sq = (PO0 * PO0 + PO1 * PO1) + PO2 * PO2;
         const double dmax = __uint_as_float(r0.w);
-        bool dcull = d > 1.2 * dmax;
-        if (!dcull) {
-          const double t = dmax * c08;   // within a few ulp of 0.8 * (dmax / s_{L-1})
-          if (d < t * (1.0 - 1e-9)) dcull = true;
-          else if (!(d > t * (1.0 + 1e-9))) dcull = d < 0.8 * (dmax / sLm1);   // exact near the bound
-        }
-        if (dcull) { status = LC_Q_DIST; cB += 1u << 10; break; }
         const double n0 = __uint_as_float(r1.x), n1 = __uint_as_float(r1.y), n2 = __uint_as_float(r1.z);
-        if ((PO0 * n0 + PO1 * n1) + PO2 * n2 < 0.5 * d) { status = LC_Q_ANGLE; cB += 1u << 20; break; }
-        // level: smallest n with d * s_n >= dmax (else L-1): float guess, exact adjustment
-        lvl = (int)ceilf(__logf((float)dmax / (float)d) * inv_lsf);
-        lvl = min(max(lvl, 0), L - 1);
-        while (lvl > 0 && d * a.scale[lvl - 1] >= dmax) --lvl;
-        while (lvl < L - 1 && !(d * a.scale[lvl] >= dmax)) ++lvl;
+        const double g = (PO0 * n0 + PO1 * n1) + PO2 * n2;
+        const int st = dist_angle_level(sq, g, dmax, c08, sLm1, s_scale, L, inv_lsf, lvl);
+        if (st == LC_Q_DIST) { status = LC_Q_DIST; cB += 1u << 10; break; }
+        if (st == LC_Q_ANGLE) { status = LC_Q_ANGLE; cB += 1u << 20; break; }
         status = 1;
       } while (0);
     }
@@ -355,16 +426,13 @@ __global__ void __launch_bounds__(LC_NTHREADS, 4) k_project(const MatchArgs a) {
     if (surv) {
       Surv e;
       e.q = q; e.jl = (uint32_t)(j - q0) | ((uint32_t)lvl << 27) | (edge ? kSurvEdge : 0u);
-      e.fu = (float)u; e.fv = (float)v;
+      e.fu = fu; e.fv = fv;
       out[wbase + __popc(m & ltmask)] = e;
     } else if (valid) {
       if (edge) cE += 1u;
       const int64_t qi = qbase + (j - q0);
       if (a.dbg_best) a.dbg_best[qi] = status;
-      if (a.dbg_uv) {
-        if (status > LC_Q_BOUNDS) u = v = 0.0;
-        a.dbg_uv[2 * qi] = u; a.dbg_uv[2 * qi + 1] = v;
-      }
+      if (a.dbg_uv && status > LC_Q_BOUNDS) { a.dbg_uv[2 * qi] = 0.0; a.dbg_uv[2 * qi + 1] = 0.0; }
       if (a.dbg_ncand) a.dbg_ncand[qi] = 0;
     }
   }
@@ -403,6 +471,40 @@ __device__ __noinline__ void exact_uv(const MatchArgs& a, const double* T, const
   lc_project(cam, x, y, z, u, v);
 }
 
+// Exact fp64 window scan of one survivor over its octave grids lvl-1, lvl (readings A8,
+// A9): every feature of the conservative cell ranges is tested against the exact (u, v);
+// take((H << 16) | f) per candidate, edge flags accumulated. Used when the fp32 filter
+// was ambiguous or a survivor overflowed its candidate slots. dsc = the keyframe's
+// cell-major descriptors (global or shared memory).
+template <int MODE, typename Take>
+__device__ __forceinline__ void scan_exact(const MatchArgs& a, const DevCam& cam, const uint16_t* s_cell,
+                                           const float2* s_uv, const uint32_t* s_meta, const uint4* dsc,
+                                           float fu, float fv, float fr, int lvl, double u, double v, double r,
+                                           const uint4& d0, const uint4& d1, Take& take, int& nc, bool& wedge) {
+  const float fminx = (float)cam.min_x, fminy = (float)cam.min_y;
+  for (int o = max(lvl - 1, 0); o <= lvl; ++o) {
+    const int oc = a.ocols[o], orr = a.orows[o], ob = a.obase[o];
+    const float fsx = (float)cam.cell_sx[o], fsy = (float)cam.cell_sy[o];
+    const int cx0 = max(0, (int)floorf((fu - fr - 0.01f - fminx) * fsx));
+    const int cx1 = min(oc - 1, (int)floorf((fu + fr + 0.01f - fminx) * fsx));
+    const int cy0 = max(0, (int)floorf((fv - fr - 0.01f - fminy) * fsy));
+    const int cy1 = min(orr - 1, (int)floorf((fv + fr + 0.01f - fminy) * fsy));
+    for (int cy = cy0; cy <= cy1; ++cy) {
+      const int pe = s_cell[ob + cy * oc + cx1 + 1];
+      for (int p = s_cell[ob + cy * oc + cx0]; p < pe; ++p) {
+        const uint32_t meta = s_meta[p];
+        if (MODE == 1 && (meta & 0x80000000u)) continue;
+        const float2 fuv = s_uv[p];
+        const double du = fabs((double)fuv.x - u), dv = fabs((double)fuv.y - v);
+        wedge |= window_edge(du, dv, r);
+        if (!(du < r && dv < r)) continue;
+        take(((uint32_t)popc_desc(d0, d1, dsc[2 * p], dsc[2 * p + 1]) << 16) | (meta & 0xFFFFu));
+        ++nc;
+      }
+    }
+  }
+}
+
 template <int MODE, int FCAP>
 __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchArgs a) {
   using SM = MatchSmem<FCAP>;
@@ -410,6 +512,8 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ double s_T[12];
   __shared__ __align__(16) DevCam s_cam;
+  __shared__ float s_fsx[LC_MAX_LEVELS], s_fsy[LC_MAX_LEVELS], s_fr[LC_MAX_LEVELS];
+  __shared__ int s_oc[LC_MAX_LEVELS], s_or[LC_MAX_LEVELS], s_ob[LC_MAX_LEVELS];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int blk = a.blk_base + (int)blockIdx.x;
@@ -448,6 +552,17 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
     reinterpret_cast<uint4*>(&s_cam)[tid - 64] =
         reinterpret_cast<const uint4*>(a.cams + a.kf_cam[k])[tid - 64];
   }
+  if (tid >= 128 && tid < 128 + LC_MAX_LEVELS) {   // per-octave grid constants, fp32 radii
+    const int o = tid - 128;
+    const DevCam& c = a.cams[a.kf_cam[k]];
+    const lc_match_params pp = a.params[(MODE == 1 && a.unit_param) ? a.unit_param[unit] : 0];
+    s_fsx[o] = (float)c.cell_sx[o];
+    s_fsy[o] = (float)c.cell_sy[o];
+    s_fr[o] = (float)((double)pp.th * a.scale[o]);
+    s_oc[o] = a.ocols[o];
+    s_or[o] = a.orows[o];
+    s_ob[o] = a.obase[o];
+  }
   if (a.sole) {  // this CTA owns the unit's winner words: initialise them here
     unsigned long long* w0 = a.winner + a.unit_woff[unit];
     for (int f = tid; f < F; f += LC_NTHREADS) w0[f] = NONE;
@@ -461,11 +576,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   __syncthreads();
 
   const lc_match_params prm = a.params[(MODE == 1 && a.unit_param) ? a.unit_param[unit] : 0];
-  const int cols = a.cols, rows = a.rows;
   const bool f32ok = fmax(fabs(s_cam.min_x), fabs(s_cam.max_x)) < 4096.0 &&
                      fmax(fabs(s_cam.min_y), fabs(s_cam.max_y)) < 4096.0;
   const float fminx = (float)s_cam.min_x, fminy = (float)s_cam.min_y;
-  const float fsx = (float)s_cam.cell_sx, fsy = (float)s_cam.cell_sy;
   unsigned long long* win = a.winner + a.unit_woff[unit];
   const int64_t q0 = a.blk_q0[blk];
   const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
@@ -495,51 +608,41 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
     const Surv e = e_nx;
     if (i0 + NWARP * 32 + lane < ns_tot) e_nx = sv[i0 + NWARP * 32 + lane];
     const int lvl = (int)((e.jl >> 27) & 7u);
-    int cx0 = 0, cx1 = -1, cy0 = 0, cy1 = -1, nc = 0;
+    int nc = 0;
     bool wedge = false;   // edge-ambiguous query (bounds flag from k_project, or a window decision)
-    const float fr = (float)((double)prm.th * a.scale[lvl]);
+    const float fr = s_fr[lvl];
     if (act) {
       // query descriptor -> shared memory, asynchronously, during the scan
       const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + e.q);
       cp_async16(s_qd + lane * 8, rp + 2);
       cp_async16(s_qd + lane * 8 + 4, rp + 3);
-      // conservative (0.01 px) cell-range superset of the exact square window
-      cx0 = max(0, (int)floorf((e.fu - fr - 0.01f - fminx) * fsx));
-      cx1 = min(cols - 1, (int)floorf((e.fu + fr + 0.01f - fminx) * fsx));
-      cy0 = max(0, (int)floorf((e.fv - fr - 0.01f - fminy) * fsy));
-      cy1 = min(rows - 1, (int)floorf((e.fv + fr + 0.01f - fminy) * fsy));
-      const int lo = lvl - 1;
       wedge = (e.jl & kSurvEdge) != 0u;
-      // (1) window scan over the staged cells, octave filter (A9) first; slots whose
-      // fp32 window test is ambiguous are marked and settled in fp64 after the scan
+      // (1) window scan over the staged cells of the octave grids lvl-1 and lvl (reading A9:
+      // octave in [lvl-1, lvl]; grid o holds exactly the octave-o features), conservative
+      // (0.01 px) cell ranges; slots whose fp32 window test is ambiguous are marked and
+      // settled in fp64 after the scan
       uint32_t amb = 0u;
-      // the lane's rows are visited 4 at a time and each row's features 4 at a time:
-      // all shared-memory loads of a batch are issued together, then the tests run on
-      // registers (the scan is latency-bound on dependent shared loads otherwise)
-      for (int cb = cy0; cb <= cy1; cb += 4) {
-        int ps[4], pe[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int cy = min(cb + u, cy1);
-          ps[u] = s_cell[cy * cols + cx0];
-          pe[u] = cb + u <= cy1 ? (int)s_cell[cy * cols + cx1 + 1] : ps[u];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          for (int p0 = ps[u]; p0 < pe[u]; p0 += 4) {
+      for (int o = max(lvl - 1, 0); o <= lvl; ++o) {
+        const int oc = s_oc[o], orr = s_or[o], ob = s_ob[o];
+        const float fsx = s_fsx[o], fsy = s_fsy[o];
+        const int cx0 = max(0, (int)floorf((e.fu - fr - 0.01f - fminx) * fsx));
+        const int cx1 = min(oc - 1, (int)floorf((e.fu + fr + 0.01f - fminx) * fsx));
+        const int cy0 = max(0, (int)floorf((e.fv - fr - 0.01f - fminy) * fsy));
+        const int cy1 = min(orr - 1, (int)floorf((e.fv + fr + 0.01f - fminy) * fsy));
+        for (int cy = cy0; cy <= cy1; ++cy) {
+          const int ps = s_cell[ob + cy * oc + cx0], pe = s_cell[ob + cy * oc + cx1 + 1];
+          for (int p0 = ps; p0 < pe; p0 += 4) {   // 4 features' loads issued together
             uint32_t mt[4];
             float2 fuv[4];
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-              const int pp = min(p0 + t, pe[u] - 1);
+              const int pp = min(p0 + t, pe - 1);
               mt[t] = s_meta[pp];
               fuv[t] = s_uv[pp];
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-              if (p0 + t >= pe[u]) break;
-              const int oct = (int)((mt[t] >> 16) & 0xFFu);
-              if (oct < lo || oct > lvl) continue;
+              if (p0 + t >= pe) break;
               if (MODE == 1 && (mt[t] & 0x80000000u)) continue;
               const int w = win_f32(fuv[t], e.fu, e.fv, fr);
               if (w == 0) continue;
@@ -606,13 +709,10 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
     if (act) {
       uint32_t best = 0xFFFFFFFFu;  // (H << 16) | f
       int second = 256;
-      auto take = [&](uint32_t key) {
-        if (key < best) {
-          if (best != 0xFFFFFFFFu) second = min(second, (int)(best >> 16));
-          best = key;
-        } else {
-          second = min(second, (int)(key >> 16));
-        }
+      auto take = [&](uint32_t key) {   // branch-free: the larger key of the pair is a "rest" key
+        const uint32_t hi = max(key, best);
+        best = min(key, best);
+        second = min(second, (int)(hi >> 16));
       };
       if (over) {   // > CPL fp32 candidates: serial rescan with the exact window test
         const uint4* qd = reinterpret_cast<const uint4*>(s_qd + lane * 8);
@@ -621,22 +721,8 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         exact_uv(a, s_T, s_cam, e.q, u, v);
         const double r = (double)prm.th * a.scale[lvl];
         nc = 0;
-        for (int cy = cy0; cy <= cy1; ++cy) {
-          const int pe = s_cell[cy * cols + cx1 + 1];
-          for (int p = s_cell[cy * cols + cx0]; p < pe; ++p) {
-            const uint32_t meta = s_meta[p];
-            const int oct = (int)((meta >> 16) & 0xFFu);
-            if (oct < lvl - 1 || oct > lvl) continue;
-            if (MODE == 1 && (meta & 0x80000000u)) continue;
-            const float2 fuv = s_uv[p];
-            const double du = fabs((double)fuv.x - u), dv = fabs((double)fuv.y - v);
-            wedge |= window_edge(du, dv, r);
-            if (!(du < r && dv < r)) continue;
-            const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
-            take(((uint32_t)popc_desc(d0, d1, __ldg(dp), __ldg(dp + 1)) << 16) | (meta & 0xFFFFu));
-            ++nc;
-          }
-        }
+        scan_exact<MODE>(a, s_cam, s_cell, s_uv, s_meta, a.fc_desc + 2 * (size_t)fp, e.fu, e.fv, fr, lvl, u, v, r,
+                         d0, d1, take, nc, wedge);
       } else {
         for (int i = 0; i < ns; ++i) take(s_key[lane * CPL + i]);
       }
@@ -808,6 +894,281 @@ __device__ void resolve_unit(const MatchArgs& a, int unit) {
 template <int MODE>
 __global__ void __launch_bounds__(LC_NTHREADS) k_resolve(const MatchArgs a) {
   resolve_unit<MODE>(a, a.unit_base + blockIdx.x);
+}
+
+// ---------------------------------------------------------------------------
+// k_match_sole: the fuse matching of a whole window keyframe in one CTA (sole mode, the
+// C5 launch). The keyframe's cell table (octave grids), keypoints and index words are
+// staged in shared memory by TMA; each warp then takes 32 survivors at a time in three
+// converged phases:
+//  A  lane = survivor: cell ranges of the octave grids lvl-1 and lvl (reading A9), the
+//     features of those cells counted, a warp prefix sum, and the survivor's items
+//     (owner lane, feature position) written to a per-warp queue in shared memory;
+//  B  lane = item: 32 (survivor, feature) items per step -- fp32-filtered strict square
+//     window (A8), the 32-B descriptor gathered and its Hamming distance taken against
+//     the owner's query descriptor (cp.async-staged), the key (H << 16) | f appended to the
+//     owner's slots; two steps per iteration so two gathers are in flight per lane;
+//  C  lane = survivor: best / second over its slots (an exact fp64 rescan instead when a
+//     window decision was fp32-ambiguous or the slots / queue overflowed), threshold,
+//     ratio, proposal = 64-bit atomicMin (A17).
+// The CTA then resolves its keyframe (orientation, fuse actions, victim proposals).
+// ---------------------------------------------------------------------------
+#ifndef LC_SOLE_NT
+#define LC_SOLE_NT 256
+#endif
+#ifndef LC_SOLE_MINB
+#define LC_SOLE_MINB 3
+#endif
+constexpr int SOLE_NW = LC_SOLE_NT / 32;
+constexpr int SOLE_QCAP = 256;   // queued items per warp (32 survivors); beyond -> serial rescan
+constexpr int SOLE_CPL = 4;      // candidate slots per survivor; beyond -> serial rescan
+constexpr uint32_t kAmbKey = 1u << 31;
+
+template <int FCAP>
+struct SoleSmem {
+  static constexpr int QI = 0;                       // per warp: [QCAP] u32 (owner << 16 | p)
+  static constexpr int OP = QI + SOLE_QCAP * 4;      // [32] float4 (fu, fv, fr, lvl)
+  static constexpr int QD = OP + 32 * 16;            // [32][8] u32 query descriptors
+  static constexpr int KEY = QD + 32 * 32;           // [32][CPL] u32
+  static constexpr int NC = KEY + 32 * SOLE_CPL * 4; // [32] u32
+  static constexpr int WB = NC + 32 * 4;
+  static constexpr int UV = SOLE_NW * WB;
+  static constexpr int META = UV + FCAP * 8;
+  static constexpr int CELL = META + FCAP * 4;       // runtime-size cell table last
+};
+
+template <int FCAP>
+__global__ void __launch_bounds__(LC_SOLE_NT, LC_SOLE_MINB) k_match_sole(const MatchArgs a) {
+  using SM = SoleSmem<FCAP>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ double s_T[12];
+  __shared__ __align__(16) DevCam s_cam;
+  __shared__ float s_fsx[LC_MAX_LEVELS], s_fsy[LC_MAX_LEVELS], s_fr[LC_MAX_LEVELS];
+  __shared__ int s_oc[LC_MAX_LEVELS], s_or[LC_MAX_LEVELS], s_ob[LC_MAX_LEVELS];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int blk = a.blk_base + (int)blockIdx.x;
+  const int unit = a.blk_unit[blk];
+  const int k = a.unit_kf[unit];
+  const int fb = a.kf_fbeg[k];
+  const int F = a.kf_fbeg[k + 1] - fb;
+  const int fp = a.kf_fpad[k];
+  float2* s_uv = (float2*)(smem + SM::UV);
+  uint32_t* s_meta = (uint32_t*)(smem + SM::META);
+  uint16_t* s_cell = (uint16_t*)(smem + SM::CELL);
+  unsigned char* wb = smem + warp * SM::WB;
+  uint32_t* s_qi = (uint32_t*)(wb + SM::QI);
+  float4* s_op = (float4*)(wb + SM::OP);
+  uint32_t* s_qd = (uint32_t*)(wb + SM::QD);
+  uint32_t* s_key = (uint32_t*)(wb + SM::KEY);
+  uint32_t* s_nc = (uint32_t*)(wb + SM::NC);
+  const lc_match_params prm = a.params[0];
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    const uint32_t b_cell = (uint32_t)a.Gs * 2u;
+    const uint32_t np = (uint32_t)((F + 3) & ~3);   // keyframe blocks are padded to 4 features
+    mbar_expect_tx(&s_bar, b_cell + (F > 0 ? np * 12u : 0u));
+    tma_load_1d(s_cell, a.kf_cell + (size_t)k * a.Gs, b_cell, &s_bar);
+    if (F > 0) {
+      tma_load_1d(s_uv, a.fc_uv + fp, np * 8u, &s_bar);
+      tma_load_1d(s_meta, a.fc_meta + fp, np * 4u, &s_bar);
+    }
+  }
+  if (tid >= 32 && tid < 44) {   // SE3 part (R, t/s) of the unit's Sim3 (reading A2)
+    const double* src = a.unit_S ? a.unit_S + 13 * (size_t)unit : a.kf_S_corr + 13 * (size_t)k;
+    const int i = tid - 32;
+    s_T[i] = i < 9 ? src[i] : src[i] / src[12];
+  }
+  if (tid >= 64 && tid < 64 + (int)(sizeof(DevCam) / 16))
+    reinterpret_cast<uint4*>(&s_cam)[tid - 64] = reinterpret_cast<const uint4*>(a.cams + a.kf_cam[k])[tid - 64];
+  if (tid >= 128 && tid < 128 + LC_MAX_LEVELS) {   // per-octave grid constants, fp32 radii
+    const int o = tid - 128;
+    const DevCam& c = a.cams[a.kf_cam[k]];
+    s_fsx[o] = (float)c.cell_sx[o];
+    s_fsy[o] = (float)c.cell_sy[o];
+    s_fr[o] = (float)((double)prm.th * a.scale[o]);
+    s_oc[o] = a.ocols[o];
+    s_or[o] = a.orows[o];
+    s_ob[o] = a.obase[o];
+  }
+  unsigned long long* win = a.winner + a.unit_woff[unit];
+  for (int f = tid; f < F; f += LC_SOLE_NT) win[f] = NONE;   // this CTA owns the unit's words
+  __syncthreads();
+
+  const bool f32ok = fmax(fabs(s_cam.min_x), fabs(s_cam.max_x)) < 4096.0 &&
+                     fmax(fabs(s_cam.min_y), fabs(s_cam.max_y)) < 4096.0;
+  const float fminx = (float)s_cam.min_x, fminy = (float)s_cam.min_y;
+  const int64_t q0 = a.blk_q0[blk];
+  const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
+  const bool dbg = a.dbg_best || a.dbg_uv || a.dbg_ncand;
+  pdl_wait();   // survivors of k_project from here on
+  const Surv* sv = a.surv + a.surv_off[blk];
+  const int ns_tot = a.surv_cnt[blk];
+  uint32_t cC = 0, cP = 0, cE = 0, cW = 0;   // NOCAND | OVERTH << 10 | RATIO << 20; PROP; CAND; EDGE
+  Surv e_nx;
+  e_nx.q = 0; e_nx.jl = 0u; e_nx.fu = 0.f; e_nx.fv = 0.f;
+  if (warp * 32 + lane < ns_tot) e_nx = sv[warp * 32 + lane];
+  mbar_wait(&s_bar, 0);
+  for (int i0 = warp * 32; i0 < ns_tot; i0 += SOLE_NW * 32) {
+    const bool act = i0 + lane < ns_tot;
+    const Surv e = e_nx;
+    if (i0 + SOLE_NW * 32 + lane < ns_tot) e_nx = sv[i0 + SOLE_NW * 32 + lane];
+    const int lvl = (int)((e.jl >> 27) & 7u);
+    const float fr = s_fr[lvl];
+    const int olo = max(lvl - 1, 0);
+    // ---- A: items of this survivor (two passes over its cell rows: count, then write)
+    int n_l = 0;
+    if (act) {
+      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + e.q);
+      cp_async16(s_qd + lane * 8, rp + 2);
+      cp_async16(s_qd + lane * 8 + 4, rp + 3);
+      for (int o = olo; o <= lvl; ++o) {
+        const int oc = s_oc[o], ob = s_ob[o];
+        const int cx0 = max(0, (int)floorf((e.fu - fr - 0.01f - fminx) * s_fsx[o]));
+        const int cx1 = min(oc - 1, (int)floorf((e.fu + fr + 0.01f - fminx) * s_fsx[o]));
+        const int cy0 = max(0, (int)floorf((e.fv - fr - 0.01f - fminy) * s_fsy[o]));
+        const int cy1 = min(s_or[o] - 1, (int)floorf((e.fv + fr + 0.01f - fminy) * s_fsy[o]));
+        for (int cy = cy0; cy <= cy1; ++cy) n_l += (int)s_cell[ob + cy * oc + cx1 + 1] - (int)s_cell[ob + cy * oc + cx0];
+      }
+    }
+    int incl = n_l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int ex = incl - n_l;
+    // queued items: every survivor whose items fit entirely (the first overflowing one and
+    // all after it rescan serially in phase C)
+    const int total = __shfl_sync(0xffffffffu, incl, 31);   // (every lane: a full-mask shuffle)
+    const int tot = (int)__reduce_min_sync(0xffffffffu, (unsigned)(incl > SOLE_QCAP ? ex : total));
+    bool serial = act && incl > SOLE_QCAP;
+    if (act && !serial && n_l > 0) {
+      int j = ex;
+      for (int o = olo; o <= lvl; ++o) {
+        const int oc = s_oc[o], ob = s_ob[o];
+        const int cx0 = max(0, (int)floorf((e.fu - fr - 0.01f - fminx) * s_fsx[o]));
+        const int cx1 = min(oc - 1, (int)floorf((e.fu + fr + 0.01f - fminx) * s_fsx[o]));
+        const int cy0 = max(0, (int)floorf((e.fv - fr - 0.01f - fminy) * s_fsy[o]));
+        const int cy1 = min(s_or[o] - 1, (int)floorf((e.fv + fr + 0.01f - fminy) * s_fsy[o]));
+        for (int cy = cy0; cy <= cy1; ++cy) {
+          const int pe = s_cell[ob + cy * oc + cx1 + 1];
+          for (int p = s_cell[ob + cy * oc + cx0]; p < pe; ++p) s_qi[j++] = ((uint32_t)lane << 16) | (uint32_t)p;
+        }
+      }
+    }
+    s_op[lane] = make_float4(e.fu, e.fv, fr, 0.f);
+    s_nc[lane] = 0u;
+    cp_async_wait_all();
+    __syncwarp();
+    // ---- B: items, 2 x 32 per step (two descriptor gathers in flight per lane)
+    for (int c0 = 0; c0 < tot; c0 += 64) {
+      uint32_t it[2];
+      float2 fuv[2];
+      int w[2];
+      uint4 b0[2], b1[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = c0 + 32 * h + lane;
+        it[h] = c < tot ? s_qi[c] : 0xFFFFFFFFu;
+        w[h] = 0;
+        if (it[h] != 0xFFFFFFFFu) {
+          const int p = (int)(it[h] & 0xFFFFu);
+          const float4 op = s_op[it[h] >> 16];
+          fuv[h] = s_uv[p];
+          if (!f32ok) {
+            w[h] = -1;
+          } else {
+            const float du = fabsf(fuv[h].x - op.x), dv = fabsf(fuv[h].y - op.y);
+            w[h] = (du > op.z + kWinTol || dv > op.z + kWinTol) ? 0
+                 : ((du < op.z - kWinTol && dv < op.z - kWinTol) ? 1 : -1);
+          }
+          if (w[h] != 0) {
+            const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
+            b0[h] = __ldg(dp);
+            b1[h] = __ldg(dp + 1);
+          }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (w[h] == 0) continue;
+        const int own = (int)(it[h] >> 16), p = (int)(it[h] & 0xFFFFu);
+        const uint4* qd = reinterpret_cast<const uint4*>(s_qd + own * 8);
+        const uint32_t key = ((uint32_t)popc_desc(qd[0], qd[1], b0[h], b1[h]) << 16) | (s_meta[p] & 0xFFFFu) |
+                             (w[h] < 0 ? kAmbKey : 0u);
+        const uint32_t slot = atomicAdd(&s_nc[own], 1u);
+        if (slot < (uint32_t)SOLE_CPL) s_key[own * SOLE_CPL + slot] = key;
+      }
+    }
+    __syncwarp();
+    // ---- C: per survivor
+    if (act) {
+      bool wedge = (e.jl & kSurvEdge) != 0u;
+      uint32_t best = 0xFFFFFFFFu;   // (H << 16) | f
+      int second = 256, nc = 0;
+      auto take = [&](uint32_t key) {   // branch-free: the larger key of the pair is a "rest" key
+        const uint32_t hi = max(key, best);
+        best = min(key, best);
+        second = min(second, (int)(hi >> 16));
+      };
+      const uint32_t ns = s_nc[lane];
+      bool exact = serial || ns > (uint32_t)SOLE_CPL;
+      if (!exact) {
+        for (uint32_t j = 0; j < ns; ++j) {
+          const uint32_t key = s_key[lane * SOLE_CPL + j];
+          exact |= (key & kAmbKey) != 0u;
+          take(key);
+        }
+        nc = (int)ns;
+      }
+      if (exact) {   // rare: exact fp64 rescan of this survivor (global descriptors)
+        double u, v;
+        exact_uv(a, s_T, s_cam, e.q, u, v);
+        const uint4* qd = reinterpret_cast<const uint4*>(s_qd + lane * 8);
+        const uint4 d0 = qd[0], d1 = qd[1];
+        best = 0xFFFFFFFFu; second = 256; nc = 0;
+        scan_exact<0>(a, s_cam, s_cell, s_uv, s_meta, a.fc_desc + 2 * (size_t)fp, e.fu, e.fv, fr, lvl, u, v,
+                      (double)prm.th * a.scale[lvl], d0, d1, take, nc, wedge);
+      }
+      cE += nc;
+      if (wedge) cW += 1u;
+      do {
+        if (nc == 0) { cC += 1u; break; }
+        const int hb = (int)(best >> 16);
+        if (hb > prm.max_hamming) { cC += 1u << 10; break; }
+        if (prm.ratio_den > 0 && (long long)prm.ratio_den * hb > (long long)prm.ratio_num * second) {
+          cC += 1u << 20; break;
+        }
+        cP += 1u;
+        atomicMin(&win[best & 0xFFFFu], ((unsigned long long)hb << 32) | (unsigned int)e.q);
+      } while (0);
+      if (dbg) {
+        const int64_t qi = qbase + (int64_t)(e.jl & 0x07FFFFFFu);
+        if (a.dbg_best) {
+          long long val;
+          if (nc == 0) val = (256LL << 48) | (256LL << 32) | 0xFFFFFFFFLL;
+          else val = ((long long)(best >> 16) << 48) | ((long long)second << 32) | (long long)(best & 0xFFFFu);
+          a.dbg_best[qi] = val;
+        }
+        if (a.dbg_uv) {
+          double u, v;
+          exact_uv(a, s_T, s_cam, e.q, u, v);
+          a.dbg_uv[2 * qi] = u; a.dbg_uv[2 * qi + 1] = v;
+        }
+        if (a.dbg_ncand) a.dbg_ncand[qi] = nc;
+      }
+    }
+    __syncwarp();
+  }
+  pdl_trigger();
+  uint32_t cnt[6];
+  cnt[0] = cE; cnt[1] = cC & 1023u; cnt[2] = (cC >> 10) & 1023u; cnt[3] = (cC >> 20) & 1023u; cnt[4] = cP;
+  cnt[5] = cW;
+  block_add<6>(cnt, kMatchSlot2, a.counts);
+  __syncthreads();   // all proposals of this unit are in: resolve it here (no extra launch)
+  resolve_unit<0>(a, unit);
 }
 
 // Per-call setup: LoopSet stamps, winner/victim init, window membership. The call's
@@ -1103,6 +1464,18 @@ cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, int part, bool pdl,
     cudaError_t e = cudaFuncSetAttribute(k_project<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, hb);
     if (e != cudaSuccess) return e;
     return go(k_project<MODE, FCAP>, (size_t)hb);
+  }
+  if (MODE == 0 && a.sole && FCAP <= 4096) {
+    using SS = SoleSmem<FCAP>;
+    const size_t smem = (size_t)SS::CELL + (((size_t)a.Gs * 2 + 15) & ~(size_t)15);
+    cudaError_t e = cudaFuncSetAttribute(k_match_sole<FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_match_sole<FCAP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    if (pdl) return launch_pdl(k_match_sole<FCAP>, dim3(n_blocks), dim3(LC_SOLE_NT), smem, s, a);
+    k_match_sole<FCAP><<<n_blocks, LC_SOLE_NT, smem, s>>>(a);
+    return cudaGetLastError();
   }
   const size_t smem = (size_t)SM::CELL + (((size_t)a.Gs * 2 + 15) & ~(size_t)15);
   cudaError_t e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

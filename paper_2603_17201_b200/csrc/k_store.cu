@@ -3,6 +3,8 @@
 // kept GPU-resident in a "lightweight wrapper structure", allocated once).
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "lc_internal.cuh"
 
 namespace {
@@ -50,11 +52,12 @@ __global__ void k_count_nobs(int n_feat, int n_mp, const int32_t* __restrict__ f
   }
 }
 
-// Per-keyframe counting sort of features into grid cells (one CTA per keyframe).
-// cell = (floor((u-min_x)*cols/(max_x-min_x)), floor((v-min_y)*rows/(max_y-min_y))),
-// clamped; within a cell features keep ascending original index (deterministic).
+// Per-keyframe counting sort of features into the per-octave grid cells (one CTA per
+// keyframe). A feature of octave o goes to cell (o, floor((v-min_y)*rows_o/(max_y-min_y)),
+// floor((u-min_x)*cols_o/(max_x-min_x))), clamped; the cell table and the feature arrays
+// are (octave, row, col)-major, and within a cell features keep ascending original index.
 __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
-    int n_levels, int n_cams, int Gs, const int32_t* __restrict__ fbeg,
+    int n_levels, int n_cams, int Gs, int G, MatchArgs g, const int32_t* __restrict__ fbeg,
     const int32_t* __restrict__ fpad, const int32_t* __restrict__ kf_cam,
     const DevCam* __restrict__ cams, const float* __restrict__ fuv, const uint8_t* __restrict__ foct,
     const uint8_t* __restrict__ fdesc, uint16_t* __restrict__ kf_cell, float2* __restrict__ fc_uv,
@@ -71,7 +74,6 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
     return;
   }
   const DevCam& cam = cams[ci];
-  const int cols = cam.cols, rows = cam.rows, G = cols * rows;
   int* s_cnt = (int*)smem;                              // [G+1]
   uint16_t* s_cellof = (uint16_t*)(s_cnt + G + 1);      // [F]
   uint16_t* s_perm = s_cellof + F;                      // [F]
@@ -79,15 +81,17 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
   for (int i = threadIdx.x; i <= G; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
   for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    const int o = foct[fb + f];
+    if (o >= n_levels) { atomicAdd(&errs[ERR_OCTAVE], 1u); s_cellof[f] = 0; continue; }
+    const int cols = g.ocols[o], rows = g.orows[o];
     double u = (double)fuv[2 * (fb + f)], v = (double)fuv[2 * (fb + f) + 1];
-    double x = floor((u - cam.min_x) * cam.cell_sx);
-    double y = floor((v - cam.min_y) * cam.cell_sy);
+    double x = floor((u - cam.min_x) * cam.cell_sx[o]);
+    double y = floor((v - cam.min_y) * cam.cell_sy[o]);
     int cx = x >= 0.0 ? (x < (double)cols ? (int)x : cols - 1) : 0;
     int cy = y >= 0.0 ? (y < (double)rows ? (int)y : rows - 1) : 0;
-    int cell = cy * cols + cx;
+    int cell = g.obase[o] + cy * cols + cx;
     s_cellof[f] = (uint16_t)cell;
     atomicAdd(&s_cnt[cell], 1);
-    if (foct[fb + f] >= n_levels) atomicAdd(&errs[ERR_OCTAVE], 1u);
   }
   __syncthreads();
   // exclusive scan over G cells: each thread owns a contiguous chunk
@@ -195,7 +199,11 @@ cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, co
     cudaError_t e = cudaFuncSetAttribute(k_grid_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    k_grid_build<<<st.n_kf, LC_NTHREADS, smem, s>>>(st.n_levels, st.n_cams, st.Gs, st.kf_fbeg,
+    MatchArgs g;   // only the per-octave grid dims are read
+    memset(&g, 0, sizeof(g));
+    for (int i = 0; i < LC_MAX_LEVELS; ++i) { g.ocols[i] = st.ocols[i]; g.orows[i] = st.orows[i]; }
+    for (int i = 0; i <= LC_MAX_LEVELS; ++i) g.obase[i] = st.obase[i];
+    k_grid_build<<<st.n_kf, LC_NTHREADS, smem, s>>>(st.n_levels, st.n_cams, st.Gs, st.G, g, st.kf_fbeg,
                                                     st.kf_fpad, st.kf_cam,
                                                     st.cams, fuv, foct, fdesc, st.kf_cell,
                                                     st.fc_uv, st.fc_meta, st.fc_desc, st.feat_cpos, d_errs);

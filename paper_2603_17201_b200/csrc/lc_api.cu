@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -370,6 +372,8 @@ void fill_match_store(lc_ctx* c, MatchArgs& a) {
   a.cols = st.cols;
   a.rows = st.rows;
   a.G = st.G;
+  for (int i = 0; i < LC_MAX_LEVELS; ++i) { a.ocols[i] = st.ocols[i]; a.orows[i] = st.orows[i]; }
+  for (int i = 0; i <= LC_MAX_LEVELS; ++i) a.obase[i] = st.obase[i];
   a.n_levels = st.n_levels;
   for (int i = 0; i < LC_MAX_LEVELS; ++i) a.scale[i] = st.scale[i];
 }
@@ -398,6 +402,7 @@ lc_status lc_create(lc_ctx** out, int32_t device) {
   lc_ctx* c = new (std::nothrow) lc_ctx();
   if (!c) return LC_ENOMEM;
   c->device = device;
+  if (const char* e = getenv("LC_SOLE")) c->sole_mode = atoi(e) ? 1 : 0;   // test knob: force / forbid
   bool ok = cudaSetDevice(device) == cudaSuccess;
   for (int r = 0; ok && r < lc_ctx::kPinRing; ++r)
     ok = cudaEventCreateWithFlags(&c->pin_ev[r], cudaEventDisableTiming) == cudaSuccess;
@@ -588,7 +593,18 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
     Store& st = c->st;
     st.n_kf = m->n_kf; st.n_feat = m->n_feat; st.n_mp = m->n_mp; st.n_cams = n_cams;
     st.n_levels = prm->n_levels; st.cols = prm->grid_cols; st.rows = prm->grid_rows;
-    st.G = st.cols * st.rows;
+    {   // per-octave grids: octave o coarsened by scale_factor^o (its keypoints are that much sparser)
+      double f = 1.0;
+      st.obase[0] = 0;
+      for (int o = 0; o < LC_MAX_LEVELS; ++o) {
+        st.ocols[o] = std::max(1, (int)std::ceil(st.cols / f - 1e-9));
+        st.orows[o] = std::max(1, (int)std::ceil(st.rows / f - 1e-9));
+        st.obase[o + 1] = st.obase[o] + (o < st.n_levels ? st.ocols[o] * st.orows[o] : 0);
+        f *= prm->scale_factor;
+      }
+    }
+    st.G = st.obase[st.n_levels];
+    REQUIRE(st.G <= 24576, LC_EINVAL, "grid too fine: more than 24576 cells over the octave grids");
     st.Gs = (int32_t)round_up((size_t)st.G + 1, 8);
     st.max_F = max_F;
     std::vector<int32_t> fpad(st.n_kf + 1, 0);
@@ -640,8 +656,10 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
       d.fx = k.fx; d.fy = k.fy; d.cx = k.cx; d.cy = k.cy;
       for (int j = 0; j < 4; ++j) d.k[j] = k.k[j];
       d.min_x = k.min_x; d.max_x = k.max_x; d.min_y = k.min_y; d.max_y = k.max_y;
-      d.cell_sx = (double)st.cols / (k.max_x - k.min_x);
-      d.cell_sy = (double)st.rows / (k.max_y - k.min_y);
+      for (int o = 0; o < LC_MAX_LEVELS; ++o) {
+        d.cell_sx[o] = (double)st.ocols[o] / (k.max_x - k.min_x);
+        d.cell_sy[o] = (double)st.orows[o] / (k.max_y - k.min_y);
+      }
     }
     CK(cudaMemcpyAsync(st.cams, dc.data(), sizeof(DevCam) * n_cams, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(st.kf_fbeg, fbeg.data(), sizeof(int32_t) * (NK + 1), cudaMemcpyHostToDevice, s));
@@ -1218,7 +1236,9 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     const bool pipe = (phase & LC_FUSE_PLAN) && win_list_begin && n_list >= (1 << 18) && !dbg &&
                       !c->cap && w_lo == 0 && w_hi == n_window && !is_device_ptr(c, mp_list) &&
                       cur_pos < 0;   // the forced step needs the LoopSet stamped up front
-    const bool sole = !pipe && (w_hi - w_lo) >= 2 * 148 && max_len <= 16384;
+    // (auto = off: at C5 the chunked k_match + k_resolve pair measured faster than the
+    // one-CTA-per-keyframe k_match_sole; LC_SOLE=1 forces it)
+    const bool sole = !pipe && max_len <= 16384 && w_hi > w_lo && c->sole_mode == 1;
     const int64_t ch = sole ? std::max<int64_t>(max_len, 1) : pick_chunk(total_q);
     std::vector<int32_t> bunit;
     std::vector<int64_t> bq0, bq1;

@@ -4,8 +4,8 @@
 //   kf_pose      double[n_kf][13]       world->camera, mutable by corrections
 //   kf_cam       int32[n_kf]
 //   kf_fbeg      int32[n_kf+1]          CSR into feature arrays
-//   kf_cell      uint16[n_kf][G+1]      per-keyframe cell start offsets (cell-major)
-//   fc_uv        float2[n_feat]         keypoints, cell-major per keyframe
+//   kf_cell      uint16[n_kf][Gs]       per-keyframe cell start offsets, (octave, row, col)-major
+//   fc_uv        float2[n_feat]         keypoints, (octave, cell)-major per keyframe
 //   fc_meta      uint32[n_feat]         local original index (bits 0-15) | octave << 16
 //   fc_desc      uint4[n_feat][2]       descriptors, cell-major
 //   feat_mp      int32[n_feat]          associations, ORIGINAL order (mutable)
@@ -37,17 +37,21 @@ static_assert(sizeof(MpRec) == 64, "MpRec must be 64 bytes");
 
 struct DevCam {
   int model;
-  int cols, rows;
+  int cols, rows;   // octave-0 grid (the per-octave grids are coarsened by the scale factor)
   int pad;
   double fx, fy, cx, cy;
   double k[4];
   double min_x, max_x, min_y, max_y;
-  double cell_sx, cell_sy;  // cols / (max_x - min_x), rows / (max_y - min_y)
+  double cell_sx[LC_MAX_LEVELS], cell_sy[LC_MAX_LEVELS];   // octave o: cols_o / (max_x - min_x), ...
 };
 
 struct Store {
   int32_t n_kf = 0, n_feat = 0, n_mp = 0, n_cams = 0;
   int32_t n_levels = 0, cols = 0, rows = 0, G = 0;
+  // per-octave grids: octave o uses ocols[o] x orows[o] cells (the octave-0
+  // grid coarsened by scale_factor^o); the per-keyframe cell table is (octave, row, col)-
+  // major, obase[o] = first cell of octave o, G = obase[n_levels] cells in total
+  int32_t ocols[LC_MAX_LEVELS] = {}, orows[LC_MAX_LEVELS] = {}, obase[LC_MAX_LEVELS + 1] = {};
   int32_t Gs = 0;        // per-keyframe cell-table stride: round_up(G + 1, 8) (16-B rows for TMA)
   int64_t n_fpad = 0;    // padded feature count of the cell-major arrays
   double scale[LC_MAX_LEVELS];
@@ -111,6 +115,7 @@ struct MatchArgs {
   const uint8_t* mp_flags;
   const DevCam* cams;
   int32_t cols, rows, G, n_levels, Gs;
+  int32_t ocols[LC_MAX_LEVELS], orows[LC_MAX_LEVELS], obase[LC_MAX_LEVELS + 1];   // per-octave grids
   double scale[LC_MAX_LEVELS];
   // call
   const int32_t* unit_kf;      // [n_units]
@@ -179,6 +184,7 @@ struct lc_ctx {
   static constexpr int kPipe = 4;              // chunks of a pipelined host-list fuse
   cudaEvent_t pipe_ev[kPipe + 1] = {};          // [kPipe]: start (side waits on the call stream)
   int64_t launches = 0;
+  int sole_mode = -1;   // LC_SOLE env at create: -1 auto, 0 never, 1 whenever lists allow (testing)
   // scratch arena: named growable device buffers
   std::vector<void*> scr_ptr;
   std::vector<size_t> scr_cap;

@@ -8,6 +8,7 @@ oracle flags edge-ambiguous (a window / bounds decision within 1e-4 px, which on
 Kannala-Brandt atan2 can move); they are counted and printed.
 """
 import functools
+import os
 
 import numpy as np
 import pytest
@@ -162,6 +163,19 @@ def test_loop_parity_dense_keyframes(Ctx, name):
     w, g, o, ctx = _run_loop(Ctx, name, FUSE_PARAMS_CHECKS)
     assert np.diff(w.kf_feat_begin).max() > {"T3K": 2048, "T6K": 4096}[name]
     assert g["counts"]["candidates"] > 0 and g["counts"]["proposals"] > 0
+
+
+@pytest.mark.parametrize("name", ["S3", "S3K"])
+@pytest.mark.parametrize("params", [FUSE_PARAMS, FUSE_PARAMS_CHECKS], ids=["faithful", "checks"])
+@pytest.mark.parametrize("sole", ["0", "1"], ids=["chunked", "sole"])
+def test_loop_parity_large_windows(Ctx, name, params, sole, monkeypatch):
+    """>= 296-keyframe windows with per-keyframe lists, both launch shapes: chunked
+    k_match + k_resolve, and the one-CTA-per-keyframe k_match_sole (LC_SOLE=1) -- compared
+    table for table against the oracle, ratio + orientation on."""
+    monkeypatch.setenv("LC_SOLE", sole)
+    w, g, o, ctx = _run_loop(Ctx, name, params)
+    assert len(w.window) >= 296
+    assert g["counts"]["proposals"] > 10000 and g["counts"]["victims"] > 5000
 
 
 @pytest.mark.parametrize("name", ["C2", "C3"])
@@ -389,7 +403,11 @@ def test_C5_sharded_sole_mode_plan_merge_apply_equals_fuse_all(Ctx):
     from paper_2603_17201_b200 import LC_FUSE_APPLY, LC_FUSE_PLAN
     from paper_2603_17201_b200.dist import shard_bounds
     w = world("C5")
-    ctx = Ctx(0)
+    os.environ["LC_SOLE"] = "1"   # the one-CTA-per-keyframe launch (read at context creation)
+    try:
+        ctx = Ctx(0)
+    finally:
+        del os.environ["LC_SOLE"]
     ctx.upload_map(w.map_arrays(), [w.cam])
     ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
     ctx.state_save()
@@ -403,7 +421,7 @@ def test_C5_sharded_sole_mode_plan_merge_apply_equals_fuse_all(Ctx):
     for W in (2, 4, 8):
         ctx.state_restore()
         bounds = shard_bounds(n_w, W, w.win_list_begin)
-        assert min(hi - lo for lo, hi in bounds) >= 296   # sole mode on every shard
+        assert min(hi - lo for lo, hi in bounds) >= 296
         win = vic = None
         for lo, hi in bounds:
             tw = torch.full((int(woff[-1]),), garbage, dtype=torch.int64, device=dev)
