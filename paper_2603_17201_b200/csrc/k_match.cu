@@ -1465,7 +1465,7 @@ cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, int part, bool pdl,
     if (e != cudaSuccess) return e;
     return go(k_project<MODE, FCAP>, (size_t)hb);
   }
-  if (MODE == 0 && a.sole && FCAP <= 4096) {
+  if (MODE == 0 && a.sole == 2 && FCAP <= 4096) {
     using SS = SoleSmem<FCAP>;
     const size_t smem = (size_t)SS::CELL + (((size_t)a.Gs * 2 + 15) & ~(size_t)15);
     cudaError_t e = cudaFuncSetAttribute(k_match_sole<FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -402,7 +402,7 @@ lc_status lc_create(lc_ctx** out, int32_t device) {
   lc_ctx* c = new (std::nothrow) lc_ctx();
   if (!c) return LC_ENOMEM;
   c->device = device;
-  if (const char* e = getenv("LC_SOLE")) c->sole_mode = atoi(e) ? 1 : 0;   // test knob: force / forbid
+  if (const char* e = getenv("LC_SOLE")) c->sole_mode = atoi(e);   // test knob: 0 forbid, 1 force, 2 k_match_sole
   bool ok = cudaSetDevice(device) == cudaSuccess;
   for (int r = 0; ok && r < lc_ctx::kPinRing; ++r)
     ok = cudaEventCreateWithFlags(&c->pin_ev[r], cudaEventDisableTiming) == cudaSuccess;
@@ -1236,9 +1236,12 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     const bool pipe = (phase & LC_FUSE_PLAN) && win_list_begin && n_list >= (1 << 18) && !dbg &&
                       !c->cap && w_lo == 0 && w_hi == n_window && !is_device_ptr(c, mp_list) &&
                       cur_pos < 0;   // the forced step needs the LoopSet stamped up front
-    // (auto = off: at C5 the chunked k_match + k_resolve pair measured faster than the
-    // one-CTA-per-keyframe k_match_sole; LC_SOLE=1 forces it)
-    const bool sole = !pipe && max_len <= 16384 && w_hi > w_lo && c->sole_mode == 1;
+    // sole mode: one k_match CTA per window keyframe, which initialises and resolves its
+    // own unit (no winner-table init pass, no resolve launch) -- used when the shard fills
+    // the GPU; LC_SOLE=0 forbids it, 1 forces it, 2 forces the queued-item k_match_sole
+    // kernel (measured slower at C5)
+    const bool sole = !pipe && max_len <= 16384 && w_hi > w_lo &&
+                      (c->sole_mode < 0 ? (w_hi - w_lo) >= 2 * 148 : c->sole_mode >= 1);
     const int64_t ch = sole ? std::max<int64_t>(max_len, 1) : pick_chunk(total_q);
     std::vector<int32_t> bunit;
     std::vector<int64_t> bq0, bq1;
@@ -1373,13 +1376,12 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       a.epoch = st.ep;
       a.victim = vic;
       a.action = act;
-      a.sole = sole ? 1 : 0;
       a.unit_base = w_lo;
       a.surv = d_surv;
       a.surv_off = d_boff;
       a.surv_cnt = d_scnt;
+      a.sole = sole ? (c->sole_mode == 2 ? 2 : 1) : 0;
       if (pipe) {
-        a.loop_ep_w = st.mp_loop_ep;
         for (int k = 0; k < lc_ctx::kPipe; ++k) {
           const int b0 = pipe_b[k], nbk = pipe_b[k + 1] - pipe_b[k];
           CK(cudaStreamWaitEvent(call.s, c->pipe_ev[k], 0));

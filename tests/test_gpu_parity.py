@@ -167,7 +167,7 @@ def test_loop_parity_dense_keyframes(Ctx, name):
 
 @pytest.mark.parametrize("name", ["S3", "S3K"])
 @pytest.mark.parametrize("params", [FUSE_PARAMS, FUSE_PARAMS_CHECKS], ids=["faithful", "checks"])
-@pytest.mark.parametrize("sole", ["0", "1"], ids=["chunked", "sole"])
+@pytest.mark.parametrize("sole", ["0", "1", "2"], ids=["chunked", "sole", "sole-queued"])
 def test_loop_parity_large_windows(Ctx, name, params, sole, monkeypatch):
     """>= 296-keyframe windows with per-keyframe lists, both launch shapes: chunked
     k_match + k_resolve, and the one-CTA-per-keyframe k_match_sole (LC_SOLE=1) -- compared
