@@ -10,9 +10,10 @@ Between steps (untimed) the mutable map state is restored from a device-side cop
 (lc_state_restore) and L2 is flushed by a 512 MB write, so every step does identical
 work from a cold L2. value = candidate matches per step / device step time.
 
-Multi-GPU (torchrun, NCCL): WINDOW and ALL are replicated (~10 us, cheaper than a
-collective), fusion is keyframe-sharded: PLAN on the shard, one all_reduce(MIN) of the
-int64 [winner | victim] words, APPLY on every rank (paper_2603_17201_b200/dist.py).
+Multi-GPU (torchrun, NCCL): WINDOW and ALL are replicated, fusion is keyframe-sharded:
+PLAN on the shard, all_reduce(MIN) of the int64 victim words + all_gather of the sparse
+ADD lists, APPLY on every rank (paper_2603_17201_b200/dist.py); the merged result is
+checked against an unsharded FUSE_ALL once before timing.
 Total work is fixed as N grows -> "scaling": "strong".
 
 --impl reference times the CPU oracle (oracle/, the plain definition) on bounded
@@ -264,7 +265,8 @@ def main():
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     cnt_fuse = None
 
-    comm_ev = []   # (start, end) around the all-reduce of the current step (N > 1)
+    comm_ev = []   # (start, end) around the exchange of the current step (N > 1)
+    last_info = {}
 
     def step():
         ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
@@ -274,9 +276,10 @@ def main():
                          action=False, host=False)
             c = r["counts"]
         else:
-            c, _, _ = lcdist.fuse_sharded(ctx, w.window, mp_list_d, FUSE_PARAMS, window_S=w.win_S,
-                                          win_list_begin=w.win_list_begin, device=dev, tables=tables,
-                                          events=comm_ev[0] if comm_ev else None)
+            c, _, info = lcdist.fuse_sharded(ctx, w.window, mp_list_d, FUSE_PARAMS, window_S=w.win_S,
+                                             win_list_begin=w.win_list_begin, device=dev, tables=tables,
+                                             events=comm_ev[0] if comm_ev else None)
+            last_info.update(info)
         ctx.correct_all(S_opt_d, host=False)
         return c
 
@@ -295,6 +298,27 @@ def main():
     cand_rank = int(cf[counts.index("candidates")])
     q_rank = int(cf[counts.index("queries")])
     prop_rank = int(cf[counts.index("proposals")])
+
+    # N > 1: the merged result must equal an unsharded FUSE_ALL of the same loop event on
+    # this rank (victim words and the final associations), checked once, untimed
+    merge_check = None
+    if ws > 1:
+        reset()
+        step()
+        torch.cuda.synchronize()
+        vic_sh = vic_t.clone()
+        fm_sh = ctx.download_map()["feat_mp"]
+        reset()
+        ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
+        ref = ctx.fuse(w.window, mp_list_d, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin,
+                       action=False, host=False)
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(ref["victim"], vic_sh)) and bool(np.array_equal(ctx.download_map()["feat_mp"], fm_sh))
+        okt = torch.tensor([1 if ok else 0], dtype=torch.int64, device=dev)
+        tdist.all_reduce(okt, op=tdist.ReduceOp.MIN)
+        merge_check = "equal to the unsharded FUSE_ALL" if int(okt.item()) == 1 else "MISMATCH"
+        if merge_check != "equal to the unsharded FUSE_ALL":
+            raise SystemExit("bench: sharded fusion differs from the unsharded FUSE_ALL")
 
     # timed region: barrier + sync on both sides, events per step on the launching stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -336,9 +360,16 @@ def main():
         cm = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in comm_pairs]))], dtype=torch.float64,
                           device=dev)
         tdist.all_reduce(cm, op=tdist.ReduceOp.MAX)
-        multi = {"allreduce_ms_per_step": round(float(cm.item()), 5), "allreduce_bytes": int(tables.numel() * 8),
-                 "collective": "all_reduce(MIN) int64 [winner | victim] (" + tdist.get_backend() + ")",
-                 "compute_ms_per_step": round(ms_step - float(cm.item()), 5)}
+        eb = last_info.get("exchange_bytes", {})
+        multi = {"exchange_ms_per_step": round(float(cm.item()), 5),
+                 "compute_ms_per_step": round(ms_step - float(cm.item()), 5),
+                 "victim_allreduce_bytes": int(eb.get("victim_allreduce", 0)),
+                 "adds_allgather_bytes": int(eb.get("adds_allgather", 0)),
+                 "n_adds": int(last_info.get("n_adds", 0)),
+                 "collectives": "all_reduce(MIN) int64 victim words + all_gather of sparse (index, word) "
+                                "ADD lists (" + tdist.get_backend() + ")",
+                 "replicated": "WINDOW correction, APPLY, ALL correction (deterministic; DESIGN.md §7)",
+                 "merge_check": merge_check}
     value = cand_total / (ms_step / 1000.0)
 
     # roofline of the dominant stage: fuse matching = k_project -> k_match (one launch each

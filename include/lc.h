@@ -515,6 +515,30 @@ lc_status lc_fuse(lc_ctx* ctx, int32_t phase, int32_t w_lo, int32_t w_hi, int32_
                   void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
+ * lc_fuse_adds -- the sparse ADD exchange of a keyframe-sharded fusion (SURVEY.md §8(e):
+ * "all_gather of ADD lists, as (global feature index, q) pairs"; the
+ * window keyframes are independent, so each rank plans a shard).
+ *
+ * APPLY reads a winner word only where the slot is empty (an ADD); every other effect of
+ * PLAN travels in the victim words. So after PLAN on window positions [w_lo, w_hi):
+ *   op LC_ADDS_PACK  : compacts the winner words of that shard whose slot is empty into
+ *                      (io_idx[i] = window-major feature index, io_word[i] = winner word),
+ *                      i < *io_n (written; order unspecified). LC_ECAPACITY (nothing
+ *                      written beyond capacity, *io_n = the required count) if too small.
+ *   op LC_ADDS_UNPACK: io_winner[0 .. sum F(window)) <- LC_NONE, then io_winner[io_idx[i]]
+ *                      = io_word[i] for i < *io_n (the all_gathered lists of every rank):
+ *                      the dense table APPLY takes.
+ * io_winner [host|dev] [sum_i F(window_kf[i])]; io_idx, io_word [host|dev] int64,
+ * capacity entries; io_n [host]. window_kf [host] as in lc_fuse. PACK synchronises the
+ * stream (it reads the count back).
+ * Errors: LC_ESTATE (no map), LC_EINVAL, LC_ERANGE, LC_ECAPACITY. */
+#define LC_ADDS_PACK 1
+#define LC_ADDS_UNPACK 2
+lc_status lc_fuse_adds(lc_ctx* ctx, int32_t op, int32_t n_window, const int32_t* window_kf, int32_t w_lo,
+                       int32_t w_hi, int64_t* io_winner, int64_t* io_idx, int64_t* io_word, int64_t* io_n,
+                       int64_t capacity, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
  * lc_search_by_projection -- batched read-only projection search
  * (PAPER.md:200). Pair p = (keyframe pair_kf[p], transform
  * pair_S[p], parameter set params[pair_param[p]], list mp_list[pair_list_begin[p]

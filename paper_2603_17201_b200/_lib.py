@@ -17,6 +17,7 @@ STATUS_NAMES = {0: "LC_OK", -1: "LC_EINVAL", -2: "LC_ESTATE", -3: "LC_ECUDA", -4
 LC_NONE = (1 << 63) - 1
 LC_CORRECT_WINDOW, LC_CORRECT_ALL, LC_DRY_RUN = 1, 2, 4
 LC_FUSE_PLAN, LC_FUSE_APPLY, LC_FUSE_ALL = 1, 2, 3
+LC_ADDS_PACK, LC_ADDS_UNPACK = 1, 2
 LC_REFRESH_DESC, LC_REFRESH_NORMAL = 1, 2
 COUNTER_NAMES = [
     "queries", "skip_bad", "skip_found", "cull_depth", "cull_bounds", "cull_dist",
@@ -111,6 +112,7 @@ def load():
         "lc_correct_sim3": (i32, [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp]),
         "lc_fuse": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, vp, i64, P(lc_match_params), i32, vp, vp,
                           vp, vp, vp, vp, vp]),
+        "lc_fuse_adds": (i32, [vp, i32, i32, vp, i32, i32, vp, vp, vp, vp, i64, vp]),
         "lc_search_by_projection": (i32, [vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp,
                                           vp, vp]),
         "lc_refresh_mappoints": (i32, [vp, i32, vp, i32, vp, vp]),
@@ -136,6 +138,6 @@ def load():
 def exported_symbols():
     return ["lc_create", "lc_destroy", "lc_last_error", "lc_kernel_launches", "lc_profile_enable",
             "lc_profile_read", "lc_upload_map",
-            "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse",
+            "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse", "lc_fuse_adds",
             "lc_search_by_projection", "lc_refresh_mappoints", "lc_update_connections", "lc_sim3_ransac", "lc_sim3_refine", "lc_pgo_sim3", "lc_graph_begin", "lc_graph_end", "lc_graph_launch",
             "lc_graph_destroy"]

@@ -1242,6 +1242,43 @@ __global__ void k_forced(int n_mp, const uint32_t* __restrict__ ep, int fb, int 
   block_add<1>(loc, slot, counts);
 }
 
+// Sparse ADD exchange (lc_fuse_adds): PACK compacts the shard's winner words on empty
+// slots; UNPACK scatters gathered (index, word) pairs into a NONE-filled dense table.
+__global__ void k_adds_pack(int64_t lo, int64_t hi, const int32_t* __restrict__ wpos_kf,
+                            const int64_t* __restrict__ woff, int n_w, const int32_t* __restrict__ kf_fbeg,
+                            const int32_t* __restrict__ feat_mp, const unsigned long long* __restrict__ winner,
+                            long long* __restrict__ out_idx, long long* __restrict__ out_word,
+                            unsigned long long* __restrict__ n_out, long long capacity) {
+  for (int64_t j = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < hi; j += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long w = winner[j];
+    bool add = false;
+    if (w != NONE) {
+      int a = 0, b = n_w - 1;   // window position of j: last i with woff[i] <= j
+      while (a < b) {
+        const int mid = (a + b + 1) >> 1;
+        if (woff[mid] <= j) a = mid; else b = mid - 1;
+      }
+      add = feat_mp[kf_fbeg[wpos_kf[a]] + (j - woff[a])] == -1;
+    }
+    if (add) {
+      const unsigned long long i = atomicAdd(n_out, 1ull);
+      if ((long long)i < capacity) { out_idx[i] = (long long)j; out_word[i] = (long long)w; }
+    }
+  }
+}
+
+__global__ void k_adds_unpack(int64_t n_wfeat, int64_t n, const long long* __restrict__ idx,
+                              const long long* __restrict__ word, unsigned long long* __restrict__ winner) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_wfeat; j += (int64_t)gridDim.x * blockDim.x)
+    winner[j] = NONE;
+  __threadfence();
+}
+__global__ void k_adds_scatter(int64_t n_wfeat, int64_t n, const long long* __restrict__ idx,
+                               const long long* __restrict__ word, unsigned long long* __restrict__ winner) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (idx[i] >= 0 && idx[i] < n_wfeat) winner[idx[i]] = (unsigned long long)word[i];
+}
+
 // Victim marking: flags |= bad, replaced_by = survivor (reading O9 (iv)), victim bitmap.
 __global__ void k_fuse_victims(int n_mp, const unsigned long long* __restrict__ victim,
                                uint8_t* __restrict__ flags, int32_t* __restrict__ replaced_by,
@@ -1573,6 +1610,25 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
                    (const int32_t*)st.kf_dirty, st.feat_mp, st.mp_nobs, H, counts);
     if (e != cudaSuccess) return e;
     c->launches += 2;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adds(lc_ctx* c, int op, int n_w, const int32_t* d_window, const int64_t* d_woff, int64_t n_wfeat,
+                        int64_t lo, int64_t hi, unsigned long long* winner, long long* idx, long long* word,
+                        unsigned long long* d_n, int64_t n_in, int64_t capacity, cudaStream_t s) {
+  Store& st = c->st;
+  if (op == LC_ADDS_PACK) {
+    cudaError_t e = cudaMemsetAsync(d_n, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    if (hi > lo)
+      k_adds_pack<<<grid_for(hi - lo), LC_NTHREADS, 0, s>>>(lo, hi, d_window, d_woff, n_w, st.kf_fbeg, st.feat_mp,
+                                                           winner, idx, word, d_n, (long long)capacity);
+    c->launches++;
+  } else {
+    k_adds_unpack<<<grid_for(n_wfeat), LC_NTHREADS, 0, s>>>(n_wfeat, n_in, idx, word, winner);
+    if (n_in > 0) k_adds_scatter<<<grid_for(n_in), LC_NTHREADS, 0, s>>>(n_wfeat, n_in, idx, word, winner);
+    c->launches += n_in > 0 ? 2 : 1;
   }
   return cudaGetLastError();
 }

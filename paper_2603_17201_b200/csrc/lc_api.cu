@@ -1418,6 +1418,52 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
 }
 
 // ----------------------------------------------------------------------------
+lc_status lc_fuse_adds(lc_ctx* c, int32_t op, int32_t n_window, const int32_t* window_kf, int32_t w_lo,
+                       int32_t w_hi, int64_t* io_winner, int64_t* io_idx, int64_t* io_word, int64_t* io_n,
+                       int64_t capacity, void* stream) {
+  return guarded(c, [&] {
+    capture_gate(c, stream, op == LC_ADDS_UNPACK);
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    REQUIRE(op == LC_ADDS_PACK || op == LC_ADDS_UNPACK, LC_EINVAL, "bad op");
+    REQUIRE(io_winner && io_n && capacity >= 0 && (capacity == 0 || (io_idx && io_word)), LC_EINVAL, "null argument");
+    mark_window(c, n_window, window_kf);
+    REQUIRE(0 <= w_lo && w_lo <= w_hi && w_hi <= n_window, LC_EINVAL, "bad shard range");
+    Store& st = c->st;
+    std::vector<int64_t> woff(n_window + 1, 0);
+    for (int i = 0; i < n_window; ++i) woff[i + 1] = woff[i] + (st.h_fbeg[window_kf[i] + 1] - st.h_fbeg[window_kf[i]]);
+    Call call(c, stream);
+    const int32_t* d_win = nullptr;
+    const int64_t* d_woff = nullptr;
+    call.arg(window_kf, n_window, &d_win);
+    call.arg(woff.data(), woff.size(), &d_woff);
+    call.commit();
+    const int64_t n_wfeat = woff[n_window];
+    if (op == LC_ADDS_PACK) {
+      const int64_t* d_w = call.in(io_winner, (size_t)n_wfeat);
+      int64_t* d_i = capacity ? call.out(io_idx, (size_t)capacity) : nullptr;
+      int64_t* d_o = capacity ? call.out(io_word, (size_t)capacity) : nullptr;
+      unsigned long long* d_n = (unsigned long long*)call.scratch(sizeof(unsigned long long));
+      CK(launch_adds(c, op, n_window, d_win, d_woff, n_wfeat, woff[w_lo], woff[w_hi], (unsigned long long*)d_w,
+                     (long long*)d_i, (long long*)d_o, d_n, 0, capacity, call.s));
+      unsigned long long n = 0;
+      CK(cudaMemcpyAsync(&n, d_n, sizeof(n), cudaMemcpyDeviceToHost, call.s));
+      call.finish();
+      CK(cudaStreamSynchronize(call.s));
+      *io_n = (int64_t)n;
+      REQUIRE((int64_t)n <= capacity, LC_ECAPACITY, "lc_fuse_adds: more ADDs than capacity");
+      return;
+    }
+    REQUIRE(*io_n >= 0 && *io_n <= capacity, LC_EINVAL, "io_n outside [0, capacity]");
+    int64_t* d_w = call.out(io_winner, (size_t)n_wfeat);
+    const int64_t* d_i = call.in(io_idx, (size_t)*io_n);
+    const int64_t* d_o = call.in(io_word, (size_t)*io_n);
+    CK(launch_adds(c, op, n_window, d_win, d_woff, n_wfeat, 0, 0, (unsigned long long*)d_w, (long long*)d_i,
+                   (long long*)d_o, nullptr, *io_n, capacity, call.s));
+    call.finish();
+  });
+}
+
+// ----------------------------------------------------------------------------
 lc_status lc_search_by_projection(lc_ctx* c, int32_t n_pairs, const int32_t* pair_kf,
                                   const lc_sim3* pair_S, const int32_t* pair_param,
                                   const lc_match_params* params, int32_t n_params,

@@ -354,6 +354,9 @@ cudaError_t launch_correct_dry(lc_ctx* c, int n_batch, int n_slots, const int32_
                                const double* d_Scw, void* scratch, double* d_outS, int32_t* d_mp_begin,
                                int64_t capacity, int32_t* d_idx, float* d_pos, unsigned long long* counts,
                                cudaStream_t s);   // WINDOW | DRY_RUN batch (zeroes counts)
+cudaError_t launch_adds(lc_ctx* c, int op, int n_w, const int32_t* d_window, const int64_t* d_woff, int64_t n_wfeat,
+                        int64_t lo, int64_t hi, unsigned long long* winner, long long* idx, long long* word,
+                        unsigned long long* d_n, int64_t n_in, int64_t capacity, cudaStream_t s);
 cudaError_t launch_fill_u64(lc_ctx* c, unsigned long long* p, int64_t n, unsigned long long v,
                             cudaStream_t s);
 cudaError_t launch_state_copy(lc_ctx* c, bool save, cudaStream_t s);

@@ -494,6 +494,31 @@ class Context:
             out.update(dd)
         return out
 
+    # -- lc_fuse_adds (sparse ADD exchange of a sharded fusion) --------------------
+    def fuse_adds_pack(self, window, w_lo, w_hi, winner, idx, word):
+        """Compact the shard's winner words on empty slots into (idx, word); returns n."""
+        k = self._keep(False)
+        window = np.ascontiguousarray(window, np.int32)
+        n = C.c_int64(0)
+        st = self.lib.lc_fuse_adds(self.h, _lib.LC_ADDS_PACK, len(window), k.ptr(window), int(w_lo), int(w_hi),
+                                   k.ptr(winner), k.ptr(idx), k.ptr(word), C.byref(n), int(idx.numel()),
+                                   self._stream())
+        self._check("lc_fuse_adds", st)
+        return int(n.value)
+
+    def fuse_adds_unpack(self, window, winner, idx, word):
+        """winner <- NONE, winner[idx] = word (the dense table APPLY reads)."""
+        k = self._keep(False)
+        window = np.ascontiguousarray(window, np.int32)
+        n = C.c_int64(int(idx.numel()))
+        idx = idx.contiguous()
+        word = word.contiguous()
+        st = self.lib.lc_fuse_adds(self.h, _lib.LC_ADDS_UNPACK, len(window), k.ptr(window), 0, len(window),
+                                   k.ptr(winner), k.ptr(idx) if idx.numel() else None,
+                                   k.ptr(word) if word.numel() else None, C.byref(n), int(idx.numel()),
+                                   self._stream())
+        self._check("lc_fuse_adds", st)
+
     # -- lc_search_by_projection ----------------------------------------------------
     def search_by_projection(self, pair_kf, pair_S, pair_param, params, pair_list_begin, mp_list,
                              pair_taken=None, debug=False, host=True):

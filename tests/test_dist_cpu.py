@@ -26,10 +26,30 @@ class OracleFuser:
         return self.om.window_feat_total(kfs)
 
     def fuse(self, window, mp_list, params, *, window_S=None, win_list_begin=None, phase=3,
-             w_lo=0, w_hi=None, winner=None, victim=None, action=True, host=True):
+             w_lo=0, w_hi=None, winner=None, victim=None, action=True, host=True, cur_kf=-1, forced_mp=None):
         return self.om.fuse(window, mp_list, params, window_S=window_S,
                             win_list_begin=win_list_begin, phase=phase, w_lo=w_lo, w_hi=w_hi,
-                            winner=winner, victim=victim)
+                            winner=winner, victim=victim, cur_kf=cur_kf, forced_mp=forced_mp)
+
+    def _gidx(self, window):
+        fb = self.om.kf_feat_begin
+        return np.concatenate([np.arange(fb[k], fb[k + 1]) for k in window])
+
+    def fuse_adds_pack(self, window, w_lo, w_hi, winner, idx, word):
+        """lc_fuse_adds(PACK) restated in numpy: the shard's winner words on empty slots."""
+        F = np.array([self.om.n_feat_of(int(k)) for k in window])
+        woff = np.r_[0, np.cumsum(F)]
+        w = winner.numpy() if hasattr(winner, "numpy") else winner
+        g = self._gidx(window)
+        j = np.arange(woff[w_lo], woff[w_hi])
+        sel = j[(w[j] != np.iinfo(np.int64).max) & (self.om.feat_mp[g[j]] == -1)]
+        idx[:len(sel)] = torch.from_numpy(sel)
+        word[:len(sel)] = torch.from_numpy(w[sel])
+        return len(sel)
+
+    def fuse_adds_unpack(self, window, winner, idx, word):
+        winner.fill_(np.iinfo(np.int64).max)
+        winner[idx] = word
 
 
 def _free_port():
@@ -51,11 +71,13 @@ def _worker(rank, world, port, name, params, out_dir):
     om = oracle.OracleMap(w)
     if w.win_S is None:
         om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
-    plan_c, app_c, tables = lcdist.fuse_sharded(OracleFuser(om), w.window, w.mp_list, params,
-                                                window_S=w.win_S, win_list_begin=w.win_list_begin)
+    plan_c, app_c, info = lcdist.fuse_sharded(OracleFuser(om), w.window, w.mp_list, params,
+                                              window_S=w.win_S, win_list_begin=w.win_list_begin,
+                                              gather_winner=True)
     plan_sum = lcdist.sum_counts(plan_c)
     np.savez(os.path.join(out_dir, f"r{rank}.npz"), feat_mp=om.feat_mp, flags=om.mp_flags,
-             rep=om.mp_replaced_by, nobs=om.mp_nobs, tables=tables.numpy(),
+             rep=om.mp_replaced_by, nobs=om.mp_nobs, winner=info["winner"].numpy(),
+             victim=info["victim"].numpy(), n_adds=info["n_adds"],
              cand=plan_sum["candidates"], victims=app_c["victims"])
     dist.destroy_process_group()
 
@@ -79,11 +101,56 @@ def test_fuse_sharded_gloo_equals_single(tmp_path, name, world):
         assert np.array_equal(z["flags"], om.mp_flags)
         assert np.array_equal(z["rep"], om.mp_replaced_by)
         assert np.array_equal(z["nobs"], om.mp_nobs)
-        nw = len(ref["winner"])
-        assert np.array_equal(z["tables"][:nw], ref["winner"])
-        assert np.array_equal(z["tables"][nw:], ref["victim"])
+        assert np.array_equal(z["winner"], ref["winner"])
+        assert np.array_equal(z["victim"], ref["victim"])
+        assert int(z["n_adds"]) == ref["counts"]["add"]
         assert int(z["cand"]) == ref["counts"]["candidates"]
         assert int(z["victims"]) == ref["counts"]["victims"]
+
+
+class OracleSearcher:
+    def __init__(self, om):
+        self.om = om
+
+    def n_feat_of(self, kfs):
+        return self.om.window_feat_total(kfs)
+
+    def search_by_projection(self, pair_kf, pair_S, pair_param, params, pair_list_begin, mp_list,
+                             pair_taken=None):
+        return self.om.search_by_projection(pair_kf, pair_S, pair_param, params, pair_list_begin, mp_list,
+                                            pair_taken=pair_taken)
+
+
+def _search_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from lcsynth import make_world
+    from lcsynth.world import SBP_PARAMS
+    from paper_2603_17201_b200 import dist as lcdist
+    w = make_world("C4", 0)
+    fm, fd, cn = lcdist.search_sharded(OracleSearcher(oracle.OracleMap(w)), w.pair_kf, w.pair_S, w.pair_param,
+                                       SBP_PARAMS, w.pair_list_begin, w.pair_mp_list, pair_taken=w.pair_taken)
+    np.savez(os.path.join(out_dir, f"s{rank}.npz"), fm=fm.numpy(), fd=fd.numpy(), cn=cn.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_search_sharded_gloo_equals_single(tmp_path, world):
+    """C4's 32 hypotheses x 4 pairs split across ranks (replicas of the map, pair blocks,
+    all_gather of the output tables) == the single-process batched search."""
+    import oracle
+    from lcsynth import make_world
+    from lcsynth.world import SBP_PARAMS
+    mp.spawn(_search_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    w = make_world("C4", 0)
+    ref = oracle.OracleMap(w).search_by_projection(w.pair_kf, w.pair_S, w.pair_param, SBP_PARAMS,
+                                                   w.pair_list_begin, w.pair_mp_list, pair_taken=w.pair_taken)
+    for r in range(world):
+        z = np.load(tmp_path / f"s{r}.npz")
+        assert np.array_equal(z["fm"], ref["feat_mp"]) and np.array_equal(z["fd"], ref["feat_dist"])
+        assert np.array_equal(z["cn"], ref["counts"])
 
 
 def test_shard_bounds_balanced_and_covering():
