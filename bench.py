@@ -52,7 +52,9 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="skip the secondary measurement of the step replayed as a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=5.0,
+                    help="bounded sample of the single-thread brute-force oracle (context)")
+    ap.add_argument("--seeds", type=int, default=5, help="worlds timed (seed, seed + 1, ...); SURVEY §8(d)")
     ap.add_argument("--profile-only", action="store_true",
                     help="few steps, no e2e/cpu legs (for ncu)")
     return ap.parse_args()
@@ -109,16 +111,22 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def roofline_bytes(w, n_queries, n_proposals):
-    """Algorithmic bytes of the fuse matching stage (SURVEY.md §8(d) per-unit figures;
-    DESIGN.md "Roofline"), split by the kernel that moves them:
-      k_project: 68 B per query (list entry 4 + 64-B map-point record);
-      k_match:   48 B per window-keyframe feature (uv 8 + octave/index 4 + descriptor 32
-                 + association 4) + 8 B per proposal (winner word).
-    The survivor buffer between the two kernels is an L2-resident intermediate and is not
-    counted (it is not algorithmic traffic)."""
+def roofline_bytes(w, c_fuse, c_window):
+    """Algorithmic bytes per step (SURVEY.md §8(d) "Algorithmic bytes B_alg"),
+    by the unit each figure is quoted for:
+      k_project : 68 B per query (list entry 4 + 64-B map-point record);
+      k_match   : 48 B per window-keyframe feature (uv 8 + octave/index 4 + descriptor 32 +
+                  association 4) + 8 B per window feature (its winner word, written once);
+      whole step: the above + 8 B per victim + 4 B per map feature (APPLY's association
+                  scan) + WINDOW (4 B per window feature + 28 B per corrected point) + ALL
+                  (32 B per map point + 208 B per keyframe).
+    Intermediates (the survivor buffer, scratch tables) are not algorithmic traffic."""
     n_wfeat = int(np.sum(np.diff(w.kf_feat_begin)[w.window]))
-    return {"k_project": 68 * int(n_queries), "k_match": 48 * n_wfeat + 8 * int(n_proposals)}
+    n_feat = int(w.kf_feat_begin[-1])
+    b = {"k_project": 68 * int(c_fuse["queries"]), "k_match": (48 + 8) * n_wfeat}
+    b["whole_step"] = (b["k_project"] + b["k_match"] + 8 * int(c_fuse["victims"]) + 4 * n_feat
+                       + 4 * n_wfeat + 28 * int(c_window["corr_mp"]) + 32 * int(w.n_mp) + 208 * int(w.n_kf))
+    return b
 
 
 def load_peaks():
@@ -136,42 +144,70 @@ def load_traffic():
 
 
 # ----------------------------------------------------------------------------
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_plan(w, threads):
+    """The oracle's timing mode (oracle/ orc_fuse_plan_grid: cell grid, keyframes over
+    `threads` POSIX threads, tables equal to the brute-force definition -- tests) on the
+    benchmark's whole loop event: WINDOW correction (untimed setup), then the fuse PLAN of
+    every window keyframe. Returns (seconds, candidates, the oracle map, its grid)."""
+    import oracle
+    from lcsynth.world import FUSE_PARAMS
+    om = oracle.OracleMap(w)
+    om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    g = om.grid()
+    t0 = time.perf_counter()
+    r = om.fuse_plan_grid(g, threads, w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S,
+                          win_list_begin=w.win_list_begin)
+    return time.perf_counter() - t0, int(r["counts"]["candidates"]), om, g
+
+
 def run_reference(args, w, ws, rank):
-    """CPU oracle (as it stands) on bounded samples of the same workload."""
+    """The CPU oracle (as it stands) on this host's cores: its grid / threaded PLAN over the
+    whole benchmark window per step (the definition's tables, SURVEY §8(d) "Grid mode is the
+    timed baseline ... at T = all host cores")."""
     import oracle
     from lcsynth.world import FUSE_PARAMS
     if rank != 0:
         return
+    T = host_cores()
     om = oracle.OracleMap(w)
     om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
-    # size the fuse sample so one step takes ~2 s
-    n_kf_sample = 4
-    t0 = time.time()
-    om.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin,
-            phase=1, w_lo=0, w_hi=n_kf_sample)
-    per_kf = (time.time() - t0) / n_kf_sample
-    nwin = len(w.window)
-    n_kf_sample = min(nwin, max(1, int(2.0 / max(per_kf, 1e-6))))
-    times, cands, lo = [], [], 0
+    g = om.grid()
+    times, cands = [], []
     for step in range(args.warmup + args.steps):
-        lo = (lo + n_kf_sample) % max(nwin - n_kf_sample + 1, 1)
         t0 = time.perf_counter()
-        r = om.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S,
-                    win_list_begin=w.win_list_begin, phase=1, w_lo=lo, w_hi=lo + n_kf_sample)
+        r = om.fuse_plan_grid(g, T, w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S,
+                              win_list_begin=w.win_list_begin)
         dt = time.perf_counter() - t0
         if step >= args.warmup:
             times.append(dt)
             cands.append(r["counts"]["candidates"])
     value = float(np.sum(cands) / np.sum(times))
-    sample = (f"oracle fuse PLAN (projection + brute-force windowed Hamming match + conflicts) "
-              f"over {n_kf_sample} of {nwin} window keyframes per step ({args.config}, seed {args.seed})")
+    sample = (f"oracle fuse PLAN (projection + windowed Hamming match + conflicts + victim proposals), "
+              f"cell-grid timing mode on {T} threads, the whole {len(w.window)}-keyframe window per step "
+              f"({args.config}, seed {args.seed}; host: {cpu_model()}); WINDOW / APPLY / ALL not timed")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * float(np.mean(times)), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} sampled: {n_kf_sample} window KFs/step",
-                       "seed": args.seed},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "config": {"workload": f"{args.config}: the whole fusion window's PLAN per step", "seed": args.seed},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "oracle (grid mode)",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -189,24 +225,28 @@ def pgo_cpu_baseline(seed):
 
 
 def cpu_baseline(w, seconds):
-    """Oracle (never tuned) on a bounded sample of the benchmark workload."""
+    """The oracle (never tuned) on this host: its grid / threaded timing mode at T = all host
+    cores over the WHOLE window PLAN, plus the brute-force definition on one
+    core over a bounded sample (context)."""
     import oracle
     from lcsynth.world import FUSE_PARAMS
-    om = oracle.OracleMap(w)
-    om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    T = host_cores()
+    dt, cands, om, _ = oracle_plan(w, T)
     t0 = time.perf_counter()
-    n, cands, lo = 0, 0, 0
-    step = 8
+    n, bc, lo, step = 0, 0, 0, 8
     while time.perf_counter() - t0 < seconds and lo < len(w.window):
         r = om.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S,
                     win_list_begin=w.win_list_begin, phase=1, w_lo=lo, w_hi=min(lo + step, len(w.window)))
-        cands += r["counts"]["candidates"]
+        bc += r["counts"]["candidates"]
         n += min(step, len(w.window) - lo)
         lo += step
-    dt = time.perf_counter() - t0
-    return {"value": cands / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"fuse PLAN of the first {n} of {len(w.window)} window keyframes "
-                      f"({cands} candidate matches, {dt:.1f} s, single thread)"}
+    bdt = time.perf_counter() - t0
+    return {"value": cands / dt, "unit": UNIT, "cores": T, "kind": "oracle (grid mode)",
+            "sample": f"fuse PLAN of all {len(w.window)} window keyframes ({cands} candidate matches) in "
+                      f"{dt:.2f} s on {T} threads ({cpu_model()}); WINDOW / APPLY / ALL not timed",
+            "brute_force_1_thread": {"value": bc / bdt, "cores": 1,
+                                     "sample": f"definition (no grid) over the first {n} window keyframes, "
+                                               f"{bc} candidate matches, {bdt:.1f} s"}}
 
 
 # ----------------------------------------------------------------------------
@@ -268,15 +308,18 @@ def main():
     comm_ev = []   # (start, end) around the exchange of the current step (N > 1)
     last_info = {}
 
-    def step():
-        ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
+    cnt_window = []
+
+    def step(params=FUSE_PARAMS):
+        _, cw = ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
+        cnt_window[:] = [cw]
         if ws == 1:
-            r = ctx.fuse(w.window, mp_list_d, FUSE_PARAMS, window_S=w.win_S,
+            r = ctx.fuse(w.window, mp_list_d, params, window_S=w.win_S,
                          win_list_begin=w.win_list_begin, winner=win_t, victim=vic_t,
                          action=False, host=False)
             c = r["counts"]
         else:
-            c, _, info = lcdist.fuse_sharded(ctx, w.window, mp_list_d, FUSE_PARAMS, window_S=w.win_S,
+            c, _, info = lcdist.fuse_sharded(ctx, w.window, mp_list_d, params, window_S=w.win_S,
                                              win_list_begin=w.win_list_begin, device=dev, tables=tables,
                                              events=comm_ev[0] if comm_ev else None)
             last_info.update(info)
@@ -296,8 +339,7 @@ def main():
     cf = cnt_fuse.cpu().numpy() if hasattr(cnt_fuse, "cpu") else np.asarray(list(cnt_fuse.values()))
     fuse_counts = {n: int(v) for n, v in zip(counts, cf)}
     cand_rank = int(cf[counts.index("candidates")])
-    q_rank = int(cf[counts.index("queries")])
-    prop_rank = int(cf[counts.index("proposals")])
+    win_counts = {n: int(v) for n, v in zip(counts, cnt_window[0].cpu().numpy())}
 
     # N > 1: the merged result must equal an unsharded FUSE_ALL of the same loop event on
     # this rank (victim words and the final associations), checked once, untimed
@@ -372,32 +414,32 @@ def main():
                  "merge_check": merge_check}
     value = cand_total / (ms_step / 1000.0)
 
-    # roofline of the dominant stage: fuse matching = k_project -> k_match (one launch each
-    # per step in this configuration), per-kernel device time from lc_profile events
+    # roofline: the dominant kernel (k_match, one launch per step, its duration
+    # from lc_profile CUDA events on the launching stream), the matching stage, the whole step
     fam_ms = {k: v[0] / args.steps for k, v in prof.items() if v[1]}
-    Bk = roofline_bytes(w, q_rank, prop_rank) if ws == 1 else None
+    Bk = roofline_bytes(w, fuse_counts, win_counts) if ws == 1 else None
     peaks = load_peaks()
     peak = peaks.get("hbm_gbs")
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md)"
     peak = peak or 6650.0
-    traffic = load_traffic().get("match_stage", {}).get(args.config)
+    traffic = load_traffic().get("k_match", {}).get(args.config)
     roof = None
-    stage_ms = fam_ms.get("project", 0.0) + fam_ms.get("match", 0.0)
-    if Bk is not None and stage_ms > 0:
-        B = sum(Bk.values())
-        ach = B / (stage_ms / 1000.0) / 1e9
-        per = {}
-        for kname, fam in (("k_project", "project"), ("k_match", "match")):
-            kms = fam_ms.get(fam, 0.0)
-            if kms > 0:
-                a_k = Bk[kname] / (kms / 1000.0) / 1e9
-                per[kname] = {"ms": round(kms, 5), "bytes": Bk[kname], "achieved": round(a_k, 1),
-                              "frac": round(a_k / peak, 4)}
-        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": traffic,
-                "kernel": "fuse matching stage: k_project -> k_match",
-                "algorithmic_bytes": B, "kernel_ms": round(stage_ms, 5), "peak_source": peak_src,
-                "step_share": round(stage_ms / ms_step, 4), "kernels": per}
+    if Bk is not None and fam_ms.get("match", 0.0) > 0:
+        def rl(name, B, kms):
+            a_k = B / (kms / 1000.0) / 1e9
+            return {"ms": round(kms, 5), "algorithmic_bytes": int(B), "achieved": round(a_k, 1),
+                    "frac": round(a_k / peak, 4)}
+        km = rl("k_match", Bk["k_match"], fam_ms["match"])
+        stage_ms = fam_ms.get("project", 0.0) + fam_ms["match"]
+        roof = {"bound": "hbm", "achieved": km["achieved"], "peak": peak, "unit": "GB/s", "frac": km["frac"],
+                "traffic": traffic,
+                "kernel": "k_match (window scan + Hamming + conflicts" + (" + per-keyframe resolve)" if
+                                                                          "resolve" not in fam_ms else ")"),
+                "algorithmic_bytes": Bk["k_match"], "kernel_ms": km["ms"], "peak_source": peak_src,
+                "step_share": round(fam_ms["match"] / ms_step, 4),
+                "kernels": {"k_project": rl("k_project", Bk["k_project"], fam_ms.get("project", 1e-9)), "k_match": km},
+                "stage": rl("stage", Bk["k_project"] + Bk["k_match"], stage_ms),
+                "whole_step": rl("whole_step", Bk["whole_step"], ms_step)}
 
     # e2e through the public API with host (pinned) buffers: H2D of the loop event's
     # inputs and D2H of its result (counts + victim table) inside the timed region
@@ -455,6 +497,61 @@ def main():
         graph = {"ms_per_step": round(g_ms, 5), "value": round(cand_total / (g_ms / 1000.0), 1),
                  "capture_instantiate_ms": round(cap_ms, 3)}
         cap.graph.close()
+
+    # secondary: the same C5 step with the ratio and orientation checks on (north_star "ratio
+    # and orientation checks"; FUSE_PARAMS_CHECKS = ratio 4/5 + rotation histogram), and the
+    # headline step on seeds 1..4 (5 seeds = the paper's 5 runs)
+    checks = seeds = None
+    if ws == 1 and not args.profile_only:
+        from lcsynth.world import FUSE_PARAMS_CHECKS
+        cms, ccnt = [], None
+        for i in range(args.warmup + args.steps):
+            reset()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ccnt = step(FUSE_PARAMS_CHECKS)
+            b.record(stream)
+            b.synchronize()
+            if i >= args.warmup:
+                cms.append(a.elapsed_time(b))
+        cc = {n: int(v) for n, v in zip(counts, ccnt.cpu().numpy())}
+        c_ms = float(np.mean(cms))
+        checks = {"params": "th 4, max 50, ratio 4/5, orientation on", "ms_per_step": round(c_ms, 5),
+                  "value": round(cc["candidates"] / (c_ms / 1000.0), 1), "unit": UNIT,
+                  "ratio_rej": cc["ratio_rej"], "orient_rej": cc["orient_rej"], "proposals": cc["proposals"]}
+        if args.seeds > 1:
+            per = []
+            for sd in range(args.seed, args.seed + args.seeds):
+                ws_ = w if sd == args.seed else make_world(args.config, sd)
+                cs = Context(local)
+                cs.upload_map(ws_.map_arrays(), [ws_.cam], grid=grid)
+                cs.state_save()
+                lst = torch.from_numpy(ws_.mp_list).to(dev)
+                Sop = torch.from_numpy(ws_.S_opt).to(dev)
+                sms, scnt = [], None
+                for i in range(3 + max(3, args.steps // 2)):
+                    cs.state_restore()
+                    flush.fill_(1.0)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    cs.correct_window(ws_.cur_kf, ws_.S_cw_corr, ws_.window, host=False)
+                    rr = cs.fuse(ws_.window, lst, FUSE_PARAMS, window_S=ws_.win_S, win_list_begin=ws_.win_list_begin,
+                                 action=False, host=False)
+                    cs.correct_all(Sop, host=False)
+                    b.record(stream)
+                    b.synchronize()
+                    if i >= 3:
+                        sms.append(a.elapsed_time(b))
+                    scnt = rr["counts"]
+                cand_s = int(scnt[counts.index("candidates")].item())
+                m_s = float(np.mean(sms))
+                per.append({"seed": sd, "ms_per_step": round(m_s, 5), "value": round(cand_s / (m_s / 1000.0), 1)})
+                cs.close()
+            v = np.array([x["value"] for x in per])
+            t = np.array([x["ms_per_step"] for x in per])
+            seeds = {"runs": per, "value_mean": round(float(v.mean()), 1), "value_std": round(float(v.std(ddof=1)), 1),
+                     "ms_mean": round(float(t.mean()), 5), "ms_std": round(float(t.std(ddof=1)), 5),
+                     "note": "the same loop event on independently generated worlds (seeds), L2 flushed"}
 
     # secondary: SURVEY §8(f) f2, refresh of the loop's map points after the event
     # (observation transpose + medoid descriptor + normal / depth range)
@@ -564,7 +661,7 @@ def main():
         # the same loop event on the EuRoC- and TUM-VI-shaped maps:
         # device-timed like the headline (L2 flushed, state restored between steps)
         loops = {}
-        for cname in ("C2", "C3"):
+        for cname in ("C1", "C2", "C3"):
             wc = make_world(cname, args.seed)
             cc = Context(local)
             cc.upload_map(wc.map_arrays(), [wc.cam], grid=grid)
@@ -699,6 +796,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "graph": graph,
+            "checks": checks,
+            "seeds": seeds,
             "upload": upload,
             "sbp": sbp,
             "refresh": refresh,
