@@ -375,25 +375,40 @@ lc_status lc_graph_launch(lc_ctx* ctx, lc_graph* graph, void* cuda_stream);
 lc_status lc_graph_destroy(lc_ctx* ctx, lc_graph* graph);
 
 /* ---------------------------------------------------------------------------
- * lc_upload_map -- GPU-resident keyframe storage.
+ * lc_upload_map -- GPU-resident keyframe storage (§IV.A: "transfer
+ * each newly created keyframe to GPU-resident KeyFrame Storage"; §IV.E:
+ * allocated once, pinned memory).
  *
  * Packs the SoA view into the device store: map-point records (position, dmax,
- * normal, angle, descriptor) as 64-byte AoS rows; keyframe features re-ordered
- * cell-major per keyframe by a GPU counting sort into grid_cols x grid_rows
- * cells over [min_x,max_x) x [min_y,max_y) of the keyframe's camera (cell =
- * floor((u-min_x) * cols / (max_x-min_x)), clamped), keeping the original local
- * index; association slots, angles and poses in original order. Replaces any
- * previous map (the store is re-allocated only if it grows). Synchronises the
- * stream before returning (validation reads back one error count).
+ * normal, angle, descriptor) as 64-byte AoS rows; keyframe features re-ordered per
+ * keyframe by a GPU counting sort into per-octave grids (octave o: the grid_cols x
+ * grid_rows grid coarsened by scale_factor^o, over [min_x,max_x) x [min_y,max_y) of the
+ * keyframe's camera; cell = floor((u-min_x) * cols_o / (max_x-min_x)), clamped), keeping
+ * the original local index; association slots, angles and poses in original order.
+ *   flags LC_UPLOAD_REPLACE: the view is the whole map; replaces any previous one.
+ *   flags LC_UPLOAD_APPEND : the view holds NEW keyframes and NEW map points only,
+ *     appended after the stored ones (the paper's per-keyframe transfer): keyframe i of
+ *     the view becomes store keyframe n_kf_old + i, map point j becomes n_mp_old + j;
+ *     feat_mp and mp_ref_kf use STORE indices (old or new entries); cams / n_cams / prm
+ *     are ignored (the stored ones apply); n_obs of every referenced point is updated.
+ *     The store grows geometrically (no re-allocation on most appends); a saved state
+ *     (lc_state_save) is dropped. N appends give the same store as one REPLACE of the
+ *     concatenated map, byte for byte.
+ * Host arrays may be pageable (copied through the library's pinned staging ring in
+ * 8-MB chunks, the host copy overlapping the DMA) or page-locked (copied directly).
+ * Synchronises the stream before returning (validation reads back one error count).
  *   map   [host] struct; its arrays [host|dev]
  *   cams  [host] n_cams cameras; prm [host]
  * Errors: LC_EINVAL (null arrays, n_* < 0, non-monotone kf_feat_begin, camera
  * bounds empty, n_levels outside [1, LC_MAX_LEVELS], scale_factor <= 1, grid
- * outside [1, 1024]^2), LC_ERANGE (feat_mp / mp_ref_kf / kf_cam / octave out of
- * range), LC_ECAPACITY (a keyframe with more than LC_MAX_FEAT_PER_KF features),
- * LC_ENOMEM, LC_ECUDA. */
+ * outside [1, 1024]^2 or more than 24576 cells over the octave grids, bad flags),
+ * LC_ESTATE (APPEND before a map), LC_ERANGE (feat_mp / mp_ref_kf / kf_cam / octave
+ * out of range), LC_ECAPACITY (a keyframe with more than LC_MAX_FEAT_PER_KF
+ * features), LC_ENOMEM, LC_ECUDA. */
+#define LC_UPLOAD_REPLACE 0
+#define LC_UPLOAD_APPEND 1
 lc_status lc_upload_map(lc_ctx* ctx, const lc_map_view* map, const lc_camera* cams,
-                        int32_t n_cams, const lc_map_params* prm, void* cuda_stream);
+                        int32_t n_cams, const lc_map_params* prm, int32_t flags, void* cuda_stream);
 
 /* Copy the mutable map state out (any member NULL = skipped). [host|dev]. */
 lc_status lc_download_map(lc_ctx* ctx, const lc_map_state* out, void* cuda_stream);

@@ -18,6 +18,7 @@ LC_NONE = (1 << 63) - 1
 LC_CORRECT_WINDOW, LC_CORRECT_ALL, LC_DRY_RUN = 1, 2, 4
 LC_FUSE_PLAN, LC_FUSE_APPLY, LC_FUSE_ALL = 1, 2, 3
 LC_ADDS_PACK, LC_ADDS_UNPACK = 1, 2
+LC_UPLOAD_REPLACE, LC_UPLOAD_APPEND = 0, 1
 LC_REFRESH_DESC, LC_REFRESH_NORMAL = 1, 2
 COUNTER_NAMES = [
     "queries", "skip_bad", "skip_found", "cull_depth", "cull_bounds", "cull_dist",
@@ -105,7 +106,7 @@ def load():
         "lc_kernel_launches": (i64, [vp]),
         "lc_profile_enable": (i32, [vp, i32]),
         "lc_profile_read": (i32, [vp, vp, vp]),
-        "lc_upload_map": (i32, [vp, P(lc_map_view), vp, i32, P(lc_map_params), vp]),
+        "lc_upload_map": (i32, [vp, P(lc_map_view), vp, i32, P(lc_map_params), i32, vp]),
         "lc_download_map": (i32, [vp, P(lc_map_state), vp]),
         "lc_state_save": (i32, [vp, vp]),
         "lc_state_restore": (i32, [vp, vp]),

@@ -57,18 +57,19 @@ __global__ void k_count_nobs(int n_feat, int n_mp, const int32_t* __restrict__ f
 // floor((u-min_x)*cols_o/(max_x-min_x))), clamped; the cell table and the feature arrays
 // are (octave, row, col)-major, and within a cell features keep ascending original index.
 __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
-    int n_levels, int n_cams, int Gs, int G, MatchArgs g, const int32_t* __restrict__ fbeg,
+    int kf0, int f0, int n_levels, int n_cams, int Gs, int G, MatchArgs g, const int32_t* __restrict__ fbeg,
     const int32_t* __restrict__ fpad, const int32_t* __restrict__ kf_cam,
     const DevCam* __restrict__ cams, const float* __restrict__ fuv, const uint8_t* __restrict__ foct,
     const uint8_t* __restrict__ fdesc, uint16_t* __restrict__ kf_cell, float2* __restrict__ fc_uv,
     uint32_t* __restrict__ fc_meta, uint4* __restrict__ fc_desc, int32_t* __restrict__ feat_cpos,
     uint32_t* __restrict__ errs) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int k = blockIdx.x;
+  const int k = kf0 + blockIdx.x;     // keyframes [kf0, kf0 + gridDim.x) of the store
   const int fb = fbeg[k];
   const int F = fbeg[k + 1] - fb;
   const int fp = fpad[k];
   const int ci = kf_cam[k];
+  const int fi = fb - f0;             // the inputs hold the features from store index f0 on
   if (ci < 0 || ci >= n_cams) {
     if (threadIdx.x == 0) atomicAdd(&errs[ERR_CAM], 1u);
     return;
@@ -81,10 +82,10 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
   for (int i = threadIdx.x; i <= G; i += blockDim.x) s_cnt[i] = 0;
   __syncthreads();
   for (int f = threadIdx.x; f < F; f += blockDim.x) {
-    const int o = foct[fb + f];
+    const int o = foct[fi + f];
     if (o >= n_levels) { atomicAdd(&errs[ERR_OCTAVE], 1u); s_cellof[f] = 0; continue; }
     const int cols = g.ocols[o], rows = g.orows[o];
-    double u = (double)fuv[2 * (fb + f)], v = (double)fuv[2 * (fb + f) + 1];
+    double u = (double)fuv[2 * (fi + f)], v = (double)fuv[2 * (fi + f) + 1];
     double x = floor((u - cam.min_x) * cam.cell_sx[o]);
     double y = floor((v - cam.min_y) * cam.cell_sy[o]);
     int cx = x >= 0.0 ? (x < (double)cols ? (int)x : cols - 1) : 0;
@@ -132,10 +133,10 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_grid_build(
   __syncthreads();
   for (int p = threadIdx.x; p < F; p += blockDim.x) {
     int f = s_perm[p];
-    fc_uv[fp + p] = make_float2(fuv[2 * (fb + f)], fuv[2 * (fb + f) + 1]);
-    fc_meta[fp + p] = (uint32_t)f | ((uint32_t)foct[fb + f] << 16);
+    fc_uv[fp + p] = make_float2(fuv[2 * (fi + f)], fuv[2 * (fi + f) + 1]);
+    fc_meta[fp + p] = (uint32_t)f | ((uint32_t)foct[fi + f] << 16);
     feat_cpos[fb + f] = fp + p;   // original order -> cell-major position
-    const uint8_t* d = fdesc + 32 * (size_t)(fb + f);
+    const uint8_t* d = fdesc + 32 * (size_t)(fi + f);
     uint32_t w[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -177,23 +178,25 @@ cudaError_t launch_fill_u64(lc_ctx* c, unsigned long long* p, int64_t n, unsigne
   return cudaGetLastError();
 }
 
-cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, const float* dmax,
-                               const uint8_t* desc, const float* ang, const float* fuv,
-                               const uint8_t* foct, const uint8_t* fdesc, uint32_t* d_errs,
-                               cudaStream_t s) {
+// Packs the store entries [kf0, n_kf), [f0, n_feat), [mp0, n_mp) from the caller's SoA
+// inputs (which hold exactly those entries): a whole map (REPLACE: all offsets 0) or the
+// keyframes / map points appended by LC_UPLOAD_APPEND.
+cudaError_t launch_upload_pack(lc_ctx* c, int kf0, int f0, int mp0, const float* pos, const float* nrm,
+                               const float* dmax, const uint8_t* desc, const float* ang, const float* fuv,
+                               const uint8_t* foct, const uint8_t* fdesc, uint32_t* d_errs, cudaStream_t s) {
   Store& st = c->st;
-  if (st.n_mp > 0) {
-    k_pack_mp<<<grid_for(st.n_mp), LC_NTHREADS, 0, s>>>(
-        st.n_mp, st.n_kf, pos, nrm, dmax, desc, ang, st.mp_ref_kf, st.mp_rec, st.mp_replaced_by,
-        st.mp_corr_ref, st.mp_loop_ep, st.mp_nobs, d_errs);
+  const int n_mp = st.n_mp - mp0, n_feat = st.n_feat - f0, n_kf = st.n_kf - kf0;
+  if (n_mp > 0) {
+    k_pack_mp<<<grid_for(n_mp), LC_NTHREADS, 0, s>>>(
+        n_mp, st.n_kf, pos, nrm, dmax, desc, ang, st.mp_ref_kf + mp0, st.mp_rec + mp0, st.mp_replaced_by + mp0,
+        st.mp_corr_ref + mp0, st.mp_loop_ep + mp0, st.mp_nobs + mp0, d_errs);
     c->launches++;
   }
-  if (st.n_feat > 0) {
-    k_count_nobs<<<grid_for(st.n_feat), LC_NTHREADS, 0, s>>>(st.n_feat, st.n_mp, st.feat_mp,
-                                                             st.mp_nobs, d_errs);
+  if (n_feat > 0) {   // n_obs of the referenced points (old or new) += new observations
+    k_count_nobs<<<grid_for(n_feat), LC_NTHREADS, 0, s>>>(n_feat, st.n_mp, st.feat_mp + f0, st.mp_nobs, d_errs);
     c->launches++;
   }
-  if (st.n_kf > 0) {
+  if (n_kf > 0) {
     size_t smem = sizeof(int) * (size_t)(st.G + 1) + 2 * sizeof(uint16_t) * (size_t)st.max_F;
     smem = (smem + 15) & ~(size_t)15;
     cudaError_t e = cudaFuncSetAttribute(k_grid_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -203,10 +206,9 @@ cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, co
     memset(&g, 0, sizeof(g));
     for (int i = 0; i < LC_MAX_LEVELS; ++i) { g.ocols[i] = st.ocols[i]; g.orows[i] = st.orows[i]; }
     for (int i = 0; i <= LC_MAX_LEVELS; ++i) g.obase[i] = st.obase[i];
-    k_grid_build<<<st.n_kf, LC_NTHREADS, smem, s>>>(st.n_levels, st.n_cams, st.Gs, st.G, g, st.kf_fbeg,
-                                                    st.kf_fpad, st.kf_cam,
-                                                    st.cams, fuv, foct, fdesc, st.kf_cell,
-                                                    st.fc_uv, st.fc_meta, st.fc_desc, st.feat_cpos, d_errs);
+    k_grid_build<<<n_kf, LC_NTHREADS, smem, s>>>(kf0, f0, st.n_levels, st.n_cams, st.Gs, st.G, g, st.kf_fbeg,
+                                                 st.kf_fpad, st.kf_cam, st.cams, fuv, foct, fdesc, st.kf_cell,
+                                                 st.fc_uv, st.fc_meta, st.fc_desc, st.feat_cpos, d_errs);
     c->launches++;
   }
   return cudaGetLastError();

@@ -168,6 +168,39 @@ struct Call {
     for (auto& f : arg_fix) *f.first = d_args + f.second;
   }
 
+  // host -> device copy of `bytes`: page-locked sources (and small or captured copies)
+  // directly; pageable sources in chunks through the context's pinned staging ring, so the
+  // host memcpy of one chunk overlaps the DMA of the previous ones (lc.h "Ownership")
+  void upload(void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    cudaPointerAttributes at;
+    const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (pinned || c->cap || bytes < lc_ctx::kStageMin) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+      return;
+    }
+    for (size_t off = 0; off < bytes; off += lc_ctx::kStageChunk) {
+      const size_t n = std::min(lc_ctx::kStageChunk, bytes - off);
+      const int r = c->stg_next;
+      c->stg_next = (r + 1) % lc_ctx::kStageRing;
+      if (!c->stg[r]) {
+        if (cudaHostAlloc(&c->stg[r], lc_ctx::kStageChunk, cudaHostAllocDefault) != cudaSuccess) {
+          cudaGetLastError();
+          c->stg[r] = nullptr;
+          CK(cudaMemcpyAsync((char*)dst + off, (const char*)src + off, bytes - off, cudaMemcpyHostToDevice, s));
+          return;
+        }
+        CK(cudaEventCreateWithFlags(&c->stg_ev[r], cudaEventDisableTiming));
+      } else {
+        CK(cudaEventSynchronize(c->stg_ev[r]));   // its previous chunk has left the buffer
+      }
+      memcpy(c->stg[r], (const char*)src + off, n);
+      CK(cudaMemcpyAsync((char*)dst + off, c->stg[r], n, cudaMemcpyHostToDevice, s));
+      CK(cudaEventRecord(c->stg_ev[r], s));
+    }
+  }
+
   // [host|dev] input: device pointer as-is, host data copied to scratch
   template <typename T>
   const T* in(const T* p, size_t n) {
@@ -175,7 +208,7 @@ struct Call {
     if (is_device_ptr(c, p)) return p;
     if (c->cap) require_pinned(p);
     T* d = (T*)scratch(sizeof(T) * n);
-    CK(cudaMemcpyAsync(d, p, sizeof(T) * n, cudaMemcpyDefault, s));
+    upload(d, p, sizeof(T) * n);
     return d;
   }
 
@@ -378,6 +411,23 @@ void fill_match_store(lc_ctx* c, MatchArgs& a) {
   for (int i = 0; i < LC_MAX_LEVELS; ++i) a.scale[i] = st.scale[i];
 }
 
+// Grow a device array from `used` to at least `need` entries (capacity `cap` -> max(need,
+// 1.5 cap)), keeping its first `used` entries (LC_UPLOAD_APPEND).
+template <typename T>
+void grow(lc_ctx* c, T** p, int64_t used, int64_t need, int64_t cap, int64_t new_cap, cudaStream_t s) {
+  if (need <= cap && *p) return;
+  T* q = nullptr;
+  if (cudaMalloc((void**)&q, std::max<size_t>(sizeof(T) * (size_t)new_cap, 16)) != cudaSuccess) {
+    cudaGetLastError();
+    set_err(c, "device store allocation failed");
+    throw Fail{LC_ENOMEM};
+  }
+  if (used > 0 && *p) CK(cudaMemcpyAsync(q, *p, sizeof(T) * (size_t)used, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  if (*p) cudaFree(*p);
+  *p = q;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -432,6 +482,10 @@ lc_status lc_destroy(lc_ctx* c) {
   for (int r = 0; r < lc_ctx::kPinRing; ++r) {
     if (c->pin[r]) cudaFreeHost(c->pin[r]);
     if (c->pin_ev[r]) cudaEventDestroy(c->pin_ev[r]);
+  }
+  for (int r = 0; r < lc_ctx::kStageRing; ++r) {
+    if (c->stg[r]) cudaFreeHost(c->stg[r]);
+    if (c->stg_ev[r]) cudaEventDestroy(c->stg_ev[r]);
   }
   if (c->sv) cudaFree(c->sv);
   if (c->side) cudaStreamDestroy(c->side);
@@ -544,21 +598,27 @@ lc_status lc_profile_read(lc_ctx* c, double* ms, int64_t* launches) {
 
 // ----------------------------------------------------------------------------
 lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, int32_t n_cams,
-                        const lc_map_params* prm, void* stream) {
+                        const lc_map_params* prm, int32_t flags, void* stream) {
   return guarded(c, [&] {
     capture_gate(c, stream, false);
-    REQUIRE(m && cams && prm && n_cams >= 1, LC_EINVAL, "null map/camera/params");
-    REQUIRE(m->n_kf >= 0 && m->n_feat >= 0 && m->n_mp >= 0, LC_EINVAL, "negative sizes");
-    REQUIRE(prm->n_levels >= 1 && prm->n_levels <= LC_MAX_LEVELS, LC_EINVAL, "n_levels out of range");
-    REQUIRE(prm->scale_factor > 1.0, LC_EINVAL, "scale_factor must be > 1");
-    REQUIRE(prm->grid_cols >= 1 && prm->grid_rows >= 1 && prm->grid_cols <= 1024 &&
-                prm->grid_rows <= 1024 && prm->grid_cols * prm->grid_rows <= 16384,
-            LC_EINVAL, "grid size out of range");
-    for (int i = 0; i < n_cams; ++i) {
-      const lc_camera& k = cams[i];
-      REQUIRE(k.model == 0 || k.model == 1, LC_EINVAL, "camera model must be 0 or 1");
-      REQUIRE(k.max_x > k.min_x && k.max_y > k.min_y, LC_EINVAL, "empty camera bounds");
+    const bool append = (flags & LC_UPLOAD_APPEND) != 0;
+    REQUIRE(flags == LC_UPLOAD_REPLACE || flags == LC_UPLOAD_APPEND, LC_EINVAL, "bad flags");
+    REQUIRE(m, LC_EINVAL, "null map");
+    REQUIRE(!append || c->has_map, LC_ESTATE, "LC_UPLOAD_APPEND before any map upload");
+    if (!append) {
+      REQUIRE(cams && prm && n_cams >= 1, LC_EINVAL, "null map/camera/params");
+      REQUIRE(prm->n_levels >= 1 && prm->n_levels <= LC_MAX_LEVELS, LC_EINVAL, "n_levels out of range");
+      REQUIRE(prm->scale_factor > 1.0, LC_EINVAL, "scale_factor must be > 1");
+      REQUIRE(prm->grid_cols >= 1 && prm->grid_rows >= 1 && prm->grid_cols <= 1024 &&
+                  prm->grid_rows <= 1024 && prm->grid_cols * prm->grid_rows <= 16384,
+              LC_EINVAL, "grid size out of range");
+      for (int i = 0; i < n_cams; ++i) {
+        const lc_camera& k = cams[i];
+        REQUIRE(k.model == 0 || k.model == 1, LC_EINVAL, "camera model must be 0 or 1");
+        REQUIRE(k.max_x > k.min_x && k.max_y > k.min_y, LC_EINVAL, "empty camera bounds");
+      }
     }
+    REQUIRE(m->n_kf >= 0 && m->n_feat >= 0 && m->n_mp >= 0, LC_EINVAL, "negative sizes");
     const bool need = m->n_kf > 0;
     REQUIRE(!need || (m->kf_pose && m->kf_cam && m->kf_feat_begin), LC_EINVAL, "null keyframe arrays");
     REQUIRE(m->n_feat == 0 || (m->feat_uv && m->feat_octave && m->feat_angle && m->feat_desc &&
@@ -567,7 +627,7 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
                              m->mp_angle && m->mp_ref_kf && m->mp_flags), LC_EINVAL, "null map-point arrays");
     Call call(c, stream);
     cudaStream_t s = call.s;
-    // host copy of the keyframe CSR (validation + launch configuration)
+    // host copy of the (new) keyframes' CSR (validation + launch configuration)
     std::vector<int32_t> fbeg(m->n_kf + 1, 0);
     if (m->n_kf > 0) {
       if (is_device_ptr(c, m->kf_feat_begin)) {
@@ -585,112 +645,157 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
       max_F = std::max(max_F, fbeg[k + 1] - fbeg[k]);
     }
     REQUIRE(max_F <= LC_MAX_FEAT_PER_KF, LC_ECAPACITY, "keyframe exceeds LC_MAX_FEAT_PER_KF features");
-
     CK(cudaStreamSynchronize(s));
-    free_store(c->st);
+    Store& st = c->st;
+    // old extents (APPEND) / zero (REPLACE); the new entries go to [kf0, ...), [f0, ...), [mp0, ...)
+    int kf0 = 0, f0 = 0, mp0 = 0;
+    int64_t fp0 = 0;
+    if (append) {
+      kf0 = st.n_kf; f0 = st.n_feat; mp0 = st.n_mp; fp0 = st.n_fpad;
+      REQUIRE((int64_t)kf0 + m->n_kf < (1LL << 31) && (int64_t)f0 + m->n_feat < (1LL << 31) &&
+                  (int64_t)mp0 + m->n_mp < (1LL << 31), LC_ECAPACITY, "store index space exhausted");
+    } else {
+      free_store(st);
+      st.n_cams = n_cams;
+      st.n_levels = prm->n_levels; st.cols = prm->grid_cols; st.rows = prm->grid_rows;
+      {   // per-octave grids: octave o coarsened by scale_factor^o (its keypoints are that much sparser)
+        double f = 1.0;
+        st.obase[0] = 0;
+        for (int o = 0; o < LC_MAX_LEVELS; ++o) {
+          st.ocols[o] = std::max(1, (int)std::ceil(st.cols / f - 1e-9));
+          st.orows[o] = std::max(1, (int)std::ceil(st.rows / f - 1e-9));
+          st.obase[o + 1] = st.obase[o] + (o < st.n_levels ? st.ocols[o] * st.orows[o] : 0);
+          f *= prm->scale_factor;
+        }
+      }
+      st.G = st.obase[st.n_levels];
+      REQUIRE(st.G <= 24576, LC_EINVAL, "grid too fine: more than 24576 cells over the octave grids");
+      st.Gs = (int32_t)round_up((size_t)st.G + 1, 8);
+      st.scale[0] = 1.0;
+      for (int n = 1; n < LC_MAX_LEVELS; ++n) st.scale[n] = st.scale[n - 1] * prm->scale_factor;
+      st.h_fbeg.assign(1, 0);
+      st.h_in_win.clear();
+      c->ep_used = 0;
+    }
     c->has_map = false;
     c->has_saved = false;
-    Store& st = c->st;
-    st.n_kf = m->n_kf; st.n_feat = m->n_feat; st.n_mp = m->n_mp; st.n_cams = n_cams;
-    st.n_levels = prm->n_levels; st.cols = prm->grid_cols; st.rows = prm->grid_rows;
-    {   // per-octave grids: octave o coarsened by scale_factor^o (its keypoints are that much sparser)
-      double f = 1.0;
-      st.obase[0] = 0;
-      for (int o = 0; o < LC_MAX_LEVELS; ++o) {
-        st.ocols[o] = std::max(1, (int)std::ceil(st.cols / f - 1e-9));
-        st.orows[o] = std::max(1, (int)std::ceil(st.rows / f - 1e-9));
-        st.obase[o + 1] = st.obase[o] + (o < st.n_levels ? st.ocols[o] * st.orows[o] : 0);
-        f *= prm->scale_factor;
-      }
+    const int64_t NK = (int64_t)kf0 + m->n_kf, NF = (int64_t)f0 + m->n_feat, NM = (int64_t)mp0 + m->n_mp;
+    // padded (multiple-of-4) per-keyframe blocks of the cell-major feature arrays
+    std::vector<int32_t> fpad_new(m->n_kf + 1, 0);
+    fpad_new[0] = (int32_t)fp0;
+    for (int k = 0; k < m->n_kf; ++k)
+      fpad_new[k + 1] = fpad_new[k] + (int32_t)round_up((size_t)(fbeg[k + 1] - fbeg[k]), 4);
+    const int64_t NPad = fpad_new[m->n_kf];
+    const int64_t NP = NPad + 4;
+    // capacities: exact for REPLACE, geometric for APPEND
+    auto ncap = [&](int64_t need_n, int64_t cap) { return append ? std::max<int64_t>(need_n, cap + cap / 2) : need_n; };
+    const int64_t ck = ncap(NK, st.cap_kf), cf = ncap(NF, st.cap_feat), cp = ncap(NP, st.cap_fpad), cm = ncap(NM, st.cap_mp);
+    const bool gk = NK > st.cap_kf || !append, gf = NF > st.cap_feat || !append, gp = NP > st.cap_fpad || !append,
+               gm = NM > st.cap_mp || !append;
+    const int64_t uk = append ? kf0 : 0, uf = append ? f0 : 0, up = append ? fp0 + 4 : 0, um = append ? mp0 : 0;
+    if (gk) {
+      grow(c, &st.kf_pose, 13 * uk, 13 * NK, 0, 13 * ck, s);
+      grow(c, &st.kf_cam, uk, NK, 0, ck, s);
+      grow(c, &st.kf_fbeg, uk + 1, NK + 1, 0, ck + 1, s);
+      grow(c, &st.kf_fpad, uk + 1, NK + 1, 0, ck + 1, s);
+      grow(c, &st.kf_cell, uk * st.Gs, NK * st.Gs, 0, ck * st.Gs, s);
+      grow(c, &st.kf_S_corr, 13 * uk, 13 * NK, 0, 13 * ck, s);
+      grow(c, &st.kf_in_win, uk, NK, 0, ck, s);
+      grow(c, &st.kf_win_ep, uk, NK, 0, ck, s);
+      grow(c, &st.kf_win_pos, uk, NK, 0, ck, s);
+      grow(c, &st.kf_dirty, uk + 1, NK + 1, 0, ck + 1, s);
+      st.cap_kf = ck;
     }
-    st.G = st.obase[st.n_levels];
-    REQUIRE(st.G <= 24576, LC_EINVAL, "grid too fine: more than 24576 cells over the octave grids");
-    st.Gs = (int32_t)round_up((size_t)st.G + 1, 8);
-    st.max_F = max_F;
-    std::vector<int32_t> fpad(st.n_kf + 1, 0);
-    for (int k = 0; k < st.n_kf; ++k) fpad[k + 1] = fpad[k] + (int32_t)round_up((size_t)(fbeg[k + 1] - fbeg[k]), 4);
-    st.n_fpad = fpad[st.n_kf];
-    st.scale[0] = 1.0;
-    for (int n = 1; n < LC_MAX_LEVELS; ++n) st.scale[n] = st.scale[n - 1] * prm->scale_factor;
-    st.h_fbeg = fbeg;
-    st.h_in_win.assign(st.n_kf, 0);
-    const size_t NK = st.n_kf, NF = st.n_feat, NM = st.n_mp;
-    dev_alloc(c, &st.kf_pose, 13 * NK);
-    dev_alloc(c, &st.kf_cam, NK);
-    dev_alloc(c, &st.kf_fbeg, NK + 1);
-    const size_t NP = (size_t)st.n_fpad + 4;
-    dev_alloc(c, &st.kf_fpad, NK + 1);
-    dev_alloc(c, &st.kf_cell, NK * (size_t)st.Gs);
-    dev_alloc(c, &st.fc_uv, NP);
-    dev_alloc(c, &st.fc_meta, NP);
-    dev_alloc(c, &st.fc_desc, 2 * NP);
-    CK(cudaMemsetAsync(st.kf_cell, 0, sizeof(uint16_t) * NK * st.Gs, s));
-    CK(cudaMemsetAsync(st.fc_uv, 0, sizeof(float2) * NP, s));
-    CK(cudaMemsetAsync(st.fc_meta, 0, sizeof(uint32_t) * NP, s));
-    CK(cudaMemcpyAsync(st.kf_fpad, fpad.data(), sizeof(int32_t) * (NK + 1), cudaMemcpyHostToDevice, s));
-    dev_alloc(c, &st.feat_mp, NF);
-    dev_alloc(c, &st.feat_angle, NF);
-    dev_alloc(c, &st.feat_cpos, NF);
-    dev_alloc(c, &st.mp_rec, NM);
-    dev_alloc(c, &st.mp_flags, NM);
-    dev_alloc(c, &st.mp_ref_kf, NM);
-    dev_alloc(c, &st.mp_replaced_by, NM);
-    dev_alloc(c, &st.mp_nobs, NM);
-    dev_alloc(c, &st.mp_corr_ref, NM);
-    dev_alloc(c, &st.mp_loop_ep, NM);
-    dev_alloc(c, &st.mp_owner, NM);
-    dev_alloc(c, &st.kf_S_corr, 13 * NK);
-    dev_alloc(c, &st.kf_in_win, NK);
-    dev_alloc(c, &st.kf_win_ep, NK);
-    dev_alloc(c, &st.ep, 2);
-    dev_alloc(c, &st.kf_win_pos, NK);
-    dev_alloc(c, &st.mp_vbits, (NM + 31) / 32 + 1);
-    dev_alloc(c, &st.kf_dirty, NK + 1);
-    dev_alloc(c, &st.cams, n_cams);
-    std::vector<DevCam> dc(n_cams);
-    for (int i = 0; i < n_cams; ++i) {
-      const lc_camera& k = cams[i];
-      DevCam& d = dc[i];
-      memset(&d, 0, sizeof(d));
-      d.model = k.model; d.cols = st.cols; d.rows = st.rows;
-      d.fx = k.fx; d.fy = k.fy; d.cx = k.cx; d.cy = k.cy;
-      for (int j = 0; j < 4; ++j) d.k[j] = k.k[j];
-      d.min_x = k.min_x; d.max_x = k.max_x; d.min_y = k.min_y; d.max_y = k.max_y;
-      for (int o = 0; o < LC_MAX_LEVELS; ++o) {
-        d.cell_sx[o] = (double)st.ocols[o] / (k.max_x - k.min_x);
-        d.cell_sy[o] = (double)st.orows[o] / (k.max_y - k.min_y);
-      }
+    if (gf) {
+      grow(c, &st.feat_mp, uf, NF, 0, cf, s);
+      grow(c, &st.feat_angle, uf, NF, 0, cf, s);
+      grow(c, &st.feat_cpos, uf, NF, 0, cf, s);
+      st.cap_feat = cf;
     }
-    CK(cudaMemcpyAsync(st.cams, dc.data(), sizeof(DevCam) * n_cams, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(st.kf_fbeg, fbeg.data(), sizeof(int32_t) * (NK + 1), cudaMemcpyHostToDevice, s));
+    if (gp) {
+      grow(c, &st.fc_uv, up, NP, 0, cp, s);
+      grow(c, &st.fc_meta, up, NP, 0, cp, s);
+      grow(c, &st.fc_desc, 2 * up, 2 * NP, 0, 2 * cp, s);
+      st.cap_fpad = cp;
+    }
+    if (gm) {
+      grow(c, &st.mp_rec, um, NM, 0, cm, s);
+      grow(c, &st.mp_flags, um, NM, 0, cm, s);
+      grow(c, &st.mp_ref_kf, um, NM, 0, cm, s);
+      grow(c, &st.mp_replaced_by, um, NM, 0, cm, s);
+      grow(c, &st.mp_nobs, um, NM, 0, cm, s);
+      grow(c, &st.mp_corr_ref, um, NM, 0, cm, s);
+      grow(c, &st.mp_loop_ep, um, NM, 0, cm, s);
+      grow(c, &st.mp_owner, um, NM, 0, cm, s);
+      grow(c, &st.mp_vbits, append ? (um + 31) / 32 : 0, (NM + 31) / 32 + 1, 0, (cm + 31) / 32 + 1, s);
+      st.cap_mp = cm;
+    }
+    if (!append) {
+      dev_alloc(c, &st.ep, 2);
+      dev_alloc(c, &st.cams, n_cams);
+      std::vector<DevCam> dc(n_cams);
+      for (int i = 0; i < n_cams; ++i) {
+        const lc_camera& k = cams[i];
+        DevCam& d = dc[i];
+        memset(&d, 0, sizeof(d));
+        d.model = k.model; d.cols = st.cols; d.rows = st.rows;
+        d.fx = k.fx; d.fy = k.fy; d.cx = k.cx; d.cy = k.cy;
+        for (int j = 0; j < 4; ++j) d.k[j] = k.k[j];
+        d.min_x = k.min_x; d.max_x = k.max_x; d.min_y = k.min_y; d.max_y = k.max_y;
+        for (int o = 0; o < LC_MAX_LEVELS; ++o) {
+          d.cell_sx[o] = (double)st.ocols[o] / (k.max_x - k.min_x);
+          d.cell_sy[o] = (double)st.orows[o] / (k.max_y - k.min_y);
+        }
+      }
+      CK(cudaMemcpyAsync(st.cams, dc.data(), sizeof(DevCam) * n_cams, cudaMemcpyHostToDevice, s));
+      CK(cudaMemsetAsync(st.ep, 0, sizeof(uint32_t) * 2, s));
+    }
+    st.n_kf = (int32_t)NK; st.n_feat = (int32_t)NF; st.n_mp = (int32_t)NM;
+    st.n_fpad = NPad;
+    st.max_F = std::max(st.max_F, max_F);
+    for (int k = 0; k < m->n_kf; ++k) st.h_fbeg.push_back(f0 + fbeg[k + 1]);
+    st.h_in_win.resize(NK, 0);
+    // new keyframe / feature / map-point entries
+    const size_t nk = m->n_kf, nf = m->n_feat, nm = m->n_mp;
+    std::vector<int32_t> fbeg_g(nk + 1), fpad_g(nk + 1);
+    for (size_t k = 0; k <= nk; ++k) { fbeg_g[k] = f0 + fbeg[k]; fpad_g[k] = fpad_new[k]; }
+    CK(cudaMemsetAsync(st.kf_cell + (size_t)kf0 * st.Gs, 0, sizeof(uint16_t) * nk * st.Gs, s));
+    CK(cudaMemsetAsync(st.fc_uv + fp0, 0, sizeof(float2) * (size_t)(NP - fp0), s));
+    CK(cudaMemsetAsync(st.fc_meta + fp0, 0, sizeof(uint32_t) * (size_t)(NP - fp0), s));
+    if (nk) {
+      CK(cudaMemcpyAsync(st.kf_fpad + kf0, fpad_g.data(), sizeof(int32_t) * (nk + 1), cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(st.kf_fbeg + kf0, fbeg_g.data(), sizeof(int32_t) * (nk + 1), cudaMemcpyHostToDevice, s));
+    }
     auto copy_in = [&](void* dst, const void* src, size_t bytes) {
-      if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
+      if (!bytes) return;
+      if (is_device_ptr(c, src)) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+      else call.upload(dst, src, bytes);
     };
-    copy_in(st.kf_pose, m->kf_pose, sizeof(double) * 13 * NK);
-    copy_in(st.kf_cam, m->kf_cam, sizeof(int32_t) * NK);
-    copy_in(st.feat_mp, m->feat_mp, sizeof(int32_t) * NF);
-    copy_in(st.feat_angle, m->feat_angle, sizeof(float) * NF);
-    copy_in(st.mp_flags, m->mp_flags, NM);
-    copy_in(st.mp_ref_kf, m->mp_ref_kf, sizeof(int32_t) * NM);
-    CK(cudaMemsetAsync(st.kf_S_corr, 0, sizeof(double) * 13 * NK, s));
-    CK(cudaMemsetAsync(st.kf_in_win, 0, sizeof(int32_t) * NK, s));
-    CK(cudaMemsetAsync(st.kf_win_ep, 0, sizeof(uint32_t) * NK, s));
-    CK(cudaMemsetAsync(st.ep, 0, sizeof(uint32_t) * 2, s));
-    c->ep_used = 0;
+    copy_in(st.kf_pose + 13 * (size_t)kf0, m->kf_pose, sizeof(double) * 13 * nk);
+    copy_in(st.kf_cam + kf0, m->kf_cam, sizeof(int32_t) * nk);
+    copy_in(st.feat_mp + f0, m->feat_mp, sizeof(int32_t) * nf);
+    copy_in(st.feat_angle + f0, m->feat_angle, sizeof(float) * nf);
+    copy_in(st.mp_flags + mp0, m->mp_flags, nm);
+    copy_in(st.mp_ref_kf + mp0, m->mp_ref_kf, sizeof(int32_t) * nm);
+    if (nk) {
+      CK(cudaMemsetAsync(st.kf_S_corr + 13 * (size_t)kf0, 0, sizeof(double) * 13 * nk, s));
+      CK(cudaMemsetAsync(st.kf_in_win + kf0, 0, sizeof(int32_t) * nk, s));
+      CK(cudaMemsetAsync(st.kf_win_ep + kf0, 0, sizeof(uint32_t) * nk, s));
+    }
     // raw SoA inputs the packing kernels read (device pointers used in place)
-    const float* pos = call.in(m->mp_pos, 3 * NM);
-    const float* nrm = call.in(m->mp_normal, 3 * NM);
-    const float* dmx = call.in(m->mp_max_dist, NM);
-    const uint8_t* mdesc = call.in(m->mp_desc, 32 * NM);
-    const float* ang = call.in(m->mp_angle, NM);
-    const float* fuv = call.in(m->feat_uv, 2 * NF);
-    const uint8_t* foct = call.in(m->feat_octave, NF);
-    const uint8_t* fdesc = call.in(m->feat_desc, 32 * NF);
+    const float* pos = call.in(m->mp_pos, 3 * nm);
+    const float* nrm = call.in(m->mp_normal, 3 * nm);
+    const float* dmx = call.in(m->mp_max_dist, nm);
+    const uint8_t* mdesc = call.in(m->mp_desc, 32 * nm);
+    const float* ang = call.in(m->mp_angle, nm);
+    const float* fuv = call.in(m->feat_uv, 2 * nf);
+    const uint8_t* foct = call.in(m->feat_octave, nf);
+    const uint8_t* fdesc = call.in(m->feat_desc, 32 * nf);
     uint32_t* d_errs = (uint32_t*)call.scratch(64);
     CK(cudaMemsetAsync(d_errs, 0, 64, s));
     {
       Prof pr(c, LC_PROF_UPLOAD, s);
-      CK(launch_upload_pack(c, pos, nrm, dmx, mdesc, ang, fuv, foct, fdesc, d_errs, s));
+      CK(launch_upload_pack(c, kf0, f0, mp0, pos, nrm, dmx, mdesc, ang, fuv, foct, fdesc, d_errs, s));
     }
     uint32_t errs[16];
     CK(cudaMemcpyAsync(errs, d_errs, 64, cudaMemcpyDeviceToHost, s));

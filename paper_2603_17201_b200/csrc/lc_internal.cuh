@@ -56,6 +56,9 @@ struct Store {
   int64_t n_fpad = 0;    // padded feature count of the cell-major arrays
   double scale[LC_MAX_LEVELS];
   int32_t max_F = 0;
+  // capacities (entries) of the KF-, feature-, padded-feature- and MP-indexed device arrays:
+  // LC_UPLOAD_APPEND grows them geometrically
+  int64_t cap_kf = 0, cap_feat = 0, cap_fpad = 0, cap_mp = 0;
   // device arrays
   double* kf_pose = nullptr;
   int32_t* kf_cam = nullptr;
@@ -196,6 +199,13 @@ struct lc_ctx {
   cudaEvent_t pin_ev[kPinRing] = {};   // recorded after the H2D out of that slot
   bool pin_ev_pending[kPinRing] = {};
   int pin_next = 0;
+  // staging ring for pageable host inputs (Call::upload): chunks of kStageChunk bytes
+  static constexpr int kStageRing = 4;
+  static constexpr size_t kStageChunk = size_t(8) << 20;
+  static constexpr size_t kStageMin = size_t(1) << 20;   // smaller pageable copies go direct
+  void* stg[kStageRing] = {};
+  cudaEvent_t stg_ev[kStageRing] = {};
+  int stg_next = 0;
   // saved state (lc_state_save)
   void* sv = nullptr;
   size_t sv_cap = 0;
@@ -324,10 +334,9 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 // ---------------------------------------------------------------------------
 // kernel launchers (defined in the .cu files)
 // ---------------------------------------------------------------------------
-cudaError_t launch_upload_pack(lc_ctx* c, const float* pos, const float* nrm, const float* dmax,
-                               const uint8_t* desc, const float* ang, const float* fuv,
-                               const uint8_t* foct, const uint8_t* fdesc, uint32_t* d_errs,
-                               cudaStream_t s);
+cudaError_t launch_upload_pack(lc_ctx* c, int kf0, int f0, int mp0, const float* pos, const float* nrm,
+                               const float* dmax, const uint8_t* desc, const float* ang, const float* fuv,
+                               const uint8_t* foct, const uint8_t* fdesc, uint32_t* d_errs, cudaStream_t s);
 cudaError_t launch_match(lc_ctx* c, int mode, const MatchArgs& a, int n_blocks, int F_max, int part,
                          cudaStream_t s, bool pdl = true);  // part 0: k_project, 1: k_match; blocks [a.blk_base, +n_blocks)
 // winner words [0, n_wfeat) are set to NONE except [skip_lo, skip_hi) (sole-mode units)

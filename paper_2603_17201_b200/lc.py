@@ -205,7 +205,9 @@ class Context:
         torch.cuda.current_stream(self.device).synchronize()
 
     # -- lc_upload_map ------------------------------------------------------------
-    def upload_map(self, arrays: dict, cams, n_levels=8, scale_factor=1.2, grid=(64, 48)):
+    def upload_map(self, arrays: dict, cams, n_levels=8, scale_factor=1.2, grid=(64, 48), append=False):
+        """lc_upload_map: the whole map (REPLACE), or with append=True new keyframes / map
+        points after the stored ones (feat_mp / mp_ref_kf in store indices)."""
         k = _Keep()
         a = arrays
         v = _lib.lc_map_view()
@@ -222,11 +224,19 @@ class Context:
         cams = list(cams) if isinstance(cams, (list, tuple)) else [cams]
         carr = (_lib.lc_camera * len(cams))(*[camera_struct(c) for c in cams])
         prm = _lib.lc_map_params(int(n_levels), int(grid[0]), int(grid[1]), 0, float(scale_factor))
-        st = self.lib.lc_upload_map(self.h, C.byref(v), carr, len(cams), C.byref(prm), self._stream())
+        flags = _lib.LC_UPLOAD_APPEND if append else _lib.LC_UPLOAD_REPLACE
+        st = self.lib.lc_upload_map(self.h, C.byref(v), carr, len(cams), C.byref(prm), flags, self._stream())
         self._check("lc_upload_map", st)
-        self.n_kf, self.n_feat, self.n_mp = v.n_kf, v.n_feat, v.n_mp
         fb = a["kf_feat_begin"]
-        self.kf_feat_begin = (fb.cpu().numpy() if isinstance(fb, torch.Tensor) else np.asarray(fb)).astype(np.int64)
+        fb = (fb.cpu().numpy() if isinstance(fb, torch.Tensor) else np.asarray(fb)).astype(np.int64)
+        if append and getattr(self, "kf_feat_begin", None) is not None:
+            self.kf_feat_begin = np.r_[self.kf_feat_begin, self.kf_feat_begin[-1] + fb[1:]]
+            self.n_kf += v.n_kf
+            self.n_feat += v.n_feat
+            self.n_mp += v.n_mp
+        else:
+            self.n_kf, self.n_feat, self.n_mp = v.n_kf, v.n_feat, v.n_mp
+            self.kf_feat_begin = fb
 
     def n_feat_of(self, kfs):
         if self.kf_feat_begin is None:   # no map: the library reports LC_ESTATE

@@ -1,6 +1,7 @@
 """GPU (liblc) vs CPU oracle for the round-2 boundary additions: forced loop matches in
 lc_fuse (O9.4 / A23), lc_correct_sim3(WINDOW | DRY_RUN) batches (O3', SURVEY.md §8(d)
-C4), the edge-ambiguous counter (§8(c) O11) at constructed distances. Bars as in
+C4), the edge-ambiguous counter (§8(c) O11) at constructed distances, and the per-keyframe
+LC_UPLOAD_APPEND store against one REPLACE upload. Bars as in
 test_gpu_parity.py: index tables, counters and maps bit-exact; fp64 Sim3 results and
 fp32 positions bit-exact (same expression order, -fmad=false / -ffp-contract=off)."""
 import functools
@@ -191,3 +192,88 @@ def test_edge_counter_constructed(Ctx, fu, fv, x):
     g = ctx.fuse([0], np.array([0], np.int32), (4, 50, 0, 0, 0), window_S=tm.IDENT[None])
     assert g["counts"] == o["counts"]
     ctx.close()
+
+
+def _chunks(w, n_chunks):
+    """Split a world's map into keyframe chunks with the map points whose reference
+    keyframe falls in the chunk (map points are ordered by reference keyframe, and a point's
+    observers come at or after it, so every chunk references only stored points)."""
+    a = {k: np.asarray(v) for k, v in w.map_arrays().items()}
+    ref = a["mp_ref_kf"]
+    assert np.all(np.diff(ref) >= 0)
+    fb = a["kf_feat_begin"]
+    cuts = np.linspace(0, len(fb) - 1, n_chunks + 1).astype(int)
+    out = []
+    for k0, k1 in zip(cuts[:-1], cuts[1:]):
+        m0, m1 = np.searchsorted(ref, k0), np.searchsorted(ref, k1)
+        f0, f1 = fb[k0], fb[k1]
+        out.append(dict(kf_pose=a["kf_pose"][k0:k1], kf_cam=a["kf_cam"][k0:k1],
+                        kf_feat_begin=(fb[k0:k1 + 1] - f0).astype(np.int32),
+                        feat_uv=a["feat_uv"][f0:f1], feat_octave=a["feat_octave"][f0:f1],
+                        feat_angle=a["feat_angle"][f0:f1], feat_desc=a["feat_desc"][f0:f1],
+                        feat_mp=a["feat_mp"][f0:f1], mp_pos=a["mp_pos"][m0:m1], mp_normal=a["mp_normal"][m0:m1],
+                        mp_max_dist=a["mp_max_dist"][m0:m1], mp_desc=a["mp_desc"][m0:m1],
+                        mp_angle=a["mp_angle"][m0:m1], mp_ref_kf=a["mp_ref_kf"][m0:m1],
+                        mp_flags=a["mp_flags"][m0:m1]))
+    return out
+
+
+@pytest.mark.parametrize("name,n_chunks", [("T5", 7), ("C2", 25), ("S3", 40)])
+def test_upload_append_equals_replace(Ctx, name, n_chunks):
+    """PAPER.md:147-148 §IV.A ("transfer each newly created keyframe to GPU-resident
+    KeyFrame Storage"): N LC_UPLOAD_APPEND calls give the store one LC_UPLOAD_REPLACE of
+    the whole map gives -- downloaded state equal byte for byte, and the same loop event
+    (WINDOW correction, fuse, ALL propagation) produces identical tables and maps."""
+    w = world(name)
+    ref = Ctx(0)
+    ref.upload_map(w.map_arrays(), [w.cam])
+    app = Ctx(0)
+    parts = _chunks(w, n_chunks)
+    app.upload_map(parts[0], [w.cam])
+    for part in parts[1:]:
+        app.upload_map(part, [w.cam], append=True)
+    assert (app.n_kf, app.n_feat, app.n_mp) == (ref.n_kf, ref.n_feat, ref.n_mp)
+    a, r = app.download_map(), ref.download_map()
+    for key in r:
+        assert np.array_equal(a[key], r[key]), key
+    out = []
+    for ctx in (app, ref):
+        ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+        g = ctx.fuse(w.window, w.mp_list, FUSE_PARAMS_CHECKS, window_S=w.win_S, win_list_begin=w.win_list_begin,
+                     debug=True)
+        ctx.correct_all(w.S_opt)
+        out.append((g, ctx.download_map()))
+    (ga, ma), (gr, mr) = out
+    for key in ("winner", "victim", "action", "best", "ncand"):
+        assert np.array_equal(ga[key], gr[key]), key
+    assert ga["counts"] == gr["counts"]
+    for key in mr:
+        assert np.array_equal(ma[key], mr[key]), key
+    app.close()
+    ref.close()
+
+
+def test_upload_pinned_and_pageable_and_append_errors(Ctx):
+    from paper_2603_17201_b200 import _lib
+    from paper_2603_17201_b200._lib import LcError
+    w = world("C2")
+    arrays = w.map_arrays()
+    pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in arrays.items()}
+    c1, c2 = Ctx(0), Ctx(0)
+    c1.upload_map(arrays, [w.cam])       # pageable: through the staging ring (> 1 MB arrays)
+    c2.upload_map(pinned, [w.cam])       # page-locked: direct
+    a, b = c1.download_map(), c2.download_map()
+    for key in a:
+        assert np.array_equal(a[key], b[key]), key
+    c3 = Ctx(0)
+    with pytest.raises(LcError) as e:
+        c3.upload_map(arrays, [w.cam], append=True)
+    assert e.value.status == _lib.LC_ESTATE
+    bad = _chunks(w, 2)[1]
+    bad = dict(bad, feat_mp=np.full_like(bad["feat_mp"], 10 ** 7))
+    c3.upload_map(_chunks(w, 2)[0], [w.cam])
+    with pytest.raises(LcError) as e:
+        c3.upload_map(bad, [w.cam], append=True)
+    assert e.value.status == _lib.LC_ERANGE
+    for c in (c1, c2, c3):
+        c.close()
