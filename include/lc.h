@@ -282,7 +282,9 @@ lc_status lc_refresh_mappoints(lc_ctx* ctx, int32_t n, const int32_t* mp_idx, in
  *   weight(k, k2) = number of distinct non-bad map points held by both k and k2 != k;
  *   edges: every k2 with weight >= th, or, if there is none, the single strongest
  *   (max weight, lowest id); ordered by weight descending, then keyframe id.
- *   out_n [host|dev] [n]: number of edges of row i (may exceed max_edges);
+ *   out_n [host|dev] [n]: number of edges of row i (may exceed max_edges; any number
+ *   of edges is ranked exactly -- the first 2048 in shared memory, beyond that against
+ *   the weight array);
  *   out_kf, out_w [host|dev] nullable, [n][max_edges]: the first min(out_n[i],
  *   max_edges) edges of row i (the rest of the row is left unchanged).
  *   out_counts [host|dev] nullable, [LC_NCOUNT] (CONN_KF, CONN_EDGES).

@@ -103,7 +103,22 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_connections(const ConnArgs a) {
       ne = s_best >= 0 ? 1 : 0;
     }
     // A40: rank of each edge key (distinct keys) -> output slot
-    const int nr = min(ne, EDGE_CAP);
+    if (ne > EDGE_CAP) {   // rare: more edges than the shared list holds -> rank every edge
+      for (int k2 = threadIdx.x; k2 < a.n_kf; k2 += blockDim.x) {   // against the weight array itself
+        const int w = s_w[k2];
+        if (w < a.th) continue;
+        int r = 0;
+        for (int j = 0; j < a.n_kf && r < a.max_edges; ++j) {
+          const int wj = s_w[j];
+          r += (wj >= a.th) && (wj > w || (wj == w && j < k2));
+        }
+        if (r < a.max_edges && a.out_kf) {
+          a.out_kf[(size_t)t * a.max_edges + r] = k2;
+          a.out_w[(size_t)t * a.max_edges + r] = w;
+        }
+      }
+    }
+    const int nr = ne > EDGE_CAP ? 0 : ne;
     for (int e = threadIdx.x; e < nr; e += blockDim.x) {
       const unsigned long long key = s_e[e];
       int r = 0;

@@ -256,3 +256,16 @@ def test_two_components_each_with_a_fixed_vertex(ctx, solver):
     M = np.concatenate([g1.M, g2.M])
     gr = ctx.pgo_sim3(S0, fixed, E, M, max_iter=30, solver=solver, **TIGHT)
     compare(gr, oracle.pgo(S0, fixed, E, M, max_iter=30))
+
+
+@pytest.mark.slow
+def test_pgo_matches_oracle_C2_graph(ctx):
+    """The 300-keyframe EuRoC-shaped C2 essential graph (2,093 unknowns) against oracle O15
+    (dense LDL^T, ~1 s per iteration), banded solver, the same tolerance as the small
+    graphs: decisions, lambda schedule, iteration count and stop reason exactly, chi2 and
+    |delta| per iteration to 1e-6, estimates to 1e-8."""
+    g = make_pose_graph("C2", 0)
+    gr = ctx.pgo_sim3(g.S_init, g.fixed, g.edges, g.M, max_iter=10, solver="band", **TIGHT)
+    orr = oracle.pgo(g.S_init, g.fixed, g.edges, g.M, max_iter=10)
+    compare(gr, orr)
+    assert gr[3]["pgo_band"] > 0

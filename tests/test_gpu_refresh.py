@@ -122,3 +122,28 @@ def test_connections_spec_example_on_gpu(Ctx):
     n, kf, wt, c = ctx.update_connections(None, th=5, max_edges=4)
     assert list(n) == [2, 1, 1, 0]
     assert list(kf[0, :2]) == [1, 2] and list(wt[0, :2]) == [20, 5]
+
+
+def test_connections_more_edges_than_the_shared_list():
+    """A keyframe covisible with 2500 others (> the 2048-edge shared list): the exact
+    ranking path (weight desc, id asc) against oracle O12."""
+    from paper_2603_17201_b200 import Context
+    import oracle
+    from tests import tinymap as tm
+    n = 2500
+    d = np.zeros(32, np.uint8)
+    central = dict(feats=[dict(u=float(i % 400), v=float(i // 400), desc=d, mp=i) for i in range(n)])
+    others = [dict(feats=[dict(u=10.0, v=10.0, desc=d, mp=i)] + ([dict(u=20.0, v=10.0, desc=d, mp=(i + 1) % n)]
+                                                                  if i % 7 == 0 else [])) for i in range(n)]
+    mps = [dict(pos=(0.0, 0.0, 1.0), desc=d) for _ in range(n)]
+    arrays = tm.build([central] + others, mps)
+    om = oracle.OracleMap(arrays=arrays, cams=[tm.PIN])
+    on, okf, ow, _ = om.update_connections(None, th=1, max_edges=64)
+    ctx = Context(0)
+    ctx.upload_map(arrays, [tm.PIN])
+    gn, gkf, gw, _ = ctx.update_connections(None, th=1, max_edges=64)
+    assert on[0] == n and np.array_equal(gn, on)
+    for i in range(len(on)):
+        m = min(int(on[i]), 64)
+        assert np.array_equal(gkf[i, :m], okf[i, :m]) and np.array_equal(gw[i, :m], ow[i, :m]), i
+    ctx.close()
