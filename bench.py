@@ -297,7 +297,8 @@ def main():
               "bytes": int(sum(np.asarray(v).nbytes for v in arrays.values()))}
     ctx.state_save()
 
-    mp_list_d = torch.from_numpy(w.mp_list).to(dev)
+    mp_list_d = torch.from_numpy(w.mp_list).to(dev)   # the loop event's inputs, resident in HBM
+    win_S_d = torch.from_numpy(np.ascontiguousarray(w.win_S)).to(dev)
     S_opt_d = torch.from_numpy(w.S_opt).to(dev)
     n_wfeat = ctx.n_feat_of(w.window)
     tables = torch.empty(n_wfeat + w.n_mp, dtype=torch.int64, device=dev)
@@ -314,12 +315,12 @@ def main():
         _, cw = ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
         cnt_window[:] = [cw]
         if ws == 1:
-            r = ctx.fuse(w.window, mp_list_d, params, window_S=w.win_S,
+            r = ctx.fuse(w.window, mp_list_d, params, window_S=win_S_d,
                          win_list_begin=w.win_list_begin, winner=win_t, victim=vic_t,
                          action=False, host=False)
             c = r["counts"]
         else:
-            c, _, info = lcdist.fuse_sharded(ctx, w.window, mp_list_d, params, window_S=w.win_S,
+            c, _, info = lcdist.fuse_sharded(ctx, w.window, mp_list_d, params, window_S=win_S_d,
                                              win_list_begin=w.win_list_begin, device=dev, tables=tables,
                                              events=comm_ev[0] if comm_ev else None)
             last_info.update(info)
@@ -370,7 +371,6 @@ def main():
     torch.cuda.synchronize()
     clocks = Clocks(local)
     l0 = ctx.kernel_launches()
-    ctx.profile_enable(True)
     comm_pairs = []
     for i in range(args.steps):
         reset()
@@ -384,10 +384,17 @@ def main():
     comm_ev.clear()
     if ws > 1:
         tdist.barrier()
+    launches_timed = ctx.kernel_launches() - l0   # (the untimed state restores are copies, not launches)
+    clk = clocks.stop()
+    # per-kernel device times (lc_profile CUDA events around each launch group) from a
+    # second, identical pass -- kept out of the timed steps so they carry no instrumentation
+    ctx.profile_enable(True)
+    for i in range(args.steps):
+        reset()
+        step()
+    torch.cuda.synchronize()
     prof = ctx.profile_read()
     ctx.profile_enable(False)
-    launches_timed = ctx.kernel_launches() - l0 - prof["state"][1]
-    clk = clocks.stop()
     ms = np.array([a.elapsed_time(b) for a, b in ev])
     ms_mean = float(ms.mean())
     ms_t = torch.tensor([ms_mean], dtype=torch.float64, device=dev)

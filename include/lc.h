@@ -506,7 +506,7 @@ lc_status lc_correct_sim3(lc_ctx* ctx, int32_t mode, int32_t n_batch, const int3
  * phase LC_FUSE_APPLY : apply from io_winner / io_victim (e.g. after an NCCL MIN
  *                       all-reduce of the shards' tables). w_lo / w_hi ignored.
  * phase LC_FUSE_ALL   : PLAN over the whole window, then APPLY.
- *   window_kf, window_S (nullable), win_list_begin (nullable) [host], n_window >= 1
+ *   window_kf, win_list_begin (nullable) [host]; window_S (nullable) [host|dev]; n_window >= 1
  *   distinct keyframes; mp_list [host|dev] n_list entries, each list ascending
  *   and unique (not checked on device; duplicates give duplicate queries).
  *   A host mp_list with per-keyframe lists (win_list_begin) on a full-range PLAN

@@ -162,7 +162,7 @@ cudaError_t launch_connections(lc_ctx* c, int n_sel, const int32_t* d_idx, int t
     c->launches++;
   }
   const size_t smem = sizeof(int32_t) * (size_t)std::max(st.n_kf, 1);
-  cudaError_t e = cudaFuncSetAttribute(k_connections, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_attr((const void*)k_connections, (int)smem);
   if (e != cudaSuccess) return e;
   k_connections<<<std::min(n_sel, 148 * 4), LC_NTHREADS, smem, s>>>(a);
   c->launches++;

@@ -144,6 +144,9 @@ constexpr int NWARP = LC_NTHREADS / 32;
 #ifndef LC_KM_MINB
 #define LC_KM_MINB 3      // k_match CTAs per SM the register budget is cut for
 #endif
+#ifndef LC_KM_B
+#define LC_KM_B 2         // k_match window scan: features per batch of shared-memory loads
+#endif
 #ifndef LC_KP_MINB
 #define LC_KP_MINB 4      // k_project CTAs per SM the register budget is cut for
 #endif
@@ -631,17 +634,17 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         const int cy1 = min(orr - 1, (int)floorf((e.fv + fr + 0.01f - fminy) * fsy));
         for (int cy = cy0; cy <= cy1; ++cy) {
           const int ps = s_cell[ob + cy * oc + cx0], pe = s_cell[ob + cy * oc + cx1 + 1];
-          for (int p0 = ps; p0 < pe; p0 += 4) {   // 4 features' loads issued together
-            uint32_t mt[4];
-            float2 fuv[4];
+          for (int p0 = ps; p0 < pe; p0 += LC_KM_B) {   // LC_KM_B features' loads issued together
+            uint32_t mt[LC_KM_B];
+            float2 fuv[LC_KM_B];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < LC_KM_B; ++t) {
               const int pp = min(p0 + t, pe - 1);
-              mt[t] = s_meta[pp];
+              if (MODE == 1) mt[t] = s_meta[pp];   // (the octave is implicit in the grid)
               fuv[t] = s_uv[pp];
             }
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < LC_KM_B; ++t) {
               if (p0 + t >= pe) break;
               if (MODE == 1 && (mt[t] & 0x80000000u)) continue;
               const int w = win_f32(fuv[t], e.fu, e.fv, fr);
@@ -1498,27 +1501,21 @@ cudaError_t launch_match_t(const MatchArgs& a, int n_blocks, int part, bool pdl,
   };
   if (part == 0) {
     const int hb = HashSize<FCAP>::HS * (int)sizeof(int32_t) + 3 * LC_NTHREADS * 32;   // hash + record ring
-    cudaError_t e = cudaFuncSetAttribute(k_project<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, hb);
+    cudaError_t e = set_smem_attr((const void*)k_project<MODE, FCAP>, hb);
     if (e != cudaSuccess) return e;
     return go(k_project<MODE, FCAP>, (size_t)hb);
   }
   if (MODE == 0 && a.sole == 2 && FCAP <= 4096) {
     using SS = SoleSmem<FCAP>;
     const size_t smem = (size_t)SS::CELL + (((size_t)a.Gs * 2 + 15) & ~(size_t)15);
-    cudaError_t e = cudaFuncSetAttribute(k_match_sole<FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_match_sole<FCAP>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
+    cudaError_t e = set_smem_attr((const void*)k_match_sole<FCAP>, (int)smem, true);
     if (e != cudaSuccess) return e;
     if (pdl) return launch_pdl(k_match_sole<FCAP>, dim3(n_blocks), dim3(LC_SOLE_NT), smem, s, a);
     k_match_sole<FCAP><<<n_blocks, LC_SOLE_NT, smem, s>>>(a);
     return cudaGetLastError();
   }
   const size_t smem = (size_t)SM::CELL + (((size_t)a.Gs * 2 + 15) & ~(size_t)15);
-  cudaError_t e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_match<MODE, FCAP>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           cudaSharedmemCarveoutMaxShared);
+  cudaError_t e = set_smem_attr((const void*)k_match<MODE, FCAP>, (int)smem, true);
   if (e != cudaSuccess) return e;
   return go(k_match<MODE, FCAP>, smem);
 }
@@ -1602,7 +1599,7 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
     const int H = ((Fm + Fm / 2 + 1) + 31) & ~31;
     size_t smem = (size_t)H * 8 + (size_t)(1 << (FILT_LOG2 - 3)) + (size_t)Fm * 9 + 16;
     smem = (smem + 15) & ~(size_t)15;
-    e = cudaFuncSetAttribute(k_apply_fix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = set_smem_attr((const void*)k_apply_fix, (int)smem);
     if (e != cudaSuccess) return e;
     e = launch_pdl(k_apply_fix, dim3(std::min(st.n_kf, 148 * 4)), dim3(LC_NTHREADS), smem, s,
                    (const uint32_t*)st.ep, (const int32_t*)st.kf_fbeg, (const uint32_t*)st.kf_win_ep,

@@ -199,8 +199,7 @@ cudaError_t launch_upload_pack(lc_ctx* c, int kf0, int f0, int mp0, const float*
   if (n_kf > 0) {
     size_t smem = sizeof(int) * (size_t)(st.G + 1) + 2 * sizeof(uint16_t) * (size_t)st.max_F;
     smem = (smem + 15) & ~(size_t)15;
-    cudaError_t e = cudaFuncSetAttribute(k_grid_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = set_smem_attr((const void*)k_grid_build, (int)smem);
     if (e != cudaSuccess) return e;
     MatchArgs g;   // only the per-octave grid dims are read
     memset(&g, 0, sizeof(g));

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -68,12 +69,15 @@ struct Call {
   lc_ctx* c;
   cudaStream_t s;
   int slot = 0;
-  std::vector<char> args;                 // host argument block
+  std::vector<char>& args;                // host argument block (the context's, capacity kept)
   std::vector<std::pair<const void**, size_t>> arg_fix;   // (where to store dev ptr, offset)
   std::vector<lc_ctx::HostOut> outs;
   char* d_args = nullptr;
 
-  Call(lc_ctx* ctx, void* stream) : c(ctx), s((cudaStream_t)stream) {}
+  Call(lc_ctx* ctx, void* stream) : c(ctx), s((cudaStream_t)stream), args(ctx->arg_host) {
+    args.clear();
+    if (args.capacity() < (size_t(1) << 20)) args.reserve(size_t(1) << 20);
+  }
 
   void* scratch(size_t bytes) {
     bytes = std::max<size_t>(round_up(bytes, 256), 256);
@@ -240,6 +244,30 @@ struct Call {
   void finish() {
     for (auto& o : outs) CK(cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDefault, s));
     CK(cudaGetLastError());
+  }
+};
+
+// LC_HOST_PROF=1: host-side time of a call's phases to stderr (enqueue-cost analysis)
+struct HostProf {
+  bool on;
+  const char* name;
+  std::chrono::steady_clock::time_point t0, t;
+  std::string line;
+  HostProf(lc_ctx*, const char* n) : on(getenv("LC_HOST_PROF") != nullptr), name(n) {
+    if (on) t0 = t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    auto n = std::chrono::steady_clock::now();
+    line += std::string(" ") + what + "=" +
+            std::to_string(std::chrono::duration<double, std::micro>(n - t).count()).substr(0, 6);
+    t = n;
+  }
+  ~HostProf() {
+    if (!on) return;
+    auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[host] %s us:%s total=%.1f\n", name, line.c_str(),
+            std::chrono::duration<double, std::micro>(n - t0).count());
   }
 };
 
@@ -1285,6 +1313,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
                   int64_t* io_winner, int64_t* io_victim, int8_t* out_action,
                   const lc_query_debug* dbg, int64_t* out_counts, void* stream) {
   return guarded(c, [&] {
+    HostProf hp(c, "lc_fuse");
     capture_gate(c, stream, true);
     REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
     REQUIRE(phase == LC_FUSE_PLAN || phase == LC_FUSE_APPLY || phase == LC_FUSE_ALL, LC_EINVAL, "bad phase");
@@ -1292,6 +1321,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     REQUIRE(n_list >= 0 && (n_list == 0 || mp_list), LC_EINVAL, "bad mp_list");
     Store& st = c->st;
     mark_window(c, n_window, window_kf);
+    hp.mark("mark");
     if (phase != LC_FUSE_PLAN) { w_lo = 0; w_hi = n_window; }
     if (phase == LC_FUSE_APPLY) { w_lo = w_hi = 0; }
     REQUIRE(0 <= w_lo && w_lo <= w_hi && w_hi <= n_window, LC_EINVAL, "bad shard range");
@@ -1350,6 +1380,9 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     const int64_t ch = sole ? std::max<int64_t>(max_len, 1) : pick_chunk(total_q);
     std::vector<int32_t> bunit;
     std::vector<int64_t> bq0, bq1;
+    bunit.reserve(w_hi - w_lo + 64);
+    bq0.reserve(w_hi - w_lo + 64);
+    bq1.reserve(w_hi - w_lo + 64);
     for (int i = w_lo; i < w_hi; ++i) {
       int64_t b = lbeg[i];
       int64_t e = b + (win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list);
@@ -1367,6 +1400,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     }
     std::vector<int64_t> boff(bunit.size() + 1, 0);
     for (size_t b = 0; b < bunit.size(); ++b) boff[b + 1] = boff[b] + (bq1[b] - bq0[b]);
+    hp.mark("blocks");
     MatchArgs a;
     memset(&a, 0, sizeof(a));
     fill_match_store(c, a);
@@ -1385,8 +1419,13 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     call.arg(bq1.data(), bq1.size(), &d_bq1);
     call.arg(params, 1, &d_prm);
     call.arg(boff.data(), boff.size(), &d_boff);
-    if (window_S) call.arg((const double*)window_S, 13 * (size_t)n_window, &d_S);
+    if (window_S) {   // device-resident transforms are used in place, host ones ride in the block
+      if (is_device_ptr(c, window_S)) d_S = (const double*)window_S;
+      else call.arg((const double*)window_S, 13 * (size_t)n_window, &d_S);
+    }
+    hp.mark("tables");
     call.commit();
+    hp.mark("commit");
     Surv* d_surv = (Surv*)call.scratch(sizeof(Surv) * std::max<int64_t>(boff.back(), 1));
     int32_t* d_scnt = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(bunit.size(), 1));
     const int32_t* d_list = nullptr;
@@ -1517,7 +1556,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       Prof pr(c, LC_PROF_APPLY, call.s);
       CK(launch_fuse_apply(c, d_woff, win, vic, cnt, call.s));
     }
-
+    hp.mark("launches");
     call.finish();
   });
 }

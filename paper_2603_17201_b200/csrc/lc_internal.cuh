@@ -19,7 +19,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "lc.h"
@@ -199,6 +201,7 @@ struct lc_ctx {
   cudaEvent_t pin_ev[kPinRing] = {};   // recorded after the H2D out of that slot
   bool pin_ev_pending[kPinRing] = {};
   int pin_next = 0;
+  std::vector<char> arg_host;   // the host argument block of the current call (reused)
   // staging ring for pageable host inputs (Call::upload): chunks of kStageChunk bytes
   static constexpr int kStageRing = 4;
   static constexpr size_t kStageChunk = size_t(8) << 20;
@@ -329,6 +332,22 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+// Kernel attributes are process-wide: set the dynamic shared-memory limit (and the
+// shared-memory carveout) of a kernel once per larger value instead of on every launch
+// (a driver call each; the host enqueue of a C5 fuse call was dominated by them).
+inline cudaError_t set_smem_attr(const void* fn, int bytes, bool carveout = false) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find(fn);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && carveout)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) done[fn] = bytes;
+  return e;
 }
 
 // ---------------------------------------------------------------------------

@@ -472,7 +472,8 @@ class Context:
         n_w = len(window)
         w_hi = n_w if w_hi is None else int(w_hi)
         wb = None if win_list_begin is None else np.ascontiguousarray(win_list_begin, np.int32)
-        wS = None if window_S is None else np.ascontiguousarray(window_S, np.float64)
+        wS = None if window_S is None else (window_S if isinstance(window_S, torch.Tensor)
+                                            else np.ascontiguousarray(window_S, np.float64))
         n_list = int(mp_list.shape[0]) if hasattr(mp_list, "shape") else len(mp_list)
         nwf = self.n_feat_of(window)
         nq = int(wb[-1]) if wb is not None else n_w * n_list
@@ -489,7 +490,7 @@ class Context:
             dd = dict(best=mk(nq, torch.int64, np.int64), uv=mk(2 * nq, torch.float64, np.float64),
                       ncand=mk(nq, torch.int32, np.int32))
             dbg = _lib.lc_query_debug(k.ptr(dd["best"]), k.ptr(dd["uv"]), k.ptr(dd["ncand"]))
-        st = self.lib.lc_fuse(self.h, int(phase), int(w_lo), int(w_hi), n_w, k.ptr(window), k.ptr(wS),
+        st = self.lib.lc_fuse(self.h, int(phase), int(w_lo), int(w_hi), n_w, k.ptr(window), k.ptr(wS, np.float64),
                               k.ptr(wb), k.ptr(mp_list, np.int32), n_list, C.byref(_params(params)),
                               int(cur_kf), k.ptr(forced_mp, np.int32),
                               k.ptr(winner), k.ptr(victim), k.ptr(act),

@@ -266,7 +266,8 @@ def test_device_and_host_pointer_paths_agree(Ctx):
     h = ctx.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
     ctx.state_restore()
     dev = torch.device("cuda:0")
-    d = ctx.fuse(w.window, torch.from_numpy(w.mp_list).to(dev), FUSE_PARAMS, window_S=w.win_S,
+    d = ctx.fuse(w.window, torch.from_numpy(w.mp_list).to(dev), FUSE_PARAMS,
+                 window_S=torch.from_numpy(np.ascontiguousarray(w.win_S)).to(dev),   # device-resident inputs
                  win_list_begin=w.win_list_begin, host=False)
     torch.cuda.synchronize()
     assert np.array_equal(h["winner"], d["winner"].cpu().numpy())
