@@ -222,6 +222,8 @@ class World:
     pair_list_begin: Optional[np.ndarray] = None
     pair_mp_list: Optional[np.ndarray] = None
     pair_taken: Optional[np.ndarray] = None      # (sum F(pair_kf),) i32, -1 free
+    list_src_begin: Optional[np.ndarray] = None  # loop lists = MPs of these keyframes (CSR)
+    list_src_kf: Optional[np.ndarray] = None
     hyp_cur: Optional[np.ndarray] = None         # C4: per hypothesis, its current keyframe
     hyp_S_cw: Optional[np.ndarray] = None        # (H, 13) its loop Sim3
     hyp_win_begin: Optional[np.ndarray] = None   # (H+1,) CSR into hyp_window
@@ -545,15 +547,21 @@ def make_world(name: str, seed: int = 0) -> World:
         matched = cur - K
         loop_kfs = [matched] + _top_covisible(covis, matched, cfg.loop_covis, lambda j: j < K)
         w.mp_list = _kf_mps(w, loop_kfs)
+        w.list_src_begin = np.asarray([0, len(loop_kfs)], np.int32)   # one shared list
+        w.list_src_kf = np.asarray(loop_kfs, np.int32)
     else:
         w.window = np.asarray([cur] + list(range(K, n_kf - 1)), np.int32)
-        lists, begin = [], [0]
+        lists, begin, src, sbeg = [], [0], [], [0]
         for k in w.window:
             j = int(k) - K
             nb = [(j + o) % K if cfg.closed else min(max(j + o, 0), K - 1) for o in range(-5, 6)]
             lst = _kf_mps(w, sorted(set(nb)))
             lists.append(lst)
             begin.append(begin[-1] + len(lst))
+            src += sorted(set(nb))
+            sbeg.append(len(src))
+        w.list_src_begin = np.asarray(sbeg, np.int32)   # the lists' source keyframes (CSR)
+        w.list_src_kf = np.asarray(src, np.int32)
         w.win_list_begin = np.asarray(begin, np.int32)
         w.mp_list = np.concatenate(lists).astype(np.int32)
         w.win_S = np.stack([_to13(_compose(_noise(rng, 1e-3), ideal[int(k)])) for k in w.window])

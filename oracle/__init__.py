@@ -86,6 +86,7 @@ def lib():
                    "orc_refresh", "orc_update_connections", "orc_sim3_ransac", "orc_sim3_refine", "orc_pgo",
                    "orc_correct_window_batch", "orc_fuse_plan_grid"):
             getattr(_lib, fn).restype = C.c_int
+        _lib.orc_loop_lists.restype = C.c_int64
         _lib.orc_grid_build.restype = C.c_void_p
         _lib.orc_grid_free.argtypes = [C.c_void_p]
     return _lib
@@ -344,6 +345,21 @@ class OracleMap:
             raise ValueError("orc_fuse: invalid arguments")
         return dict(winner=winner, victim=victim, action=action,
                     counts=dict(zip(COUNTER_NAMES, cnt.tolist())), **dbg)
+
+    # -- loop map-point lists ------------------------------------------------
+    def loop_lists(self, src_begin, src_kf):
+        """List l = ascending unique map points held by keyframes src_kf[src_begin[l]:src_begin[l+1]]:
+        returns (begin [n + 1], lists)."""
+        sb = np.ascontiguousarray(src_begin, np.int32)
+        sk = np.ascontiguousarray(src_kf, np.int32)
+        n = len(sb) - 1
+        cap = int(sum(self.n_feat_of(int(k)) for k in sk))
+        ob = np.zeros(n + 1, np.int32)
+        ol = np.zeros(max(cap, 1), np.int32)
+        tot = lib().orc_loop_lists(C.byref(self._m), C.c_int32(n), _p(sb), _p(sk), _p(ob), _p(ol), C.c_int64(cap))
+        if tot < 0:
+            raise ValueError("orc_loop_lists: invalid arguments")
+        return ob, ol[:tot]
 
     # -- timing-only grid / threaded PLAN (bench.py cpu_baseline) --------------
     def grid(self, cols=64, rows=48):

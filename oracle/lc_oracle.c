@@ -19,6 +19,8 @@
  *   - the same window correction as a batch of dry runs (no write-back), one per
  *     loop-candidate hypothesis (§IV.C: candidates in batches)
  *                                                               -> orc_correct_window_batch (O3')
+ *   - the loop map-point lists (MPs of the matched keyframe's covisibles), built
+ *     from the map (SURVEY.md §8(d) "Loop list")           -> orc_loop_lists
  *   - a thread-parallel, cell-grid version of the fuse PLAN for TIMING ONLY (the
  *     CPU baseline); it is tested equal to the brute-force definition
  *                                                               -> orc_fuse_plan_grid
@@ -709,6 +711,51 @@ int orc_fuse(orc_map *m, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t n_w,
   free(woff);
   free(qoff);
   return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Loop map-point lists ("Loop list = MPs of the matched pass-A KF */
+/* and its top-10 covisibles, ascending unique"; C5 "each has its own list: MPs of   */
+/* its 10 nearest pass-A KFs"; EXT LoopClosing: mvpLoopMapPoints = the map points of */
+/* the matched keyframe and its covisibles). List l = the ascending unique map points */
+/* (>= 0, bad ones included: the queries skip them, O4) held by the keyframes         */
+/* src_kf[src_begin[l] .. src_begin[l+1]). out_begin [n+1]; out_list >= the total.    */
+/* Returns the total, or -1 on bad arguments.                                         */
+/* ------------------------------------------------------------------------- */
+static int cmp_i32_asc(const void *a, const void *b) {
+  int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+  return (x > y) - (x < y);
+}
+
+int64_t orc_loop_lists(const orc_map *m, int32_t n, const int32_t *src_begin, const int32_t *src_kf,
+                       int32_t *out_begin, int32_t *out_list, int64_t capacity) {
+  if (n < 0 || (n > 0 && src_begin[0] != 0)) return -1;
+  int64_t total = 0;
+  out_begin[0] = 0;
+  for (int32_t l = 0; l < n; ++l) {
+    int64_t cnt = 0;
+    for (int32_t j = src_begin[l]; j < src_begin[l + 1]; ++j) {
+      int32_t k = src_kf[j];
+      if (k < 0 || k >= m->n_kf) return -1;
+      cnt += m->kf_feat_begin[k + 1] - m->kf_feat_begin[k];
+    }
+    int32_t *tmp = (int32_t *)malloc(sizeof(int32_t) * (size_t)(cnt > 0 ? cnt : 1));
+    int64_t t = 0;
+    for (int32_t j = src_begin[l]; j < src_begin[l + 1]; ++j)
+      for (int32_t f = m->kf_feat_begin[src_kf[j]]; f < m->kf_feat_begin[src_kf[j] + 1]; ++f)
+        if (m->feat_mp[f] >= 0) tmp[t++] = m->feat_mp[f];
+    qsort(tmp, (size_t)t, sizeof(int32_t), cmp_i32_asc);
+    int64_t u = 0;
+    for (int64_t i = 0; i < t; ++i)
+      if (i == 0 || tmp[i] != tmp[i - 1]) {
+        if (total + u < capacity) out_list[total + u] = tmp[i];
+        ++u;
+      }
+    free(tmp);
+    total += u;
+    out_begin[l + 1] = (int32_t)total;
+  }
+  return total;
 }
 
 /* ------------------------------------------------------------------------- */

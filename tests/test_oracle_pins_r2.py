@@ -341,3 +341,33 @@ def test_grid_plan_equals_brute_force(name, checks):
         co, cg = dict(o["counts"]), dict(r["counts"])
         co.pop("edge_amb"), cg.pop("edge_amb")
         assert co == cg
+
+
+# ------------------------------------------------------------ loop map-point lists
+@pytest.mark.parametrize("name", ["C1", "T5", "C2"])
+def test_loop_lists_equal_set_union(name):
+    """The loop list of a window keyframe is the ascending unique union of its source
+    keyframes' map points; restated with numpy set algebra."""
+    from lcsynth import make_world
+    w = make_world(name, 0)
+    om = oracle.OracleMap(w)
+    ob, ol = om.loop_lists(w.list_src_begin, w.list_src_kf)
+    fb = w.kf_feat_begin
+    for l in range(len(ob) - 1):
+        ks = w.list_src_kf[w.list_src_begin[l]:w.list_src_begin[l + 1]]
+        s = np.concatenate([w.feat_mp[fb[k]:fb[k + 1]] for k in ks])
+        assert np.array_equal(ol[ob[l]:ob[l + 1]], np.unique(s[s >= 0])), l
+    if w.win_list_begin is not None:   # the world's own lists
+        assert np.array_equal(ob, w.win_list_begin) and np.array_equal(ol, w.mp_list)
+    else:
+        assert np.array_equal(ol, w.mp_list)
+
+
+def test_loop_lists_duplicates_bad_and_empty():
+    d = np.zeros(32, np.uint8)
+    kfs = [dict(feats=[dict(u=1.0, v=1.0, desc=d, mp=m) for m in ms]) for ms in ([3, 1, -1], [1, 2], [], [4])]
+    mps = [dict(pos=(0.0, 0.0, 1.0), desc=d, flags=(1 if i == 2 else 0)) for i in range(5)]
+    om = oracle.OracleMap(arrays=tm.build(kfs, mps), cams=[tm.PIN])
+    ob, ol = om.loop_lists([0, 2, 3, 3, 5], [0, 1, 2, 2, 3])
+    assert ob.tolist() == [0, 3, 3, 3, 4]
+    assert ol.tolist() == [1, 2, 3, 4]      # bad point 2 included (the queries skip it, O4)
