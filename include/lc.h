@@ -35,9 +35,13 @@
  *    all-reduce merges them (lowest H, then lowest q).
  *  - Pointers marked [host|dev] may be host memory (pageable or pinned) or
  *    device memory of the context's device; the library detects which
- *    (cudaPointerGetAttributes) and copies host data through its own pinned
- *    staging. Pointers marked [host] must be host memory (small control
- *    arrays the library validates and uses to configure launches).
+ *    (cudaPointerGetAttributes): device data is used in place, page-locked host
+ *    data is copied directly, pageable host data through the CUDA driver's staging
+ *    (or the library's chunked pinned ring with LC_STAGE=1; measured slower, see
+ *    lc_upload_map). Small control arrays marked [host] travel in one page-locked
+ *    argument block per call (a ring of 8, so the host only waits when it laps
+ *    it). Pointers marked [host] must be host memory (arrays the library
+ *    validates and uses to configure launches).
  *  - Asynchrony: every call enqueues work on `cuda_stream` (a cudaStream_t,
  *    NULL = legacy default stream) and returns; outputs (device or host) are
  *    valid once that stream has reached the call's work. Inputs must stay valid
@@ -396,8 +400,9 @@ lc_status lc_graph_destroy(lc_ctx* ctx, lc_graph* graph);
  *     The store grows geometrically (no re-allocation on most appends); a saved state
  *     (lc_state_save) is dropped. N appends give the same store as one REPLACE of the
  *     concatenated map, byte for byte.
- * Host arrays may be pageable (copied through the library's pinned staging ring in
- * 8-MB chunks, the host copy overlapping the DMA) or page-locked (copied directly).
+ * Host arrays may be page-locked (copied directly: C5's 558 MB in 36-64 ms) or pageable
+ * (copied by the CUDA driver's own staging, 91-108 ms; the library's chunked pinned ring,
+ * LC_STAGE=1, measured slower -- 118 ms -- so it is off by default).
  * Synchronises the stream before returning (validation reads back one error count).
  *   map   [host] struct; its arrays [host|dev]
  *   cams  [host] n_cams cameras; prm [host]
@@ -530,6 +535,26 @@ lc_status lc_fuse(lc_ctx* ctx, int32_t phase, int32_t w_lo, int32_t w_hi, int32_
                   int64_t* io_winner, int64_t* io_victim,
                   int8_t* out_action, const lc_query_debug* dbg, int64_t* out_counts,
                   void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
+ * lc_loop_lists -- the loop map-point lists, built on the device from the resident map
+ * (SURVEY.md §8(d) "Loop list = MPs of the matched pass-A KF and its top-10 covisibles,
+ * ascending unique"; C5 "MPs of its 10 nearest pass-A KFs"; EXT LoopClosing
+ * mvpLoopMapPoints; oracle orc_loop_lists). The paper assembles them on the CPU; here a
+ * loop event uploads keyframe ids (C5: 110 KB) instead of map-point lists (35 MB).
+ *
+ * List l = the ascending unique map points (>= 0; bad ones included -- the queries skip
+ * them, reading O4) associated with the keyframes src_kf[src_begin[l] .. src_begin[l+1]),
+ * from the CURRENT associations (after any fuse / append). The result is the
+ * (win_list_begin, mp_list) pair lc_fuse takes.
+ *   src_begin [host] [n+1], src_kf [host]; out_begin [host] [n+1] (written);
+ *   out_list [host|dev] capacity entries.
+ * Synchronises the stream (the offsets come back to the host). A list may hold at most
+ * 24576 distinct map points.
+ * Errors: LC_ESTATE (no map), LC_EINVAL, LC_ERANGE (keyframe id), LC_ECAPACITY (total >
+ * capacity -- out_begin is complete -- or a list over the limit). */
+lc_status lc_loop_lists(lc_ctx* ctx, int32_t n, const int32_t* src_begin, const int32_t* src_kf,
+                        int32_t* out_begin, int32_t* out_list, int64_t capacity, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
  * lc_fuse_adds -- the sparse ADD exchange of a keyframe-sharded fusion (SURVEY.md §8(e):

@@ -113,6 +113,7 @@ def load():
         "lc_correct_sim3": (i32, [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp]),
         "lc_fuse": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, vp, i64, P(lc_match_params), i32, vp, vp,
                           vp, vp, vp, vp, vp]),
+        "lc_loop_lists": (i32, [vp, i32, vp, vp, vp, vp, i64, vp]),
         "lc_fuse_adds": (i32, [vp, i32, i32, vp, i32, i32, vp, vp, vp, vp, i64, vp]),
         "lc_search_by_projection": (i32, [vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp,
                                           vp, vp]),
@@ -139,6 +140,6 @@ def load():
 def exported_symbols():
     return ["lc_create", "lc_destroy", "lc_last_error", "lc_kernel_launches", "lc_profile_enable",
             "lc_profile_read", "lc_upload_map",
-            "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse", "lc_fuse_adds",
+            "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse", "lc_fuse_adds", "lc_loop_lists",
             "lc_search_by_projection", "lc_refresh_mappoints", "lc_update_connections", "lc_sim3_ransac", "lc_sim3_refine", "lc_pgo_sim3", "lc_graph_begin", "lc_graph_end", "lc_graph_launch",
             "lc_graph_destroy"]

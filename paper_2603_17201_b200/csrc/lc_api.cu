@@ -180,7 +180,7 @@ struct Call {
     cudaPointerAttributes at;
     const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
     cudaGetLastError();
-    if (pinned || c->cap || bytes < lc_ctx::kStageMin) {
+    if (pinned || c->cap || bytes < lc_ctx::kStageMin || !c->stage_on) {
       CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
       return;
     }
@@ -481,6 +481,7 @@ lc_status lc_create(lc_ctx** out, int32_t device) {
   if (!c) return LC_ENOMEM;
   c->device = device;
   if (const char* e = getenv("LC_SOLE")) c->sole_mode = atoi(e);   // test knob: 0 forbid, 1 force, 2 k_match_sole
+  if (const char* e = getenv("LC_STAGE")) c->stage_on = atoi(e) != 0;   // pageable inputs via the staging ring
   bool ok = cudaSetDevice(device) == cudaSuccess;
   for (int r = 0; ok && r < lc_ctx::kPinRing; ++r)
     ok = cudaEventCreateWithFlags(&c->pin_ev[r], cudaEventDisableTiming) == cudaSuccess;
@@ -1557,6 +1558,108 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       CK(launch_fuse_apply(c, d_woff, win, vic, cnt, call.s));
     }
     hp.mark("launches");
+    call.finish();
+  });
+}
+
+// ----------------------------------------------------------------------------
+lc_status lc_loop_lists(lc_ctx* c, int32_t n, const int32_t* src_begin, const int32_t* src_kf, int32_t* out_begin,
+                        int32_t* out_list, int64_t capacity, void* stream) {
+  return guarded(c, [&] {
+    capture_gate(c, stream, false);
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    REQUIRE(n >= 0 && src_begin && out_begin && capacity >= 0 && (capacity == 0 || out_list), LC_EINVAL,
+            "null argument / negative size");
+    REQUIRE(src_begin[0] == 0, LC_EINVAL, "src_begin[0] must be 0");
+    Store& st = c->st;
+    std::vector<int64_t> reg_off((size_t)n + 1, 0);
+    const int umax = lists_max_unique();
+    for (int l = 0; l < n; ++l) {
+      REQUIRE(src_begin[l + 1] >= src_begin[l], LC_EINVAL, "src_begin not monotone");
+      int64_t ub = 0;
+      for (int j = src_begin[l]; j < src_begin[l + 1]; ++j) {
+        const int k = src_kf[j];
+        REQUIRE(k >= 0 && k < st.n_kf, LC_ERANGE, "source keyframe out of range");
+        ub += st.h_fbeg[k + 1] - st.h_fbeg[k];
+      }
+      reg_off[l + 1] = reg_off[l] + std::min<int64_t>(ub, umax);
+    }
+    out_begin[0] = 0;
+    if (n == 0) return;
+    Call call(c, stream);
+    const int32_t *d_sb = nullptr, *d_sk = nullptr;
+    const int64_t* d_ro = nullptr;
+    call.arg(src_begin, (size_t)n + 1, &d_sb);
+    call.arg(src_kf, (size_t)std::max(src_begin[n], 1), &d_sk);
+    call.arg(reg_off.data(), reg_off.size(), &d_ro);
+    call.commit();
+    // bitmap path (ascending unique by construction): a small bitmap per list first; the
+    // lists whose id range is wider (-1 counts) again with the large one; beyond that the
+    // general hash + sort path
+    const int w1 = lists_bitmap_words(), w2 = lists_bitmap_words_max();
+    uint32_t* d_bm = (uint32_t*)call.scratch(sizeof(uint32_t) * (size_t)n * w1);
+    int32_t* d_lo = (int32_t*)call.scratch(sizeof(int32_t) * 2 * (size_t)n);   // first id, words
+    int32_t* d_cnt = (int32_t*)call.scratch(sizeof(int32_t) * (size_t)n);
+    int2* d_rng = (int2*)call.scratch(sizeof(int2) * (size_t)std::max(src_begin[n], 1));
+    CK(launch_kf_idrange(c, src_begin[n], d_sk, d_rng, call.s));
+    CK(launch_lists_bitmap(c, n, n, nullptr, w1, d_rng, d_bm, d_lo, d_cnt, d_sb, d_sk, call.s));
+    std::vector<int32_t> cnt(n);
+    CK(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, call.s));
+    CK(cudaStreamSynchronize(call.s));
+    std::vector<int64_t> bm_off(n);
+    for (int l = 0; l < n; ++l) bm_off[l] = (int64_t)l * w1;
+    std::vector<int32_t> wide;
+    for (int l = 0; l < n; ++l)
+      if (cnt[l] < 0) wide.push_back(l);
+    uint32_t* d_bm2 = nullptr;
+    if (!wide.empty()) {
+      d_bm2 = (uint32_t*)call.scratch(sizeof(uint32_t) * wide.size() * (size_t)w2);
+      const int32_t* d_wide = call.in(wide.data(), wide.size());
+      CK(launch_lists_bitmap(c, (int)wide.size(), n, d_wide, w2, d_rng, d_bm2, d_lo, d_cnt, d_sb, d_sk, call.s));
+      CK(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, call.s));
+      CK(cudaStreamSynchronize(call.s));
+      for (size_t i = 0; i < wide.size(); ++i) bm_off[wide[i]] = (int64_t)(d_bm2 - d_bm) + (int64_t)i * w2;
+    }
+    std::vector<int32_t> hashed;   // still too wide (maps of more than 1.8M points): hash + sort
+    for (int l = 0; l < n; ++l)
+      if (cnt[l] < 0) hashed.push_back(l);
+    int32_t* d_reg = nullptr;
+    if (!hashed.empty()) {
+      d_reg = (int32_t*)call.scratch(sizeof(int32_t) * (size_t)std::max<int64_t>(reg_off[n], 1));
+      const int32_t* d_h = call.in(hashed.data(), hashed.size());
+      int32_t* d_hcnt = (int32_t*)call.scratch(sizeof(int32_t) * (size_t)n);
+      std::vector<int32_t> hcnt(n);
+      CK(launch_lists_dedup(c, false, (int)hashed.size(), d_h, d_sb, d_sk, d_ro, d_reg, d_hcnt, call.s));
+      CK(cudaMemcpyAsync(hcnt.data(), d_hcnt, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, call.s));
+      CK(cudaStreamSynchronize(call.s));
+      std::vector<int32_t> big;
+      for (int l : hashed)
+        if (hcnt[l] < 0) big.push_back(l);
+      if (!big.empty()) {
+        const int32_t* d_big = call.in(big.data(), big.size());
+        CK(launch_lists_dedup(c, true, (int)big.size(), d_big, d_sb, d_sk, d_ro, d_reg, d_hcnt, call.s));
+        CK(cudaMemcpyAsync(hcnt.data(), d_hcnt, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, call.s));
+        CK(cudaStreamSynchronize(call.s));
+      }
+      for (int l : hashed) {
+        REQUIRE(hcnt[l] >= 0, LC_ECAPACITY, "a loop list holds more than " + std::to_string(umax) + " map points");
+        cnt[l] = hcnt[l];
+      }
+    }
+    for (int l = 0; l < n; ++l) out_begin[l + 1] = out_begin[l] + cnt[l];
+    REQUIRE((int64_t)out_begin[n] <= capacity, LC_ECAPACITY,
+            "loop lists: " + std::to_string(out_begin[n]) + " entries exceed capacity");
+    const int32_t* d_ob = call.in(out_begin, (size_t)n + 1);
+    const int64_t* d_bmo = call.in(bm_off.data(), bm_off.size());
+    int32_t* d_out = call.out(out_list, (size_t)out_begin[n]);
+    // the hashed lists keep -1 in the bitmap counts: k_lists_emit skips them
+    CK(launch_lists_emit(c, n, d_bm, d_bmo, d_lo, d_cnt, d_ob, d_out, call.s));
+    for (int l : hashed) {   // bitonic sort into place (one launch each; only maps over 1.8M points)
+      const int64_t* d_one_ro = call.in(&reg_off[l], 2);
+      const int32_t ob2[2] = {0, cnt[l]};
+      const int32_t* d_ob2 = call.in(ob2, 2);   // (pageable -> staged before the call returns)
+      CK(launch_lists_sort(c, 1, cnt[l], d_one_ro, d_reg, d_ob2, d_out + out_begin[l], call.s));
+    }
     call.finish();
   });
 }

@@ -209,6 +209,7 @@ struct lc_ctx {
   void* stg[kStageRing] = {};
   cudaEvent_t stg_ev[kStageRing] = {};
   int stg_next = 0;
+  bool stage_on = false;   // LC_STAGE=1: pageable copies through the ring (measured slower than the driver's)
   // saved state (lc_state_save)
   void* sv = nullptr;
   size_t sv_cap = 0;
@@ -385,6 +386,21 @@ cudaError_t launch_correct_dry(lc_ctx* c, int n_batch, int n_slots, const int32_
 cudaError_t launch_adds(lc_ctx* c, int op, int n_w, const int32_t* d_window, const int64_t* d_woff, int64_t n_wfeat,
                         int64_t lo, int64_t hi, unsigned long long* winner, long long* idx, long long* word,
                         unsigned long long* d_n, int64_t n_in, int64_t capacity, cudaStream_t s);
+int lists_bitmap_words();       // bitmap path, first pass: id range (32-bit words) a list may span
+int lists_bitmap_words_max();   // ... second pass (the wide lists)
+cudaError_t launch_kf_idrange(lc_ctx* c, int n_src, const int32_t* d_skf, int2* d_rng, cudaStream_t s);
+cudaError_t launch_lists_bitmap(lc_ctx* c, int n, int n_lists, const int32_t* d_sel, int maxw, const int2* d_rng,
+                                uint32_t* d_bm, int32_t* d_lo, int32_t* d_counts, const int32_t* d_sbeg,
+                                const int32_t* d_skf, cudaStream_t s);
+cudaError_t launch_lists_emit(lc_ctx* c, int n, const uint32_t* d_bm, const int64_t* d_bm_off, const int32_t* d_lo,
+                              const int32_t* d_counts, const int32_t* d_out_begin, int32_t* d_out, cudaStream_t s);
+int lists_max_unique();     // distinct map points a loop list may hold
+int lists_small_unique();   // ... in the first (small hash) pass
+cudaError_t launch_lists_dedup(lc_ctx* c, bool large, int n, const int32_t* d_sel, const int32_t* d_sbeg,
+                               const int32_t* d_skf, const int64_t* d_reg_off, int32_t* d_reg, int32_t* d_counts,
+                               cudaStream_t s);
+cudaError_t launch_lists_sort(lc_ctx* c, int n, int max_u, const int64_t* d_reg_off, const int32_t* d_reg,
+                              const int32_t* d_out_begin, int32_t* d_out, cudaStream_t s);
 cudaError_t launch_fill_u64(lc_ctx* c, unsigned long long* p, int64_t n, unsigned long long v,
                             cudaStream_t s);
 cudaError_t launch_state_copy(lc_ctx* c, bool save, cudaStream_t s);

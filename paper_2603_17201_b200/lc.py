@@ -505,6 +505,26 @@ class Context:
             out.update(dd)
         return out
 
+    # -- lc_loop_lists ---------------------------------------------------------------
+    def loop_lists(self, src_begin, src_kf, out=None, host=True):
+        """Loop map-point lists from the resident map: list l = ascending unique map points of
+        keyframes src_kf[src_begin[l]:src_begin[l+1]]. Returns (begin [n+1] numpy, lists);
+        lists is written into `out` (a device or pinned tensor, >= total entries) if given."""
+        k = self._keep(host)
+        sb = np.ascontiguousarray(src_begin, np.int32)
+        sk = np.ascontiguousarray(src_kf, np.int32)
+        n = len(sb) - 1
+        ob = np.zeros(n + 1, np.int32)
+        if out is None:
+            fb = self.kf_feat_begin
+            ok = sk[(sk >= 0) & (sk < len(fb) - 1)]   # (out-of-range ids: the library reports LC_ERANGE)
+            cap = int(np.sum(fb[ok + 1] - fb[ok])) if len(ok) else 0
+            out = np.zeros(max(cap, 1), np.int32) if host else self._dev(max(cap, 1), torch.int32)
+        cap = int(out.numel() if isinstance(out, torch.Tensor) else out.size)
+        st = self.lib.lc_loop_lists(self.h, n, k.ptr(sb), k.ptr(sk), k.ptr(ob), k.ptr(out), cap, self._stream())
+        self._check("lc_loop_lists", st)
+        return ob, out[:int(ob[-1])]
+
     # -- lc_fuse_adds (sparse ADD exchange of a sharded fusion) --------------------
     def fuse_adds_pack(self, window, w_lo, w_hi, winner, idx, word):
         """Compact the shard's winner words on empty slots into (idx, word); returns n."""

@@ -277,3 +277,56 @@ def test_upload_pinned_and_pageable_and_append_errors(Ctx):
     assert e.value.status == _lib.LC_ERANGE
     for c in (c1, c2, c3):
         c.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "T2", "C2", "C3", "S3", "C5"])
+def test_loop_lists_parity(Ctx, name):
+    """lc_loop_lists against oracle orc_loop_lists (ascending unique map points of each
+    list's source keyframes): on the uploaded map -- where they equal the world's own lists
+    -- and again after a fuse changed the associations."""
+    w = world(name)
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    om = oracle.OracleMap(w)
+    gb, gl = ctx.loop_lists(w.list_src_begin, w.list_src_kf)
+    ob, ol = om.loop_lists(w.list_src_begin, w.list_src_kf)
+    assert np.array_equal(gb, ob) and np.array_equal(gl, ol)
+    if w.win_list_begin is not None:
+        assert np.array_equal(gb, w.win_list_begin) and np.array_equal(gl, w.mp_list)
+    dev = torch.device("cuda:0")
+    out = torch.empty(len(ol) + 5, dtype=torch.int32, device=dev)
+    db, dl = ctx.loop_lists(w.list_src_begin, w.list_src_kf, out=out, host=False)
+    torch.cuda.synchronize()
+    assert np.array_equal(db, ob) and np.array_equal(dl.cpu().numpy(), ol)
+    if name != "C5":
+        ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+        om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+        ctx.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+        om.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+        gb, gl = ctx.loop_lists(w.list_src_begin, w.list_src_kf)
+        ob, ol = om.loop_lists(w.list_src_begin, w.list_src_kf)
+        assert np.array_equal(gb, ob) and np.array_equal(gl, ol)
+    ctx.close()
+
+
+def test_loop_lists_large_and_errors(Ctx):
+    """A list over the small hash (the whole C2 map's map points: the retry with the large
+    hash), empty lists, and the error paths."""
+    from paper_2603_17201_b200 import _lib
+    from paper_2603_17201_b200._lib import LcError
+    w = world("C2")
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    om = oracle.OracleMap(w)
+    sb = np.array([0, 0, 150, 150, 170], np.int32)     # empty, 150 keyframes (> 6144 points), empty, 20
+    sk = np.r_[np.arange(150), np.arange(200, 220)].astype(np.int32)
+    gb, gl = ctx.loop_lists(sb, sk)
+    ob, ol = om.loop_lists(sb, sk)
+    assert gb[2] - gb[1] > 6144 and np.array_equal(gb, ob) and np.array_equal(gl, ol)
+    with pytest.raises(LcError) as e:
+        ctx.loop_lists([0, 1], [10 ** 6])
+    assert e.value.status == _lib.LC_ERANGE
+    with pytest.raises(LcError) as e:
+        ctx.loop_lists(sb, sk, out=np.zeros(10, np.int32))
+    assert e.value.status == _lib.LC_ECAPACITY
+    ctx.close()
