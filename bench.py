@@ -224,6 +224,25 @@ def pgo_cpu_baseline(seed):
     return (time.perf_counter() - t0) * 1000.0
 
 
+def host_band_solve_ms(n_unknown, kd, reps=3):
+    """A fair host reference for one PGO linear solve: LAPACK's banded Cholesky (dpbtrf +
+    dpbtrs through scipy, threaded BLAS) on a diagonally dominant SPD band matrix of the same
+    order and bandwidth as the device's RCM-ordered system (the cost depends on the shape
+    only). Context for lc_pgo_sim3, not the oracle."""
+    import scipy.linalg as sl
+    rng = np.random.default_rng(0)
+    ab = rng.standard_normal((kd + 1, n_unknown)) * 0.01
+    ab[0] = kd + 2.0
+    b = rng.standard_normal(n_unknown)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        c = sl.cholesky_banded(ab, lower=True)
+        sl.cho_solve_banded((c, True), b)
+        ts.append(time.perf_counter() - t0)
+    return min(ts) * 1000.0
+
+
 def cpu_baseline(w, seconds):
     """The oracle (never tuned) on this host: its grid / threaded timing mode at T = all host
     cores over the WHOLE window PLAN, plus the brute-force definition on one
@@ -752,10 +771,29 @@ def main():
                           "accepted": int(pc[counts.index("pgo_accepted")]),
                           "solver_iterations": int(pc[counts.index("pgo_solver_iters")]),
                           "chi2": [float(p2[0]), float(p2[1])],
-                          "solver": "banded Cholesky (RCM order)" if pc[counts.index("pgo_band")] > 0
-                          else "block-Jacobi CG"}
+                          "solver": ("block cyclic reduction (RCM order)" if pc[counts.index("pgo_cr_levels")] > 0
+                                     else "banded Cholesky (RCM order)" if pc[counts.index("pgo_band")] > 0
+                                     else "block-Jacobi CG")}
             bw = int(pc[counts.index("pgo_band")]) - 1
-            if bw >= 0:
+            lev = int(pc[counts.index("pgo_cr_levels")])
+            if bw >= 0 and lev > 0:
+                # FLOPs of the cyclic-reduction solves: per eliminated super-block (D = 7 bw
+                # unknowns) a Cholesky (D^3/3), the triangular solves of [A_il | A_ir] (2 D^3)
+                # and the Schur products of its two neighbours and the new coupling (3 x 2 D^3,
+                # computed as full blocks) = 8.33 D^3; N - 1 eliminations per solve. Against the
+                # whole chip's fp64 peak (148 SMs x 64 FMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s).
+                # The LM time includes the linearisation and trials: a lower bound on the
+                # solver's own rate.
+                D = 7 * max(bw, 1)
+                nsb = (g.n_v + max(bw, 1) - 1) // max(bw, 1)
+                flops = float(pgo[gname]["lm_iterations"]) * (nsb - 1) * (D ** 3) * (1.0 / 3 + 2 + 6)
+                ach = flops / (pgo[gname]["ms_per_call"] * 1e-3) / 1e9
+                pgo[gname]["bandwidth_blocks"] = bw
+                pgo[gname]["cr_levels"] = lev
+                pgo[gname]["roofline"] = {"bound": "phase latency (log2 N levels, grid barriers)",
+                                          "achieved": round(ach, 2), "peak": 37222.0,
+                                          "unit": "GFLOP/s fp64 (148 SMs)", "frac": round(ach / 37222.0, 4)}
+            elif bw >= 0:
                 # window-update FLOPs of the banded factorisations (BW(BW+1)/2 block pairs x
                 # 7x7x7 FMAs per position; the panel, Cholesky and solves are < 10% more)
                 # against ONE SM's fp64 peak (64 FMA/clk x 2 x 1.965 GHz = 251 GFLOP/s,
@@ -766,6 +804,13 @@ def main():
                 pgo[gname]["roofline"] = {"bound": "latency (one-CTA banded factorisation)", "achieved": round(ach, 2),
                                           "peak": 251.5, "unit": "GFLOP/s fp64 (one SM)",
                                           "frac": round(ach / 251.5, 4)}
+            if bw >= 0 and rank == 0 and not args.no_cpu_baseline:
+                hb = host_band_solve_ms(7 * g.n_v, 7 * (bw + 1) - 1)
+                pgo[gname]["cpu_banded_solve"] = {
+                    "ms_per_solve": round(hb, 3),
+                    "ms_for_the_lm_solves": round(hb * pgo[gname]["lm_iterations"], 2),
+                    "cores": host_cores(), "kind": "LAPACK dpbtrf + dpbtrs (scipy) on a same-shape SPD band matrix",
+                    "note": "the linear solves alone; the device ms_per_call also linearises and evaluates trials"}
         if rank == 0 and not args.no_cpu_baseline:
             # one LM iteration on C2, device vs the oracle on one host core (context)
             g2 = make_pose_graph("C2", args.seed)

@@ -207,6 +207,7 @@ enum {
   LC_COUNT_EDGE_AMB,       /* queries whose bounds or window decision lies within 1e-4 px of
                               the edge (SURVEY.md §8(c) "Edge-ambiguous"): the only queries
                               where a differently-rounded projection may decide otherwise */
+  LC_COUNT_PGO_CR_LEVELS,  /* pose graph: block cyclic-reduction levels (0 = not that solver) */
   LC_NCOUNT
 };
 
@@ -633,7 +634,7 @@ lc_status lc_search_by_projection(lc_ctx* ctx, int32_t n_pairs, const int32_t* p
  *     |delta| (-1 if failed), solver iterations (CG iterations; 1 for the banded solve).
  *   out_chi2 [host|dev] nullable [2]: initial and final chi2.
  *   out_counts [host|dev] nullable [LC_NCOUNT] (PGO_ITERS, PGO_ACCEPTED,
- *     PGO_SOLVER_ITERS, PGO_STOP, PGO_BAND).
+ *     PGO_SOLVER_ITERS, PGO_STOP, PGO_BAND, PGO_CR_LEVELS).
  * The whole loop runs in one cooperative kernel (no host round trip per iteration);
  * results are deterministic for a given problem. Capturable (lc_graph_*): the edge
  * list, fixed flags and the host-built incidence / RCM order are constants of the graph.
@@ -647,15 +648,20 @@ typedef struct {
   double eps_dx;         /* stop when |delta| < eps_dx (1e-8)                            */
   double eps_chi2;       /* stop when an accepted step lowers chi2 by < eps_chi2 relative */
   double cg_tol;         /* CG relative residual target (1e-10)                          */
-  int32_t solver;        /* LC_PGO_SOLVER_AUTO / _BAND / _CG                              */
+  int32_t solver;        /* LC_PGO_SOLVER_AUTO / _BAND / _CG / _CR                        */
   int32_t reserved;
 } lc_pgo_params;
 
-/* Linear solver of lc_pgo_sim3 (A54). AUTO: the banded Cholesky when the reverse
- * Cuthill-McKee ordering of the free vertices has a block bandwidth <= 28 (the
- * shared-memory window of one CTA), else CG. BAND: banded Cholesky (LC_EINVAL if the
- * bandwidth exceeds 28). CG: block-Jacobi preconditioned conjugate gradients. */
-enum { LC_PGO_SOLVER_AUTO = 0, LC_PGO_SOLVER_BAND = 1, LC_PGO_SOLVER_CG = 2 };
+/* Linear solver of lc_pgo_sim3 (A54, A54b), all in the reverse Cuthill-McKee order of the
+ * free vertices (block bandwidth bw). CR: block cyclic reduction -- the band cut into
+ * super-blocks of max(bw, 1) positions is block tridiagonal; odd-even elimination over
+ * log2(n_v / bw) levels, each level's eliminations and Schur updates spread over the SMs
+ * (LC_EINVAL if bw > 18: a super-block must fit one CTA's shared memory). BAND: the
+ * banded Cholesky chain in one CTA (LC_EINVAL if bw > 28). CG: block-Jacobi
+ * preconditioned conjugate gradients. AUTO: CR when bw <= 18 and n_v >= 4 max(bw, 1),
+ * else BAND when bw <= 28, else CG. CR and BAND are the same factorisation up to
+ * rounding (the order of the eliminations differs). */
+enum { LC_PGO_SOLVER_AUTO = 0, LC_PGO_SOLVER_BAND = 1, LC_PGO_SOLVER_CG = 2, LC_PGO_SOLVER_CR = 3 };
 
 enum { LC_PGO_STOP_DX = 1, LC_PGO_STOP_CHI2 = 2, LC_PGO_STOP_MAX_ITER = 3, LC_PGO_STOP_LAMBDA = 4,
        LC_PGO_STOP_ZERO = 5 };

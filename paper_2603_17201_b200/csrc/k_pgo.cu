@@ -235,7 +235,15 @@ struct PgoArgs {
   double* band;            // [n_v][bw+1][49] assembled H in band storage: (p + d, p) blocks
   double* lband;           // [n_v][bw+1][49] Cholesky factor, same layout
   double* yb;              // [n_v][8] forward-substitution result
-  double* bres;            // [2] fail flag, |delta|^2
+  double* bres;            // [8] fail flag, |delta|^2 (banded); [2 + parity] cyclic-reduction fail flags
+  // block cyclic reduction (A54b): cr_s > 0 selects it; super-blocks of cr_s positions
+  int cr_s, cr_N, cr_levels;
+  double* crA;             // [cr_N][D][D] damped diagonal super-blocks, then their Cholesky factors
+  double* crC;             // [cr_N][D][D] coupling with the current left neighbour, then X_l
+  double* crX;             // [cr_N][D][D] X_r of an eliminated super-block
+  double* cry;             // [cr_N][D] right-hand side, then L^-1 (rhs)
+  double* crx;             // [cr_N][D] solution
+  long long* ctim;         // LC_PGO_TIMING: [8] elimination sub-phase cycles (CTA 0)
   unsigned int* bar;       // grid barrier counter (zeroed before launch)
   double* trace;           // [max_iter][6] or null
   double* chi2_out;        // [2] or null
@@ -837,6 +845,520 @@ __device__ void band_solve(const PgoArgs& a, double lambda, double* sm, double* 
 #endif
 }
 
+// ---------------------------------------------------------------------------
+// Block cyclic reduction (A54b). The damped band matrix (block bandwidth bw, RCM order)
+// is cut into N super-blocks of s = max(bw, 1) consecutive positions (D = 7 s unknowns;
+// positions past n_v are identity padding). Super-blocks I and I + 2 share no nonzero,
+// so the matrix is block tridiagonal and odd-even elimination applies: at stride st the
+// super-blocks i = st (2k + 1) are eliminated, each independently (one CTA: dense
+// Cholesky of A_i in shared memory, X_l = L_i^-1 A_il, X_r = L_i^-1 A_ir, y_i = L_i^-1 b_i),
+// then every survivor J = 2 st k takes its Schur update (one CTA: A_J -= X^T X from both
+// eliminated neighbours, the new left coupling -X_r^T X_l, b_J -= X^T y). log2 N levels
+// replace the n_v-step chain of the banded factorisation and spread over the SMs; the back
+// substitution x_i = L_i^-T (y_i - X_l x_l - X_r x_r) runs the levels in reverse. This is
+// the Cholesky factorisation of the same matrix in the odd-even order of its super-blocks
+// (no pivoting; a non-positive pivot fails the solve, as in the banded path).
+// ---------------------------------------------------------------------------
+constexpr int kCrPC = 64;      // column panel of the triangular solves and products
+constexpr int kCrSMax = 18;    // largest super-block (positions): D <= 126
+
+// entry (r, c) of block (P1, P2) of the damped matrix; positions >= n_v are identity padding
+__device__ __forceinline__ double cr_entry(const PgoArgs& a, double lambda, int P1, int P2, int r, int c) {
+  if (P1 >= a.n_v || P2 >= a.n_v) return (P1 == P2 && r == c) ? 1.0 : 0.0;
+  if (P1 < P2) {
+    const int tp = P1; P1 = P2; P2 = tp;
+    const int tr = r; r = c; c = tr;
+  }
+  const int d = P1 - P2;
+  if (d > a.bw) return 0.0;
+  double v = __ldcg(a.band + ((size_t)P2 * (a.bw + 1) + d) * 49 + 7 * r + c);
+  if (d == 0 && r == c) v = v + lambda * v;
+  return v;
+}
+
+// grid-wide: dense super-blocks and right-hand side from band storage (warp per row)
+__device__ void cr_assemble(const PgoArgs& a, double lambda) {
+  const int s = a.cr_s, N = a.cr_N, D = 7 * s;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * kT + threadIdx.x) >> 5, nwarp = (gridDim.x * kT) >> 5;
+  for (int task = warp; task < N * D; task += nwarp) {
+    const int I = task / D, ra = task - I * D;
+    const int P1 = I * s + ra / 7, r = ra % 7;
+    double* Ar = a.crA + ((size_t)I * D + ra) * D;
+    double* Cr = a.crC + ((size_t)I * D + ra) * D;
+    for (int cb = lane; cb < D; cb += 32) {
+      const int P2 = I * s + cb / 7, c = cb % 7;
+      Ar[cb] = cr_entry(a, lambda, P1, P2, r, c);
+      Cr[cb] = I > 0 ? cr_entry(a, lambda, P1, P2 - s, r, c) : 0.0;
+    }
+    if (lane == 0) a.cry[(size_t)I * D + ra] = P1 < a.n_v ? -__ldcg(a.vd + (size_t)a.ord[P1] * kVD + 49 + r) : 0.0;
+  }
+}
+
+// CTA: in-place Cholesky of the D x D matrix in shared memory (pitch D, lower triangle).
+// Step k updates the trailing triangle with the unscaled column k (A_ij -= A_ik A_jk / d_k,
+// one barrier per step); the thread that updates A_{k+1,k+1} also stores its reciprocal,
+// so no step waits on a division. The columns are scaled at the end (L_ik = A_ik / sqrt(d_k)).
+// Outputs for the triangular solves: inv[k] = 1 / L_kk and, per 7 x 7 diagonal block q,
+// its inverse Binv[q] (lower triangular, row-major 49). rcp: D scratch doubles.
+// Returns false (CTA-uniform) on a non-positive pivot.
+__device__ bool cr_chol(double* A, int D, double* inv, double* Binv, double* rcp) {
+  const int t = threadIdx.x, ty = t >> 4, tx = t & 15;
+  if (t == 0) rcp[0] = 1.0 / A[0];
+  __syncthreads();
+  for (int k = 0; k < D; ++k) {
+    const double dk = A[k * D + k];
+    if (!(dk > 0.0)) return false;
+    const double rk = rcp[k];
+    for (int i = k + 1 + ty; i < D; i += 16) {
+      const double f = A[i * D + k] * rk;
+      for (int j = k + 1 + tx; j <= i; j += 16) {
+        const double v = A[i * D + j] - f * A[j * D + k];
+        A[i * D + j] = v;
+        if (i == k + 1 && j == k + 1) rcp[k + 1] = 1.0 / v;
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = t; k < D; k += kT) {
+    const double l = sqrt(A[k * D + k]);
+    inv[k] = 1.0 / l;
+    A[k * D + k] = l;
+  }
+  __syncthreads();
+  for (int e = t; e < D * D; e += kT) {
+    const int i = e / D, k = e - i * D;
+    if (k < i) A[e] = A[e] * inv[k];
+  }
+  __syncthreads();
+  // inverse of each diagonal 7 x 7 block: thread per (block, column), forward substitution
+  for (int w = t; w < D; w += kT) {
+    const int q = w / 7, c = w - 7 * q, o = 7 * q;
+    double y[7];
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+      double sacc = r == c ? 1.0 : 0.0;
+#pragma unroll
+      for (int m = 0; m < r; ++m) sacc -= A[(o + r) * D + o + m] * y[m];
+      y[r] = r < c ? 0.0 : sacc * inv[o + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 7; ++r) Binv[49 * q + 7 * r + c] = y[r];
+  }
+  __syncthreads();
+  return true;
+}
+
+// CTA: B <- L^-1 B for a D x pc panel (pitch kCrPC) in shared memory, L lower (pitch D),
+// Binv the inverses of its 7 x 7 diagonal blocks: per 7-row block, X_q = Binv_q B_q (thread
+// per column), then the rank-7 update of the rows below (thread per (row, column) tile)
+__device__ void cr_trsm(const double* L, const double* Binv, int D, double* B, int pc) {
+  const int t = threadIdx.x, ty = t >> 4, tx = t & 15;
+  for (int q = 0; q < D; q += 7) {
+    if (t < pc) {
+      double b[7];
+#pragma unroll
+      for (int r = 0; r < 7; ++r) b[r] = B[(q + r) * kCrPC + t];
+      const double* Bi = Binv + 7 * q;   // 49 (q / 7)
+#pragma unroll
+      for (int r = 0; r < 7; ++r) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int m = 0; m <= r; ++m) sacc += Bi[7 * r + m] * b[m];
+        B[(q + r) * kCrPC + t] = sacc;
+      }
+    }
+    __syncthreads();
+    if (q + 7 < D) {
+      double xv[4][7];
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+#pragma unroll
+        for (int m = 0; m < 7; ++m) xv[v][m] = (tx + 16 * v < pc) ? B[(q + m) * kCrPC + tx + 16 * v] : 0.0;
+      for (int row = q + 7 + ty; row < D; row += 16) {
+        double l[7];
+#pragma unroll
+        for (int m = 0; m < 7; ++m) l[m] = L[row * D + q + m];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int c = tx + 16 * v;
+          if (c < pc) {
+            double sacc = B[row * kCrPC + c];
+#pragma unroll
+            for (int m = 0; m < 7; ++m) sacc -= l[m] * xv[v][m];
+            B[row * kCrPC + c] = sacc;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// CTA: acc[u][v] = sum_m P[m][a_u] Q[m][c_v], a_u = ty + 16 u (< D), c_v = tx + 16 v (< pc)
+__device__ __forceinline__ void cr_gemm_tn(const double* P, int ldp, const double* Q, int ldq, int D, int pc,
+                                           double (&acc)[8][4]) {
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+  int au[8], cv[4];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) au[u] = min(ty + 16 * u, D - 1);
+#pragma unroll
+  for (int v = 0; v < 4; ++v) cv[v] = min(tx + 16 * v, pc - 1);
+#pragma unroll 2
+  for (int m = 0; m < D; ++m) {
+    double p[8], q[4];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) p[u] = P[m * ldp + au[u]];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) q[v] = Q[m * ldq + cv[v]];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] += p[u] * q[v];
+  }
+}
+
+// CTA: z <- L^-T z (L lower in shared memory, pitch D, inv = 1 / diag; z in shared
+// memory), one warp, right-looking: lane owns z_m for m = lane mod 32 in registers; x_r from
+// its owner by shuffle, then every lane subtracts L_rm x_r from its z_m (m < r)
+__device__ void cr_ltsolve(const double* L, const double* inv, int D, double* z) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double zr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) zr[u] = lane + 32 * u < D ? z[lane + 32 * u] : 0.0;
+    for (int r = D - 1; r >= 0; --r) {
+      const int u0 = r >> 5;
+      double own = zr[0];
+#pragma unroll
+      for (int u = 1; u < 4; ++u) own = u == u0 ? zr[u] : own;
+      const double xr = __shfl_sync(0xffffffffu, own, r & 31) * inv[r];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m = lane + 32 * u;
+        if (m < r) zr[u] -= L[r * D + m] * xr;
+        else if (m == r) zr[u] = xr;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (lane + 32 * u < D) z[lane + 32 * u] = zr[u];
+  }
+  __syncthreads();
+}
+
+// global (L2) -> shared, 8 loads in flight per thread
+__device__ __forceinline__ void cr_load(double* dst, const double* src, int n) {
+  for (int e0 = threadIdx.x; e0 < n; e0 += 8 * kT) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = e0 + u * kT < n ? __ldcg(src + e0 + u * kT) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (e0 + u * kT < n) dst[e0 + u * kT] = v[u];
+  }
+}
+
+// eliminate super-block i at stride st (CTA); false on a non-positive pivot
+__device__ bool cr_eliminate(const PgoArgs& a, int i, int st, double* sm, long long* et) {
+#ifdef LC_PGO_TIMING
+  long long tl = clock64();
+#define CE_TIC(k) do { if (et && threadIdx.x == 0) { const long long c_ = clock64(); et[k] += c_ - tl; tl = c_; } } while (0)
+#else
+#define CE_TIC(k) do { (void)et; } while (0)
+#endif
+  const int D = 7 * a.cr_s, N = a.cr_N, r = i + st;
+  const size_t DD = (size_t)D * D;
+  double* sL = sm;
+  double* sB = sm + DD;
+  double* sInv = sB + (size_t)D * kCrPC;
+  double* sBinv = sInv + D;   // [D / 7][49]
+  double* sRcp = sBinv + 7 * D;
+  cr_load(sL, a.crA + i * DD, (int)DD);
+  __syncthreads();
+  CE_TIC(0);
+  if (!cr_chol(sL, D, sInv, sBinv, sRcp)) return false;
+  CE_TIC(1);
+  for (int e = threadIdx.x; e < (int)DD; e += kT) a.crA[i * DD + e] = sL[e];
+  const int ncol = D + (r < N ? D : 0) + 1;   // [A_il | A_ir | b_i]
+  double* Ci = a.crC + i * DD;
+  const double* Cr = a.crC + (size_t)r * DD;  // A_ri (rows r, cols i): A_ir = Cr^T
+  double* Xi = a.crX + i * DD;
+  double* yi = a.cry + (size_t)i * D;
+  for (int c0 = 0; c0 < ncol; c0 += kCrPC) {
+    const int pc = min(kCrPC, ncol - c0);
+    // 8 loads in flight per thread; A_il and b_i row-major, A_ir = A_ri^T read along A_ri's rows
+    for (int e0 = threadIdx.x; e0 < D * pc; e0 += 8 * kT) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kT;
+        v[u] = 0.0;
+        if (e < D * pc) {
+          const int ra = e / pc, c = e - ra * pc, g = c0 + c;
+          if (g < D) v[u] = __ldcg(Ci + (size_t)ra * D + g);
+          else if (g == ncol - 1) v[u] = __ldcg(yi + ra);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kT;
+        if (e < D * pc) {
+          const int ra = e / pc, c = e - ra * pc, g = c0 + c;
+          if (g < D || g == ncol - 1) sB[ra * kCrPC + c] = v[u];
+        }
+      }
+    }
+    for (int e0 = threadIdx.x; e0 < D * pc; e0 += 8 * kT) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kT;
+        v[u] = 0.0;
+        if (e < D * pc) {
+          const int c = e / D, ra = e - c * D, g = c0 + c;
+          if (g >= D && g < ncol - 1) v[u] = __ldcg(Cr + (size_t)(g - D) * D + ra);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * kT;
+        if (e < D * pc) {
+          const int c = e / D, ra = e - c * D, g = c0 + c;
+          if (g >= D && g < ncol - 1) sB[ra * kCrPC + c] = v[u];
+        }
+      }
+    }
+    __syncthreads();
+    CE_TIC(2);
+    cr_trsm(sL, sBinv, D, sB, pc);
+    CE_TIC(3);
+    for (int e = threadIdx.x; e < D * pc; e += kT) {
+      const int ra = e / pc, c = e - ra * pc, g = c0 + c;
+      const double v = sB[ra * kCrPC + c];
+      if (g < D) Ci[(size_t)ra * D + g] = v;
+      else if (g < ncol - 1) Xi[(size_t)ra * D + (g - D)] = v;
+      else yi[ra] = v;
+    }
+    __syncthreads();
+  }
+  CE_TIC(4);
+#undef CE_TIC
+  return true;
+}
+
+// Schur update of survivor J at stride st (CTA)
+__device__ void cr_update(const PgoArgs& a, int J, int st, double* sm) {
+  const int D = 7 * a.cr_s, N = a.cr_N;
+  const size_t DD = (size_t)D * D;
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  double* sP = sm;
+  double* sQ = sm + DD;
+  double* sy = sQ + (size_t)D * kCrPC;
+  double* AJ = a.crA + (size_t)J * DD;
+  double* bJ = a.cry + (size_t)J * D;
+  for (int side = 0; side < 2; ++side) {
+    const int i = side == 0 ? J - st : J + st;   // eliminated neighbour: left (J is its r) or right (J is its l)
+    if (i < 0 || i >= N) continue;
+    const double* Pm = side == 0 ? a.crX + (size_t)i * DD : a.crC + (size_t)i * DD;   // X_r(i) / X_l(i)
+    cr_load(sP, Pm, (int)DD);
+    cr_load(sy, a.cry + (size_t)i * D, D);
+    __syncthreads();
+    // A_J -= P^T P (lower triangle read later; the full block is kept symmetric)
+    for (int c0 = 0; c0 < D; c0 += kCrPC) {
+      const int pc = min(kCrPC, D - c0);
+      double acc[8][4];
+      double old[8][4];   // issued before the products: 32 loads in flight
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int ar = ty + 16 * u, c = tx + 16 * v;
+          old[u][v] = (ar < D && c < pc) ? __ldcg(AJ + (size_t)ar * D + c0 + c) : 0.0;
+        }
+      cr_gemm_tn(sP, D, sP + c0, D, D, pc, acc);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int ar = ty + 16 * u, c = tx + 16 * v;
+          if (ar < D && c < pc) AJ[(size_t)ar * D + c0 + c] = old[u][v] - acc[u][v];
+        }
+    }
+    // b_J -= P^T y_i
+    for (int ar = threadIdx.x; ar < D; ar += kT) {
+      double sacc = 0.0;
+      for (int m = 0; m < D; ++m) sacc += sP[m * D + ar] * sy[m];
+      bJ[ar] = __ldcg(bJ + ar) - sacc;
+    }
+    if (side == 0) {
+      // new left coupling of J (with i - st): -X_r(i)^T X_l(i)
+      const double* Xl = a.crC + (size_t)i * DD;
+      double* CJ = a.crC + (size_t)J * DD;
+      for (int c0 = 0; c0 < D; c0 += kCrPC) {
+        const int pc = min(kCrPC, D - c0);
+        for (int e0 = threadIdx.x; e0 < D * pc; e0 += 8 * kT) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * kT, m = e / pc, c = e - m * pc;
+            v[u] = e < D * pc ? __ldcg(Xl + (size_t)m * D + c0 + c) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * kT, m = e / pc, c = e - m * pc;
+            if (e < D * pc) sQ[m * kCrPC + c] = v[u];
+          }
+        }
+        __syncthreads();
+        double acc[8][4];
+        cr_gemm_tn(sP, D, sQ, kCrPC, D, pc, acc);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int ar = ty + 16 * u, c = tx + 16 * v;
+            if (ar < D && c < pc) CJ[(size_t)ar * D + c0 + c] = -acc[u][v];
+          }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// back substitution of eliminated super-block i at stride st (CTA)
+__device__ void cr_backsub(const PgoArgs& a, int i, int st, double* sm) {
+  const int D = 7 * a.cr_s, N = a.cr_N, r = i + st, l = i - st;
+  const size_t DD = (size_t)D * D;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sL = sm;
+  double* z = sm + DD;
+  double* xl = z + D;
+  double* xr = xl + D;
+  double* sInv = xr + D;
+  cr_load(sL, a.crA + (size_t)i * DD, (int)DD);
+  cr_load(xl, a.crx + (size_t)l * D, D);
+  if (r < N) cr_load(xr, a.crx + (size_t)r * D, D);
+  for (int e = threadIdx.x; e < D; e += kT) sInv[e] = 1.0 / __ldcg(a.crA + (size_t)i * DD + (size_t)e * D + e);
+  __syncthreads();
+  const double* Xl = a.crC + (size_t)i * DD;
+  const double* Xr = a.crX + (size_t)i * DD;
+  for (int ar = warp; ar < D; ar += kT / 32) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int m = lane + 32 * u;
+      if (m < D) {
+        sacc += __ldcg(Xl + (size_t)ar * D + m) * xl[m];
+        if (r < N) sacc += __ldcg(Xr + (size_t)ar * D + m) * xr[m];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0) z[ar] = __ldcg(a.cry + (size_t)i * D + ar) - sacc;
+  }
+  __syncthreads();
+  cr_ltsolve(sL, sInv, D, z);
+  for (int e = threadIdx.x; e < D; e += kT) a.crx[(size_t)i * D + e] = z[e];
+}
+
+// the whole solve, every CTA (grid barriers inside); X <- delta (vertex order). Returns
+// the CTA-uniform fail flag and |delta|^2 in out2.
+__device__ void cr_solve(const PgoArgs& a, double lambda, double* sm, double* X, unsigned int& bt,
+                         double (*shR)[4], int nsolve, double* out2) {
+  const int D = 7 * a.cr_s, N = a.cr_N, s = a.cr_s;
+  const size_t DD = (size_t)D * D;
+  double* fail = a.bres + 2 + (nsolve & 1);
+#ifdef LC_PGO_TIMING
+  // CTA 0 (eliminates super-block st, updates survivor 0 at each level): per-phase cycles
+  long long tim[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = clock64();
+#define CR_TIC(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) { const long long c_ = clock64(); tim[k] += c_ - tlast; tlast = c_; } } while (0)
+#else
+#define CR_TIC(k) do { } while (0)
+#endif
+  cr_assemble(a, lambda);
+  CR_TIC(6);
+  grid_barrier(a.bar, bt);
+  CR_TIC(7);
+  // every CTA has read the previous solve's flag (before this solve's first barrier)
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.bres[2 + ((nsolve + 1) & 1)] = 0.0;
+  int st = 1;
+  for (; st < N; st *= 2) {
+    for (int i = st + 2 * st * (int)blockIdx.x; i < N; i += 2 * st * (int)gridDim.x)
+      if (!cr_eliminate(a, i, st, sm,
+#ifdef LC_PGO_TIMING
+                        blockIdx.x == 0 ? a.ctim : nullptr
+#else
+                        nullptr
+#endif
+                        ) && threadIdx.x == 0)
+        *fail = 1.0;
+    CR_TIC(0);
+    grid_barrier(a.bar, bt);
+    CR_TIC(1);
+    for (int J = 2 * st * (int)blockIdx.x; J < N; J += 2 * st * (int)gridDim.x) cr_update(a, J, st, sm);
+    CR_TIC(2);
+    grid_barrier(a.bar, bt);
+    CR_TIC(3);
+  }
+  if (blockIdx.x == 0) {   // the root super-block 0: x_0 = A_0^-1 b_0
+    double* sL = sm;
+    double* sB = sm + DD;
+    double* sInv = sB + (size_t)D * kCrPC;
+    double* sBinv = sInv + D;
+    double* sRcp = sBinv + 7 * D;
+    cr_load(sL, a.crA, (int)DD);
+    for (int e = threadIdx.x; e < D; e += kT) sB[e * kCrPC] = __ldcg(a.cry + e);
+    __syncthreads();
+    if (cr_chol(sL, D, sInv, sBinv, sRcp)) {
+      cr_trsm(sL, sBinv, D, sB, 1);
+      double* z = sRcp;
+      for (int e = threadIdx.x; e < D; e += kT) z[e] = sB[e * kCrPC];
+      __syncthreads();
+      cr_ltsolve(sL, sInv, D, z);
+      for (int e = threadIdx.x; e < D; e += kT) a.crx[e] = z[e];
+    } else if (threadIdx.x == 0) {
+      *fail = 1.0;
+    }
+  }
+  CR_TIC(5);
+  grid_barrier(a.bar, bt);
+  CR_TIC(7);
+  for (st >>= 1; st >= 1; st >>= 1) {
+    for (int i = st + 2 * st * (int)blockIdx.x; i < N; i += 2 * st * (int)gridDim.x) cr_backsub(a, i, st, sm);
+    __syncthreads();
+    CR_TIC(4);
+    grid_barrier(a.bar, bt);
+    CR_TIC(7);
+  }
+#ifdef LC_PGO_TIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int k = 0; k < 8; ++k) a.counts[k] += (unsigned long long)tim[k];
+    for (int k = 0; k < 5; ++k) a.counts[8 + k] += (unsigned long long)a.ctim[k];
+  }
+#endif
+#undef CR_TIC
+  // positions -> vertices, |delta|^2 (fixed grid order: deterministic)
+  double xx = 0.0;
+  for (int e = blockIdx.x * kT + threadIdx.x; e < a.n_v * 7; e += gridDim.x * kT) {
+    const int P = e / 7, r = e - 7 * P, I = P / s;
+    const double v = __ldcg(a.crx + (size_t)I * D + 7 * (P - I * s) + r);
+    X[(size_t)a.ord[P] * kVec + r] = v;
+    xx += v * v;
+  }
+  double tot[4];
+  cta_partial(xx, 0.0, 0.0, 0.0, a.part, shR);
+  grid_barrier(a.bar, bt);
+  grid_total(a.part, tot, shR);
+  out2[0] = __ldcg(fail);
+  out2[1] = tot[0];
+}
+
 __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
   __shared__ double shJ[(kT / 16) * 112];
   __shared__ double shR[kT / 32][4];
@@ -858,6 +1380,8 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
     a.S_out[k] = s;
     a.S_tmp[k] = s;
   }
+  if (tid < 2) a.bres[2 + tid] = 0.0;   // cyclic-reduction fail flags
+  int nsolve = 0;
   grid_barrier(a.bar, bt);
   double* S = a.S_out;
   double* St = a.S_tmp;
@@ -909,9 +1433,18 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
         band_dirty = false;
         grid_barrier(a.bar, bt);
       }
-      if (blockIdx.x == 0) band_solve(a, lambda, dsm, X);
-      grid_barrier(a.bar, bt);
-      const double bfail = __ldcg(a.bres), bxx = __ldcg(a.bres + 1);
+      double bfail, bxx;
+      if (a.cr_s > 0) {
+        double o2[2];
+        cr_solve(a, lambda, dsm, X, bt, shR, nsolve++, o2);
+        bfail = o2[0];
+        bxx = o2[1];
+      } else {
+        if (blockIdx.x == 0) band_solve(a, lambda, dsm, X);
+        grid_barrier(a.bar, bt);
+        bfail = __ldcg(a.bres);
+        bxx = __ldcg(a.bres + 1);
+      }
       ++it;
       row = (lead && a.trace) ? a.trace + 6 * (size_t)(it - 1) : nullptr;
       if (row) { row[0] = chi2; row[1] = lambda; row[2] = -1.0; row[3] = 0.0; row[4] = -1.0; row[5] = 1.0; }
@@ -1105,6 +1638,7 @@ __global__ void __launch_bounds__(kT, 1) k_pgo(PgoArgs a) {
     a.counts[LC_COUNT_PGO_SOLVER_ITERS] = (unsigned long long)cg_total;
     a.counts[LC_COUNT_PGO_STOP] = (unsigned long long)stop;
     a.counts[LC_COUNT_PGO_BAND] = (unsigned long long)(a.bw + 1);
+    a.counts[LC_COUNT_PGO_CR_LEVELS] = (unsigned long long)a.cr_levels;
   }
 }
 
@@ -1115,33 +1649,45 @@ static size_t band_smem_bytes(int bw) {
   const size_t NB = (size_t)bw + 1;
   return sizeof(double) * (NB * (NB + 1) / 2 * 49 + NB * 8 * 3 + 16 + NB * 49) + 2 * NB * NB;
 }
+static size_t cr_smem_bytes(int s) {
+  const size_t D = 7 * (size_t)s;
+  return sizeof(double) * (D * D + D * kCrPC + 9 * D);
+}
+static size_t pgo_smem_bytes(int bw, int cr_s) { return cr_s > 0 ? cr_smem_bytes(cr_s) : band_smem_bytes(bw); }
 
 int pgo_max_bw() { return kBWMax; }
+int pgo_cr_max_s() { return kCrSMax; }
+int pgo_cr_s(int bw) { return std::max(bw, 1); }
 
-size_t pgo_scratch_bytes(int n_v, int n_e, int grid, int bw) {
+size_t pgo_scratch_bytes(int n_v, int n_e, int grid, int bw, int cr_s) {
   size_t d = (size_t)n_e * kRec + (size_t)n_v * (kVD + kVL + 6 * kVec + 13) + 4 * (size_t)grid + 8;
   if (bw >= 0) d += 2 * (size_t)n_v * (bw + 1) * 49 + (size_t)n_v * 8;
+  if (cr_s > 0) {
+    const size_t D = 7 * (size_t)cr_s, N = ((size_t)n_v + cr_s - 1) / cr_s;
+    d += 3 * N * D * D + 2 * N * D;
+  }
   return sizeof(double) * d + 256;
 }
 
-int pgo_grid(lc_ctx* c, int n_v, int n_e, int bw) {
+int pgo_grid(lc_ctx* c, int n_v, int n_e, int bw, int cr_s) {
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = band_smem_bytes(bw);
+  const size_t smem = pgo_smem_bytes(bw, cr_s);
   cudaFuncSetAttribute(k_pgo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pgo, kT, smem);
   (void)c;
-  const int64_t work = std::max<int64_t>((int64_t)n_e * 16, (int64_t)n_v * 8);
+  int64_t work = std::max<int64_t>((int64_t)n_e * 16, (int64_t)n_v * 8);
+  if (cr_s > 0) work = std::max<int64_t>(work, (int64_t)((n_v + cr_s - 1) / cr_s) * kT);   // CTA per super-block
   const int need = (int)std::max<int64_t>(1, (work + kT - 1) / kT);
   return std::max(1, std::min(need, sms * std::max(per, 1)));
 }
 
 cudaError_t launch_pgo(lc_ctx* c, int n_v, int n_e, const int32_t* d_eij, const double* d_M, const double* d_S_in,
                        const uint8_t* d_fixed, const int32_t* d_vbeg, const int32_t* d_vinc, int bw,
-                       const int32_t* d_pos, const int32_t* d_ord, const lc_pgo_params& p, double* d_S_out,
-                       void* scratch, int grid, double* d_trace, double* d_chi2, unsigned long long* counts,
-                       cudaStream_t s) {
+                       const int32_t* d_pos, const int32_t* d_ord, int cr_s, const lc_pgo_params& p,
+                       double* d_S_out, void* scratch, int grid, double* d_trace, double* d_chi2,
+                       unsigned long long* counts, cudaStream_t s) {
   PgoArgs a;
   a.vinc2 = (const int2*)d_vinc;
   a.n_v = n_v; a.n_e = n_e; a.max_iter = p.max_iter; a.cg_max = p.cg_max_iter;
@@ -1163,12 +1709,26 @@ cudaError_t launch_pgo(lc_ctx* c, int n_v, int n_e, const int32_t* d_eij, const 
     a.lband = base; base += (size_t)n_v * (bw + 1) * 49;
     a.yb = base; base += (size_t)n_v * 8;
   }
+  a.cr_s = cr_s; a.cr_N = 0; a.cr_levels = 0;
+  a.crA = a.crC = a.crX = a.cry = a.crx = nullptr;
+  if (cr_s > 0) {
+    const size_t D = 7 * (size_t)cr_s;
+    const int N = (n_v + cr_s - 1) / cr_s;
+    a.cr_N = N;
+    while ((1 << a.cr_levels) < N) ++a.cr_levels;
+    a.crA = base; base += (size_t)N * D * D;
+    a.crC = base; base += (size_t)N * D * D;
+    a.crX = base; base += (size_t)N * D * D;
+    a.cry = base; base += (size_t)N * D;
+    a.crx = base; base += (size_t)N * D;
+  }
+  a.ctim = (long long*)((char*)base + 128);   // inside the zeroed 256-byte barrier block
   a.bar = (unsigned int*)base;
   a.trace = d_trace; a.chi2_out = d_chi2; a.counts = counts;
   cudaError_t e = cudaMemsetAsync(a.bar, 0, 256, s);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
-  e = cudaLaunchCooperativeKernel((const void*)k_pgo, dim3(grid), dim3(kT), args, band_smem_bytes(bw), s);
+  e = cudaLaunchCooperativeKernel((const void*)k_pgo, dim3(grid), dim3(kT), args, pgo_smem_bytes(bw, cr_s), s);
   c->launches++;
   return e;
 }

@@ -1130,7 +1130,7 @@ lc_status lc_pgo_sim3(lc_ctx* c, int32_t n_v, const lc_sim3* S_init, const uint8
     REQUIRE(params, LC_EINVAL, "null params");
     const lc_pgo_params p = *params;
     REQUIRE(n_v >= 0 && n_e >= 0 && n_e < (1 << 30) && p.max_iter >= 0 && p.cg_max_iter >= 1 && p.lambda0 > 0.0 &&
-                p.eps_dx >= 0.0 && p.eps_chi2 >= 0.0 && p.cg_tol >= 0.0 && p.solver >= 0 && p.solver <= 2,
+                p.eps_dx >= 0.0 && p.eps_chi2 >= 0.0 && p.cg_tol >= 0.0 && p.solver >= 0 && p.solver <= 3,
             LC_EINVAL, "bad sizes / parameters");
     REQUIRE(n_v == 0 || (S_init && fixed && out_S), LC_EINVAL, "null vertex array");
     REQUIRE(n_e == 0 || (edge_ij && M), LC_EINVAL, "null edge array");
@@ -1181,24 +1181,32 @@ lc_status lc_pgo_sim3(lc_ctx* c, int32_t n_v, const lc_sim3* S_init, const uint8
     double* dT = out_trace ? call.out(out_trace, 6 * (size_t)std::max(p.max_iter, 1)) : nullptr;
     double* dC = out_chi2 ? call.out(out_chi2, 2) : nullptr;
     if (dT) CK(cudaMemsetAsync(dT, 0, 6 * sizeof(double) * std::max(p.max_iter, 1), call.s));
-    // solver (A54): banded Cholesky in a reverse Cuthill-McKee order when the block
-    // bandwidth fits the shared-memory window, else block-Jacobi CG
+    // solver (A54/A54b): in a reverse Cuthill-McKee order, block cyclic reduction over
+    // super-blocks of bw positions when they fit one CTA's shared memory and there are at
+    // least 4 of them, else the banded Cholesky when the bandwidth fits its window, else
+    // block-Jacobi CG
     std::vector<int32_t> pos, ord;
     int bw = pgo_rcm(n_v, fixed, n_e, edge_ij, pos, ord);
     REQUIRE(!(p.solver == LC_PGO_SOLVER_BAND && bw > pgo_max_bw()), LC_EINVAL,
             "LC_PGO_SOLVER_BAND: block bandwidth exceeds the banded solver's window");
-    if (p.solver == LC_PGO_SOLVER_CG || bw > pgo_max_bw()) bw = -1;
+    REQUIRE(!(p.solver == LC_PGO_SOLVER_CR && pgo_cr_s(bw) > pgo_cr_max_s()), LC_EINVAL,
+            "LC_PGO_SOLVER_CR: block bandwidth exceeds the cyclic-reduction super-block");
+    int cr_s = 0;
+    if (p.solver == LC_PGO_SOLVER_CR ||
+        (p.solver == LC_PGO_SOLVER_AUTO && pgo_cr_s(bw) <= pgo_cr_max_s() && n_v >= 4 * pgo_cr_s(bw)))
+      cr_s = pgo_cr_s(bw);
+    if (p.solver == LC_PGO_SOLVER_CG || (cr_s == 0 && bw > pgo_max_bw())) bw = -1;
     const int32_t *d_pos = nullptr, *d_ord = nullptr;
     if (bw >= 0) {
       call.arg(pos.data(), pos.size(), &d_pos);
       call.arg(ord.data(), ord.size(), &d_ord);
     }
     call.commit();
-    const int grid = pgo_grid(c, n_v, n_e, bw);
-    void* scr = call.scratch(pgo_scratch_bytes(n_v, n_e, grid, bw));
+    const int grid = pgo_grid(c, n_v, n_e, bw, cr_s);
+    void* scr = call.scratch(pgo_scratch_bytes(n_v, n_e, grid, bw, cr_s));
     {
       Prof pr(c, LC_PROF_PGO, call.s);
-      CK(launch_pgo(c, n_v, n_e, d_eij, dM, dS0, d_fixed, d_vbeg, d_vinc, bw, d_pos, d_ord, p, dS, scr, grid,
+      CK(launch_pgo(c, n_v, n_e, d_eij, dM, dS0, d_fixed, d_vbeg, d_vinc, bw, d_pos, d_ord, cr_s, p, dS, scr, grid,
                     dT, dC, cnt, call.s));
     }
     call.finish();

@@ -429,10 +429,12 @@ cudaError_t launch_refresh(lc_ctx* c, int n_sel, const int32_t* d_idx, int what,
                            int32_t* d_cursor, int32_t* d_bsum, int32_t* d_obs, int32_t* d_obs_kf,
                            unsigned long long* counts, cudaStream_t s);
 int pgo_max_bw();
-size_t pgo_scratch_bytes(int n_v, int n_e, int grid, int bw);
-int pgo_grid(lc_ctx* c, int n_v, int n_e, int bw);
+int pgo_cr_max_s();
+int pgo_cr_s(int bw);
+size_t pgo_scratch_bytes(int n_v, int n_e, int grid, int bw, int cr_s);
+int pgo_grid(lc_ctx* c, int n_v, int n_e, int bw, int cr_s);
 cudaError_t launch_pgo(lc_ctx* c, int n_v, int n_e, const int32_t* d_eij, const double* d_M, const double* d_S_in,
                        const uint8_t* d_fixed, const int32_t* d_vbeg, const int32_t* d_vinc, int bw,
-                       const int32_t* d_pos, const int32_t* d_ord, const lc_pgo_params& p, double* d_S_out,
-                       void* scratch, int grid, double* d_trace, double* d_chi2, unsigned long long* counts,
-                       cudaStream_t s);
+                       const int32_t* d_pos, const int32_t* d_ord, int cr_s, const lc_pgo_params& p,
+                       double* d_S_out, void* scratch, int grid, double* d_trace, double* d_chi2,
+                       unsigned long long* counts, cudaStream_t s);

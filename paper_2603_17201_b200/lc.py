@@ -379,7 +379,7 @@ class Context:
         n_e = len(E)
         fx = np.ascontiguousarray(fixed, np.uint8)
         prm = _lib.lc_pgo_params(int(max_iter), int(cg_max_iter), float(lambda0), float(eps_dx),
-                                 float(eps_chi2), float(cg_tol), {"auto": 0, "band": 1, "cg": 2}[solver], 0)
+                                 float(eps_chi2), float(cg_tol), {"auto": 0, "band": 1, "cg": 2, "cr": 3}[solver], 0)
         rows = max(int(max_iter), 1)
         if host:
             S = np.zeros((n_v, 13), np.float64)
