@@ -317,7 +317,7 @@ def main():
     ctx.state_save()
 
     mp_list_d = torch.from_numpy(w.mp_list).to(dev)   # the loop event's inputs, resident in HBM
-    win_S_d = torch.from_numpy(np.ascontiguousarray(w.win_S)).to(dev)
+    win_S_d = None if w.win_S is None else torch.from_numpy(np.ascontiguousarray(w.win_S)).to(dev)
     S_opt_d = torch.from_numpy(w.S_opt).to(dev)
     n_wfeat = ctx.n_feat_of(w.window)
     tables = torch.empty(n_wfeat + w.n_mp, dtype=torch.int64, device=dev)
@@ -473,7 +473,7 @@ def main():
     # Sim3, the optimised Sim3s -- and reads the result counters back, inside the timed
     # region (CUDA events on the stream + host wall clock; lc_loop_lists synchronises once)
     e2e = None
-    if not args.no_e2e and not args.profile_only and ws == 1:
+    if not args.no_e2e and not args.profile_only and ws == 1 and w.win_S is not None and w.win_list_begin is not None:
         Sopt_pin = torch.from_numpy(w.S_opt).pin_memory()
         winS_pin = torch.from_numpy(np.ascontiguousarray(w.win_S)).pin_memory()
         sb_pin = torch.from_numpy(w.list_src_begin).pin_memory()

@@ -24,7 +24,7 @@ COUNTER_NAMES = [
     "victims", "rewired", "dup_cleared", "added", "corr_kf", "corr_mp",
     "refresh_mp", "refresh_obs", "conn_kf", "conn_edges", "ransac_hyp", "ransac_inliers",
     "refine_iters", "refine_inliers", "pgo_iters", "pgo_accepted", "pgo_solver_iters", "pgo_stop",
-    "pgo_band", "forced", "edge_amb",
+    "pgo_band", "forced", "edge_amb", "pgo_cr_levels",   # pgo_cr_levels: a device-solver counter, always 0 here
 ]
 NONE64 = np.iinfo(np.int64).max
 

@@ -80,7 +80,7 @@ enum {
   C_VICTIMS, C_REWIRED, C_DUP_CLEARED, C_ADDED, C_CORR_KF, C_CORR_MP,
   C_REFRESH_MP, C_REFRESH_OBS, C_CONN_KF, C_CONN_EDGES, C_RANSAC_HYP, C_RANSAC_INLIERS,
   C_REFINE_ITERS, C_REFINE_INLIERS, C_PGO_ITERS, C_PGO_ACCEPTED, C_PGO_SOLVER_ITERS,
-  C_PGO_STOP, C_PGO_BAND, C_FORCED, C_EDGE_AMB, C_N
+  C_PGO_STOP, C_PGO_BAND, C_FORCED, C_EDGE_AMB, C_PGO_CR_LEVELS /* device solver only: always 0 */, C_N
 };
 
 /* query status codes written to out_status (negative = culled/skipped) */

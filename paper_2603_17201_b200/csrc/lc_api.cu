@@ -482,6 +482,7 @@ lc_status lc_create(lc_ctx** out, int32_t device) {
   c->device = device;
   if (const char* e = getenv("LC_SOLE")) c->sole_mode = atoi(e);   // test knob: 0 forbid, 1 force, 2 k_match_sole
   if (const char* e = getenv("LC_STAGE")) c->stage_on = atoi(e) != 0;   // pageable inputs via the staging ring
+  if (const char* e = getenv("LC_PIPE_MIN")) c->pipe_min = atoll(e);   // test knob: force / forbid the pipelined list upload
   bool ok = cudaSetDevice(device) == cudaSuccess;
   for (int r = 0; ok && r < lc_ctx::kPinRing; ++r)
     ok = cudaEventCreateWithFlags(&c->pin_ev[r], cudaEventDisableTiming) == cudaSuccess;
@@ -1377,7 +1378,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     // memory uploads them in kPipe chunks on a side stream; k_project / k_match run
     // on each chunk's blocks as it lands (k_project stamps the LoopSet), the resolve
     // after all of them
-    const bool pipe = (phase & LC_FUSE_PLAN) && win_list_begin && n_list >= (1 << 18) && !dbg &&
+    const bool pipe = (phase & LC_FUSE_PLAN) && win_list_begin && n_list >= c->pipe_min && !dbg &&
                       !c->cap && w_lo == 0 && w_hi == n_window && !is_device_ptr(c, mp_list) &&
                       cur_pos < 0;   // the forced step needs the LoopSet stamped up front
     // sole mode: one k_match CTA per window keyframe, which initialises and resolves its
@@ -1534,6 +1535,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       a.surv_off = d_boff;
       a.surv_cnt = d_scnt;
       a.sole = sole ? (c->sole_mode == 2 ? 2 : 1) : 0;
+      a.loop_ep_w = pipe ? st.mp_loop_ep : nullptr;   // the pipelined mode stamps the LoopSet in k_project
       if (pipe) {
         for (int k = 0; k < lc_ctx::kPipe; ++k) {
           const int b0 = pipe_b[k], nbk = pipe_b[k + 1] - pipe_b[k];

@@ -190,6 +190,7 @@ struct lc_ctx {
   cudaEvent_t pipe_ev[kPipe + 1] = {};          // [kPipe]: start (side waits on the call stream)
   int64_t launches = 0;
   int sole_mode = -1;   // LC_SOLE env at create: -1 auto, 0 never, 1 whenever lists allow (testing)
+  int64_t pipe_min = 1 << 18;   // LC_PIPE_MIN env at create: smallest host list that takes the pipelined upload
   // scratch arena: named growable device buffers
   std::vector<void*> scr_ptr;
   std::vector<size_t> scr_cap;

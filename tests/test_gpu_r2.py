@@ -79,6 +79,65 @@ def test_forced_matches_parity(Ctx, name, params):
     ctx.close()
 
 
+def _loopset_world(name="T5", n_add=6):
+    """A world where reading A21 fires: victims of the base run are appended to window
+    keyframe 0's loop list, so they join the LoopSet (the union of all window lists) and
+    the slots they hold are never fused (loop_skip) -- the synthetic worlds alone never
+    put a window slot's map point into a loop list."""
+    w = world(name)
+    om = oracle.OracleMap(w)
+    om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    o = om.fuse(w.window, w.mp_list, FUSE_PARAMS_CHECKS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+    vic = np.flatnonzero(o["victim"] != NONE)[:n_add].astype(np.int32)
+    assert len(vic) == n_add
+    lb = np.asarray(w.win_list_begin, np.int32).copy()
+    lst = np.concatenate([w.mp_list[:lb[1]], vic, w.mp_list[lb[1]:]]).astype(np.int32)
+    lb[1:] += n_add
+    return w, lst, lb
+
+
+@pytest.mark.parametrize("mode", ["device-lists", "host-pipelined", "sole", "sharded"])
+def test_loopset_skip_parity(Ctx, monkeypatch, mode):
+    """Reading A21 (a slot holding a LoopSet map point is skipped, never a victim) against
+    the oracle with loop_skip > 0, through the device-list, pipelined host-list (k_project
+    stamps the LoopSet), sole and sharded-PLAN launches."""
+    from paper_2603_17201_b200 import LC_FUSE_APPLY, LC_FUSE_PLAN
+    w, lst, lb = _loopset_world()
+    if mode == "host-pipelined":
+        monkeypatch.setenv("LC_PIPE_MIN", "1")
+    if mode == "sole":
+        monkeypatch.setenv("LC_SOLE", "1")
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    om = oracle.OracleMap(w)
+    ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    o = om.fuse(w.window, lst, FUSE_PARAMS_CHECKS, window_S=w.win_S, win_list_begin=lb)
+    assert o["counts"]["loop_skip"] > 0
+    L = lst if mode == "host-pipelined" else torch.from_numpy(lst).cuda()
+    if mode == "sharded":
+        cuts = np.linspace(0, len(w.window), 4).astype(int)
+        tabs = [ctx.fuse(w.window, L, FUSE_PARAMS_CHECKS, window_S=w.win_S, win_list_begin=lb, phase=LC_FUSE_PLAN,
+                         w_lo=cuts[r], w_hi=cuts[r + 1]) for r in range(3)]
+        win = np.minimum.reduce([t["winner"] for t in tabs])
+        vic = np.minimum.reduce([t["victim"] for t in tabs])
+        assert sum(t["counts"]["loop_skip"] for t in tabs) == o["counts"]["loop_skip"]
+        assert np.array_equal(win, o["winner"]) and np.array_equal(vic, o["victim"])
+        ctx.fuse(w.window, L, FUSE_PARAMS_CHECKS, window_S=w.win_S, win_list_begin=lb, phase=LC_FUSE_APPLY,
+                 winner=win, victim=vic)
+    else:
+        g = ctx.fuse(w.window, L, FUSE_PARAMS_CHECKS, window_S=w.win_S, win_list_begin=lb)
+        assert np.array_equal(g["winner"], o["winner"]) and np.array_equal(g["victim"], o["victim"])
+        assert np.array_equal(g["action"], o["action"])
+        assert g["counts"] == o["counts"], {k: (g["counts"][k], o["counts"][k]) for k in g["counts"]
+                                            if g["counts"][k] != o["counts"][k]}
+    st = ctx.download_map()
+    for key, ref in (("feat_mp", om.feat_mp), ("mp_flags", om.mp_flags), ("mp_replaced_by", om.mp_replaced_by),
+                     ("mp_nobs", om.mp_nobs)):
+        assert np.array_equal(st[key], ref), key
+    ctx.close()
+
+
 def test_forced_matches_sharded_plan_equals_fuse_all(Ctx):
     """Every shard's PLAN carries the forced matches (idempotent on an already forced map):
     PLAN per shard on one device, MIN merge, APPLY == FUSE_ALL."""
