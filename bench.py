@@ -448,7 +448,10 @@ def main():
     peak = peaks.get("hbm_gbs")
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md)"
     peak = peak or 6650.0
-    traffic = load_traffic().get("k_match", {}).get(args.config)
+    # ncu dram__bytes_read + dram__bytes_write of one k_match launch (profiles/traffic.json,
+    # written by scripts/ncu_summary.py --update-traffic from a --set full capture)
+    traffic = next((v for kname, v in load_traffic().get("per_kernel", {}).get(args.config, {}).items()
+                    if "k_match<" in kname), None)
     roof = None
     if Bk is not None and fam_ms.get("match", 0.0) > 0:
         def rl(name, B, kms):
@@ -505,6 +508,7 @@ def main():
         assert int(cnt_pin[counts.index("candidates")]) == cand_rank
         e_ms = float(np.mean(ee))
         e2e = {"value": cand_rank / (e_ms / 1000.0), "unit": UNIT, "ms_per_step": round(e_ms, 4),
+               "ms_median": round(float(np.median(ee)), 4), "ms_max": round(float(np.max(ee)), 4),
                "host_wall_ms_per_step": round(float(np.mean(hh)), 4),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "inputs": "window, window Sim3s, loop-list source keyframes (lists built on the device), "
