@@ -42,15 +42,18 @@ __device__ __forceinline__ void own_min(int32_t* owner, int m, int i) {
   atomicMin(&owner[m], i);
 }
 
-__device__ __forceinline__ void load13(const double* __restrict__ src, double* d) {
+// (a predecessor's output read after the PDL wait: plain coherent loads through a pointer
+// without __restrict__ -- an ld.global.nc / const __restrict__ load may be scheduled above
+// griddepcontrol.wait)
+__device__ __forceinline__ void load13(const double* src, double* d) {
   const double2* s2 = reinterpret_cast<const double2*>(src);
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
-    const double2 x = __ldg(s2 + i);
+    const double2 x = s2[i];
     d[2 * i] = x.x;
     d[2 * i + 1] = x.y;
   }
-  d[12] = __ldg(src + 12);
+  d[12] = src[12];
 }
 
 __device__ __forceinline__ void warp_count(uint32_t n, unsigned long long* dst) {
@@ -130,8 +133,8 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_win_mark(
 // Blocks [0, nb_mp): p <- fl32( inverse(S_o^corr)( T_o,w^old(p) ) ), corr_ref <- window[o]
 // (or -1); blocks [nb_mp, ...): window pose write-back T_iw <- SE3(S_i^corr).
 __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_win_b(
-    int n_mp, int nb_mp, int n_w, const int32_t* __restrict__ owner, const uint8_t* __restrict__ flags,
-    const int32_t* __restrict__ window, const double* __restrict__ scr, MpRec* __restrict__ rec,
+    int n_mp, int nb_mp, int n_w, const int32_t* owner, const uint8_t* __restrict__ flags,
+    const int32_t* __restrict__ window, const double* scr, MpRec* __restrict__ rec,
     int32_t* __restrict__ corr_ref, double* __restrict__ kf_pose,
     unsigned long long* __restrict__ counts) {
   uint32_t n = 0;
@@ -217,8 +220,8 @@ __global__ void k_all_kf(int n_kf, const double* __restrict__ Sopt, double* __re
 // order, so the two 13-double transforms are loaded once): every per-point load is
 // issued before the PDL wait, the transform gather after it.
 __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_all_points(
-    int n_mp, const double* __restrict__ scr, const int32_t* __restrict__ ref_kf,
-    const uint8_t* __restrict__ flags, MpRec* __restrict__ rec, int32_t* __restrict__ corr_ref,
+    int n_mp, const double* scr, const int32_t* __restrict__ ref_kf,
+    const uint8_t* flags, MpRec* __restrict__ rec, int32_t* __restrict__ corr_ref,
     unsigned long long* __restrict__ counts) {
   uint32_t n = 0;
   const int q0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x);

@@ -279,6 +279,31 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
     s_cam = a.cams[a.kf_cam[k]];
     s_cnt = 0;
   }
+  // software pipeline: the 32-B record (geometry sector) of the query two steps ahead
+  // is copied by cp.async into a per-thread 3-slot ring behind the hash (no registers
+  // held), its flag and the list entry three steps ahead are in flight in registers.
+  // The prologue is issued before the association hash is built, so the first records'
+  // latency overlaps the setup (the ring does not alias the hash).
+  const int64_t q0 = a.blk_q0[blk], q1 = a.blk_q1[blk];
+  uint4* s_rec = reinterpret_cast<uint4*>(s_hash + HS);   // [3][LC_NTHREADS][2]
+  auto list_at = [&](int64_t jj) -> int32_t { return jj < q1 ? __ldg(a.mp_list + jj) : -1; };
+  auto flag_at = [&](int32_t qq) -> uint8_t {
+    return (unsigned)qq < (unsigned)a.n_mp ? __ldg(a.mp_flags + qq) : (uint8_t)1;
+  };
+  auto issue = [&](int32_t qq, int slot) {
+    if ((unsigned)qq < (unsigned)a.n_mp) {
+      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + qq);
+      uint4* d = s_rec + 2 * (slot * LC_NTHREADS + tid);
+      cp_async16(d, rp);
+      cp_async16(d + 1, rp + 1);
+    }
+    cp_async_commit();   // one group per step, empty or not
+  };
+  int32_t qa = list_at(q0 + tid), qb = list_at(q0 + tid + LC_NTHREADS);
+  int32_t qc = list_at(q0 + tid + 2 * LC_NTHREADS);
+  uint8_t fa = flag_at(qa), fbl = flag_at(qb);
+  issue(qa, 0);
+  issue(qb, 1);
   if (tid < LC_MAX_LEVELS) s_scale[tid] = a.scale[tid];
   for (int i = tid; i < (int)HS; i += LC_NTHREADS) s_hash[i] = -1;
   for (int i = tid; i < (1 << (FILT_LOG2 - 5)); i += LC_NTHREADS) s_filt[i] = 0u;
@@ -309,34 +334,10 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
   const double c08 = 0.8 / sLm1;   // for the division-free pre-test only
   const bool pinhole = s_cam.model == 0;
   const float inv_lsf = 1.0f / logf((float)a.scale[1]);
-  const int64_t q0 = a.blk_q0[blk], q1 = a.blk_q1[blk];
-  const uint32_t epoch = a.loop_ep_w ? *a.epoch : 0u;
   const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
   Surv* out = a.surv + a.surv_off[blk];
   uint32_t cA = 0, cB = 0, cQ = 0;   // packed 10-bit counters (<= 64 queries per thread per block)
   uint32_t cE = 0;                   // edge-ambiguous culled queries (survivors: flag to k_match)
-  // software pipeline: the 32-B record (geometry sector) of the query two steps ahead
-  // is copied by cp.async into a per-thread 3-slot ring behind the hash (no registers
-  // held), its flag and the list entry three steps ahead are in flight in registers
-  uint4* s_rec = reinterpret_cast<uint4*>(s_hash + HS);   // [3][LC_NTHREADS][2]
-  auto list_at = [&](int64_t jj) -> int32_t { return jj < q1 ? __ldg(a.mp_list + jj) : -1; };
-  auto flag_at = [&](int32_t qq) -> uint8_t {
-    return (unsigned)qq < (unsigned)a.n_mp ? __ldg(a.mp_flags + qq) : (uint8_t)1;
-  };
-  auto issue = [&](int32_t qq, int slot) {
-    if ((unsigned)qq < (unsigned)a.n_mp) {
-      const uint4* rp = reinterpret_cast<const uint4*>(a.mp_rec + qq);
-      uint4* d = s_rec + 2 * (slot * LC_NTHREADS + tid);
-      cp_async16(d, rp);
-      cp_async16(d + 1, rp + 1);
-    }
-    cp_async_commit();   // one group per step, empty or not
-  };
-  int32_t qa = list_at(q0 + tid), qb = list_at(q0 + tid + LC_NTHREADS);
-  int32_t qc = list_at(q0 + tid + 2 * LC_NTHREADS);
-  uint8_t fa = flag_at(qa), fbl = flag_at(qb);
-  issue(qa, 0);
-  issue(qb, 1);
   int slot = 0;
   for (int64_t jb = q0; jb < q1; jb += LC_NTHREADS, slot = slot == 2 ? 0 : slot + 1) {
     const int64_t j = jb + tid;
@@ -351,7 +352,6 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
     const uint4 r1 = s_rec[2 * (slot * LC_NTHREADS + tid) + 1];
     qa = qb; fa = fbl; qb = qc; fbl = fc; qc = qd;
     const bool in_range = valid && (unsigned)q < (unsigned)a.n_mp;
-    if (a.loop_ep_w && in_range) a.loop_ep_w[q] = epoch;   // LoopSet stamp (pipelined mode)
     int status = 0;
     float fu = 0.f, fv = 0.f;
     int lvl = 0;
@@ -446,7 +446,14 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
   cnt[0] = cQ; cnt[1] = cA & 1023u; cnt[2] = (cA >> 10) & 1023u; cnt[3] = (cA >> 20) & 1023u;
   cnt[4] = cB & 1023u; cnt[5] = (cB >> 10) & 1023u; cnt[6] = (cB >> 20) & 1023u; cnt[7] = cE;
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
-  pdl_wait();   // (PDL) k_fuse_prep zeroes the counters: add after it completed
+  pdl_wait();   // (PDL) k_fuse_prep zeroes the counters and publishes the epoch
+  if (a.loop_ep_w) {   // LoopSet stamps of this block's list entries (L2-hot re-read)
+    const uint32_t epoch = *a.epoch;
+    for (int64_t j = q0 + tid; j < q1; j += LC_NTHREADS) {
+      const int32_t q = __ldg(a.mp_list + j);
+      if ((unsigned)q < (unsigned)a.n_mp) a.loop_ep_w[q] = epoch;
+    }
+  }
   block_add<8>(cnt, kProjSlot, cdst);
 }
 
@@ -1222,9 +1229,9 @@ __global__ void k_fuse_prep(int phase, int zero_counts, int64_t skip_lo, int64_t
 // Forced loop matches of the current keyframe (reading O9.4 / A23), thread per feature f
 // of cur_kf: the tables of a separate apply that runs before the search. Map points are
 // held once per keyframe, so every victim word gets at most one proposal.
-__global__ void k_forced(int n_mp, const uint32_t* __restrict__ ep, int fb, int F,
-                         const int32_t* __restrict__ forced, const int32_t* __restrict__ feat_mp,
-                         const uint8_t* __restrict__ flags, const uint32_t* __restrict__ loop_ep,
+__global__ void k_forced(int n_mp, const uint32_t* ep, int fb, int F,
+                         const int32_t* __restrict__ forced, const int32_t* feat_mp,
+                         const uint8_t* flags, const uint32_t* loop_ep,
                          unsigned long long* __restrict__ win_cur, unsigned long long* __restrict__ victim,
                          unsigned long long* __restrict__ counts) {
   pdl_wait();   // k_fuse_prep: tables initialised, LoopSet stamped, epoch published
@@ -1283,7 +1290,7 @@ __global__ void k_adds_scatter(int64_t n_wfeat, int64_t n, const long long* __re
 }
 
 // Victim marking: flags |= bad, replaced_by = survivor (reading O9 (iv)), victim bitmap.
-__global__ void k_fuse_victims(int n_mp, const unsigned long long* __restrict__ victim,
+__global__ void k_fuse_victims(int n_mp, const unsigned long long* victim,
                                uint8_t* __restrict__ flags, int32_t* __restrict__ replaced_by,
                                uint32_t* __restrict__ vbits, unsigned long long* __restrict__ counts) {
   pdl_wait();
@@ -1314,10 +1321,10 @@ __global__ void k_fuse_victims(int n_mp, const unsigned long long* __restrict__ 
 // winner on an empty window slot) -> compact list. One warp per keyframe, 16-B loads,
 // no shared memory (the victim bitmap stays L1-resident).
 __global__ void __launch_bounds__(LC_NTHREADS) k_apply_mark(
-    int n_kf, const uint32_t* __restrict__ ep, const int32_t* __restrict__ kf_fbeg,
-    const uint32_t* __restrict__ kf_win_ep, const int32_t* __restrict__ kf_win_pos,
-    const int64_t* __restrict__ woff_of_pos, const unsigned long long* __restrict__ winner,
-    const uint32_t* __restrict__ vbits, const int32_t* __restrict__ feat_mp,
+    int n_kf, const uint32_t* ep, const int32_t* __restrict__ kf_fbeg,
+    const uint32_t* kf_win_ep, const int32_t* kf_win_pos,
+    const int64_t* woff_of_pos, const unsigned long long* winner,
+    const uint32_t* vbits, const int32_t* __restrict__ feat_mp,
     int32_t* __restrict__ dirty_list) {
   pdl_wait();
   pdl_trigger();   // one wave: k_apply_fix may take the remaining slots now
@@ -1347,7 +1354,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_mark(
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int32_t mm = m[u];
-        if (mm >= 0) dirty |= (__ldg(vbits + (mm >> 5)) >> (mm & 31)) & 1u;
+        if (mm >= 0) dirty |= (vbits[mm >> 5] >> (mm & 31)) & 1u;
         else if (mm != INT32_MIN && wpos >= 0)
           dirty |= winner[f0 + 128 * (u >> 2) + 4 * lane + (u & 3) + wshift] != NONE;
       }
@@ -1368,11 +1375,11 @@ __device__ __constant__ int kApplySlot[A_N] = {LC_COUNT_REWIRED, LC_COUNT_DUP_CL
                                                LC_COUNT_ADDED};
 
 __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
-    const uint32_t* __restrict__ ep, const int32_t* __restrict__ kf_fbeg,
-    const uint32_t* __restrict__ kf_win_ep, const int32_t* __restrict__ kf_win_pos,
-    const int64_t* __restrict__ woff_of_pos, const unsigned long long* __restrict__ winner,
-    const unsigned long long* __restrict__ victim, const uint32_t* __restrict__ vbits,
-    const int32_t* __restrict__ dirty_list, int32_t* __restrict__ feat_mp, int32_t* __restrict__ nobs,
+    const uint32_t* ep, const int32_t* __restrict__ kf_fbeg,
+    const uint32_t* kf_win_ep, const int32_t* kf_win_pos,
+    const int64_t* woff_of_pos, const unsigned long long* winner,
+    const unsigned long long* victim, const uint32_t* vbits,
+    const int32_t* dirty_list, int32_t* __restrict__ feat_mp, int32_t* __restrict__ nobs,
     int hash_size, unsigned long long* __restrict__ counts) {
   pdl_wait();
   const uint32_t epoch = *ep;
@@ -1421,7 +1428,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int f = base + u * (int)blockDim.x + (int)threadIdx.x;
-        const bool isv = m[u] >= 0 && ((__ldg(vbits + (m[u] >> 5)) >> (m[u] & 31)) & 1u);
+        const bool isv = m[u] >= 0 && ((vbits[m[u] >> 5] >> (m[u] & 31)) & 1u);
         w[u] = isv ? victim[m[u]] : ((m[u] == -1 && wpos >= 0) ? winner[woff + f] : NONE);
         if (!isv && m[u] >= 0) w[u] = NONE;
       }
@@ -1475,6 +1482,124 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
         if (m >= 0) atomicSub(&nobs[m], 1);
         if (nv >= 0) atomicAdd(&nobs[nv], 1);
       }
+    }
+    __syncthreads();
+  }
+  block_add<A_N>(cnt, kApplySlot, counts);
+}
+
+// Apply pass 2 for keyframes of <= SPT * LC_NTHREADS slots: the same three steps with each
+// thread's SPT slots (f = u * LC_NTHREADS + tid) held in registers across them, so the only
+// shared state is the hash of the changed slots' new map points (+ its pre-filter), and only
+// the hash entries a keyframe used are reset after it (no per-keyframe table clear).
+// Step 2 marks a hashed map point held by an unchanged slot with the key f < 2^16, below
+// every changed slot's key (priority 1 or 2 in bits 16-17), exactly as k_apply_fix does.
+template <int SPT>
+__global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix_r(
+    const uint32_t* ep, const int32_t* __restrict__ kf_fbeg,
+    const uint32_t* kf_win_ep, const int32_t* kf_win_pos,
+    const int64_t* woff_of_pos, const unsigned long long* winner,
+    const unsigned long long* victim, const uint32_t* vbits,
+    const int32_t* dirty_list, int32_t* __restrict__ feat_mp, int32_t* __restrict__ nobs,
+    int hash_size, unsigned long long* __restrict__ counts) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t HS = (uint32_t)hash_size;
+  int32_t* s_key = (int32_t*)smem;
+  uint32_t* s_val = (uint32_t*)(s_key + hash_size);
+  uint32_t* s_filt = s_val + hash_size;   // 2^15-bit pre-filter
+#if LC_APPLY_WAIT_FIRST
+  pdl_wait();
+#endif
+  for (int i = threadIdx.x; i < (int)HS; i += blockDim.x) { s_key[i] = -1; s_val[i] = 0xFFFFFFFFu; }
+  for (int i = threadIdx.x; i < (1 << (FILT_LOG2 - 5)); i += blockDim.x) s_filt[i] = 0u;
+  pdl_wait();
+  const uint32_t epoch = *ep;
+  const int nd = dirty_list[0];
+  uint32_t cnt[A_N] = {0, 0, 0};
+  __syncthreads();
+  for (int di = blockIdx.x; di < nd; di += gridDim.x) {
+    const int k = dirty_list[1 + di];
+    const int fb = kf_fbeg[k], F = kf_fbeg[k + 1] - fb;
+    const int wpos = (kf_win_ep[k] == epoch) ? kf_win_pos[k] : -1;
+    const int64_t woff = wpos >= 0 ? woff_of_pos[wpos] : 0;
+    int32_t m[SPT], nv[SPT], h[SPT];
+    uint32_t prb = 0;   // 2 bits per slot: 0 unchanged, 1 ADD, 2 rewired
+    // (1) new value per slot, every load of a phase issued together
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      const int f = u * LC_NTHREADS + (int)threadIdx.x;
+      m[u] = f < F ? feat_mp[fb + f] : INT32_MIN;
+    }
+    bool isv[SPT];
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) isv[u] = m[u] >= 0 && ((vbits[m[u] >> 5] >> (m[u] & 31)) & 1u);
+    unsigned long long w[SPT];
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      const int f = u * LC_NTHREADS + (int)threadIdx.x;
+      w[u] = isv[u] ? victim[m[u]] : ((m[u] == -1 && wpos >= 0) ? winner[woff + f] : NONE);
+    }
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      const int f = u * LC_NTHREADS + (int)threadIdx.x;
+      nv[u] = m[u];
+      h[u] = -1;
+      if (w[u] != NONE) {
+        const uint32_t pr = isv[u] ? 2u : 1u;
+        nv[u] = (int32_t)(w[u] & 0xFFFFFFFFull);
+        prb |= pr << (2 * u);
+        if (pr == 2) cnt[A_REWIRED]++;
+        uint32_t hh = hslot(nv[u], HS);
+        while (true) {
+          const int32_t prev = atomicCAS(&s_key[hh], -1, nv[u]);
+          if (prev == -1 || prev == nv[u]) break;
+          hh = (hh + 1 == HS) ? 0 : hh + 1;
+        }
+        h[u] = (int)hh;
+        atomicMin(&s_val[hh], (pr << 16) | (uint32_t)f);
+        const uint32_t b = fslot(nv[u]);
+        atomicOr(&s_filt[b >> 5], 1u << (b & 31));
+      }
+    }
+    __syncthreads();
+    // (2) an unchanged slot holding a hashed map point keeps it (priority 0 wins)
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      if (((prb >> (2 * u)) & 3u) || nv[u] < 0) continue;
+      const uint32_t b = fslot(nv[u]);
+      if (!((s_filt[b >> 5] >> (b & 31)) & 1u)) continue;
+      uint32_t hh = hslot(nv[u], HS);
+      while (true) {
+        const int32_t v = s_key[hh];
+        if (v == nv[u]) { atomicMin(&s_val[hh], (uint32_t)(u * LC_NTHREADS + (int)threadIdx.x)); break; }
+        if (v == -1) break;
+        hh = (hh + 1 == HS) ? 0 : hh + 1;
+      }
+    }
+    __syncthreads();
+    // (3) losers of a hashed map point are cleared; changed slots written, n_obs deltas
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      const uint32_t pr = (prb >> (2 * u)) & 3u;
+      if (!pr) continue;
+      const int f = u * LC_NTHREADS + (int)threadIdx.x;
+      int32_t v = nv[u];
+      if (s_val[h[u]] != ((pr << 16) | (uint32_t)f)) { v = -1; cnt[A_DUP]++; }
+      else if (pr == 1) cnt[A_ADDED]++;
+      if (v != m[u]) {
+        feat_mp[fb + f] = v;
+        if (m[u] >= 0) atomicSub(&nobs[m[u]], 1);
+        if (v >= 0) atomicAdd(&nobs[v], 1);
+      }
+    }
+    __syncthreads();
+    // reset the entries this keyframe used (every set filter word belongs to a changed slot)
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      if (h[u] < 0) continue;
+      s_key[h[u]] = -1;
+      s_val[h[u]] = 0xFFFFFFFFu;
+      s_filt[fslot(nv[u]) >> 5] = 0u;
     }
     __syncthreads();
   }
@@ -1597,6 +1722,29 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
     if (e != cudaSuccess) return e;
     const int Fm = st.max_F > 0 ? st.max_F : 1;
     const int H = ((Fm + Fm / 2 + 1) + 31) & ~31;
+    if (Fm <= 8 * LC_NTHREADS && !getenv("LC_APPLY_SMEM")) {   // slots in registers (k_apply_fix_r)
+      const size_t sm = (size_t)H * 8 + (size_t)(1 << (FILT_LOG2 - 3));
+      auto go = [&](auto kern) -> cudaError_t {
+        cudaError_t e2 = set_smem_attr((const void*)kern, (int)sm);
+        if (e2 != cudaSuccess) return e2;
+#if LC_APPLY_NOPDL
+        kern<<<std::min(st.n_kf, 148 * 4), LC_NTHREADS, sm, s>>>(
+                          (const uint32_t*)st.ep, (const int32_t*)st.kf_fbeg, (const uint32_t*)st.kf_win_ep,
+                          (const int32_t*)st.kf_win_pos, d_woff, winner, victim, (const uint32_t*)st.mp_vbits,
+                          (const int32_t*)st.kf_dirty, st.feat_mp, st.mp_nobs, H, counts);
+        return cudaGetLastError();
+#endif
+        return launch_pdl(kern, dim3(std::min(st.n_kf, 148 * 4)), dim3(LC_NTHREADS), sm, s,
+                          (const uint32_t*)st.ep, (const int32_t*)st.kf_fbeg, (const uint32_t*)st.kf_win_ep,
+                          (const int32_t*)st.kf_win_pos, d_woff, winner, victim, (const uint32_t*)st.mp_vbits,
+                          (const int32_t*)st.kf_dirty, st.feat_mp, st.mp_nobs, H, counts);
+      };
+      e = Fm <= 2 * LC_NTHREADS ? go(k_apply_fix_r<2>) : Fm <= 4 * LC_NTHREADS ? go(k_apply_fix_r<4>)
+                                                                                 : go(k_apply_fix_r<8>);
+      if (e != cudaSuccess) return e;
+      c->launches += 2;
+      return cudaGetLastError();
+    }
     size_t smem = (size_t)H * 8 + (size_t)(1 << (FILT_LOG2 - 3)) + (size_t)Fm * 9 + 16;
     smem = (smem + 15) & ~(size_t)15;
     e = set_smem_attr((const void*)k_apply_fix, (int)smem);

@@ -1387,6 +1387,12 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     // kernel (measured slower at C5)
     const bool sole = !pipe && max_len <= 16384 && w_hi > w_lo &&
                       (c->sole_mode < 0 ? (w_hi - w_lo) >= 2 * 148 : c->sole_mode >= 1);
+    // a full-range PLAN without forced matches stamps the LoopSet in k_project (after its
+    // PDL wait, from its own list entries) instead of a separate pass over the lists in
+    // k_fuse_prep; a shard's PLAN needs the whole window's LoopSet, so prep stamps it there
+    static const bool stamp_prep_only = getenv("LC_STAMP_PREP") != nullptr;   // test knob
+    const bool stamp_proj = (phase & LC_FUSE_PLAN) && win_list_begin && w_lo == 0 && w_hi == n_window &&
+                            cur_pos < 0 && !stamp_prep_only;
     const int64_t ch = sole ? std::max<int64_t>(max_len, 1) : pick_chunk(total_q);
     std::vector<int32_t> bunit;
     std::vector<int64_t> bq0, bq1;
@@ -1502,7 +1508,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       // table (the other shards' units included) is set to NONE here (lc.h contract)
       const int64_t skip_lo = sole ? woff[w_lo] : 0, skip_hi = sole ? woff[w_hi] : 0;
       CK(launch_fuse_prep(c, phase, cur_pos < 0 ? 1 : 0, skip_lo, skip_hi, n_window, d_win, n_wfeat, d_list,
-                          pipe ? 0 : n_list, win, vic, cnt, call.s));
+                          (pipe || stamp_proj) ? 0 : n_list, win, vic, cnt, call.s));
     }
     if (phase & LC_FUSE_PLAN) {
       a.unit_kf = d_win;
@@ -1535,7 +1541,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       a.surv_off = d_boff;
       a.surv_cnt = d_scnt;
       a.sole = sole ? (c->sole_mode == 2 ? 2 : 1) : 0;
-      a.loop_ep_w = pipe ? st.mp_loop_ep : nullptr;   // the pipelined mode stamps the LoopSet in k_project
+      a.loop_ep_w = (pipe || stamp_proj) ? st.mp_loop_ep : nullptr;   // k_project stamps the LoopSet
       if (pipe) {
         for (int k = 0; k < lc_ctx::kPipe; ++k) {
           const int b0 = pipe_b[k], nbk = pipe_b[k + 1] - pipe_b[k];
