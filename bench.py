@@ -570,19 +570,21 @@ def main():
                 cs.state_save()
                 lst = torch.from_numpy(ws_.mp_list).to(dev)
                 Sop = torch.from_numpy(ws_.S_opt).to(dev)
+                wS = torch.from_numpy(np.ascontiguousarray(ws_.win_S)).to(dev)   # resident, as in the headline step
                 sms, scnt = [], None
-                for i in range(3 + max(3, args.steps // 2)):
+                nw = max(args.warmup, 5)   # (a new context: its first calls allocate scratch and pinned staging)
+                for i in range(nw + max(3, args.steps // 2)):
                     cs.state_restore()
                     flush.fill_(1.0)
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     a.record(stream)
                     cs.correct_window(ws_.cur_kf, ws_.S_cw_corr, ws_.window, host=False)
-                    rr = cs.fuse(ws_.window, lst, FUSE_PARAMS, window_S=ws_.win_S, win_list_begin=ws_.win_list_begin,
+                    rr = cs.fuse(ws_.window, lst, FUSE_PARAMS, window_S=wS, win_list_begin=ws_.win_list_begin,
                                  action=False, host=False)
                     cs.correct_all(Sop, host=False)
                     b.record(stream)
                     b.synchronize()
-                    if i >= 3:
+                    if i >= nw:
                         sms.append(a.elapsed_time(b))
                     scnt = rr["counts"]
                 cand_s = int(scnt[counts.index("candidates")].item())

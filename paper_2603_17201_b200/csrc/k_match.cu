@@ -1354,7 +1354,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_mark(
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int32_t mm = m[u];
-        if (mm >= 0) dirty |= (vbits[mm >> 5] >> (mm & 31)) & 1u;
+        if (mm >= 0) dirty |= (ld_nc_after_wait(vbits + (mm >> 5)) >> (mm & 31)) & 1u;
         else if (mm != INT32_MIN && wpos >= 0)
           dirty |= winner[f0 + 128 * (u >> 2) + 4 * lane + (u & 3) + wshift] != NONE;
       }
@@ -1428,7 +1428,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int f = base + u * (int)blockDim.x + (int)threadIdx.x;
-        const bool isv = m[u] >= 0 && ((vbits[m[u] >> 5] >> (m[u] & 31)) & 1u);
+        const bool isv = m[u] >= 0 && ((ld_nc_after_wait(vbits + (m[u] >> 5)) >> (m[u] & 31)) & 1u);
         w[u] = isv ? victim[m[u]] : ((m[u] == -1 && wpos >= 0) ? winner[woff + f] : NONE);
         if (!isv && m[u] >= 0) w[u] = NONE;
       }
@@ -1532,7 +1532,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix_r(
     }
     bool isv[SPT];
 #pragma unroll
-    for (int u = 0; u < SPT; ++u) isv[u] = m[u] >= 0 && ((vbits[m[u] >> 5] >> (m[u] & 31)) & 1u);
+    for (int u = 0; u < SPT; ++u) isv[u] = m[u] >= 0 && ((ld_nc_after_wait(vbits + (m[u] >> 5)) >> (m[u] & 31)) & 1u);
     unsigned long long w[SPT];
 #pragma unroll
     for (int u = 0; u < SPT; ++u) {

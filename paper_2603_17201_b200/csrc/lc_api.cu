@@ -156,7 +156,11 @@ struct Call {
       if (c->pin[r]) CK(cudaFreeHost(c->pin[r]));
       c->pin[r] = nullptr;
       c->pin_cap[r] = 0;
-      size_t cap = std::max<size_t>(bytes * 2, 1 << 16);
+      // every slot grows to the largest block seen so far (calls of different sizes rotate
+      // through the ring, so a per-slot size would reallocate -- cudaHostAlloc, ~1 ms --
+      // each time a large block first lands on a slot that held small ones)
+      size_t cap = std::max<size_t>({bytes * 2, (size_t)1 << 20, c->pin_cap_max});
+      c->pin_cap_max = cap;
       if (cudaHostAlloc(&c->pin[r], cap, cudaHostAllocDefault) != cudaSuccess) {
         cudaGetLastError();
         set_err(c, "pinned staging allocation failed");

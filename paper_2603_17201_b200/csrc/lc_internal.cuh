@@ -199,6 +199,7 @@ struct lc_ctx {
   static constexpr int kPinRing = 8;
   void* pin[kPinRing] = {};
   size_t pin_cap[kPinRing] = {};
+  size_t pin_cap_max = 0;               // capacity every slot is (re)allocated with
   cudaEvent_t pin_ev[kPinRing] = {};   // recorded after the H2D out of that slot
   bool pin_ev_pending[kPinRing] = {};
   int pin_next = 0;
@@ -319,6 +320,14 @@ __device__ __forceinline__ void lc_project(const DevCam& c, double x, double y, 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Read-only-path load of a predecessor's output after pdl_wait(): a volatile asm statement
+// keeps its place after griddepcontrol.wait (an __ldg / const __restrict__ load may be
+// treated as invariant and scheduled above the wait).
+__device__ __forceinline__ uint32_t ld_nc_after_wait(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
