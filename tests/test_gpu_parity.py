@@ -292,6 +292,30 @@ def test_state_save_restore_and_determinism(Ctx):
             assert np.array_equal(r[2][k], runs[0][2][k]), k
 
 
+@pytest.mark.parametrize("name", ["S3", "C2"])
+def test_first_call_equals_later_calls(Ctx, name):
+    """A fresh context's FIRST loop event must equal its later ones (the first launch of a
+    kernel is when lazy module loading and PDL early starts interact; a predecessor's
+    output read through a const __restrict__ pointer was once scheduled above the PDL
+    wait and made the first APPLY skip keyframes)."""
+    w = world(name)
+    runs = []
+    for _ in range(2):   # two fresh contexts: the first call of each is checked
+        ctx, _ = _pair(Ctx, w)
+        ctx.state_save()
+        for _ in range(3):
+            ctx.state_restore()
+            ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+            g = ctx.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+            ctx.correct_all(w.S_opt)
+            runs.append((g["winner"].copy(), g["victim"].copy(), ctx.download_map()))
+        ctx.close()
+    for i, r in enumerate(runs[1:], 1):
+        assert np.array_equal(r[0], runs[0][0]) and np.array_equal(r[1], runs[0][1]), f"run {i}: tables"
+        for k in r[2]:
+            assert np.array_equal(r[2][k], runs[0][2][k]), f"run {i}: {k}"
+
+
 def test_sharded_plan_merge_apply_equals_single(Ctx):
     """The multi-GPU protocol on one device: PLAN per keyframe shard, elementwise MIN of
     the tables (what NCCL all_reduce(MIN) computes), APPLY -> identical to FUSE_ALL."""
