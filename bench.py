@@ -331,19 +331,26 @@ def main():
     cnt_window = []
 
     def step(params=FUSE_PARAMS):
-        _, cw = ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
-        cnt_window[:] = [cw]
         if ws == 1:
+            _, cw = ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
+            cnt_window[:] = [cw]
             r = ctx.fuse(w.window, mp_list_d, params, window_S=win_S_d,
                          win_list_begin=w.win_list_begin, winner=win_t, victim=vic_t,
                          action=False, host=False)
-            c = r["counts"]
-        else:
-            c, _, info = lcdist.fuse_sharded(ctx, w.window, mp_list_d, params, window_S=win_S_d,
-                                             win_list_begin=w.win_list_begin, device=dev, tables=tables,
-                                             events=comm_ev[0] if comm_ev else None)
-            last_info.update(info)
-        ctx.correct_all(S_opt_d, host=False)
+            ctx.correct_all(S_opt_d, host=False)
+            return r["counts"]
+        # N > 1: WINDOW / ALL point passes by map-point slice + position
+        # all_gathers, the fuse by keyframe shard + victim MIN + sparse ADD all_gather
+        ev = comm_ev[0] if comm_ev else None
+        cw, nb_w = lcdist.correct_window_sharded(ctx, w.cur_kf, w.S_cw_corr, w.window, device=dev,
+                                                 events=ev[0] if ev else None)
+        cnt_window[:] = [cw]
+        c, _, info = lcdist.fuse_sharded(ctx, w.window, mp_list_d, params, window_S=win_S_d,
+                                         win_list_begin=w.win_list_begin, device=dev, tables=tables,
+                                         events=ev[1] if ev else None)
+        _, nb_a = lcdist.correct_all_sharded(ctx, S_opt_d, device=dev, events=ev[2] if ev else None)
+        last_info.update(info)
+        last_info["positions_allgather"] = nb_w + nb_a
         return c
 
     def reset():
@@ -369,18 +376,21 @@ def main():
         step()
         torch.cuda.synchronize()
         vic_sh = vic_t.clone()
-        fm_sh = ctx.download_map()["feat_mp"]
+        st_sh = ctx.download_map()
         reset()
         ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window, host=False)
         ref = ctx.fuse(w.window, mp_list_d, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin,
                        action=False, host=False)
+        ctx.correct_all(S_opt_d, host=False)
         torch.cuda.synchronize()
-        ok = bool(torch.equal(ref["victim"], vic_sh)) and bool(np.array_equal(ctx.download_map()["feat_mp"], fm_sh))
+        st_ref = ctx.download_map()
+        ok = bool(torch.equal(ref["victim"], vic_sh)) and all(
+            np.array_equal(st_ref[k], st_sh[k]) for k in ("feat_mp", "mp_pos", "kf_pose", "mp_nobs", "mp_flags"))
         okt = torch.tensor([1 if ok else 0], dtype=torch.int64, device=dev)
         tdist.all_reduce(okt, op=tdist.ReduceOp.MIN)
-        merge_check = "equal to the unsharded FUSE_ALL" if int(okt.item()) == 1 else "MISMATCH"
-        if merge_check != "equal to the unsharded FUSE_ALL":
-            raise SystemExit("bench: sharded fusion differs from the unsharded FUSE_ALL")
+        merge_check = "equal to the unsharded loop event" if int(okt.item()) == 1 else "MISMATCH"
+        if merge_check != "equal to the unsharded loop event":
+            raise SystemExit("bench: the sharded loop event differs from the unsharded one")
 
     # timed region: barrier + sync on both sides, events per step on the launching stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -394,7 +404,8 @@ def main():
     for i in range(args.steps):
         reset()
         if ws > 1:
-            comm_ev[:] = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))]
+            comm_ev[:] = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                           for _ in range(3)]]   # position gather (WINDOW), fuse exchange, position gather (ALL)
             comm_pairs.append(comm_ev[0])
         ev[i][0].record(stream)
         step()
@@ -425,7 +436,8 @@ def main():
     cand_total = int(cand_t.item())
     multi = None
     if ws > 1:   # the exchange's share of the step (max over ranks)
-        cm = torch.tensor([float(np.mean([a.elapsed_time(b) for a, b in comm_pairs]))], dtype=torch.float64,
+        cm = torch.tensor([float(np.mean([sum(a.elapsed_time(b) for a, b in prs) for prs in comm_pairs]))],
+                          dtype=torch.float64,
                           device=dev)
         tdist.all_reduce(cm, op=tdist.ReduceOp.MAX)
         eb = last_info.get("exchange_bytes", {})
@@ -433,10 +445,13 @@ def main():
                  "compute_ms_per_step": round(ms_step - float(cm.item()), 5),
                  "victim_allreduce_bytes": int(eb.get("victim_allreduce", 0)),
                  "adds_allgather_bytes": int(eb.get("adds_allgather", 0)),
+                 "positions_allgather_bytes": int(last_info.get("positions_allgather", 0)),
                  "n_adds": int(last_info.get("n_adds", 0)),
                  "collectives": "all_reduce(MIN) int64 victim words + all_gather of sparse (index, word) "
-                                "ADD lists (" + tdist.get_backend() + ")",
-                 "replicated": "WINDOW correction, APPLY, ALL correction (deterministic; DESIGN.md §7)",
+                                "ADD lists + 2 all_gathers of fp32 position slices (" + tdist.get_backend() + ")",
+                 "sharded": "fuse PLAN by keyframe shard; WINDOW / ALL point passes by map-point slice",
+                 "replicated": "WINDOW / ALL keyframe poses + owner election, fuse APPLY (deterministic; "
+                               "DESIGN.md §7)",
                  "merge_check": merge_check}
     value = cand_total / (ms_step / 1000.0)
 

@@ -582,6 +582,29 @@ lc_status lc_fuse_adds(lc_ctx* ctx, int32_t op, int32_t n_window, const int32_t*
                        int64_t capacity, void* cuda_stream);
 
 /* ---------------------------------------------------------------------------
+ * lc_set_point_range / lc_mp_positions -- the map-point slices of a sharded correction
+ * (SURVEY.md §8(e) "Correction": "ALL mode is sharded by MP index range, followed by
+ * all_gather of corrected position slices"; WINDOW "point correction is sharded by MP
+ * index range, followed by all_gather of the slices"; §III.B).
+ *
+ * lc_set_point_range: every later lc_correct_sim3 call (LC_CORRECT_WINDOW, LC_CORRECT_ALL;
+ *   not LC_DRY_RUN) rewrites the positions of the map points in [mp_lo, mp_hi) only, and
+ *   its CORR_MP counter counts those. Everything else it does stays replicated on every
+ *   rank: keyframe poses, S^corr, the owner election and the per-point corr_ref record of
+ *   which window keyframe re-anchored a point (so the ranks' stores stay identical once
+ *   the position slices are exchanged). mp_hi < 0 restores "all points". Persists until
+ *   changed; lc_upload_map resets it. Errors: LC_ESTATE (no map), LC_EINVAL
+ *   (mp_lo < 0, mp_lo > mp_hi, mp_hi > number of map points).
+ * lc_mp_positions: op LC_POS_GET copies the fp32 positions of map points [mp_lo, mp_hi)
+ *   into xyz, op LC_POS_SET writes xyz into the store; xyz [host|dev] [(mp_hi - mp_lo) * 3]
+ *   (x, y, z per point). Errors: LC_ESTATE, LC_EINVAL (op, range, null xyz with a
+ *   non-empty range). */
+lc_status lc_set_point_range(lc_ctx* ctx, int32_t mp_lo, int32_t mp_hi);
+#define LC_POS_GET 1
+#define LC_POS_SET 2
+lc_status lc_mp_positions(lc_ctx* ctx, int32_t op, int32_t mp_lo, int32_t mp_hi, float* xyz, void* cuda_stream);
+
+/* ---------------------------------------------------------------------------
  * lc_search_by_projection -- batched read-only projection search
  * (PAPER.md:200). Pair p = (keyframe pair_kf[p], transform
  * pair_S[p], parameter set params[pair_param[p]], list mp_list[pair_list_begin[p]

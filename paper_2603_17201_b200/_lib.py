@@ -18,6 +18,7 @@ LC_NONE = (1 << 63) - 1
 LC_CORRECT_WINDOW, LC_CORRECT_ALL, LC_DRY_RUN = 1, 2, 4
 LC_FUSE_PLAN, LC_FUSE_APPLY, LC_FUSE_ALL = 1, 2, 3
 LC_ADDS_PACK, LC_ADDS_UNPACK = 1, 2
+LC_POS_GET, LC_POS_SET = 1, 2
 LC_UPLOAD_REPLACE, LC_UPLOAD_APPEND = 0, 1
 LC_REFRESH_DESC, LC_REFRESH_NORMAL = 1, 2
 COUNTER_NAMES = [
@@ -115,6 +116,8 @@ def load():
                           vp, vp, vp, vp, vp]),
         "lc_loop_lists": (i32, [vp, i32, vp, vp, vp, vp, i64, vp]),
         "lc_fuse_adds": (i32, [vp, i32, i32, vp, i32, i32, vp, vp, vp, vp, i64, vp]),
+        "lc_set_point_range": (i32, [vp, i32, i32]),
+        "lc_mp_positions": (i32, [vp, i32, i32, i32, vp, vp]),
         "lc_search_by_projection": (i32, [vp, i32, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp,
                                           vp, vp]),
         "lc_refresh_mappoints": (i32, [vp, i32, vp, i32, vp, vp]),
@@ -141,5 +144,6 @@ def exported_symbols():
     return ["lc_create", "lc_destroy", "lc_last_error", "lc_kernel_launches", "lc_profile_enable",
             "lc_profile_read", "lc_upload_map",
             "lc_download_map", "lc_state_save", "lc_state_restore", "lc_correct_sim3", "lc_fuse", "lc_fuse_adds", "lc_loop_lists",
+            "lc_set_point_range", "lc_mp_positions",
             "lc_search_by_projection", "lc_refresh_mappoints", "lc_update_connections", "lc_sim3_ransac", "lc_sim3_refine", "lc_pgo_sim3", "lc_graph_begin", "lc_graph_end", "lc_graph_launch",
             "lc_graph_destroy"]

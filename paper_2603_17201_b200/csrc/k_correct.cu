@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_win_mark(
 // Blocks [0, nb_mp): p <- fl32( inverse(S_o^corr)( T_o,w^old(p) ) ), corr_ref <- window[o]
 // (or -1); blocks [nb_mp, ...): window pose write-back T_iw <- SE3(S_i^corr).
 __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_win_b(
-    int n_mp, int nb_mp, int n_w, const int32_t* owner, const uint8_t* __restrict__ flags,
+    int n_mp, int nb_mp, int n_w, int mp_lo, int mp_hi, const int32_t* owner, const uint8_t* __restrict__ flags,
     const int32_t* __restrict__ window, const double* scr, MpRec* __restrict__ rec,
     int32_t* __restrict__ corr_ref, double* __restrict__ kf_pose,
     unsigned long long* __restrict__ counts) {
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_win_b(
       pf[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (q0 + u < n_mp) {
         fl[u] = flags[q0 + u];
-        pf[u] = *reinterpret_cast<const float4*>(rec + q0 + u);
+        if (q0 + u >= mp_lo && q0 + u < mp_hi) pf[u] = *reinterpret_cast<const float4*>(rec + q0 + u);
       }
     }
     pdl_wait();
@@ -165,6 +165,8 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_win_b(
         corr_ref[q] = -1;
         continue;
       }
+      corr_ref[q] = window[o[u]];   // (every point: the owner bookkeeping stays replicated)
+      if (q < mp_lo || q >= mp_hi) continue;   // another rank's point slice (lc_set_point_range)
       if (o[u] != have) {
         const double* S = scr + (size_t)WSTR * o[u];
         load13(S, T);
@@ -177,7 +179,6 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_win_b(
       rec[q].pos[0] = __double2float_rn(pw[0]);
       rec[q].pos[1] = __double2float_rn(pw[1]);
       rec[q].pos[2] = __double2float_rn(pw[2]);
-      corr_ref[q] = window[o[u]];
       ++n;
     }
     warp_count(n, &counts[LC_COUNT_CORR_MP]);
@@ -220,7 +221,7 @@ __global__ void k_all_kf(int n_kf, const double* __restrict__ Sopt, double* __re
 // order, so the two 13-double transforms are loaded once): every per-point load is
 // issued before the PDL wait, the transform gather after it.
 __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_all_points(
-    int n_mp, const double* scr, const int32_t* __restrict__ ref_kf,
+    int n_mp, int mp_lo, int mp_hi, const double* scr, const int32_t* __restrict__ ref_kf,
     const uint8_t* flags, MpRec* __restrict__ rec, int32_t* __restrict__ corr_ref,
     unsigned long long* __restrict__ counts) {
   uint32_t n = 0;
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_all_points(
       cr[u] = corr_ref[q0 + u];
       rk[u] = ref_kf[q0 + u];
       fl[u] = flags[q0 + u];
-      pf[u] = *reinterpret_cast<const float4*>(rec + q0 + u);
+      if (q0 + u >= mp_lo && q0 + u < mp_hi) pf[u] = *reinterpret_cast<const float4*>(rec + q0 + u);
     }
   }
   pdl_wait();
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_all_points(
     const int q = q0 + u;
     if (q >= n_mp) break;
     if (cr[u] >= 0) corr_ref[q] = -1;
-    if (fl[u] & 1u) continue;
+    if ((fl[u] & 1u) || q < mp_lo || q >= mp_hi) continue;   // bad, or another rank's slice
     const int r = cr[u] >= 0 ? cr[u] : rk[u];
     if (r != have) {
       const double* S = scr + (size_t)ASTR * r;
@@ -437,7 +438,7 @@ cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t
   const int nb_mp = st.n_mp > 0 ? (st.n_mp + 2 * LC_NTHREADS - 1) / (2 * LC_NTHREADS) : 0;
   const int nb_w = (n_w + LC_NTHREADS - 1) / LC_NTHREADS;
   if ((e = launch_pdl(k_win_b, dim3(nb_mp + nb_w), dim3(LC_NTHREADS), 0, s, st.n_mp, nb_mp, n_w,
-                      st.mp_owner, st.mp_flags, d_window, d_scr, st.mp_rec, st.mp_corr_ref, st.kf_pose,
+                      c->mp_lo, c->mp_hi < 0 ? st.n_mp : c->mp_hi, st.mp_owner, st.mp_flags, d_window, d_scr, st.mp_rec, st.mp_corr_ref, st.kf_pose,
                       counts)) != cudaSuccess)
     return e;
   c->launches += 3;
@@ -452,12 +453,40 @@ cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
   c->launches++;
   if (st.n_mp > 0) {
     cudaError_t e = launch_pdl(k_all_points, dim3((st.n_mp + 2 * LC_NTHREADS - 1) / (2 * LC_NTHREADS)),
-                               dim3(LC_NTHREADS), 0, s, st.n_mp, (const double*)d_scr,
+                               dim3(LC_NTHREADS), 0, s, st.n_mp, c->mp_lo,
+                               c->mp_hi < 0 ? st.n_mp : c->mp_hi, (const double*)d_scr,
                                (const int32_t*)st.mp_ref_kf, (const uint8_t*)st.mp_flags, st.mp_rec,
                                st.mp_corr_ref, counts);
     if (e != cudaSuccess) return e;
     c->launches++;
   }
+  return cudaGetLastError();
+}
+
+namespace {
+// lc_mp_positions: fp32 positions of map points [lo, hi) out of / into the records
+__global__ void k_pos_get(int lo, int hi, const MpRec* __restrict__ rec, float* __restrict__ xyz) {
+  for (int q = lo + blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += gridDim.x * blockDim.x) {
+    const float4 p = *reinterpret_cast<const float4*>(rec + q);
+    float* o = xyz + 3 * (size_t)(q - lo);
+    o[0] = p.x; o[1] = p.y; o[2] = p.z;
+  }
+}
+__global__ void k_pos_set(int lo, int hi, const float* __restrict__ xyz, MpRec* __restrict__ rec) {
+  for (int q = lo + blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += gridDim.x * blockDim.x) {
+    const float* i = xyz + 3 * (size_t)(q - lo);
+    rec[q].pos[0] = i[0]; rec[q].pos[1] = i[1]; rec[q].pos[2] = i[2];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_mp_positions(lc_ctx* c, int op, int lo, int hi, float* xyz, cudaStream_t s) {
+  if (hi <= lo) return cudaSuccess;
+  const int g = std::min((hi - lo + LC_NTHREADS - 1) / LC_NTHREADS, 148 * 8);
+  if (op == LC_POS_GET) k_pos_get<<<g, LC_NTHREADS, 0, s>>>(lo, hi, c->st.mp_rec, xyz);
+  else k_pos_set<<<g, LC_NTHREADS, 0, s>>>(lo, hi, xyz, c->st.mp_rec);
+  c->launches++;
   return cudaGetLastError();
 }
 

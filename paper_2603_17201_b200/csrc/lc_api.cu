@@ -146,27 +146,36 @@ struct Call {
       for (auto& f : arg_fix) *f.first = d_args + f.second;
       return;
     }
+    // the whole ring is (re)allocated at once, every slot at the largest block seen so far
+    // (x2, >= 1 MB): page-locked allocation synchronises with the device and takes ~1 ms+,
+    // so it must not happen slot by slot in the steps that follow the first call (calls of
+    // different sizes rotate through the ring)
+    if (c->pin_cap_max < bytes) {
+      const size_t cap = std::max<size_t>(bytes * 2, (size_t)1 << 20);
+      for (int q = 0; q < lc_ctx::kPinRing; ++q) {
+        if (c->pin_ev_pending[q]) {
+          CK(cudaEventSynchronize(c->pin_ev[q]));
+          c->pin_ev_pending[q] = false;
+        }
+        if (c->pin[q]) CK(cudaFreeHost(c->pin[q]));
+        c->pin[q] = nullptr;
+        c->pin_cap[q] = 0;
+        if (cudaHostAlloc(&c->pin[q], cap, cudaHostAllocDefault) != cudaSuccess) {
+          cudaGetLastError();
+          c->pin[q] = nullptr;
+          c->pin_cap_max = 0;
+          set_err(c, "pinned staging allocation failed");
+          throw Fail{LC_ENOMEM};
+        }
+        c->pin_cap[q] = cap;
+      }
+      c->pin_cap_max = cap;
+    }
     const int r = c->pin_next;
     c->pin_next = (r + 1) % lc_ctx::kPinRing;
     if (c->pin_ev_pending[r]) {
       CK(cudaEventSynchronize(c->pin_ev[r]));
       c->pin_ev_pending[r] = false;
-    }
-    if (c->pin_cap[r] < bytes) {
-      if (c->pin[r]) CK(cudaFreeHost(c->pin[r]));
-      c->pin[r] = nullptr;
-      c->pin_cap[r] = 0;
-      // every slot grows to the largest block seen so far (calls of different sizes rotate
-      // through the ring, so a per-slot size would reallocate -- cudaHostAlloc, ~1 ms --
-      // each time a large block first lands on a slot that held small ones)
-      size_t cap = std::max<size_t>({bytes * 2, (size_t)1 << 20, c->pin_cap_max});
-      c->pin_cap_max = cap;
-      if (cudaHostAlloc(&c->pin[r], cap, cudaHostAllocDefault) != cudaSuccess) {
-        cudaGetLastError();
-        set_err(c, "pinned staging allocation failed");
-        throw Fail{LC_ENOMEM};
-      }
-      c->pin_cap[r] = cap;
     }
     memcpy(c->pin[r], args.data(), args.size());
     d_args = (char*)scratch(bytes);
@@ -838,6 +847,8 @@ lc_status lc_upload_map(lc_ctx* c, const lc_map_view* m, const lc_camera* cams, 
     REQUIRE(errs[1] == 0, LC_ERANGE, "feat_mp out of range");
     REQUIRE(errs[2] == 0, LC_ERANGE, "mp_ref_kf out of range");
     REQUIRE(errs[3] == 0, LC_ERANGE, "kf_cam out of range");
+    c->mp_lo = 0;   // lc_set_point_range: back to all points
+    c->mp_hi = -1;
     c->has_map = true;
   });
 }
@@ -1247,12 +1258,14 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t n_batch, const int32_
                           void* stream) {
   return guarded(c, [&] {
     const bool dry = mode == (LC_CORRECT_WINDOW | LC_DRY_RUN);
+    HostProf hp(c, "lc_correct_sim3");
     capture_gate(c, stream, !dry);
     REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
     REQUIRE(mode == LC_CORRECT_WINDOW || mode == LC_CORRECT_ALL || dry, LC_EINVAL, "bad mode");
     Store& st = c->st;
     Call call(c, stream);
     unsigned long long* cnt = call.counts(out_counts, LC_NCOUNT);   // zeroed by the first kernel
+    hp.mark("counts");
     if (mode & LC_CORRECT_WINDOW) {
       REQUIRE(cur_kf && S_cw_corr && window_begin && window_kf, LC_EINVAL, "null WINDOW argument");
       REQUIRE(dry ? n_batch >= 1 : n_batch == 1, LC_EINVAL, "n_batch must be 1 (>= 1 with LC_DRY_RUN)");
@@ -1270,7 +1283,9 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t n_batch, const int32_
       call.arg(window_kf, n_slots, &d_win);
       call.arg((const double*)S_cw_corr, 13 * (size_t)n_batch, &d_S);
       call.arg(window_begin, (size_t)n_batch + 1, &d_wb);
+      hp.mark("validate");
       call.commit();
+      hp.mark("commit");
       if (dry) {
         REQUIRE(out_S_corr && out_mp_begin && out_capacity >= 0 && (out_capacity == 0 || (out_mp_idx && out_mp_pos)),
                 LC_EINVAL, "null DRY_RUN output");
@@ -1295,10 +1310,12 @@ lc_status lc_correct_sim3(lc_ctx* c, int32_t mode, int32_t n_batch, const int32_
       const int n_window = n_slots;
       double* scr = (double*)call.scratch(sizeof(double) * correct_window_scratch_stride() * (size_t)n_window);
       double* d_outS = (out_S_corr && is_device_ptr(c, out_S_corr)) ? (double*)out_S_corr : nullptr;
+      hp.mark("scratch");
       {
         Prof pr(c, LC_PROF_CORRECT_WINDOW, call.s);
         CK(launch_correct_window(c, 0, n_window, d_win, d_S, scr, d_outS, cnt, call.s));
       }
+      hp.mark("launch");
       if (out_S_corr && !d_outS) {
         CK(cudaMemcpy2DAsync(out_S_corr, sizeof(lc_sim3), scr + 28, sizeof(double) * correct_window_scratch_stride(),
                              sizeof(lc_sim3), n_window, cudaMemcpyDefault, call.s));
@@ -1680,6 +1697,34 @@ lc_status lc_loop_lists(lc_ctx* c, int32_t n, const int32_t* src_begin, const in
       const int32_t* d_ob2 = call.in(ob2, 2);   // (pageable -> staged before the call returns)
       CK(launch_lists_sort(c, 1, cnt[l], d_one_ro, d_reg, d_ob2, d_out + out_begin[l], call.s));
     }
+    call.finish();
+  });
+}
+
+// ----------------------------------------------------------------------------
+lc_status lc_set_point_range(lc_ctx* c, int32_t mp_lo, int32_t mp_hi) {
+  return guarded(c, [&] {
+    capture_gate(c, (void*)c->cap_stream, true);
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    if (mp_hi < 0) { c->mp_lo = 0; c->mp_hi = -1; return; }
+    REQUIRE(mp_lo >= 0 && mp_lo <= mp_hi && mp_hi <= c->st.n_mp, LC_EINVAL, "bad map-point range");
+    c->mp_lo = mp_lo;
+    c->mp_hi = mp_hi;
+  });
+}
+
+lc_status lc_mp_positions(lc_ctx* c, int32_t op, int32_t mp_lo, int32_t mp_hi, float* xyz, void* stream) {
+  return guarded(c, [&] {
+    capture_gate(c, stream, true);
+    REQUIRE(c->has_map, LC_ESTATE, "no map uploaded");
+    REQUIRE(op == LC_POS_GET || op == LC_POS_SET, LC_EINVAL, "bad op");
+    REQUIRE(mp_lo >= 0 && mp_lo <= mp_hi && mp_hi <= c->st.n_mp, LC_EINVAL, "bad map-point range");
+    const size_t n = 3 * (size_t)(mp_hi - mp_lo);
+    REQUIRE(n == 0 || xyz, LC_EINVAL, "null xyz");
+    if (n == 0) return;
+    Call call(c, stream);
+    float* d = op == LC_POS_GET ? call.out(xyz, n) : const_cast<float*>(call.in((const float*)xyz, n));
+    CK(launch_mp_positions(c, op, mp_lo, mp_hi, d, call.s));
     call.finish();
   });
 }

@@ -200,6 +200,9 @@ struct lc_ctx {
   void* pin[kPinRing] = {};
   size_t pin_cap[kPinRing] = {};
   size_t pin_cap_max = 0;               // capacity every slot is (re)allocated with
+  // lc_set_point_range: the map-point slice [mp_lo, mp_hi) whose positions the correction
+  // passes rewrite on this rank (mp_hi < 0: all)
+  int32_t mp_lo = 0, mp_hi = -1;
   cudaEvent_t pin_ev[kPinRing] = {};   // recorded after the H2D out of that slot
   bool pin_ev_pending[kPinRing] = {};
   int pin_next = 0;
@@ -386,6 +389,7 @@ cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t
                                   unsigned long long* counts, cudaStream_t s);   // zeroes counts
 int correct_window_scratch_stride();
 int correct_all_scratch_stride();
+cudaError_t launch_mp_positions(lc_ctx* c, int op, int lo, int hi, float* xyz, cudaStream_t s);
 cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
                                unsigned long long* counts, cudaStream_t s);   // zeroes counts
 size_t correct_dry_scratch_bytes(int n_batch, int n_slots, int n_mp);

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from ._lib import LC_FUSE_APPLY, LC_FUSE_PLAN
+from ._lib import LC_FUSE_APPLY, LC_FUSE_PLAN, LC_POS_GET, LC_POS_SET
 
 
 def shard_bounds(n_window: int, world: int, win_list_begin=None, n_list: int = 0):
@@ -111,6 +111,68 @@ def fuse_sharded(fuser, window, mp_list, params, *, window_S=None, win_list_begi
     info = dict(winner=full_win, victim=vic, n_adds=int(sum(ns)),
                 exchange_bytes=dict(victim_allreduce=int(n_mp * 8), adds_allgather=int(world * 2 * m * 8)))
     return plan["counts"], app["counts"], info
+
+
+def point_bounds(n_mp: int, world: int):
+    """Contiguous map-point slices [lo_r, hi_r) of the sharded point passes (equal sizes)."""
+    return [(n_mp * r // world, n_mp * (r + 1) // world) for r in range(world)]
+
+
+def exchange_positions(corrector, group=None, device=None, events=None):
+    """all_gather of the ranks' corrected position slices (SURVEY.md §8(e) "all_gather of
+    corrected position slices"): every rank reads its slice out of its store
+    (lc_mp_positions GET), the slices (padded to the largest) are all-gathered, and every
+    other rank's slice is written into the local store (SET). Returns the bytes gathered."""
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    b = point_bounds(corrector.n_mp, world)
+    L = max(max(h - l for l, h in b), 1)
+    host = device is None or torch.device(device).type == "cpu"
+    dev = torch.device("cpu") if host else torch.device(device)
+    lo, hi = b[rank]
+    send = torch.zeros((L, 3), dtype=torch.float32, device=dev)
+    if hi > lo:
+        corrector.mp_positions(LC_POS_GET, lo, hi, send[:hi - lo], host=host)
+    recv = [torch.empty((L, 3), dtype=torch.float32, device=dev) for _ in range(world)]
+    if events is not None:
+        events[0].record()
+    dist.all_gather(recv, send, group=group)
+    if events is not None:
+        events[1].record()
+    for r, (l, h) in enumerate(b):
+        if r != rank and h > l:
+            corrector.mp_positions(LC_POS_SET, l, h, recv[r][:h - l], host=host)
+    return int(world * L * 12)
+
+
+def correct_window_sharded(corrector, cur_kf, S_cw_corr, window, *, group=None, device=None, events=None):
+    """WINDOW correction with the point pass sharded by map-point range (SURVEY.md §8(e):
+    the pose correction and owner election replicated, "point correction is sharded by MP
+    index range, followed by all_gather of the slices"). Returns (counts, bytes gathered);
+    the CORR_MP counter is this rank's slice."""
+    rank = dist.get_rank(group)
+    lo, hi = point_bounds(corrector.n_mp, dist.get_world_size(group))[rank]
+    host = device is None or torch.device(device).type == "cpu"
+    corrector.set_point_range(lo, hi)
+    try:
+        _, c = corrector.correct_window(cur_kf, S_cw_corr, window, host=host)
+    finally:
+        corrector.set_point_range()
+    return c, exchange_positions(corrector, group=group, device=device, events=events)
+
+
+def correct_all_sharded(corrector, S_opt, *, group=None, device=None, events=None):
+    """ALL correction (optimised Sim3 propagation) sharded by map-point range + all_gather of
+    the corrected position slices; keyframe poses replicated."""
+    rank = dist.get_rank(group)
+    lo, hi = point_bounds(corrector.n_mp, dist.get_world_size(group))[rank]
+    host = device is None or torch.device(device).type == "cpu"
+    corrector.set_point_range(lo, hi)
+    try:
+        c = corrector.correct_all(S_opt, host=host)
+    finally:
+        corrector.set_point_range()
+    return c, exchange_positions(corrector, group=group, device=device, events=events)
 
 
 def search_sharded(searcher, pair_kf, pair_S, pair_param, params, pair_list_begin, mp_list, *,

@@ -550,6 +550,25 @@ class Context:
                                    self._stream())
         self._check("lc_fuse_adds", st)
 
+    # -- lc_set_point_range / lc_mp_positions (sharded correction) -------------------
+    def set_point_range(self, lo=0, hi=-1):
+        """Later WINDOW / ALL corrections rewrite the positions of map points [lo, hi) only
+        (hi < 0: all); poses, owners and corr_ref stay replicated."""
+        self._check("lc_set_point_range", self.lib.lc_set_point_range(self.h, int(lo), int(hi)))
+
+    def mp_positions(self, op, lo, hi, xyz=None, host=True):
+        """LC_POS_GET: fp32 positions of map points [lo, hi) into xyz (new if None);
+        LC_POS_SET: xyz [hi - lo][3] into the store. Returns xyz."""
+        k = self._keep(host)
+        n = max(int(hi) - int(lo), 0)
+        if xyz is None:
+            xyz = np.zeros((n, 3), np.float32) if host else self._dev(3 * n, torch.float32).view(n, 3)
+        st = self.lib.lc_mp_positions(self.h, int(op), int(lo), int(hi), k.ptr(xyz) if n else None, self._stream())
+        self._check("lc_mp_positions", st)
+        if host and op == _lib.LC_POS_GET:
+            self.synchronize()
+        return xyz
+
     # -- lc_search_by_projection ----------------------------------------------------
     def search_by_projection(self, pair_kf, pair_S, pair_param, params, pair_list_begin, mp_list,
                              pair_taken=None, debug=False, host=True):

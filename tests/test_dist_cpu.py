@@ -166,3 +166,94 @@ def test_shard_bounds_balanced_and_covering():
             loads = [wb[h] - wb[l] for l, h in b]
             assert max(loads) <= wb[-1] / W + wb[1:].__sub__(wb[:-1]).max() + 1
     assert shard_bounds(10, 4, None, 7) == [(0, 3), (3, 5), (5, 8), (8, 10)]
+
+
+class OracleCorrector:
+    """lc_set_point_range / lc_correct_sim3 / lc_mp_positions adapter over the CPU oracle
+    (test infrastructure): a correction with a point range runs the oracle's whole
+    correction and keeps the positions outside the range as they were -- the library's
+    contract (poses, owners and corr_ref replicated; positions of the slice only)."""
+
+    def __init__(self, om):
+        self.om = om
+        self.n_mp = om.n_mp
+        self.lo, self.hi = 0, om.n_mp
+
+    def set_point_range(self, lo=0, hi=-1):
+        self.lo, self.hi = (0, self.om.n_mp) if hi < 0 else (int(lo), int(hi))
+
+    def _slice_only(self, fn):
+        before = self.om.mp_pos.copy()
+        r = fn()
+        keep = np.ones(self.om.n_mp, bool)
+        keep[self.lo:self.hi] = False
+        self.om.mp_pos[keep] = before[keep]
+        return r
+
+    def correct_window(self, cur_kf, S_cw_corr, window, host=True):
+        return self._slice_only(lambda: self.om.correct_window(cur_kf, S_cw_corr, window))
+
+    def correct_all(self, S_opt, host=True):
+        return self._slice_only(lambda: self.om.correct_all(S_opt))
+
+    def mp_positions(self, op, lo, hi, xyz, host=True):
+        from paper_2603_17201_b200._lib import LC_POS_GET
+        if op == LC_POS_GET:
+            xyz[:] = torch.from_numpy(self.om.mp_pos[lo:hi].copy())
+        else:
+            self.om.mp_pos[lo:hi] = xyz.numpy()
+        return xyz
+
+
+def _loop_worker(rank, world, port, name, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from lcsynth import make_world
+    from lcsynth.world import FUSE_PARAMS
+    from paper_2603_17201_b200 import dist as lcdist
+    w = make_world(name, 0)
+    om = oracle.OracleMap(w)
+    cor = OracleCorrector(om)
+    _, nb_w = lcdist.correct_window_sharded(cor, w.cur_kf, w.S_cw_corr, w.window)
+    lcdist.fuse_sharded(OracleFuser(om), w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S,
+                        win_list_begin=w.win_list_begin)
+    _, nb_a = lcdist.correct_all_sharded(cor, w.S_opt)
+    np.savez(os.path.join(out_dir, f"l{rank}.npz"), pos=om.mp_pos, pose=om.kf_pose, feat_mp=om.feat_mp,
+             nb=nb_w + nb_a)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world", [("C1", 2), ("T5", 3)])
+def test_loop_event_sharded_corrections_gloo_equal_single(tmp_path, name, world):
+    """The whole loop event with the point passes of WINDOW and ALL sharded by map-point
+    slice and the slices all-gathered (SURVEY.md §8(e) "Correction"), the fusion by keyframe
+    shard: every rank's store == the single-process oracle's (positions, poses, associations)."""
+    import oracle
+    from lcsynth import make_world
+    from lcsynth.world import FUSE_PARAMS
+    from paper_2603_17201_b200.dist import point_bounds
+    mp.spawn(_loop_worker, args=(world, _free_port(), name, str(tmp_path)), nprocs=world, join=True)
+    w = make_world(name, 0)
+    om = oracle.OracleMap(w)
+    om.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    om.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+    om.correct_all(w.S_opt)
+    b = point_bounds(om.n_mp, world)
+    L = max(h - l for l, h in b)
+    for r in range(world):
+        z = np.load(tmp_path / f"l{r}.npz")
+        assert np.array_equal(z["pos"], om.mp_pos), f"rank {r}: positions"
+        assert np.array_equal(z["pose"], om.kf_pose), f"rank {r}: poses"
+        assert np.array_equal(z["feat_mp"], om.feat_mp), f"rank {r}: associations"
+        assert int(z["nb"]) == 2 * world * L * 12
+
+
+def test_point_bounds_cover():
+    from paper_2603_17201_b200.dist import point_bounds
+    for n in (0, 1, 7, 1000, 977802):
+        for W in (1, 2, 3, 8):
+            b = point_bounds(n, W)
+            assert b[0][0] == 0 and b[-1][1] == n and all(b[i][1] == b[i + 1][0] for i in range(W - 1))
+            assert max(h - l for l, h in b) - min(h - l for l, h in b) <= 1

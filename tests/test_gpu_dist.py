@@ -28,7 +28,7 @@ def _free_port():
 def _worker(rank, world, port, name, on_device, out_path):
     import torch.distributed as dist
     from paper_2603_17201_b200 import Context
-    from paper_2603_17201_b200.dist import fuse_sharded
+    from paper_2603_17201_b200.dist import correct_all_sharded, correct_window_sharded, fuse_sharded
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -36,16 +36,20 @@ def _worker(rank, world, port, name, on_device, out_path):
     w = make_world(name, 0)
     ctx = Context(0)
     ctx.upload_map(w.map_arrays(), [w.cam])
-    ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
     dev = torch.device("cuda:0") if on_device else None
+    # the whole loop event sharded: WINDOW and ALL point passes by map-point
+    # slice + position all_gather, the fuse by keyframe shard + victim MIN + ADD gather
+    cw, _ = correct_window_sharded(ctx, w.cur_kf, w.S_cw_corr, w.window, device=dev)
     lst = torch.from_numpy(w.mp_list).cuda() if on_device else w.mp_list
     pc, ac, info = fuse_sharded(ctx, w.window, lst, FUSE_PARAMS, window_S=w.win_S,
                                 win_list_begin=w.win_list_begin, device=dev, gather_winner=True)
+    S_opt = torch.from_numpy(w.S_opt).cuda() if on_device else w.S_opt
+    ca, _ = correct_all_sharded(ctx, S_opt, device=dev)
     torch.cuda.synchronize()
     st = ctx.download_map()
     np.savez(f"{out_path}.{rank}.npz", winner=info["winner"].cpu().numpy(), victim=info["victim"].cpu().numpy(),
              feat_mp=st["feat_mp"], mp_flags=st["mp_flags"], mp_replaced_by=st["mp_replaced_by"],
-             mp_nobs=st["mp_nobs"])
+             mp_nobs=st["mp_nobs"], mp_pos=st["mp_pos"], kf_pose=st["kf_pose"])
     ctx.close()
     dist.destroy_process_group()
 
@@ -66,12 +70,13 @@ def test_sharded_fuse_two_ranks_equals_single_gpu(tmp_path, name, on_device):
     ctx.upload_map(w.map_arrays(), [w.cam])
     ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
     g = ctx.fuse(w.window, w.mp_list, FUSE_PARAMS, window_S=w.win_S, win_list_begin=w.win_list_begin)
+    ctx.correct_all(w.S_opt)
     st = ctx.download_map()
     for r in range(2):
         d = np.load(f"{out}.{r}.npz")
         assert np.array_equal(d["winner"], g["winner"]), f"rank {r}: gathered winner table"
         assert np.array_equal(d["victim"], g["victim"]), f"rank {r}: merged victim table"
-        for key in ("feat_mp", "mp_flags", "mp_replaced_by", "mp_nobs"):
+        for key in ("feat_mp", "mp_flags", "mp_replaced_by", "mp_nobs", "mp_pos", "kf_pose"):
             assert np.array_equal(d[key], st[key]), f"rank {r}: {key}"
 
 
@@ -96,5 +101,6 @@ def test_bench_two_ranks_gloo_one_device(config):
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["value"] > 0
     assert line["multi_gpu"]["victim_allreduce_bytes"] > 0
-    assert line["multi_gpu"]["merge_check"] == "equal to the unsharded FUSE_ALL"
+    assert line["multi_gpu"]["merge_check"] == "equal to the unsharded loop event"
+    assert line["multi_gpu"]["positions_allgather_bytes"] > 0
     assert line["config"]["parallelism"] == "keyframe-sharded x2"

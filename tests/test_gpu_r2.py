@@ -389,3 +389,67 @@ def test_loop_lists_large_and_errors(Ctx):
         ctx.loop_lists(sb, sk, out=np.zeros(10, np.int32))
     assert e.value.status == _lib.LC_ECAPACITY
     ctx.close()
+
+
+@pytest.mark.parametrize("name,W", [("C2", 2), ("S3", 3)])
+def test_point_range_slices_equal_full_correction(Ctx, name, W):
+    """lc_set_point_range + lc_mp_positions (SURVEY.md §8(e) "Correction"): W contexts, each
+    correcting only its map-point slice (WINDOW, then ALL), with the slices exchanged through
+    lc_mp_positions GET / SET in between and at the end, equal one context correcting every
+    point -- positions, poses, and the CORR_MP counts summed over the slices. The ALL pass
+    reads corr_ref, which every slice keeps for every point."""
+    from paper_2603_17201_b200._lib import LC_POS_GET, LC_POS_SET
+    from paper_2603_17201_b200.dist import point_bounds
+    w = world(name)
+    ref = Ctx(0)
+    ref.upload_map(w.map_arrays(), [w.cam])
+    _, c_w = ref.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    c_a = ref.correct_all(w.S_opt)
+    full = ref.download_map()
+    ref.close()
+    b = point_bounds(w.n_mp, W)
+    ctxs = []
+    for r in range(W):
+        c = Ctx(0)
+        c.upload_map(w.map_arrays(), [w.cam])
+        ctxs.append(c)
+
+    def exchange():
+        sl = [c.mp_positions(LC_POS_GET, *b[r]) for r, c in enumerate(ctxs)]
+        for r, c in enumerate(ctxs):
+            for r2, (l, h) in enumerate(b):
+                if r2 != r:
+                    c.mp_positions(LC_POS_SET, l, h, sl[r2])
+
+    n_w = n_a = 0
+    for r, c in enumerate(ctxs):
+        c.set_point_range(*b[r])
+        n_w += c.correct_window(w.cur_kf, w.S_cw_corr, w.window)[1]["corr_mp"]
+    exchange()
+    for r, c in enumerate(ctxs):
+        n_a += c.correct_all(w.S_opt)["corr_mp"]
+        c.set_point_range()
+    exchange()
+    assert n_w == c_w["corr_mp"] and n_a == c_a["corr_mp"]
+    for c in ctxs:
+        st = c.download_map()
+        assert np.array_equal(st["mp_pos"], full["mp_pos"]) and np.array_equal(st["kf_pose"], full["kf_pose"])
+        c.close()
+
+
+def test_point_range_errors(Ctx):
+    from paper_2603_17201_b200._lib import LC_POS_GET, LcError
+    w = world("C1")
+    c = Ctx(0)
+    with pytest.raises(LcError):
+        c.set_point_range(0, 1)   # no map
+    c.upload_map(w.map_arrays(), [w.cam])
+    for lo, hi in ((-1, 5), (5, 4), (0, w.n_mp + 1)):
+        with pytest.raises(LcError):
+            c.set_point_range(lo, hi)
+        with pytest.raises(LcError):
+            c.mp_positions(LC_POS_GET, lo, hi)
+    with pytest.raises(LcError):
+        c.mp_positions(7, 0, 1)
+    assert c.mp_positions(LC_POS_GET, 3, 3).shape == (0, 3)
+    c.close()
