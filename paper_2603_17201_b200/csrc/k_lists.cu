@@ -166,7 +166,10 @@ __global__ void __launch_bounds__(LIST_NT) k_kf_idrange(int n_src, const int32_t
 
 // lists sel[i] (or i) -> bitmap region i * maxw of bm; lo_out[l] / lo_out[n_lists + l] =
 // the list's first id / its bitmap words, counts[l] = distinct ids (-1: range too wide)
+// only_wide: lists whose count is still -1 (too wide for the first pass) only, counted in
+// shared memory without a global bitmap (lo_out words stored negated: "rebuild at emit")
 __global__ void __launch_bounds__(LIST_NT) k_lists_bitmap(int n, int n_lists, const int32_t* __restrict__ sel, int maxw,
+                                                          int only_wide,
                                                           const int2* __restrict__ src_rng,
                                                           const int32_t* __restrict__ sbeg,
                                                           const int32_t* __restrict__ skf,
@@ -178,6 +181,7 @@ __global__ void __launch_bounds__(LIST_NT) k_lists_bitmap(int n, int n_lists, co
   __shared__ int s_lo, s_hi, s_cnt;
   for (int li = blockIdx.x; li < n; li += gridDim.x) {
     const int l = sel ? sel[li] : li;
+    if (only_wide && counts[l] >= 0) continue;   // (uniform over the CTA; written below after syncs)
     if (threadIdx.x == 0) {   // the list's id range from its sources' ranges
       int lo0 = 0x7FFFFFFF, hi0 = -1;
       for (int j = sbeg[l]; j < sbeg[l + 1]; ++j) {
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(LIST_NT) k_lists_bitmap(int n, int n_lists, co
     const int lo = s_lo, hi = s_hi;
     const int words = hi >= lo ? ((hi - lo) >> 5) + 1 : 0;
     if (words > maxw) {   // id range too wide for this bitmap: a larger one (or the general path)
-      if (threadIdx.x == 0) counts[l] = -1;
+      if (threadIdx.x == 0) { counts[l] = -1; lo_out[n_lists + l] = -1; }
       __syncthreads();
       continue;
     }
@@ -201,18 +205,22 @@ __global__ void __launch_bounds__(LIST_NT) k_lists_bitmap(int n, int n_lists, co
       atomicOr(&s_bm[b >> 5], 1u << (b & 31));
     });
     __syncthreads();
-    uint32_t* g = bm + (size_t)li * maxw;
+    uint32_t* g = only_wide ? nullptr : bm + (size_t)li * maxw;
     int c = 0;
     for (int i = threadIdx.x; i < words; i += LIST_NT) {
       const uint32_t x = s_bm[i];
-      g[i] = x;
+      if (g) g[i] = x;
       c += __popc(x);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_cnt, c);
     __syncthreads();
-    if (threadIdx.x == 0) { counts[l] = s_cnt; lo_out[l] = words ? lo : 0; lo_out[n_lists + l] = words; }
+    if (threadIdx.x == 0) {
+      counts[l] = s_cnt;
+      lo_out[l] = words ? lo : 0;
+      lo_out[n_lists + l] = only_wide ? -words : words;
+    }
     __syncthreads();
   }
 }
@@ -228,7 +236,7 @@ __global__ void __launch_bounds__(LIST_NT) k_lists_emit(int n, const uint32_t* _
   __shared__ int s_w[LIST_NT / 32 + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int l = blockIdx.x; l < n; l += gridDim.x) {
-    if (counts[l] < 0) continue;   // (uniform over the CTA)
+    if (counts[l] < 0 || lo_in[n + l] < 0) continue;   // (uniform; hashed / rebuilt at emit)
     const int words = lo_in[n + l], lo = lo_in[l];
     const int cnt = counts[l];
     const uint32_t* g = bm + bm_off[l];
@@ -267,6 +275,92 @@ __global__ void __launch_bounds__(LIST_NT) k_lists_emit(int n, const uint32_t* _
     }
     if (cnt <= EMIT_STAGE) {
       for (int j = threadIdx.x; j < cnt; j += LIST_NT) dst[j] = s_ids[j];
+      __syncthreads();
+    }
+  }
+}
+
+// device-resident offsets (lc_loop_lists with a device out_begin): out_begin[0] = 0,
+// out_begin[l + 1] = out_begin[l] + counts[l], one CTA
+__global__ void __launch_bounds__(1024) k_lists_scan(int n, const int32_t* __restrict__ counts,
+                                                     int32_t* __restrict__ out_begin) {
+  __shared__ int s_w[33];
+  __shared__ int s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { s_carry = 0; out_begin[0] = 0; }
+  __syncthreads();
+  for (int b = 0; b < n; b += 1024) {
+    const int i = b + threadIdx.x;
+    const int c = i < n ? counts[i] : 0;
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int t = 0; t < 32; ++t) { const int v = s_w[t]; s_w[t] = acc; acc += v; }
+      s_w[32] = acc;
+    }
+    __syncthreads();
+    if (i < n) out_begin[i + 1] = s_carry + s_w[warp] + incl;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += s_w[32];
+    __syncthreads();
+  }
+}
+
+// the lists counted by the only_wide pass (words stored negated): bitmap rebuilt in shared
+// memory from their sources' associations and the ids written in order at out_begin[l]
+__global__ void __launch_bounds__(LIST_NT) k_lists_emit_wide(int n, const int32_t* __restrict__ sbeg,
+                                                             const int32_t* __restrict__ skf,
+                                                             const int32_t* __restrict__ kf_fbeg,
+                                                             const int32_t* __restrict__ feat_mp,
+                                                             const int32_t* __restrict__ lo_in,
+                                                             const int32_t* __restrict__ out_begin,
+                                                             int32_t* __restrict__ out) {
+  extern __shared__ uint32_t s_bm[];
+  __shared__ int s_w[LIST_NT / 32 + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int l = blockIdx.x; l < n; l += gridDim.x) {
+    if (lo_in[n + l] >= 0) continue;   // (uniform) not rebuilt here
+    const int words = -lo_in[n + l], lo = lo_in[l];
+    for (int i = threadIdx.x; i < words; i += LIST_NT) s_bm[i] = 0u;
+    __syncthreads();
+    for_assoc(l, sbeg, skf, kf_fbeg, feat_mp, [&](int32_t m) {
+      const int b = m - lo;
+      atomicOr(&s_bm[b >> 5], 1u << (b & 31));
+    });
+    __syncthreads();
+    int32_t* dst = out + out_begin[l];
+    int base = 0;
+    for (int w0 = 0; w0 < words; w0 += LIST_NT) {
+      const int i = w0 + threadIdx.x;
+      uint32_t x = i < words ? s_bm[i] : 0u;
+      const int c = __popc(x);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_w[warp] = incl;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int t = 0; t < LIST_NT / 32; ++t) { const int v = s_w[t]; s_w[t] = acc; acc += v; }
+        s_w[LIST_NT / 32] = acc;
+      }
+      __syncthreads();
+      int r = base + s_w[warp] + incl - c;
+      while (x) {
+        dst[r++] = lo + 32 * i + (__ffs(x) - 1);
+        x &= x - 1;
+      }
+      base += s_w[LIST_NT / 32];
       __syncthreads();
     }
   }
@@ -320,12 +414,13 @@ cudaError_t launch_kf_idrange(lc_ctx* c, int n_src, const int32_t* d_skf, int2* 
 
 cudaError_t launch_lists_bitmap(lc_ctx* c, int n, int n_lists, const int32_t* d_sel, int maxw, const int2* d_rng,
                                 uint32_t* d_bm, int32_t* d_lo, int32_t* d_counts, const int32_t* d_sbeg,
-                                const int32_t* d_skf, cudaStream_t s) {
+                                const int32_t* d_skf, cudaStream_t s, bool only_wide) {
   if (n <= 0) return cudaSuccess;
   cudaError_t e = set_smem_attr((const void*)k_lists_bitmap, maxw * 4);
   if (e != cudaSuccess) return e;
   const int per_sm = std::max(1, 200 * 1024 / (maxw * 4 + 1024));
-  k_lists_bitmap<<<std::min(n, 148 * per_sm), LIST_NT, maxw * 4, s>>>(n, n_lists, d_sel, maxw, d_rng, d_sbeg, d_skf,
+  k_lists_bitmap<<<std::min(n, 148 * per_sm), LIST_NT, maxw * 4, s>>>(n, n_lists, d_sel, maxw, only_wide ? 1 : 0,
+                                                                     d_rng, d_sbeg, d_skf,
                                                                      c->st.kf_fbeg, c->st.feat_mp, d_bm,
                                                                      d_lo, d_counts);
   c->launches++;
@@ -336,6 +431,23 @@ cudaError_t launch_lists_emit(lc_ctx* c, int n, const uint32_t* d_bm, const int6
                               const int32_t* d_counts, const int32_t* d_out_begin, int32_t* d_out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   k_lists_emit<<<std::min(n, 148 * 6), LIST_NT, 0, s>>>(n, d_bm, d_bm_off, d_lo, d_counts, d_out_begin, d_out);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lists_scan(lc_ctx* c, int n, const int32_t* d_counts, int32_t* d_out_begin, cudaStream_t s) {
+  k_lists_scan<<<1, 1024, 0, s>>>(n, d_counts, d_out_begin);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lists_emit_wide(lc_ctx* c, int n, int maxw, const int32_t* d_sbeg, const int32_t* d_skf,
+                                   const int32_t* d_lo, const int32_t* d_out_begin, int32_t* d_out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  cudaError_t e = set_smem_attr((const void*)k_lists_emit_wide, maxw * 4);
+  if (e != cudaSuccess) return e;
+  k_lists_emit_wide<<<std::min(n, 148), LIST_NT, maxw * 4, s>>>(n, d_sbeg, d_skf, c->st.kf_fbeg, c->st.feat_mp, d_lo,
+                                                               d_out_begin, d_out);
   c->launches++;
   return cudaGetLastError();
 }

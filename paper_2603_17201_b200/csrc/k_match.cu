@@ -1606,6 +1606,19 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix_r(
   block_add<A_N>(cnt, kApplySlot, counts);
 }
 
+// lc_fuse with device-resident list offsets: unit i = block i = list i, its queries
+// [begin[i], begin[i+1]); t = [lbeg | qoff | blk_q0 | blk_q1 | surv_off] (n each)
+__global__ void k_csr_units(int n, const int32_t* __restrict__ begin, int64_t* __restrict__ t) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t b = begin[i], e = begin[i + 1];
+  t[i] = b;
+  t[n + i] = b;
+  t[2 * (size_t)n + i] = b;
+  t[3 * (size_t)n + i] = e;
+  t[4 * (size_t)n + i] = b;
+}
+
 int grid_for(int64_t n) {
   int64_t b = (n + LC_NTHREADS - 1) / LC_NTHREADS;
   if (b < 1) b = 1;
@@ -1667,6 +1680,13 @@ cudaError_t launch_resolve(lc_ctx* c, int mode, const MatchArgs& a, int n_units,
   if (n_units <= 0) return cudaSuccess;
   if (mode == 0) k_resolve<0><<<n_units, LC_NTHREADS, 0, s>>>(a);
   else k_resolve<1><<<n_units, LC_NTHREADS, 0, s>>>(a);
+  c->launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_csr_units(lc_ctx* c, int n, const int32_t* d_begin, int64_t* d_t, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_csr_units<<<(n + LC_NTHREADS - 1) / LC_NTHREADS, LC_NTHREADS, 0, s>>>(n, d_begin, d_t);
   c->launches++;
   return cudaGetLastError();
 }

@@ -1356,11 +1356,20 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     if (phase != LC_FUSE_PLAN) { w_lo = 0; w_hi = n_window; }
     if (phase == LC_FUSE_APPLY) { w_lo = w_hi = 0; }
     REQUIRE(0 <= w_lo && w_lo <= w_hi && w_hi <= n_window, LC_EINVAL, "bad shard range");
-    if (win_list_begin) {
+    // device-resident list offsets (e.g. lc_loop_lists with a device out_begin): nothing is
+    // read back; n_list is then the list buffer's capacity (>= the offsets' total)
+    const bool dev_csr = win_list_begin && is_device_ptr(c, win_list_begin);
+    if (win_list_begin && !dev_csr) {
       REQUIRE(win_list_begin[0] == 0 && win_list_begin[n_window] == n_list, LC_EINVAL,
               "win_list_begin must span [0, n_list]");
       for (int i = 0; i < n_window; ++i)
         REQUIRE(win_list_begin[i + 1] >= win_list_begin[i], LC_EINVAL, "win_list_begin not monotone");
+    }
+    if (dev_csr && (phase & LC_FUSE_PLAN)) {
+      REQUIRE(w_lo == 0 && w_hi == n_window, LC_EINVAL, "device win_list_begin: full-window PLAN only");
+      REQUIRE(!dbg, LC_EINVAL, "device win_list_begin: no per-query debug outputs");
+      REQUIRE(!forced_mp, LC_EINVAL, "device win_list_begin: no forced matches");
+      REQUIRE(n_list == 0 || is_device_ptr(c, mp_list), LC_EINVAL, "device win_list_begin needs a device mp_list");
     }
     int cur_pos = -1;   // forced loop matches (O9.4): cur_kf must be a window keyframe
     if (forced_mp && (phase & LC_FUSE_PLAN)) {
@@ -1378,28 +1387,29 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     for (int i = 0; i < n_window; ++i) {
       int k = window_kf[i];
       woff[i + 1] = woff[i] + (st.h_fbeg[k + 1] - st.h_fbeg[k]);
-      lbeg[i] = win_list_begin ? win_list_begin[i] : 0;
-      qoff[i] = win_list_begin ? win_list_begin[i] : (int64_t)i * n_list;
+      lbeg[i] = dev_csr ? 0 : win_list_begin ? win_list_begin[i] : 0;
+      qoff[i] = dev_csr ? 0 : win_list_begin ? win_list_begin[i] : (int64_t)i * n_list;
     }
     const int64_t n_wfeat = woff[n_window];
     int64_t total_q = 0;
     int F_max = 0;
     for (int i = w_lo; i < w_hi; ++i) {
-      int64_t len = win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list;
+      int64_t len = dev_csr ? 0 : win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list;
       total_q += len;
       F_max = std::max<int>(F_max, (int)(woff[i + 1] - woff[i]));
     }
+    if (dev_csr) total_q = n_list;
     // sole mode: one CTA per window keyframe, which initialises and resolves its own
     // winner words (no winner-table init pass, no separate resolve launch). Used when
     // the shard already has enough keyframes to fill the GPU and no list is huge.
     int64_t max_len = 0;
-    for (int i = w_lo; i < w_hi; ++i)
+    for (int i = w_lo; i < w_hi && !dev_csr; ++i)
       max_len = std::max<int64_t>(max_len, win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list);
     // pipelined host list: a full-range PLAN whose per-keyframe lists are in host
     // memory uploads them in kPipe chunks on a side stream; k_project / k_match run
     // on each chunk's blocks as it lands (k_project stamps the LoopSet), the resolve
     // after all of them
-    const bool pipe = (phase & LC_FUSE_PLAN) && win_list_begin && n_list >= c->pipe_min && !dbg &&
+    const bool pipe = (phase & LC_FUSE_PLAN) && win_list_begin && !dev_csr && n_list >= c->pipe_min && !dbg &&
                       !c->cap && w_lo == 0 && w_hi == n_window && !is_device_ptr(c, mp_list) &&
                       cur_pos < 0;   // the forced step needs the LoopSet stamped up front
     // sole mode: one k_match CTA per window keyframe, which initialises and resolves its
@@ -1407,7 +1417,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     // the GPU; LC_SOLE=0 forbids it, 1 forces it, 2 forces the queued-item k_match_sole
     // kernel (measured slower at C5)
     const bool sole = !pipe && max_len <= 16384 && w_hi > w_lo &&
-                      (c->sole_mode < 0 ? (w_hi - w_lo) >= 2 * 148 : c->sole_mode >= 1);
+                      (dev_csr || (c->sole_mode < 0 ? (w_hi - w_lo) >= 2 * 148 : c->sole_mode >= 1));
     // a full-range PLAN without forced matches stamps the LoopSet in k_project (after its
     // PDL wait, from its own list entries) instead of a separate pass over the lists in
     // k_fuse_prep; a shard's PLAN needs the whole window's LoopSet, so prep stamps it there
@@ -1422,7 +1432,7 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     bq1.reserve(w_hi - w_lo + 64);
     for (int i = w_lo; i < w_hi; ++i) {
       int64_t b = lbeg[i];
-      int64_t e = b + (win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list);
+      int64_t e = dev_csr ? 0 : b + (win_list_begin ? (int64_t)win_list_begin[i + 1] - win_list_begin[i] : n_list);
       if (sole) {
         bunit.push_back(i);
         bq0.push_back(b);
@@ -1449,13 +1459,15 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     const lc_match_params* d_prm = nullptr;
     call.arg(window_kf, n_window, &d_win);
     call.arg(woff.data(), n_window + 1, &d_woff);
-    call.arg(lbeg.data(), n_window, &d_lbeg);
-    call.arg(qoff.data(), n_window, &d_qoff);
-    call.arg(bunit.data(), bunit.size(), &d_bunit);
-    call.arg(bq0.data(), bq0.size(), &d_bq0);
-    call.arg(bq1.data(), bq1.size(), &d_bq1);
     call.arg(params, 1, &d_prm);
-    call.arg(boff.data(), boff.size(), &d_boff);
+    call.arg(bunit.data(), bunit.size(), &d_bunit);
+    if (!dev_csr) {
+      call.arg(lbeg.data(), n_window, &d_lbeg);
+      call.arg(qoff.data(), n_window, &d_qoff);
+      call.arg(bq0.data(), bq0.size(), &d_bq0);
+      call.arg(bq1.data(), bq1.size(), &d_bq1);
+      call.arg(boff.data(), boff.size(), &d_boff);
+    }
     if (window_S) {   // device-resident transforms are used in place, host ones ride in the block
       if (is_device_ptr(c, window_S)) d_S = (const double*)window_S;
       else call.arg((const double*)window_S, 13 * (size_t)n_window, &d_S);
@@ -1463,7 +1475,13 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     hp.mark("tables");
     call.commit();
     hp.mark("commit");
-    Surv* d_surv = (Surv*)call.scratch(sizeof(Surv) * std::max<int64_t>(boff.back(), 1));
+    if (dev_csr) {   // the unit / block tables from the device offsets (one block per unit)
+      int64_t* t = (int64_t*)call.scratch(sizeof(int64_t) * (5 * (size_t)n_window + 1));
+      d_lbeg = t; d_qoff = t + n_window; d_bq0 = t + 2 * (size_t)n_window; d_bq1 = t + 3 * (size_t)n_window;
+      d_boff = t + 4 * (size_t)n_window;
+      CK(launch_csr_units(c, n_window, win_list_begin, t, call.s));
+    }
+    Surv* d_surv = (Surv*)call.scratch(sizeof(Surv) * std::max<int64_t>(dev_csr ? n_list : boff.back(), 1));
     int32_t* d_scnt = (int32_t*)call.scratch(sizeof(int32_t) * std::max<size_t>(bunit.size(), 1));
     const int32_t* d_list = nullptr;
     int pipe_b[lc_ctx::kPipe + 1] = {};   // block boundaries of the chunks
@@ -1611,6 +1629,7 @@ lc_status lc_loop_lists(lc_ctx* c, int32_t n, const int32_t* src_begin, const in
     Store& st = c->st;
     std::vector<int64_t> reg_off((size_t)n + 1, 0);
     const int umax = lists_max_unique();
+    int64_t ub_sum = 0, ub_max = 0;   // upper bounds of the lists' lengths (their sources' features)
     for (int l = 0; l < n; ++l) {
       REQUIRE(src_begin[l + 1] >= src_begin[l], LC_EINVAL, "src_begin not monotone");
       int64_t ub = 0;
@@ -1620,8 +1639,25 @@ lc_status lc_loop_lists(lc_ctx* c, int32_t n, const int32_t* src_begin, const in
         ub += st.h_fbeg[k + 1] - st.h_fbeg[k];
       }
       reg_off[l + 1] = reg_off[l] + std::min<int64_t>(ub, umax);
+      ub_sum += ub;
+      ub_max = std::max(ub_max, ub);
     }
-    out_begin[0] = 0;
+    const bool dev_mode = is_device_ptr(c, out_begin);
+    if (dev_mode) {
+      REQUIRE(capacity == 0 || is_device_ptr(c, out_list), LC_EINVAL, "a device out_begin needs a device out_list");
+      REQUIRE((int64_t)st.n_mp <= 32 * (int64_t)lists_bitmap_words_max(), LC_ECAPACITY,
+              "device out_begin: maps of more than " + std::to_string(32 * lists_bitmap_words_max()) +
+              " map points need the host-offset path");
+      REQUIRE(ub_sum <= capacity, LC_ECAPACITY,
+              "device out_begin: capacity must hold the lists' upper bound " + std::to_string(ub_sum));
+      REQUIRE(ub_max <= 261888, LC_ECAPACITY, "device out_begin: a list may exceed 261888 entries");
+      if (n == 0) {
+        CK(cudaMemsetAsync(out_begin, 0, sizeof(int32_t), (cudaStream_t)stream));
+        return;
+      }
+    } else {
+      out_begin[0] = 0;
+    }
     if (n == 0) return;
     Call call(c, stream);
     const int32_t *d_sb = nullptr, *d_sk = nullptr;
@@ -1629,7 +1665,31 @@ lc_status lc_loop_lists(lc_ctx* c, int32_t n, const int32_t* src_begin, const in
     call.arg(src_begin, (size_t)n + 1, &d_sb);
     call.arg(src_kf, (size_t)std::max(src_begin[n], 1), &d_sk);
     call.arg(reg_off.data(), reg_off.size(), &d_ro);
+    std::vector<int64_t> bmo0;
+    const int64_t* d_bmo0 = nullptr;
+    if (dev_mode) {   // bitmap offsets of the first pass (l * w1), in the argument block
+      bmo0.resize(n);
+      for (int l = 0; l < n; ++l) bmo0[l] = (int64_t)l * lists_bitmap_words();
+      call.arg(bmo0.data(), bmo0.size(), &d_bmo0);
+    }
     call.commit();
+    if (dev_mode) {
+      // device-resident offsets, no host synchronisation (lc.h): first pass (small bitmaps,
+      // global), the wide lists counted in a second pass (large shared-memory bitmap), a scan
+      // of the counts into out_begin, then both emissions (the wide lists' bitmaps rebuilt)
+      const int w1 = lists_bitmap_words(), w2 = lists_bitmap_words_max();
+      uint32_t* d_bm = (uint32_t*)call.scratch(sizeof(uint32_t) * (size_t)n * w1);
+      int32_t* d_lo = (int32_t*)call.scratch(sizeof(int32_t) * 2 * (size_t)n);
+      int32_t* d_cnt = (int32_t*)call.scratch(sizeof(int32_t) * (size_t)n);
+      int2* d_rng = (int2*)call.scratch(sizeof(int2) * (size_t)std::max(src_begin[n], 1));
+      CK(launch_kf_idrange(c, src_begin[n], d_sk, d_rng, call.s));
+      CK(launch_lists_bitmap(c, n, n, nullptr, w1, d_rng, d_bm, d_lo, d_cnt, d_sb, d_sk, call.s));
+      CK(launch_lists_bitmap(c, n, n, nullptr, w2, d_rng, nullptr, d_lo, d_cnt, d_sb, d_sk, call.s, true));
+      CK(launch_lists_scan(c, n, d_cnt, out_begin, call.s));
+      CK(launch_lists_emit(c, n, d_bm, d_bmo0, d_lo, d_cnt, out_begin, out_list, call.s));
+      CK(launch_lists_emit_wide(c, n, w2, d_sb, d_sk, d_lo, out_begin, out_list, call.s));
+      return;
+    }
     // bitmap path (ascending unique by construction): a small bitmap per list first; the
     // lists whose id range is wider (-1 counts) again with the large one; beyond that the
     // general hash + sort path

@@ -389,6 +389,7 @@ cudaError_t launch_correct_window(lc_ctx* c, int cur_pos, int n_w, const int32_t
                                   unsigned long long* counts, cudaStream_t s);   // zeroes counts
 int correct_window_scratch_stride();
 int correct_all_scratch_stride();
+cudaError_t launch_csr_units(lc_ctx* c, int n, const int32_t* d_begin, int64_t* d_t, cudaStream_t s);
 cudaError_t launch_mp_positions(lc_ctx* c, int op, int lo, int hi, float* xyz, cudaStream_t s);
 cudaError_t launch_correct_all(lc_ctx* c, const double* d_Sopt, double* d_scr,
                                unsigned long long* counts, cudaStream_t s);   // zeroes counts
@@ -405,7 +406,10 @@ int lists_bitmap_words_max();   // ... second pass (the wide lists)
 cudaError_t launch_kf_idrange(lc_ctx* c, int n_src, const int32_t* d_skf, int2* d_rng, cudaStream_t s);
 cudaError_t launch_lists_bitmap(lc_ctx* c, int n, int n_lists, const int32_t* d_sel, int maxw, const int2* d_rng,
                                 uint32_t* d_bm, int32_t* d_lo, int32_t* d_counts, const int32_t* d_sbeg,
-                                const int32_t* d_skf, cudaStream_t s);
+                                const int32_t* d_skf, cudaStream_t s, bool only_wide = false);
+cudaError_t launch_lists_scan(lc_ctx* c, int n, const int32_t* d_counts, int32_t* d_out_begin, cudaStream_t s);
+cudaError_t launch_lists_emit_wide(lc_ctx* c, int n, int maxw, const int32_t* d_sbeg, const int32_t* d_skf,
+                                   const int32_t* d_lo, const int32_t* d_out_begin, int32_t* d_out, cudaStream_t s);
 cudaError_t launch_lists_emit(lc_ctx* c, int n, const uint32_t* d_bm, const int64_t* d_bm_off, const int32_t* d_lo,
                               const int32_t* d_counts, const int32_t* d_out_begin, int32_t* d_out, cudaStream_t s);
 int lists_max_unique();     // distinct map points a loop list may hold

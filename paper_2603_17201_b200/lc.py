@@ -471,12 +471,15 @@ class Context:
         window = np.ascontiguousarray(window, np.int32)
         n_w = len(window)
         w_hi = n_w if w_hi is None else int(w_hi)
-        wb = None if win_list_begin is None else np.ascontiguousarray(win_list_begin, np.int32)
+        if isinstance(win_list_begin, torch.Tensor) and win_list_begin.is_cuda:
+            wb = win_list_begin   # device offsets (lc_loop_lists(device=True)); mp_list = its buffer
+        else:
+            wb = None if win_list_begin is None else np.ascontiguousarray(win_list_begin, np.int32)
         wS = None if window_S is None else (window_S if isinstance(window_S, torch.Tensor)
                                             else np.ascontiguousarray(window_S, np.float64))
         n_list = int(mp_list.shape[0]) if hasattr(mp_list, "shape") else len(mp_list)
         nwf = self.n_feat_of(window)
-        nq = int(wb[-1]) if wb is not None else n_w * n_list
+        nq = (n_list if isinstance(wb, torch.Tensor) else int(wb[-1])) if wb is not None else n_w * n_list
         mk = (lambda n, dt, npdt: np.zeros(n, npdt)) if host else (lambda n, dt, npdt: self._dev(n, dt))
         if winner is None:
             winner = mk(nwf, torch.int64, np.int64)
@@ -506,14 +509,31 @@ class Context:
         return out
 
     # -- lc_loop_lists ---------------------------------------------------------------
-    def loop_lists(self, src_begin, src_kf, out=None, host=True):
+    def loop_list_bound(self, src_begin, src_kf):
+        """Upper bound of the lists' total length (their source keyframes' features)."""
+        fb = self.kf_feat_begin
+        sk = np.asarray(src_kf, np.int64)
+        return int(np.sum(fb[sk + 1] - fb[sk])) if len(sk) else 0
+
+    def loop_lists(self, src_begin, src_kf, out=None, host=True, device_offsets=False):
         """Loop map-point lists from the resident map: list l = ascending unique map points of
         keyframes src_kf[src_begin[l]:src_begin[l+1]]. Returns (begin [n+1] numpy, lists);
-        lists is written into `out` (a device or pinned tensor, >= total entries) if given."""
+        lists is written into `out` (a device or pinned tensor, >= total entries) if given.
+        device_offsets: begin is a device tensor and nothing is read back (no host
+        synchronisation); `out` (device) must hold loop_list_bound() entries and is returned
+        whole -- pass both to fuse() as mp_list / win_list_begin."""
         k = self._keep(host)
         sb = np.ascontiguousarray(src_begin, np.int32)
         sk = np.ascontiguousarray(src_kf, np.int32)
         n = len(sb) - 1
+        if device_offsets:
+            ob = self._dev(n + 1, torch.int32)
+            if out is None:
+                out = self._dev(max(self.loop_list_bound(sb, sk), 1), torch.int32)
+            st = self.lib.lc_loop_lists(self.h, n, k.ptr(sb), k.ptr(sk), k.ptr(ob), k.ptr(out), int(out.numel()),
+                                        self._stream())
+            self._check("lc_loop_lists", st)
+            return ob, out
         ob = np.zeros(n + 1, np.int32)
         if out is None:
             fb = self.kf_feat_begin

@@ -453,3 +453,52 @@ def test_point_range_errors(Ctx):
         c.mp_positions(7, 0, 1)
     assert c.mp_positions(LC_POS_GET, 3, 3).shape == (0, 3)
     c.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "S3", "C5"])
+def test_device_offsets_lists_and_fuse(Ctx, name):
+    """lc_loop_lists with a device out_begin (no host synchronisation: a scan of the counts on
+    the device, the wide lists' bitmaps rebuilt at emission) == the oracle's lists; lc_fuse
+    taking those device offsets (and the whole list buffer as mp_list) == lc_fuse with host
+    offsets: tables, counters and the post-apply map, byte for byte."""
+    w = world(name)
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    ob, ol = oracle.OracleMap(w).loop_lists(w.list_src_begin, w.list_src_kf)
+    db, buf = ctx.loop_lists(w.list_src_begin, w.list_src_kf, host=False, device_offsets=True)
+    torch.cuda.synchronize()
+    gb = db.cpu().numpy()
+    assert np.array_equal(gb, ob)
+    assert np.array_equal(buf[:int(gb[-1])].cpu().numpy(), ol)
+    if w.window is None or len(ob) != len(w.window) + 1:   # (C1: one list shared by the window)
+        ctx.close()
+        return
+    ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    ctx.state_save()
+    ref = ctx.fuse(w.window, ol, FUSE_PARAMS, window_S=w.win_S, win_list_begin=ob)
+    st_ref = ctx.download_map()
+    ctx.state_restore()
+    got = ctx.fuse(w.window, buf, FUSE_PARAMS, window_S=w.win_S, win_list_begin=db)
+    st = ctx.download_map()
+    assert np.array_equal(got["winner"], ref["winner"]) and np.array_equal(got["victim"], ref["victim"])
+    assert got["counts"] == ref["counts"]
+    for k in st:
+        assert np.array_equal(st[k], st_ref[k]), k
+    ctx.close()
+
+
+def test_device_offsets_errors(Ctx):
+    from paper_2603_17201_b200._lib import LcError
+    w = world("C2")
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    small = torch.empty(10, dtype=torch.int32, device="cuda:0")
+    with pytest.raises(LcError):   # capacity below the lists' upper bound
+        ctx.loop_lists(w.list_src_begin, w.list_src_kf, out=small, host=False, device_offsets=True)
+    db, buf = ctx.loop_lists(w.list_src_begin, w.list_src_kf, host=False, device_offsets=True)
+    ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    with pytest.raises(LcError):   # a shard's PLAN needs host offsets
+        ctx.fuse(w.window, buf, FUSE_PARAMS, window_S=w.win_S, win_list_begin=db, phase=1, w_lo=0, w_hi=3)
+    with pytest.raises(LcError):   # so do the per-query debug outputs
+        ctx.fuse(w.window, buf, FUSE_PARAMS, window_S=w.win_S, win_list_begin=db, debug=True)
+    ctx.close()
