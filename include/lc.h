@@ -512,7 +512,12 @@ lc_status lc_correct_sim3(lc_ctx* ctx, int32_t mode, int32_t n_batch, const int3
  * phase LC_FUSE_APPLY : apply from io_winner / io_victim (e.g. after an NCCL MIN
  *                       all-reduce of the shards' tables). w_lo / w_hi ignored.
  * phase LC_FUSE_ALL   : PLAN over the whole window, then APPLY.
- *   window_kf, win_list_begin (nullable) [host]; window_S (nullable) [host|dev]; n_window >= 1
+ *   window_kf [host]; win_list_begin (nullable) [host|dev]; window_S (nullable) [host|dev];
+ *   n_window >= 1. A DEVICE win_list_begin (e.g. lc_loop_lists' device offsets) is not
+ *   read back: n_list is then the list buffer's capacity (>= win_list_begin[n_window]),
+ *   mp_list must be device memory, every list must hold <= 261888 entries, and only a
+ *   full-window PLAN / ALL without forced matches or dbg is accepted (LC_EINVAL
+ *   otherwise); each window keyframe is then one block (its own CTA).
  *   distinct keyframes; mp_list [host|dev] n_list entries, each list ascending
  *   and unique (not checked on device; duplicates give duplicate queries).
  *   A host mp_list with per-keyframe lists (win_list_begin) on a full-range PLAN
@@ -548,10 +553,17 @@ lc_status lc_fuse(lc_ctx* ctx, int32_t phase, int32_t w_lo, int32_t w_hi, int32_
  * them, reading O4) associated with the keyframes src_kf[src_begin[l] .. src_begin[l+1]),
  * from the CURRENT associations (after any fuse / append). The result is the
  * (win_list_begin, mp_list) pair lc_fuse takes.
- *   src_begin [host] [n+1], src_kf [host]; out_begin [host] [n+1] (written);
+ *   src_begin [host] [n+1], src_kf [host]; out_begin [host|dev] [n+1] (written);
  *   out_list [host|dev] capacity entries.
- * Synchronises the stream (the offsets come back to the host). A list may hold at most
- * 24576 distinct map points.
+ * Host out_begin: synchronises the stream (the offsets come back to the host). A list
+ * may hold at most 24576 distinct map points.
+ * Device out_begin (device offsets): nothing is read back and the call does not
+ * synchronise; the offsets are a device scan of the lists' counts, so lc_fuse can take
+ * (out_begin, out_list) as its (win_list_begin, mp_list) with no host round trip. Then
+ * out_list must be device memory of capacity >= U = the sum over lists of their source
+ * keyframes' feature counts (an upper bound of the total, known before the lists are
+ * built), each list's bound must be <= 261888 and the map must hold <= 1835008 map points
+ * (every list's id range fits one shared-memory bitmap); otherwise LC_ECAPACITY.
  * Errors: LC_ESTATE (no map), LC_EINVAL, LC_ERANGE (keyframe id), LC_ECAPACITY (total >
  * capacity -- out_begin is complete -- or a list over the limit). */
 lc_status lc_loop_lists(lc_ctx* ctx, int32_t n, const int32_t* src_begin, const int32_t* src_kf,
