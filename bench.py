@@ -307,12 +307,17 @@ def main():
     stream = torch.cuda.current_stream(dev)
     torch.cuda.synchronize()
     u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.profile_enable(True)
     u0.record(stream)
     ctx.upload_map(arrays, [w.cam], grid=grid)   # SURVEY §8 a1 + a2 (once per map)
     u1.record(stream)
     u1.synchronize()
+    up_prof = ctx.profile_read()
+    ctx.profile_enable(False)
     upload = {"ms": round(u0.elapsed_time(u1), 3), "note": "lc_upload_map incl. H2D of the host "
               "SoA map (pageable) + SoA pack + per-keyframe grid build; once per map, not per step",
+              "kernels_ms": round(up_prof.get("upload", (0.0, 0))[0], 3),
+              "kernels": "SoA pack + n_obs count + per-octave cell-grid build (counting sort), device time",
               "bytes": int(sum(np.asarray(v).nbytes for v in arrays.values()))}
     ctx.state_save()
 
@@ -427,6 +432,7 @@ def main():
     ctx.profile_enable(False)
     ms = np.array([a.elapsed_time(b) for a, b in ev])
     ms_mean = float(ms.mean())
+    ms_median = float(np.median(ms))
     ms_t = torch.tensor([ms_mean], dtype=torch.float64, device=dev)
     cand_t = torch.tensor([cand_rank], dtype=torch.int64, device=dev)
     if ws > 1:
@@ -878,6 +884,7 @@ def main():
                        "parallelism": f"keyframe-sharded x{ws}" if ws > 1 else "1 GPU",
                        "l2": "flushed between steps (512 MB write) after an untimed state restore"},
             "ms_per_loop": round(ms_step, 5),
+            "ms_median": round(ms_median, 5),
             "kernel_ms_per_step": {k: round(v, 5) for k, v in fam_ms.items()},
             "fuse_counts": fuse_counts if ws == 1 else None,
             "gpu_launches": int(launches_timed),
