@@ -155,30 +155,52 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_win_b(
 #pragma unroll
     for (int u = 0; u < 2; ++u)
       if (q0 + u < n_mp) o[u] = owner[q0 + u];
-    double T[13], Si[13];
-    int have = -1;
+    bool go[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int q = q0 + u;
-      if (q >= n_mp) break;
+      go[u] = false;
+      if (q >= n_mp) continue;
       if (o[u] == OWNER_NONE || (fl[u] & 1u)) {   // unobserved by the window, or bad
         corr_ref[q] = -1;
         continue;
       }
       corr_ref[q] = window[o[u]];   // (every point: the owner bookkeeping stays replicated)
-      if (q < mp_lo || q >= mp_hi) continue;   // another rank's point slice (lc_set_point_range)
-      if (o[u] != have) {
-        const double* S = scr + (size_t)WSTR * o[u];
-        load13(S, T);
-        load13(S + 14, Si);
-        have = o[u];
+      go[u] = q >= mp_lo && q < mp_hi;   // (else another rank's point slice, lc_set_point_range)
+    }
+    double T[13], Si[13];
+    if (go[0] || go[1]) {
+      const double* S = scr + (size_t)WSTR * (go[0] ? o[0] : o[1]);
+      load13(S, T);
+      load13(S + 14, Si);
+    }
+    double pw[2][3];
+    if (go[0] && go[1] && o[0] == o[1]) {   // one owner (the common case): two chains interleaved
+      double p0[3] = {pf[0].x, pf[0].y, pf[0].z}, p1[3] = {pf[1].x, pf[1].y, pf[1].z}, c0[3], c1[3];
+      lc_sim3_apply(T, p0, c0);
+      lc_sim3_apply(T, p1, c1);
+      lc_sim3_apply(Si, c0, pw[0]);
+      lc_sim3_apply(Si, c1, pw[1]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!go[u]) continue;
+        if (u == 1 && go[0] && o[1] != o[0]) {
+          const double* S = scr + (size_t)WSTR * o[1];
+          load13(S, T);
+          load13(S + 14, Si);
+        }
+        double p[3] = {pf[u].x, pf[u].y, pf[u].z}, pc[3];
+        lc_sim3_apply(T, p, pc);
+        lc_sim3_apply(Si, pc, pw[u]);
       }
-      double p[3] = {pf[u].x, pf[u].y, pf[u].z}, pc[3], pw[3];
-      lc_sim3_apply(T, p, pc);
-      lc_sim3_apply(Si, pc, pw);
-      rec[q].pos[0] = __double2float_rn(pw[0]);
-      rec[q].pos[1] = __double2float_rn(pw[1]);
-      rec[q].pos[2] = __double2float_rn(pw[2]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!go[u]) continue;
+      rec[q0 + u].pos[0] = __double2float_rn(pw[u][0]);
+      rec[q0 + u].pos[1] = __double2float_rn(pw[u][1]);
+      rec[q0 + u].pos[2] = __double2float_rn(pw[u][2]);
       ++n;
     }
     warp_count(n, &counts[LC_COUNT_CORR_MP]);
@@ -240,27 +262,48 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_all_points(
     }
   }
   pdl_wait();
-  double pre[13], inv[13];
-  int have = -1;
+  bool go[2];
+  int r[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int q = q0 + u;
-    if (q >= n_mp) break;
-    if (cr[u] >= 0) corr_ref[q] = -1;
-    if ((fl[u] & 1u) || q < mp_lo || q >= mp_hi) continue;   // bad, or another rank's slice
-    const int r = cr[u] >= 0 ? cr[u] : rk[u];
-    if (r != have) {
-      const double* S = scr + (size_t)ASTR * r;
-      load13(S, pre);
-      load13(S + 14, inv);
-      have = r;
+    go[u] = q < n_mp && !(fl[u] & 1u) && q >= mp_lo && q < mp_hi;   // not bad, this rank's slice
+    r[u] = cr[u] >= 0 ? cr[u] : rk[u];
+    if (q < n_mp && cr[u] >= 0) corr_ref[q] = -1;
+  }
+  double pre[13], inv[13];
+  if (go[0] || go[1]) {
+    const double* S = scr + (size_t)ASTR * (go[0] ? r[0] : r[1]);
+    load13(S, pre);
+    load13(S + 14, inv);
+  }
+  double pw[2][3];
+  if (go[0] && go[1] && r[0] == r[1]) {   // the common case (creation order): both points with
+    double p0[3] = {pf[0].x, pf[0].y, pf[0].z}, p1[3] = {pf[1].x, pf[1].y, pf[1].z}, c0[3], c1[3];
+    lc_sim3_apply(pre, p0, c0);             // one transform pair, the two fp64 chains interleaved
+    lc_sim3_apply(pre, p1, c1);
+    lc_sim3_apply(inv, c0, pw[0]);
+    lc_sim3_apply(inv, c1, pw[1]);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!go[u]) continue;
+      if (u == 1 && go[0] && r[1] != r[0]) {
+        const double* S = scr + (size_t)ASTR * r[1];
+        load13(S, pre);
+        load13(S + 14, inv);
+      }
+      double p[3] = {pf[u].x, pf[u].y, pf[u].z}, pc[3];
+      lc_sim3_apply(pre, p, pc);
+      lc_sim3_apply(inv, pc, pw[u]);
     }
-    double p[3] = {pf[u].x, pf[u].y, pf[u].z}, pc[3], pw[3];
-    lc_sim3_apply(pre, p, pc);
-    lc_sim3_apply(inv, pc, pw);
-    rec[q].pos[0] = __double2float_rn(pw[0]);
-    rec[q].pos[1] = __double2float_rn(pw[1]);
-    rec[q].pos[2] = __double2float_rn(pw[2]);
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (!go[u]) continue;
+    rec[q0 + u].pos[0] = __double2float_rn(pw[u][0]);
+    rec[q0 + u].pos[1] = __double2float_rn(pw[u][1]);
+    rec[q0 + u].pos[2] = __double2float_rn(pw[u][2]);
     ++n;
   }
   warp_count(n, &counts[LC_COUNT_CORR_MP]);

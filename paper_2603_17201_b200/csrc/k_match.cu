@@ -1336,7 +1336,9 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_mark(
     const int fb = kf_fbeg[k], fe = kf_fbeg[k + 1];
     const int wpos = (kf_win_ep[k] == epoch) ? kf_win_pos[k] : -1;
     const int64_t wshift = wpos >= 0 ? woff_of_pos[wpos] - fb : 0;   // winner index = f + wshift
-    int dirty = 0;
+    // a window keyframe is listed without the scan: nearly all of them change (their
+    // duplicates were fused), and APPLY on an unchanged keyframe writes nothing
+    int dirty = wpos >= 0 ? 1 : 0;
     // 4 x 16-B association loads in flight per lane (512 slots per warp round)
     for (int f0 = fb; f0 < fe && !__any_sync(0xffffffffu, dirty); f0 += 512) {
       int32_t m[16];
