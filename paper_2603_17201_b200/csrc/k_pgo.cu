@@ -949,6 +949,118 @@ __device__ bool cr_chol(double* A, int D, double* inv, double* Binv, double* rcp
   return true;
 }
 
+#ifndef LC_CR_BLOCKED
+#define LC_CR_BLOCKED 1
+#endif
+// Blocked (7-wide block columns) right-looking Cholesky of the D x D SPD super-block, same
+// outputs as cr_chol: per block column K (o = 7K) -- (1) warp 0 factors the 7 x 7 diagonal
+// block in registers (lane r = row r, pivots and columns by shuffle) and forms its inverse
+// Binv_K; (2) thread per row i >= o + 7: L_iK = A_iK Binv_K^T; (3) the trailing lower
+// triangle A_ij -= sum_m L_im L_jm over 4 x 4 register tiles (the 7-term products summed
+// in registers: 0.8 shared-memory accesses per FMA instead of 3) -- three barriers per
+// block column instead of one per column. Returns false (CTA-uniform) on a non-positive pivot.
+__device__ bool cr_chol_blocked(double* A, int D, double* inv, double* Binv, int* bad) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nb = D / 7;
+  if (t == 0) *bad = 0;
+  __syncthreads();
+  for (int K = 0; K < nb; ++K) {
+    const int o = 7 * K;
+    if (warp == 0) {   // (1) diagonal block
+      double row[7];
+#pragma unroll
+      for (int c = 0; c < 7; ++c) row[c] = (lane < 7 && c <= lane) ? A[(o + lane) * D + o + c] : 0.0;
+      double il[7];
+#pragma unroll
+      for (int c = 0; c < 7; ++c) {
+        const double piv = __shfl_sync(0xffffffffu, row[c], c);
+        if (!(piv > 0.0) && lane == 0) *bad = 1;
+        const double l = sqrt(piv);
+        il[c] = 1.0 / l;
+        if (lane == c) row[c] = l;
+        else if (lane > c && lane < 7) row[c] *= il[c];
+#pragma unroll
+        for (int j = c + 1; j < 7; ++j) {
+          const double ljc = __shfl_sync(0xffffffffu, row[c], j);
+          if (lane < 7 && lane >= j) row[j] -= row[c] * ljc;
+        }
+      }
+      if (lane < 7) {
+#pragma unroll
+        for (int c = 0; c < 7; ++c)
+          if (c <= lane) A[(o + lane) * D + o + c] = row[c];
+#pragma unroll
+        for (int c = 0; c < 7; ++c)
+          if (c == lane) inv[o + c] = il[c];
+      }
+      // Binv_K: lane c (< 7) forms column c of L_KK^-1 by forward substitution
+      double y[7];
+#pragma unroll
+      for (int r = 0; r < 7; ++r) {
+        double sacc = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int m = 0; m < r; ++m) sacc -= __shfl_sync(0xffffffffu, row[m], r) * y[m];
+        y[r] = r < lane ? 0.0 : sacc * il[r];
+      }
+      if (lane < 7) {
+#pragma unroll
+        for (int r = 0; r < 7; ++r) Binv[49 * K + 7 * r + lane] = y[r];
+      }
+    }
+    __syncthreads();
+    if (*bad) return false;
+    const int n = D - o - 7;
+    if (n <= 0) break;
+    // (2) panel: L_iK = A_iK Binv_K^T (lower-triangular Binv: m <= c)
+    for (int i = o + 7 + t; i < D; i += kT) {
+      double av[7];
+#pragma unroll
+      for (int m = 0; m < 7; ++m) av[m] = A[i * D + o + m];
+      const double* Bi = Binv + 49 * K;
+#pragma unroll
+      for (int c = 0; c < 7; ++c) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int m = 0; m <= c; ++m) sacc += av[m] * Bi[7 * c + m];
+        A[i * D + o + c] = sacc;
+      }
+    }
+    __syncthreads();
+    // (3) trailing update over 4 x 4 tiles (ti >= tj), rows / columns >= o + 7
+    const int T = (n + 3) >> 2;
+    const int npair = T * (T + 1) / 2;
+    for (int pi = t; pi < npair; pi += kT) {
+      int ti = (int)((sqrtf(8.0f * (float)pi + 1.0f) - 1.0f) * 0.5f);   // pi = ti (ti + 1) / 2 + tj
+      while ((ti + 1) * (ti + 2) / 2 <= pi) ++ti;
+      while (ti * (ti + 1) / 2 > pi) --ti;
+      const int tj = pi - ti * (ti + 1) / 2;
+      const int i0 = o + 7 + 4 * ti, j0 = o + 7 + 4 * tj;
+      double li[4][7], lj[4][7];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int m = 0; m < 7; ++m) {
+          li[u][m] = i0 + u < D ? A[(i0 + u) * D + o + m] : 0.0;
+          lj[u][m] = j0 + u < D ? A[(j0 + u) * D + o + m] : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int i = i0 + u, j = j0 + v;
+          if (i < D && j <= i) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int m = 0; m < 7; ++m) sacc += li[u][m] * lj[v][m];
+            A[i * D + j] -= sacc;
+          }
+        }
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
 // CTA: B <- L^-1 B for a D x pc panel (pitch kCrPC) in shared memory, L lower (pitch D),
 // Binv the inverses of its 7 x 7 diagonal blocks: per 7-row block, X_q = Binv_q B_q (thread
 // per column), then the rank-7 update of the rows below (thread per (row, column) tile)
@@ -1081,7 +1193,11 @@ __device__ bool cr_eliminate(const PgoArgs& a, int i, int st, double* sm, long l
   cr_load(sL, a.crA + i * DD, (int)DD);
   __syncthreads();
   CE_TIC(0);
+#if LC_CR_BLOCKED
+  if (!cr_chol_blocked(sL, D, sInv, sBinv, (int*)sRcp)) return false;
+#else
   if (!cr_chol(sL, D, sInv, sBinv, sRcp)) return false;
+#endif
   CE_TIC(1);
   for (int e = threadIdx.x; e < (int)DD; e += kT) a.crA[i * DD + e] = sL[e];
   const int ncol = D + (r < N ? D : 0) + 1;   // [A_il | A_ir | b_i]
@@ -1315,7 +1431,11 @@ __device__ void cr_solve(const PgoArgs& a, double lambda, double* sm, double* X,
     cr_load(sL, a.crA, (int)DD);
     for (int e = threadIdx.x; e < D; e += kT) sB[e * kCrPC] = __ldcg(a.cry + e);
     __syncthreads();
+#if LC_CR_BLOCKED
+    if (cr_chol_blocked(sL, D, sInv, sBinv, (int*)sRcp)) {
+#else
     if (cr_chol(sL, D, sInv, sBinv, sRcp)) {
+#endif
       cr_trsm(sL, sBinv, D, sB, 1);
       double* z = sRcp;
       for (int e = threadIdx.x; e < D; e += kT) z[e] = sB[e * kCrPC];
