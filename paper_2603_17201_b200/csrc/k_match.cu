@@ -1292,6 +1292,7 @@ __global__ void k_adds_scatter(int64_t n_wfeat, int64_t n, const long long* __re
 // Victim marking: flags |= bad, replaced_by = survivor (reading O9 (iv)), victim bitmap.
 __global__ void k_fuse_victims(int n_mp, const unsigned long long* victim,
                                uint8_t* __restrict__ flags, int32_t* __restrict__ replaced_by,
+                               int32_t* __restrict__ nobs,
                                uint32_t* __restrict__ vbits, unsigned long long* __restrict__ counts) {
   pdl_wait();
   uint32_t n = 0;
@@ -1305,6 +1306,12 @@ __global__ void k_fuse_victims(int n_mp, const unsigned long long* victim,
         isv = true;
         flags[q] |= 1u;
         replaced_by[q] = (int32_t)(v & 0xFFFFFFFFull);
+        // every slot holding a victim is rewired (or cleared) by APPLY, and n_obs counts the
+        // slots holding a point (the store's invariant: counted at upload, kept by APPLY), so
+        // the victim's count ends at 0 -- set here instead of one atomicSub per slot (a slot
+        // rewired to a point that is itself a victim -- a forced-match chain -- still gets
+        // its +1 in APPLY, after this)
+        nobs[q] = 0;
         ++n;
       }
     }
@@ -1481,7 +1488,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix(
       const int32_t m = s_old[f];
       if (nv != m) {
         feat_mp[fb + f] = nv;
-        if (m >= 0) atomicSub(&nobs[m], 1);
+        // (m >= 0 here only for a victim, whose count k_fuse_victims already set to 0)
         if (nv >= 0) atomicAdd(&nobs[nv], 1);
       }
     }
@@ -1590,7 +1597,7 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix_r(
       else if (pr == 1) cnt[A_ADDED]++;
       if (v != m[u]) {
         feat_mp[fb + f] = v;
-        if (m[u] >= 0) atomicSub(&nobs[m[u]], 1);
+        // (m >= 0 here only for a victim, whose count k_fuse_victims already set to 0)
         if (v >= 0) atomicAdd(&nobs[v], 1);
       }
     }
@@ -1731,7 +1738,7 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
   Store& st = c->st;
   if (st.n_mp > 0) {
     cudaError_t e = launch_pdl(k_fuse_victims, dim3(grid_for(st.n_mp)), dim3(LC_NTHREADS), 0, s, st.n_mp,
-                               victim, st.mp_flags, st.mp_replaced_by, st.mp_vbits, counts);
+                               victim, st.mp_flags, st.mp_replaced_by, st.mp_nobs, st.mp_vbits, counts);
     if (e != cudaSuccess) return e;
     c->launches++;
   }
