@@ -601,13 +601,15 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   // strict square window |fuv - uv| < r (reading A8). fp32 filter: |(float)a - fu| is
   // within 2.5e-4 px of the exact |a - u| for |u| < 4096 px, so a decision farther
   // than 1e-3 px from the edge is exact; -1 = ambiguous (decide in fp64)
-  auto win_f32 = [&](const float2 fuv, float fu, float fv, float fr) -> int {
-    if (!f32ok) return -1;
-    const float du = fabsf(fuv.x - fu), dv = fabsf(fuv.y - fv);
-    if (du > fr + kWinTol || dv > fr + kWinTol) return 0;
-    if (du < fr - kWinTol && dv < fr - kWinTol) return 1;
+  // (frp = fr + tol, frm = fr - tol per survivor; tol = +inf when fp32 cannot decide:
+  // every test is then ambiguous)
+  auto win_f32 = [&](const float2 fuv, float fu, float fv, float frp, float frm) -> int {
+    const float dm = fmaxf(fabsf(fuv.x - fu), fabsf(fuv.y - fv));
+    if (dm > frp) return 0;   // du > fr + tol || dv > fr + tol
+    if (dm < frm) return 1;   // du < fr - tol && dv < fr - tol
     return -1;
   };
+  const float wtol = f32ok ? kWinTol : INFINITY;
 
   // the next step's survivor entries are in flight while the current step runs
   Surv e_nx;
@@ -632,13 +634,17 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
       // (0.01 px) cell ranges; slots whose fp32 window test is ambiguous are marked and
       // settled in fp64 after the scan
       uint32_t amb = 0u;
+      const float frp = fr + wtol, frm = fr - wtol;
+      // the window's conservative pixel range (the same fp32 expressions per octave before)
+      const float ulo = e.fu - fr - 0.01f - fminx, uhi = e.fu + fr + 0.01f - fminx;
+      const float vlo = e.fv - fr - 0.01f - fminy, vhi = e.fv + fr + 0.01f - fminy;
       for (int o = max(lvl - 1, 0); o <= lvl; ++o) {
         const int oc = s_oc[o], orr = s_or[o], ob = s_ob[o];
         const float fsx = s_fsx[o], fsy = s_fsy[o];
-        const int cx0 = max(0, (int)floorf((e.fu - fr - 0.01f - fminx) * fsx));
-        const int cx1 = min(oc - 1, (int)floorf((e.fu + fr + 0.01f - fminx) * fsx));
-        const int cy0 = max(0, (int)floorf((e.fv - fr - 0.01f - fminy) * fsy));
-        const int cy1 = min(orr - 1, (int)floorf((e.fv + fr + 0.01f - fminy) * fsy));
+        const int cx0 = max(0, (int)floorf(ulo * fsx));
+        const int cx1 = min(oc - 1, (int)floorf(uhi * fsx));
+        const int cy0 = max(0, (int)floorf(vlo * fsy));
+        const int cy1 = min(orr - 1, (int)floorf(vhi * fsy));
         for (int cy = cy0; cy <= cy1; ++cy) {
           const int ps = s_cell[ob + cy * oc + cx0], pe = s_cell[ob + cy * oc + cx1 + 1];
           for (int p0 = ps; p0 < pe; p0 += LC_KM_B) {   // LC_KM_B features' loads issued together
@@ -654,7 +660,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
             for (int t = 0; t < LC_KM_B; ++t) {
               if (p0 + t >= pe) break;
               if (MODE == 1 && (mt[t] & 0x80000000u)) continue;
-              const int w = win_f32(fuv[t], e.fu, e.fv, fr);
+              const int w = win_f32(fuv[t], e.fu, e.fv, frp, frm);
               if (w == 0) continue;
               if (nc < CPL) {
                 s_cand[lane * CPL + nc] = (uint16_t)(p0 + t);
