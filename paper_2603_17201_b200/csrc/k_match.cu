@@ -464,7 +464,7 @@ struct MatchSmem {
   // query descriptors [32][8] u32 (cp.async destination)
   static constexpr int WKEY = 0;
   static constexpr int WCAND = WKEY + 32 * CPL * 4;
-  static constexpr int WQD = (WCAND + 32 * CPL * 2 + 15) & ~15;
+  static constexpr int WQD = (WCAND + 32 * (CPL + 1) * 2 + 15) & ~15;   // (+1: overflow sink)
   static constexpr int WB = WQD + 32 * 32;
   static constexpr int UV = 0;
   static constexpr int META = UV + ((FCAP * 8 + 15) & ~15);
@@ -522,8 +522,11 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ double s_T[12];
   __shared__ __align__(16) DevCam s_cam;
-  __shared__ float s_fsx[LC_MAX_LEVELS], s_fsy[LC_MAX_LEVELS], s_fr[LC_MAX_LEVELS];
-  __shared__ int s_oc[LC_MAX_LEVELS], s_or[LC_MAX_LEVELS], s_ob[LC_MAX_LEVELS];
+  __shared__ float s_fr[LC_MAX_LEVELS];
+  // per octave: {cols, rows, first cell, fp32 cell scale x} + fp32 cell scale y (one
+  // 16-B and one 4-B shared load per octave in the scan)
+  __shared__ int4 s_og[LC_MAX_LEVELS];
+  __shared__ float s_fsy[LC_MAX_LEVELS];
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int blk = a.blk_base + (int)blockIdx.x;
@@ -537,7 +540,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   uint32_t* s_meta = (uint32_t*)(smem + SM::META);
   unsigned char* wb = smem + SM::QUEUE + warp * SM::WB;
   uint32_t* s_key = (uint32_t*)(wb + SM::WKEY);     // [32][CPL] candidate keys
-  uint16_t* s_cand = (uint16_t*)(wb + SM::WCAND);   // [32][CPL] candidate positions
+  uint16_t* s_cand = (uint16_t*)(wb + SM::WCAND);   // [32][CPL + 1] candidate positions
   uint32_t* s_qd = (uint32_t*)(wb + SM::WQD);       // [32][8] query descriptors
   const int64_t toff = (MODE == 1 && a.taken) ? a.unit_toff[unit] : 0;
   if (tid == 0) {
@@ -566,12 +569,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
     const int o = tid - 128;
     const DevCam& c = a.cams[a.kf_cam[k]];
     const lc_match_params pp = a.params[(MODE == 1 && a.unit_param) ? a.unit_param[unit] : 0];
-    s_fsx[o] = (float)c.cell_sx[o];
     s_fsy[o] = (float)c.cell_sy[o];
     s_fr[o] = (float)((double)pp.th * a.scale[o]);
-    s_oc[o] = a.ocols[o];
-    s_or[o] = a.orows[o];
-    s_ob[o] = a.obase[o];
+    s_og[o] = make_int4(a.ocols[o], a.orows[o], a.obase[o], __float_as_int((float)c.cell_sx[o]));
   }
   if (a.sole) {  // this CTA owns the unit's winner words: initialise them here
     unsigned long long* w0 = a.winner + a.unit_woff[unit];
@@ -639,8 +639,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
       const float ulo = e.fu - fr - 0.01f - fminx, uhi = e.fu + fr + 0.01f - fminx;
       const float vlo = e.fv - fr - 0.01f - fminy, vhi = e.fv + fr + 0.01f - fminy;
       for (int o = max(lvl - 1, 0); o <= lvl; ++o) {
-        const int oc = s_oc[o], orr = s_or[o], ob = s_ob[o];
-        const float fsx = s_fsx[o], fsy = s_fsy[o];
+        const int4 og = s_og[o];
+        const int oc = og.x, orr = og.y, ob = og.z;
+        const float fsx = __int_as_float(og.w), fsy = s_fsy[o];
         const int cx0 = max(0, (int)floorf(ulo * fsx));
         const int cx1 = min(oc - 1, (int)floorf(uhi * fsx));
         const int cy0 = max(0, (int)floorf(vlo * fsy));
@@ -662,10 +663,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
               if (MODE == 1 && (mt[t] & 0x80000000u)) continue;
               const int w = win_f32(fuv[t], e.fu, e.fv, frp, frm);
               if (w == 0) continue;
-              if (nc < CPL) {
-                s_cand[lane * CPL + nc] = (uint16_t)(p0 + t);
-                if (w < 0) amb |= 1u << nc;
-              }
+              const int sl = min(nc, CPL);   // slot CPL: a sink for the overflow (rescanned)
+              s_cand[lane * (CPL + 1) + sl] = (uint16_t)(p0 + t);
+              amb |= (w < 0 ? 1u : 0u) << sl;
               ++nc;
             }
           }
@@ -677,14 +677,14 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         const double r = (double)prm.th * a.scale[lvl];
         int m = 0;
         for (int i = 0; i < nc; ++i) {
-          const int p = s_cand[lane * CPL + i];
+          const int p = s_cand[lane * (CPL + 1) + i];
           const float2 fuv = s_uv[p];
           if ((amb >> i) & 1u) {
             const double du = fabs((double)fuv.x - u), dv = fabs((double)fuv.y - v);
             wedge |= window_edge(du, dv, r);
             if (!(du < r && dv < r)) continue;
           }
-          s_cand[lane * CPL + m++] = (uint16_t)p;
+          s_cand[lane * (CPL + 1) + m++] = (uint16_t)p;
         }
         nc = m;
       }
@@ -713,7 +713,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
       const int oex = __shfl_sync(0xffffffffu, ex2, own);
       if (c < tot2) {
         const int slot = own * CPL + (c - oex);
-        const int p = s_cand[slot];
+        const int p = s_cand[own * (CPL + 1) + (c - oex)];
         const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
         const uint4 b0 = __ldg(dp), b1 = __ldg(dp + 1);
         const uint4* qd = reinterpret_cast<const uint4*>(s_qd + own * 8);
