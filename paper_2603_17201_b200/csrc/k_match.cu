@@ -464,7 +464,8 @@ struct MatchSmem {
   // query descriptors [32][8] u32 (cp.async destination)
   static constexpr int WKEY = 0;
   static constexpr int WCAND = WKEY + 32 * CPL * 4;
-  static constexpr int WQD = (WCAND + 32 * (CPL + 1) * 2 + 15) & ~15;   // (+1: overflow sink)
+  static constexpr int WOWN = WCAND + 32 * (CPL + 1) * 2;               // (+1: overflow sink)
+  static constexpr int WQD = (WOWN + 32 * CPL * 2 + 15) & ~15;
   static constexpr int WB = WQD + 32 * 32;
   static constexpr int UV = 0;
   static constexpr int META = UV + ((FCAP * 8 + 15) & ~15);
@@ -541,6 +542,8 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
   unsigned char* wb = smem + SM::QUEUE + warp * SM::WB;
   uint32_t* s_key = (uint32_t*)(wb + SM::WKEY);     // [32][CPL] candidate keys
   uint16_t* s_cand = (uint16_t*)(wb + SM::WCAND);   // [32][CPL + 1] candidate positions
+  uint16_t* s_own = (uint16_t*)(wb + SM::WOWN);     // [32 CPL] owner map of the flattened candidates
+  const bool dbg_any = a.dbg_best || a.dbg_uv || a.dbg_ncand;
   uint32_t* s_qd = (uint32_t*)(wb + SM::WQD);       // [32][8] query descriptors
   const int64_t toff = (MODE == 1 && a.taken) ? a.unit_toff[unit] : 0;
   if (tid == 0) {
@@ -702,18 +705,18 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
     }
     const int tot2 = __shfl_sync(0xffffffffu, incl, 31);
     const int ex2 = incl - ns;
+    // owner map of the flattened candidates: entry ex2 + i = (lane << 8) | i
+#pragma unroll
+    for (int i = 0; i < CPL; ++i)
+      if (i < ns) s_own[ex2 + i] = (uint16_t)((lane << 8) | i);
+    __syncwarp();
     for (int c0 = 0; c0 < tot2; c0 += 32) {
       const int c = c0 + lane;
-      int own = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int ex = __shfl_sync(0xffffffffu, ex2, own + step);
-        if (c < tot2 && ex <= c) own += step;
-      }
-      const int oex = __shfl_sync(0xffffffffu, ex2, own);
       if (c < tot2) {
-        const int slot = own * CPL + (c - oex);
-        const int p = s_cand[own * (CPL + 1) + (c - oex)];
+        const uint32_t oi = s_own[c];
+        const int own = (int)(oi >> 8), ci = (int)(oi & 0xFFu);
+        const int slot = own * CPL + ci;
+        const int p = s_cand[own * (CPL + 1) + ci];
         const uint4* dp = a.fc_desc + 2 * (size_t)(fp + p);
         const uint4 b0 = __ldg(dp), b1 = __ldg(dp + 1);
         const uint4* qd = reinterpret_cast<const uint4*>(s_qd + own * 8);
@@ -740,7 +743,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         scan_exact<MODE>(a, s_cam, s_cell, s_uv, s_meta, a.fc_desc + 2 * (size_t)fp, e.fu, e.fv, fr, lvl, u, v, r,
                          d0, d1, take, nc, wedge);
       } else {
-        for (int i = 0; i < ns; ++i) take(s_key[lane * CPL + i]);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i)
+          if (i < ns) take(s_key[lane * CPL + i]);
       }
       cE += nc;
       if (wedge) cW += 1u;
@@ -754,6 +759,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         cP += 1u;
         atomicMin(&win[best & 0xFFFFu], ((unsigned long long)hb << 32) | (unsigned int)e.q);
       } while (0);
+      if (dbg_any) {
       const int64_t qi = qbase + (int64_t)(e.jl & 0x07FFFFFFu);   // bits 27-29 level, 30 edge
       if (a.dbg_best) {
         long long val;
@@ -767,6 +773,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         a.dbg_uv[2 * qi] = u; a.dbg_uv[2 * qi + 1] = v;
       }
       if (a.dbg_ncand) a.dbg_ncand[qi] = nc;
+      }
     }
     __syncwarp();
   }
