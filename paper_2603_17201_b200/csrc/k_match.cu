@@ -214,7 +214,8 @@ __device__ __noinline__ int dal_exact(double sq, double g, double dmax, double s
 // distance / angle / level from s = |PO|^2 and g = PO . n: 1 (kept, lvl set), LC_Q_DIST or
 // LC_Q_ANGLE; identical decisions to dal_exact (which it calls inside the bands)
 __device__ __forceinline__ int dist_angle_level(double sq, double g, double dmax, double c08, double sLm1,
-                                                const double* scale, int L, float inv_lsf, int& lvl) {
+                                                const double* scale, const double* scale2, int L, float inv_lsf,
+                                                int& lvl) {
   const double hi = 1.2 * dmax, hi2 = hi * hi;
   const double lo = dmax * c08, lo2 = lo * lo;   // lo within a few ulp of 0.8 * (dmax / s_{L-1})
   if (sq > hi2 * (1.0 + 1e-12) || sq < lo2 * (1.0 - 1e-9)) return LC_Q_DIST;
@@ -224,13 +225,13 @@ __device__ __forceinline__ int dist_angle_level(double sq, double g, double dmax
   if (g2 < q4 * (1.0 - 1e-12)) return LC_Q_ANGLE;
   if (!(g2 > q4 * (1.0 + 1e-12))) return dal_exact(sq, g, dmax, sLm1, scale, L, lvl);
   // level: d * s_n >= dmax  <=>  s * s_n^2 >= dmax^2 outside the band
-  const double dm2 = dmax * dmax;
+  const double dm2 = dmax * dmax, dm2h = dm2 * (1.0 + 1e-12), dm2l = dm2 * (1.0 - 1e-12);
   int n = (int)ceilf(0.5f * __logf((float)dm2 / (float)sq) * inv_lsf);
   n = min(max(n, 0), L - 1);
-  auto cmp = [&](int k) -> int {   // 1 true, 0 false, -1 inside the band
-    const double t = sq * (scale[k] * scale[k]);
-    if (t > dm2 * (1.0 + 1e-12)) return 1;
-    if (t < dm2 * (1.0 - 1e-12)) return 0;
+  auto cmp = [&](int k) -> int {   // 1 true, 0 false, -1 inside the band (scale2[k] = scale[k]^2)
+    const double t = sq * scale2[k];
+    if (t > dm2h) return 1;
+    if (t < dm2l) return 0;
     return -1;
   };
   while (n > 0) {
@@ -257,8 +258,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
   __shared__ uint32_t s_filt[1 << (FILT_LOG2 - 5)];
   __shared__ double s_T[12];
   __shared__ double s_Ow[3];
-  __shared__ double s_scale[LC_MAX_LEVELS];
+  __shared__ double s_scale[LC_MAX_LEVELS], s_scale2[LC_MAX_LEVELS];
   __shared__ DevCam s_cam;
+  __shared__ double s_box[4];   // image centre x, half width, centre y, half height
   __shared__ int s_cnt;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -277,6 +279,10 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
     for (int i = 0; i < 12; ++i) s_T[i] = T[i];
     for (int i = 0; i < 3; ++i) s_Ow[i] = -lc_col3(T, i, T + 9);
     s_cam = a.cams[a.kf_cam[k]];
+    s_box[0] = 0.5 * (s_cam.min_x + s_cam.max_x);
+    s_box[1] = 0.5 * (s_cam.max_x - s_cam.min_x);
+    s_box[2] = 0.5 * (s_cam.min_y + s_cam.max_y);
+    s_box[3] = 0.5 * (s_cam.max_y - s_cam.min_y);
     s_cnt = 0;
   }
   // software pipeline: the 32-B record (geometry sector) of the query two steps ahead
@@ -304,7 +310,10 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
   uint8_t fa = flag_at(qa), fbl = flag_at(qb);
   issue(qa, 0);
   issue(qb, 1);
-  if (tid < LC_MAX_LEVELS) s_scale[tid] = a.scale[tid];
+  if (tid < LC_MAX_LEVELS) {
+    s_scale[tid] = a.scale[tid];
+    s_scale2[tid] = a.scale[tid] * a.scale[tid];
+  }
   for (int i = tid; i < (int)HS; i += LC_NTHREADS) s_hash[i] = -1;
   for (int i = tid; i < (1 << (FILT_LOG2 - 5)); i += LC_NTHREADS) s_filt[i] = 0u;
   __syncthreads();
@@ -377,16 +386,17 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
           const double ua = A * rz * (2.0 - z * rz) + s_cam.cx;   // one Newton step
           const double va = B * rz * (2.0 - z * rz) + s_cam.cy;
           const double e2 = e + kEdgeEps;
-          if (ua < s_cam.min_x - e || ua >= s_cam.max_x + e || va < s_cam.min_y - e ||
-              va >= s_cam.max_y + e) {
+          // distances from the image centre against the half extents (s_box): the same
+          // certain decisions as against each bound (up to an ulp, inside the margin e;
+          // a value exactly on a shifted bound goes to the exact path)
+          const double ax = fabs(ua - s_box[0]), ay = fabs(va - s_box[2]);
+          if (ax > s_box[1] + e || ay > s_box[3] + e) {
             // certainly culled; edge-ambiguous only if u or v is within 1e-4 px of a
             // bound, which needs ua or va within e + 1e-4 of one: decide exactly then
-            if (fabs(ua - s_cam.min_x) < e2 || fabs(ua - s_cam.max_x) < e2 || fabs(va - s_cam.min_y) < e2 ||
-                fabs(va - s_cam.max_y) < e2)
-              cE += edge_exact(s_cam, x, y, z) ? 1u : 0u;
+            if (fabs(ax - s_box[1]) < e2 || fabs(ay - s_box[3]) < e2) cE += edge_exact(s_cam, x, y, z) ? 1u : 0u;
             status = LC_Q_BOUNDS; cB += 1u; break;
           }
-          if (ua >= s_cam.min_x + e2 && ua < s_cam.max_x - e2 && va >= s_cam.min_y + e2 && va < s_cam.max_y - e2) {
+          if (ax < s_box[1] - e2 && ay < s_box[3] - e2) {
             // certainly inside and no bound within 1e-4 px: the fp32 survivor pixel is
             // taken from the refined estimate (|ua - u| << the fp32 window tolerance)
             fu = (float)ua; fv = (float)va;
@@ -415,7 +425,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
         const double dmax = __uint_as_float(r0.w);
         const double n0 = __uint_as_float(r1.x), n1 = __uint_as_float(r1.y), n2 = __uint_as_float(r1.z);
         const double g = (PO0 * n0 + PO1 * n1) + PO2 * n2;
-        const int st = dist_angle_level(sq, g, dmax, c08, sLm1, s_scale, L, inv_lsf, lvl);
+        const int st = dist_angle_level(sq, g, dmax, c08, sLm1, s_scale, s_scale2, L, inv_lsf, lvl);
         if (st == LC_Q_DIST) { status = LC_Q_DIST; cB += 1u << 10; break; }
         if (st == LC_Q_ANGLE) { status = LC_Q_ANGLE; cB += 1u << 20; break; }
         status = 1;
