@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
   Surv* out = a.surv + a.surv_off[blk];
   uint32_t cA = 0, cB = 0, cQ = 0;   // packed 10-bit counters (<= 64 queries per thread per block)
   uint32_t cE = 0;                   // edge-ambiguous culled queries (survivors: flag to k_match)
+  const bool dbg_any = a.dbg_best || a.dbg_uv || a.dbg_ncand;
   int slot = 0;
   for (int64_t jb = q0; jb < q1; jb += LC_NTHREADS, slot = slot == 2 ? 0 : slot + 1) {
     const int64_t j = jb + tid;
@@ -442,11 +443,13 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
       e.fu = fu; e.fv = fv;
       out[wbase + __popc(m & ltmask)] = e;
     } else if (valid) {
-      if (edge) cE += 1u;
-      const int64_t qi = qbase + (j - q0);
-      if (a.dbg_best) a.dbg_best[qi] = status;
-      if (a.dbg_uv && status > LC_Q_BOUNDS) { a.dbg_uv[2 * qi] = 0.0; a.dbg_uv[2 * qi + 1] = 0.0; }
-      if (a.dbg_ncand) a.dbg_ncand[qi] = 0;
+      cE += edge ? 1u : 0u;
+      if (dbg_any) {
+        const int64_t qi = qbase + (j - q0);
+        if (a.dbg_best) a.dbg_best[qi] = status;
+        if (a.dbg_uv && status > LC_Q_BOUNDS) { a.dbg_uv[2 * qi] = 0.0; a.dbg_uv[2 * qi + 1] = 0.0; }
+        if (a.dbg_ncand) a.dbg_ncand[qi] = 0;
+      }
     }
   }
   __syncthreads();
