@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
   const float inv_lsf = 1.0f / logf((float)a.scale[1]);
   const int64_t qbase = a.unit_qoff[unit] + (q0 - a.unit_lbeg[unit]);
   Surv* out = a.surv + a.surv_off[blk];
-  uint32_t cA = 0, cB = 0, cQ = 0;   // packed 10-bit counters (<= 64 queries per thread per block)
+  uint32_t cA = 0, cB = 0;   // packed 10-bit counters (<= 1023 queries per thread per block)
   uint32_t cE = 0;                   // edge-ambiguous culled queries (survivors: flag to k_match)
   const bool dbg_any = a.dbg_best || a.dbg_uv || a.dbg_ncand;
   int slot = 0;
@@ -367,7 +367,6 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
     int lvl = 0;
     bool edge = false;
     if (valid) {
-      cQ += 1u;
       do {
         if (!in_range || (flag & 1u)) { status = LC_Q_BAD; cA += 1u; break; }
         const uint32_t fb2 = fslot(q);
@@ -456,7 +455,8 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
   if (tid == 0) a.surv_cnt[blk] = s_cnt;
   pdl_trigger();
   uint32_t cnt[8];
-  cnt[0] = cQ; cnt[1] = cA & 1023u; cnt[2] = (cA >> 10) & 1023u; cnt[3] = (cA >> 20) & 1023u;
+  cnt[0] = tid == 0 ? (uint32_t)(q1 - q0) : 0u;   // the block's queries
+  cnt[1] = cA & 1023u; cnt[2] = (cA >> 10) & 1023u; cnt[3] = (cA >> 20) & 1023u;
   cnt[4] = cB & 1023u; cnt[5] = (cB >> 10) & 1023u; cnt[6] = (cB >> 20) & 1023u; cnt[7] = cE;
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
   pdl_wait();   // (PDL) k_fuse_prep zeroes the counters and publishes the epoch
