@@ -1739,7 +1739,10 @@ cudaError_t launch_fuse_prep(lc_ctx* c, int phase, int zero_counts, int64_t skip
     if (skip_hi - skip_lo < n_wfeat) n = std::max<int64_t>(n, n_wfeat);
     n = std::max<int64_t>(n, st.n_mp);
   }
-  k_fuse_prep<<<grid_for(n), LC_NTHREADS, 0, s>>>(phase, zero_counts, skip_lo, skip_hi, st.ep, n_w, d_window, n_wfeat,
+  // (a grid of at most 2 CTAs per SM: every CTA ends with an atomic on the one epoch word,
+  // and 2,368 of them serialised on it cost more than the fills)
+  k_fuse_prep<<<std::min(grid_for(n), 148 * 2), LC_NTHREADS, 0, s>>>(phase, zero_counts, skip_lo, skip_hi, st.ep, n_w,
+                                                                   d_window, n_wfeat,
                                                  mp_list, n_list_total, st.n_mp, winner, victim,
                                                  st.mp_loop_ep, st.kf_win_ep, st.kf_win_pos,
                                                  st.mp_vbits, n_vbits, st.kf_dirty, counts);
