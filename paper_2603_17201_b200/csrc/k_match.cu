@@ -1237,9 +1237,15 @@ __global__ void k_fuse_prep(int phase, int zero_counts, int64_t skip_lo, int64_t
     }
     // every winner word is NONE after PLAN except those a sole-mode match CTA owns
     // ([skip_lo, skip_hi): the shard's own units, initialised by their CTAs)
-    for (int64_t i = t0; i < n_wfeat; i += stride)
-      if (i < skip_lo || i >= skip_hi) winner[i] = NONE;
-    for (int64_t i = t0; i < n_mp; i += stride) victim[i] = NONE;
+    const int64_t lo = min(max(skip_lo, (int64_t)0), n_wfeat), hi = max(min(skip_hi, n_wfeat), lo);
+    for (int64_t i = t0; i < lo; i += stride) winner[i] = NONE;   // (no pass over the owned range)
+    for (int64_t i = hi + t0; i < n_wfeat; i += stride) winner[i] = NONE;
+    const int64_t head = (reinterpret_cast<uintptr_t>(victim) & 15u) ? 1 : 0;   // (a caller's table slice)
+    if (head && t0 == 0 && n_mp > 0) victim[0] = NONE;
+    for (int64_t i = head + 2 * t0; i < n_mp; i += 2 * stride) {   // 16-B stores from a 16-B boundary
+      if (i + 1 < n_mp) *reinterpret_cast<ulonglong2*>(victim + i) = make_ulonglong2(NONE, NONE);
+      else victim[i] = NONE;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
