@@ -255,7 +255,7 @@ template <int MODE, int FCAP>
 __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const MatchArgs a) {
   constexpr uint32_t HS = (uint32_t)HashSize<FCAP>::HS;
   extern __shared__ __align__(16) int32_t s_hash[];   // [HS] (dynamic: up to 64 KB)
-  __shared__ uint32_t s_filt[1 << (FILT_LOG2 - 5)];
+  __shared__ __align__(16) uint32_t s_filt[1 << (FILT_LOG2 - 5)];
   __shared__ double s_T[12];
   __shared__ double s_Ow[3];
   __shared__ double s_scale[LC_MAX_LEVELS], s_scale2[LC_MAX_LEVELS];
@@ -314,8 +314,10 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
     s_scale[tid] = a.scale[tid];
     s_scale2[tid] = a.scale[tid] * a.scale[tid];
   }
-  for (int i = tid; i < (int)HS; i += LC_NTHREADS) s_hash[i] = -1;
-  for (int i = tid; i < (1 << (FILT_LOG2 - 5)); i += LC_NTHREADS) s_filt[i] = 0u;
+  // (16-B stores: HS is a multiple of 32, the filter 1024 words)
+  for (int i = tid; i < (int)HS / 4; i += LC_NTHREADS) reinterpret_cast<int4*>(s_hash)[i] = make_int4(-1, -1, -1, -1);
+  for (int i = tid; i < (1 << (FILT_LOG2 - 5)) / 4; i += LC_NTHREADS)
+    reinterpret_cast<uint4*>(s_filt)[i] = make_uint4(0u, 0u, 0u, 0u);
   __syncthreads();
   // the keyframe's associations: 8 loads per thread in flight, then the inserts
   const int32_t* assoc = (MODE == 0) ? a.feat_mp + fb : (a.taken ? a.taken + toff : nullptr);
