@@ -664,25 +664,34 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KM_MINB) k_match(const MatchAr
         const int cx1 = min(oc - 1, (int)floorf(uhi * fsx));
         const int cy0 = max(0, (int)floorf(vlo * fsy));
         const int cy1 = min(orr - 1, (int)floorf(vhi * fsy));
-        for (int cy = cy0; cy <= cy1; ++cy) {
-          const int ps = s_cell[ob + cy * oc + cx0], pe = s_cell[ob + cy * oc + cx1 + 1];
-          for (int p0 = ps; p0 < pe; p0 += LC_KM_B) {   // LC_KM_B features' loads issued together
+        // two rows at a time: their feature ranges [psA, peA) and [psB, peB) walked as one
+        // index range (k < nA: row A), so a lane's loop trips do not depend on whether its
+        // window spans one row or two (the common cases)
+        for (int cy = cy0; cy <= cy1; cy += 2) {
+          const int rb = ob + cy * oc;
+          const int psA = s_cell[rb + cx0], peA = s_cell[rb + cx1 + 1];
+          int psB = 0, peB = 0;
+          if (cy < cy1) { psB = s_cell[rb + oc + cx0]; peB = s_cell[rb + oc + cx1 + 1]; }
+          const int nA = peA - psA, n = nA + (peB - psB);
+          for (int k0 = 0; k0 < n; k0 += LC_KM_B) {   // LC_KM_B features' loads issued together
             uint32_t mt[LC_KM_B];
             float2 fuv[LC_KM_B];
+            int pp[LC_KM_B];
 #pragma unroll
             for (int t = 0; t < LC_KM_B; ++t) {
-              const int pp = min(p0 + t, pe - 1);
-              if (MODE == 1) mt[t] = s_meta[pp];   // (the octave is implicit in the grid)
-              fuv[t] = s_uv[pp];
+              const int kk = min(k0 + t, n - 1);
+              pp[t] = kk < nA ? psA + kk : psB + (kk - nA);
+              if (MODE == 1) mt[t] = s_meta[pp[t]];   // (the octave is implicit in the grid)
+              fuv[t] = s_uv[pp[t]];
             }
 #pragma unroll
             for (int t = 0; t < LC_KM_B; ++t) {
-              if (p0 + t >= pe) break;
+              if (k0 + t >= n) break;
               if (MODE == 1 && (mt[t] & 0x80000000u)) continue;
               const int w = win_f32(fuv[t], e.fu, e.fv, frp, frm);
               if (w == 0) continue;
               const int sl = min(nc, CPL);   // slot CPL: a sink for the overflow (rescanned)
-              s_cand[lane * (CPL + 1) + sl] = (uint16_t)(p0 + t);
+              s_cand[lane * (CPL + 1) + sl] = (uint16_t)pp[t];
               amb |= (w < 0 ? 1u : 0u) << sl;
               ++nc;
             }
