@@ -502,3 +502,30 @@ def test_device_offsets_errors(Ctx):
     with pytest.raises(LcError):   # so do the per-query debug outputs
         ctx.fuse(w.window, buf, FUSE_PARAMS, window_S=w.win_S, win_list_begin=db, debug=True)
     ctx.close()
+
+
+def test_point_range_does_not_touch_dry_runs_and_forced_needs_host_offsets(Ctx):
+    """A point range set for a sharded correction does not restrict LC_DRY_RUN batches (they
+    write no positions: the whole batch is returned); a fuse with device list offsets
+    refuses forced matches (their LoopSet must be stamped before the search)."""
+    from paper_2603_17201_b200._lib import LcError
+    w = world("C4")
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    ref = ctx.correct_window_batch(w.hyp_cur, w.hyp_S_cw, w.hyp_win_begin, w.hyp_window)
+    ctx.set_point_range(0, w.n_mp // 3)
+    got = ctx.correct_window_batch(w.hyp_cur, w.hyp_S_cw, w.hyp_win_begin, w.hyp_window)
+    ctx.set_point_range()
+    for a_, b_ in zip(ref[:4], got[:4]):
+        assert np.array_equal(a_, b_)
+    ctx.close()
+    w = world("C2")
+    ctx = Ctx(0)
+    ctx.upload_map(w.map_arrays(), [w.cam])
+    db, buf = ctx.loop_lists(w.list_src_begin, w.list_src_kf, host=False, device_offsets=True)
+    ctx.correct_window(w.cur_kf, w.S_cw_corr, w.window)
+    forced = np.full(int(w.kf_feat_begin[w.cur_kf + 1] - w.kf_feat_begin[w.cur_kf]), -1, np.int32)
+    with pytest.raises(LcError):
+        ctx.fuse(w.window, buf, FUSE_PARAMS, window_S=w.win_S, win_list_begin=db, cur_kf=int(w.cur_kf),
+                 forced_mp=forced)
+    ctx.close()
