@@ -85,6 +85,17 @@ class Clocks:
         except Exception:
             self.p = None
 
+    def wait_first(self, timeout=3.0):
+        """Block until the first sample is written (or timeout)."""
+        t0 = time.time()
+        while self.p is not None and time.time() - t0 < timeout:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    return
+            except OSError:
+                return
+            time.sleep(0.02)
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -362,6 +373,10 @@ def main():
         ctx.state_restore()
         flush.fill_(1.0)
 
+    # the clocks sampler is started before the warm-up and its first sample awaited:
+    # nvidia-smi's start-up (NVML initialisation) must not stall the timed launches
+    clocks = Clocks(local)
+    clocks.wait_first()
     # warm-up
     for _ in range(args.warmup):
         reset()
@@ -403,7 +418,6 @@ def main():
     if ws > 1:
         tdist.barrier()
     torch.cuda.synchronize()
-    clocks = Clocks(local)
     l0 = ctx.kernel_launches()
     comm_pairs = []
     for i in range(args.steps):
@@ -885,6 +899,7 @@ def main():
                        "l2": "flushed between steps (512 MB write) after an untimed state restore"},
             "ms_per_loop": round(ms_step, 5),
             "ms_median": round(ms_median, 5),
+            "ms_max": round(float(ms.max()), 5),
             "kernel_ms_per_step": {k: round(v, 5) for k, v in fam_ms.items()},
             "fuse_counts": fuse_counts if ws == 1 else None,
             "gpu_launches": int(launches_timed),
