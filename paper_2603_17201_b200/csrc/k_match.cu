@@ -1559,9 +1559,6 @@ __global__ void __launch_bounds__(LC_NTHREADS) k_apply_fix_r(
   int32_t* s_key = (int32_t*)smem;
   uint32_t* s_val = (uint32_t*)(s_key + hash_size);
   uint32_t* s_filt = s_val + hash_size;   // 2^15-bit pre-filter
-#if LC_APPLY_WAIT_FIRST
-  pdl_wait();
-#endif
   for (int i = threadIdx.x; i < (int)HS; i += blockDim.x) { s_key[i] = -1; s_val[i] = 0xFFFFFFFFu; }
   for (int i = threadIdx.x; i < (1 << (FILT_LOG2 - 5)); i += blockDim.x) s_filt[i] = 0u;
   pdl_wait();
@@ -1802,13 +1799,6 @@ cudaError_t launch_fuse_apply(lc_ctx* c, const int64_t* d_woff, const unsigned l
       auto go = [&](auto kern) -> cudaError_t {
         cudaError_t e2 = set_smem_attr((const void*)kern, (int)sm);
         if (e2 != cudaSuccess) return e2;
-#if LC_APPLY_NOPDL
-        kern<<<std::min(st.n_kf, 148 * 4), LC_NTHREADS, sm, s>>>(
-                          (const uint32_t*)st.ep, (const int32_t*)st.kf_fbeg, (const uint32_t*)st.kf_win_ep,
-                          (const int32_t*)st.kf_win_pos, d_woff, winner, victim, (const uint32_t*)st.mp_vbits,
-                          (const int32_t*)st.kf_dirty, st.feat_mp, st.mp_nobs, H, counts);
-        return cudaGetLastError();
-#endif
         return launch_pdl(kern, dim3(std::min(st.n_kf, 148 * 4)), dim3(LC_NTHREADS), sm, s,
                           (const uint32_t*)st.ep, (const int32_t*)st.kf_fbeg, (const uint32_t*)st.kf_win_ep,
                           (const int32_t*)st.kf_win_pos, d_woff, winner, victim, (const uint32_t*)st.mp_vbits,

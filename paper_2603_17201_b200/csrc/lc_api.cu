@@ -1421,9 +1421,8 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
     // a full-range PLAN without forced matches stamps the LoopSet in k_project (after its
     // PDL wait, from its own list entries) instead of a separate pass over the lists in
     // k_fuse_prep; a shard's PLAN needs the whole window's LoopSet, so prep stamps it there
-    static const bool stamp_prep_only = getenv("LC_STAMP_PREP") != nullptr;   // test knob
     const bool stamp_proj = (phase & LC_FUSE_PLAN) && win_list_begin && w_lo == 0 && w_hi == n_window &&
-                            cur_pos < 0 && !stamp_prep_only;
+                            cur_pos < 0;
     const int64_t ch = sole ? std::max<int64_t>(max_len, 1) : pick_chunk(total_q);
     std::vector<int32_t> bunit;
     std::vector<int64_t> bq0, bq1;
