@@ -364,6 +364,9 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
     const uint4 r1 = s_rec[2 * (slot * LC_NTHREADS + tid) + 1];
     qa = qb; fa = fbl; qb = qc; fbl = fc; qc = qd;
     const bool in_range = valid && (unsigned)q < (unsigned)a.n_mp;
+    // LoopSet stamp with the host-known epoch (eager calls; prep does not touch loop_ep
+    // here and nothing reads it before k_match's wait)
+    if (a.stamp_epoch && in_range) a.loop_ep_w[q] = a.stamp_epoch;
     int status = 0;
     float fu = 0.f, fv = 0.f;
     int lvl = 0;
@@ -462,7 +465,7 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_KP_MINB) k_project(const Match
   cnt[4] = cB & 1023u; cnt[5] = (cB >> 10) & 1023u; cnt[6] = (cB >> 20) & 1023u; cnt[7] = cE;
   unsigned long long* cdst = a.counts + (MODE == 1 ? (size_t)unit * LC_NCOUNT : 0);
   pdl_wait();   // (PDL) k_fuse_prep zeroes the counters and publishes the epoch
-  if (a.loop_ep_w) {   // LoopSet stamps of this block's list entries (L2-hot re-read)
+  if (a.loop_ep_w && !a.stamp_epoch) {   // (graph capture: the replay's epoch is on the device)
     const uint32_t epoch = *a.epoch;
     for (int64_t j = q0 + tid; j < q1; j += LC_NTHREADS) {
       const int32_t q = __ldg(a.mp_list + j);

@@ -1580,6 +1580,10 @@ lc_status lc_fuse(lc_ctx* c, int32_t phase, int32_t w_lo, int32_t w_hi, int32_t 
       a.surv_cnt = d_scnt;
       a.sole = sole ? (c->sole_mode == 2 ? 2 : 1) : 0;
       a.loop_ep_w = (pipe || stamp_proj) ? st.mp_loop_ep : nullptr;   // k_project stamps the LoopSet
+      // eager calls know the epoch on the host: k_fuse_prep's epoch = ep[0] + 1 and every
+      // fuse epoch is reserved through ep_used (epoch_reserve), so ep_used is this call's
+      // (main) epoch; a captured call's replays take theirs from the device counter
+      a.stamp_epoch = (a.loop_ep_w && !c->cap) ? (uint32_t)c->ep_used : 0u;
       if (pipe) {
         for (int k = 0; k < lc_ctx::kPipe; ++k) {
           const int b0 = pipe_b[k], nbk = pipe_b[k + 1] - pipe_b[k];

@@ -161,6 +161,7 @@ struct MatchArgs {
   int32_t unit_base;   // k_resolve: unit = unit_base + blockIdx.x
   int32_t blk_base;    // k_project / k_match: block = blk_base + blockIdx.x (pipelined chunks)
   uint32_t* loop_ep_w; // non-null: k_project stamps the LoopSet (pipelined host-list mode)
+  uint32_t stamp_epoch; // != 0: that epoch (host-known, eager calls), stamped inline in k_project's loop
 };
 
 struct lc_graph {
