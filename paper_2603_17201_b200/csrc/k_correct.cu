@@ -145,16 +145,19 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_win_b(
 #pragma unroll
     for (int u = 0; u < 2; ++u) {   // independent of the predecessors: before the PDL wait
       pf[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (q0 + u < n_mp) {
-        fl[u] = flags[q0 + u];
-        if (q0 + u >= mp_lo && q0 + u < mp_hi) pf[u] = *reinterpret_cast<const float4*>(rec + q0 + u);
-      }
+      if (q0 + u < n_mp) fl[u] = flags[q0 + u];
     }
     pdl_wait();
     int o[2] = {OWNER_NONE, OWNER_NONE};
 #pragma unroll
     for (int u = 0; u < 2; ++u)
       if (q0 + u < n_mp) o[u] = owner[q0 + u];
+    // the records only of the points this pass re-anchors (owned, not bad, this rank's
+    // slice): the map points no window keyframe observes -- half of them at C5 -- are not read
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (q0 + u < n_mp && o[u] != OWNER_NONE && !(fl[u] & 1u) && q0 + u >= mp_lo && q0 + u < mp_hi)
+        pf[u] = *reinterpret_cast<const float4*>(rec + q0 + u);
     bool go[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
