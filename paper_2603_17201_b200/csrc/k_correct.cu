@@ -261,9 +261,14 @@ __global__ void __launch_bounds__(LC_NTHREADS, LC_PT_MINB) k_all_points(
       cr[u] = corr_ref[q0 + u];
       rk[u] = ref_kf[q0 + u];
       fl[u] = flags[q0 + u];
-      if (q0 + u >= mp_lo && q0 + u < mp_hi) pf[u] = *reinterpret_cast<const float4*>(rec + q0 + u);
     }
   }
+  // the records of the points this pass moves only (not bad -- the fused duplicates are --
+  // and this rank's slice); the flags are final (the fuse that set them has completed)
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+    if (q0 + u < n_mp && !(fl[u] & 1u) && q0 + u >= mp_lo && q0 + u < mp_hi)
+      pf[u] = *reinterpret_cast<const float4*>(rec + q0 + u);
   pdl_wait();
   bool go[2];
   int r[2];
